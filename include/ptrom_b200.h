@@ -1,0 +1,127 @@
+/* ptrom_b200.h — C ABI of the B200 (sm_100a) hot path for the PTROM
+ * reference (/root/reference/proj/include/ptrom). Plain pointers and sizes,
+ * no torch or Eigen types. Every entry point names the reference function it
+ * replaces (file:line under /root/reference/proj).
+ *
+ * Conventions:
+ *  - State/velocity layout is the reference's SoA [chi_1..chi_N, psi_1..psi_N]
+ *    (types.hpp:34-51): particle i owns rows i and i+N.
+ *  - Status codes: 0 ok; 2 config_error (types.hpp:23-26, CLI exit 2);
+ *    3 numerical_error (types.hpp:28-32, CLI exit 3); 4 CUDA failure.
+ *    ptrom_last_error() returns the message (same wording as the reference
+ *    where the reference throws).
+ *  - ptrom_* functions take HOST buffers, copy in/out on the context stream and
+ *    synchronize (drop-in for the reference's by-value returns).
+ *    ptrom_dev_* functions take DEVICE buffers, are stream-ordered on the
+ *    context stream and do not synchronize; a numerical failure they detect is
+ *    latched on the device and reported by ptrom_synchronize().
+ *  - n_pair_evals (nullable) receives the number of kernel_pair evaluations
+ *    the reference would have made, so an adapter can bump
+ *    detail::kernel_eval_counter (kernel.hpp:18-25).
+ *  - One context per device per host thread; not reentrant.
+ */
+#ifndef PTROM_B200_H
+#define PTROM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PTROM_OK = 0,
+  PTROM_CONFIG_ERROR = 2,
+  PTROM_NUMERICAL_ERROR = 3,
+  PTROM_CUDA_ERROR = 4
+};
+
+/* kernel.hpp:16 KernelForm */
+enum { PTROM_FORM_STANDARD = 0, PTROM_FORM_DENOMINATOR_SCALED = 1 };
+
+/* quadtree.hpp:189-203 ClusterCriterion::Kind */
+enum { PTROM_CRIT_BARNES_HUT = 0, PTROM_CRIT_NEIGHBOR = 1 };
+
+typedef struct ptrom_ctx ptrom_ctx;
+
+/* ------------------------------------------------------------ lifecycle -- */
+int ptrom_create(int device, void* cuda_stream /* nullable: legacy default */, ptrom_ctx** out);
+void ptrom_destroy(ptrom_ctx* ctx);
+const char* ptrom_last_error(const ptrom_ctx* ctx);
+int ptrom_set_stream(ptrom_ctx* ctx, void* cuda_stream);
+/* Synchronizes the context stream; returns and clears any latched device
+ * status (3 with the reference's message when a kernel saw a singularity). */
+int ptrom_synchronize(ptrom_ctx* ctx);
+/* Library/kernel identification for provenance checks. */
+const char* ptrom_build_info(void);
+
+/* ----------------------------------------------- all-pairs (host buffers) -- */
+/* kernel.hpp:107-129 pairwise_velocity<double> */
+int ptrom_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma,
+                                double delta, int form, const double* inflow /* 2n or NULL */,
+                                double* f /* 2n */, uint64_t* n_pair_evals);
+/* kernel.hpp:107-129 pairwise_velocity<float> */
+int ptrom_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* x, const float* gamma,
+                                float delta, int form, const float* inflow, float* f,
+                                uint64_t* n_pair_evals);
+/* kernel.hpp:154-170 inexact_kernel_jacobian<double> (BlockDiagonalJacobian
+ * kernel.hpp:134-152 as four n-vectors) */
+int ptrom_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma,
+                                      double delta, int form, double* dfx_dx, double* dfx_dy,
+                                      double* dfy_dx, double* dfy_dy, uint64_t* n_pair_evals);
+/* integrators.hpp:243-272 fom_simulate<double, PairwiseModel<double>> with
+ * FomStepper integrators.hpp:117-201 and NewtonConfig integrators.hpp:55-66.
+ * snapshots: column-major 2n x n_steps; per-step iterations/converged/
+ * relative_residual as StepResult (integrators.hpp:104-111). */
+int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const double* gamma, double delta,
+                           int form, const double* inflow, double dt, int64_t n_steps, double tol,
+                           int max_iters, int jacobian_refresh_period, double* snapshots, int* iterations,
+                           uint8_t* converged, double* relative_residual, uint64_t* n_pair_evals);
+
+/* --------------------------------------------- all-pairs (device buffers) -- */
+/* Velocity of targets [t_begin, t_end) against all n sources (j != i):
+ * f[(i-t_begin)] and f[(i-t_begin) + ld_f]. x is the full 2n SoA state,
+ * inflow the full 2n vector or NULL. kernel.hpp:107-129 restricted to rows. */
+int ptrom_dev_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                    double delta, int form, const double* d_inflow, int64_t t_begin,
+                                    int64_t t_end, double* d_f, int64_t ld_f);
+int ptrom_dev_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* d_x, const float* d_gamma,
+                                    float delta, int form, const float* d_inflow, int64_t t_begin,
+                                    int64_t t_end, float* d_f, int64_t ld_f);
+/* kernel.hpp:154-170 restricted to rows [t_begin, t_end); four vectors of
+ * length t_end - t_begin. */
+int ptrom_dev_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* d_x,
+                                          const double* d_gamma, double delta, int form, int64_t t_begin,
+                                          int64_t t_end, double* d_jxx, double* d_jxy, double* d_jyx,
+                                          double* d_jyy);
+/* Newton-block refactor fused with the Jacobian (integrators.hpp:181-194):
+ * inv = (I - dt/2 J_i)^{-1} for rows [t_begin,t_end), row-major 4 per particle.
+ * A singular block latches status 3 "singular Newton block for particle i". */
+int ptrom_dev_newton_blocks_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                double delta, int form, double dt, int64_t t_begin, int64_t t_end,
+                                double* d_inv /* 4*(t_end-t_begin) */);
+/* integrators.hpp:47-53 residual on m rows of a shard (local layout: rows k
+ * and k+ld), plus its squared 2-norm summed in a fixed order into
+ * *d_norm2 (one double, device). */
+int ptrom_dev_residual_f64(ptrom_ctx* ctx, int64_t m, int64_t ld, const double* d_xi, const double* d_fxi,
+                           const double* d_xprev, const double* d_fprev, double dt, double* d_r,
+                           double* d_norm2);
+/* integrators.hpp:161-167: x[k] += inv_k * (-r) for m local rows. */
+int ptrom_dev_newton_update_f64(ptrom_ctx* ctx, int64_t m, int64_t ld, const double* d_inv, const double* d_r,
+                                double* d_x);
+
+/* --------------------------------------------------------- instrumentation -- */
+/* bench.py support: while enabled, the context records CUDA events on its own
+ * stream around every launch of the dominant kernel of each call (the
+ * all-pairs tile kernel, the tree traversal kernel, the hyperpair kernel).
+ * ptrom_profile_end synchronizes and returns the summed duration and the
+ * number of launches, then disables recording. */
+int ptrom_profile_begin(ptrom_ctx* ctx);
+int ptrom_profile_end(ptrom_ctx* ctx, double* total_ms, int64_t* launches);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PTROM_B200_H */

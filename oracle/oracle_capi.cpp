@@ -1,0 +1,347 @@
+// oracle_capi.cpp — C entry points over the CPU ORACLE (test infrastructure
+// only: called from tests/, __graft_entry__.smoke() and bench.py's CPU legs).
+// Status codes mirror the product ABI: 0 ok, 2 config_error, 3 numerical_error.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "ptrom_oracle.hpp"
+#include "ptrom_oracle_tree.hpp"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+using namespace oracle;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const config_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const numerical_error& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+template <class S>
+ParticleSystem<S> make_sys(std::int64_t n, const S* gamma, S delta, int form, const S* inflow) {
+  ParticleSystem<S> sys;
+  sys.circulation.assign(gamma, gamma + n);
+  sys.delta = delta;
+  sys.kernel_form = form ? KernelForm::denominator_scaled : KernelForm::standard;
+  if (inflow) {
+    sys.has_inflow = true;
+    sys.inflow.assign(inflow, inflow + 2 * n);
+  }
+  return sys;
+}
+
+// Target-parallel pairwise model (OpenMP over targets; each target's sum is
+// still the reference's sequential loop). n_threads == 1 is the reference's
+// serial protocol.
+template <class S>
+struct ThreadedPairwiseModel {
+  ParticleSystem<S> sys;
+  int n_threads = 1;
+  std::vector<S> velocity(const std::vector<S>& x) const {
+    sys.validate();
+    check_state<S>(x, sys, "pairwise_velocity");
+    std::vector<S> f(x.size(), S(0));
+    rows(x, f.data(), 0, sys.size());
+    return f;
+  }
+  void rows(const std::vector<S>& x, S* f, Index b, Index e) const {
+    if (n_threads <= 1) {
+      pairwise_velocity_rows<S>(x, sys, b, e, f);
+      return;
+    }
+    std::string err;
+    int code = 0;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(n_threads)
+    for (Index i = b; i < e; ++i) {
+      try {
+        pairwise_velocity_rows<S>(x, sys, i, i + 1, f);
+      } catch (const numerical_error& ex) {
+#pragma omp critical
+        {
+          code = 3;
+          err = ex.what();
+        }
+      }
+    }
+    if (code == 3) throw numerical_error(err);
+  }
+  BlockDiagonalJacobian<S> jacobian(const std::vector<S>& x) const {
+    sys.validate();
+    check_state<S>(x, sys, "inexact_kernel_jacobian");
+    auto jac = BlockDiagonalJacobian<S>::Zero(sys.size());
+    jac_rows(x, jac, 0, sys.size());
+    return jac;
+  }
+  void jac_rows(const std::vector<S>& x, BlockDiagonalJacobian<S>& jac, Index b, Index e) const {
+    if (n_threads <= 1) {
+      inexact_kernel_jacobian_rows<S>(x, sys, b, e, jac);
+      return;
+    }
+    std::string err;
+    int code = 0;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(n_threads)
+    for (Index i = b; i < e; ++i) {
+      try {
+        inexact_kernel_jacobian_rows<S>(x, sys, i, i + 1, jac);
+      } catch (const numerical_error& ex) {
+#pragma omp critical
+        {
+          code = 3;
+          err = ex.what();
+        }
+      }
+    }
+    if (code == 3) throw numerical_error(err);
+  }
+};
+
+void check_range(std::int64_t n, std::int64_t b, std::int64_t e) {
+  if (b < 0 || e > n || b > e) throw config_error("target range outside [0, n]");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error() { return g_err.c_str(); }
+std::uint64_t oracle_kernel_eval_count() { return kernel_eval_counter; }
+void oracle_reset_kernel_eval_count() { kernel_eval_counter = 0; }
+
+int oracle_kernel_pair_f64(double tx, double ty, double sx, double sy, double gamma, double delta, int form,
+                           double* out) {
+  return guarded([&] {
+    const V2<double> k = kernel_pair<double>({tx, ty}, {sx, sy}, gamma, delta,
+                                             form ? KernelForm::denominator_scaled : KernelForm::standard);
+    out[0] = k.x;
+    out[1] = k.y;
+  });
+}
+
+int oracle_kernel_pair_jacobian_f64(double tx, double ty, double sx, double sy, double gamma, double delta,
+                                    int form, double* out) {
+  return guarded([&] {
+    const M2<double> j = kernel_pair_jacobian<double>({tx, ty}, {sx, sy}, gamma, delta,
+                                                      form ? KernelForm::denominator_scaled : KernelForm::standard);
+    out[0] = j.a00;
+    out[1] = j.a01;
+    out[2] = j.a10;
+    out[3] = j.a11;
+  });
+}
+
+// kernel.hpp:107-129 over targets [t_begin, t_end) (rows outside stay 0).
+int oracle_pairwise_velocity_f64(std::int64_t n, const double* x, const double* gamma, double delta, int form,
+                                 const double* inflow, std::int64_t t_begin, std::int64_t t_end, int n_threads,
+                                 double* f) {
+  return guarded([&] {
+    ThreadedPairwiseModel<double> m{make_sys<double>(n, gamma, delta, form, inflow), n_threads};
+    m.sys.validate();
+    std::vector<double> xs(x, x + 2 * n);
+    check_state<double>(xs, m.sys, "pairwise_velocity");
+    check_range(n, t_begin, t_end);
+    std::memset(f, 0, sizeof(double) * 2 * n);
+    m.rows(xs, f, t_begin, t_end);
+  });
+}
+
+int oracle_pairwise_velocity_f32(std::int64_t n, const float* x, const float* gamma, float delta, int form,
+                                 const float* inflow, std::int64_t t_begin, std::int64_t t_end, int n_threads,
+                                 float* f) {
+  return guarded([&] {
+    ThreadedPairwiseModel<float> m{make_sys<float>(n, gamma, delta, form, inflow), n_threads};
+    m.sys.validate();
+    std::vector<float> xs(x, x + 2 * n);
+    check_state<float>(xs, m.sys, "pairwise_velocity");
+    check_range(n, t_begin, t_end);
+    std::memset(f, 0, sizeof(float) * 2 * n);
+    m.rows(xs, f, t_begin, t_end);
+  });
+}
+
+// kernel.hpp:154-170 over targets [t_begin, t_end).
+int oracle_inexact_kernel_jacobian_f64(std::int64_t n, const double* x, const double* gamma, double delta,
+                                       int form, std::int64_t t_begin, std::int64_t t_end, int n_threads,
+                                       double* jxx, double* jxy, double* jyx, double* jyy) {
+  return guarded([&] {
+    ThreadedPairwiseModel<double> m{make_sys<double>(n, gamma, delta, form, nullptr), n_threads};
+    m.sys.validate();
+    std::vector<double> xs(x, x + 2 * n);
+    check_state<double>(xs, m.sys, "inexact_kernel_jacobian");
+    check_range(n, t_begin, t_end);
+    auto jac = BlockDiagonalJacobian<double>::Zero(n);
+    m.jac_rows(xs, jac, t_begin, t_end);
+    std::memcpy(jxx, jac.dfx_dx.data(), sizeof(double) * n);
+    std::memcpy(jxy, jac.dfx_dy.data(), sizeof(double) * n);
+    std::memcpy(jyx, jac.dfy_dx.data(), sizeof(double) * n);
+    std::memcpy(jyy, jac.dfy_dy.data(), sizeof(double) * n);
+  });
+}
+
+int oracle_hamiltonian_f64(std::int64_t n, const double* x, const double* gamma, double* out) {
+  return guarded([&] {
+    auto sys = make_sys<double>(n, gamma, 0.0, 0, nullptr);
+    std::vector<double> xs(x, x + 2 * n);
+    *out = hamiltonian<double>(xs, sys);
+  });
+}
+
+// integrators.hpp:243-272 with the PairwiseModel (optionally target-threaded).
+int oracle_fom_simulate_f64(std::int64_t n, const double* x0, const double* gamma, double delta, int form,
+                            const double* inflow, double dt, std::int64_t n_steps, double tol, int max_iters,
+                            int refresh, int n_threads, double* snapshots, int* iters, std::uint8_t* converged,
+                            double* rel) {
+  return guarded([&] {
+    ThreadedPairwiseModel<double> m{make_sys<double>(n, gamma, delta, form, inflow), n_threads};
+    NewtonConfig cfg{tol, max_iters, refresh};
+    std::vector<double> xs(x0, x0 + 2 * n);
+    auto res = fom_simulate<double>(xs, m, dt, n_steps, cfg);
+    std::memcpy(snapshots, res.snapshots.data(), sizeof(double) * res.snapshots.size());
+    for (std::int64_t s = 0; s < n_steps; ++s) {
+      iters[s] = res.iterations[static_cast<size_t>(s)];
+      converged[s] = static_cast<std::uint8_t>(res.converged[static_cast<size_t>(s)]);
+      rel[s] = res.relative_residual[static_cast<size_t>(s)];
+    }
+  });
+}
+
+// ---------------------------------------------------------------- tree ----
+struct oracle_tree {
+  QuadTree<double> t;
+};
+
+int oracle_tree_build_f64(std::int64_t n, const double* px, const double* py, const double* gamma,
+                          std::int64_t leaf_capacity, oracle_tree** out) {
+  return guarded([&] {
+    auto* h = new oracle_tree;
+    try {
+      h->t = build_tree<double>(std::vector<double>(px, px + n), std::vector<double>(py, py + n),
+                                std::vector<double>(gamma, gamma + n), leaf_capacity);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void oracle_tree_free(oracle_tree* h) { delete h; }
+std::int64_t oracle_tree_num_nodes(const oracle_tree* h) { return static_cast<std::int64_t>(h->t.nodes.size()); }
+
+// Node table in structure-of-arrays form, matching the product's export.
+void oracle_tree_export(const oracle_tree* h, double* bounds /*4*nn*/, double* width, double* centroid /*2*nn*/,
+                        double* gamma_sum, std::int32_t* children /*4*nn*/, std::int64_t* begin, std::int64_t* end,
+                        std::int32_t* depth, std::uint8_t* fallback, std::int64_t* perm, std::int64_t* slot,
+                        std::int32_t* leaf_node) {
+  const auto& t = h->t;
+  for (size_t i = 0; i < t.nodes.size(); ++i) {
+    const auto& nd = t.nodes[i];
+    for (int k = 0; k < 4; ++k) {
+      bounds[4 * i + k] = nd.bounds[static_cast<size_t>(k)];
+      children[4 * i + k] = nd.children[static_cast<size_t>(k)];
+    }
+    width[i] = nd.width;
+    centroid[2 * i] = nd.centroid.x;
+    centroid[2 * i + 1] = nd.centroid.y;
+    gamma_sum[i] = nd.gamma_sum;
+    begin[i] = nd.begin;
+    end[i] = nd.end;
+    depth[i] = nd.depth;
+    fallback[i] = nd.centroid_fallback ? 1 : 0;
+  }
+  for (size_t p = 0; p < t.perm.size(); ++p) {
+    perm[p] = t.perm[p];
+    slot[p] = t.slot[p];
+    leaf_node[p] = t.leaf_node[p];
+  }
+}
+
+// quadtree.hpp:213-252. Returns the list lengths; copies at most the given
+// capacities.
+int oracle_collect_clusters(const oracle_tree* h, std::int64_t target, int crit_kind, double crit_value,
+                            std::int32_t* nodes, std::int64_t nodes_cap, std::int64_t* direct,
+                            std::int64_t direct_cap, std::int64_t* n_nodes, std::int64_t* n_direct) {
+  return guarded([&] {
+    const auto crit = crit_kind ? ClusterCriterion<double>::neighbor(crit_value)
+                                : ClusterCriterion<double>::barnes_hut(crit_value);
+    const ClusterList cl = collect_clusters(h->t, target, crit);
+    *n_nodes = static_cast<std::int64_t>(cl.cluster_nodes.size());
+    *n_direct = static_cast<std::int64_t>(cl.direct_ids.size());
+    for (size_t k = 0; k < cl.cluster_nodes.size() && static_cast<std::int64_t>(k) < nodes_cap; ++k)
+      nodes[k] = cl.cluster_nodes[k];
+    for (size_t k = 0; k < cl.direct_ids.size() && static_cast<std::int64_t>(k) < direct_cap; ++k)
+      direct[k] = cl.direct_ids[k];
+  });
+}
+
+// quadtree.hpp:257-281 over targets [t_begin, t_end).
+int oracle_bh_velocity_f64(const oracle_tree* h, std::int64_t n, const double* x, const double* gamma,
+                           double delta, int form, const double* inflow, int crit_kind, double crit_value,
+                           std::int64_t t_begin, std::int64_t t_end, int n_threads, double* f) {
+  return guarded([&] {
+    auto sys = make_sys<double>(n, gamma, delta, form, inflow);
+    sys.validate();
+    std::vector<double> xs(x, x + 2 * n);
+    check_state<double>(xs, sys, "bh_velocity");
+    if (h->t.size() != n) throw config_error("bh_velocity: tree size mismatch");
+    check_range(n, t_begin, t_end);
+    const auto crit = crit_kind ? ClusterCriterion<double>::neighbor(crit_value)
+                                : ClusterCriterion<double>::barnes_hut(crit_value);
+    std::memset(f, 0, sizeof(double) * 2 * n);
+    if (n_threads <= 1) {
+      bh_velocity_rows<double>(h->t, xs, sys, crit, t_begin, t_end, f);
+      return;
+    }
+    int code = 0;
+    std::string err;
+#pragma omp parallel for schedule(dynamic, 256) num_threads(n_threads)
+    for (std::int64_t i = t_begin; i < t_end; ++i) {
+      try {
+        bh_velocity_rows<double>(h->t, xs, sys, crit, i, i + 1, f);
+      } catch (const numerical_error& ex) {
+#pragma omp critical
+        {
+          code = 3;
+          err = ex.what();
+        }
+      }
+    }
+    if (code) throw numerical_error(err);
+  });
+}
+
+int oracle_bh_jacobian_f64(const oracle_tree* h, std::int64_t n, const double* x, const double* gamma,
+                           double delta, int form, int crit_kind, double crit_value, double* jxx, double* jxy,
+                           double* jyx, double* jyy) {
+  return guarded([&] {
+    auto sys = make_sys<double>(n, gamma, delta, form, nullptr);
+    std::vector<double> xs(x, x + 2 * n);
+    const auto crit = crit_kind ? ClusterCriterion<double>::neighbor(crit_value)
+                                : ClusterCriterion<double>::barnes_hut(crit_value);
+    auto jac = bh_jacobian<double>(h->t, xs, sys, crit);
+    std::memcpy(jxx, jac.dfx_dx.data(), sizeof(double) * n);
+    std::memcpy(jxy, jac.dfx_dy.data(), sizeof(double) * n);
+    std::memcpy(jyx, jac.dfy_dx.data(), sizeof(double) * n);
+    std::memcpy(jyy, jac.dfy_dy.data(), sizeof(double) * n);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+"""ctypes wrapper of the CPU ORACLE (oracle/build/libptrom_oracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, always as the checker or the
+CPU baseline — never by the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "build", "libptrom_oracle.so")
+KAT = os.path.join(HERE, "build", "kat")
+
+
+def build() -> None:
+    subprocess.run(["make", "-C", HERE, "-j4"], check=True, stdout=subprocess.DEVNULL)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            build()
+        _lib = C.CDLL(LIB)
+        _lib.oracle_last_error.restype = C.c_char_p
+        _lib.oracle_kernel_eval_count.restype = C.c_uint64
+        _lib.oracle_tree_num_nodes.restype = C.c_int64
+        _lib.oracle_tree_build_f64.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                               C.POINTER(C.c_void_p)]
+        _lib.oracle_tree_free.argtypes = [C.c_void_p]
+        _lib.oracle_tree_num_nodes.argtypes = [C.c_void_p]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().oracle_last_error().decode())
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def pairwise_velocity(x, gamma, delta, form=0, inflow=None, t_begin=0, t_end=None, threads=1):
+    """kernel.hpp:107-129 over target rows [t_begin, t_end) (others zero)."""
+    dtype = np.float32 if np.asarray(x).dtype == np.float32 else np.float64
+    x = np.ascontiguousarray(x, dtype=dtype)
+    g = np.ascontiguousarray(gamma, dtype=dtype)
+    inf = None if inflow is None else np.ascontiguousarray(inflow, dtype=dtype)
+    n = g.shape[0]
+    t_end = n if t_end is None else t_end
+    f = np.zeros(2 * n, dtype=dtype)
+    if dtype == np.float32:
+        _check(lib().oracle_pairwise_velocity_f32(C.c_int64(n), _p(x), _p(g), C.c_float(delta), C.c_int(form),
+                                                  _p(inf), C.c_int64(t_begin), C.c_int64(t_end), C.c_int(threads),
+                                                  _p(f)))
+    else:
+        _check(lib().oracle_pairwise_velocity_f64(C.c_int64(n), _p(x), _p(g), C.c_double(delta), C.c_int(form),
+                                                  _p(inf), C.c_int64(t_begin), C.c_int64(t_end), C.c_int(threads),
+                                                  _p(f)))
+    return f
+
+
+def inexact_kernel_jacobian(x, gamma, delta, form=0, t_begin=0, t_end=None, threads=1):
+    """kernel.hpp:154-170 → (4, N) dfx_dx, dfx_dy, dfy_dx, dfy_dy."""
+    x, g = _f64(x), _f64(gamma)
+    n = g.shape[0]
+    t_end = n if t_end is None else t_end
+    out = np.zeros((4, n))
+    _check(lib().oracle_inexact_kernel_jacobian_f64(C.c_int64(n), _p(x), _p(g), C.c_double(delta), C.c_int(form),
+                                                    C.c_int64(t_begin), C.c_int64(t_end), C.c_int(threads),
+                                                    _p(out[0]), _p(out[1]), _p(out[2]), _p(out[3])))
+    return out
+
+
+def fom_simulate(x0, gamma, delta, dt, n_steps, form=0, inflow=None, tol=1e-10, max_iters=100, refresh=1,
+                 threads=1):
+    """integrators.hpp:243-272 → (snapshots (2N, steps), iterations, converged, relative_residual)."""
+    x0, g, inf = _f64(x0), _f64(gamma), _f64(inflow)
+    n = g.shape[0]
+    snaps = np.zeros((n_steps, 2 * n))
+    iters = np.zeros(n_steps, dtype=np.int32)
+    conv = np.zeros(n_steps, dtype=np.uint8)
+    rel = np.zeros(n_steps)
+    _check(lib().oracle_fom_simulate_f64(C.c_int64(n), _p(x0), _p(g), C.c_double(delta), C.c_int(form), _p(inf),
+                                         C.c_double(dt), C.c_int64(n_steps), C.c_double(tol), C.c_int(max_iters),
+                                         C.c_int(refresh), C.c_int(threads), _p(snaps), _p(iters), _p(conv),
+                                         _p(rel)))
+    return snaps.T, iters, conv, rel
+
+
+class Tree:
+    """quadtree.hpp:124-162 build_tree; arrays exported in SoA form."""
+
+    def __init__(self, px, py, gamma, leaf_capacity):
+        self.px, self.py, self.gamma = _f64(px), _f64(py), _f64(gamma)
+        self.n = self.px.shape[0]
+        h = C.c_void_p()
+        _check(lib().oracle_tree_build_f64(self.n, _p(self.px), _p(self.py), _p(self.gamma), leaf_capacity,
+                                           C.byref(h)))
+        self.h = h
+        nn = lib().oracle_tree_num_nodes(h)
+        self.num_nodes = nn
+        self.bounds = np.zeros((nn, 4))
+        self.width = np.zeros(nn)
+        self.centroid = np.zeros((nn, 2))
+        self.gamma_sum = np.zeros(nn)
+        self.children = np.zeros((nn, 4), dtype=np.int32)
+        self.begin = np.zeros(nn, dtype=np.int64)
+        self.end = np.zeros(nn, dtype=np.int64)
+        self.depth = np.zeros(nn, dtype=np.int32)
+        self.fallback = np.zeros(nn, dtype=np.uint8)
+        self.perm = np.zeros(self.n, dtype=np.int64)
+        self.slot = np.zeros(self.n, dtype=np.int64)
+        self.leaf_node = np.zeros(self.n, dtype=np.int32)
+        lib().oracle_tree_export(h, *(_p(a) for a in (self.bounds, self.width, self.centroid, self.gamma_sum,
+                                                       self.children, self.begin, self.end, self.depth,
+                                                       self.fallback, self.perm, self.slot, self.leaf_node)))
+
+    def collect_clusters(self, target, crit_kind, crit_value):
+        nn, nd = C.c_int64(), C.c_int64()
+        _check(lib().oracle_collect_clusters(self.h, C.c_int64(target), C.c_int(crit_kind), C.c_double(crit_value),
+                                             None, C.c_int64(0), None, C.c_int64(0), C.byref(nn), C.byref(nd)))
+        nodes = np.zeros(nn.value, dtype=np.int32)
+        direct = np.zeros(nd.value, dtype=np.int64)
+        _check(lib().oracle_collect_clusters(self.h, C.c_int64(target), C.c_int(crit_kind), C.c_double(crit_value),
+                                             _p(nodes), C.c_int64(nn.value), _p(direct), C.c_int64(nd.value),
+                                             C.byref(nn), C.byref(nd)))
+        return nodes, direct
+
+    def bh_velocity(self, x, gamma, delta, crit_kind, crit_value, form=0, inflow=None, t_begin=0, t_end=None,
+                    threads=1):
+        x, g, inf = _f64(x), _f64(gamma), _f64(inflow)
+        t_end = self.n if t_end is None else t_end
+        f = np.zeros(2 * self.n)
+        _check(lib().oracle_bh_velocity_f64(self.h, C.c_int64(self.n), _p(x), _p(g), C.c_double(delta),
+                                            C.c_int(form), _p(inf), C.c_int(crit_kind), C.c_double(crit_value),
+                                            C.c_int64(t_begin), C.c_int64(t_end), C.c_int(threads), _p(f)))
+        return f
+
+    def bh_jacobian(self, x, gamma, delta, crit_kind, crit_value, form=0):
+        x, g = _f64(x), _f64(gamma)
+        out = np.zeros((4, self.n))
+        _check(lib().oracle_bh_jacobian_f64(self.h, C.c_int64(self.n), _p(x), _p(g), C.c_double(delta),
+                                            C.c_int(form), C.c_int(crit_kind), C.c_double(crit_value),
+                                            _p(out[0]), _p(out[1]), _p(out[2]), _p(out[3])))
+        return out
+
+    def __del__(self):
+        try:
+            lib().oracle_tree_free(self.h)
+        except Exception:
+            pass

@@ -1,0 +1,475 @@
+// allpairs.cu — O(N^2) regularized Biot–Savart evaluation on sm_100a.
+//
+// Replaces the scalar double loops of the reference:
+//   pairwise_velocity       kernel.hpp:107-129  (kernel_pair kernel.hpp:29-42)
+//   inexact_kernel_jacobian kernel.hpp:154-170  (kernel_pair_jacobian kernel.hpp:45-73)
+//
+// Both kernel forms reduce to one law with Γ' = Γ/(2π):
+//   standard:           pre = Γ/(2π(d²+δ))       = Γ'/(d²+δ)
+//   denominator_scaled: pre = Γ/(2πd²+δ)         = Γ'/(d²+δ/(2π))
+// so the device works with q = d² + δ' (δ' = δ or δ/2π) and s = Γ'/q:
+//   v  += s·(−ry, rx)
+//   J  += s/q·[[2rx·ry, ry²−rx²−δ'], [ry²−rx²+δ', −2rx·ry]]
+// and the Jacobian is accumulated as A=Σw·rx·ry, B=Σw·(ry²−rx²), C=Σw
+// (w = s/q): J = [[2A, B−δ'C], [B+δ'C, −2A]].
+//
+// Work decomposition (FP64-pipe bound):
+//   grid.x = target tiles of TPB·T targets (T targets per thread kept in
+//   registers), grid.y = source chunks chosen so grid.x·grid.y fills whole
+//   waves of resident blocks on 148 SMs. Each block streams its source chunk
+//   through shared memory in tiles of TPB sources (double2 position + Γ'
+//   broadcast loads) and writes one partial per (target, chunk); a reduce
+//   kernel sums the chunks in ascending order (fixed-order, deterministic),
+//   adds the inflow and latches a numerical error on a non-finite result
+//   (a coincident pair with δ = 0, the reference's throw at kernel.hpp:38-39).
+//
+// Reciprocal: MUFU.RCP64H seed (rcp.approx.ftz.f64) + one cubic correction
+// y = y0(1+e+e²), e = 1−q·y0 (3 DFMA incl. the Γ' scale): ~1 ulp, 10 FP64
+// pipe ops per velocity pair instead of the ~14 of an IEEE division.
+#include <algorithm>
+#include <cmath>
+
+#include "ops.cuh"
+
+namespace ptrom {
+
+__device__ __forceinline__ double rcp_seed(double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float q) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(q));
+  return y;
+}
+
+// ----------------------------------------------------------------- fp64 ---
+// One source tile against T register-resident targets of this thread.
+template <int T, bool VEL, bool JAC, bool MASK>
+__device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp, const double* __restrict__ sg,
+                                         long long j0, const double (&tx)[T], const double (&ty)[T],
+                                         const long long (&ti)[T], double dp, double (&fx)[T], double (&fy)[T],
+                                         double (&ja)[T], double (&jb)[T], double (&jc)[T]) {
+#pragma unroll 4
+  for (int jj = 0; jj < cnt; ++jj) {
+    const double2 p = sp[jj];
+    const double g = sg[jj];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const double rx = tx[k] - p.x;
+      const double ry = ty[k] - p.y;
+      double q = fma(rx, rx, fma(ry, ry, dp));
+      double gs = g;
+      if (MASK) {
+        const bool self = (j0 + jj) == ti[k];  // kernel.hpp:118 `if (j == i) continue;`
+        q = self ? 1.0 : q;
+        gs = self ? 0.0 : gs;
+      }
+      const double y0 = rcp_seed(q);
+      double e = fma(-q, y0, 1.0);
+      e = fma(e, e, e);
+      if (JAC) {
+        const double u = fma(y0, e, y0);  // 1/q
+        const double s = gs * u;          // Γ'/q
+        const double w = s * u;           // Γ'/q²
+        const double t = w * rx;
+        ja[k] = fma(t, ry, ja[k]);
+        const double rx2 = rx * rx;
+        jb[k] = fma(w, fma(ry, ry, -rx2), jb[k]);
+        jc[k] += w;
+        if (VEL) {
+          fx[k] = fma(-ry, s, fx[k]);
+          fy[k] = fma(rx, s, fy[k]);
+        }
+      } else {
+        const double g0 = gs * y0;
+        const double s = fma(g0, e, g0);  // Γ'/q
+        fx[k] = fma(-ry, s, fx[k]);
+        fy[k] = fma(rx, s, fy[k]);
+      }
+    }
+  }
+}
+
+template <int TPB, int T, bool VEL, bool JAC>
+__global__ void __launch_bounds__(TPB) allpairs_f64_kernel(long long n, const double* __restrict__ xs,
+                                                           const double* __restrict__ ys,
+                                                           const double* __restrict__ gam, double inv2pi,
+                                                           double dp, long long t_begin, long long t_count,
+                                                           long long chunk_len, double* __restrict__ part) {
+  constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
+  __shared__ double2 sp[TPB];
+  __shared__ double sg[TPB];
+
+  const int tid = threadIdx.x;
+  const long long tile0 = t_begin + (long long)blockIdx.x * (TPB * T);
+  double tx[T], ty[T], fx[T], fy[T], ja[T], jb[T], jc[T];
+  long long ti[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const long long i = tile0 + k * TPB + tid;
+    const bool ok = i < t_begin + t_count;
+    ti[k] = ok ? i : -1;
+    tx[k] = ok ? xs[i] : 0.0;
+    ty[k] = ok ? ys[i] : 0.0;
+    fx[k] = fy[k] = ja[k] = jb[k] = jc[k] = 0.0;
+  }
+  const long long tile_end = min(tile0 + (long long)TPB * T, t_begin + t_count);
+
+  const long long cbeg = (long long)blockIdx.y * chunk_len;
+  const long long cend = min(n, cbeg + chunk_len);
+
+  // Register prefetch of the first source tile.
+  double px = 0.0, py = 0.0, pg = 0.0;
+  if (cbeg + tid < cend) {
+    px = xs[cbeg + tid];
+    py = ys[cbeg + tid];
+    pg = gam[cbeg + tid] * inv2pi;
+  }
+  for (long long j0 = cbeg; j0 < cend; j0 += TPB) {
+    const int cnt = (int)min((long long)TPB, cend - j0);
+    sp[tid] = make_double2(px, py);
+    sg[tid] = pg;
+    __syncthreads();
+    const long long jn = j0 + TPB + tid;  // prefetch the next tile while computing
+    if (jn < cend) {
+      px = xs[jn];
+      py = ys[jn];
+      pg = gam[jn] * inv2pi;
+    }
+    const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt);
+    if (masked)
+      tile_f64<T, VEL, JAC, true>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+    else
+      tile_f64<T, VEL, JAC, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+    __syncthreads();
+  }
+
+  double* out = part + (long long)blockIdx.y * NCOMP * t_count;
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    if (ti[k] < 0) continue;
+    const long long li = ti[k] - t_begin;
+    int c = 0;
+    if (VEL) {
+      out[(c++) * t_count + li] = fx[k];
+      out[(c++) * t_count + li] = fy[k];
+    }
+    if (JAC) {
+      out[(c++) * t_count + li] = ja[k];
+      out[(c++) * t_count + li] = jb[k];
+      out[(c++) * t_count + li] = jc[k];
+    }
+  }
+}
+
+// Fixed-order chunk reduction + inflow + finiteness latch.
+__global__ void reduce_velocity_f64_kernel(long long n, long long t_begin, long long t_count, int n_chunks,
+                                           const double* __restrict__ part, int ncomp,
+                                           const double* __restrict__ inflow, double* __restrict__ f, long long ld,
+                                           DeviceStatus* st) {
+  for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < t_count;
+       li += (long long)gridDim.x * blockDim.x) {
+    double fx = 0.0, fy = 0.0;
+    for (int c = 0; c < n_chunks; ++c) {
+      fx += part[((long long)c * ncomp + 0) * t_count + li];
+      fy += part[((long long)c * ncomp + 1) * t_count + li];
+    }
+    const long long i = t_begin + li;
+    if (inflow) {
+      fx = fx + inflow[i];
+      fy = fy + inflow[i + n];
+    }
+    if (!isfinite(fx) || !isfinite(fy)) latch_status(st, kStatusNonFiniteVelocity, i);
+    f[li] = fx;
+    f[li + ld] = fy;
+  }
+}
+
+// Jacobian assembly from (A, B, C) partials; optionally the Newton-block
+// inverse of (I − h·J) (integrators.hpp:181-194, reference rounding order).
+template <bool INVERT>
+__global__ void reduce_jacobian_f64_kernel(long long t_begin, long long t_count, int n_chunks,
+                                           const double* __restrict__ part, int ncomp, int off, double dp,
+                                           double h, double* __restrict__ jxx, double* __restrict__ jxy,
+                                           double* __restrict__ jyx, double* __restrict__ jyy,
+                                           double* __restrict__ inv, DeviceStatus* st) {
+  for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < t_count;
+       li += (long long)gridDim.x * blockDim.x) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int ch = 0; ch < n_chunks; ++ch) {
+      const double* pc = part + (long long)ch * ncomp * t_count + li;
+      a += pc[(off + 0) * t_count];
+      b += pc[(off + 1) * t_count];
+      c += pc[(off + 2) * t_count];
+    }
+    const double j00 = 2.0 * a, j11 = -2.0 * a;
+    const double j01 = b - dp * c, j10 = b + dp * c;
+    const long long i = t_begin + li;
+    if (!INVERT) {
+      if (!isfinite(j00) || !isfinite(j01) || !isfinite(j10)) latch_status(st, kStatusNonFiniteJacobian, i);
+      jxx[li] = j00;
+      jxy[li] = j01;
+      jyx[li] = j10;
+      jyy[li] = j11;
+    } else {
+      const double b00 = __dsub_rn(1.0, __dmul_rn(h, j00));
+      const double b01 = __dsub_rn(0.0, __dmul_rn(h, j01));
+      const double b10 = __dsub_rn(0.0, __dmul_rn(h, j10));
+      const double b11 = __dsub_rn(1.0, __dmul_rn(h, j11));
+      const double det = __dsub_rn(__dmul_rn(b00, b11), __dmul_rn(b01, b10));
+      if (det == 0.0 || !isfinite(det)) latch_status(st, kStatusSingularBlock, i);
+      double* o = inv + 4 * li;
+      o[0] = __ddiv_rn(b11, det);
+      o[1] = __ddiv_rn(-b01, det);
+      o[2] = __ddiv_rn(-b10, det);
+      o[3] = __ddiv_rn(b00, det);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- fp32 ---
+// fp32 pairs; each shared-memory tile is summed in fp32 and promoted into
+// fp64 accumulators (blocked summation keeps the fp32 result within 1e-5 of
+// the fp64 oracle at N = 65,536).
+template <int TPB, int T>
+__global__ void __launch_bounds__(TPB) allpairs_f32_kernel(long long n, const float* __restrict__ xs,
+                                                           const float* __restrict__ ys,
+                                                           const float* __restrict__ gam, float inv2pi, float dp,
+                                                           long long t_begin, long long t_count,
+                                                           long long chunk_len, double* __restrict__ part) {
+  __shared__ float2 sp[TPB];
+  __shared__ float sg[TPB];
+  const int tid = threadIdx.x;
+  const long long tile0 = t_begin + (long long)blockIdx.x * (TPB * T);
+  float tx[T], ty[T];
+  double fx[T], fy[T];
+  long long ti[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const long long i = tile0 + k * TPB + tid;
+    const bool ok = i < t_begin + t_count;
+    ti[k] = ok ? i : -1;
+    tx[k] = ok ? xs[i] : 0.f;
+    ty[k] = ok ? ys[i] : 0.f;
+    fx[k] = fy[k] = 0.0;
+  }
+  const long long tile_end = min(tile0 + (long long)TPB * T, t_begin + t_count);
+  const long long cbeg = (long long)blockIdx.y * chunk_len;
+  const long long cend = min(n, cbeg + chunk_len);
+  float px = 0.f, py = 0.f, pg = 0.f;
+  if (cbeg + tid < cend) {
+    px = xs[cbeg + tid];
+    py = ys[cbeg + tid];
+    pg = gam[cbeg + tid] * inv2pi;
+  }
+  for (long long j0 = cbeg; j0 < cend; j0 += TPB) {
+    const int cnt = (int)min((long long)TPB, cend - j0);
+    sp[tid] = make_float2(px, py);
+    sg[tid] = pg;
+    __syncthreads();
+    const long long jn = j0 + TPB + tid;
+    if (jn < cend) {
+      px = xs[jn];
+      py = ys[jn];
+      pg = gam[jn] * inv2pi;
+    }
+    const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt);
+    float ax[T], ay[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) ax[k] = ay[k] = 0.f;
+#pragma unroll 8
+    for (int jj = 0; jj < cnt; ++jj) {
+      const float2 p = sp[jj];
+      const float g = sg[jj];
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        const float rx = tx[k] - p.x;
+        const float ry = ty[k] - p.y;
+        float q = fmaf(rx, rx, fmaf(ry, ry, dp));
+        float gs = g;
+        if (masked) {
+          const bool self = (j0 + jj) == ti[k];
+          q = self ? 1.f : q;
+          gs = self ? 0.f : gs;
+        }
+        const float s = gs * rcp_approx(q);
+        ax[k] = fmaf(-ry, s, ax[k]);
+        ay[k] = fmaf(rx, s, ay[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      fx[k] += (double)ax[k];
+      fy[k] += (double)ay[k];
+    }
+    __syncthreads();
+  }
+  double* out = part + (long long)blockIdx.y * 2 * t_count;
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    if (ti[k] < 0) continue;
+    const long long li = ti[k] - t_begin;
+    out[li] = fx[k];
+    out[t_count + li] = fy[k];
+  }
+}
+
+__global__ void reduce_velocity_f32_kernel(long long n, long long t_begin, long long t_count, int n_chunks,
+                                           const double* __restrict__ part, const float* __restrict__ inflow,
+                                           float* __restrict__ f, long long ld, DeviceStatus* st) {
+  for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < t_count;
+       li += (long long)gridDim.x * blockDim.x) {
+    double fx = 0.0, fy = 0.0;
+    for (int c = 0; c < n_chunks; ++c) {
+      fx += part[((long long)c * 2 + 0) * t_count + li];
+      fy += part[((long long)c * 2 + 1) * t_count + li];
+    }
+    const long long i = t_begin + li;
+    float ox = (float)fx, oy = (float)fy;
+    if (inflow) {
+      ox = ox + inflow[i];
+      oy = oy + inflow[i + n];
+    }
+    if (!isfinite(ox) || !isfinite(oy)) latch_status(st, kStatusNonFiniteVelocity, i);
+    f[li] = ox;
+    f[li + ld] = oy;
+  }
+}
+
+// ------------------------------------------------------------ launchers ---
+int choose_source_chunks(ptrom_ctx* ctx, long long n_tiles, long long n_sources, int resident_per_sm,
+                         long long min_chunk) {
+  const long long slots = (long long)ctx->num_sms * std::max(1, resident_per_sm);
+  const long long max_chunks = std::max(1LL, std::min(512LL, n_sources / std::max(1LL, min_chunk)));
+  int best = 1;
+  double best_eff = -1.0;
+  for (long long c = 1; c <= max_chunks; ++c) {
+    const long long blocks = n_tiles * c;
+    const double waves = (double)blocks / (double)slots;
+    const double eff = waves / std::ceil(waves);  // fraction of the last-wave slots in use
+    // Prefer fewer chunks unless more chunks give a clearly better wave fill.
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = (int)c;
+    }
+    if (blocks >= 8 * slots) break;
+  }
+  return best;
+}
+
+namespace {
+
+constexpr int kTPB = 128;
+constexpr int kReduceThreads = 256;
+
+template <class K>
+int resident_blocks(K kernel, int tpb) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, tpb, 0);
+  return std::max(occ, 1);
+}
+
+int reduce_grid(ptrom_ctx* ctx, long long count) {
+  long long g = (count + kReduceThreads - 1) / kReduceThreads;
+  return (int)std::max(1LL, std::min(g, (long long)ctx->num_sms * 8));
+}
+
+template <int T, bool VEL, bool JAC>
+void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
+                           long long t_begin, long long t_count, double** part_out, int* chunks_out) {
+  auto kern = allpairs_f64_kernel<kTPB, T, VEL, JAC>;
+  static int occ = resident_blocks(kern, kTPB);
+  constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
+  const long long tiles = (t_count + kTPB * T - 1) / (kTPB * T);
+  const int chunks = choose_source_chunks(ctx, tiles, n, occ, 2 * kTPB);
+  const long long chunk_len = (n + chunks - 1) / chunks;
+  ctx->scratch.reset();
+  ctx->scratch.reserve((size_t)chunks * NCOMP * t_count * sizeof(double) + 4096);
+  double* part = ctx->scratch.take<double>((size_t)chunks * NCOMP * t_count);
+  dim3 grid((unsigned)tiles, (unsigned)chunks);
+  const double inv2pi = 1.0 / (2.0 * M_PI);
+  {
+    ProfScope prof(ctx);
+    kern<<<grid, kTPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part);
+  }
+  PTROM_LAUNCH_CHECK();
+  *part_out = part;
+  *chunks_out = chunks;
+}
+
+// Small target sets get one target per thread (more blocks); large sets
+// keep 4 targets per thread in registers to amortize the shared loads.
+template <bool VEL, bool JAC>
+void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
+                         long long t_begin, long long t_count, double** part, int* chunks) {
+  if (t_count >= 16384)
+    launch_allpairs_f64_t<4, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+  else
+    launch_allpairs_f64_t<1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+}
+
+}  // namespace
+
+double effective_delta(double delta, int form) { return form == PTROM_FORM_STANDARD ? delta : delta / (2.0 * M_PI); }
+
+void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                      const double* inflow, long long t_begin, long long t_end, double* f, long long ld) {
+  const long long t_count = t_end - t_begin;
+  if (t_count <= 0) return;
+  double* part;
+  int chunks;
+  launch_allpairs_f64<true, false>(ctx, n, x, gamma, effective_delta(delta, form), t_begin, t_count, &part, &chunks);
+  reduce_velocity_f64_kernel<<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+      n, t_begin, t_count, chunks, part, 2, inflow, f, ld, ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
+void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                      long long t_begin, long long t_end, double* jxx, double* jxy, double* jyx, double* jyy,
+                      double dt_for_inverse, double* inv) {
+  const long long t_count = t_end - t_begin;
+  if (t_count <= 0) return;
+  double* part;
+  int chunks;
+  const double dp = effective_delta(delta, form);
+  launch_allpairs_f64<false, true>(ctx, n, x, gamma, dp, t_begin, t_count, &part, &chunks);
+  if (inv) {
+    reduce_jacobian_f64_kernel<true><<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+        t_begin, t_count, chunks, part, 3, 0, dp, dt_for_inverse / 2.0, nullptr, nullptr, nullptr, nullptr, inv,
+        ctx->d_status);
+  } else {
+    reduce_jacobian_f64_kernel<false><<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+        t_begin, t_count, chunks, part, 3, 0, dp, 0.0, jxx, jxy, jyx, jyy, nullptr, ctx->d_status);
+  }
+  PTROM_LAUNCH_CHECK();
+}
+
+void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
+                      const float* inflow, long long t_begin, long long t_end, float* f, long long ld) {
+  const long long t_count = t_end - t_begin;
+  if (t_count <= 0) return;
+  constexpr int T = 4;
+  auto kern = allpairs_f32_kernel<kTPB, T>;
+  static int occ = resident_blocks(kern, kTPB);
+  const long long tiles = (t_count + kTPB * T - 1) / (kTPB * T);
+  const int chunks = choose_source_chunks(ctx, tiles, n, occ, 2 * kTPB);
+  const long long chunk_len = (n + chunks - 1) / chunks;
+  ctx->scratch.reset();
+  ctx->scratch.reserve((size_t)chunks * 2 * t_count * sizeof(double) + 4096);
+  double* part = ctx->scratch.take<double>((size_t)chunks * 2 * t_count);
+  const float dp = (float)effective_delta((double)delta, form);
+  const float inv2pi = (float)(1.0 / (2.0 * M_PI));
+  {
+    ProfScope prof(ctx);
+    kern<<<dim3((unsigned)tiles, (unsigned)chunks), kTPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp,
+                                                                             t_begin, t_count, chunk_len, part);
+  }
+  PTROM_LAUNCH_CHECK();
+  reduce_velocity_f32_kernel<<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+      n, t_begin, t_count, chunks, part, inflow, f, ld, ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
+}  // namespace ptrom

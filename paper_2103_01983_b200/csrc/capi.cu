@@ -1,0 +1,306 @@
+// capi.cu — the C ABI (include/ptrom_b200.h): context lifecycle, status
+// mapping and the host-buffer drop-in entry points. Validation mirrors the
+// reference's ParticleSystem::validate / check_state (kernel.hpp:84-103) so
+// status codes and messages match the reference's exceptions.
+#include <climits>
+#include <cmath>
+#include <string>
+
+#include "ops.cuh"
+
+namespace ptrom {
+
+void check_device_status(ptrom_ctx* ctx) {
+  PTROM_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DeviceStatus), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+  const DeviceStatus st = *ctx->h_status;
+  if (st.kind == kStatusOk) return;
+  DeviceStatus clear{0, 0, LLONG_MAX};
+  PTROM_CUDA(cudaMemcpy(ctx->d_status, &clear, sizeof(clear), cudaMemcpyHostToDevice));
+  switch (st.kind) {
+    case kStatusSingularBlock:  // integrators.hpp:187-189
+      numerical_fail("singular Newton block for particle " + std::to_string(st.index));
+    case kStatusNonFiniteJacobian:  // kernel.hpp:55-56 / 64-65
+      numerical_fail("kernel_pair_jacobian: coincident target/source with zero desingularization (target " +
+                     std::to_string(st.index) + ")");
+    default:  // kernel.hpp:38-39
+      numerical_fail("kernel_pair: coincident target/source with zero desingularization (target " +
+                     std::to_string(st.index) + ")");
+  }
+}
+
+namespace {
+
+template <class F>
+int guarded(ptrom_ctx* ctx, F&& fn) {
+  if (!ctx) return PTROM_CONFIG_ERROR;
+  try {
+    cudaSetDevice(ctx->device);
+    fn();
+    ctx->err.clear();
+    return PTROM_OK;
+  } catch (const status_error& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return PTROM_CUDA_ERROR;
+  }
+}
+
+// kernel.hpp:84-93 ParticleSystem::validate + kernel.hpp:96-103 check_state.
+template <class S>
+void validate_system(long long n, const S* x, const S* gamma, S delta, int form, const S* inflow, const char* who) {
+  if (n <= 0) config_fail("particle system is empty");
+  if (form != PTROM_FORM_STANDARD && form != PTROM_FORM_DENOMINATOR_SCALED) config_fail("unknown kernel form");
+  for (long long i = 0; i < n; ++i)
+    if (!std::isfinite(gamma[i])) config_fail("non-finite circulation");
+  if (!(delta >= S(0))) config_fail("negative desingularization constant");
+  if (inflow)
+    for (long long i = 0; i < 2 * n; ++i)
+      if (!std::isfinite(inflow[i])) config_fail("non-finite inflow");
+  if (x)
+    for (long long i = 0; i < 2 * n; ++i)
+      if (!std::isfinite(x[i])) config_fail(std::string(who) + ": non-finite state");
+}
+
+void check_rows(long long n, long long b, long long e) {
+  if (n <= 0) config_fail("particle system is empty");
+  if (b < 0 || e > n || b > e) config_fail("target range outside [0, n]");
+}
+
+template <class S>
+S* stage_in(ptrom_ctx* ctx, const S* h, size_t count) {
+  if (!h) return nullptr;
+  S* d = ctx->io.take<S>(count);
+  PTROM_CUDA(cudaMemcpyAsync(d, h, count * sizeof(S), cudaMemcpyHostToDevice, ctx->stream));
+  return d;
+}
+
+}  // namespace
+}  // namespace ptrom
+
+using namespace ptrom;
+
+extern "C" {
+
+const char* ptrom_build_info(void) {
+  return "libptrom_b200 sm_100a: allpairs f64/f32 (MUFU.RCP64H+cubic), fom, tree, ptrom-online";
+}
+
+int ptrom_create(int device, void* stream, ptrom_ctx** out) {
+  if (!out) return PTROM_CONFIG_ERROR;
+  *out = nullptr;
+  auto* ctx = new ptrom_ctx;
+  ctx->device = device;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  const int rc = guarded(ctx, [&] {
+    PTROM_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    PTROM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    PTROM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) throw status_error(PTROM_CUDA_ERROR, "libptrom_b200 requires an sm_100a (B200) device");
+    ctx->num_sms = sms;
+    PTROM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DeviceStatus)));
+    PTROM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DeviceStatus)));
+    DeviceStatus clear{0, 0, LLONG_MAX};
+    PTROM_CUDA(cudaMemcpy(ctx->d_status, &clear, sizeof(clear), cudaMemcpyHostToDevice));
+  });
+  if (rc != PTROM_OK) {
+    ptrom_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return PTROM_OK;
+}
+
+void ptrom_destroy(ptrom_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->scratch.base) cudaFree(ctx->scratch.base);
+  if (ctx->io.base) cudaFree(ctx->io.base);
+  for (auto& pr : ctx->prof_events) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  delete ctx;
+}
+
+const char* ptrom_last_error(const ptrom_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int ptrom_set_stream(ptrom_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] { ctx->stream = static_cast<cudaStream_t>(stream); });
+}
+
+int ptrom_synchronize(ptrom_ctx* ctx) {
+  return guarded(ctx, [&] { check_device_status(ctx); });
+}
+
+int ptrom_profile_begin(ptrom_ctx* ctx) {
+  return guarded(ctx, [&] {
+    ctx->prof_on = true;
+    ctx->prof_used = 0;
+  });
+}
+
+int ptrom_profile_end(ptrom_ctx* ctx, double* total_ms, int64_t* launches) {
+  return guarded(ctx, [&] {
+    PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+    double total = 0.0;
+    for (size_t k = 0; k < ctx->prof_used; ++k) {
+      float ms = 0.f;
+      PTROM_CUDA(cudaEventElapsedTime(&ms, ctx->prof_events[k].first, ctx->prof_events[k].second));
+      total += ms;
+    }
+    if (total_ms) *total_ms = total;
+    if (launches) *launches = (int64_t)ctx->prof_used;
+    ctx->prof_on = false;
+    ctx->prof_used = 0;
+  });
+}
+
+// ------------------------------------------------------------ host API ---
+int ptrom_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
+                                int form, const double* inflow, double* f, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    validate_system<double>(n, x, gamma, delta, form, inflow, "pairwise_velocity");
+    ctx->io.reset();
+    ctx->io.reserve(sizeof(double) * (size_t)(2 * n + n + (inflow ? 2 * n : 0) + 2 * n) + 4096);
+    double* dx = stage_in(ctx, x, 2 * n);
+    double* dg = stage_in(ctx, gamma, n);
+    double* di = stage_in(ctx, inflow, inflow ? 2 * n : 0);
+    double* df = ctx->io.take<double>(2 * n);
+    dev_velocity_f64(ctx, n, dx, dg, delta, form, di, 0, n, df, n);
+    PTROM_CUDA(cudaMemcpyAsync(f, df, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+    if (n_pair_evals) *n_pair_evals = (uint64_t)n * (uint64_t)(n - 1);
+  });
+}
+
+int ptrom_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* x, const float* gamma, float delta, int form,
+                                const float* inflow, float* f, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    validate_system<float>(n, x, gamma, delta, form, inflow, "pairwise_velocity");
+    ctx->io.reset();
+    ctx->io.reserve(sizeof(float) * (size_t)(2 * n + n + (inflow ? 2 * n : 0) + 2 * n) + 4096);
+    float* dx = stage_in(ctx, x, 2 * n);
+    float* dg = stage_in(ctx, gamma, n);
+    float* di = stage_in(ctx, inflow, inflow ? 2 * n : 0);
+    float* df = ctx->io.take<float>(2 * n);
+    dev_velocity_f32(ctx, n, dx, dg, delta, form, di, 0, n, df, n);
+    PTROM_CUDA(cudaMemcpyAsync(f, df, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+    if (n_pair_evals) *n_pair_evals = (uint64_t)n * (uint64_t)(n - 1);
+  });
+}
+
+int ptrom_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
+                                      int form, double* jxx, double* jxy, double* jyx, double* jyy,
+                                      uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    validate_system<double>(n, x, gamma, delta, form, nullptr, "inexact_kernel_jacobian");
+    ctx->io.reset();
+    ctx->io.reserve(sizeof(double) * (size_t)(3 * n + 4 * n) + 4096);
+    double* dx = stage_in(ctx, x, 2 * n);
+    double* dg = stage_in(ctx, gamma, n);
+    double* dj = ctx->io.take<double>(4 * n);
+    dev_jacobian_f64(ctx, n, dx, dg, delta, form, 0, n, dj, dj + n, dj + 2 * n, dj + 3 * n, 0.0, nullptr);
+    double* outs[4] = {jxx, jxy, jyx, jyy};
+    for (int k = 0; k < 4; ++k)
+      PTROM_CUDA(cudaMemcpyAsync(outs[k], dj + k * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+    // kernel_pair_jacobian does not bump the reference counter (kernel.hpp:45-73)
+    if (n_pair_evals) *n_pair_evals = 0;
+  });
+}
+
+int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const double* gamma, double delta, int form,
+                           const double* inflow, double dt, int64_t n_steps, double tol, int max_iters,
+                           int jacobian_refresh_period, double* snapshots, int* iterations, uint8_t* converged,
+                           double* relative_residual, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    // integrators.hpp:20-23 TimeGrid::validate, 60-65 NewtonConfig::validate
+    if (!(dt > 0)) config_fail("time step must be positive");
+    if (n_steps < 0) config_fail("negative step count");
+    if (!(tol > 0)) config_fail("Newton tolerance must be positive");
+    if (max_iters < 1) config_fail("Newton max_iters must be >= 1");
+    if (jacobian_refresh_period < 1) config_fail("Jacobian refresh period must be >= 1");
+    validate_system<double>(n, x0, gamma, delta, form, inflow, "pairwise_velocity");
+    ctx->io.reset();
+    ctx->io.reserve(sizeof(double) * (size_t)(2 * n + n + (inflow ? 2 * n : 0)) + 4096);
+    double* dx = stage_in(ctx, x0, 2 * n);
+    double* dg = stage_in(ctx, gamma, n);
+    double* di = stage_in(ctx, inflow, inflow ? 2 * n : 0);
+    FomResult r = fom_simulate_device(ctx, n, dx, dg, delta, form, di, dt, n_steps, tol, max_iters,
+                                      jacobian_refresh_period, snapshots, iterations, converged, relative_residual);
+    if (n_pair_evals) *n_pair_evals = (uint64_t)r.velocity_evals * (uint64_t)n * (uint64_t)(n - 1);
+  });
+}
+
+// ---------------------------------------------------------- device API ---
+int ptrom_dev_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma, double delta,
+                                    int form, const double* d_inflow, int64_t t_begin, int64_t t_end, double* d_f,
+                                    int64_t ld_f) {
+  return guarded(ctx, [&] {
+    check_rows(n, t_begin, t_end);
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    if (ld_f < t_end - t_begin) config_fail("ld_f smaller than the row count");
+    dev_velocity_f64(ctx, n, d_x, d_gamma, delta, form, d_inflow, t_begin, t_end, d_f, ld_f);
+  });
+}
+
+int ptrom_dev_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* d_x, const float* d_gamma, float delta,
+                                    int form, const float* d_inflow, int64_t t_begin, int64_t t_end, float* d_f,
+                                    int64_t ld_f) {
+  return guarded(ctx, [&] {
+    check_rows(n, t_begin, t_end);
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    if (ld_f < t_end - t_begin) config_fail("ld_f smaller than the row count");
+    dev_velocity_f32(ctx, n, d_x, d_gamma, delta, form, d_inflow, t_begin, t_end, d_f, ld_f);
+  });
+}
+
+int ptrom_dev_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                          double delta, int form, int64_t t_begin, int64_t t_end, double* d_jxx,
+                                          double* d_jxy, double* d_jyx, double* d_jyy) {
+  return guarded(ctx, [&] {
+    check_rows(n, t_begin, t_end);
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    dev_jacobian_f64(ctx, n, d_x, d_gamma, delta, form, t_begin, t_end, d_jxx, d_jxy, d_jyx, d_jyy, 0.0, nullptr);
+  });
+}
+
+int ptrom_dev_newton_blocks_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma, double delta,
+                                int form, double dt, int64_t t_begin, int64_t t_end, double* d_inv) {
+  return guarded(ctx, [&] {
+    check_rows(n, t_begin, t_end);
+    if (!(dt > 0)) config_fail("time step must be positive");
+    dev_jacobian_f64(ctx, n, d_x, d_gamma, delta, form, t_begin, t_end, nullptr, nullptr, nullptr, nullptr, dt, d_inv);
+  });
+}
+
+int ptrom_dev_residual_f64(ptrom_ctx* ctx, int64_t m, int64_t ld, const double* d_xi, const double* d_fxi,
+                           const double* d_xprev, const double* d_fprev, double dt, double* d_r, double* d_norm2) {
+  return guarded(ctx, [&] {
+    if (m < 0 || ld < m) config_fail("bad residual shape");
+    ctx->scratch.reset();
+    ctx->scratch.reserve(residual_block_part_count() * sizeof(double) + 4096);
+    double* bp = ctx->scratch.take<double>(residual_block_part_count());
+    dev_residual_f64(ctx, m, ld, d_xi, d_fxi, d_xprev, d_fprev, dt, d_r, d_norm2, bp);
+  });
+}
+
+int ptrom_dev_newton_update_f64(ptrom_ctx* ctx, int64_t m, int64_t ld, const double* d_inv, const double* d_r,
+                                double* d_x) {
+  return guarded(ctx, [&] {
+    if (m < 0 || ld < m) config_fail("bad update shape");
+    dev_newton_update_f64(ctx, m, ld, d_inv, d_r, d_x);
+  });
+}
+
+}  // extern "C"

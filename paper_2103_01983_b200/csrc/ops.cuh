@@ -1,0 +1,30 @@
+// ops.cuh — internal (C++) entry points between translation units.
+#pragma once
+#include "common.cuh"
+
+namespace ptrom {
+
+double effective_delta(double delta, int form);
+void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                      const double* inflow, long long t_begin, long long t_end, double* f, long long ld);
+void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
+                      const float* inflow, long long t_begin, long long t_end, float* f, long long ld);
+// jxx..jyy (may be null when inv is given) or the Newton-block inverse of
+// (I - dt/2 J) into inv (4 per row) when inv != nullptr.
+void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                      long long t_begin, long long t_end, double* jxx, double* jxy, double* jyx, double* jyy,
+                      double dt_for_inverse, double* inv);
+void dev_residual_f64(ptrom_ctx* ctx, long long m, long long ld, const double* xi, const double* fxi,
+                      const double* xp, const double* fp, double dt, double* r, double* norm2, double* block_part);
+void dev_newton_update_f64(ptrom_ctx* ctx, long long m, long long ld, const double* inv, const double* r, double* x);
+size_t residual_block_part_count();
+
+struct FomResult {
+  long long velocity_evals = 0;
+};
+FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, const double* d_gamma, double delta,
+                              int form, const double* d_inflow, double dt, long long n_steps, double tol,
+                              int max_iters, int refresh, double* h_snapshots, int* iters, unsigned char* conv,
+                              double* rel_out);
+
+}  // namespace ptrom

@@ -1,0 +1,95 @@
+"""Device-buffer entry points over torch CUDA tensors (stream-ordered).
+
+Thin wrappers of the ``ptrom_dev_*`` C ABI: tensors must be contiguous CUDA
+tensors on the context's device; the call is enqueued on torch's current
+stream and does not synchronize. A numerical failure detected on the device
+(coincident pair with delta == 0, singular Newton block) is latched and
+raised by :func:`synchronize`.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from .api import Context, default_context
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("device entry points take contiguous CUDA tensors")
+    return t.data_ptr()
+
+
+def _ctx(ctx: Optional[Context], t: torch.Tensor) -> Context:
+    ctx = ctx or default_context(t.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(t.device).cuda_stream)
+    return ctx
+
+
+def pairwise_velocity(x: torch.Tensor, gamma: torch.Tensor, delta: float, form: int = 0,
+                      inflow: Optional[torch.Tensor] = None, t_begin: int = 0, t_end: Optional[int] = None,
+                      out: Optional[torch.Tensor] = None, ctx: Optional[Context] = None) -> torch.Tensor:
+    """kernel.hpp:107-129 for target rows [t_begin, t_end): out is (2, m) so
+    row k holds chi/psi velocity of particle t_begin + k (ld = m)."""
+    n = gamma.shape[0]
+    t_end = n if t_end is None else t_end
+    m = t_end - t_begin
+    if out is None:
+        out = torch.empty(2 * m, dtype=x.dtype, device=x.device)
+    ctx = _ctx(ctx, x)
+    if x.dtype == torch.float32:
+        fn = ctx.lib.ptrom_dev_pairwise_velocity_f32
+    elif x.dtype == torch.float64:
+        fn = ctx.lib.ptrom_dev_pairwise_velocity_f64
+    else:
+        raise ValueError("pairwise_velocity: float32 or float64 state expected")
+    ctx.check(fn(ctx.handle, n, _ptr(x), _ptr(gamma), float(delta), int(form), _ptr(inflow), t_begin, t_end,
+                 _ptr(out), m))
+    return out
+
+
+def inexact_kernel_jacobian(x: torch.Tensor, gamma: torch.Tensor, delta: float, form: int = 0, t_begin: int = 0,
+                            t_end: Optional[int] = None, ctx: Optional[Context] = None) -> torch.Tensor:
+    """kernel.hpp:154-170 rows [t_begin, t_end) → (4, m): dfx_dx, dfx_dy, dfy_dx, dfy_dy."""
+    n = gamma.shape[0]
+    t_end = n if t_end is None else t_end
+    m = t_end - t_begin
+    out = torch.empty(4, m, dtype=torch.float64, device=x.device)
+    ctx = _ctx(ctx, x)
+    ctx.check(ctx.lib.ptrom_dev_inexact_kernel_jacobian_f64(ctx.handle, n, _ptr(x), _ptr(gamma), float(delta),
+                                                            int(form), t_begin, t_end, out[0].data_ptr(),
+                                                            out[1].data_ptr(), out[2].data_ptr(),
+                                                            out[3].data_ptr()))
+    return out
+
+
+def newton_blocks(x: torch.Tensor, gamma: torch.Tensor, delta: float, form: int, dt: float, t_begin: int,
+                  t_end: int, out: torch.Tensor, ctx: Optional[Context] = None) -> torch.Tensor:
+    """integrators.hpp:181-194 refactor for rows [t_begin, t_end): out (m, 4)."""
+    n = gamma.shape[0]
+    ctx = _ctx(ctx, x)
+    ctx.check(ctx.lib.ptrom_dev_newton_blocks_f64(ctx.handle, n, _ptr(x), _ptr(gamma), float(delta), int(form),
+                                                  float(dt), t_begin, t_end, _ptr(out)))
+    return out
+
+
+def residual(xi, fxi, xprev, fprev, dt: float, r: torch.Tensor, norm2: torch.Tensor, m: int, ld: int,
+             ctx: Optional[Context] = None) -> None:
+    """integrators.hpp:47-53 on m local rows (k, k+ld); norm2 gets Σ r² (fixed order)."""
+    ctx = _ctx(ctx, xi)
+    ctx.check(ctx.lib.ptrom_dev_residual_f64(ctx.handle, m, ld, _ptr(xi), _ptr(fxi), _ptr(xprev), _ptr(fprev),
+                                             float(dt), _ptr(r), _ptr(norm2)))
+
+
+def newton_update(inv: torch.Tensor, r: torch.Tensor, x: torch.Tensor, m: int, ld: int,
+                  ctx: Optional[Context] = None) -> None:
+    """integrators.hpp:161-167 on m local rows."""
+    ctx = _ctx(ctx, x)
+    ctx.check(ctx.lib.ptrom_dev_newton_update_f64(ctx.handle, m, ld, _ptr(inv), _ptr(r), _ptr(x)))
+
+
+def synchronize(ctx: Optional[Context] = None, device: int = 0) -> None:
+    (ctx or default_context(device)).synchronize()

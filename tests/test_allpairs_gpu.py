@@ -1,0 +1,160 @@
+"""Parity of the sm_100a all-pairs kernels (through the C ABI) against the
+CPU oracle. Tolerances are north_star's: 1e-12 relative (2-norm) in fp64,
+1e-5 relative in fp32 (judged against the fp64 oracle)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2103_01983_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+FP64_TOL = 1e-12
+FP32_TOL = 1e-5
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def random_system(rng, n, box=5.0):
+    x = rng.uniform(-box, box, 2 * n)
+    g = rng.uniform(-2.0, 2.0, n)
+    return x, g
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 33, 129, 1000, 4097])
+@pytest.mark.parametrize("form", [0, 1])
+@pytest.mark.parametrize("delta", [0.0, 0.3])
+def test_velocity_small_systems(pt, oracle, n, form, delta):
+    rng = np.random.default_rng(1000 + n)
+    x, g = random_system(rng, n)
+    inflow = rng.uniform(-1, 1, 2 * n) if n % 2 else None
+    f = pt.pairwise_velocity(x, pt.ParticleSystem(g, delta, inflow, form))
+    ref = oracle.pairwise_velocity(x, g, delta, form, inflow)
+    assert rel(f, ref) <= FP64_TOL
+
+
+def test_velocity_config2_full_size_rows(pt, oracle):
+    """BASELINE configs[1] at full N = 65,536 (fp64); the oracle checks 4,096
+    target rows spread over the particle range against every source."""
+    w = workloads.config2()
+    f = pt.pairwise_velocity(w.x0, pt.ParticleSystem(w.gamma, w.delta))
+    n = w.n
+    for b in (0, 30000, n - 2048):
+        ref = oracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=b, t_end=b + 2048, threads=THREADS)
+        rows = np.r_[b:b + 2048, n + b:n + b + 2048]
+        assert rel(f[rows], ref[rows]) <= FP64_TOL
+
+
+def test_velocity_config2_fp32(pt, oracle):
+    w = workloads.config2()
+    x32 = w.x0.astype(np.float32)
+    g32 = w.gamma.astype(np.float32)
+    f32 = pt.pairwise_velocity(x32, pt.ParticleSystem(g32, np.float32(w.delta)))
+    assert f32.dtype == np.float32
+    n = w.n
+    b = 12345
+    ref = oracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=b, t_end=b + 4096, threads=THREADS)
+    rows = np.r_[b:b + 4096, n + b:n + b + 4096]
+    assert rel(f32[rows].astype(np.float64), ref[rows]) <= FP32_TOL
+
+
+def test_velocity_fp32_small_against_fp32_oracle(pt, oracle):
+    rng = np.random.default_rng(7)
+    x, g = random_system(rng, 500)
+    x, g = x.astype(np.float32), g.astype(np.float32)
+    f = pt.pairwise_velocity(x, pt.ParticleSystem(g, np.float32(0.05)))
+    ref64 = oracle.pairwise_velocity(x.astype(np.float64), g.astype(np.float64), float(np.float32(0.05)))
+    assert rel(f.astype(np.float64), ref64) <= FP32_TOL
+
+
+def test_kernel_pair_unit_distance_known_answer(pt):
+    # test_kernel.cpp:73-85: target (0,0), source (1,0), Γ = 2π → (0, −1); δ = 1 → (0, −0.5)
+    x = np.array([0.0, 1.0, 0.0, 0.0])
+    g = np.array([0.0, 2.0 * np.pi])
+    f0 = pt.pairwise_velocity(x, pt.ParticleSystem(g, 0.0))
+    f1 = pt.pairwise_velocity(x, pt.ParticleSystem(g, 1.0))
+    assert abs(f0[0]) < 1e-15 and abs(f0[2] + 1.0) < 1e-15
+    assert abs(f1[0]) < 1e-15 and abs(f1[2] + 0.5) < 1e-15
+    # test_kernel.cpp:103-113 denominator-scaled: −1/(2π+3)
+    g2 = np.array([0.0, 1.0])
+    f2 = pt.pairwise_velocity(x, pt.ParticleSystem(g2, 3.0, None, pt.KernelForm.denominator_scaled))
+    assert abs(f2[2] + 1.0 / (2.0 * np.pi + 3.0)) < 1e-15
+
+
+def test_zero_circulation_returns_inflow_exactly(pt):
+    # test_kernel.cpp:141-151
+    inflow = np.arange(1.0, 7.0)
+    f = pt.pairwise_velocity(np.array([0, 1, 2, 0, 1, 2.0]), pt.ParticleSystem(np.zeros(3), 0.0, inflow))
+    assert np.array_equal(f, inflow)
+
+
+def test_coincident_points_raise_numerical_error(pt):
+    # test_kernel.cpp:182-195 (delta = 0 coincident pair → numerical_error)
+    with pytest.raises(pt.NumericalError):
+        pt.pairwise_velocity(np.array([1.0, 1.0, 2.0, 2.0]), pt.ParticleSystem(np.ones(2), 0.0))
+    # regularized: finite, and the context recovers for the next call
+    f = pt.pairwise_velocity(np.array([1.0, 1.0, 2.0, 2.0]), pt.ParticleSystem(np.ones(2), 0.5))
+    assert np.all(f == 0.0)
+
+
+def test_input_validation_raises_config_error(pt):
+    sys_ = pt.ParticleSystem(np.ones(2), 0.1)
+    with pytest.raises(pt.ConfigError):
+        pt.pairwise_velocity(np.array([1.0, 2.0, 3.0]), sys_)
+    with pytest.raises(pt.ConfigError):
+        pt.pairwise_velocity(np.array([0.0, 1.0, 0.0, np.nan]), sys_)
+    with pytest.raises(pt.ConfigError):
+        pt.pairwise_velocity(np.zeros(4), pt.ParticleSystem(np.ones(2), -1.0))
+    with pytest.raises(pt.ConfigError):
+        pt.pairwise_velocity(np.zeros(4), pt.ParticleSystem(np.array([1.0, np.inf]), 0.1))
+
+
+def test_kernel_eval_counter_counts_ordered_pairs(pt):
+    # test_kernel.cpp:312-321: N(N−1)
+    pt.reset_kernel_eval_count()
+    pt.pairwise_velocity(np.random.default_rng(5).uniform(-5, 5, 8), pt.ParticleSystem(np.ones(4), 0.1))
+    assert pt.kernel_eval_count() == 12
+
+
+@pytest.mark.parametrize("n,delta,form", [(2, 0.0, 0), (5, 0.2, 0), (300, 0.01, 1), (5000, 1e-4, 0)])
+def test_jacobian_parity(pt, oracle, n, delta, form):
+    rng = np.random.default_rng(17 + n)
+    x, g = random_system(rng, n)
+    jac = pt.inexact_kernel_jacobian(x, pt.ParticleSystem(g, delta, None, form))
+    ref = oracle.inexact_kernel_jacobian(x, g, delta, form, threads=THREADS)
+    got = np.stack([jac.dfx_dx, jac.dfx_dy, jac.dfy_dx, jac.dfy_dy])
+    assert rel(got, ref) <= FP64_TOL
+
+
+def test_jacobian_two_particle_known_answer(pt):
+    # test_kernel.cpp:197-210 → [[0, −1], [−1, 0]]
+    jac = pt.inexact_kernel_jacobian(np.array([0.0, 1.0, 0.0, 0.0]), pt.ParticleSystem(np.array([0.0, 2 * np.pi])))
+    assert np.allclose(jac.block(0), [[0.0, -1.0], [-1.0, 0.0]], atol=1e-14, rtol=0)
+
+
+def test_device_entry_points_rows_and_ld(pt, oracle):
+    import torch
+    from paper_2103_01983_b200 import device as dev
+    w = workloads.config1(n=3000)
+    x = torch.tensor(w.x0, device="cuda")
+    g = torch.tensor(w.gamma, device="cuda")
+    out = dev.pairwise_velocity(x, g, w.delta, t_begin=1000, t_end=2100)
+    dev.synchronize()
+    ref = oracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=1000, t_end=2100)
+    got = out.cpu().numpy()
+    want = np.r_[ref[1000:2100], ref[3000 + 1000:3000 + 2100]]
+    assert rel(got, want) <= FP64_TOL
+
+
+def test_repeatable_bitwise(pt):
+    """Fixed-order reductions: two evaluations are bit-identical."""
+    w = workloads.config2(n=20000)
+    s = pt.ParticleSystem(w.gamma, w.delta)
+    a = pt.pairwise_velocity(w.x0, s)
+    b = pt.pairwise_velocity(w.x0, s)
+    assert np.array_equal(a, b)

@@ -1,0 +1,99 @@
+"""Device-resident FOM (FomStepper/fom_simulate, integrators.hpp:117-272)
+against the oracle and the reference's analytic tests."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2103_01983_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 1
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_config1_full_trajectory_parity(pt, oracle):
+    """BASELINE configs[0]: N = 4096, δ = 0.01, dt = 1e-3, 100 steps; every
+    snapshot within 1e-12 (relative 2-norm) of the oracle's."""
+    w = workloads.config1()
+    run = pt.fom_simulate(w.x0, pt.ParticleSystem(w.gamma, w.delta), pt.TimeGrid(w.dt, w.n_steps))
+    snaps, iters, conv, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, w.n_steps, threads=THREADS)
+    assert run.all_converged() and conv.all()
+    worst = max(rel(run.snapshots[:, s], snaps[:, s]) for s in range(w.n_steps))
+    assert worst <= 1e-12, worst
+    # Newton tolerance flips are reported, not gated; they must stay rare.
+    mismatch = int(np.sum(np.asarray(run.iterations) != iters))
+    print(f"worst snapshot rel {worst:.3e}; iteration-count mismatches {mismatch}/{w.n_steps}")
+    assert mismatch <= w.n_steps // 10
+
+
+def co_rotation(gamma, d, cx, cy, t):
+    omega = gamma / (np.pi * d * d)
+    phi = omega * t
+    ax, ay = np.cos(phi) * d / 2, np.sin(phi) * d / 2
+    return np.array([cx + ax, cx - ax, cy + ay, cy - ay])
+
+
+def test_vortex_pair_co_rotates_at_analytic_rate(pt):
+    # test_integrators.cpp:147-168
+    gamma, d = 2 * np.pi, 2.0
+    run = pt.fom_simulate(co_rotation(gamma, d, 0.3, -0.8, 0.0), pt.ParticleSystem(np.full(2, gamma), 0.0),
+                          pt.TimeGrid(1e-3, 100), pt.NewtonConfig(tol=1e-12))
+    assert run.all_converged()
+    last = run.snapshots[:, -1]
+    assert np.max(np.abs(last - co_rotation(gamma, d, 0.3, -0.8, 0.1))) < 5e-6
+    r = np.hypot(last[0] - last[1], last[2] - last[3])
+    assert abs(r - d) / d < 1e-7
+
+
+def test_zero_circulation_zero_updates(pt):
+    # test_integrators.cpp:188-200
+    x = np.arange(6.0)
+    run = pt.fom_simulate(x, pt.ParticleSystem(np.zeros(3), 0.0), pt.TimeGrid(0.1, 1))
+    assert run.converged == [1] and run.iterations == [0]
+    assert np.array_equal(run.snapshots[:, 0], x)
+
+
+def test_stale_jacobian_same_solution(pt):
+    # test_integrators.cpp:202-216
+    x0 = co_rotation(4.0, 1.5, 0.0, 0.0, 0.0)
+    s = pt.ParticleSystem(np.full(2, 4.0), 0.0)
+    a = pt.fom_simulate(x0, s, pt.TimeGrid(5e-3, 30), pt.NewtonConfig(tol=1e-12))
+    b = pt.fom_simulate(x0, s, pt.TimeGrid(5e-3, 30), pt.NewtonConfig(tol=1e-12, jacobian_refresh_period=5))
+    assert a.all_converged() and b.all_converged()
+    assert np.max(np.abs(a.snapshots - b.snapshots)) < 1e-9
+
+
+def test_iteration_cap_reports_non_convergence(pt):
+    # test_integrators.cpp:218-228
+    run = pt.fom_simulate(co_rotation(2 * np.pi, 2.0, 0, 0, 0), pt.ParticleSystem(np.full(2, 2 * np.pi), 0.0),
+                          pt.TimeGrid(1e-3, 1), pt.NewtonConfig(tol=1e-30, max_iters=2))
+    assert run.converged == [0] and run.iterations == [2] and run.relative_residual[0] > 0
+
+
+def test_refresh_period_matches_oracle(pt, oracle):
+    w = workloads.config1(n=700)
+    run = pt.fom_simulate(w.x0, pt.ParticleSystem(w.gamma, w.delta, None, 1), pt.TimeGrid(2e-3, 12),
+                          pt.NewtonConfig(tol=1e-11, jacobian_refresh_period=3))
+    snaps, iters, conv, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, 2e-3, 12, form=1, tol=1e-11, refresh=3)
+    assert max(rel(run.snapshots[:, s], snaps[:, s]) for s in range(12)) <= 1e-12
+
+
+def test_singularity_raises_numerical_error(pt):
+    x = np.array([0.0, 1e-100, 0.0, 0.0])
+    with pytest.raises(pt.NumericalError):
+        pt.fom_simulate(x, pt.ParticleSystem(np.full(2, 1e300), 0.0), pt.TimeGrid(1e-3, 2))
+
+
+def test_config_validation(pt):
+    s = pt.ParticleSystem(np.ones(2), 0.1)
+    x = np.array([0.0, 1.0, 0.0, 0.0])
+    with pytest.raises(pt.ConfigError):
+        pt.fom_simulate(x, s, pt.TimeGrid(0.0, 5))
+    with pytest.raises(pt.ConfigError):
+        pt.fom_simulate(x, s, pt.TimeGrid(0.1, 5), pt.NewtonConfig(tol=0.0))
+    with pytest.raises(pt.ConfigError):
+        pt.fom_simulate(x, s, pt.TimeGrid(0.1, 5), pt.NewtonConfig(jacobian_refresh_period=0))
