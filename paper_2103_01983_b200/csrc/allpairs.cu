@@ -23,9 +23,16 @@
 //   adds the inflow and latches a numerical error on a non-finite result
 //   (a coincident pair with δ = 0, the reference's throw at kernel.hpp:38-39).
 //
-// Reciprocal: MUFU.RCP64H seed (rcp.approx.ftz.f64) + one cubic correction
-// y = y0(1+e+e²), e = 1−q·y0 (3 DFMA incl. the Γ' scale): ~1 ulp, 10 FP64
-// pipe ops per velocity pair instead of the ~14 of an IEEE division.
+// Reciprocal (the FP64 pipe is the bound):
+//  * fast path (δ' ≥ 2^-100 and every coordinate of the tile and of the
+//    block's targets below 2^60, so q ∈ [2^-100, 2^122]): the double q is
+//    re-biased into an fp32 bit pattern with integer ops (ALU pipe), seeded
+//    with MUFU.RCP (fp32, ≤ 2^-22 rel incl. truncation) and refined by one
+//    fp64 Newton step fused with the Γ' scale: s = g0 + g0·e, g0 = Γ'·y0,
+//    e = 1 − q·y0 → |rel err| ≤ 6e-14. 9 FP64 ops per velocity pair.
+//  * safe path (δ' tiny or huge coordinates, masked self tiles): MUFU.RCP64H
+//    seed + cubic correction y0(1+e+e²) (~1 ulp, 10 FP64 ops); q = 0
+//    propagates inf/NaN so a coincident pair with δ = 0 is detected.
 #include <algorithm>
 #include <cmath>
 
@@ -38,6 +45,19 @@ __device__ __forceinline__ double rcp_seed(double q) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
   return y;
 }
+// fp32 reciprocal seed of a double q ∈ [2^-100, 2^122] through integer
+// exponent re-biasing (no FP64-pipe conversion instructions).
+__device__ __forceinline__ double rcp_seed_via_f32(double q) {
+  const int hi = __double2hiint(q), lo = __double2loint(q);
+  const unsigned fb = __funnelshift_l((unsigned)lo, (unsigned)hi, 3) - (896u << 23);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__uint_as_float(fb)));
+  const unsigned rb = __float_as_uint(r);
+  return __hiloint2double((int)((rb >> 3) + (896u << 20)), (int)(rb << 29));
+}
+__device__ __forceinline__ bool coord_ok(double v) {  // |v| < 2^60 (also false for inf/NaN)
+  return (__double2hiint(v) & 0x7fffffff) < 0x43B00000;
+}
 __device__ __forceinline__ float rcp_approx(float q) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(q));
@@ -46,7 +66,7 @@ __device__ __forceinline__ float rcp_approx(float q) {
 
 // ----------------------------------------------------------------- fp64 ---
 // One source tile against T register-resident targets of this thread.
-template <int T, bool VEL, bool JAC, bool MASK>
+template <int T, bool VEL, bool JAC, bool MASK, bool FAST>
 __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp, const double* __restrict__ sg,
                                          long long j0, const double (&tx)[T], const double (&ty)[T],
                                          const long long (&ti)[T], double dp, double (&fx)[T], double (&fy)[T],
@@ -66,9 +86,15 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
         q = self ? 1.0 : q;
         gs = self ? 0.0 : gs;
       }
-      const double y0 = rcp_seed(q);
-      double e = fma(-q, y0, 1.0);
-      e = fma(e, e, e);
+      double y0, e;
+      if (FAST) {
+        y0 = rcp_seed_via_f32(q);
+        e = fma(-q, y0, 1.0);
+      } else {
+        y0 = rcp_seed(q);
+        e = fma(-q, y0, 1.0);
+        e = fma(e, e, e);
+      }
       if (JAC) {
         const double u = fma(y0, e, y0);  // 1/q
         const double s = gs * u;          // Γ'/q
@@ -120,6 +146,11 @@ __global__ void __launch_bounds__(TPB) allpairs_f64_kernel(long long n, const do
   const long long cbeg = (long long)blockIdx.y * chunk_len;
   const long long cend = min(n, cbeg + chunk_len);
 
+  bool my_ok = true;
+#pragma unroll
+  for (int k = 0; k < T; ++k) my_ok = my_ok && coord_ok(tx[k]) && coord_ok(ty[k]);
+  const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-100;
+
   // Register prefetch of the first source tile.
   double px = 0.0, py = 0.0, pg = 0.0;
   if (cbeg + tid < cend) {
@@ -131,7 +162,7 @@ __global__ void __launch_bounds__(TPB) allpairs_f64_kernel(long long n, const do
     const int cnt = (int)min((long long)TPB, cend - j0);
     sp[tid] = make_double2(px, py);
     sg[tid] = pg;
-    __syncthreads();
+    const bool fast = __syncthreads_and(coord_ok(px) && coord_ok(py)) && targets_ok;
     const long long jn = j0 + TPB + tid;  // prefetch the next tile while computing
     if (jn < cend) {
       px = xs[jn];
@@ -140,9 +171,11 @@ __global__ void __launch_bounds__(TPB) allpairs_f64_kernel(long long n, const do
     }
     const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt);
     if (masked)
-      tile_f64<T, VEL, JAC, true>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, VEL, JAC, true, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+    else if (fast)
+      tile_f64<T, VEL, JAC, false, true>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else
-      tile_f64<T, VEL, JAC, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, VEL, JAC, false, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     __syncthreads();
   }
 
