@@ -66,12 +66,12 @@ __device__ __forceinline__ float rcp_approx(float q) {
 
 // ----------------------------------------------------------------- fp64 ---
 // One source tile against T register-resident targets of this thread.
-template <int T, bool VEL, bool JAC, bool MASK, bool FAST>
+template <int T, int UNR, bool VEL, bool JAC, bool MASK, bool FAST>
 __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp, const double* __restrict__ sg,
                                          long long j0, const double (&tx)[T], const double (&ty)[T],
                                          const long long (&ti)[T], double dp, double (&fx)[T], double (&fy)[T],
                                          double (&ja)[T], double (&jb)[T], double (&jc)[T]) {
-#pragma unroll 4
+#pragma unroll UNR
   for (int jj = 0; jj < cnt; ++jj) {
     const double2 p = sp[jj];
     const double g = sg[jj];
@@ -118,8 +118,8 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
   }
 }
 
-template <int TPB, int T, bool VEL, bool JAC>
-__global__ void __launch_bounds__(TPB) allpairs_f64_kernel(long long n, const double* __restrict__ xs,
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC>
+__global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, const double* __restrict__ xs,
                                                            const double* __restrict__ ys,
                                                            const double* __restrict__ gam, double inv2pi,
                                                            double dp, long long t_begin, long long t_count,
@@ -171,11 +171,11 @@ __global__ void __launch_bounds__(TPB) allpairs_f64_kernel(long long n, const do
     }
     const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt);
     if (masked)
-      tile_f64<T, VEL, JAC, true, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, true, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else if (fast)
-      tile_f64<T, VEL, JAC, false, true>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, false, true>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else
-      tile_f64<T, VEL, JAC, false, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, false, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     __syncthreads();
   }
 
@@ -409,14 +409,14 @@ int reduce_grid(ptrom_ctx* ctx, long long count) {
   return (int)std::max(1LL, std::min(g, (long long)ctx->num_sms * 8));
 }
 
-template <int T, bool VEL, bool JAC>
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC>
 void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                            long long t_begin, long long t_count, double** part_out, int* chunks_out) {
-  auto kern = allpairs_f64_kernel<kTPB, T, VEL, JAC>;
-  static int occ = resident_blocks(kern, kTPB);
+  auto kern = allpairs_f64_kernel<TPB, T, UNR, MINB, VEL, JAC>;
+  static int occ = resident_blocks(kern, TPB);
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
-  const long long tiles = (t_count + kTPB * T - 1) / (kTPB * T);
-  const int chunks = choose_source_chunks(ctx, tiles, n, occ, 2 * kTPB);
+  const long long tiles = (t_count + TPB * T - 1) / (TPB * T);
+  const int chunks = choose_source_chunks(ctx, tiles, n, occ, 2 * TPB);
   const long long chunk_len = (n + chunks - 1) / chunks;
   ctx->scratch.reset();
   ctx->scratch.reserve((size_t)chunks * NCOMP * t_count * sizeof(double) + 4096);
@@ -425,22 +425,54 @@ void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const d
   const double inv2pi = 1.0 / (2.0 * M_PI);
   {
     ProfScope prof(ctx);
-    kern<<<grid, kTPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part);
+    kern<<<grid, TPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part);
   }
   PTROM_LAUNCH_CHECK();
   *part_out = part;
   *chunks_out = chunks;
 }
 
+using LaunchFn = void (*)(ptrom_ctx*, long long, const double*, const double*, double, long long, long long,
+                          double**, int*);
+
+// Velocity-kernel shapes (TPB, targets/thread, source unroll, min blocks/SM);
+// entry 0 is the default, the rest are kept for tools/tune_allpairs.py
+// (PTROM_ALLPAIRS_VARIANT selects one at context creation).
+#define PTROM_VEL_VARIANTS(X) \
+  X(128, 4, 4, 1)             \
+  X(128, 4, 2, 1)             \
+  X(128, 4, 8, 1)             \
+  X(128, 2, 4, 1)             \
+  X(128, 2, 8, 1)             \
+  X(128, 8, 2, 1)             \
+  X(256, 4, 4, 1)             \
+  X(128, 4, 4, 8)             \
+  X(128, 2, 4, 10)            \
+  X(256, 2, 4, 4)             \
+  X(64, 4, 4, 1)              \
+  X(128, 1, 8, 1)             \
+  X(128, 3, 4, 1)             \
+  X(128, 4, 1, 1)             \
+  X(128, 6, 2, 1)             \
+  X(128, 2, 2, 8)
+
+#define PTROM_VEL_ENTRY(TPB, T, UNR, MINB) launch_allpairs_f64_t<TPB, T, UNR, MINB, true, false>,
+const LaunchFn kVelVariants[] = {PTROM_VEL_VARIANTS(PTROM_VEL_ENTRY)};
+constexpr int kNumVelVariants = sizeof(kVelVariants) / sizeof(kVelVariants[0]);
+
 // Small target sets get one target per thread (more blocks); large sets
-// keep 4 targets per thread in registers to amortize the shared loads.
+// keep several targets per thread in registers to amortize the shared loads.
 template <bool VEL, bool JAC>
 void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                          long long t_begin, long long t_count, double** part, int* chunks) {
-  if (t_count >= 16384)
-    launch_allpairs_f64_t<4, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
-  else
-    launch_allpairs_f64_t<1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+  if (t_count < 16384) {
+    launch_allpairs_f64_t<kTPB, 1, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+  } else if (VEL && !JAC) {
+    const int v = (ctx->allpairs_variant >= 0 && ctx->allpairs_variant < kNumVelVariants) ? ctx->allpairs_variant : 0;
+    kVelVariants[v](ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+  } else {
+    launch_allpairs_f64_t<kTPB, 4, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+  }
 }
 
 }  // namespace

@@ -97,6 +97,7 @@ struct ptrom_ctx {
   bool prof_on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
+  int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
 };
 
 namespace ptrom {
