@@ -24,12 +24,12 @@
 //   (a coincident pair with δ = 0, the reference's throw at kernel.hpp:38-39).
 //
 // Reciprocal (the FP64 pipe is the bound):
-//  * fast path (δ' ≥ 2^-100 and every coordinate of the tile and of the
-//    block's targets below 2^60, so q ∈ [2^-100, 2^122]): the double q is
-//    re-biased into an fp32 bit pattern with integer ops (ALU pipe), seeded
-//    with MUFU.RCP (fp32, ≤ 2^-22 rel incl. truncation) and refined by one
-//    fp64 Newton step fused with the Γ' scale: s = g0 + g0·e, g0 = Γ'·y0,
-//    e = 1 − q·y0 → |rel err| ≤ 6e-14. 9 FP64 ops per velocity pair.
+//  * fast path (δ' ≥ 2^-62 and every coordinate of the tile and of the
+//    block's targets below 2^29, so q ∈ [2^-62, 2^61]): two targets share one
+//    reciprocal of P = q1·q2 (Montgomery); the double P is re-biased into an
+//    fp32 bit pattern with integer ops (ALU pipe), seeded with MUFU.RCP (fp32,
+//    ≤ 2^-22 rel incl. truncation) and refined by one fp64 Newton step:
+//    |rel err| ≤ 1e-13 per term. 9 FP64 + 2 ALU/MUFU ops per velocity pair.
 //  * safe path (δ' tiny or huge coordinates, masked self tiles): MUFU.RCP64H
 //    seed + cubic correction y0(1+e+e²) (~1 ulp, 10 FP64 ops); q = 0
 //    propagates inf/NaN so a coincident pair with δ = 0 is detected.
@@ -55,8 +55,11 @@ __device__ __forceinline__ double rcp_seed_via_f32(double q) {
   const unsigned rb = __float_as_uint(r);
   return __hiloint2double((int)((rb >> 3) + (896u << 20)), (int)(rb << 29));
 }
-__device__ __forceinline__ bool coord_ok(double v) {  // |v| < 2^60 (also false for inf/NaN)
-  return (__double2hiint(v) & 0x7fffffff) < 0x43B00000;
+__device__ __forceinline__ bool coord_ok(double v) {  // |v| < 2^29 (also false for inf/NaN)
+  return (__double2hiint(v) & 0x7fffffff) < 0x41C00000;
+}
+__device__ __forceinline__ bool coord_ok4(double v) {  // |v| < 2^14: q ∈ [δ', 2^31]
+  return (__double2hiint(v) & 0x7fffffff) < 0x40D00000;
 }
 __device__ __forceinline__ float rcp_approx(float q) {
   float y;
@@ -65,8 +68,32 @@ __device__ __forceinline__ float rcp_approx(float q) {
 }
 
 // ----------------------------------------------------------------- fp64 ---
+// Per-pair accumulation given s = Γ'/q and u = 1/q (u only used for JAC).
+template <bool VEL, bool JAC>
+__device__ __forceinline__ void accumulate(double rx, double ry, double s, double u, double& fx, double& fy,
+                                           double& ja, double& jb, double& jc) {
+  if (JAC) {
+    const double w = s * u;  // Γ'/q²
+    const double t = w * rx;
+    ja = fma(t, ry, ja);
+    const double rx2 = rx * rx;
+    jb = fma(w, fma(ry, ry, -rx2), jb);
+    jc += w;
+  }
+  if (VEL) {
+    fx = fma(-ry, s, fx);
+    fy = fma(rx, s, fy);
+  }
+}
+
 // One source tile against T register-resident targets of this thread.
-template <int T, int UNR, bool VEL, bool JAC, bool MASK, bool FAST>
+//  FAST: targets are taken two at a time and share one reciprocal
+//        (Montgomery): u = 1/(q1·q2) from the fp32 seed + one Newton step,
+//        then 1/q1 = q2·u, 1/q2 = q1·u. Per pair 9 FP64 ops and 2 ALU/MUFU
+//        ops instead of 9 + 4 (the SMSP dispatch, not the FP64 pipe, is the
+//        limit: tools/fp64mix.cu). Needs q ∈ [2^-62, 2^61] (tile guard).
+//  safe: MUFU.RCP64H + cubic correction per pair (propagates q = 0 as inf/NaN).
+template <int T, int UNR, bool VEL, bool JAC, bool MASK, int FAST>
 __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp, const double* __restrict__ sg,
                                          long long j0, const double (&tx)[T], const double (&ty)[T],
                                          const long long (&ti)[T], double dp, double (&fx)[T], double (&fy)[T],
@@ -75,44 +102,81 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
   for (int jj = 0; jj < cnt; ++jj) {
     const double2 p = sp[jj];
     const double g = sg[jj];
+    if (FAST == 4 && !MASK && (T % 4 == 0)) {
+      // four targets share one reciprocal: P = (q1 q2)(q3 q4), q ∈ [2^-31, 2^31]
 #pragma unroll
-    for (int k = 0; k < T; ++k) {
-      const double rx = tx[k] - p.x;
-      const double ry = ty[k] - p.y;
-      double q = fma(rx, rx, fma(ry, ry, dp));
-      double gs = g;
-      if (MASK) {
-        const bool self = (j0 + jj) == ti[k];  // kernel.hpp:118 `if (j == i) continue;`
-        q = self ? 1.0 : q;
-        gs = self ? 0.0 : gs;
-      }
-      double y0, e;
-      if (FAST) {
-        y0 = rcp_seed_via_f32(q);
-        e = fma(-q, y0, 1.0);
-      } else {
-        y0 = rcp_seed(q);
-        e = fma(-q, y0, 1.0);
-        e = fma(e, e, e);
-      }
-      if (JAC) {
-        const double u = fma(y0, e, y0);  // 1/q
-        const double s = gs * u;          // Γ'/q
-        const double w = s * u;           // Γ'/q²
-        const double t = w * rx;
-        ja[k] = fma(t, ry, ja[k]);
-        const double rx2 = rx * rx;
-        jb[k] = fma(w, fma(ry, ry, -rx2), jb[k]);
-        jc[k] += w;
-        if (VEL) {
-          fx[k] = fma(-ry, s, fx[k]);
-          fy[k] = fma(rx, s, fy[k]);
+      for (int k = 0; k < T; k += 4) {
+        double rx[4], ry[4], q[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          rx[m] = tx[k + m] - p.x;
+          ry[m] = ty[k + m] - p.y;
+          q[m] = fma(rx[m], rx[m], fma(ry[m], ry[m], dp));
         }
-      } else {
-        const double g0 = gs * y0;
-        const double s = fma(g0, e, g0);  // Γ'/q
-        fx[k] = fma(-ry, s, fx[k]);
-        fy[k] = fma(rx, s, fy[k]);
+        const double p01 = q[0] * q[1], p23 = q[2] * q[3];
+        const double P = p01 * p23;
+        const double y0 = rcp_seed_via_f32(P);
+        const double e = fma(-P, y0, 1.0);
+        const double uP = fma(y0, e, y0);  // 1/P
+        if (JAC) {
+          const double u01 = uP * p23, u23 = uP * p01;  // 1/(q0 q1), 1/(q2 q3)
+          const double u[4] = {u01 * q[1], u01 * q[0], u23 * q[3], u23 * q[2]};
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            accumulate<VEL, JAC>(rx[m], ry[m], g * u[m], u[m], fx[k + m], fy[k + m], ja[k + m], jb[k + m],
+                                 jc[k + m]);
+        } else {
+          const double gu = g * uP;
+          const double g01 = gu * p23, g23 = gu * p01;  // Γ'/(q0 q1), Γ'/(q2 q3)
+          const double sv[4] = {g01 * q[1], g01 * q[0], g23 * q[3], g23 * q[2]};
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            accumulate<VEL, JAC>(rx[m], ry[m], sv[m], 0.0, fx[k + m], fy[k + m], ja[k + m], jb[k + m], jc[k + m]);
+        }
+      }
+    } else if (FAST >= 2 && !MASK && (T % 2 == 0)) {
+#pragma unroll
+      for (int k = 0; k < T; k += 2) {
+        const double rx1 = tx[k] - p.x, ry1 = ty[k] - p.y;
+        const double rx2 = tx[k + 1] - p.x, ry2 = ty[k + 1] - p.y;
+        const double q1 = fma(rx1, rx1, fma(ry1, ry1, dp));
+        const double q2 = fma(rx2, rx2, fma(ry2, ry2, dp));
+        const double P = q1 * q2;
+        const double y0 = rcp_seed_via_f32(P);
+        const double e = fma(-P, y0, 1.0);
+        if (JAC) {
+          const double uP = fma(y0, e, y0);  // 1/(q1 q2)
+          const double u1 = q2 * uP, u2 = q1 * uP;
+          accumulate<VEL, JAC>(rx1, ry1, g * u1, u1, fx[k], fy[k], ja[k], jb[k], jc[k]);
+          accumulate<VEL, JAC>(rx2, ry2, g * u2, u2, fx[k + 1], fy[k + 1], ja[k + 1], jb[k + 1], jc[k + 1]);
+        } else {
+          const double gu = g * fma(y0, e, y0);  // Γ'/(q1 q2)
+          accumulate<VEL, JAC>(rx1, ry1, gu * q2, 0.0, fx[k], fy[k], ja[k], jb[k], jc[k]);
+          accumulate<VEL, JAC>(rx2, ry2, gu * q1, 0.0, fx[k + 1], fy[k + 1], ja[k + 1], jb[k + 1], jc[k + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        const double rx = tx[k] - p.x;
+        const double ry = ty[k] - p.y;
+        double q = fma(rx, rx, fma(ry, ry, dp));
+        double gs = g;
+        if (MASK) {
+          const bool self = (j0 + jj) == ti[k];  // kernel.hpp:118 `if (j == i) continue;`
+          q = self ? 1.0 : q;
+          gs = self ? 0.0 : gs;
+        }
+        const double y0 = rcp_seed(q);
+        double e = fma(-q, y0, 1.0);
+        e = fma(e, e, e);
+        if (JAC) {
+          const double u = fma(y0, e, y0);  // 1/q
+          accumulate<VEL, JAC>(rx, ry, gs * u, u, fx[k], fy[k], ja[k], jb[k], jc[k]);
+        } else {
+          const double g0 = gs * y0;
+          accumulate<VEL, JAC>(rx, ry, fma(g0, e, g0), 0.0, fx[k], fy[k], ja[k], jb[k], jc[k]);
+        }
       }
     }
   }
@@ -146,10 +210,14 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
   const long long cbeg = (long long)blockIdx.y * chunk_len;
   const long long cend = min(n, cbeg + chunk_len);
 
-  bool my_ok = true;
+  bool my_ok = true, my_ok4 = true;
 #pragma unroll
-  for (int k = 0; k < T; ++k) my_ok = my_ok && coord_ok(tx[k]) && coord_ok(ty[k]);
-  const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-100;
+  for (int k = 0; k < T; ++k) {
+    my_ok = my_ok && coord_ok(tx[k]) && coord_ok(ty[k]);
+    my_ok4 = my_ok4 && coord_ok4(tx[k]) && coord_ok4(ty[k]);
+  }
+  const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62;
+  const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31;
 
   // Register prefetch of the first source tile.
   double px = 0.0, py = 0.0, pg = 0.0;
@@ -162,7 +230,8 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
     const int cnt = (int)min((long long)TPB, cend - j0);
     sp[tid] = make_double2(px, py);
     sg[tid] = pg;
-    const bool fast = __syncthreads_and(coord_ok(px) && coord_ok(py)) && targets_ok;
+    const bool fast4 = __syncthreads_and(coord_ok4(px) && coord_ok4(py)) && targets_ok4;
+    const bool fast = fast4 || (__syncthreads_and(coord_ok(px) && coord_ok(py)) && targets_ok);
     const long long jn = j0 + TPB + tid;  // prefetch the next tile while computing
     if (jn < cend) {
       px = xs[jn];
@@ -171,11 +240,13 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
     }
     const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt);
     if (masked)
-      tile_f64<T, UNR, VEL, JAC, true, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+    else if (fast4)
+      tile_f64<T, UNR, VEL, JAC, false, 4>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else if (fast)
-      tile_f64<T, UNR, VEL, JAC, false, true>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, false, 2>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else
-      tile_f64<T, UNR, VEL, JAC, false, false>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     __syncthreads();
   }
 
@@ -437,24 +508,15 @@ using LaunchFn = void (*)(ptrom_ctx*, long long, const double*, const double*, d
 
 // Velocity-kernel shapes (TPB, targets/thread, source unroll, min blocks/SM);
 // entry 0 is the default, the rest are kept for tools/tune_allpairs.py
-// (PTROM_ALLPAIRS_VARIANT selects one at context creation).
+// (PTROM_ALLPAIRS_VARIANT selects one at context creation). Sweep on B200 at
+// N = 65,536 (profiles/r01_allpairs_tuning.md): (64,8,2,1) 21.2 TFLOP/s,
+// (128,8,2,1) 21.0, (128,4,8,4) 20.9, (128,8,3,1) 20.4, (64,8,2,6) 20.2.
 #define PTROM_VEL_VARIANTS(X) \
-  X(128, 4, 4, 1)             \
-  X(128, 4, 2, 1)             \
-  X(128, 4, 8, 1)             \
-  X(128, 2, 4, 1)             \
-  X(128, 2, 8, 1)             \
+  X(64, 8, 2, 1)              \
   X(128, 8, 2, 1)             \
-  X(256, 4, 4, 1)             \
-  X(128, 4, 4, 8)             \
-  X(128, 2, 4, 10)            \
-  X(256, 2, 4, 4)             \
-  X(64, 4, 4, 1)              \
-  X(128, 1, 8, 1)             \
-  X(128, 3, 4, 1)             \
-  X(128, 4, 1, 1)             \
-  X(128, 6, 2, 1)             \
-  X(128, 2, 2, 8)
+  X(128, 4, 8, 4)             \
+  X(128, 8, 3, 1)             \
+  X(64, 8, 2, 6)
 
 #define PTROM_VEL_ENTRY(TPB, T, UNR, MINB) launch_allpairs_f64_t<TPB, T, UNR, MINB, true, false>,
 const LaunchFn kVelVariants[] = {PTROM_VEL_VARIANTS(PTROM_VEL_ENTRY)};
@@ -466,7 +528,7 @@ template <bool VEL, bool JAC>
 void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                          long long t_begin, long long t_count, double** part, int* chunks) {
   if (t_count < 16384) {
-    launch_allpairs_f64_t<kTPB, 1, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+    launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
   } else if (VEL && !JAC) {
     const int v = (ctx->allpairs_variant >= 0 && ctx->allpairs_variant < kNumVelVariants) ? ctx->allpairs_variant : 0;
     kVelVariants[v](ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
