@@ -106,6 +106,17 @@ def measured_peaks(device: int):
             "rcp_cubic_max_rel_err": out[6]}
 
 
+def ncu_traffic(name):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed `ncu --set full` summary of the same kernel (profiles/)."""
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        d = json.load(open(path))
+        return float(d["dram__bytes_read.sum"]) * 1e6 + float(d["dram__bytes_write.sum"])
+    except Exception:
+        return None
+
+
 def cpu_baseline_sample(w, threads: int, target_seconds: float):
     """Oracle (the reference's serial loop, kernel.hpp:107-129) on a bounded
     target sample × all sources; returns pairs/s and the sample description."""
@@ -274,8 +285,10 @@ def main():
     roofline = None
     if peaks:
         roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peaks["fp64_dfma_tflops"],
-                    "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_dfma_tflops"], "traffic": None,
-                    "kernel": "allpairs_f64_kernel<128,4,vel>",
+                    "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_dfma_tflops"],
+                    "traffic": ncu_traffic("r01_allpairs_vel64_ncu_summary.json"),
+                    "algorithmic_bytes_per_launch": 24 * n,
+                    "kernel": "allpairs_f64_kernel<64,8,2,1,vel> (csrc/allpairs.cu)",
                     "peak_source": "measured live: tools/peaks.cu DFMA chain (MEASURED_PEAKS.json has no FP64)",
                     "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": local_pairs,
                     "avg_launch_ms": avg_kernel_s * 1e3, "launches": kern_launches.value,
