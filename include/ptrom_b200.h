@@ -111,6 +111,49 @@ int ptrom_dev_residual_f64(ptrom_ctx* ctx, int64_t m, int64_t ld, const double* 
 int ptrom_dev_newton_update_f64(ptrom_ctx* ctx, int64_t m, int64_t ld, const double* d_inv, const double* d_r,
                                 double* d_x);
 
+/* ------------------------------------------------------------------ tree -- */
+/* quadtree.hpp:34-47 QuadTree, device-resident; owned by the caller, bound to
+ * the context that built it. Node ids are the reference's preorder ids. */
+typedef struct ptrom_tree ptrom_tree;
+/* quadtree.hpp:124-162 build_tree<double>(points N x 2, gamma, leaf_capacity);
+ * points given as the two columns px, py. */
+int ptrom_tree_build_f64(ptrom_ctx* ctx, int64_t n, const double* px, const double* py, const double* gamma,
+                         int64_t leaf_capacity, ptrom_tree** out);
+int ptrom_dev_tree_build_f64(ptrom_ctx* ctx, int64_t n, const double* d_px, const double* d_py,
+                             const double* d_gamma, int64_t leaf_capacity, ptrom_tree** out);
+void ptrom_tree_free(ptrom_tree* tree);
+int64_t ptrom_tree_num_nodes(const ptrom_tree* tree);
+/* TreeNode fields (quadtree.hpp:15-30) in structure-of-arrays form plus perm,
+ * slot, leaf_node (quadtree.hpp:37-39). Any pointer may be NULL. */
+int ptrom_tree_export(ptrom_ctx* ctx, const ptrom_tree* tree, double* bounds /* 4/node */, double* width,
+                      double* centroid /* 2/node */, double* gamma_sum, int32_t* children /* 4/node */,
+                      int64_t* begin, int64_t* end, int32_t* depth, uint8_t* centroid_fallback, int64_t* perm,
+                      int64_t* slot, int32_t* leaf_node);
+/* quadtree.hpp:213-252 collect_clusters for n_targets target ids, CSR output:
+ * cluster node ids (preorder) and direct ids (ascending). Two-call protocol:
+ * offsets (n_targets+1 each) are always filled; the lists are written when
+ * the capacities suffice. */
+int ptrom_collect_clusters(ptrom_ctx* ctx, ptrom_tree* tree, int crit_kind, double crit_value, int64_t n_targets,
+                           const int64_t* targets, int64_t* cluster_offsets, int32_t* clusters,
+                           int64_t clusters_cap, int64_t* direct_offsets, int64_t* direct, int64_t direct_cap);
+/* quadtree.hpp:257-281 bh_velocity<double>(tree, state, sys, criterion). */
+int ptrom_bh_velocity_f64(ptrom_ctx* ctx, ptrom_tree* tree, int64_t n, const double* x, const double* gamma,
+                          double delta, int form, int crit_kind, double crit_value, const double* inflow,
+                          double* f, uint64_t* n_pair_evals);
+/* quadtree.hpp:285-308 bh_jacobian<double>. */
+int ptrom_bh_jacobian_f64(ptrom_ctx* ctx, ptrom_tree* tree, int64_t n, const double* x, const double* gamma,
+                          double delta, int form, int crit_kind, double crit_value, double* dfx_dx,
+                          double* dfx_dy, double* dfy_dx, double* dfy_dy);
+/* integrators.hpp:96-98 BarnesHutModel::velocity: rebuild the tree from the
+ * state (leaf_capacity) and evaluate; host and device-buffer forms. */
+int ptrom_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
+                                  int form, int crit_kind, double crit_value, int64_t leaf_capacity,
+                                  const double* inflow, double* f, uint64_t* n_pair_evals);
+int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                      double delta, int form, int crit_kind, double crit_value,
+                                      int64_t leaf_capacity, const double* d_inflow, double* d_f,
+                                      uint64_t* n_pair_evals);
+
 /* --------------------------------------------------------- instrumentation -- */
 /* bench.py support: while enabled, the context records CUDA events on its own
  * stream around every launch of the dominant kernel of each call (the

@@ -46,6 +46,21 @@ PROTOTYPES = {
     "ptrom_dev_residual_f64": (
         C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp, C.c_double, c_dp, c_dp]),
     "ptrom_dev_newton_update_f64": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_dp, c_dp]),
+    "ptrom_tree_build_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, c_dp, c_i64, C.POINTER(C.c_void_p)]),
+    "ptrom_dev_tree_build_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, c_dp, c_i64, C.POINTER(C.c_void_p)]),
+    "ptrom_tree_free": (None, [C.c_void_p]),
+    "ptrom_tree_num_nodes": (c_i64, [C.c_void_p]),
+    "ptrom_tree_export": (C.c_int, [c_ctxp, C.c_void_p] + [c_dp] * 12),
+    "ptrom_collect_clusters": (C.c_int, [c_ctxp, C.c_void_p, C.c_int, C.c_double, c_i64, c_dp, c_dp, c_dp, c_i64,
+                                         c_dp, c_dp, c_i64]),
+    "ptrom_bh_velocity_f64": (C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int,
+                                        C.c_double, c_dp, c_dp, c_u64p]),
+    "ptrom_bh_jacobian_f64": (C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int,
+                                        C.c_double, c_dp, c_dp, c_dp, c_dp]),
+    "ptrom_barnes_hut_velocity_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int, C.c_double,
+                                                c_i64, c_dp, c_dp, c_u64p]),
+    "ptrom_dev_barnes_hut_velocity_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int,
+                                                    C.c_double, c_i64, c_dp, c_dp, c_u64p]),
     "ptrom_profile_begin": (C.c_int, [c_ctxp]),
     "ptrom_profile_end": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

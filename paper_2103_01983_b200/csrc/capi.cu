@@ -2,6 +2,7 @@
 // mapping and the host-buffer drop-in entry points. Validation mirrors the
 // reference's ParticleSystem::validate / check_state (kernel.hpp:84-103) so
 // status codes and messages match the reference's exceptions.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -105,6 +106,7 @@ int ptrom_create(int device, void* stream, ptrom_ctx** out) {
     if (major != 10) throw status_error(PTROM_CUDA_ERROR, "libptrom_b200 requires an sm_100a (B200) device");
     ctx->num_sms = sms;
     if (const char* v = std::getenv("PTROM_ALLPAIRS_VARIANT")) ctx->allpairs_variant = std::atoi(v);
+    if (const char* v = std::getenv("PTROM_TREE_SEQ_MAX")) ctx->tree_seq_max = std::max(1, std::atoi(v));
     PTROM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DeviceStatus)));
     PTROM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DeviceStatus)));
     DeviceStatus clear{0, 0, LLONG_MAX};

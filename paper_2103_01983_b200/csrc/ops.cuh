@@ -2,6 +2,8 @@
 #pragma once
 #include "common.cuh"
 
+#include <vector>
+
 namespace ptrom {
 
 double effective_delta(double delta, int form);
@@ -26,5 +28,13 @@ FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, c
                               int form, const double* d_inflow, double dt, long long n_steps, double tol,
                               int max_iters, int refresh, double* h_snapshots, int* iters, unsigned char* conv,
                               double* rel_out);
+
+struct Tree;
+void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const double* d_py, const double* d_g,
+                long long leaf_cap, int seq_max);
+int tree_resolve_uncertain(ptrom_ctx* ctx, Tree& t, const int* d_flag_count);
+unsigned long long tree_eval(ptrom_ctx* ctx, Tree& t, const double* d_x, const double* d_gamma, double delta,
+                             int form, int crit_kind, double crit_value, const double* d_inflow, double* d_f,
+                             double* jxx, double* jxy, double* jyx, double* jyy);
 
 }  // namespace ptrom

@@ -1,0 +1,663 @@
+// tree.cu — Barnes–Hut quadtree on sm_100a: build, aggregation, traversal.
+//
+// Replaces quadtree.hpp:51-308 (build_tree, finish_node, split_node,
+// bh_prune_check, neighbor_prune_check, collect_clusters, bh_velocity,
+// bh_jacobian) and BarnesHutModel integrators.hpp:83-102.
+//
+// Build = MSD radix sort on the replayed midpoint path, one 2-bit digit per
+// level. Level d holds the nodes created at depth d; for every node that
+// splits (count > leaf_capacity and depth < 64, quadtree.hpp:74) each member
+// computes its quadrant with the reference's arithmetic ((b0+b1)/2 midpoint,
+// `<=` goes SW, quadtree.hpp:77-85) and the members are stably partitioned
+// into SW, SE, NW, NE by a global 4-counter exclusive scan + scatter. Because
+// every partition is stable and the first order is the identity, each node's
+// segment is in ascending particle-id order when it is created — exactly the
+// order finish_node (quadtree.hpp:51-67) sums in — and leaf members end up in
+// ascending-id order inside perm like the reference's stable buckets.
+//
+// Preorder ids (quadtree.hpp:97-116 assign a child id then recurse): sorting
+// all nodes by (begin, depth) yields preorder, so ids are the rank of that
+// 64-bit key (CUB radix sort). skip[id] = first node with begin >= end is the
+// stackless-DFS successor of a pruned/leaf node.
+//
+// Aggregation: nodes with <= kSeqMax members sum their segment sequentially
+// in the reference order with _rn intrinsics (bit-identical gamma_sum and
+// centroid, "exact"); larger nodes use a fixed-order block reduction (run to
+// run deterministic) and carry a rigorous error bound on the centroid. A
+// Barnes–Hut prune test on a non-exact node whose ratio lies within that
+// bound of θ is "uncertain": the node's exact sequential sums are computed
+// and the traversal is re-run, so prune decisions — and hence cluster lists
+// — are always the reference's.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "ops.cuh"
+#include "tree.cuh"
+
+namespace ptrom {
+
+namespace {
+
+constexpr int kMaxDepth = 64;  // quadtree.hpp:13
+constexpr int kThreads = 256;
+
+template <class T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count) PTROM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+int grid_for(ptrom_ctx* ctx, long long count, int tpb = kThreads) {
+  long long g = (count + tpb - 1) / tpb;
+  return (int)std::max(1LL, std::min(g, (long long)ctx->num_sms * 16));
+}
+
+struct U4Sum {
+  __host__ __device__ uint4 operator()(const uint4& a, const uint4& b) const {
+    return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+  }
+};
+
+__device__ __forceinline__ unsigned comp(const uint4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+// ---------------------------------------------------------------- hull ---
+__global__ void hull_kernel(long long n, const double* __restrict__ px, const double* __restrict__ py,
+                            double* __restrict__ block_out) {
+  double xl = DBL_MAX, xh = -DBL_MAX, yl = DBL_MAX, yh = -DBL_MAX;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    xl = fmin(xl, px[i]);
+    xh = fmax(xh, px[i]);
+    yl = fmin(yl, py[i]);
+    yh = fmax(yh, py[i]);
+  }
+  using BR = cub::BlockReduce<double, kThreads>;
+  __shared__ typename BR::TempStorage t0, t1, t2, t3;
+  xl = BR(t0).Reduce(xl, cub::Min());
+  xh = BR(t1).Reduce(xh, cub::Max());
+  yl = BR(t2).Reduce(yl, cub::Min());
+  yh = BR(t3).Reduce(yh, cub::Max());
+  if (threadIdx.x == 0) {
+    block_out[4 * blockIdx.x + 0] = xl;
+    block_out[4 * blockIdx.x + 1] = xh;
+    block_out[4 * blockIdx.x + 2] = yl;
+    block_out[4 * blockIdx.x + 3] = yh;
+  }
+}
+
+__global__ void iota_copy_kernel(long long n, const double* __restrict__ px, const double* __restrict__ py,
+                                 const double* __restrict__ g, int* __restrict__ ord, double* __restrict__ sx,
+                                 double* __restrict__ sy, double* __restrict__ sg, int* __restrict__ pos_rec,
+                                 int root_splits) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    ord[i] = (int)i;
+    sx[i] = px[i];
+    sy[i] = py[i];
+    sg[i] = g[i];
+    pos_rec[i] = root_splits ? 0 : -1;
+  }
+}
+
+// ------------------------------------------------------------- levels ---
+// quadtree.hpp:81-86: quadrant digit of each member of a splitting node.
+__global__ void digit_kernel(long long n, const int* __restrict__ pos_rec, const double* __restrict__ sx,
+                             const double* __restrict__ sy, const double* __restrict__ rec_mid, uint4* __restrict__ flags,
+                             unsigned char* __restrict__ digit) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= n; k += (long long)gridDim.x * blockDim.x) {
+    uint4 f = make_uint4(0, 0, 0, 0);
+    if (k < n) {
+      const int r = pos_rec[k];
+      if (r >= 0) {
+        const double cx = rec_mid[2 * r], cy = rec_mid[2 * r + 1];
+        const int qx = sx[k] <= cx ? 0 : 1;
+        const int qy = sy[k] <= cy ? 0 : 1;
+        const int q = qy * 2 + qx;
+        digit[k] = (unsigned char)q;
+        f.x = q == 0;
+        f.y = q == 1;
+        f.z = q == 2;
+        f.w = q == 3;
+      }
+    }
+    flags[k] = f;
+  }
+}
+
+// Per level node: child counts (from the scan) and number of children.
+__global__ void child_count_kernel(int L, int lv_base, const int* __restrict__ rec_begin,
+                                   const int* __restrict__ rec_end, const unsigned char* __restrict__ rec_split,
+                                   const uint4* __restrict__ scan, int* __restrict__ nchild) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const int r = lv_base + l;
+  int c = 0;
+  if (rec_split[r]) {
+    const uint4 a = scan[rec_begin[r]], b = scan[rec_end[r]];
+    c = (b.x != a.x) + (b.y != a.y) + (b.z != a.z) + (b.w != a.w);
+  }
+  nchild[l] = c;
+}
+
+// quadtree.hpp:87-116: child records in SW, SE, NW, NE order.
+__global__ void make_children_kernel(int L, int lv_base, int next_base, int leaf_cap, const uint4* __restrict__ scan,
+                                     const int* __restrict__ child_off, TreeRecords rec, int* __restrict__ n_split_next) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const int r = lv_base + l;
+  if (!rec.split[r]) return;
+  const uint4 a = scan[rec.begin[r]], b = scan[rec.end[r]];
+  const double b0 = rec.bounds[4 * r], b1 = rec.bounds[4 * r + 1], b2 = rec.bounds[4 * r + 2], b3 = rec.bounds[4 * r + 3];
+  const double cx = rec.mid[2 * r], cy = rec.mid[2 * r + 1];
+  const double half = __ddiv_rn(rec.width[r], 2.0);
+  int cursor = rec.begin[r];
+  int j = 0;
+  int splits = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int cnt = (int)(comp(b, q) - comp(a, q));
+    if (cnt == 0) continue;
+    const int c = next_base + child_off[l] + (j++);
+    rec.children[4 * r + q] = c;
+    rec.begin[c] = cursor;
+    rec.end[c] = cursor + cnt;
+    cursor += cnt;
+    const double cb0 = (q & 1) ? cx : b0, cb1 = (q & 1) ? b1 : cx;
+    const double cb2 = (q & 2) ? cy : b2, cb3 = (q & 2) ? b3 : cy;
+    rec.bounds[4 * c] = cb0;
+    rec.bounds[4 * c + 1] = cb1;
+    rec.bounds[4 * c + 2] = cb2;
+    rec.bounds[4 * c + 3] = cb3;
+    rec.mid[2 * c] = __dmul_rn(__dadd_rn(cb0, cb1), 0.5);  // (b0 + b1) / 2, exact halving
+    rec.mid[2 * c + 1] = __dmul_rn(__dadd_rn(cb2, cb3), 0.5);
+    rec.width[c] = half;
+    rec.depth[c] = rec.depth[r] + 1;
+    rec.children[4 * c] = rec.children[4 * c + 1] = rec.children[4 * c + 2] = rec.children[4 * c + 3] = -1;
+    const bool sp = cnt > leaf_cap && rec.depth[r] + 1 < kMaxDepth;
+    rec.split[c] = sp ? 1 : 0;
+    splits += sp;
+  }
+  if (splits) atomicAdd(n_split_next, splits);
+}
+
+// Stable scatter of the splitting nodes' members into their children.
+__global__ void scatter_kernel(long long n, const int* __restrict__ pos_rec, const unsigned char* __restrict__ digit,
+                               const uint4* __restrict__ scan, TreeRecords rec, const int* __restrict__ ord,
+                               const double* __restrict__ sx, const double* __restrict__ sy,
+                               const double* __restrict__ sg, int* __restrict__ ord_n, double* __restrict__ sx_n,
+                               double* __restrict__ sy_n, double* __restrict__ sg_n, int* __restrict__ pos_rec_n) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const int r = pos_rec[k];
+    long long np = k;
+    int nrec = -1;
+    if (r >= 0) {
+      const int q = digit[k];
+      const int c = rec.children[4 * r + q];
+      np = rec.begin[c] + (long long)(comp(scan[k], q) - comp(scan[rec.begin[r]], q));
+      nrec = rec.split[c] ? c : -1;
+    }
+    ord_n[np] = ord[k];
+    sx_n[np] = sx[k];
+    sy_n[np] = sy[k];
+    sg_n[np] = sg[k];
+    pos_rec_n[np] = nrec;
+  }
+}
+
+// quadtree.hpp:51-67 finish_node for small nodes: sequential, reference order.
+__global__ void sums_small_kernel(int R0, int R1, TreeRecords rec, const double* __restrict__ sx,
+                                  const double* __restrict__ sy, const double* __restrict__ sg, int seq_max,
+                                  int* __restrict__ large_list, int* __restrict__ large_count) {
+  const int r = R0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R1) return;
+  const int b = rec.begin[r], e = rec.end[r];
+  if (e - b > seq_max) {
+    large_list[atomicAdd(large_count, 1)] = r;
+    return;
+  }
+  double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+  for (int k = b; k < e; ++k) {
+    const double g = sg[k], x = sx[k], y = sy[k];
+    gs = __dadd_rn(gs, g);
+    wx = __dadd_rn(wx, __dmul_rn(g, x));
+    wy = __dadd_rn(wy, __dmul_rn(g, y));
+    plx = __dadd_rn(plx, x);
+    ply = __dadd_rn(ply, y);
+  }
+  rec.gamma_sum[r] = gs;
+  const bool fb = gs == 0.0;
+  rec.fallback[r] = fb ? 1 : 0;
+  const double c = (double)(e - b);
+  rec.centroid[2 * r] = fb ? __ddiv_rn(plx, c) : __ddiv_rn(wx, gs);
+  rec.centroid[2 * r + 1] = fb ? __ddiv_rn(ply, c) : __ddiv_rn(wy, gs);
+  rec.exact[r] = 1;
+  rec.cerr[r] = 0.0;
+}
+
+// Large nodes: fixed-order block reduction + rigorous centroid error bound
+// relative to the reference's sequential order.
+__global__ void sums_large_kernel(TreeRecords rec, const double* __restrict__ sx, const double* __restrict__ sy,
+                                  const double* __restrict__ sg, const int* __restrict__ large_list,
+                                  const int* __restrict__ large_count) {
+  using BR = cub::BlockReduce<double, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ double red[8];
+  const int total = *large_count;
+  for (int li = blockIdx.x; li < total; li += gridDim.x) {
+    const int r = large_list[li];
+    const int b = rec.begin[r], e = rec.end[r];
+    double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // gs wx wy plx ply |g| |gx| |gy|
+    for (int k = b + threadIdx.x; k < e; k += kThreads) {
+      const double g = sg[k], x = sx[k], y = sy[k];
+      const double gx = __dmul_rn(g, x), gy = __dmul_rn(g, y);
+      v[0] = __dadd_rn(v[0], g);
+      v[1] = __dadd_rn(v[1], gx);
+      v[2] = __dadd_rn(v[2], gy);
+      v[3] = __dadd_rn(v[3], x);
+      v[4] = __dadd_rn(v[4], y);
+      v[5] = __dadd_rn(v[5], fabs(g));
+      v[6] = __dadd_rn(v[6], fabs(gx));
+      v[7] = __dadd_rn(v[7], fabs(gy));
+    }
+    for (int c = 0; c < 8; ++c) {
+      const double t = BR(tmp).Sum(v[c]);
+      if (threadIdx.x == 0) red[c] = t;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double m = (double)(e - b);
+      const double u = 0x1p-53;
+      // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
+      // sum; their difference within twice that (first order, padded).
+      const double k2 = 2.05 * (m + 1.0) * u;
+      const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
+      const double gs = red[0];
+      rec.gamma_sum[r] = gs;
+      const bool fb = gs == 0.0;
+      rec.fallback[r] = fb ? 1 : 0;
+      double cx, cy, err;
+      if (fb) {
+        cx = __ddiv_rn(red[3], m);
+        cy = __ddiv_rn(red[4], m);
+      } else {
+        cx = __ddiv_rn(red[1], gs);
+        cy = __ddiv_rn(red[2], gs);
+      }
+      if (fabs(gs) <= 2.0 * eg) {
+        err = INFINITY;  // the fallback flag itself is uncertain
+      } else {
+        const double ag = fabs(gs) - eg;
+        err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
+      }
+      rec.centroid[2 * r] = cx;
+      rec.centroid[2 * r + 1] = cy;
+      rec.exact[r] = 0;
+      rec.cerr[r] = err;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ preorder ---
+__global__ void preorder_keys_kernel(int R, const int* __restrict__ rbegin, const int* __restrict__ rdepth,
+                                     unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  keys[r] = ((unsigned long long)rbegin[r] << 7) | (unsigned long long)rdepth[r];
+  vals[r] = r;
+}
+
+__global__ void rec2id_kernel(int R, const int* __restrict__ order, int* __restrict__ rec2id) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < R) rec2id[order[i]] = i;
+}
+
+__global__ void emit_nodes_kernel(int R, const int* __restrict__ order, const int* __restrict__ rec2id,
+                                  const unsigned long long* __restrict__ sorted_keys, TreeRecords rec, TreeNodes nd) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= R) return;
+  const int r = order[id];
+  for (int k = 0; k < 4; ++k) {
+    nd.bounds[4 * id + k] = rec.bounds[4 * r + k];
+    const int c = rec.children[4 * r + k];
+    nd.children[4 * id + k] = c >= 0 ? rec2id[c] : -1;
+  }
+  const int b = rec.begin[r], e = rec.end[r];
+  const bool leaf = rec.children[4 * r] < 0 && rec.children[4 * r + 1] < 0 && rec.children[4 * r + 2] < 0 &&
+                    rec.children[4 * r + 3] < 0;
+  // skip: first node in preorder with begin >= e
+  const unsigned long long key = (unsigned long long)e << 7;
+  int lo = id + 1, hi = R;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sorted_keys[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  nd.width[id] = rec.width[r];
+  nd.centroid[2 * id] = rec.centroid[2 * r];
+  nd.centroid[2 * id + 1] = rec.centroid[2 * r + 1];
+  nd.gamma_sum[id] = rec.gamma_sum[r];
+  nd.begin[id] = b;
+  nd.end[id] = e;
+  nd.depth[id] = rec.depth[r];
+  nd.fallback[id] = rec.fallback[r];
+  nd.exact[id] = rec.exact[r];
+  nd.cerr[id] = rec.cerr[r];
+  nd.skip[id] = lo;
+  nd.leaf[id] = leaf ? 1 : 0;
+}
+
+__global__ void particle_maps_kernel(long long n, const int* __restrict__ perm, int* __restrict__ slot) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    slot[perm[k]] = (int)k;
+}
+
+__global__ void leaf_node_kernel(int R, TreeNodes nd, const int* __restrict__ perm, int* __restrict__ leaf_node) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= R || !nd.leaf[id]) return;
+  for (int k = nd.begin[id]; k < nd.end[id]; ++k) leaf_node[perm[k]] = id;
+}
+
+// Exact sequential sums for the flagged (uncertain) nodes: members in
+// ascending id order are {p : begin <= slot[p] < end}.
+__global__ void exact_sums_kernel(int R, long long n, TreeNodes nd, const int* __restrict__ slot,
+                                  const double* __restrict__ px, const double* __restrict__ py,
+                                  const double* __restrict__ g) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= R || !nd.need_exact[id] || nd.exact[id]) return;
+  const int b = nd.begin[id], e = nd.end[id];
+  double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+  for (long long p = 0; p < n; ++p) {
+    const int s = slot[p];
+    if (s < b || s >= e) continue;
+    const double gg = g[p], x = px[p], y = py[p];
+    gs = __dadd_rn(gs, gg);
+    wx = __dadd_rn(wx, __dmul_rn(gg, x));
+    wy = __dadd_rn(wy, __dmul_rn(gg, y));
+    plx = __dadd_rn(plx, x);
+    ply = __dadd_rn(ply, y);
+  }
+  nd.gamma_sum[id] = gs;
+  const bool fb = gs == 0.0;
+  nd.fallback[id] = fb ? 1 : 0;
+  const double c = (double)(e - b);
+  nd.centroid[2 * id] = fb ? __ddiv_rn(plx, c) : __ddiv_rn(wx, gs);
+  nd.centroid[2 * id + 1] = fb ? __ddiv_rn(ply, c) : __ddiv_rn(wy, gs);
+  nd.exact[id] = 1;
+  nd.cerr[id] = 0.0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- build ---
+void TreeRecords::alloc(size_t cap_) {
+  cap = cap_;
+  begin = dalloc<int>(cap);
+  end = dalloc<int>(cap);
+  depth = dalloc<int>(cap);
+  children = dalloc<int>(4 * cap);
+  split = dalloc<unsigned char>(cap);
+  fallback = dalloc<unsigned char>(cap);
+  exact = dalloc<unsigned char>(cap);
+  bounds = dalloc<double>(4 * cap);
+  mid = dalloc<double>(2 * cap);
+  width = dalloc<double>(cap);
+  centroid = dalloc<double>(2 * cap);
+  gamma_sum = dalloc<double>(cap);
+  cerr = dalloc<double>(cap);
+}
+void TreeRecords::free() {
+  void* ps[] = {begin, end, depth, children, split, fallback, exact, bounds, mid, width, centroid, gamma_sum, cerr};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  *this = TreeRecords{};
+}
+void TreeRecords::grow(size_t need, size_t used, cudaStream_t s) {
+  if (need <= cap) return;
+  TreeRecords n;
+  n.alloc(std::max(need, cap * 2));
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) PTROM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+  };
+  cp(n.begin, begin, used * 4);
+  cp(n.end, end, used * 4);
+  cp(n.depth, depth, used * 4);
+  cp(n.children, children, used * 16);
+  cp(n.split, split, used);
+  cp(n.fallback, fallback, used);
+  cp(n.exact, exact, used);
+  cp(n.bounds, bounds, used * 32);
+  cp(n.mid, mid, used * 16);
+  cp(n.width, width, used * 8);
+  cp(n.centroid, centroid, used * 16);
+  cp(n.gamma_sum, gamma_sum, used * 8);
+  cp(n.cerr, cerr, used * 8);
+  PTROM_CUDA(cudaStreamSynchronize(s));
+  free();
+  *this = n;
+}
+
+void TreeNodes::alloc(size_t nn) {
+  count = nn;
+  bounds = dalloc<double>(4 * nn);
+  width = dalloc<double>(nn);
+  centroid = dalloc<double>(2 * nn);
+  gamma_sum = dalloc<double>(nn);
+  cerr = dalloc<double>(nn);
+  children = dalloc<int>(4 * nn);
+  begin = dalloc<int>(nn);
+  end = dalloc<int>(nn);
+  depth = dalloc<int>(nn);
+  skip = dalloc<int>(nn);
+  fallback = dalloc<unsigned char>(nn);
+  exact = dalloc<unsigned char>(nn);
+  leaf = dalloc<unsigned char>(nn);
+  need_exact = dalloc<unsigned char>(nn);
+}
+void TreeNodes::free() {
+  void* ps[] = {bounds, width, centroid, gamma_sum, cerr, children, begin, end, depth, skip, fallback, exact, leaf,
+                need_exact};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  *this = TreeNodes{};
+}
+
+void Tree::free_all() {
+  nodes.free();
+  void* ps[] = {perm, slot, leaf_node, sx, sy, sg, px, py, g};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  perm = slot = leaf_node = nullptr;
+  sx = sy = sg = px = py = g = nullptr;
+}
+
+// quadtree.hpp:124-162 build_tree over device points (px, py) and weights g.
+void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const double* d_py, const double* d_g,
+                long long leaf_cap, int seq_max) {
+  if (n <= 0) config_fail("build_tree: no points");
+  if (n >= (1LL << 30)) config_fail("build_tree: more than 2^30 points is not supported");
+  if (leaf_cap < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+  cudaStream_t s = ctx->stream;
+  t.free_all();
+  t.n = n;
+  t.leaf_cap = leaf_cap;
+  // keep the build inputs (exact-sum fallback and collect_clusters target positions)
+  t.px = dalloc<double>(n);
+  t.py = dalloc<double>(n);
+  t.g = dalloc<double>(n);
+  PTROM_CUDA(cudaMemcpyAsync(t.px, d_px, n * 8, cudaMemcpyDeviceToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(t.py, d_py, n * 8, cudaMemcpyDeviceToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(t.g, d_g, n * 8, cudaMemcpyDeviceToDevice, s));
+
+  // ---- root: tight square hull (quadtree.hpp:139-151)
+  const int hb = std::min<long long>((n + kThreads - 1) / kThreads, 256);
+  double* hull = dalloc<double>(4 * hb);
+  hull_kernel<<<hb, kThreads, 0, s>>>(n, t.px, t.py, hull);
+  PTROM_LAUNCH_CHECK();
+  std::vector<double> hh(4 * hb);
+  PTROM_CUDA(cudaMemcpyAsync(hh.data(), hull, hh.size() * 8, cudaMemcpyDeviceToHost, s));
+  PTROM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(hull);
+  double x_lo = hh[0], x_hi = hh[1], y_lo = hh[2], y_hi = hh[3];
+  for (int b = 1; b < hb; ++b) {
+    x_lo = std::min(x_lo, hh[4 * b]);
+    x_hi = std::max(x_hi, hh[4 * b + 1]);
+    y_lo = std::min(y_lo, hh[4 * b + 2]);
+    y_hi = std::max(y_hi, hh[4 * b + 3]);
+  }
+  if (!std::isfinite(x_lo) || !std::isfinite(x_hi) || !std::isfinite(y_lo) || !std::isfinite(y_hi))
+    config_fail("build_tree: non-finite input");
+  double side = std::max(x_hi - x_lo, y_hi - y_lo);
+  if (side == 0.0) side = 1.0;
+  const double cx = (x_lo + x_hi) / 2.0, cy = (y_lo + y_hi) / 2.0;
+  const double rb[4] = {cx - side / 2.0, cx + side / 2.0, cy - side / 2.0, cy + side / 2.0};
+  const double rmid[2] = {(rb[0] + rb[1]) / 2.0, (rb[2] + rb[3]) / 2.0};
+
+  TreeRecords rec;
+  rec.alloc(std::max<size_t>(1024, (size_t)(n / std::max<long long>(1, leaf_cap)) * 2 + 16));
+  const int zero = 0, one = 1, neg[4] = {-1, -1, -1, -1};
+  const int nn32 = (int)n, d0 = 0;
+  const unsigned char root_split = (n > leaf_cap) ? 1 : 0;
+  PTROM_CUDA(cudaMemcpyAsync(rec.begin, &zero, 4, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.end, &nn32, 4, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.depth, &d0, 4, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.children, neg, 16, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.split, &root_split, 1, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.bounds, rb, 32, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.mid, rmid, 16, cudaMemcpyHostToDevice, s));
+  PTROM_CUDA(cudaMemcpyAsync(rec.width, &side, 8, cudaMemcpyHostToDevice, s));
+  (void)one;
+
+  // ---- level buffers
+  int *ord = dalloc<int>(n), *ord_n = dalloc<int>(n), *pr = dalloc<int>(n), *pr_n = dalloc<int>(n);
+  double *sx = dalloc<double>(n), *sy = dalloc<double>(n), *sg = dalloc<double>(n);
+  double *sx_n = dalloc<double>(n), *sy_n = dalloc<double>(n), *sg_n = dalloc<double>(n);
+  uint4* flags = dalloc<uint4>(n + 1);
+  uint4* scan = dalloc<uint4>(n + 1);
+  unsigned char* digit = dalloc<unsigned char>(n);
+  int* dcount = dalloc<int>(4);  // [0] splits at next level, [1] large-node count
+  int* h_counts = nullptr;
+  PTROM_CUDA(cudaMallocHost(&h_counts, 4 * sizeof(int)));
+  size_t scan_tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0), n + 1, s);
+  size_t scan2_tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan2_tmp_bytes, (int*)nullptr, (int*)nullptr, (int)std::min<long long>(n, INT_MAX), s);
+  void* tmp = dalloc<char>(std::max(scan_tmp_bytes, scan2_tmp_bytes) + 256);
+  int* nchild = nullptr;
+  int* child_off = nullptr;
+  size_t lvl_cap = 0;
+  int* large_list = dalloc<int>(std::max<long long>(1, n / std::max(1, seq_max) * 2 * kMaxDepth + 64));
+
+  iota_copy_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.px, t.py, t.g, ord, sx, sy, sg, pr, root_split);
+  PTROM_LAUNCH_CHECK();
+  // root sums
+  PTROM_CUDA(cudaMemsetAsync(dcount, 0, 16, s));
+  sums_small_kernel<<<1, 32, 0, s>>>(0, 1, rec, sx, sy, sg, seq_max, large_list, dcount + 1);
+  sums_large_kernel<<<1, kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1);
+  PTROM_LAUNCH_CHECK();
+
+  int lv_base = 0, L = 1, R = 1;
+  bool splitting = root_split;
+  while (splitting) {
+    // per-level buffers
+    if ((size_t)L > lvl_cap) {
+      if (nchild) cudaFree(nchild);
+      if (child_off) cudaFree(child_off);
+      lvl_cap = std::max<size_t>(L, lvl_cap * 2);
+      nchild = dalloc<int>(lvl_cap);
+      child_off = dalloc<int>(lvl_cap);
+    }
+    digit_kernel<<<grid_for(ctx, n + 1), kThreads, 0, s>>>(n, pr, sx, sy, rec.mid, flags, digit);
+    PTROM_LAUNCH_CHECK();
+    PTROM_CUDA(cub::DeviceScan::ExclusiveScan(tmp, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0),
+                                              n + 1, s));
+    child_count_kernel<<<(L + kThreads - 1) / kThreads, kThreads, 0, s>>>(L, lv_base, rec.begin, rec.end, rec.split,
+                                                                          scan, nchild);
+    PTROM_LAUNCH_CHECK();
+    PTROM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan2_tmp_bytes, nchild, child_off, L, s));
+    int last_off = 0, last_cnt = 0;
+    PTROM_CUDA(cudaMemcpyAsync(&h_counts[0], child_off + (L - 1), 4, cudaMemcpyDeviceToHost, s));
+    PTROM_CUDA(cudaMemcpyAsync(&h_counts[1], nchild + (L - 1), 4, cudaMemcpyDeviceToHost, s));
+    PTROM_CUDA(cudaStreamSynchronize(s));
+    last_off = h_counts[0];
+    last_cnt = h_counts[1];
+    const int C = last_off + last_cnt;
+    if (C == 0) break;
+    rec.grow((size_t)R + C, (size_t)R, s);
+    PTROM_CUDA(cudaMemsetAsync(dcount, 0, 16, s));
+    make_children_kernel<<<(L + kThreads - 1) / kThreads, kThreads, 0, s>>>(L, lv_base, R, (int)leaf_cap, scan,
+                                                                            child_off, rec, dcount);
+    PTROM_LAUNCH_CHECK();
+    scatter_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, pr, digit, scan, rec, ord, sx, sy, sg, ord_n, sx_n, sy_n,
+                                                         sg_n, pr_n);
+    PTROM_LAUNCH_CHECK();
+    std::swap(ord, ord_n);
+    std::swap(sx, sx_n);
+    std::swap(sy, sy_n);
+    std::swap(sg, sg_n);
+    std::swap(pr, pr_n);
+    sums_small_kernel<<<(C + 127) / 128, 128, 0, s>>>(R, R + C, rec, sx, sy, sg, seq_max, large_list, dcount + 1);
+    sums_large_kernel<<<std::min(C, ctx->num_sms * 4), kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1);
+    PTROM_LAUNCH_CHECK();
+    PTROM_CUDA(cudaMemcpyAsync(&h_counts[2], dcount, 4, cudaMemcpyDeviceToHost, s));
+    PTROM_CUDA(cudaStreamSynchronize(s));
+    splitting = h_counts[2] > 0;
+    lv_base = R;
+    L = C;
+    R += C;
+  }
+
+  // ---- preorder numbering (sort records by (begin, depth))
+  unsigned long long *keys = dalloc<unsigned long long>(R), *keys_s = dalloc<unsigned long long>(R);
+  int *vals = dalloc<int>(R), *order = dalloc<int>(R), *rec2id = dalloc<int>(R);
+  preorder_keys_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, rec.begin, rec.depth, keys, vals);
+  PTROM_LAUNCH_CHECK();
+  size_t sort_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys, keys_s, vals, order, R, 0, 7 + 31, s);
+  void* stmp = dalloc<char>(sort_bytes + 256);
+  PTROM_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sort_bytes, keys, keys_s, vals, order, R, 0, 7 + 31, s));
+  rec2id_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, order, rec2id);
+  t.nodes.alloc(R);
+  emit_nodes_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, order, rec2id, keys_s, rec, t.nodes);
+  PTROM_LAUNCH_CHECK();
+  PTROM_CUDA(cudaMemsetAsync(t.nodes.need_exact, 0, R, s));
+
+  t.perm = ord;
+  t.sx = sx;
+  t.sy = sy;
+  t.sg = sg;
+  t.slot = dalloc<int>(n);
+  t.leaf_node = dalloc<int>(n);
+  particle_maps_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.perm, t.slot);
+  leaf_node_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, t.nodes, t.perm, t.leaf_node);
+  PTROM_LAUNCH_CHECK();
+  PTROM_CUDA(cudaStreamSynchronize(s));
+
+  void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags, scan, digit, dcount, tmp, nchild, child_off, large_list,
+                   keys, keys_s, vals, order, rec2id, stmp};
+  for (void* p : frees)
+    if (p) cudaFree(p);
+  cudaFreeHost(h_counts);
+  rec.free();
+}
+
+// Computes exact sums for nodes flagged need_exact; returns how many.
+int tree_resolve_uncertain(ptrom_ctx* ctx, Tree& t, const int* d_flag_count) {
+  int h = 0;
+  PTROM_CUDA(cudaMemcpyAsync(&h, d_flag_count, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h == 0) return 0;
+  const int R = (int)t.nodes.count;
+  exact_sums_kernel<<<(R + 127) / 128, 128, 0, ctx->stream>>>(R, t.n, t.nodes, t.slot, t.px, t.py, t.g);
+  PTROM_LAUNCH_CHECK();
+  return h;
+}
+
+}  // namespace ptrom

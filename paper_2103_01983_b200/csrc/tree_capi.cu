@@ -1,0 +1,287 @@
+// tree_capi.cu — C ABI for the quadtree path (include/ptrom_b200.h "tree").
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "ops.cuh"
+#include "tree.cuh"
+
+namespace ptrom {
+void tree_collect(ptrom_ctx* ctx, Tree& t, int crit_kind, double crit_value, const std::vector<long long>& targets,
+                  std::vector<long long>& c_off, std::vector<int>& clusters, std::vector<long long>& d_off,
+                  std::vector<long long>& direct);
+}
+
+struct ptrom_tree {
+  int device = 0;
+  ptrom::Tree t;
+  ~ptrom_tree() {
+    cudaSetDevice(device);
+    t.free_all();
+  }
+};
+
+using namespace ptrom;
+
+namespace {
+
+template <class F>
+int guarded(ptrom_ctx* ctx, F&& fn) {
+  if (!ctx) return PTROM_CONFIG_ERROR;
+  try {
+    cudaSetDevice(ctx->device);
+    fn();
+    ctx->err.clear();
+    return PTROM_OK;
+  } catch (const status_error& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return PTROM_CUDA_ERROR;
+  }
+}
+
+// ClusterCriterion factories (quadtree.hpp:195-202)
+void check_criterion(int kind, double value) {
+  if (kind == PTROM_CRIT_BARNES_HUT) {
+    if (!(value >= 0)) config_fail("opening ratio must be >= 0");
+  } else if (kind == PTROM_CRIT_NEIGHBOR) {
+    if (!(value >= 0)) config_fail("neighborhood width factor must be >= 0");
+  } else {
+    config_fail("unknown cluster criterion");
+  }
+}
+
+// kernel.hpp:84-103 (sys.validate + check_state) for the tree evaluators.
+void validate_eval(long long n, const double* x, const double* gamma, double delta, int form, const double* inflow,
+                   const char* who) {
+  if (n <= 0) config_fail("particle system is empty");
+  if (form != PTROM_FORM_STANDARD && form != PTROM_FORM_DENOMINATOR_SCALED) config_fail("unknown kernel form");
+  for (long long i = 0; i < n; ++i)
+    if (!std::isfinite(gamma[i])) config_fail("non-finite circulation");
+  if (!(delta >= 0)) config_fail("negative desingularization constant");
+  if (inflow)
+    for (long long i = 0; i < 2 * n; ++i)
+      if (!std::isfinite(inflow[i])) config_fail("non-finite inflow");
+  for (long long i = 0; i < 2 * n; ++i)
+    if (!std::isfinite(x[i])) config_fail(std::string(who) + ": non-finite state");
+}
+
+struct DevBuf {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  template <class T>
+  T* up(const T* h, size_t count) {
+    if (!h) return nullptr;
+    T* d;
+    PTROM_CUDA(cudaMallocAsync(&d, std::max<size_t>(count, 1) * sizeof(T), s));
+    ptrs.push_back(d);
+    PTROM_CUDA(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+  }
+  template <class T>
+  T* alloc(size_t count) {
+    T* d;
+    PTROM_CUDA(cudaMallocAsync(&d, std::max<size_t>(count, 1) * sizeof(T), s));
+    ptrs.push_back(d);
+    return d;
+  }
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int ptrom_dev_tree_build_f64(ptrom_ctx* ctx, int64_t n, const double* d_px, const double* d_py, const double* d_gamma,
+                             int64_t leaf_capacity, ptrom_tree** out) {
+  return guarded(ctx, [&] {
+    if (!out) config_fail("build_tree: null output");
+    auto* h = new ptrom_tree;
+    h->device = ctx->device;
+    try {
+      tree_build(ctx, h->t, n, d_px, d_py, d_gamma, leaf_capacity, ctx->tree_seq_max);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int ptrom_tree_build_f64(ptrom_ctx* ctx, int64_t n, const double* px, const double* py, const double* gamma,
+                         int64_t leaf_capacity, ptrom_tree** out) {
+  return guarded(ctx, [&] {
+    // quadtree.hpp:127-131 validation order
+    if (n <= 0) config_fail("build_tree: no points");
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(px[i]) || !std::isfinite(py[i]) || !std::isfinite(gamma[i]))
+        config_fail("build_tree: non-finite input");
+    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+    DevBuf b{ctx->stream};
+    const double* dx = b.up(px, n);
+    const double* dy = b.up(py, n);
+    const double* dg = b.up(gamma, n);
+    auto* h = new ptrom_tree;
+    h->device = ctx->device;
+    try {
+      tree_build(ctx, h->t, n, dx, dy, dg, leaf_capacity, ctx->tree_seq_max);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void ptrom_tree_free(ptrom_tree* tree) { delete tree; }
+
+int64_t ptrom_tree_num_nodes(const ptrom_tree* tree) { return tree ? (int64_t)tree->t.nodes.count : 0; }
+
+int ptrom_tree_export(ptrom_ctx* ctx, const ptrom_tree* tree, double* bounds, double* width, double* centroid,
+                      double* gamma_sum, int32_t* children, int64_t* begin, int64_t* end, int32_t* depth,
+                      uint8_t* centroid_fallback, int64_t* perm, int64_t* slot, int32_t* leaf_node) {
+  return guarded(ctx, [&] {
+    if (!tree) config_fail("null tree");
+    const Tree& t = tree->t;
+    const size_t nn = t.nodes.count, n = (size_t)t.n;
+    cudaStream_t s = ctx->stream;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) PTROM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    };
+    d2h(bounds, t.nodes.bounds, nn * 32);
+    d2h(width, t.nodes.width, nn * 8);
+    d2h(centroid, t.nodes.centroid, nn * 16);
+    d2h(gamma_sum, t.nodes.gamma_sum, nn * 8);
+    d2h(children, t.nodes.children, nn * 16);
+    d2h(depth, t.nodes.depth, nn * 4);
+    d2h(centroid_fallback, t.nodes.fallback, nn);
+    d2h(leaf_node, t.leaf_node, n * 4);
+    std::vector<int> tmp;
+    auto widen = [&](int64_t* dst, const int* src, size_t count) {
+      if (!dst) return;
+      tmp.resize(count);
+      PTROM_CUDA(cudaMemcpyAsync(tmp.data(), src, count * 4, cudaMemcpyDeviceToHost, s));
+      PTROM_CUDA(cudaStreamSynchronize(s));
+      for (size_t i = 0; i < count; ++i) dst[i] = tmp[i];
+    };
+    widen(begin, t.nodes.begin, nn);
+    widen(end, t.nodes.end, nn);
+    widen(perm, t.perm, n);
+    widen(slot, t.slot, n);
+    PTROM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int ptrom_collect_clusters(ptrom_ctx* ctx, ptrom_tree* tree, int crit_kind, double crit_value, int64_t n_targets,
+                           const int64_t* targets, int64_t* cluster_offsets, int32_t* clusters, int64_t clusters_cap,
+                           int64_t* direct_offsets, int64_t* direct, int64_t direct_cap) {
+  return guarded(ctx, [&] {
+    if (!tree) config_fail("null tree");
+    check_criterion(crit_kind, crit_value);
+    std::vector<long long> ids(targets, targets + n_targets);
+    for (long long t : ids)
+      if (t < 0 || t >= tree->t.n) config_fail("collect_clusters: bad target id");
+    std::vector<long long> c_off, d_off, dl;
+    std::vector<int> cl;
+    tree_collect(ctx, tree->t, crit_kind, crit_value, ids, c_off, cl, d_off, dl);
+    std::copy(c_off.begin(), c_off.end(), cluster_offsets);
+    std::copy(d_off.begin(), d_off.end(), direct_offsets);
+    if (clusters && clusters_cap >= (int64_t)cl.size()) std::copy(cl.begin(), cl.end(), clusters);
+    if (direct && direct_cap >= (int64_t)dl.size()) std::copy(dl.begin(), dl.end(), direct);
+  });
+}
+
+int ptrom_bh_velocity_f64(ptrom_ctx* ctx, ptrom_tree* tree, int64_t n, const double* x, const double* gamma,
+                          double delta, int form, int crit_kind, double crit_value, const double* inflow, double* f,
+                          uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    validate_eval(n, x, gamma, delta, form, inflow, "bh_velocity");
+    if (!tree || tree->t.n != n) config_fail("bh_velocity: tree size mismatch");
+    check_criterion(crit_kind, crit_value);
+    DevBuf b{ctx->stream};
+    const double* dx = b.up(x, 2 * n);
+    const double* dg = b.up(gamma, n);
+    const double* di = b.up(inflow, inflow ? 2 * n : 0);
+    double* df = b.alloc<double>(2 * n);
+    const unsigned long long pairs =
+        tree_eval(ctx, tree->t, dx, dg, delta, form, crit_kind, crit_value, di, df, nullptr, nullptr, nullptr, nullptr);
+    PTROM_CUDA(cudaMemcpyAsync(f, df, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+    if (n_pair_evals) *n_pair_evals = pairs;
+  });
+}
+
+int ptrom_bh_jacobian_f64(ptrom_ctx* ctx, ptrom_tree* tree, int64_t n, const double* x, const double* gamma,
+                          double delta, int form, int crit_kind, double crit_value, double* dfx_dx, double* dfx_dy,
+                          double* dfy_dx, double* dfy_dy) {
+  return guarded(ctx, [&] {
+    validate_eval(n, x, gamma, delta, form, nullptr, "bh_jacobian");
+    if (!tree || tree->t.n != n) config_fail("bh_jacobian: tree size mismatch");
+    check_criterion(crit_kind, crit_value);
+    DevBuf b{ctx->stream};
+    const double* dx = b.up(x, 2 * n);
+    const double* dg = b.up(gamma, n);
+    double* dj = b.alloc<double>(4 * n);
+    tree_eval(ctx, tree->t, dx, dg, delta, form, crit_kind, crit_value, nullptr, nullptr, dj, dj + n, dj + 2 * n,
+              dj + 3 * n);
+    double* outs[4] = {dfx_dx, dfx_dy, dfy_dx, dfy_dy};
+    for (int k = 0; k < 4; ++k)
+      PTROM_CUDA(cudaMemcpyAsync(outs[k], dj + k * n, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+  });
+}
+
+int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                      double delta, int form, int crit_kind, double crit_value, int64_t leaf_capacity,
+                                      const double* d_inflow, double* d_f, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    check_criterion(crit_kind, crit_value);
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    Tree t;
+    try {
+      tree_build(ctx, t, n, d_x, d_x + n, d_gamma, leaf_capacity, ctx->tree_seq_max);
+      const unsigned long long pairs = tree_eval(ctx, t, d_x, d_gamma, delta, form, crit_kind, crit_value, d_inflow,
+                                                 d_f, nullptr, nullptr, nullptr, nullptr);
+      if (n_pair_evals) *n_pair_evals = pairs;
+    } catch (...) {
+      t.free_all();
+      throw;
+    }
+    t.free_all();
+  });
+}
+
+int ptrom_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
+                                  int form, int crit_kind, double crit_value, int64_t leaf_capacity,
+                                  const double* inflow, double* f, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    validate_eval(n, x, gamma, delta, form, inflow, "bh_velocity");
+    check_criterion(crit_kind, crit_value);
+    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+    DevBuf b{ctx->stream};
+    const double* dx = b.up(x, 2 * n);
+    const double* dg = b.up(gamma, n);
+    const double* di = b.up(inflow, inflow ? 2 * n : 0);
+    double* df = b.alloc<double>(2 * n);
+    Tree t;
+    try {
+      tree_build(ctx, t, n, dx, dx + n, dg, leaf_capacity, ctx->tree_seq_max);
+      const unsigned long long pairs =
+          tree_eval(ctx, t, dx, dg, delta, form, crit_kind, crit_value, di, df, nullptr, nullptr, nullptr, nullptr);
+      if (n_pair_evals) *n_pair_evals = pairs;
+    } catch (...) {
+      t.free_all();
+      throw;
+    }
+    t.free_all();
+    PTROM_CUDA(cudaMemcpyAsync(f, df, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+  });
+}
+
+}  // extern "C"
