@@ -154,6 +154,13 @@ int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d
                                       int64_t leaf_capacity, const double* d_inflow, double* d_f,
                                       uint64_t* n_pair_evals);
 
+/* Statistics of the last tree build / evaluation on this context: device
+ * time of the build (T1+T2) and of the final traversal pass (T3), kernel
+ * interactions and prune tests of that pass, node count, and how many targets
+ * hit an uncertain (certified-then-resolved) prune test. */
+int ptrom_tree_stats(ptrom_ctx* ctx, double* build_ms, double* eval_ms, uint64_t* interactions,
+                     uint64_t* prune_tests, uint64_t* nodes, uint64_t* resolved_targets);
+
 /* --------------------------------------------------------- instrumentation -- */
 /* bench.py support: while enabled, the context records CUDA events on its own
  * stream around every launch of the dominant kernel of each call (the

@@ -84,6 +84,13 @@ struct Arena {
 
 }  // namespace ptrom
 
+namespace ptrom {
+struct TreeStats {  // last tree build / evaluation on this context (ptrom_tree_stats)
+  double build_ms = 0, eval_ms = 0;
+  unsigned long long interactions = 0, prune_tests = 0, nodes = 0, levels = 0, resolved_targets = 0;
+};
+}  // namespace ptrom
+
 struct ptrom_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -98,6 +105,7 @@ struct ptrom_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
+  ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)
 };
 

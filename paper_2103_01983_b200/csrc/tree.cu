@@ -46,11 +46,17 @@ namespace {
 constexpr int kMaxDepth = 64;  // quadtree.hpp:13
 constexpr int kThreads = 256;
 
+// All tree buffers come from the stream-ordered pool allocator (no
+// cudaMalloc/cudaFree device synchronizations inside a build).
+thread_local cudaStream_t g_alloc_stream = nullptr;
 template <class T>
 T* dalloc(size_t count) {
   T* p = nullptr;
-  if (count) PTROM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  if (count) PTROM_CUDA(cudaMallocAsync(&p, count * sizeof(T), g_alloc_stream));
   return p;
+}
+inline void dfree(void* p) {
+  if (p) cudaFreeAsync(p, g_alloc_stream);
 }
 
 int grid_for(ptrom_ctx* ctx, long long count, int tpb = kThreads) {
@@ -415,8 +421,7 @@ void TreeRecords::alloc(size_t cap_) {
 }
 void TreeRecords::free() {
   void* ps[] = {begin, end, depth, children, split, fallback, exact, bounds, mid, width, centroid, gamma_sum, cerr};
-  for (void* p : ps)
-    if (p) cudaFree(p);
+  for (void* p : ps) dfree(p);
   *this = TreeRecords{};
 }
 void TreeRecords::grow(size_t need, size_t used, cudaStream_t s) {
@@ -439,7 +444,6 @@ void TreeRecords::grow(size_t need, size_t used, cudaStream_t s) {
   cp(n.centroid, centroid, used * 16);
   cp(n.gamma_sum, gamma_sum, used * 8);
   cp(n.cerr, cerr, used * 8);
-  PTROM_CUDA(cudaStreamSynchronize(s));
   free();
   *this = n;
 }
@@ -464,16 +468,15 @@ void TreeNodes::alloc(size_t nn) {
 void TreeNodes::free() {
   void* ps[] = {bounds, width, centroid, gamma_sum, cerr, children, begin, end, depth, skip, fallback, exact, leaf,
                 need_exact};
-  for (void* p : ps)
-    if (p) cudaFree(p);
+  for (void* p : ps) dfree(p);
   *this = TreeNodes{};
 }
 
-void Tree::free_all() {
+void Tree::free_all(cudaStream_t s) {
+  g_alloc_stream = s;
   nodes.free();
   void* ps[] = {perm, slot, leaf_node, sx, sy, sg, px, py, g};
-  for (void* p : ps)
-    if (p) cudaFree(p);
+  for (void* p : ps) dfree(p);
   perm = slot = leaf_node = nullptr;
   sx = sy = sg = px = py = g = nullptr;
 }
@@ -485,7 +488,12 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   if (n >= (1LL << 30)) config_fail("build_tree: more than 2^30 points is not supported");
   if (leaf_cap < 1) config_fail("build_tree: leaf_capacity must be >= 1");
   cudaStream_t s = ctx->stream;
-  t.free_all();
+  g_alloc_stream = s;
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, s);
+  t.free_all(s);
   t.n = n;
   t.leaf_cap = leaf_cap;
   // keep the build inputs (exact-sum fallback and collect_clusters target positions)
@@ -504,7 +512,7 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   std::vector<double> hh(4 * hb);
   PTROM_CUDA(cudaMemcpyAsync(hh.data(), hull, hh.size() * 8, cudaMemcpyDeviceToHost, s));
   PTROM_CUDA(cudaStreamSynchronize(s));
-  cudaFree(hull);
+  dfree(hull);
   double x_lo = hh[0], x_hi = hh[1], y_lo = hh[2], y_hi = hh[3];
   for (int b = 1; b < hb; ++b) {
     x_lo = std::min(x_lo, hh[4 * b]);
@@ -568,8 +576,8 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   while (splitting) {
     // per-level buffers
     if ((size_t)L > lvl_cap) {
-      if (nchild) cudaFree(nchild);
-      if (child_off) cudaFree(child_off);
+      dfree(nchild);
+      dfree(child_off);
       lvl_cap = std::max<size_t>(L, lvl_cap * 2);
       nchild = dalloc<int>(lvl_cap);
       child_off = dalloc<int>(lvl_cap);
@@ -638,12 +646,20 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   particle_maps_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.perm, t.slot);
   leaf_node_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, t.nodes, t.perm, t.leaf_node);
   PTROM_LAUNCH_CHECK();
+  cudaEventRecord(ev1, s);
   PTROM_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  ctx->tree_stats = TreeStats{};
+  ctx->tree_stats.build_ms = ms;
+  ctx->tree_stats.nodes = R;
+  ctx->tree_stats.levels = 0;
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
 
   void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags, scan, digit, dcount, tmp, nchild, child_off, large_list,
                    keys, keys_s, vals, order, rec2id, stmp};
-  for (void* p : frees)
-    if (p) cudaFree(p);
+  for (void* p : frees) dfree(p);
   cudaFreeHost(h_counts);
   rec.free();
 }

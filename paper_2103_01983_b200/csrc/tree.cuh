@@ -49,7 +49,7 @@ struct Tree {
   int* leaf_node = nullptr;  // leaf id per particle
   double *sx = nullptr, *sy = nullptr, *sg = nullptr;  // build points / weights in perm order
   double *px = nullptr, *py = nullptr, *g = nullptr;   // build points / weights by particle id
-  void free_all();
+  void free_all(cudaStream_t s);  // stream-ordered release on s
 };
 
 }  // namespace ptrom

@@ -18,7 +18,8 @@ struct ptrom_tree {
   ptrom::Tree t;
   ~ptrom_tree() {
     cudaSetDevice(device);
-    t.free_all();
+    cudaDeviceSynchronize();  // the tree may have been used on any stream
+    t.free_all(nullptr);
   }
 };
 
@@ -140,6 +141,19 @@ int ptrom_tree_build_f64(ptrom_ctx* ctx, int64_t n, const double* px, const doub
 
 void ptrom_tree_free(ptrom_tree* tree) { delete tree; }
 
+int ptrom_tree_stats(ptrom_ctx* ctx, double* build_ms, double* eval_ms, uint64_t* interactions, uint64_t* prune_tests,
+                     uint64_t* nodes, uint64_t* resolved_targets) {
+  return guarded(ctx, [&] {
+    const TreeStats& st = ctx->tree_stats;
+    if (build_ms) *build_ms = st.build_ms;
+    if (eval_ms) *eval_ms = st.eval_ms;
+    if (interactions) *interactions = st.interactions;
+    if (prune_tests) *prune_tests = st.prune_tests;
+    if (nodes) *nodes = st.nodes;
+    if (resolved_targets) *resolved_targets = st.resolved_targets;
+  });
+}
+
 int64_t ptrom_tree_num_nodes(const ptrom_tree* tree) { return tree ? (int64_t)tree->t.nodes.count : 0; }
 
 int ptrom_tree_export(ptrom_ctx* ctx, const ptrom_tree* tree, double* bounds, double* width, double* centroid,
@@ -249,10 +263,10 @@ int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d
                                                  d_f, nullptr, nullptr, nullptr, nullptr);
       if (n_pair_evals) *n_pair_evals = pairs;
     } catch (...) {
-      t.free_all();
+      t.free_all(ctx->stream);
       throw;
     }
-    t.free_all();
+    t.free_all(ctx->stream);
   });
 }
 
@@ -275,10 +289,10 @@ int ptrom_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, co
           tree_eval(ctx, t, dx, dg, delta, form, crit_kind, crit_value, di, df, nullptr, nullptr, nullptr, nullptr);
       if (n_pair_evals) *n_pair_evals = pairs;
     } catch (...) {
-      t.free_all();
+      t.free_all(ctx->stream);
       throw;
     }
-    t.free_all();
+    t.free_all(ctx->stream);
     PTROM_CUDA(cudaMemcpyAsync(f, df, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
     check_device_status(ctx);
   });
