@@ -45,7 +45,7 @@ static bool approx(double a, double b, double eps) {
   // doctest::Approx(b).epsilon(eps): |a-b| < eps * (scale + max(|a|,|b|)), scale 1
   return std::abs(a - b) < eps * (1.0 + std::max(std::abs(a), std::abs(b)));
 }
-static double vnorm(const Vec& v) {
+static double l2(const Vec& v) {
   double s = 0;
   for (double e : v) s += e * e;
   return std::sqrt(s);
@@ -70,10 +70,11 @@ struct Reg {
 };
 #define CAT2(a, b) a##b
 #define CAT(a, b) CAT2(a, b)
-#define TEST_CASE(name) \
-  static void CAT(tc_, __LINE__)(); \
-  static Reg CAT(reg_, __LINE__)(name, CAT(tc_, __LINE__)); \
-  static void CAT(tc_, __LINE__)()
+#define TEST_CASE_I(name, id) \
+  static void CAT(tc_, id)(); \
+  static Reg CAT(reg_, id)(name, CAT(tc_, id)); \
+  static void CAT(tc_, id)()
+#define TEST_CASE(name) TEST_CASE_I(name, __COUNTER__)
 
 // ------------------------------------------------------------ kernel ------
 // test_kernel.cpp:15-31
@@ -185,7 +186,7 @@ TEST_CASE("test_kernel.cpp:141 pairwise_velocity zero circulation returns inflow
   sys.has_inflow = true;
   sys.inflow = {1, 2, 3, 4, 5, 6};
   Vec x = {0, 1, 2, 0, 1, 2};
-  CHECK(vnorm(vsub(pairwise_velocity<double>(x, sys), sys.inflow)) == 0.0);
+  CHECK(l2(vsub(pairwise_velocity<double>(x, sys), sys.inflow)) == 0.0);
 }
 
 TEST_CASE("test_kernel.cpp:153 pairwise_velocity matches independent re-summation") {
@@ -200,7 +201,7 @@ TEST_CASE("test_kernel.cpp:153 pairwise_velocity matches independent re-summatio
     }
     const Vec f = pairwise_velocity<double>(x, sys);
     const Vec ref = brute_velocity(x, sys.circulation, sys.delta, sys.has_inflow ? &sys.inflow : nullptr);
-    CHECK(vnorm(vsub(f, ref)) <= 1e-14 * std::max(1.0, vnorm(ref)));
+    CHECK(l2(vsub(f, ref)) <= 1e-14 * std::max(1.0, l2(ref)));
   }
 }
 
@@ -212,7 +213,7 @@ TEST_CASE("test_kernel.cpp:170 pairwise_velocity equals explicit block-matrix pr
     const Vec x = random_state(rng, n);
     const Vec f = pairwise_velocity<double>(x, sys);
     const Vec ref = block_matrix_velocity(x, sys.circulation, sys.delta);
-    CHECK(vnorm(vsub(f, ref)) <= 1e-13 * std::max(1.0, vnorm(ref)));
+    CHECK(l2(vsub(f, ref)) <= 1e-13 * std::max(1.0, l2(ref)));
   }
 }
 
@@ -317,7 +318,7 @@ TEST_CASE("acceptance.cpp:123 criterion 1 pairwise vs block matrix (1e-13)") {
     sys.delta = 0.05;
     const Vec lib = pairwise_velocity<double>(x0, sys);
     const Vec blk = block_matrix_velocity(x0, sys.circulation, sys.delta);
-    worst = std::max(worst, vnorm(vsub(lib, blk)) / vnorm(blk));
+    worst = std::max(worst, l2(vsub(lib, blk)) / l2(blk));
   }
   CHECK(worst <= 1e-13);
 }
@@ -752,8 +753,8 @@ TEST_CASE("test_quadtree.cpp:334 moderate opening ratio stays close to the exact
   const Vec naive = pairwise_velocity<double>(state, sys);
   const auto tree = build_tree<double>(px, py, sys.circulation, 8);
   const Vec approx_v = bh_velocity<double>(tree, state, sys, ClusterCriterion<double>::barnes_hut(0.5));
-  CHECK(vnorm(vsub(approx_v, naive)) / vnorm(naive) < 1e-2);
-  CHECK(vnorm(vsub(approx_v, naive)) > 0.0);
+  CHECK(l2(vsub(approx_v, naive)) / l2(naive) < 1e-2);
+  CHECK(l2(vsub(approx_v, naive)) > 0.0);
 }
 
 TEST_CASE("test_quadtree.cpp:351 inflow is added after the tree summation") {
