@@ -161,6 +161,62 @@ int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d
 int ptrom_tree_stats(ptrom_ctx* ctx, double* build_ms, double* eval_ms, uint64_t* interactions,
                      uint64_t* prune_tests, uint64_t* nodes, uint64_t* resolved_targets);
 
+/* ----------------------------------------------------------- PTROM online -- */
+/* PODBasis (reduction.hpp:18-26): phi is n_dofs x modes column-major. */
+typedef struct ptrom_basis ptrom_basis;
+int ptrom_basis_create(ptrom_ctx* ctx, int64_t n_dofs, int64_t modes, const double* phi,
+                       const double* singular_values /* nullable */, const double* x_ref, ptrom_basis** out);
+void ptrom_basis_free(ptrom_basis* basis);
+/* GnatOperator (reduction.hpp:173-180): sorted sample ids and A = pinv(P Φ_r)
+ * (m_r x 2 n_samples, column-major); gathers Φ̄, x̄⁰ like GnatSolver's
+ * constructor (rom.hpp:264-290). m_r <= 32, modes <= 32. */
+typedef struct ptrom_gnat_op ptrom_gnat_op;
+int ptrom_gnat_op_create(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_samples, const int64_t* sample_ids,
+                         int64_t m_r, const double* A, ptrom_gnat_op** out);
+void ptrom_gnat_op_free(ptrom_gnat_op* op);
+/* SurrogateSourceBasis (reduction.hpp:280-302) in CSR form: cluster tables
+ * (phi_tilde 2N_c x M column-major, gamma_tilde, x0_tilde, zero_gamma,
+ * membership CSR of ascending ids), per-target cluster list CSR, near-field
+ * union (direct_ids, direct_phi 2U x M, direct_x0, direct_gamma) and the
+ * per-target local direct list CSR. */
+typedef struct ptrom_surrogate ptrom_surrogate;
+int ptrom_surrogate_create(ptrom_ctx* ctx, int64_t modes, int64_t n_clusters, const double* phi_tilde,
+                           const double* gamma_tilde, const double* x0_tilde, const uint8_t* zero_gamma,
+                           const int64_t* membership_offsets, const int64_t* membership_ids, int64_t n_targets,
+                           const int64_t* target_ids, const int64_t* cluster_offsets, const int64_t* cluster_list,
+                           int64_t n_direct, const int64_t* direct_ids, const double* direct_phi,
+                           const double* direct_x0, const double* direct_gamma, const int64_t* direct_offsets,
+                           const int64_t* direct_list, ptrom_surrogate** out);
+void ptrom_surrogate_free(ptrom_surrogate* sur);
+int ptrom_surrogate_export(ptrom_ctx* ctx, const ptrom_surrogate* sur, double* phi_tilde, double* gamma_tilde,
+                           double* x0_tilde, uint8_t* zero_gamma, double* direct_gamma);
+/* reduction.hpp:400-431 reassign_cluster_circulation (in place). */
+int ptrom_reassign_cluster_circulation_f64(ptrom_ctx* ctx, ptrom_surrogate* sur, int64_t n, const double* gamma,
+                                           const ptrom_basis* basis);
+/* rom.hpp:101-155 hyperpair: f (2 n_t), jac (4 x n_t rows dfx_dx, dfx_dy,
+ * dfy_dx, dfy_dy), cluster / direct positions (nullable). inflow is the full
+ * 2n vector (added at the target ids) or NULL. */
+int ptrom_hyperpair_f64(ptrom_ctx* ctx, const ptrom_surrogate* sur, const double* target_positions,
+                        const double* x_hat, double delta, int form, int64_t n, const double* inflow, double* f,
+                        double* jac, double* cluster_positions, double* direct_positions, uint64_t* n_pair_evals);
+/* rom.hpp:404-412 ptrom_simulate: reassigns the surrogate to gamma (in
+ * place, like the reference) and runs GnatSolver::simulate on the device.
+ * x_hat is M x n_steps column-major; iterations / converged per step. */
+int ptrom_ptrom_simulate_f64(ptrom_ctx* ctx, const ptrom_basis* basis, const ptrom_gnat_op* op, ptrom_surrogate* sur,
+                             int64_t n, const double* gamma, double delta, int form, const double* inflow, double dt,
+                             int64_t n_steps, double tol, int max_iters, double step_length, double* x_hat,
+                             int* iterations, uint8_t* converged, uint64_t* n_pair_evals);
+/* Batched online queries: n_inst instances of an affine
+ * circulation Γ(μ) = gamma_a + μ gamma_b (the surrogate is not modified),
+ * processed `batch` instances at a time (0 = default). x_hat is
+ * [n_inst][n_steps][M], iterations / converged [n_inst][n_steps]. */
+int ptrom_ptrom_simulate_batch_f64(ptrom_ctx* ctx, const ptrom_basis* basis, const ptrom_gnat_op* op,
+                                   const ptrom_surrogate* sur, int64_t n, const double* gamma_a,
+                                   const double* gamma_b, int64_t n_inst, const double* mu, int64_t batch,
+                                   double delta, int form, const double* inflow, double dt, int64_t n_steps,
+                                   double tol, int max_iters, double step_length, double* x_hat, int* iterations,
+                                   uint8_t* converged, uint64_t* n_pair_evals);
+
 /* --------------------------------------------------------- instrumentation -- */
 /* bench.py support: while enabled, the context records CUDA events on its own
  * stream around every launch of the dominant kernel of each call (the

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ptrom_oracle.hpp"
+#include "ptrom_oracle_rom.hpp"
 #include "ptrom_oracle_tree.hpp"
 
 #ifdef _OPENMP
@@ -341,6 +342,164 @@ int oracle_bh_jacobian_f64(const oracle_tree* h, std::int64_t n, const double* x
     std::memcpy(jxy, jac.dfx_dy.data(), sizeof(double) * n);
     std::memcpy(jyx, jac.dfy_dx.data(), sizeof(double) * n);
     std::memcpy(jyy, jac.dfy_dy.data(), sizeof(double) * n);
+  });
+}
+
+// ----------------------------------------------------------------- rom ----
+static Mat mat_from(Index rows, Index cols, const double* p) {
+  Mat m(rows, cols);
+  std::copy(p, p + rows * cols, m.a.begin());
+  return m;
+}
+
+// reduction.hpp:93-168
+int oracle_greedy_sample(std::int64_t n_dofs, std::int64_t n_r, const double* phi_r, std::int64_t n_target,
+                         std::int64_t n_preseed, const std::int64_t* preseed, std::int64_t* out) {
+  return guarded([&] {
+    std::vector<Index> pre(preseed, preseed + n_preseed);
+    const auto ids = greedy_sample(mat_from(n_dofs, n_r, phi_r), n_target, pre);
+    std::copy(ids.begin(), ids.end(), out);
+  });
+}
+
+// reduction.hpp:182-220 (A is m_r x 2 n_s, column-major)
+int oracle_build_gnat_operator(std::int64_t n_dofs, std::int64_t m_r, const double* phi_r, std::int64_t n_s,
+                               const std::int64_t* ids, double* A) {
+  return guarded([&] {
+    const auto op = build_gnat_operator(mat_from(n_dofs, m_r, phi_r), std::vector<Index>(ids, ids + n_s));
+    std::copy(op.A.a.begin(), op.A.a.end(), A);
+  });
+}
+
+struct oracle_surrogate {
+  SurrogateSourceBasis s;
+  PODBasis basis;
+};
+
+static PODBasis basis_from(std::int64_t n_dofs, std::int64_t m, const double* phi, const double* sv,
+                           const double* x_ref) {
+  PODBasis b;
+  b.phi = mat_from(n_dofs, m, phi);
+  b.singular_values.assign(sv, sv + m);
+  b.x_ref.assign(x_ref, x_ref + n_dofs);
+  return b;
+}
+
+// build_weighted_pod_tree (reduction.hpp:236-274) + cluster_pod (304-385)
+int oracle_surrogate_build(std::int64_t n, std::int64_t m, const double* phi, const double* sv, const double* x_ref,
+                           const double* gamma, std::int64_t leaf_cap, int crit_kind, double crit_value,
+                           std::int64_t n_t, const std::int64_t* targets, oracle_surrogate** out) {
+  return guarded([&] {
+    auto* h = new oracle_surrogate;
+    try {
+      h->basis = basis_from(2 * n, m, phi, sv, x_ref);
+      const auto crit = crit_kind ? ClusterCriterion<double>::neighbor(crit_value)
+                                  : ClusterCriterion<double>::barnes_hut(crit_value);
+      h->s = cluster_pod(h->basis, Vec(gamma, gamma + n), std::vector<Index>(targets, targets + n_t), crit, leaf_cap);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+void oracle_surrogate_free(oracle_surrogate* h) { delete h; }
+
+// sizes: [n_c, u, n_membership, n_cluster_list, n_direct_list, n_t]
+void oracle_surrogate_sizes(const oracle_surrogate* h, std::int64_t* sz) {
+  const auto& s = h->s;
+  sz[0] = s.num_clusters();
+  sz[1] = s.num_direct();
+  std::int64_t a = 0, b = 0, c = 0;
+  for (const auto& v : s.cluster_membership) a += static_cast<std::int64_t>(v.size());
+  for (const auto& v : s.per_target_clusters) b += static_cast<std::int64_t>(v.size());
+  for (const auto& v : s.per_target_direct) c += static_cast<std::int64_t>(v.size());
+  sz[2] = a;
+  sz[3] = b;
+  sz[4] = c;
+  sz[5] = static_cast<std::int64_t>(s.target_ids.size());
+}
+
+static void csr(const std::vector<std::vector<Index>>& v, std::int64_t* off, std::int64_t* ids) {
+  off[0] = 0;
+  for (size_t i = 0; i < v.size(); ++i) {
+    off[i + 1] = off[i] + static_cast<std::int64_t>(v[i].size());
+    std::copy(v[i].begin(), v[i].end(), ids + off[i]);
+  }
+}
+
+void oracle_surrogate_export(const oracle_surrogate* h, double* phi_tilde, double* gamma_tilde, double* x0_tilde,
+                             std::uint8_t* zero_gamma, std::int64_t* mem_off, std::int64_t* mem_ids,
+                             std::int32_t* cluster_node_ids, std::int64_t* cl_off, std::int64_t* cl_list,
+                             std::int64_t* direct_ids, double* direct_phi, double* direct_x0, double* direct_gamma,
+                             std::int64_t* d_off, std::int64_t* d_list) {
+  const auto& s = h->s;
+  std::copy(s.phi_tilde.a.begin(), s.phi_tilde.a.end(), phi_tilde);
+  std::copy(s.gamma_tilde.begin(), s.gamma_tilde.end(), gamma_tilde);
+  std::copy(s.x0_tilde.begin(), s.x0_tilde.end(), x0_tilde);
+  for (size_t c = 0; c < s.zero_gamma.size(); ++c) zero_gamma[c] = static_cast<std::uint8_t>(s.zero_gamma[c]);
+  csr(s.cluster_membership, mem_off, mem_ids);
+  std::copy(s.cluster_node_ids.begin(), s.cluster_node_ids.end(), cluster_node_ids);
+  csr(s.per_target_clusters, cl_off, cl_list);
+  std::copy(s.direct_ids.begin(), s.direct_ids.end(), direct_ids);
+  std::copy(s.direct_phi.a.begin(), s.direct_phi.a.end(), direct_phi);
+  std::copy(s.direct_x0.begin(), s.direct_x0.end(), direct_x0);
+  std::copy(s.direct_gamma.begin(), s.direct_gamma.end(), direct_gamma);
+  csr(s.per_target_direct, d_off, d_list);
+}
+
+// reduction.hpp:400-431
+int oracle_surrogate_reassign(oracle_surrogate* h, std::int64_t n, const double* gamma) {
+  return guarded([&] { reassign_cluster_circulation(h->s, Vec(gamma, gamma + n), h->basis); });
+}
+
+// rom.hpp:101-155 (jac: 4 x n_t, rows dfx_dx, dfx_dy, dfy_dx, dfy_dy)
+int oracle_hyperpair(const oracle_surrogate* h, std::int64_t n, const double* gamma, double delta, int form,
+                     const double* inflow, const double* target_positions, const double* x_hat, double* f,
+                     double* jac, double* cpos, double* dpos) {
+  return guarded([&] {
+    const auto sys = make_sys<double>(n, gamma, delta, form, inflow);
+    const Index nt = static_cast<Index>(h->s.target_ids.size());
+    const auto hp = hyperpair(h->s, Vec(target_positions, target_positions + 2 * nt),
+                              Vec(x_hat, x_hat + h->basis.modes()), sys);
+    std::copy(hp.f.begin(), hp.f.end(), f);
+    std::copy(hp.jac.dfx_dx.begin(), hp.jac.dfx_dx.end(), jac);
+    std::copy(hp.jac.dfx_dy.begin(), hp.jac.dfx_dy.end(), jac + nt);
+    std::copy(hp.jac.dfy_dx.begin(), hp.jac.dfy_dx.end(), jac + 2 * nt);
+    std::copy(hp.jac.dfy_dy.begin(), hp.jac.dfy_dy.end(), jac + 3 * nt);
+    if (cpos) std::copy(hp.cluster_positions.begin(), hp.cluster_positions.end(), cpos);
+    if (dpos) std::copy(hp.direct_positions.begin(), hp.direct_positions.end(), dpos);
+  });
+}
+
+// rom.hpp:404-412 ptrom_simulate (surrogate mutated by the reassignment);
+// with h == NULL the gappy GnatSolver baseline (rom.hpp:358-385) runs instead.
+int oracle_ptrom_simulate(oracle_surrogate* h, std::int64_t n, std::int64_t m, const double* phi, const double* sv,
+                          const double* x_ref, std::int64_t n_s, const std::int64_t* sample_ids, std::int64_t m_r,
+                          const double* A, const double* gamma, double delta, int form, const double* inflow,
+                          double dt, std::int64_t n_steps, double tol, int max_iters, double step_length,
+                          double* x_hat, int* iters, std::uint8_t* conv) {
+  return guarded([&] {
+    const auto sys = make_sys<double>(n, gamma, delta, form, inflow);
+    GnatOperator op;
+    op.sample_ids.assign(sample_ids, sample_ids + n_s);
+    for (Index k = 0; k < n_s; ++k) op.sampled_dofs.push_back(sample_ids[k]);
+    for (Index k = 0; k < n_s; ++k) op.sampled_dofs.push_back(sample_ids[k] + n);
+    op.A = mat_from(m_r, 2 * n_s, A);
+    RomConfig cfg{tol, max_iters, step_length};
+    RomTrajectory tr;
+    if (h) {
+      tr = ptrom_simulate(h->basis, op, h->s, sys, dt, n_steps, cfg);
+    } else {
+      const PODBasis b = basis_from(2 * n, m, phi, sv, x_ref);
+      GnatSolver solver(b, op, sys, dt, cfg);
+      tr = solver.simulate(n_steps);
+    }
+    std::copy(tr.x_hat.a.begin(), tr.x_hat.a.end(), x_hat);
+    for (Index s = 0; s < n_steps; ++s) {
+      iters[s] = tr.iterations[s];
+      conv[s] = static_cast<std::uint8_t>(tr.converged[s]);
+    }
   });
 }
 

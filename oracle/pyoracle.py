@@ -169,3 +169,125 @@ class Tree:
             lib().oracle_tree_free(self.h)
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ rom ----
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _fortran(m):
+    """Column-major float64 buffer of a 2-D array (Eigen layout)."""
+    return np.asfortranarray(np.asarray(m, dtype=np.float64))
+
+
+def greedy_sample(phi_r, n_target, preseed=()):
+    """reduction.hpp:93-168 → sorted sample ids."""
+    pr = _fortran(phi_r)
+    pre = _i64(list(preseed))
+    out = np.zeros(n_target, np.int64)
+    _check(lib().oracle_greedy_sample(C.c_int64(pr.shape[0]), C.c_int64(pr.shape[1]), _p(pr), C.c_int64(n_target),
+                                      C.c_int64(pre.shape[0]), _p(pre), _p(out)))
+    return out
+
+
+def build_gnat_operator(phi_r, sample_ids):
+    """reduction.hpp:182-220 → A (m_r x 2 n_s)."""
+    pr = _fortran(phi_r)
+    ids = _i64(sample_ids)
+    A = np.zeros((pr.shape[1], 2 * ids.shape[0]), order="F")
+    _check(lib().oracle_build_gnat_operator(C.c_int64(pr.shape[0]), C.c_int64(pr.shape[1]), _p(pr),
+                                            C.c_int64(ids.shape[0]), _p(ids), _p(A)))
+    return A
+
+
+class Surrogate:
+    """build_weighted_pod_tree + cluster_pod (reduction.hpp:236-385)."""
+
+    def __init__(self, phi, sv, x_ref, gamma, targets, crit_kind=1, crit_value=1.0, leaf_capacity=1):
+        self.phi, self.sv, self.x_ref = _fortran(phi), _f64(sv), _f64(x_ref)
+        self.gamma = _f64(gamma)
+        self.n = self.gamma.shape[0]
+        self.m = self.phi.shape[1]
+        t = _i64(targets)
+        h = C.c_void_p()
+        _check(lib().oracle_surrogate_build(C.c_int64(self.n), C.c_int64(self.m), _p(self.phi), _p(self.sv),
+                                            _p(self.x_ref), _p(self.gamma), C.c_int64(leaf_capacity),
+                                            C.c_int(crit_kind), C.c_double(crit_value), C.c_int64(t.shape[0]),
+                                            _p(t), C.byref(h)))
+        self.h = h
+        self.targets = t
+        self.refresh()
+
+    def refresh(self):
+        sz = np.zeros(6, np.int64)
+        lib().oracle_surrogate_sizes(self.h, _p(sz))
+        nc, u, nmem, ncl, nd, nt = (int(v) for v in sz)
+        m = self.m
+        self.n_clusters, self.n_direct = nc, u
+        self.phi_tilde = np.zeros((2 * nc, m), order="F")
+        self.gamma_tilde = np.zeros(nc)
+        self.x0_tilde = np.zeros(2 * nc)
+        self.zero_gamma = np.zeros(nc, np.uint8)
+        self.mem_off = np.zeros(nc + 1, np.int64)
+        self.mem_ids = np.zeros(max(nmem, 1), np.int64)
+        self.cluster_node_ids = np.zeros(nc, np.int32)
+        self.cl_off = np.zeros(nt + 1, np.int64)
+        self.cl_list = np.zeros(max(ncl, 1), np.int64)
+        self.direct_ids = np.zeros(u, np.int64)
+        self.direct_phi = np.zeros((2 * u, m), order="F")
+        self.direct_x0 = np.zeros(2 * u)
+        self.direct_gamma = np.zeros(u)
+        self.d_off = np.zeros(nt + 1, np.int64)
+        self.d_list = np.zeros(max(nd, 1), np.int64)
+        lib().oracle_surrogate_export(self.h, *(_p(a) for a in (
+            self.phi_tilde, self.gamma_tilde, self.x0_tilde, self.zero_gamma, self.mem_off, self.mem_ids,
+            self.cluster_node_ids, self.cl_off, self.cl_list, self.direct_ids, self.direct_phi, self.direct_x0,
+            self.direct_gamma, self.d_off, self.d_list)))
+        self.mem_ids = self.mem_ids[:nmem]
+        self.cl_list = self.cl_list[:ncl]
+        self.d_list = self.d_list[:nd]
+
+    def reassign(self, gamma):
+        g = _f64(gamma)
+        _check(lib().oracle_surrogate_reassign(self.h, C.c_int64(g.shape[0]), _p(g)))
+        self.refresh()
+
+    def hyperpair(self, target_positions, x_hat, gamma, delta, form=0, inflow=None):
+        nt = self.targets.shape[0]
+        tp, xh, g, inf = _f64(target_positions), _f64(x_hat), _f64(gamma), _f64(inflow)
+        f = np.zeros(2 * nt)
+        jac = np.zeros((4, nt))
+        cpos = np.zeros(2 * self.n_clusters)
+        dpos = np.zeros(2 * self.n_direct)
+        _check(lib().oracle_hyperpair(self.h, C.c_int64(g.shape[0]), _p(g), C.c_double(delta), C.c_int(form),
+                                      _p(inf), _p(tp), _p(xh), _p(f), _p(jac), _p(cpos), _p(dpos)))
+        return f, jac, cpos, dpos
+
+    def __del__(self):
+        try:
+            lib().oracle_surrogate_free(self.h)
+        except Exception:
+            pass
+
+
+def ptrom_simulate(surrogate, phi, sv, x_ref, sample_ids, A, gamma, delta, dt, n_steps, tol=1e-4, max_iters=100,
+                   step_length=1.0, form=0, inflow=None):
+    """rom.hpp:404-412 (surrogate=None: the gappy GnatSolver baseline)."""
+    phi_f, sv_, xr = _fortran(phi), _f64(sv), _f64(x_ref)
+    ids = _i64(sample_ids)
+    A_ = _fortran(A)
+    g, inf = _f64(gamma), _f64(inflow)
+    m = phi_f.shape[1]
+    x_hat = np.zeros((m, n_steps), order="F")
+    iters = np.zeros(n_steps, np.int32)
+    conv = np.zeros(n_steps, np.uint8)
+    _check(lib().oracle_ptrom_simulate(surrogate.h if surrogate is not None else None, C.c_int64(g.shape[0]),
+                                       C.c_int64(m), _p(phi_f), _p(sv_), _p(xr), C.c_int64(ids.shape[0]), _p(ids),
+                                       C.c_int64(A_.shape[0]), _p(A_), _p(g), C.c_double(delta), C.c_int(form),
+                                       _p(inf), C.c_double(dt), C.c_int64(n_steps), C.c_double(tol),
+                                       C.c_int(max_iters), C.c_double(step_length), _p(x_hat), _p(iters),
+                                       _p(conv)))
+    if surrogate is not None:
+        surrogate.refresh()
+    return x_hat, iters, conv

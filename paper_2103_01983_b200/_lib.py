@@ -63,6 +63,23 @@ PROTOTYPES = {
                                                     C.c_double, c_i64, c_dp, c_dp, c_u64p]),
     "ptrom_tree_stats": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_double), c_u64p, c_u64p, c_u64p,
                                    c_u64p]),
+    "ptrom_basis_create": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_dp, c_dp, C.POINTER(C.c_void_p)]),
+    "ptrom_basis_free": (None, [C.c_void_p]),
+    "ptrom_gnat_op_create": (C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_i64, c_dp, C.POINTER(C.c_void_p)]),
+    "ptrom_gnat_op_free": (None, [C.c_void_p]),
+    "ptrom_surrogate_create": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp, c_i64, c_dp, c_dp,
+                                         c_dp, c_i64, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp, C.POINTER(C.c_void_p)]),
+    "ptrom_surrogate_free": (None, [C.c_void_p]),
+    "ptrom_surrogate_export": (C.c_int, [c_ctxp, C.c_void_p, c_dp, c_dp, c_dp, c_dp, c_dp]),
+    "ptrom_reassign_cluster_circulation_f64": (C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, C.c_void_p]),
+    "ptrom_hyperpair_f64": (C.c_int, [c_ctxp, C.c_void_p, c_dp, c_dp, C.c_double, C.c_int, c_i64, c_dp, c_dp, c_dp,
+                                      c_dp, c_dp, c_u64p]),
+    "ptrom_ptrom_simulate_f64": (C.c_int, [c_ctxp, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_dp, C.c_double,
+                                           C.c_int, c_dp, C.c_double, c_i64, C.c_double, C.c_int, C.c_double, c_dp,
+                                           c_dp, c_dp, c_u64p]),
+    "ptrom_ptrom_simulate_batch_f64": (C.c_int, [c_ctxp, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_dp, c_dp, c_i64,
+                                                 c_dp, c_i64, C.c_double, C.c_int, c_dp, C.c_double, c_i64,
+                                                 C.c_double, C.c_int, C.c_double, c_dp, c_dp, c_dp, c_u64p]),
     "ptrom_profile_begin": (C.c_int, [c_ctxp]),
     "ptrom_profile_end": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

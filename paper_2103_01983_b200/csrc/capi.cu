@@ -23,6 +23,9 @@ void check_device_status(ptrom_ctx* ctx) {
   switch (st.kind) {
     case kStatusSingularBlock:  // integrators.hpp:187-189
       numerical_fail("singular Newton block for particle " + std::to_string(st.index));
+    case kStatusZeroClusterCirculation:
+      numerical_fail("affine circulation batch: cluster " + std::to_string(st.index) +
+                     " has zero net circulation for some mu (use the per-instance ptrom_simulate)");
     case kStatusNonFiniteJacobian:  // kernel.hpp:55-56 / 64-65
       numerical_fail("kernel_pair_jacobian: coincident target/source with zero desingularization (target " +
                      std::to_string(st.index) + ")");

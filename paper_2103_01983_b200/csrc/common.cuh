@@ -44,6 +44,7 @@ enum : int {
   kStatusNonFiniteVelocity = 1,  // coincident pair with zero desingularization
   kStatusSingularBlock = 2,      // integrators.hpp:187-189
   kStatusNonFiniteJacobian = 3,
+  kStatusZeroClusterCirculation = 4,  // affine batch: G_A + mu G_B == 0
 };
 struct DeviceStatus {
   int kind;

@@ -1,0 +1,749 @@
+// rom.cu — PTROM online path on sm_100a, batched over parameter instances.
+//
+// Replaces, for B instances at once:
+//   reassign_cluster_circulation  reduction.hpp:400-431
+//   hyperpair                     rom.hpp:101-155
+//   apply_residual_jacobian       rom.hpp:71-84
+//   GnatSolver::simulate          rom.hpp:292-340 (Gauss–Newton on the sampled residual)
+//   ptrom_simulate                rom.hpp:404-412
+//
+// Per Gauss–Newton evaluation of instance b:
+//   1. source positions: clusters c (x̃⁰ + Φ̃x̂, Γ̃), direct sources (x⁰_d + Φ_d x̂, Γ_d), sampled
+//      targets x̄ = x̄⁰ + Φ̄x̂ (positions_* kernels; instance-minor layout [source][b] so a warp of
+//      32 instances reads one cluster's 32 positions coalesced).
+//   2. hyperpair: one thread per (target, instance), cluster list then direct list, fused
+//      velocity + self-Jacobian (the reference's two calls kernel.hpp:29-73 per source).
+//   3. gn_eval: one CTA per instance streams the 2n_t sampled rows once: residual r̄, C = (I − h J)Φ̄
+//      formed in registers, A·C on the FP64 tensor cores (mma.sync m8n8k4 DMMA; tcgen05 has no
+//      fp64 kind), A·r̄ and Cᵀr̄ on the FP64 pipe, fixed-order cross-warp reduction, then the
+//      reference's convergence logic on ‖Cᵀr̄‖.
+//   4. qr_update: one warp per instance solves min‖AC·Δ + A r̄‖ by column-pivoted Householder QR
+//      (lane i owns row i of the 32 x 16 system) and applies x̂ += αΔ.
+//
+// Cluster tables: the batch engine evaluates Φ̃(μ) = (S_A + μ S_B)/(G_A + μ G_B) with per-cluster
+// member sums of an affine circulation Γ(μ) = Γ_a + μ Γ_b (mathematically the reference's
+// Σ_p (Γ_p/ΣΓ) Φ_p) so no per-instance table is materialised. The
+// single-instance drop-in (ptrom_ptrom_simulate_f64) instead reassigns exactly like the
+// reference (sequential member order, w_p = Γ_p / Σ Γ) and runs the same engine with B = 1.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ops.cuh"
+#include "rom.cuh"
+
+namespace ptrom {
+
+namespace {
+
+constexpr int kGnThreads = 256;  // 8 warps per instance in gn_eval
+
+__device__ __forceinline__ double rcp64(double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  double e = fma(-q, y, 1.0);
+  e = fma(e, e, e);
+  return fma(y, e, y);
+}
+
+// ---------------------------------------------------- table preparation ---
+// reduction.hpp:407-428 for one (cluster, column) pair: column j < m is
+// the Φ̃ mode j, j == m is x̃⁰; sequential member order as the reference.
+__global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __restrict__ gamma) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int cols = s.m + 1;
+  if (idx >= s.n_c * cols) return;
+  const long long c = idx / cols;
+  const int j = (int)(idx % cols);
+  const long long b0 = s.mem_off[c], b1 = s.mem_off[c + 1];
+  double gsum = 0.0;
+  for (long long k = b0; k < b1; ++k) gsum = __dadd_rn(gsum, gamma[s.mem_ids[k]]);
+  const bool fb = gsum == 0.0;
+  const double inv_count = __ddiv_rn(1.0, (double)(b1 - b0));
+  double ax = 0.0, ay = 0.0;
+  for (long long k = b0; k < b1; ++k) {
+    const long long p = s.mem_ids[k];
+    const double w = fb ? inv_count : __ddiv_rn(gamma[p], gsum);
+    const double vx = j < s.m ? b.phi[p + (long long)j * 2 * b.n] : b.x_ref[p];
+    const double vy = j < s.m ? b.phi[p + b.n + (long long)j * 2 * b.n] : b.x_ref[p + b.n];
+    ax = __dadd_rn(ax, __dmul_rn(w, vx));
+    ay = __dadd_rn(ay, __dmul_rn(w, vy));
+  }
+  if (j < s.m) {
+    s.phi_tilde[c + (long long)j * 2 * s.n_c] = ax;
+    s.phi_tilde[c + s.n_c + (long long)j * 2 * s.n_c] = ay;
+  } else {
+    s.x0_tilde[c] = ax;
+    s.x0_tilde[c + s.n_c] = ay;
+    s.gamma_tilde[c] = gsum;
+    s.zero_gamma[c] = fb ? 1 : 0;
+  }
+}
+
+__global__ void direct_gamma_kernel(DSurrogate s, const double* __restrict__ gamma) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k < s.u) s.direct_gamma[k] = gamma[s.direct_ids[k]];
+}
+
+// Affine member sums for Γ(μ) = Γa + μΓb: S_A, S_B (Φ rows), X_A, X_B
+// (x_ref), G_A, G_B per cluster.
+__global__ void affine_tables_kernel(DSurrogate s, DBasis b, const double* __restrict__ ga,
+                                     const double* __restrict__ gb, AffineTables t) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int cols = s.m + 1;
+  if (idx >= s.n_c * cols) return;
+  const long long c = idx / cols;
+  const int j = (int)(idx % cols);
+  double sax = 0, say = 0, sbx = 0, sby = 0, ga_s = 0, gb_s = 0;
+  for (long long k = s.mem_off[c]; k < s.mem_off[c + 1]; ++k) {
+    const long long p = s.mem_ids[k];
+    const double vx = j < s.m ? b.phi[p + (long long)j * 2 * b.n] : b.x_ref[p];
+    const double vy = j < s.m ? b.phi[p + b.n + (long long)j * 2 * b.n] : b.x_ref[p + b.n];
+    sax = fma(ga[p], vx, sax);
+    say = fma(ga[p], vy, say);
+    sbx = fma(gb[p], vx, sbx);
+    sby = fma(gb[p], vy, sby);
+    ga_s += ga[p];
+    gb_s += gb[p];
+  }
+  if (j < s.m) {
+    t.pa[c + (long long)j * 2 * s.n_c] = sax;
+    t.pa[c + s.n_c + (long long)j * 2 * s.n_c] = say;
+    t.pb[c + (long long)j * 2 * s.n_c] = sbx;
+    t.pb[c + s.n_c + (long long)j * 2 * s.n_c] = sby;
+  } else {
+    t.xa[c] = sax;
+    t.xa[c + s.n_c] = say;
+    t.xb[c] = sbx;
+    t.xb[c + s.n_c] = sby;
+    t.ga[c] = ga_s;
+    t.gb[c] = gb_s;
+  }
+}
+
+// ------------------------------------------------------------ positions ---
+// Clusters: exact mode cpos = x̃⁰ + Φ̃ x̂ (rom.hpp:113); affine mode
+// cpos = (X_A + S_A x̂ + μ (X_B + S_B x̂)) / (G_A + μ G_B).
+template <bool AFFINE>
+__global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, int xs, const double* __restrict__ xhat,
+                                          const double* __restrict__ mu, const unsigned char* __restrict__ active,
+                                          double* __restrict__ cx, double* __restrict__ cy, double* __restrict__ cg,
+                                          DeviceStatus* st) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= s.n_c * B) return;
+  const long long c = idx / B;
+  const int b = (int)(idx % B);
+  if (active && !active[b]) return;
+  const double* xh = xhat + (long long)b * xs;
+  const long long ld = 2 * s.n_c;
+  if (!AFFINE) {
+    double ax = 0.0, ay = 0.0;
+    for (int j = 0; j < s.m; ++j) {
+      ax = fma(s.phi_tilde[c + j * ld], xh[j], ax);
+      ay = fma(s.phi_tilde[c + s.n_c + j * ld], xh[j], ay);
+    }
+    cx[idx] = s.x0_tilde[c] + ax;
+    cy[idx] = s.x0_tilde[c + s.n_c] + ay;
+    cg[idx] = s.gamma_tilde[c];
+  } else {
+    double ax = t.xa[c], ay = t.xa[c + s.n_c], bx = t.xb[c], by = t.xb[c + s.n_c];
+    for (int j = 0; j < s.m; ++j) {
+      const double x = xh[j];
+      ax = fma(t.pa[c + j * ld], x, ax);
+      ay = fma(t.pa[c + s.n_c + j * ld], x, ay);
+      bx = fma(t.pb[c + j * ld], x, bx);
+      by = fma(t.pb[c + s.n_c + j * ld], x, by);
+    }
+    const double m = mu[b];
+    const double g = t.ga[c] + m * t.gb[c];
+    if (g == 0.0) latch_status(st, kStatusZeroClusterCirculation, c);
+    const double ig = 1.0 / g;
+    cx[idx] = fma(m, bx, ax) * ig;
+    cy[idx] = fma(m, by, ay) * ig;
+    cg[idx] = g;
+  }
+}
+
+// Direct sources: x⁰_d + Φ_d x̂ (rom.hpp:114), Γ_d(μ).
+template <bool AFFINE>
+__global__ void positions_direct_kernel(DSurrogate s, AffineTables t, int B, int xs, const double* __restrict__ xhat,
+                                        const double* __restrict__ mu, const unsigned char* __restrict__ active,
+                                        double* __restrict__ dx, double* __restrict__ dy, double* __restrict__ dg) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= s.u * B) return;
+  const long long k = idx / B;
+  const int b = (int)(idx % B);
+  if (active && !active[b]) return;
+  const double* xh = xhat + (long long)b * xs;
+  const long long ld = 2 * s.u;
+  double ax = 0.0, ay = 0.0;
+  for (int j = 0; j < s.m; ++j) {
+    ax = fma(s.direct_phi[k + j * ld], xh[j], ax);
+    ay = fma(s.direct_phi[k + s.u + j * ld], xh[j], ay);
+  }
+  dx[idx] = s.direct_x0[k] + ax;
+  dy[idx] = s.direct_x0[k + s.u] + ay;
+  dg[idx] = AFFINE ? t.dga[k] + mu[b] * t.dgb[k] : s.direct_gamma[k];
+}
+
+// Sampled targets x̄ = x̄⁰ + Φ̄ x̂ (rom.hpp:306, 329); instance-major [b][row].
+__global__ void positions_targets_kernel(DGnat g, int B, const double* __restrict__ xhat,
+                                         const unsigned char* __restrict__ active, double* __restrict__ xbar) {
+  const long long rows = 2 * g.n_s;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= rows * B) return;
+  const int b = (int)(idx / rows);
+  const long long r = idx % rows;
+  if (active && !active[b]) return;
+  const double* xh = xhat + (long long)b * g.mp;
+  double a = 0.0;
+  for (int j = 0; j < g.m; ++j) a = fma(g.phi_bar[r + j * rows], xh[j], a);
+  xbar[idx] = g.x0_bar[r] + a;
+}
+
+// ------------------------------------------------------------- hyperpair ---
+// rom.hpp:118-153 for (target t, instance b): clusters (skipping a centroid
+// exactly on its target when delta == 0, rom.hpp:129), then direct sources
+// (skipping the target's own id, rom.hpp:136), fused velocity + Jacobian,
+// inflow at the target id. f: [b][2n_t], jac: [b][n_t][4].
+__global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, int B, const double* __restrict__ xbar,
+                                                        const double* __restrict__ cx, const double* __restrict__ cy,
+                                                        const double* __restrict__ cg, const double* __restrict__ dx,
+                                                        const double* __restrict__ dy, const double* __restrict__ dg,
+                                                        double dp, double delta, const double* __restrict__ inflow,
+                                                        long long n, const unsigned char* __restrict__ active,
+                                                        double* __restrict__ f, double* __restrict__ jac,
+                                                        unsigned long long* __restrict__ pairs, DeviceStatus* st) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nt = s.n_t;
+  unsigned long long cnt = 0;
+  if (idx < nt * B) {
+    const long long t = idx / B;
+    const int b = (int)(idx % B);
+    if (!active || active[b]) {
+      const double px = xbar[(long long)b * 2 * nt + t], py = xbar[(long long)b * 2 * nt + nt + t];
+      const double inv2pi = 1.0 / (2.0 * M_PI);
+      double fx = 0, fy = 0, ja = 0, jb = 0, jc = 0;
+      auto add = [&](double sx, double sy, double gam) {
+        const double rx = px - sx, ry = py - sy;
+        const double q = fma(rx, rx, fma(ry, ry, dp));
+        const double u = rcp64(q);
+        const double sv = gam * inv2pi * u;
+        fx = fma(-ry, sv, fx);
+        fy = fma(rx, sv, fy);
+        const double w = sv * u;
+        ja = fma(w * rx, ry, ja);
+        jb = fma(w, fma(ry, ry, -(rx * rx)), jb);
+        jc += w;
+        ++cnt;
+      };
+      for (long long k = s.cl_off[t]; k < s.cl_off[t + 1]; ++k) {
+        const long long c = (long long)s.cl_list[k] * B + b;
+        const double sx = cx[c], sy = cy[c];
+        if (delta == 0.0 && sx == px && sy == py) continue;
+        add(sx, sy, cg[c]);
+      }
+      const long long pid = s.target_ids[t];
+      for (long long k = s.d_off[t]; k < s.d_off[t + 1]; ++k) {
+        const long long loc = s.d_list[k];
+        if (s.direct_ids[loc] == pid) continue;
+        const long long d = loc * B + b;
+        add(dx[d], dy[d], dg[d]);
+      }
+      if (inflow) {
+        fx = fx + inflow[pid];
+        fy = fy + inflow[pid + n];
+      }
+      const double j00 = 2.0 * ja, j01 = jb - dp * jc, j10 = jb + dp * jc;
+      if (!isfinite(fx) || !isfinite(fy) || !isfinite(j00) || !isfinite(j01) || !isfinite(j10))
+        latch_status(st, kStatusNonFiniteVelocity, pid);
+      f[(long long)b * 2 * nt + t] = fx;
+      f[(long long)b * 2 * nt + nt + t] = fy;
+      double* jj = jac + ((long long)b * nt + t) * 4;
+      jj[0] = j00;
+      jj[1] = j01;
+      jj[2] = j10;
+      jj[3] = -j00;
+    }
+  }
+  using WR = cub::WarpReduce<unsigned long long>;
+  __shared__ typename WR::TempStorage wt[4];
+  const unsigned long long sum = WR(wt[threadIdx.x / 32]).Sum(cnt);
+  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(pairs, sum);
+}
+
+// -------------------------------------------------------------- gn_eval ---
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// One CTA per instance. Streams rows k of the sampled residual in steps of 4
+// (the DMMA k-extent); each warp owns every 8th step. MR = 32 residual modes
+// (4 row tiles of A), M = 16 modes (2 column tiles of C).
+template <int MR, int M>
+__global__ void __launch_bounds__(kGnThreads) gn_eval_kernel(DGnat g, int B, double h, const double* __restrict__ xbar,
+                                                             const double* __restrict__ xprev,
+                                                             const double* __restrict__ fbar,
+                                                             const double* __restrict__ fprev,
+                                                             const double* __restrict__ jac, GnState st_, int first) {
+  static_assert(MR % 8 == 0 && M % 8 == 0, "DMMA tiles");
+  constexpr int TI = MR / 8, TN = M / 8;
+  const int b = blockIdx.x;
+  if (!st_.active[b]) return;
+  const long long nt = g.n_s, rows = 2 * nt;
+  const double* xb = xbar + (long long)b * rows;
+  const double* xp = xprev + (long long)b * rows;
+  const double* fb = fbar + (long long)b * rows;
+  const double* fp = fprev + (long long)b * rows;
+  const double* jb = jac + (long long)b * nt * 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;  // fragment row / column
+  // the update is needed unless this evaluation is the last one allowed
+  const bool need_ac = !(st_.evals[b] + 1 - 1 >= st_.max_iters);
+  double acc[TI][TN][2];
+  double ar[TI];
+  double gr[TN];
+#pragma unroll
+  for (int i = 0; i < TI; ++i) {
+    ar[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) gr[j] = 0.0;
+
+  for (long long k0 = 4LL * warp; k0 < rows; k0 += 4LL * (kGnThreads / 32)) {
+    const long long r = k0 + lc;  // this thread's residual row
+    double rv = 0.0;
+    double cv[TN];
+    if (r < rows) {
+      // rom.hpp:310 residual, integrators.hpp:47-53 evaluation order
+      rv = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
+      const long long t = r < nt ? r : r - nt;
+      const double* J = jb + 4 * t;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int m = j * 8 + lr;
+        const double px = g.phi_bar[t + m * rows], py = g.phi_bar[t + nt + m * rows];
+        // rom.hpp:79-81: row - h*(J_r0 * row_x + J_r1 * row_y)
+        const double own = r < nt ? px : py;
+        const double inner = r < nt ? __dadd_rn(__dmul_rn(J[0], px), __dmul_rn(J[1], py))
+                                    : __dadd_rn(__dmul_rn(J[2], px), __dmul_rn(J[3], py));
+        cv[j] = __dsub_rn(own, __dmul_rn(h, inner));
+        gr[j] = fma(cv[j], rv, gr[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) cv[j] = 0.0;
+    }
+    double av[TI];
+#pragma unroll
+    for (int i = 0; i < TI; ++i) {
+      const long long ka = k0 + lc;
+      av[i] = ka < rows ? g.A[(i * 8 + lr) + ka * MR] : 0.0;
+      ar[i] = fma(av[i], rv, ar[i]);
+    }
+    if (need_ac) {
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j], av[i], cv[j]);
+    }
+  }
+  // ---- fixed-order reductions: over lc (lanes of a row group), then a
+  // pairwise tree over the 8 warps (4+4, 2+2, 1+1) through shared memory.
+  constexpr int NW = kGnThreads / 32;
+  __shared__ double red_ac[NW / 2][MR * M];
+  __shared__ double red_ar[NW][MR];
+  __shared__ double red_gr[NW][M];
+#pragma unroll
+  for (int i = 0; i < TI; ++i) {
+    double v = ar[i];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (lc == 0) red_ar[warp][i * 8 + lr] = v;
+  }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    double v = gr[j];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (lc == 0) red_gr[warp][j * 8 + lr] = v;
+  }
+  for (int half = NW / 2; half >= 1; half >>= 1) {
+    if (warp >= half && warp < 2 * half) {
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const int row = i * 8 + lr, col = j * 8 + lc * 2;
+          red_ac[warp - half][row + col * MR] = acc[i][j][0];
+          red_ac[warp - half][row + (col + 1) * MR] = acc[i][j][1];
+        }
+    }
+    __syncthreads();
+    if (warp < half) {
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const int row = i * 8 + lr, col = j * 8 + lc * 2;
+          acc[i][j][0] += red_ac[warp][row + col * MR];
+          acc[i][j][1] += red_ac[warp][row + (col + 1) * MR];
+        }
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int row = i * 8 + lr, col = j * 8 + lc * 2;
+        st_.ac[(long long)b * MR * M + row + col * MR] = acc[i][j][0];
+        st_.ac[(long long)b * MR * M + row + (col + 1) * MR] = acc[i][j][1];
+      }
+  }
+  if (threadIdx.x < MR) {
+    double v = 0.0;
+    for (int w = 0; w < NW; ++w) v += red_ar[w][threadIdx.x];
+    st_.ar[(long long)b * MR + threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ss = 0.0;
+    for (int m = 0; m < M; ++m) {
+      double v = 0.0;
+      for (int w = 0; w < NW; ++w) v += red_gr[w][m];
+      ss += v * v;
+    }
+    const double gn = sqrt(ss);
+    // rom.hpp:309-324
+    const int evals = ++st_.evals[b];
+    bool done = false, conv = false;
+    if (evals == 1) {
+      st_.g0[b] = gn;
+      if (gn == 0.0) done = conv = true;
+    } else if (gn / st_.g0[b] <= st_.tol) {
+      done = conv = true;
+    }
+    if (!done && evals - 1 >= st_.max_iters) done = true;
+    st_.converged[b] = conv ? 1 : 0;
+    if (done) st_.active[b] = 0;
+    else atomicAdd(st_.n_active, 1);
+  }
+}
+
+// --------------------------------------------------------------- update ---
+// rom.hpp:325-329: Δ = argmin ‖(A C) Δ + A r̄‖ (ColPivHouseholderQR), x̂ += αΔ.
+// One warp per instance; lane i owns row i of the MR x M system.
+template <int MR, int M>
+__global__ void qr_update_kernel(int B, GnState st_, double alpha, double* __restrict__ xhat) {
+  const int b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B || !st_.active[b]) return;
+  static_assert(MR == 32, "one lane per residual mode (padded)");
+  double a[M];
+  const double* ac = st_.ac + (long long)b * MR * M;
+#pragma unroll
+  for (int j = 0; j < M; ++j) a[j] = ac[lane + j * MR];
+  double rhs = -st_.ar[(long long)b * MR + lane];
+  int perm[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) perm[j] = j;
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  double rdiag[M];
+  int rank = 0;
+  double maxpiv = 0.0;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    // pivot: largest remaining column norm (rows >= j)
+    int best = j;
+    double bestn = -1.0;
+#pragma unroll
+    for (int c = j; c < M; ++c) {
+      const double nc = wsum(lane >= j ? a[c] * a[c] : 0.0);
+      if (nc > bestn) {
+        bestn = nc;
+        best = c;
+      }
+    }
+#pragma unroll
+    for (int c = j + 1; c < M; ++c)
+      if (c == best) {
+        const double t = a[j];
+        a[j] = a[c];
+        a[c] = t;
+        const int tp = perm[j];
+        perm[j] = perm[c];
+        perm[c] = tp;
+      }
+    // Householder on column j, rows >= j (Eigen's makeHouseholder convention)
+    const double x0 = __shfl_sync(0xffffffffu, a[j], j);
+    const double tail = wsum(lane > j ? a[j] * a[j] : 0.0);
+    double beta = x0, tau = 0.0, denom = 1.0;
+    if (tail > 2.2250738585072014e-308) {
+      beta = sqrt(x0 * x0 + tail);
+      if (x0 >= 0) beta = -beta;
+      tau = (beta - x0) / beta;
+      denom = x0 - beta;
+    }
+    const double v = lane == j ? 1.0 : (lane > j ? a[j] / denom : 0.0);
+    // apply H = I - tau v v^T to the remaining columns and the rhs
+#pragma unroll
+    for (int c = j + 1; c < M; ++c) {
+      const double w = tau * wsum(v * a[c]);
+      a[c] -= w * v;
+    }
+    rhs -= tau * wsum(v * rhs) * v;
+    rdiag[j] = beta;
+    if (j == 0) maxpiv = fabs(beta);
+    if (fabs(beta) > 2.220446049250313e-16 * M * maxpiv) rank = j + 1;
+    if (lane == j) a[j] = beta;
+    else if (lane > j) a[j] = 0.0;
+  }
+  // back substitution on the leading rank rows (lane i holds row i of R)
+  double z[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) z[j] = 0.0;
+  for (int i = rank - 1; i >= 0; --i) {
+    double s = __shfl_sync(0xffffffffu, rhs, i);
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+      if (j > i && j < rank) s -= __shfl_sync(0xffffffffu, a[j], i) * z[j];
+    z[i] = s / rdiag[i];
+  }
+  if (lane == 0) {
+    double* xh = xhat + (long long)b * M;
+#pragma unroll
+    for (int j = 0; j < M; ++j) xh[perm[j]] += alpha * z[j];
+  }
+}
+
+__global__ void record_step_kernel(int B, int M, int MP, long long step, long long n_steps,
+                                   const double* __restrict__ xhat, GnState st_, double* __restrict__ xhat_out,
+                                   int* __restrict__ iters, unsigned char* __restrict__ conv) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  for (int j = 0; j < M; ++j) xhat_out[((long long)b * n_steps + step) * M + j] = xhat[(long long)b * MP + j];
+  iters[(long long)b * n_steps + step] = st_.evals[b];
+  conv[(long long)b * n_steps + step] = st_.converged[b];
+}
+
+__global__ void reset_step_kernel(int B, GnState st_) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  st_.evals[b] = 0;
+  st_.active[b] = 1;
+  st_.converged[b] = 0;
+}
+
+int blocks_for(long long count, int tpb) { return (int)std::max(1LL, (count + tpb - 1) / tpb); }
+
+}  // namespace
+
+// ------------------------------------------------------------- drivers ---
+void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma) {
+  const long long work = s.n_c * (s.m + 1);
+  if (work > 0) reassign_exact_kernel<<<blocks_for(work, 128), 128, 0, ctx->stream>>>(s, b, d_gamma);
+  if (s.u > 0) direct_gamma_kernel<<<blocks_for(s.u, 256), 256, 0, ctx->stream>>>(s, d_gamma);
+  PTROM_LAUNCH_CHECK();
+}
+
+void rom_affine_tables(ptrom_ctx* ctx, const DSurrogate& s, const DBasis& b, const double* d_ga, const double* d_gb,
+                       AffineTables& t) {
+  const long long work = s.n_c * (s.m + 1);
+  if (work > 0) affine_tables_kernel<<<blocks_for(work, 128), 128, 0, ctx->stream>>>(s, b, d_ga, d_gb, t);
+  PTROM_LAUNCH_CHECK();
+}
+
+// Positions + hyperpair for B instances (active mask may be null).
+unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t, int B,
+                                 int xs, const double* d_xhat, const double* d_mu, const unsigned char* d_active,
+                                 const double* d_xbar_in, double* d_xbar_out, double delta, int form,
+                                 const double* d_inflow, long long n, RomScratch& w, double* d_f, double* d_jac,
+                                 bool count_pairs) {
+  cudaStream_t st = ctx->stream;
+  AffineTables empty{};
+  const AffineTables& tt = t ? *t : empty;
+  if (s.n_c > 0) {
+    if (t)
+      positions_clusters_kernel<true><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
+                                                                                 w.cx, w.cy, w.cg, ctx->d_status);
+    else
+      positions_clusters_kernel<false><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
+                                                                                  w.cx, w.cy, w.cg, ctx->d_status);
+  }
+  if (s.u > 0) {
+    if (t)
+      positions_direct_kernel<true><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active, w.dx,
+                                                                            w.dy, w.dg);
+    else
+      positions_direct_kernel<false><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
+                                                                             w.dx, w.dy, w.dg);
+  }
+  const double* xbar = d_xbar_in;
+  if (g) {
+    positions_targets_kernel<<<blocks_for(2 * g->n_s * B, 256), 256, 0, st>>>(*g, B, d_xhat, d_active, d_xbar_out);
+    xbar = d_xbar_out;
+  }
+  PTROM_LAUNCH_CHECK();
+  if (count_pairs) PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
+  {
+    ProfScope prof(ctx);
+    hyperpair_kernel<<<blocks_for(s.n_t * B, 128), 128, 0, st>>>(s, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy, w.dg,
+                                                                 effective_delta(delta, form), delta, d_inflow, n,
+                                                                 d_active, d_f, d_jac, w.pairs, ctx->d_status);
+  }
+  PTROM_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  if (count_pairs) {
+    PTROM_CUDA(cudaMemcpyAsync(&h, w.pairs, 8, cudaMemcpyDeviceToHost, st));
+    PTROM_CUDA(cudaStreamSynchronize(st));
+  }
+  return h;
+}
+
+void RomScratch::ensure(const DSurrogate& s, long long nt, int B) {
+  const size_t need_c = (size_t)std::max<long long>(1, s.n_c) * B, need_d = (size_t)std::max<long long>(1, s.u) * B;
+  if (need_c > cap_c) {
+    cudaFree(cx);
+    cudaFree(cy);
+    cudaFree(cg);
+    PTROM_CUDA(cudaMalloc(&cx, need_c * 8));
+    PTROM_CUDA(cudaMalloc(&cy, need_c * 8));
+    PTROM_CUDA(cudaMalloc(&cg, need_c * 8));
+    cap_c = need_c;
+  }
+  if (need_d > cap_d) {
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dg);
+    PTROM_CUDA(cudaMalloc(&dx, need_d * 8));
+    PTROM_CUDA(cudaMalloc(&dy, need_d * 8));
+    PTROM_CUDA(cudaMalloc(&dg, need_d * 8));
+    cap_d = need_d;
+  }
+  if (!pairs) PTROM_CUDA(cudaMalloc(&pairs, 16));
+  (void)nt;
+}
+void RomScratch::release() {
+  void* ps[] = {cx, cy, cg, dx, dy, dg, pairs};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  *this = RomScratch{};
+}
+
+// GnatSolver::simulate (rom.hpp:292-340) for B instances in lock step.
+// Outputs: xhat_out [B][n_steps][M], iters/conv [B][n_steps].
+template <int MP>
+unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DGnat& g, const AffineTables* t, int B,
+                                   const double* d_mu, double delta, int form, const double* d_inflow, long long n,
+                                   double dt, long long n_steps, double tol, int max_iters, double alpha,
+                                   double* d_xhat_out, int* d_iters, unsigned char* d_conv) {
+  cudaStream_t st = ctx->stream;
+  const long long nt = g.n_s, rows = 2 * nt;
+  RomScratch w;
+  w.ensure(s, nt, B);
+  struct Bufs {
+    std::vector<void*> p;
+    cudaStream_t s;
+    RomScratch* w;
+    ~Bufs() {
+      for (void* q : p) cudaFreeAsync(q, s);
+      cudaStreamSynchronize(s);
+      w->release();
+    }
+  } bufs{{}, st, &w};
+  auto alloc = [&](size_t bytes) {
+    void* q;
+    PTROM_CUDA(cudaMallocAsync(&q, std::max<size_t>(bytes, 8), st));
+    bufs.p.push_back(q);
+    return q;
+  };
+  double* xhat = (double*)alloc((size_t)B * MP * 8);
+  double* xbar = (double*)alloc((size_t)B * rows * 8);
+  double* xprev = (double*)alloc((size_t)B * rows * 8);
+  double* fbar = (double*)alloc((size_t)B * rows * 8);
+  double* fprev = (double*)alloc((size_t)B * rows * 8);
+  double* jac = (double*)alloc((size_t)B * nt * 4 * 8);
+  GnState gs;
+  gs.ac = (double*)alloc((size_t)B * 32 * MP * 8);
+  gs.ar = (double*)alloc((size_t)B * 32 * 8);
+  gs.g0 = (double*)alloc((size_t)B * 8);
+  gs.evals = (int*)alloc((size_t)B * 4);
+  gs.active = (unsigned char*)alloc(B);
+  gs.converged = (unsigned char*)alloc(B);
+  gs.n_active = (int*)alloc(4);
+  gs.tol = tol;
+  gs.max_iters = max_iters;
+  int* h_active = nullptr;
+  PTROM_CUDA(cudaMallocHost(&h_active, 4));
+  PTROM_CUDA(cudaMemsetAsync(xhat, 0, (size_t)B * MP * 8, st));
+  PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
+  const double h = dt / 2.0;
+  // rom.hpp:298-300: x̄_prev = x̄⁰, f̄_prev = hyperpair(x̄⁰, 0); jac scratch is overwritten below
+  rom_hyperpair(ctx, s, &g, t, B, MP, xhat, d_mu, nullptr, nullptr, xprev, delta, form, d_inflow, n, w, fprev, jac,
+                false);
+  for (long long step = 0; step < n_steps; ++step) {
+    reset_step_kernel<<<blocks_for(B, 256), 256, 0, st>>>(B, gs);
+    // x̄ = x̄⁰ + Φ̄ x̂; (f̄, J) = hyperpair(x̄, x̂)   (rom.hpp:306-307)
+    rom_hyperpair(ctx, s, &g, t, B, MP, xhat, d_mu, nullptr, nullptr, xbar, delta, form, d_inflow, n, w, fbar, jac,
+                  false);
+    while (true) {
+      PTROM_CUDA(cudaMemsetAsync(gs.n_active, 0, 4, st));
+      gn_eval_kernel<32, MP><<<B, kGnThreads, 0, st>>>(g, B, h, xbar, xprev, fbar, fprev, jac, gs, 0);
+      PTROM_LAUNCH_CHECK();
+      PTROM_CUDA(cudaMemcpyAsync(h_active, gs.n_active, 4, cudaMemcpyDeviceToHost, st));
+      PTROM_CUDA(cudaStreamSynchronize(st));
+      if (*h_active == 0) break;
+      qr_update_kernel<32, MP><<<blocks_for(B, 4), 128, 0, st>>>(B, gs, alpha, xhat);
+      PTROM_LAUNCH_CHECK();
+      rom_hyperpair(ctx, s, &g, t, B, MP, xhat, d_mu, gs.active, nullptr, xbar, delta, form, d_inflow, n, w, fbar,
+                    jac, false);
+    }
+    record_step_kernel<<<blocks_for(B, 128), 128, 0, st>>>(B, g.m, MP, step, n_steps, xhat, gs, d_xhat_out, d_iters,
+                                                            d_conv);
+    PTROM_LAUNCH_CHECK();
+    // rom.hpp:336-337: history <- accepted state
+    std::swap(xprev, xbar);
+    std::swap(fprev, fbar);
+  }
+  unsigned long long pairs = 0;
+  PTROM_CUDA(cudaMemcpyAsync(&pairs, w.pairs, 8, cudaMemcpyDeviceToHost, st));
+  PTROM_CUDA(cudaStreamSynchronize(st));
+  cudaFreeHost(h_active);
+  check_device_status(ctx);
+  return pairs;
+}
+
+unsigned long long rom_gnat_simulate(ptrom_ctx* ctx, const DSurrogate& s, const DGnat& g, const AffineTables* t,
+                                     int B, const double* d_mu, double delta, int form, const double* d_inflow,
+                                     long long n, double dt, long long n_steps, double tol, int max_iters,
+                                     double alpha, double* d_xhat_out, int* d_iters, unsigned char* d_conv) {
+  if (g.m_r > 32 || g.m > 32) config_fail("ptrom online engine supports at most 32 modes and 32 residual modes");
+  switch (g.mp) {
+    case 8:
+      return gnat_simulate_t<8>(ctx, s, g, t, B, d_mu, delta, form, d_inflow, n, dt, n_steps, tol, max_iters, alpha,
+                                d_xhat_out, d_iters, d_conv);
+    case 16:
+      return gnat_simulate_t<16>(ctx, s, g, t, B, d_mu, delta, form, d_inflow, n, dt, n_steps, tol, max_iters, alpha,
+                                 d_xhat_out, d_iters, d_conv);
+    case 24:
+      return gnat_simulate_t<24>(ctx, s, g, t, B, d_mu, delta, form, d_inflow, n, dt, n_steps, tol, max_iters, alpha,
+                                 d_xhat_out, d_iters, d_conv);
+    default:
+      return gnat_simulate_t<32>(ctx, s, g, t, B, d_mu, delta, form, d_inflow, n, dt, n_steps, tol, max_iters, alpha,
+                                 d_xhat_out, d_iters, d_conv);
+  }
+}
+
+}  // namespace ptrom

@@ -1,0 +1,416 @@
+// rom_capi.cu — C ABI for the PTROM online path (include/ptrom_b200.h "ptrom").
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "ops.cuh"
+#include "rom.cuh"
+
+namespace ptrom {
+void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma);
+void rom_affine_tables(ptrom_ctx* ctx, const DSurrogate& s, const DBasis& b, const double* d_ga, const double* d_gb,
+                       AffineTables& t);
+unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t, int B,
+                                 int xs, const double* d_xhat, const double* d_mu, const unsigned char* d_active,
+                                 const double* d_xbar_in, double* d_xbar_out, double delta, int form,
+                                 const double* d_inflow, long long n, RomScratch& w, double* d_f, double* d_jac,
+                                 bool count_pairs);
+unsigned long long rom_gnat_simulate(ptrom_ctx* ctx, const DSurrogate& s, const DGnat& g, const AffineTables* t,
+                                     int B, const double* d_mu, double delta, int form, const double* d_inflow,
+                                     long long n, double dt, long long n_steps, double tol, int max_iters,
+                                     double alpha, double* d_xhat_out, int* d_iters, unsigned char* d_conv);
+}  // namespace ptrom
+
+using namespace ptrom;
+
+namespace {
+
+struct DevAllocs {
+  std::vector<void*> p;
+  ~DevAllocs() {
+    for (void* q : p) cudaFree(q);
+  }
+  template <class T>
+  T* up(const T* h, size_t count) {
+    T* d = nullptr;
+    PTROM_CUDA(cudaMalloc(&d, std::max<size_t>(count, 1) * sizeof(T)));
+    p.push_back(d);
+    if (h && count) PTROM_CUDA(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  template <class T>
+  T* zeros(size_t count) {
+    T* d = up<T>(nullptr, count);
+    PTROM_CUDA(cudaMemset(d, 0, std::max<size_t>(count, 1) * sizeof(T)));
+    return d;
+  }
+};
+
+template <class F>
+int guarded(ptrom_ctx* ctx, F&& fn) {
+  if (!ctx) return PTROM_CONFIG_ERROR;
+  try {
+    cudaSetDevice(ctx->device);
+    fn();
+    ctx->err.clear();
+    return PTROM_OK;
+  } catch (const status_error& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return PTROM_CUDA_ERROR;
+  }
+}
+
+void check_finite(const double* v, size_t count, const char* what) {
+  for (size_t i = 0; i < count; ++i)
+    if (!std::isfinite(v[i])) config_fail(std::string(what) + ": non-finite input");
+}
+
+}  // namespace
+
+struct ptrom_basis {
+  int device = 0;
+  DBasis b;
+  DevAllocs mem;
+};
+struct ptrom_gnat_op {
+  int device = 0;
+  DGnat g;
+  std::vector<long long> ids;
+  DevAllocs mem;
+};
+struct ptrom_surrogate {
+  int device = 0;
+  DSurrogate s;
+  std::vector<long long> target_ids;
+  DevAllocs mem;
+};
+
+extern "C" {
+
+int ptrom_basis_create(ptrom_ctx* ctx, int64_t n_dofs, int64_t modes, const double* phi, const double* singular_values,
+                       const double* x_ref, ptrom_basis** out) {
+  return guarded(ctx, [&] {
+    if (n_dofs <= 0 || n_dofs % 2 != 0) config_fail("state dimension must be even");
+    if (modes < 1) config_fail("basis needs at least one mode");
+    check_finite(phi, (size_t)(n_dofs * modes), "basis");
+    check_finite(x_ref, (size_t)n_dofs, "basis reference state");
+    auto* h = new ptrom_basis;
+    h->device = ctx->device;
+    try {
+      h->b.n = n_dofs / 2;
+      h->b.m = (int)modes;
+      h->b.phi = h->mem.up(phi, (size_t)(n_dofs * modes));
+      h->b.x_ref = h->mem.up(x_ref, (size_t)n_dofs);
+      h->b.sv = h->mem.up(singular_values, singular_values ? (size_t)modes : 0);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+void ptrom_basis_free(ptrom_basis* b) {
+  if (b) {
+    cudaSetDevice(b->device);
+    delete b;
+  }
+}
+
+int ptrom_gnat_op_create(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_samples, const int64_t* sample_ids,
+                         int64_t m_r, const double* A, ptrom_gnat_op** out) {
+  return guarded(ctx, [&] {
+    if (!basis) config_fail("null basis");
+    const DBasis& b = basis->b;
+    if (n_samples < 1) config_fail("build_gnat_operator: no sample ids");
+    std::vector<long long> ids(sample_ids, sample_ids + n_samples);
+    if (!std::is_sorted(ids.begin(), ids.end()) || std::adjacent_find(ids.begin(), ids.end()) != ids.end())
+      config_fail("GnatOperator: sample ids must be sorted and unique");
+    if (ids.front() < 0 || ids.back() >= b.n) config_fail("build_gnat_operator: sample id out of range");
+    if (m_r < 1 || m_r > 32) config_fail("ptrom online engine supports 1..32 residual modes");
+    if (b.m > 32) config_fail("ptrom online engine supports at most 32 modes");
+    check_finite(A, (size_t)(m_r * 2 * n_samples), "GNAT operator");
+    auto* h = new ptrom_gnat_op;
+    h->device = ctx->device;
+    try {
+      const long long ns = n_samples, rows = 2 * ns;
+      const int mp = (b.m + 7) / 8 * 8;
+      h->ids = ids;
+      DGnat& g = h->g;
+      g.n_s = ns;
+      g.m_r = (int)m_r;
+      g.m = b.m;
+      g.mp = mp;
+      g.ids = h->mem.up(ids.data(), ids.size());
+      // A padded to 32 rows (zero rows do not change the least-squares problem)
+      std::vector<double> Ap((size_t)32 * rows, 0.0);
+      for (long long k = 0; k < rows; ++k)
+        for (int i = 0; i < m_r; ++i) Ap[i + 32 * k] = A[i + m_r * k];
+      g.A = h->mem.up(Ap.data(), Ap.size());
+      // Φ̄ and x̄⁰ gathered on the host from the device basis (rom.hpp:279-289)
+      std::vector<double> phi((size_t)2 * b.n * b.m), xr((size_t)2 * b.n);
+      PTROM_CUDA(cudaMemcpy(phi.data(), b.phi, phi.size() * 8, cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(xr.data(), b.x_ref, xr.size() * 8, cudaMemcpyDeviceToHost));
+      std::vector<double> pb((size_t)rows * mp, 0.0), x0b((size_t)rows);
+      for (long long k = 0; k < ns; ++k) {
+        const long long p = ids[k];
+        for (int j = 0; j < b.m; ++j) {
+          pb[k + rows * j] = phi[p + 2 * b.n * j];
+          pb[k + ns + rows * j] = phi[p + b.n + 2 * b.n * j];
+        }
+        x0b[k] = xr[p];
+        x0b[k + ns] = xr[p + b.n];
+      }
+      g.phi_bar = h->mem.up(pb.data(), pb.size());
+      g.x0_bar = h->mem.up(x0b.data(), x0b.size());
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+void ptrom_gnat_op_free(ptrom_gnat_op* g) {
+  if (g) {
+    cudaSetDevice(g->device);
+    delete g;
+  }
+}
+
+int ptrom_surrogate_create(ptrom_ctx* ctx, int64_t modes, int64_t n_clusters, const double* phi_tilde,
+                           const double* gamma_tilde, const double* x0_tilde, const uint8_t* zero_gamma,
+                           const int64_t* membership_offsets, const int64_t* membership_ids, int64_t n_targets,
+                           const int64_t* target_ids, const int64_t* cluster_offsets, const int64_t* cluster_list,
+                           int64_t n_direct, const int64_t* direct_ids, const double* direct_phi,
+                           const double* direct_x0, const double* direct_gamma, const int64_t* direct_offsets,
+                           const int64_t* direct_list, ptrom_surrogate** out) {
+  return guarded(ctx, [&] {
+    if (n_targets < 1) config_fail("cluster_pod: no targets");
+    if (modes < 1 || modes > 32) config_fail("surrogate supports 1..32 modes");
+    auto* h = new ptrom_surrogate;
+    h->device = ctx->device;
+    try {
+      DSurrogate& s = h->s;
+      s.m = (int)modes;
+      s.n_c = n_clusters;
+      s.u = n_direct;
+      s.n_t = n_targets;
+      const size_t nc = (size_t)n_clusters, u = (size_t)n_direct, nt = (size_t)n_targets;
+      s.phi_tilde = h->mem.up(phi_tilde, 2 * nc * modes);
+      s.x0_tilde = h->mem.up(x0_tilde, 2 * nc);
+      s.gamma_tilde = h->mem.up(gamma_tilde, nc);
+      s.zero_gamma = h->mem.up(zero_gamma, zero_gamma ? nc : 0);
+      s.mem_off = h->mem.up(reinterpret_cast<const long long*>(membership_offsets), nc + 1);
+      s.mem_ids = h->mem.up(reinterpret_cast<const long long*>(membership_ids), (size_t)membership_offsets[nc]);
+      h->target_ids.assign(target_ids, target_ids + nt);
+      s.target_ids = h->mem.up(reinterpret_cast<const long long*>(target_ids), nt);
+      s.cl_off = h->mem.up(reinterpret_cast<const long long*>(cluster_offsets), nt + 1);
+      std::vector<int> cl(cluster_list, cluster_list + cluster_offsets[nt]);
+      for (int c : cl)
+        if (c < 0 || c >= n_clusters) config_fail("surrogate: cluster index out of range");
+      s.cl_list = h->mem.up(cl.data(), cl.size());
+      s.d_off = h->mem.up(reinterpret_cast<const long long*>(direct_offsets), nt + 1);
+      std::vector<int> dl(direct_list, direct_list + direct_offsets[nt]);
+      for (int d : dl)
+        if (d < 0 || d >= n_direct) config_fail("surrogate: direct index out of range");
+      s.d_list = h->mem.up(dl.data(), dl.size());
+      s.direct_ids = h->mem.up(reinterpret_cast<const long long*>(direct_ids), u);
+      s.direct_phi = h->mem.up(direct_phi, 2 * u * modes);
+      s.direct_x0 = h->mem.up(direct_x0, 2 * u);
+      s.direct_gamma = h->mem.up(direct_gamma, u);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+void ptrom_surrogate_free(ptrom_surrogate* s) {
+  if (s) {
+    cudaSetDevice(s->device);
+    delete s;
+  }
+}
+
+int ptrom_surrogate_export(ptrom_ctx* ctx, const ptrom_surrogate* sur, double* phi_tilde, double* gamma_tilde,
+                           double* x0_tilde, uint8_t* zero_gamma, double* direct_gamma) {
+  return guarded(ctx, [&] {
+    const DSurrogate& s = sur->s;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) PTROM_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    };
+    d2h(phi_tilde, s.phi_tilde, (size_t)2 * s.n_c * s.m * 8);
+    d2h(gamma_tilde, s.gamma_tilde, (size_t)s.n_c * 8);
+    d2h(x0_tilde, s.x0_tilde, (size_t)2 * s.n_c * 8);
+    d2h(zero_gamma, s.zero_gamma, (size_t)s.n_c);
+    d2h(direct_gamma, s.direct_gamma, (size_t)s.u * 8);
+  });
+}
+
+int ptrom_reassign_cluster_circulation_f64(ptrom_ctx* ctx, ptrom_surrogate* sur, int64_t n, const double* gamma,
+                                           const ptrom_basis* basis) {
+  return guarded(ctx, [&] {
+    if (!sur || !basis) config_fail("null surrogate or basis");
+    if (n != basis->b.n) config_fail("reassign_cluster_circulation: gamma size mismatch");
+    check_finite(gamma, (size_t)n, "reassign_cluster_circulation");
+    DevAllocs tmp;
+    const double* dg = tmp.up(gamma, (size_t)n);
+    rom_reassign_exact(ctx, sur->s, basis->b, dg);
+    PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ptrom_hyperpair_f64(ptrom_ctx* ctx, const ptrom_surrogate* sur, const double* target_positions,
+                        const double* x_hat, double delta, int form, int64_t n, const double* inflow, double* f,
+                        double* jac, double* cluster_positions, double* direct_positions, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    if (!sur) config_fail("null surrogate");
+    const DSurrogate& s = sur->s;
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    DevAllocs tmp;
+    const long long nt = s.n_t;
+    const double* dtp = tmp.up(target_positions, (size_t)2 * nt);
+    const double* dxh = tmp.up(x_hat, (size_t)s.m);
+    const double* dinf = inflow ? tmp.up(inflow, (size_t)2 * n) : nullptr;
+    double* df = tmp.zeros<double>((size_t)2 * nt);
+    double* dj = tmp.zeros<double>((size_t)4 * nt);
+    RomScratch w;
+    w.ensure(s, nt, 1);
+    unsigned long long pairs = 0;
+    try {
+      pairs = rom_hyperpair(ctx, s, nullptr, nullptr, 1, s.m, dxh, nullptr, nullptr, dtp, nullptr, delta, form, dinf,
+                            n, w, df, dj, true);
+      check_device_status(ctx);
+      PTROM_CUDA(cudaMemcpy(f, df, 16 * nt, cudaMemcpyDeviceToHost));
+      std::vector<double> jh((size_t)4 * nt);
+      PTROM_CUDA(cudaMemcpy(jh.data(), dj, jh.size() * 8, cudaMemcpyDeviceToHost));
+      for (long long t = 0; t < nt; ++t)
+        for (int k = 0; k < 4; ++k) jac[k * nt + t] = jh[4 * t + k];
+      if (cluster_positions) {
+        PTROM_CUDA(cudaMemcpy(cluster_positions, w.cx, 8 * s.n_c, cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy(cluster_positions + s.n_c, w.cy, 8 * s.n_c, cudaMemcpyDeviceToHost));
+      }
+      if (direct_positions) {
+        PTROM_CUDA(cudaMemcpy(direct_positions, w.dx, 8 * s.u, cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy(direct_positions + s.u, w.dy, 8 * s.u, cudaMemcpyDeviceToHost));
+      }
+    } catch (...) {
+      w.release();
+      throw;
+    }
+    w.release();
+    if (n_pair_evals) *n_pair_evals = pairs;
+  });
+}
+
+// rom.hpp:404-412: reassign (mutates the surrogate) + GnatSolver::simulate.
+int ptrom_ptrom_simulate_f64(ptrom_ctx* ctx, const ptrom_basis* basis, const ptrom_gnat_op* op, ptrom_surrogate* sur,
+                             int64_t n, const double* gamma, double delta, int form, const double* inflow, double dt,
+                             int64_t n_steps, double tol, int max_iters, double step_length, double* x_hat,
+                             int* iterations, uint8_t* converged, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    if (!basis || !op || !sur) config_fail("null basis / operator / surrogate");
+    if (!(dt > 0)) config_fail("time step must be positive");
+    if (n_steps < 0) config_fail("negative step count");
+    if (!(tol > 0)) config_fail("ROM tolerance must be positive");
+    if (max_iters < 1) config_fail("ROM max_iters must be >= 1");
+    if (!(step_length > 0)) config_fail("ROM step length must be positive");
+    if (n != basis->b.n) config_fail("GnatSolver: basis dimension does not match particle count");
+    if (sur->target_ids != op->ids) config_fail("GnatSolver: surrogate targets must equal the sampled particle ids");
+    check_finite(gamma, (size_t)n, "non-finite circulation");
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    if (inflow) check_finite(inflow, (size_t)2 * n, "non-finite inflow");
+    DevAllocs tmp;
+    const double* dg = tmp.up(gamma, (size_t)n);
+    const double* dinf = inflow ? tmp.up(inflow, (size_t)2 * n) : nullptr;
+    rom_reassign_exact(ctx, sur->s, basis->b, dg);
+    const int m = basis->b.m;
+    double* dxh = tmp.zeros<double>((size_t)m * std::max<int64_t>(n_steps, 1));
+    int* dit = tmp.zeros<int>((size_t)std::max<int64_t>(n_steps, 1));
+    unsigned char* dcv = tmp.zeros<unsigned char>((size_t)std::max<int64_t>(n_steps, 1));
+    const unsigned long long pairs = rom_gnat_simulate(ctx, sur->s, op->g, nullptr, 1, nullptr, delta, form, dinf, n,
+                                                       dt, n_steps, tol, max_iters, step_length, dxh, dit, dcv);
+    // x_hat: M x n_steps column-major (RomTrajectory::x_hat, rom.hpp:31)
+    if (n_steps > 0) {
+      PTROM_CUDA(cudaMemcpy(x_hat, dxh, (size_t)m * n_steps * 8, cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(iterations, dit, (size_t)n_steps * 4, cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(converged, dcv, (size_t)n_steps, cudaMemcpyDeviceToHost));
+    }
+    if (n_pair_evals) *n_pair_evals = pairs;
+  });
+}
+
+// Batched online queries for an affine circulation Γ(μ) = Γa + μ Γb over
+// n_inst parameters (SURVEY.md §8b ptrom_gnat_simulate_batch). The
+// surrogate's topology is shared; its tables are not modified. Outputs:
+// x_hat [n_inst][n_steps][M], iterations / converged [n_inst][n_steps].
+int ptrom_ptrom_simulate_batch_f64(ptrom_ctx* ctx, const ptrom_basis* basis, const ptrom_gnat_op* op,
+                                   const ptrom_surrogate* sur, int64_t n, const double* gamma_a,
+                                   const double* gamma_b, int64_t n_inst, const double* mu, int64_t batch,
+                                   double delta, int form, const double* inflow, double dt, int64_t n_steps,
+                                   double tol, int max_iters, double step_length, double* x_hat, int* iterations,
+                                   uint8_t* converged, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    if (!basis || !op || !sur) config_fail("null basis / operator / surrogate");
+    if (!(dt > 0)) config_fail("time step must be positive");
+    if (n_steps < 0) config_fail("negative step count");
+    if (!(tol > 0)) config_fail("ROM tolerance must be positive");
+    if (max_iters < 1) config_fail("ROM max_iters must be >= 1");
+    if (!(step_length > 0)) config_fail("ROM step length must be positive");
+    if (n != basis->b.n) config_fail("GnatSolver: basis dimension does not match particle count");
+    if (sur->target_ids != op->ids) config_fail("GnatSolver: surrogate targets must equal the sampled particle ids");
+    if (n_inst < 1) config_fail("batch needs at least one instance");
+    check_finite(gamma_a, (size_t)n, "non-finite circulation");
+    check_finite(gamma_b, (size_t)n, "non-finite circulation");
+    check_finite(mu, (size_t)n_inst, "non-finite parameter");
+    DevAllocs tmp;
+    const double* dga = tmp.up(gamma_a, (size_t)n);
+    const double* dgb = tmp.up(gamma_b, (size_t)n);
+    const double* dinf = inflow ? tmp.up(inflow, (size_t)2 * n) : nullptr;
+    const DSurrogate& s = sur->s;
+    AffineTables t;
+    t.pa = tmp.zeros<double>((size_t)2 * s.n_c * s.m);
+    t.pb = tmp.zeros<double>((size_t)2 * s.n_c * s.m);
+    t.xa = tmp.zeros<double>((size_t)2 * s.n_c);
+    t.xb = tmp.zeros<double>((size_t)2 * s.n_c);
+    t.ga = tmp.zeros<double>((size_t)s.n_c);
+    t.gb = tmp.zeros<double>((size_t)s.n_c);
+    // direct circulations Γa[id], Γb[id]
+    std::vector<long long> dids((size_t)s.u);
+    PTROM_CUDA(cudaMemcpy(dids.data(), s.direct_ids, dids.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> dga_h(dids.size()), dgb_h(dids.size());
+    for (size_t k = 0; k < dids.size(); ++k) {
+      dga_h[k] = gamma_a[dids[k]];
+      dgb_h[k] = gamma_b[dids[k]];
+    }
+    t.dga = tmp.up(dga_h.data(), dga_h.size());
+    t.dgb = tmp.up(dgb_h.data(), dgb_h.size());
+    rom_affine_tables(ctx, s, basis->b, dga, dgb, t);
+    const int m = basis->b.m;
+    const int64_t B = std::max<int64_t>(1, std::min<int64_t>(batch > 0 ? batch : 256, n_inst));
+    const int64_t steps = std::max<int64_t>(n_steps, 1);
+    double* dmu = tmp.up(mu, (size_t)n_inst);
+    double* dxh = tmp.zeros<double>((size_t)B * m * steps);
+    int* dit = tmp.zeros<int>((size_t)B * steps);
+    unsigned char* dcv = tmp.zeros<unsigned char>((size_t)B * steps);
+    unsigned long long pairs = 0;
+    for (int64_t b0 = 0; b0 < n_inst; b0 += B) {
+      const int nb = (int)std::min<int64_t>(B, n_inst - b0);
+      pairs += rom_gnat_simulate(ctx, s, op->g, &t, nb, dmu + b0, delta, form, dinf, n, dt, n_steps, tol, max_iters,
+                                 step_length, dxh, dit, dcv);
+      if (n_steps > 0) {
+        PTROM_CUDA(cudaMemcpy(x_hat + (size_t)b0 * n_steps * m, dxh, (size_t)nb * n_steps * m * 8,
+                              cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy(iterations + (size_t)b0 * n_steps, dit, (size_t)nb * n_steps * 4,
+                              cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy(converged + (size_t)b0 * n_steps, dcv, (size_t)nb * n_steps, cudaMemcpyDeviceToHost));
+      }
+    }
+    if (n_pair_evals) *n_pair_evals = pairs;
+  });
+}
+
+}  // extern "C"

@@ -105,3 +105,58 @@ def config5(n: int = 1 << 22, seed: int = 5) -> Workload:
     y = rng.uniform(n)
     g = rng.normal(n) / n
     return Workload("config5_sharded_fom_n4194304", n, np.concatenate([x, y]), g, 1e-3 ** 2, 1e-3, 20)
+
+
+@dataclass
+class PtromWorkload:
+    """BASELINE configs[3] inputs."""
+    name: str
+    n: int
+    x0: np.ndarray         # reference state x_ref (SoA)
+    gamma_a: np.ndarray    # Γ(μ) = gamma_a + μ·gamma_b  (patch A fixed, patch B scaled by μ)
+    gamma_b: np.ndarray
+    phi: np.ndarray        # 2N x M POD basis (column-major / Fortran order)
+    sv: np.ndarray         # M singular values (weighted POD space, reduction.hpp:74-77)
+    phi_r: np.ndarray      # 2N x M_r residual basis
+    mu: np.ndarray         # instance parameters
+    delta: float
+    dt: float
+    n_steps: int
+    n_samples: int
+
+
+def _orthonormal(a: np.ndarray) -> np.ndarray:
+    q, r = np.linalg.qr(a)
+    q = q * np.sign(np.diag(r))[None, :]
+    return np.asfortranarray(q)
+
+
+def config4(n: int = 1 << 20, n_inst: int = 4096, modes: int = 16, modes_r: int = 32, n_steps: int = 50,
+            seed: int = 4) -> PtromWorkload:
+    """Two patches as config 3; Γ(μ) = 2/N on patch A and μ·2/N on patch B, μ ~ U[0.5, 2] (seeded).
+
+    Φ: M smooth Fourier displacement fields (seeded wavenumbers/phases) evaluated at the bodies and
+    orthonormalized — it stands in for the offline POD of seeded random snapshots (build_pod is an
+    offline producer, out of scope), with singular values 2^{-k/2}. Φ_r: seeded
+    random orthonormal 2N x M_r (as test_rom.cpp:50-58). Samples n = ceil(0.02 N)."""
+    base = config3(n, seed=3)
+    rng = SplitMix64(seed)
+    x, y = base.x0[:n], base.x0[n:]
+    half = n // 2
+    ga = np.zeros(n)
+    gb = np.zeros(n)
+    ga[:half] = 2.0 / n
+    gb[half:] = 2.0 / n
+    waves = rng.uniform(4 * modes) * 6.0 - 3.0
+    phases = rng.uniform(2 * modes) * 2.0 * np.pi
+    fields = np.empty((2 * n, modes))
+    for k in range(modes):
+        a, b, c, e = waves[4 * k:4 * k + 4] * np.pi
+        fields[:n, k] = np.cos(a * x + b * y + phases[2 * k])
+        fields[n:, k] = np.sin(c * x + e * y + phases[2 * k + 1])
+    phi = _orthonormal(fields)
+    sv = 2.0 ** (-0.5 * np.arange(1, modes + 1))
+    phi_r = _orthonormal(rng.normal(2 * n * modes_r).reshape(modes_r, 2 * n).T)
+    mu = 0.5 + 1.5 * rng.uniform(n_inst)
+    return PtromWorkload("config4_ptrom_n%d" % n, n, base.x0.copy(), ga, gb, phi, sv, phi_r, mu, 0.005 ** 2, 1e-3,
+                         n_steps, int(np.ceil(0.02 * n)))

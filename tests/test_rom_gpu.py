@@ -1,0 +1,168 @@
+"""PTROM online path on the B200 vs the oracle (reduction.hpp:400-431,
+rom.hpp:71-412). Offline tables (greedy samples, A = pinv(PΦ_r), surrogate)
+come from the oracle so the online kernels are checked in isolation;
+reduced states within 1e-12 relative (north_star)."""
+import numpy as np
+import pytest
+
+from paper_2103_01983_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def to_device(rom, s, ctx=None):
+    return rom.SurrogateSourceBasis.from_tables(
+        s.phi_tilde, s.gamma_tilde, s.x0_tilde, s.zero_gamma, s.mem_off, s.mem_ids, s.targets, s.cl_off, s.cl_list,
+        s.direct_ids, s.direct_phi, s.direct_x0, s.direct_gamma, s.d_off, s.d_list, ctx=ctx)
+
+
+class Problem:
+    def __init__(self, oracle, n=4096, modes=16, modes_r=32, n_inst=6, seed=4):
+        w = workloads.config4(n=n, n_inst=n_inst, modes=modes, modes_r=modes_r, seed=seed)
+        self.w = w
+        self.ids = oracle.greedy_sample(w.phi_r, w.n_samples)
+        self.A = oracle.build_gnat_operator(w.phi_r, self.ids)
+        self.g1 = w.gamma_a + w.gamma_b  # nominal μ = 1 (surrogate build)
+        self.oracle = oracle
+
+    def surrogate(self):
+        w = self.w
+        return self.oracle.Surrogate(w.phi, w.sv, w.x0, self.g1, self.ids, 1, 1.0, 1)
+
+
+@pytest.fixture(scope="module")
+def prob(oracle):
+    return Problem(oracle)
+
+
+def test_reassign_is_bit_exact(pt, prob):
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    os_ = prob.surrogate()
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    ds = to_device(rom, os_)
+    g = w.gamma_a + 1.37 * w.gamma_b
+    os_.reassign(g)
+    ds.reassign_cluster_circulation(g, basis)
+    e = ds.export()
+    np.testing.assert_array_equal(e["phi_tilde"], os_.phi_tilde)
+    np.testing.assert_array_equal(e["x0_tilde"], os_.x0_tilde)
+    np.testing.assert_array_equal(e["gamma_tilde"], os_.gamma_tilde)
+    np.testing.assert_array_equal(e["direct_gamma"], os_.direct_gamma)
+
+
+@pytest.mark.parametrize("delta,form", [(2.5e-5, 0), (0.01, 1)])
+def test_hyperpair_parity(pt, prob, delta, form):
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    os_ = prob.surrogate()
+    ds = to_device(rom, os_)
+    rng = np.random.default_rng(48)
+    xh = rng.uniform(-0.1, 0.1, w.phi.shape[1])
+    nt = len(prob.ids)
+    tp = np.r_[w.x0[prob.ids] + w.phi[prob.ids] @ xh, w.x0[prob.ids + w.n] + w.phi[prob.ids + w.n] @ xh]
+    inflow = rng.uniform(-1, 1, 2 * w.n)
+    f, jac, cpos, dpos = os_.hyperpair(tp, xh, prob.g1, delta, form, inflow)
+    sys_ = pt.ParticleSystem(prob.g1, delta, inflow, form)
+    pt.reset_kernel_eval_count()
+    hp = rom.hyperpair(ds, tp, xh, sys_)
+    assert pt.kernel_eval_count() == len(os_.cl_list) + len(os_.d_list)  # test_rom.cpp:401-433
+    assert rel(hp.f, f) <= 1e-12
+    got = np.stack([hp.jac.dfx_dx, hp.jac.dfx_dy, hp.jac.dfy_dx, hp.jac.dfy_dy])
+    assert rel(got, jac) <= 1e-12
+    assert rel(hp.cluster_positions, cpos) <= 1e-14
+    assert rel(hp.direct_positions, dpos) <= 1e-14
+    assert nt == hp.f.shape[0] // 2
+
+
+def test_hyperpair_drops_coincident_cluster_and_flags_collision(pt):
+    # test_rom.cpp:254-301
+    from paper_2103_01983_b200 import rom
+    sur = rom.SurrogateSourceBasis.from_tables(
+        np.zeros((2, 3)), [0.7], [1.0, 2.0], [0], [0, 1], [0], [0], [0, 1], [0], [1], np.zeros((2, 3)), [3.0, 2.0],
+        [0.5], [0, 1], [0])
+    sys0 = pt.ParticleSystem(np.ones(2), 0.0)
+    hp = rom.hyperpair(sur, [1.0, 2.0], np.zeros(3), sys0)
+    d = pt.pairwise_velocity(np.array([1.0, 3.0, 2.0, 2.0]), pt.ParticleSystem(np.array([0.0, 0.5]), 0.0))
+    assert abs(hp.f[0] - d[0]) <= 1e-15 and abs(hp.f[1] - d[2]) <= 1e-15
+    col = rom.SurrogateSourceBasis.from_tables(
+        np.zeros((2, 3)), [0.7], [1.0, 2.0], [0], [0, 1], [0], [0], [0, 1], [0], [1], np.zeros((2, 3)), [1.0, 2.0],
+        [0.5], [0, 1], [0])
+    with pytest.raises(pt.NumericalError):
+        rom.hyperpair(col, [1.0, 2.0], np.zeros(3), sys0)
+
+
+@pytest.mark.parametrize("tol,max_iters,steps", [(1e-300, 5, 20), (1e-6, 100, 15)])
+def test_ptrom_simulate_parity(pt, prob, tol, max_iters, steps):
+    """rom.hpp:404-412 single instance: reassign to Γ(μ = 1.6), march."""
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    g = w.gamma_a + 1.6 * w.gamma_b
+    os_ = prob.surrogate()
+    xo, it_o, cv_o = prob.oracle.ptrom_simulate(os_, w.phi, w.sv, w.x0, prob.ids, prob.A, g, w.delta, w.dt, steps,
+                                                tol, max_iters)
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, prob.ids, prob.A)
+    ds = to_device(rom, prob.surrogate())
+    tr = rom.ptrom_simulate(basis, op, ds, pt.ParticleSystem(g, w.delta), pt.TimeGrid(w.dt, steps),
+                            rom.RomConfig(tol, max_iters, 1.0))
+    np.testing.assert_array_equal(tr.iterations, it_o)
+    np.testing.assert_array_equal(tr.converged, cv_o)
+    worst = max(rel(tr.x_hat[:, s], xo[:, s]) for s in range(steps))
+    assert worst <= 1e-12, worst
+
+
+def test_batch_affine_matches_per_instance_oracle(pt, prob):
+    """Batched online queries over μ: every instance equals the oracle's
+    ptrom_simulate with Γ(μ) = Γa + μ Γb (fresh surrogate each)."""
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    steps = 12
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, prob.ids, prob.A)
+    ds = to_device(rom, prob.surrogate())
+    mu = np.array([0.5, 0.8, 1.0, 1.3, 1.7, 2.0])
+    cfg = rom.RomConfig(1e-300, 5, 1.0)
+    tr = rom.ptrom_simulate_batch(basis, op, ds, w.gamma_a, w.gamma_b, mu, pt.ParticleSystem(prob.g1, w.delta),
+                                  pt.TimeGrid(w.dt, steps), cfg, batch=4)
+    for i, m in enumerate(mu):
+        xo, it_o, _ = prob.oracle.ptrom_simulate(prob.surrogate(), w.phi, w.sv, w.x0, prob.ids, prob.A,
+                                                 w.gamma_a + m * w.gamma_b, w.delta, w.dt, steps, 1e-300, 5)
+        np.testing.assert_array_equal(tr.iterations[i], it_o)
+        worst = max(rel(tr.x_hat[i, s], xo[:, s]) for s in range(steps))
+        assert worst <= 1e-12, (m, worst)
+
+
+def test_padded_modes(pt, oracle):
+    """M = 6, M_r = 8 (DMMA tiles padded with zero columns/rows)."""
+    from paper_2103_01983_b200 import rom
+    p = Problem(oracle, n=2048, modes=6, modes_r=8, seed=9)
+    w = p.w
+    g = w.gamma_a + 0.9 * w.gamma_b
+    xo, it_o, _ = oracle.ptrom_simulate(p.surrogate(), w.phi, w.sv, w.x0, p.ids, p.A, g, w.delta, w.dt, 10, 1e-300, 4)
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, p.ids, p.A)
+    tr = rom.ptrom_simulate(basis, op, to_device(rom, p.surrogate()), pt.ParticleSystem(g, w.delta),
+                            pt.TimeGrid(w.dt, 10), rom.RomConfig(1e-300, 4, 1.0))
+    np.testing.assert_array_equal(tr.iterations, it_o)
+    assert max(rel(tr.x_hat[:, s], xo[:, s]) for s in range(10)) <= 1e-12
+
+
+def test_validation(pt, prob):
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    with pytest.raises(pt.ConfigError):
+        rom.GnatOperator(basis, prob.ids[::-1], prob.A)  # unsorted ids
+    op = rom.GnatOperator(basis, prob.ids, prob.A)
+    ds = to_device(rom, prob.surrogate())
+    with pytest.raises(pt.ConfigError):
+        rom.ptrom_simulate(basis, op, ds, pt.ParticleSystem(prob.g1, w.delta), pt.TimeGrid(0.0, 3))
+    with pytest.raises(pt.ConfigError):
+        rom.ptrom_simulate(basis, op, ds, pt.ParticleSystem(prob.g1, w.delta), pt.TimeGrid(w.dt, 3),
+                           rom.RomConfig(tol=0.0))
