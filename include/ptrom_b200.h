@@ -217,6 +217,27 @@ int ptrom_ptrom_simulate_batch_f64(ptrom_ctx* ctx, const ptrom_basis* basis, con
                                    double tol, int max_iters, double step_length, double* x_hat, int* iterations,
                                    uint8_t* converged, uint64_t* n_pair_evals);
 
+/* ------------------------------------------------- PTROM offline producers -- */
+/* reduction.hpp:93-168 greedy_sample (device scoring/selection). phi_r is
+ * n_dofs x n_r column-major; out_ids receives n_target sorted ids. */
+int ptrom_greedy_sample_f64(ptrom_ctx* ctx, int64_t n_dofs, int64_t n_r, const double* phi_r, int64_t n_target,
+                            int64_t n_preseed, const int64_t* preseed, int64_t* out_ids);
+/* reduction.hpp:182-220 build_gnat_operator: A (m_r x 2 n_s, column-major). */
+int ptrom_build_gnat_operator_f64(ptrom_ctx* ctx, int64_t n_dofs, int64_t m_r, const double* phi_r, int64_t n_s,
+                                  const int64_t* ids, double* A);
+/* reduction.hpp:236-274 + 304-385: weighted POD tree and cluster_pod on the
+ * device (the basis must carry singular values). */
+int ptrom_cluster_pod_f64(ptrom_ctx* ctx, const ptrom_basis* basis, const double* gamma, int64_t leaf_capacity,
+                          int crit_kind, double crit_value, int64_t n_targets, const int64_t* targets,
+                          ptrom_surrogate** out);
+/* sizes: n_clusters, n_direct, n_targets, membership entries, cluster-list
+ * entries, direct-list entries. */
+int ptrom_surrogate_sizes(const ptrom_surrogate* sur, int64_t* sizes);
+int ptrom_surrogate_export_lists(ptrom_ctx* ctx, const ptrom_surrogate* sur, int32_t* cluster_node_ids,
+                                 int64_t* mem_off, int64_t* mem_ids, int64_t* cl_off, int64_t* cl_list,
+                                 int64_t* direct_ids, int64_t* d_off, int64_t* d_list, double* direct_phi,
+                                 double* direct_x0);
+
 /* --------------------------------------------------------- instrumentation -- */
 /* bench.py support: while enabled, the context records CUDA events on its own
  * stream around every launch of the dominant kernel of each call (the

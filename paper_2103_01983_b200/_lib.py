@@ -80,6 +80,12 @@ PROTOTYPES = {
     "ptrom_ptrom_simulate_batch_f64": (C.c_int, [c_ctxp, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_dp, c_dp, c_i64,
                                                  c_dp, c_i64, C.c_double, C.c_int, c_dp, C.c_double, c_i64,
                                                  C.c_double, C.c_int, C.c_double, c_dp, c_dp, c_dp, c_u64p]),
+    "ptrom_greedy_sample_f64": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp]),
+    "ptrom_build_gnat_operator_f64": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_i64, c_dp, c_dp]),
+    "ptrom_cluster_pod_f64": (C.c_int, [c_ctxp, C.c_void_p, c_dp, c_i64, C.c_int, C.c_double, c_i64, c_dp,
+                                        C.POINTER(C.c_void_p)]),
+    "ptrom_surrogate_sizes": (C.c_int, [C.c_void_p, c_dp]),
+    "ptrom_surrogate_export_lists": (C.c_int, [c_ctxp, C.c_void_p] + [c_dp] * 10),
     "ptrom_profile_begin": (C.c_int, [c_ctxp]),
     "ptrom_profile_end": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

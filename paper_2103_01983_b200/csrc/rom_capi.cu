@@ -20,6 +20,13 @@ unsigned long long rom_gnat_simulate(ptrom_ctx* ctx, const DSurrogate& s, const 
                                      int B, const double* d_mu, double delta, int form, const double* d_inflow,
                                      long long n, double dt, long long n_steps, double tol, int max_iters,
                                      double alpha, double* d_xhat_out, int* d_iters, unsigned char* d_conv);
+std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, int n_r, const double* phi_r,
+                                             long long n_target, const std::vector<long long>& preseed);
+std::vector<double> offline_gnat_operator(long long n_dofs, int m_r, const double* phi_r,
+                                          const std::vector<long long>& ids);
+void offline_cluster_pod(ptrom_ctx* ctx, const DBasis& b, const double* d_gamma, long long leaf_cap, int crit_kind,
+                         double crit_value, const std::vector<long long>& targets, DSurrogate& s,
+                         std::vector<void*>& allocs, std::vector<int>& cluster_node_ids);
 }  // namespace ptrom
 
 using namespace ptrom;
@@ -86,6 +93,8 @@ struct ptrom_surrogate {
   int device = 0;
   DSurrogate s;
   std::vector<long long> target_ids;
+  std::vector<int> cluster_node_ids;  // provenance (reduction.hpp:285), when built on the device
+  long long n_membership = 0, n_cluster_list = 0, n_direct_list = 0;
   DevAllocs mem;
 };
 
@@ -199,6 +208,9 @@ int ptrom_surrogate_create(ptrom_ctx* ctx, int64_t modes, int64_t n_clusters, co
       s.u = n_direct;
       s.n_t = n_targets;
       const size_t nc = (size_t)n_clusters, u = (size_t)n_direct, nt = (size_t)n_targets;
+      h->n_membership = membership_offsets[nc];
+      h->n_cluster_list = cluster_offsets[nt];
+      h->n_direct_list = direct_offsets[nt];
       s.phi_tilde = h->mem.up(phi_tilde, 2 * nc * modes);
       s.x0_tilde = h->mem.up(x0_tilde, 2 * nc);
       s.gamma_tilde = h->mem.up(gamma_tilde, nc);
@@ -410,6 +422,94 @@ int ptrom_ptrom_simulate_batch_f64(ptrom_ctx* ctx, const ptrom_basis* basis, con
       }
     }
     if (n_pair_evals) *n_pair_evals = pairs;
+  });
+}
+
+// ------------------------------------------------------ offline producers --
+int ptrom_greedy_sample_f64(ptrom_ctx* ctx, int64_t n_dofs, int64_t n_r, const double* phi_r, int64_t n_target,
+                            int64_t n_preseed, const int64_t* preseed, int64_t* out_ids) {
+  return guarded(ctx, [&] {
+    std::vector<long long> pre(preseed, preseed + n_preseed);
+    const std::vector<long long> ids = offline_greedy_sample(ctx, n_dofs, (int)n_r, phi_r, n_target, pre);
+    std::copy(ids.begin(), ids.end(), out_ids);
+  });
+}
+
+int ptrom_build_gnat_operator_f64(ptrom_ctx* ctx, int64_t n_dofs, int64_t m_r, const double* phi_r, int64_t n_s,
+                                  const int64_t* ids, double* A) {
+  return guarded(ctx, [&] {
+    const std::vector<double> a = offline_gnat_operator(n_dofs, (int)m_r, phi_r, std::vector<long long>(ids, ids + n_s));
+    std::copy(a.begin(), a.end(), A);
+  });
+}
+
+int ptrom_cluster_pod_f64(ptrom_ctx* ctx, const ptrom_basis* basis, const double* gamma, int64_t leaf_capacity,
+                          int crit_kind, double crit_value, int64_t n_targets, const int64_t* targets,
+                          ptrom_surrogate** out) {
+  return guarded(ctx, [&] {
+    if (!basis) config_fail("null basis");
+    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+    if (crit_kind == PTROM_CRIT_BARNES_HUT ? !(crit_value >= 0) : !(crit_value >= 0))
+      config_fail(crit_kind == PTROM_CRIT_BARNES_HUT ? "opening ratio must be >= 0"
+                                                     : "neighborhood width factor must be >= 0");
+    const long long n = basis->b.n;
+    check_finite(gamma, (size_t)n, "cluster_pod");
+    auto* h = new ptrom_surrogate;
+    h->device = ctx->device;
+    try {
+      const double* dg = h->mem.up(gamma, (size_t)n);
+      std::vector<long long> t(targets, targets + n_targets);
+      offline_cluster_pod(ctx, basis->b, dg, leaf_capacity, crit_kind, crit_value, t, h->s, h->mem.p,
+                          h->cluster_node_ids);
+      h->target_ids = t;
+      PTROM_CUDA(cudaMemcpy(&h->n_membership, h->s.mem_off + h->s.n_c, 8, cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(&h->n_cluster_list, h->s.cl_off + h->s.n_t, 8, cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(&h->n_direct_list, h->s.d_off + h->s.n_t, 8, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int ptrom_surrogate_sizes(const ptrom_surrogate* sur, int64_t* sizes) {
+  if (!sur) return PTROM_CONFIG_ERROR;
+  sizes[0] = sur->s.n_c;
+  sizes[1] = sur->s.u;
+  sizes[2] = sur->s.n_t;
+  sizes[3] = sur->n_membership;
+  sizes[4] = sur->n_cluster_list;
+  sizes[5] = sur->n_direct_list;
+  return PTROM_OK;
+}
+
+int ptrom_surrogate_export_lists(ptrom_ctx* ctx, const ptrom_surrogate* sur, int32_t* cluster_node_ids,
+                                 int64_t* mem_off, int64_t* mem_ids, int64_t* cl_off, int64_t* cl_list,
+                                 int64_t* direct_ids, int64_t* d_off, int64_t* d_list, double* direct_phi,
+                                 double* direct_x0) {
+  return guarded(ctx, [&] {
+    const DSurrogate& s = sur->s;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) PTROM_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    };
+    if (cluster_node_ids) std::copy(sur->cluster_node_ids.begin(), sur->cluster_node_ids.end(), cluster_node_ids);
+    d2h(mem_off, s.mem_off, (size_t)(s.n_c + 1) * 8);
+    d2h(mem_ids, s.mem_ids, (size_t)sur->n_membership * 8);
+    d2h(cl_off, s.cl_off, (size_t)(s.n_t + 1) * 8);
+    d2h(d_off, s.d_off, (size_t)(s.n_t + 1) * 8);
+    d2h(direct_ids, s.direct_ids, (size_t)s.u * 8);
+    d2h(direct_phi, s.direct_phi, (size_t)2 * s.u * s.m * 8);
+    d2h(direct_x0, s.direct_x0, (size_t)2 * s.u * 8);
+    std::vector<int> tmp;
+    auto widen = [&](int64_t* dst, const int* src, size_t count) {
+      if (!dst || !count) return;
+      tmp.resize(count);
+      PTROM_CUDA(cudaMemcpy(tmp.data(), src, count * 4, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < count; ++i) dst[i] = tmp[i];
+    };
+    widen(cl_list, s.cl_list, (size_t)sur->n_cluster_list);
+    widen(d_list, s.d_list, (size_t)sur->n_direct_list);
   });
 }
 

@@ -107,6 +107,34 @@ class SurrogateSourceBasis:  # reduction.hpp:280-302
                                                  _p(arrs[12]), _p(arrs[13]), _p(arrs[14]), C.byref(h)))
         return SurrogateSourceBasis(ctx, h, m, nc, u, nt, arrs[6])
 
+    @staticmethod
+    def cluster_pod(basis: PODBasis, gamma, target_ids, criterion, leaf_capacity: int = 1) -> "SurrogateSourceBasis":
+        """reduction.hpp:388-395: weighted POD tree + cluster_pod, on the device."""
+        ctx = basis.ctx
+        g, t = _f64(gamma), _i64(target_ids)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.ptrom_cluster_pod_f64(ctx.handle, basis._h, _p(g), int(leaf_capacity), criterion.kind,
+                                                criterion.value, t.shape[0], _p(t), C.byref(h)))
+        sz = np.zeros(6, np.int64)
+        ctx.check(ctx.lib.ptrom_surrogate_sizes(h, _p(sz)))
+        return SurrogateSourceBasis(ctx, h, basis.modes(), int(sz[0]), int(sz[1]), int(sz[2]), t)
+
+    def export_lists(self) -> dict:
+        sz = np.zeros(6, np.int64)
+        self.ctx.check(self.ctx.lib.ptrom_surrogate_sizes(self._h, _p(sz)))
+        nc, u, nt, nm, ncl, ndl = (int(v) for v in sz)
+        out = dict(cluster_node_ids=np.zeros(nc, np.int32), mem_off=np.zeros(nc + 1, np.int64),
+                   mem_ids=np.zeros(max(nm, 1), np.int64), cl_off=np.zeros(nt + 1, np.int64),
+                   cl_list=np.zeros(max(ncl, 1), np.int64), direct_ids=np.zeros(max(u, 1), np.int64),
+                   d_off=np.zeros(nt + 1, np.int64), d_list=np.zeros(max(ndl, 1), np.int64),
+                   direct_phi=np.zeros((2 * u, self.m), order="F"), direct_x0=np.zeros(2 * u))
+        self.ctx.check(self.ctx.lib.ptrom_surrogate_export_lists(self.ctx.handle, self._h, *(_p(out[k]) for k in (
+            "cluster_node_ids", "mem_off", "mem_ids", "cl_off", "cl_list", "direct_ids", "d_off", "d_list",
+            "direct_phi", "direct_x0"))))
+        out["mem_ids"], out["cl_list"], out["d_list"] = out["mem_ids"][:nm], out["cl_list"][:ncl], out["d_list"][:ndl]
+        out["direct_ids"] = out["direct_ids"][:u]
+        return out
+
     def export(self) -> dict:
         nc, u, m = self.n_clusters, self.n_direct, self.m
         out = dict(phi_tilde=np.zeros((2 * nc, m), order="F"), gamma_tilde=np.zeros(nc), x0_tilde=np.zeros(2 * nc),
@@ -133,6 +161,28 @@ class HyperpairResult:  # rom.hpp:94-99
     jac: BlockDiagonalJacobian
     cluster_positions: np.ndarray
     direct_positions: np.ndarray
+
+
+def greedy_sample(phi_r, n_target: int, preseed=(), ctx: Optional[Context] = None) -> np.ndarray:
+    """reduction.hpp:93-168 (device scoring and selection)."""
+    ctx = ctx or default_context()
+    pr = _fortran(phi_r)
+    pre = _i64(list(preseed))
+    out = np.zeros(int(n_target), np.int64)
+    ctx.check(ctx.lib.ptrom_greedy_sample_f64(ctx.handle, pr.shape[0], pr.shape[1], _p(pr), int(n_target),
+                                              pre.shape[0], _p(pre), _p(out)))
+    return out
+
+
+def build_gnat_operator(phi_r, sample_ids, ctx: Optional[Context] = None) -> np.ndarray:
+    """reduction.hpp:182-220 → A = pinv(P Φ_r) (m_r x 2 n_s)."""
+    ctx = ctx or default_context()
+    pr = _fortran(phi_r)
+    ids = _i64(sample_ids)
+    A = np.zeros((pr.shape[1], 2 * ids.shape[0]), order="F")
+    ctx.check(ctx.lib.ptrom_build_gnat_operator_f64(ctx.handle, pr.shape[0], pr.shape[1], _p(pr), ids.shape[0],
+                                                    _p(ids), _p(A)))
+    return A
 
 
 def hyperpair(sur: SurrogateSourceBasis, target_positions, x_hat, sys: ParticleSystem) -> HyperpairResult:

@@ -166,3 +166,90 @@ def test_validation(pt, prob):
     with pytest.raises(pt.ConfigError):
         rom.ptrom_simulate(basis, op, ds, pt.ParticleSystem(prob.g1, w.delta), pt.TimeGrid(w.dt, 3),
                            rom.RomConfig(tol=0.0))
+
+
+# ------------------------------------------------------- offline producers --
+@pytest.mark.parametrize("n,nr,nt", [(30, 3, 4), (30, 7, 9), (30, 12, 15), (25, 20, 6), (12, 5, 12), (4000, 32, 80)])
+def test_greedy_sample_ids_equal_oracle(pt, oracle, n, nr, nt):
+    # test_reduction.cpp:238-250 shapes (numpy-seeded matrices)
+    from paper_2103_01983_b200 import rom
+    phi_r = np.random.default_rng(81 + n + nr).uniform(-1, 1, (2 * n, nr))
+    np.testing.assert_array_equal(rom.greedy_sample(phi_r, nt), oracle.greedy_sample(phi_r, nt))
+
+
+def test_greedy_sample_hand_cases(pt):
+    # test_reduction.cpp:271-292: single column, lower index wins ties, preseeds
+    from paper_2103_01983_b200 import rom
+    phi_r = np.zeros((10, 1))
+    phi_r[[0, 1, 2, 3, 4, 7], 0] = [0.1, 0.9, 0.5, 0.2, 0.3, 0.6]
+    assert list(rom.greedy_sample(phi_r, 1)) == [1]
+    assert list(rom.greedy_sample(phi_r, 2)) == [1, 2]
+    tie = np.zeros((12, 1))
+    tie[1, 0] = tie[4, 0] = 0.5
+    assert list(rom.greedy_sample(tie, 1)) == [1]
+    ids = rom.greedy_sample(np.random.default_rng(101).uniform(-1, 1, (40, 6)), 8, preseed=[17, 3])
+    assert 17 in ids and 3 in ids and list(ids) == sorted(ids)
+    with pytest.raises(pt.ConfigError):
+        rom.greedy_sample(phi_r, 6)
+
+
+def test_gnat_operator_matches_oracle_and_rank_check(pt, oracle, prob):
+    from paper_2103_01983_b200 import rom
+    A = rom.build_gnat_operator(prob.w.phi_r, prob.ids)
+    assert rel(A, prob.A) <= 1e-12
+    defi = np.zeros((8, 2))
+    defi[0, :] = 1.0
+    defi[4, :] = 2.0
+    defi[1, 0] = 1.0
+    defi[2, 1] = 1.0
+    with pytest.raises(pt.NumericalError, match="rank 1"):
+        rom.build_gnat_operator(defi, [0])
+
+
+def test_device_cluster_pod_tables_equal_oracle(pt, prob):
+    """build_weighted_pod_tree(leaf 1) + cluster_pod(neighbor 1) on the device:
+    lists byte-equal, tables bit-equal (same member order and formula)."""
+    from paper_2103_01983_b200 import rom
+    from paper_2103_01983_b200.tree import ClusterCriterion
+    w = prob.w
+    os_ = prob.surrogate()
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    ds = rom.SurrogateSourceBasis.cluster_pod(basis, prob.g1, prob.ids, ClusterCriterion.neighbor(1.0), 1)
+    L = ds.export_lists()
+    np.testing.assert_array_equal(L["cluster_node_ids"], os_.cluster_node_ids)
+    for k, ok in (("mem_off", os_.mem_off), ("mem_ids", os_.mem_ids), ("cl_off", os_.cl_off),
+                  ("cl_list", os_.cl_list), ("direct_ids", os_.direct_ids), ("d_off", os_.d_off),
+                  ("d_list", os_.d_list)):
+        np.testing.assert_array_equal(L[k], ok, err_msg=k)
+    np.testing.assert_array_equal(L["direct_phi"], os_.direct_phi)
+    np.testing.assert_array_equal(L["direct_x0"], os_.direct_x0)
+    e = ds.export()
+    np.testing.assert_array_equal(e["phi_tilde"], os_.phi_tilde)
+    np.testing.assert_array_equal(e["x0_tilde"], os_.x0_tilde)
+    np.testing.assert_array_equal(e["gamma_tilde"], os_.gamma_tilde)
+    np.testing.assert_array_equal(e["direct_gamma"], os_.direct_gamma)
+
+
+def test_config4_pipeline_built_on_device(pt, oracle):
+    """BASELINE configs[3] recipe at N = 65,536 end to end with product-built
+    offline tables: sample ids, surrogate lists equal the oracle's and the
+    batched x̂ match the oracle's per-instance ptrom_simulate."""
+    from paper_2103_01983_b200 import rom
+    from paper_2103_01983_b200.tree import ClusterCriterion
+    w = workloads.config4(n=1 << 16, n_inst=4)
+    ids = rom.greedy_sample(w.phi_r, w.n_samples)
+    np.testing.assert_array_equal(ids, oracle.greedy_sample(w.phi_r, w.n_samples))
+    A = rom.build_gnat_operator(w.phi_r, ids)
+    g1 = w.gamma_a + w.gamma_b
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, ids, A)
+    ds = rom.SurrogateSourceBasis.cluster_pod(basis, g1, ids, ClusterCriterion.neighbor(1.0), 1)
+    steps = 5
+    tr = rom.ptrom_simulate_batch(basis, op, ds, w.gamma_a, w.gamma_b, w.mu, pt.ParticleSystem(g1, w.delta),
+                                  pt.TimeGrid(w.dt, steps), rom.RomConfig(1e-300, 5, 1.0))
+    A_o = oracle.build_gnat_operator(w.phi_r, ids)
+    for i, m in enumerate(w.mu):
+        os_ = oracle.Surrogate(w.phi, w.sv, w.x0, g1, ids, 1, 1.0, 1)
+        xo, it_o, _ = oracle.ptrom_simulate(os_, w.phi, w.sv, w.x0, ids, A_o, w.gamma_a + m * w.gamma_b, w.delta,
+                                            w.dt, steps, 1e-300, 5)
+        assert max(rel(tr.x_hat[i, s], xo[:, s]) for s in range(steps)) <= 1e-12
