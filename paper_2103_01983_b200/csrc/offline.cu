@@ -303,13 +303,31 @@ std::vector<double> offline_gnat_operator(long long n_dofs, int m_r, const doubl
     numerical_fail("build_gnat_operator: sampled residual basis has rank " + std::to_string(qr.rank) + " < " +
                    std::to_string(m_r) + "; dependent columns: " + cols);
   }
-  std::vector<double> A((size_t)m_r * nd);  // column k = pinv * e_k
-  std::vector<double> e(nd);
-  for (long long k = 0; k < nd; ++k) {
-    std::fill(e.begin(), e.end(), 0.0);
-    e[k] = 1.0;
-    const std::vector<double> x = qr.solve(e);
-    for (int i = 0; i < m_r; ++i) A[i + k * m_r] = x[i];
+  // pinv = P R^{-1} Q1^T: form Q1 (nd x m_r) by applying the reflectors to the
+  // first m_r identity columns, then back-substitute R on its rows.
+  std::vector<double> q1((size_t)nd * m_r, 0.0);
+  for (int j = 0; j < m_r; ++j) {
+    double* col = &q1[(size_t)j * nd];
+    col[j] = 1.0;
+    for (int r = m_r - 1; r >= 0; --r) {  // Q e_j = H_0 ... H_{m_r-1} e_j
+      if (qr.taus[r] == 0) continue;
+      const double* v = &qr.a[(size_t)r * nd];
+      double w = col[r];
+      for (long long i = r + 1; i < nd; ++i) w += v[i] * col[i];
+      w *= qr.taus[r];
+      col[r] -= w;
+      for (long long i = r + 1; i < nd; ++i) col[i] -= w * v[i];
+    }
+  }
+  std::vector<double> A((size_t)m_r * nd);
+  std::vector<double> z(m_r);
+  for (long long k = 0; k < nd; ++k) {  // column k of pinv: R^{-1} (row k of Q1)^T, then P
+    for (int i = m_r - 1; i >= 0; --i) {
+      double s2 = q1[k + (size_t)i * nd];
+      for (int j = i + 1; j < m_r; ++j) s2 -= qr.a[i + (size_t)j * nd] * z[j];
+      z[i] = s2 / qr.a[i + (size_t)i * nd];
+    }
+    for (int j = 0; j < m_r; ++j) A[qr.piv[j] + (size_t)k * m_r] = z[j];
   }
   return A;
 }

@@ -48,6 +48,12 @@ __device__ __forceinline__ double rcp64(double q) {
   return fma(y, e, y);
 }
 
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 // ---------------------------------------------------- table preparation ---
 // reduction.hpp:407-428 for one (cluster, column) pair: column j < m is
 // the Φ̃ mode j, j == m is x̃⁰; sequential member order as the reference.
@@ -88,38 +94,72 @@ __global__ void direct_gamma_kernel(DSurrogate s, const double* __restrict__ gam
 }
 
 // Affine member sums for Γ(μ) = Γa + μΓb: S_A, S_B (Φ rows), X_A, X_B
-// (x_ref), G_A, G_B per cluster.
+// (x_ref), G_A, G_B per cluster — an algebraic reformulation, so any order:
+// one warp per (cluster, column), lanes striding over the members.
 __global__ void affine_tables_kernel(DSurrogate s, DBasis b, const double* __restrict__ ga,
                                      const double* __restrict__ gb, AffineTables t) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   const int cols = s.m + 1;
-  if (idx >= s.n_c * cols) return;
-  const long long c = idx / cols;
-  const int j = (int)(idx % cols);
-  double sax = 0, say = 0, sbx = 0, sby = 0, ga_s = 0, gb_s = 0;
-  for (long long k = s.mem_off[c]; k < s.mem_off[c + 1]; ++k) {
+  if (wid >= s.n_c * cols) return;
+  const long long c = wid / cols;
+  const int j = (int)(wid % cols);
+  double v[6] = {0, 0, 0, 0, 0, 0};  // sax say sbx sby ga gb
+  for (long long k = s.mem_off[c] + lane; k < s.mem_off[c + 1]; k += 32) {
     const long long p = s.mem_ids[k];
     const double vx = j < s.m ? b.phi[p + (long long)j * 2 * b.n] : b.x_ref[p];
     const double vy = j < s.m ? b.phi[p + b.n + (long long)j * 2 * b.n] : b.x_ref[p + b.n];
-    sax = fma(ga[p], vx, sax);
-    say = fma(ga[p], vy, say);
-    sbx = fma(gb[p], vx, sbx);
-    sby = fma(gb[p], vy, sby);
-    ga_s += ga[p];
-    gb_s += gb[p];
+    const double a = ga[p], bb = gb[p];
+    v[0] = fma(a, vx, v[0]);
+    v[1] = fma(a, vy, v[1]);
+    v[2] = fma(bb, vx, v[2]);
+    v[3] = fma(bb, vy, v[3]);
+    v[4] += a;
+    v[5] += bb;
   }
+#pragma unroll
+  for (int e = 0; e < 6; ++e)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[e] += __shfl_xor_sync(0xffffffffu, v[e], o);
+  if (lane != 0) return;
   if (j < s.m) {
-    t.pa[c + (long long)j * 2 * s.n_c] = sax;
-    t.pa[c + s.n_c + (long long)j * 2 * s.n_c] = say;
-    t.pb[c + (long long)j * 2 * s.n_c] = sbx;
-    t.pb[c + s.n_c + (long long)j * 2 * s.n_c] = sby;
+    t.pa[c + (long long)j * 2 * s.n_c] = v[0];
+    t.pa[c + s.n_c + (long long)j * 2 * s.n_c] = v[1];
+    t.pb[c + (long long)j * 2 * s.n_c] = v[2];
+    t.pb[c + s.n_c + (long long)j * 2 * s.n_c] = v[3];
   } else {
-    t.xa[c] = sax;
-    t.xa[c + s.n_c] = say;
-    t.xb[c] = sbx;
-    t.xb[c + s.n_c] = sby;
-    t.ga[c] = ga_s;
-    t.gb[c] = gb_s;
+    t.xa[c] = v[0];
+    t.xa[c + s.n_c] = v[1];
+    t.xb[c] = v[2];
+    t.xb[c + s.n_c] = v[3];
+    t.ga[c] = v[4];
+    t.gb[c] = v[5];
+  }
+}
+
+// Row-major engine tables from the column-major reference layouts.
+__global__ void engine_tables_kernel(DSurrogate s, AffineTables t, DGnat g, int Q, int MP, EngineTables e) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nct = s.n_c * Q * MP, ndt = s.u * 2 * MP, npb = 2 * g.n_s * MP;
+  if (idx < nct) {
+    const long long c = idx / (Q * MP);
+    const int q = (int)((idx / MP) % Q), k = (int)(idx % MP);
+    double v = 0.0;
+    if (k < s.m) {
+      const long long row = c + ((q & 1) ? s.n_c : 0), col = (long long)k * 2 * s.n_c;
+      v = Q == 2 ? s.phi_tilde[row + col] : (q < 2 ? t.pa[row + col] : t.pb[row + col]);
+    }
+    e.ct[idx] = v;
+  } else if (idx < nct + ndt) {
+    const long long i = idx - nct;
+    const long long d = i / (2 * MP);
+    const int q = (int)((i / MP) % 2), k = (int)(i % MP);
+    e.dt[i] = k < s.m ? s.direct_phi[d + (q ? s.u : 0) + (long long)k * 2 * s.u] : 0.0;
+  } else if (idx < nct + ndt + npb) {
+    const long long i = idx - nct - ndt;
+    const long long r = i / MP;
+    const int k = (int)(i % MP);
+    e.pbr[i] = g.phi_bar[r + (long long)k * 2 * g.n_s];
   }
 }
 
@@ -166,6 +206,106 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
   }
 }
 
+
+// Cluster positions as a DMMA GEMM: one warp computes a tile of 2 clusters x
+// 4 quantities (X_A+S_A x̂ and X_B+S_B x̂ for x and y) x 8 instances with
+// K = MP modes (tables are the A operand, x̂ of 8 instances the B operand),
+// then combines (a + μ b)/(G_A + μ G_B) in the epilogue. Exact mode: 4
+// clusters x (x, y) per tile, x̃⁰ + Φ̃ x̂.
+template <bool AFFINE, int MP>
+__global__ void positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et, int B,
+                                              const double* __restrict__ xhat,
+                                              const double* __restrict__ mu, const unsigned char* __restrict__ active,
+                                              double* __restrict__ cx, double* __restrict__ cy, DeviceStatus* st) {
+  constexpr int CPT = AFFINE ? 2 : 4;  // clusters per tile
+  const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long ctiles = (s.n_c + CPT - 1) / CPT;
+  const int btiles = (B + 7) / 8;
+  if (warp_id >= ctiles * btiles) return;
+  const long long c0 = (warp_id / btiles) * CPT;
+  const int b0 = (int)(warp_id % btiles) * 8;
+  const int lr = lane >> 2, lc = lane & 3;
+  const long long ld = 2 * s.n_c;
+  // A-operand row lr
+  const long long ca = c0 + (AFFINE ? (lr >> 2) : (lr >> 1));
+  const int q = AFFINE ? (lr & 3) : (lr & 1);  // 0 ax, 1 ay, 2 bx, 3 by
+  const bool c_ok = ca < s.n_c;
+  const double* trow = et.ct + (ca * (AFFINE ? 4 : 2) + q) * (long long)MP;
+  double acc[2] = {0.0, 0.0};
+  const int bb = b0 + lr;  // B-operand column (instance)
+  (void)ld;
+#pragma unroll
+  for (int k0 = 0; k0 < MP; k0 += 4) {
+    const int k = k0 + lc;
+    const double a = c_ok ? trow[k] : 0.0;
+    const double x = bb < B ? xhat[(long long)bb * MP + k] : 0.0;
+    dmma(acc, a, x);
+  }
+  // accumulator: row lr (same (cluster, quantity) mapping), instances b0 + 2*lc + {0,1}
+  if (AFFINE) {
+    const double o0 = __shfl_down_sync(0xffffffffu, acc[0], 8);  // bx/by partner (row + 2)
+    const double o1 = __shfl_down_sync(0xffffffffu, acc[1], 8);
+    if (q < 2 && c_ok) {
+      const double base_a = q == 0 ? t.xa[ca] : t.xa[ca + s.n_c];
+      const double base_b = q == 0 ? t.xb[ca] : t.xb[ca + s.n_c];
+      const double ga = t.ga[ca], gb = t.gb[ca];
+      for (int e = 0; e < 2; ++e) {
+        const int b = b0 + 2 * lc + e;
+        if (b >= B || (active && !active[b])) continue;
+        const double m = mu[b];
+        const double G = ga + m * gb;
+        if (G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+        const double v = fma(m, base_b + (e ? o1 : o0), base_a + acc[e]) / G;
+        (q == 0 ? cx : cy)[ca * B + b] = v;
+      }
+    }
+  } else if (c_ok) {
+    const double base = s.x0_tilde[ca + (q ? s.n_c : 0)];
+    for (int e = 0; e < 2; ++e) {
+      const int b = b0 + 2 * lc + e;
+      if (b >= B || (active && !active[b])) continue;
+      (q == 0 ? cx : cy)[ca * B + b] = base + acc[e];
+    }
+  }
+}
+
+// Direct-source positions x⁰_d + Φ_d x̂ as a DMMA GEMM (4 sources x (x, y)
+// x 8 instances per warp tile).
+template <int MP>
+__global__ void positions_direct_mma_kernel(DSurrogate s, EngineTables et, int B, const double* __restrict__ xhat,
+                                            const unsigned char* __restrict__ active, double* __restrict__ dx,
+                                            double* __restrict__ dy) {
+  const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long dtiles = (s.u + 3) / 4;
+  const int btiles = (B + 7) / 8;
+  if (warp_id >= dtiles * btiles) return;
+  const long long d0 = (warp_id / btiles) * 4;
+  const int b0 = (int)(warp_id % btiles) * 8;
+  const int lr = lane >> 2, lc = lane & 3;
+  const long long d = d0 + (lr >> 1);
+  const int q = lr & 1;
+  const bool ok = d < s.u;
+  const double* trow = et.dt + (d * 2 + q) * (long long)MP;
+  double acc[2] = {0.0, 0.0};
+  const int bb = b0 + lr;
+#pragma unroll
+  for (int k0 = 0; k0 < MP; k0 += 4) {
+    const int k = k0 + lc;
+    const double a = ok ? trow[k] : 0.0;
+    const double x = bb < B ? xhat[(long long)bb * MP + k] : 0.0;
+    dmma(acc, a, x);
+  }
+  if (!ok) return;
+  const double base = s.direct_x0[d + (q ? s.u : 0)];
+  for (int e = 0; e < 2; ++e) {
+    const int b = b0 + 2 * lc + e;
+    if (b >= B || (active && !active[b])) continue;
+    (q == 0 ? dx : dy)[d * B + b] = base + acc[e];
+  }
+}
+
 // Direct sources: x⁰_d + Φ_d x̂ (rom.hpp:114), Γ_d(μ).
 template <bool AFFINE>
 __global__ void positions_direct_kernel(DSurrogate s, AffineTables t, int B, int xs, const double* __restrict__ xhat,
@@ -208,7 +348,8 @@ __global__ void positions_targets_kernel(DGnat g, int B, const double* __restric
 // exactly on its target when delta == 0, rom.hpp:129), then direct sources
 // (skipping the target's own id, rom.hpp:136), fused velocity + Jacobian,
 // inflow at the target id. f: [b][2n_t], jac: [b][n_t][4].
-__global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, int B, const double* __restrict__ xbar,
+__global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTables at, const double* __restrict__ mu,
+                                                        int B, const double* __restrict__ xbar,
                                                         const double* __restrict__ cx, const double* __restrict__ cy,
                                                         const double* __restrict__ cg, const double* __restrict__ dx,
                                                         const double* __restrict__ dy, const double* __restrict__ dg,
@@ -239,18 +380,20 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, int B, con
         jc += w;
         ++cnt;
       };
+      const double mub = mu ? mu[b] : 0.0;
       for (long long k = s.cl_off[t]; k < s.cl_off[t + 1]; ++k) {
-        const long long c = (long long)s.cl_list[k] * B + b;
+        const long long ci = s.cl_list[k];
+        const long long c = ci * B + b;
         const double sx = cx[c], sy = cy[c];
         if (delta == 0.0 && sx == px && sy == py) continue;
-        add(sx, sy, cg[c]);
+        add(sx, sy, mu ? fma(mub, at.gb[ci], at.ga[ci]) : s.gamma_tilde[ci]);
       }
       const long long pid = s.target_ids[t];
       for (long long k = s.d_off[t]; k < s.d_off[t + 1]; ++k) {
         const long long loc = s.d_list[k];
         if (s.direct_ids[loc] == pid) continue;
         const long long d = loc * B + b;
-        add(dx[d], dy[d], dg[d]);
+        add(dx[d], dy[d], mu ? fma(mub, at.dgb[loc], at.dga[loc]) : s.direct_gamma[loc]);
       }
       if (inflow) {
         fx = fx + inflow[pid];
@@ -275,11 +418,6 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, int B, con
 }
 
 // -------------------------------------------------------------- gn_eval ---
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
 
 // One CTA per instance. Streams rows k of the sampled residual in steps of 4
 // (the DMMA k-extent); each warp owns every 8th step. MR = 32 residual modes
@@ -438,6 +576,137 @@ __global__ void __launch_bounds__(kGnThreads) gn_eval_kernel(DGnat g, int B, dou
   }
 }
 
+
+// Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
+// slice of the sampled rows; A and Φ̄ rows of the slice are shared by the 8
+// warps through L1. Partials [slice][b][32·M + 32 + M] are reduced in slice
+// order by gn_finish_kernel (deterministic).
+template <int M>
+__global__ void __launch_bounds__(256) gn_partial_kernel(DGnat g, EngineTables et, int B, double h,
+                                                         const double* __restrict__ xbar,
+                                                         const double* __restrict__ xprev,
+                                                         const double* __restrict__ fbar,
+                                                         const double* __restrict__ fprev,
+                                                         const double* __restrict__ jac, GnState st_,
+                                                         long long slice_len, double* __restrict__ part) {
+  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  if (b >= B || !st_.active[b]) return;
+  const long long nt = g.n_s, rows = 2 * nt;
+  const double* xb = xbar + (long long)b * rows;
+  const double* xp = xprev + (long long)b * rows;
+  const double* fb = fbar + (long long)b * rows;
+  const double* fp = fprev + (long long)b * rows;
+  const double* jb = jac + (long long)b * nt * 4;
+  const int lr = lane >> 2, lc = lane & 3;
+  const bool need_ac = !(st_.evals[b] >= st_.max_iters);
+  double acc[TI][TN][2];
+  double ar[TI];
+  double gr[TN];
+#pragma unroll
+  for (int i = 0; i < TI; ++i) {
+    ar[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) gr[j] = 0.0;
+  const long long k_begin = blockIdx.y * slice_len, k_end = min(rows, k_begin + slice_len);
+  for (long long k0 = k_begin; k0 < k_end; k0 += 4) {
+    const long long r = k0 + lc;
+    double rv = 0.0;
+    double cv[TN];
+    if (r < k_end) {
+      rv = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
+      const long long t = r < nt ? r : r - nt;
+      const double4 J = *reinterpret_cast<const double4*>(jb + 4 * t);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int m = j * 8 + lr;
+        const double px = et.pbr[t * M + m], py = et.pbr[(t + nt) * M + m];
+        const double own = r < nt ? px : py;
+        const double inner = r < nt ? __dadd_rn(__dmul_rn(J.x, px), __dmul_rn(J.y, py))
+                                    : __dadd_rn(__dmul_rn(J.z, px), __dmul_rn(J.w, py));
+        cv[j] = __dsub_rn(own, __dmul_rn(h, inner));
+        gr[j] = fma(cv[j], rv, gr[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) cv[j] = 0.0;
+    }
+    double av[TI];
+#pragma unroll
+    for (int i = 0; i < TI; ++i) {
+      av[i] = r < k_end ? g.A[(i * 8 + lr) + r * MR] : 0.0;
+      ar[i] = fma(av[i], rv, ar[i]);
+    }
+    if (need_ac) {
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j], av[i], cv[j]);
+    }
+  }
+  double* out = part + ((long long)blockIdx.y * B + b) * PART;
+#pragma unroll
+  for (int i = 0; i < TI; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int row = i * 8 + lr, col = j * 8 + lc * 2;
+      out[row + col * MR] = acc[i][j][0];
+      out[row + (col + 1) * MR] = acc[i][j][1];
+    }
+#pragma unroll
+  for (int i = 0; i < TI; ++i) {
+    double v = ar[i];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (lc == 0) out[MR * M + i * 8 + lr] = v;
+  }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    double v = gr[j];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (lc == 0) out[MR * M + MR + j * 8 + lr] = v;
+  }
+}
+
+// Slice-ordered reduction + the convergence logic of rom.hpp:309-324.
+template <int M>
+__global__ void gn_finish_kernel(int B, int S, const double* __restrict__ part, GnState st_) {
+  constexpr int MR = 32, PART = MR * M + MR + M;
+  const int b = blockIdx.x;
+  if (!st_.active[b]) return;
+  __shared__ double grad[M];
+  for (int e = threadIdx.x; e < PART; e += blockDim.x) {
+    double v = 0.0;
+    for (int sl = 0; sl < S; ++sl) v += part[((long long)sl * B + b) * PART + e];
+    if (e < MR * M) st_.ac[(long long)b * MR * M + e] = v;
+    else if (e < MR * M + MR) st_.ar[(long long)b * MR + (e - MR * M)] = v;
+    else grad[e - MR * M - MR] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ss = 0.0;
+    for (int m = 0; m < M; ++m) ss += grad[m] * grad[m];
+    const double gn = sqrt(ss);
+    const int evals = ++st_.evals[b];
+    bool done = false, conv = false;
+    if (evals == 1) {
+      st_.g0[b] = gn;
+      if (gn == 0.0) done = conv = true;
+    } else if (gn / st_.g0[b] <= st_.tol) {
+      done = conv = true;
+    }
+    if (!done && evals - 1 >= st_.max_iters) done = true;
+    st_.converged[b] = conv ? 1 : 0;
+    if (done) st_.active[b] = 0;
+    else atomicAdd(st_.n_active, 1);
+  }
+}
+
 // --------------------------------------------------------------- update ---
 // rom.hpp:325-329: Δ = argmin ‖(A C) Δ + A r̄‖ (ColPivHouseholderQR), x̂ += αΔ.
 // One warp per instance; lane i owns row i of the MR x M system.
@@ -561,34 +830,72 @@ void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const do
 void rom_affine_tables(ptrom_ctx* ctx, const DSurrogate& s, const DBasis& b, const double* d_ga, const double* d_gb,
                        AffineTables& t) {
   const long long work = s.n_c * (s.m + 1);
-  if (work > 0) affine_tables_kernel<<<blocks_for(work, 128), 128, 0, ctx->stream>>>(s, b, d_ga, d_gb, t);
+  if (work > 0) affine_tables_kernel<<<blocks_for(work * 32, 256), 256, 0, ctx->stream>>>(s, b, d_ga, d_gb, t);
   PTROM_LAUNCH_CHECK();
 }
 
-// Positions + hyperpair for B instances (active mask may be null).
-unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t, int B,
-                                 int xs, const double* d_xhat, const double* d_mu, const unsigned char* d_active,
-                                 const double* d_xbar_in, double* d_xbar_out, double delta, int form,
-                                 const double* d_inflow, long long n, RomScratch& w, double* d_f, double* d_jac,
-                                 bool count_pairs) {
+template <int MP>
+void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTables* t, const EngineTables& et, int B,
+                          const double* d_xhat, const double* d_mu, const unsigned char* d_active, RomScratch& w) {
   cudaStream_t st = ctx->stream;
   AffineTables empty{};
   const AffineTables& tt = t ? *t : empty;
+  const long long btiles = (B + 7) / 8;
   if (s.n_c > 0) {
-    if (t)
-      positions_clusters_kernel<true><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
-                                                                                 w.cx, w.cy, w.cg, ctx->d_status);
-    else
-      positions_clusters_kernel<false><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
-                                                                                  w.cx, w.cy, w.cg, ctx->d_status);
+    if (t) {
+      const long long warps = ((s.n_c + 1) / 2) * btiles;
+      positions_clusters_mma_kernel<true, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
+          s, tt, et, B, d_xhat, d_mu, d_active, w.cx, w.cy, ctx->d_status);
+    } else {
+      const long long warps = ((s.n_c + 3) / 4) * btiles;
+      positions_clusters_mma_kernel<false, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
+          s, tt, et, B, d_xhat, d_mu, d_active, w.cx, w.cy, ctx->d_status);
+    }
   }
   if (s.u > 0) {
-    if (t)
-      positions_direct_kernel<true><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active, w.dx,
-                                                                            w.dy, w.dg);
-    else
-      positions_direct_kernel<false><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
-                                                                             w.dx, w.dy, w.dg);
+    const long long warps = ((s.u + 3) / 4) * btiles;
+    positions_direct_mma_kernel<MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(s, et, B, d_xhat, d_active, w.dx,
+                                                                                w.dy);
+  }
+  PTROM_LAUNCH_CHECK();
+}
+
+// Positions + hyperpair for B instances (active mask may be null). With
+// engine tables (the batched march) source positions use the DMMA kernels;
+// without (single hyperpair calls) the scalar ones.
+unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t,
+                                 const EngineTables* et, int B, int xs, const double* d_xhat, const double* d_mu,
+                                 const unsigned char* d_active, const double* d_xbar_in, double* d_xbar_out,
+                                 double delta, int form, const double* d_inflow, long long n, RomScratch& w,
+                                 double* d_f, double* d_jac, bool count_pairs) {
+  cudaStream_t st = ctx->stream;
+  AffineTables empty{};
+  const AffineTables& tt = t ? *t : empty;
+  if (et) {
+    switch (xs) {
+      case 8: launch_positions_mma<8>(ctx, s, t, *et, B, d_xhat, d_mu, d_active, w); break;
+      case 16: launch_positions_mma<16>(ctx, s, t, *et, B, d_xhat, d_mu, d_active, w); break;
+      case 24: launch_positions_mma<24>(ctx, s, t, *et, B, d_xhat, d_mu, d_active, w); break;
+      default: launch_positions_mma<32>(ctx, s, t, *et, B, d_xhat, d_mu, d_active, w); break;
+    }
+  } else {
+    if (s.n_c > 0) {
+      if (t)
+        positions_clusters_kernel<true><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
+                                                                                   w.cx, w.cy, w.cg, ctx->d_status);
+      else
+        positions_clusters_kernel<false><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu,
+                                                                                    d_active, w.cx, w.cy, w.cg,
+                                                                                    ctx->d_status);
+    }
+    if (s.u > 0) {
+      if (t)
+        positions_direct_kernel<true><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
+                                                                               w.dx, w.dy, w.dg);
+      else
+        positions_direct_kernel<false><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
+                                                                                w.dx, w.dy, w.dg);
+    }
   }
   const double* xbar = d_xbar_in;
   if (g) {
@@ -599,9 +906,10 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
   if (count_pairs) PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
   {
     ProfScope prof(ctx);
-    hyperpair_kernel<<<blocks_for(s.n_t * B, 128), 128, 0, st>>>(s, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy, w.dg,
-                                                                 effective_delta(delta, form), delta, d_inflow, n,
-                                                                 d_active, d_f, d_jac, w.pairs, ctx->d_status);
+    hyperpair_kernel<<<blocks_for(s.n_t * B, 128), 128, 0, st>>>(s, tt, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg,
+                                                                 w.dx, w.dy, w.dg, effective_delta(delta, form), delta,
+                                                                 d_inflow, n, d_active, d_f, d_jac, w.pairs,
+                                                                 ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
@@ -685,30 +993,49 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
   gs.n_active = (int*)alloc(4);
   gs.tol = tol;
   gs.max_iters = max_iters;
+  EngineTables et;
+  et.q = t ? 4 : 2;
+  et.ct = (double*)alloc((size_t)s.n_c * et.q * MP * 8);
+  et.dt = (double*)alloc((size_t)s.u * 2 * MP * 8);
+  et.pbr = (double*)alloc((size_t)rows * MP * 8);
+  {
+    AffineTables empty{};
+    const long long total = s.n_c * et.q * MP + s.u * 2 * MP + rows * MP;
+    engine_tables_kernel<<<blocks_for(total, 256), 256, 0, st>>>(s, t ? *t : empty, g, et.q, MP, et);
+    PTROM_LAUNCH_CHECK();
+  }
+  // split-K shape: ~4 CTAs per SM over ceil(B/8) instance groups
+  const long long groups = (B + 7) / 8;
+  const int S = (int)std::max<long long>(1, std::min<long long>(64, (4LL * ctx->num_sms + groups - 1) / groups));
+  const long long slice_len = ((rows + S - 1) / S + 3) / 4 * 4;
+  double* part = (double*)alloc((size_t)S * B * (32 * MP + 32 + MP) * 8);
   int* h_active = nullptr;
   PTROM_CUDA(cudaMallocHost(&h_active, 4));
   PTROM_CUDA(cudaMemsetAsync(xhat, 0, (size_t)B * MP * 8, st));
   PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
   const double h = dt / 2.0;
   // rom.hpp:298-300: x̄_prev = x̄⁰, f̄_prev = hyperpair(x̄⁰, 0); jac scratch is overwritten below
-  rom_hyperpair(ctx, s, &g, t, B, MP, xhat, d_mu, nullptr, nullptr, xprev, delta, form, d_inflow, n, w, fprev, jac,
-                false);
+  rom_hyperpair(ctx, s, &g, t, &et, B, MP, xhat, d_mu, nullptr, nullptr, xprev, delta, form, d_inflow, n, w, fprev,
+                jac, false);
   for (long long step = 0; step < n_steps; ++step) {
     reset_step_kernel<<<blocks_for(B, 256), 256, 0, st>>>(B, gs);
     // x̄ = x̄⁰ + Φ̄ x̂; (f̄, J) = hyperpair(x̄, x̂)   (rom.hpp:306-307)
-    rom_hyperpair(ctx, s, &g, t, B, MP, xhat, d_mu, nullptr, nullptr, xbar, delta, form, d_inflow, n, w, fbar, jac,
-                  false);
+    rom_hyperpair(ctx, s, &g, t, &et, B, MP, xhat, d_mu, nullptr, nullptr, xbar, delta, form, d_inflow, n, w, fbar,
+                  jac, false);
     while (true) {
       PTROM_CUDA(cudaMemsetAsync(gs.n_active, 0, 4, st));
-      gn_eval_kernel<32, MP><<<B, kGnThreads, 0, st>>>(g, B, h, xbar, xprev, fbar, fprev, jac, gs, 0);
+      gn_partial_kernel<MP><<<dim3((unsigned)((B + 7) / 8), (unsigned)S), 256, 0, st>>>(g, et, B, h, xbar, xprev,
+                                                                                      fbar, fprev, jac, gs,
+                                                                                      slice_len, part);
+      gn_finish_kernel<MP><<<B, 128, 0, st>>>(B, S, part, gs);
       PTROM_LAUNCH_CHECK();
       PTROM_CUDA(cudaMemcpyAsync(h_active, gs.n_active, 4, cudaMemcpyDeviceToHost, st));
       PTROM_CUDA(cudaStreamSynchronize(st));
       if (*h_active == 0) break;
       qr_update_kernel<32, MP><<<blocks_for(B, 4), 128, 0, st>>>(B, gs, alpha, xhat);
       PTROM_LAUNCH_CHECK();
-      rom_hyperpair(ctx, s, &g, t, B, MP, xhat, d_mu, gs.active, nullptr, xbar, delta, form, d_inflow, n, w, fbar,
-                    jac, false);
+      rom_hyperpair(ctx, s, &g, t, &et, B, MP, xhat, d_mu, gs.active, nullptr, xbar, delta, form, d_inflow, n, w,
+                    fbar, jac, false);
     }
     record_step_kernel<<<blocks_for(B, 128), 128, 0, st>>>(B, g.m, MP, step, n_steps, xhat, gs, d_xhat_out, d_iters,
                                                             d_conv);

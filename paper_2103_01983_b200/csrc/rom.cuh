@@ -55,6 +55,18 @@ struct AffineTables {
   double *dga = nullptr, *dgb = nullptr;  // u (direct circulations)
 };
 
+// Engine-private row-major copies (tile-friendly operand layouts):
+//   ct  [n_c][Q][mp]  cluster rows (Q = 4 affine: S_A x, S_A y, S_B x, S_B y;
+//                     Q = 2 exact: Φ̃ x, Φ̃ y), zero-padded to mp modes
+//   dt  [u][2][mp]    direct rows Φ_d x, Φ_d y
+//   pbr [2 n_t][mp]   Φ̄ rows (x rows then y rows)
+struct EngineTables {
+  double* ct = nullptr;
+  double* dt = nullptr;
+  double* pbr = nullptr;
+  int q = 2;
+};
+
 // Per-instance Gauss–Newton state.
 struct GnState {
   double* ac = nullptr;  // [B][32 x mp]

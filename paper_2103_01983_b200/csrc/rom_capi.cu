@@ -11,11 +11,11 @@ namespace ptrom {
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma);
 void rom_affine_tables(ptrom_ctx* ctx, const DSurrogate& s, const DBasis& b, const double* d_ga, const double* d_gb,
                        AffineTables& t);
-unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t, int B,
-                                 int xs, const double* d_xhat, const double* d_mu, const unsigned char* d_active,
-                                 const double* d_xbar_in, double* d_xbar_out, double delta, int form,
-                                 const double* d_inflow, long long n, RomScratch& w, double* d_f, double* d_jac,
-                                 bool count_pairs);
+unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t,
+                                 const EngineTables* et, int B, int xs, const double* d_xhat, const double* d_mu,
+                                 const unsigned char* d_active, const double* d_xbar_in, double* d_xbar_out,
+                                 double delta, int form, const double* d_inflow, long long n, RomScratch& w,
+                                 double* d_f, double* d_jac, bool count_pairs);
 unsigned long long rom_gnat_simulate(ptrom_ctx* ctx, const DSurrogate& s, const DGnat& g, const AffineTables* t,
                                      int B, const double* d_mu, double delta, int form, const double* d_inflow,
                                      long long n, double dt, long long n_steps, double tol, int max_iters,
@@ -293,8 +293,8 @@ int ptrom_hyperpair_f64(ptrom_ctx* ctx, const ptrom_surrogate* sur, const double
     w.ensure(s, nt, 1);
     unsigned long long pairs = 0;
     try {
-      pairs = rom_hyperpair(ctx, s, nullptr, nullptr, 1, s.m, dxh, nullptr, nullptr, dtp, nullptr, delta, form, dinf,
-                            n, w, df, dj, true);
+      pairs = rom_hyperpair(ctx, s, nullptr, nullptr, nullptr, 1, s.m, dxh, nullptr, nullptr, dtp, nullptr, delta,
+                            form, dinf, n, w, df, dj, true);
       check_device_status(ctx);
       PTROM_CUDA(cudaMemcpy(f, df, 16 * nt, cudaMemcpyDeviceToHost));
       std::vector<double> jh((size_t)4 * nt);
