@@ -417,6 +417,14 @@ void offline_cluster_pod(ptrom_ctx* ctx, const DBasis& b, const double* d_gamma,
                                                   s.mem_off + 1, st));
   }
   s.target_ids = (long long*)up(targets.data(), nt * 8);
+  {  // spatial processing order: targets sorted by their slot in the weighted tree
+    std::vector<int> slot(n);
+    PTROM_CUDA(cudaMemcpy(slot.data(), tree.slot, n * 4, cudaMemcpyDeviceToHost));
+    std::vector<int> order(nt);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b2) { return slot[targets[a]] < slot[targets[b2]]; });
+    s.t_order = (int*)up(order.data(), nt * 4);
+  }
   s.cl_off = (long long*)up(c_off.data(), c_off.size() * 8);
   s.cl_list = (int*)up(cl_list.data(), cl_list.size() * 4);
   s.d_off = (long long*)up(d_off.data(), d_off.size() * 8);

@@ -214,58 +214,76 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
 // clusters x (x, y) per tile, x̃⁰ + Φ̃ x̂.
 template <bool AFFINE, int MP>
 __global__ void positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et, int B,
-                                              const double* __restrict__ xhat,
-                                              const double* __restrict__ mu, const unsigned char* __restrict__ active,
-                                              double* __restrict__ cx, double* __restrict__ cy, DeviceStatus* st) {
-  constexpr int CPT = AFFINE ? 2 : 4;  // clusters per tile
+                                              const double* __restrict__ xhat, const double* __restrict__ mu,
+                                              const unsigned char* __restrict__ active, double* __restrict__ cx,
+                                              double* __restrict__ cy, DeviceStatus* st) {
+  // One warp per cluster tile; its table rows (the A operand) stay in
+  // registers while it sweeps all instance tiles of 8.
+  constexpr int CPT = AFFINE ? 2 : 4;
+  constexpr int KS = MP / 4;
   const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long ctiles = (s.n_c + CPT - 1) / CPT;
-  const int btiles = (B + 7) / 8;
-  if (warp_id >= ctiles * btiles) return;
-  const long long c0 = (warp_id / btiles) * CPT;
-  const int b0 = (int)(warp_id % btiles) * 8;
+  if (warp_id >= ctiles) return;
+  const long long c0 = warp_id * CPT;
   const int lr = lane >> 2, lc = lane & 3;
-  const long long ld = 2 * s.n_c;
-  // A-operand row lr
   const long long ca = c0 + (AFFINE ? (lr >> 2) : (lr >> 1));
   const int q = AFFINE ? (lr & 3) : (lr & 1);  // 0 ax, 1 ay, 2 bx, 3 by
   const bool c_ok = ca < s.n_c;
   const double* trow = et.ct + (ca * (AFFINE ? 4 : 2) + q) * (long long)MP;
-  double acc[2] = {0.0, 0.0};
-  const int bb = b0 + lr;  // B-operand column (instance)
-  (void)ld;
+  double a[KS];
 #pragma unroll
-  for (int k0 = 0; k0 < MP; k0 += 4) {
-    const int k = k0 + lc;
-    const double a = c_ok ? trow[k] : 0.0;
-    const double x = bb < B ? xhat[(long long)bb * MP + k] : 0.0;
-    dmma(acc, a, x);
-  }
-  // accumulator: row lr (same (cluster, quantity) mapping), instances b0 + 2*lc + {0,1}
-  if (AFFINE) {
-    const double o0 = __shfl_down_sync(0xffffffffu, acc[0], 8);  // bx/by partner (row + 2)
-    const double o1 = __shfl_down_sync(0xffffffffu, acc[1], 8);
-    if (q < 2 && c_ok) {
-      const double base_a = q == 0 ? t.xa[ca] : t.xa[ca + s.n_c];
-      const double base_b = q == 0 ? t.xb[ca] : t.xb[ca + s.n_c];
-      const double ga = t.ga[ca], gb = t.gb[ca];
-      for (int e = 0; e < 2; ++e) {
-        const int b = b0 + 2 * lc + e;
-        if (b >= B || (active && !active[b])) continue;
-        const double m = mu[b];
-        const double G = ga + m * gb;
-        if (G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
-        const double v = fma(m, base_b + (e ? o1 : o0), base_a + acc[e]) / G;
-        (q == 0 ? cx : cy)[ca * B + b] = v;
-      }
+  for (int k = 0; k < KS; ++k) a[k] = c_ok ? trow[4 * k + lc] : 0.0;
+  double base_a = 0, base_b = 0, ga = 0, gb = 0;
+  if (c_ok) {
+    if (AFFINE) {
+      base_a = (q & 1) ? t.xa[ca + s.n_c] : t.xa[ca];
+      base_b = (q & 1) ? t.xb[ca + s.n_c] : t.xb[ca];
+      ga = t.ga[ca];
+      gb = t.gb[ca];
+    } else {
+      base_a = s.x0_tilde[ca + (q ? s.n_c : 0)];
     }
-  } else if (c_ok) {
-    const double base = s.x0_tilde[ca + (q ? s.n_c : 0)];
-    for (int e = 0; e < 2; ++e) {
-      const int b = b0 + 2 * lc + e;
-      if (b >= B || (active && !active[b])) continue;
-      (q == 0 ? cx : cy)[ca * B + b] = base + acc[e];
+  }
+  double* out = (q & 1) ? cy : cx;
+  for (int b0 = 0; b0 < B; b0 += 8) {
+    double acc[2] = {0.0, 0.0};
+    const int bb = b0 + lr;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const double x = bb < B ? xhat[(long long)bb * MP + 4 * k + lc] : 0.0;
+      dmma(acc, a[k], x);
+    }
+    if (AFFINE) {
+      const double o0 = __shfl_down_sync(0xffffffffu, acc[0], 8);  // S_B row partner (row + 2)
+      const double o1 = __shfl_down_sync(0xffffffffu, acc[1], 8);
+      if (q < 2 && c_ok) {
+        const int b = b0 + 2 * lc;  // two consecutive instances per lane: one 16-byte store
+        double v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double m = b + e < B ? mu[b + e] : 0.0;
+          const double G = fma(m, gb, ga);
+          if (b + e < B && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+          v[e] = fma(m, base_b + (e ? o1 : o0), base_a + acc[e]) / G;
+        }
+        if (b + 1 < B && !active && (B % 2 == 0)) {
+          *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(v[0], v[1]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = v[e];
+        }
+      }
+    } else if (c_ok) {
+      const int b = b0 + 2 * lc;
+      if (b + 1 < B && !active && (B % 2 == 0)) {
+        *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(base_a + acc[0], base_a + acc[1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = base_a + acc[e];
+      }
     }
   }
 }
@@ -357,12 +375,25 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
                                                         long long n, const unsigned char* __restrict__ active,
                                                         double* __restrict__ f, double* __restrict__ jac,
                                                         unsigned long long* __restrict__ pairs, DeviceStatus* st) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // Work mapping: with B >= 32 a warp is (target, 32-instance chunk) and the
+  // chunk is the slow grid dimension, so concurrently resident warps sweep
+  // spatially adjacent targets (t_order) for the same instances and share
+  // cluster positions in L2; with B < 32 one thread per (target, instance).
+  const long long gidx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nt = s.n_t;
   unsigned long long cnt = 0;
-  if (idx < nt * B) {
-    const long long t = idx / B;
-    const int b = (int)(idx % B);
+  long long tt, bb_;
+  if (B >= 32) {
+    const long long wid = gidx >> 5;
+    tt = wid % nt;
+    bb_ = (wid / nt) * 32 + (gidx & 31);
+  } else {
+    tt = gidx / B;
+    bb_ = gidx % B;
+  }
+  if (tt < nt && bb_ < B) {
+    const long long t = s.t_order ? s.t_order[tt] : tt;
+    const int b = (int)bb_;
     if (!active || active[b]) {
       const double px = xbar[(long long)b * 2 * nt + t], py = xbar[(long long)b * 2 * nt + nt + t];
       const double inv2pi = 1.0 / (2.0 * M_PI);
@@ -843,11 +874,11 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
   const long long btiles = (B + 7) / 8;
   if (s.n_c > 0) {
     if (t) {
-      const long long warps = ((s.n_c + 1) / 2) * btiles;
+      const long long warps = (s.n_c + 1) / 2;
       positions_clusters_mma_kernel<true, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
           s, tt, et, B, d_xhat, d_mu, d_active, w.cx, w.cy, ctx->d_status);
     } else {
-      const long long warps = ((s.n_c + 3) / 4) * btiles;
+      const long long warps = (s.n_c + 3) / 4;
       positions_clusters_mma_kernel<false, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
           s, tt, et, B, d_xhat, d_mu, d_active, w.cx, w.cy, ctx->d_status);
     }
@@ -906,7 +937,8 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
   if (count_pairs) PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
   {
     ProfScope prof(ctx);
-    hyperpair_kernel<<<blocks_for(s.n_t * B, 128), 128, 0, st>>>(s, tt, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg,
+    const long long threads = B >= 32 ? s.n_t * 32 * ((B + 31) / 32) : s.n_t * B;
+    hyperpair_kernel<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg,
                                                                  w.dx, w.dy, w.dg, effective_delta(delta, form), delta,
                                                                  d_inflow, n, d_active, d_f, d_jac, w.pairs,
                                                                  ctx->d_status);

@@ -37,6 +37,7 @@ struct DSurrogate {
   long long* mem_off = nullptr;  // n_c + 1
   long long* mem_ids = nullptr;  // ascending particle ids per cluster
   long long* target_ids = nullptr;
+  int* t_order = nullptr;  // processing order of the targets (spatial; null = identity)
   long long* cl_off = nullptr;  // n_t + 1
   int* cl_list = nullptr;       // cluster indices
   long long* d_off = nullptr;   // n_t + 1
