@@ -1,0 +1,197 @@
+"""Multi-GPU drivers, one process per GPU over torch.distributed.
+
+ShardedFom — the implicit-trapezoidal FOM (integrators.hpp:117-272) with the
+targets split evenly across ranks. Per Newton iteration:
+  * residual on the rank's rows and its squared norm; the G partial norms are
+    all-gathered and summed in rank order on every rank (NCCL's all-reduce is
+    not order-deterministic across G), so every rank takes the same
+    convergence decision (integrators.hpp:140-155);
+  * the Newton update of the rank's rows (2x2 blocks are local: the Jacobian
+    self-blocks need no exchange);
+  * all-gather of the updated source positions (x then y, NVLink/NVSwitch),
+    then the all-pairs velocity of the rank's targets against all sources.
+
+PtromInstanceSplit — μ instances of the PTROM online path split evenly across
+ranks (no communication during the march); reduced states gathered at the end.
+
+The compute backend is pluggable: CudaBackend (libptrom_b200.so through the
+device C ABI) is the product; tests drive the same control logic with a CPU
+backend over gloo.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Even contiguous split of n targets (rank r owns [lo, hi))."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+class CudaBackend:
+    """Per-rank device kernels through the C ABI (ptrom_dev_*)."""
+
+    def __init__(self, gamma: torch.Tensor, delta: float, form: int = 0, inflow: Optional[torch.Tensor] = None):
+        from . import device as dev
+        self.dev = dev
+        self.gamma, self.delta, self.form, self.inflow = gamma, float(delta), int(form), inflow
+        self.device = gamma.device
+
+    def velocity_rows(self, x_full, lo, hi, out):
+        self.dev.pairwise_velocity(x_full, self.gamma, self.delta, self.form, self.inflow, lo, hi, out)
+
+    def newton_blocks(self, x_full, lo, hi, dt, out):
+        self.dev.newton_blocks(x_full, self.gamma, self.delta, self.form, dt, lo, hi, out)
+
+    def residual(self, xi, fxi, xp, fp, dt, r, norm2, m):
+        self.dev.residual(xi, fxi, xp, fp, dt, r, norm2, m, m)
+
+    def newton_update(self, inv, r, x, m):
+        self.dev.newton_update(inv, r, x, m, m)
+
+    def check(self):
+        self.dev.synchronize()
+
+
+@dataclass
+class ShardedResult:
+    snapshots_local: torch.Tensor  # (n_steps, 2m): rank's rows [x_lo..x_hi, y_lo..y_hi] per step
+    iterations: list
+    converged: list
+    relative_residual: list
+    lo: int
+    hi: int
+
+
+class ShardedFom:
+    def __init__(self, n: int, backend, group=None):
+        self.n = n
+        self.backend = backend
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.lo, self.hi = shard_bounds(n, self.rank, self.world)
+        self.m = self.hi - self.lo
+
+    def _gather_positions(self, x_local, x_full):
+        """Local SoA rows → full SoA state on every rank (the per-iteration exchange)."""
+        n, m = self.n, self.m
+        if self.world == 1:
+            x_full.copy_(x_local)
+            return
+        counts = [shard_bounds(n, r, self.world)[1] - shard_bounds(n, r, self.world)[0] for r in range(self.world)]
+        if len(set(counts)) == 1:
+            dist.all_gather_into_tensor(x_full[:n], x_local[:m].contiguous(), group=self.group)
+            dist.all_gather_into_tensor(x_full[n:], x_local[m:].contiguous(), group=self.group)
+        else:  # uneven shards: pad every rank's block to the largest one
+            mx = max(counts)
+            buf = torch.zeros(2 * mx, dtype=x_local.dtype, device=x_local.device)
+            buf[:m] = x_local[:m]
+            buf[mx:mx + m] = x_local[m:]
+            out = torch.empty(self.world * 2 * mx, dtype=x_local.dtype, device=x_local.device)
+            dist.all_gather_into_tensor(out, buf, group=self.group)
+            out = out.view(self.world, 2, mx)
+            x_full[:n].copy_(torch.cat([out[r, 0, :counts[r]] for r in range(self.world)]))
+            x_full[n:].copy_(torch.cat([out[r, 1, :counts[r]] for r in range(self.world)]))
+
+    def _global_norm(self, norm2_local) -> float:
+        """Fixed-order global ‖r‖: all-gather the partials, sum in rank order."""
+        if self.world == 1:
+            return math.sqrt(float(norm2_local.item()))
+        parts = torch.empty(self.world, dtype=torch.float64, device=norm2_local.device)
+        dist.all_gather_into_tensor(parts, norm2_local.reshape(1), group=self.group)
+        total = 0.0
+        for v in parts.cpu().tolist():
+            total += v
+        return math.sqrt(total)
+
+    def simulate(self, x0_full: torch.Tensor, dt: float, n_steps: int, tol: float = 1e-10, max_iters: int = 100,
+                 refresh: int = 1) -> ShardedResult:
+        """integrators.hpp:243-272 over the rank's targets."""
+        if not dt > 0:
+            raise ValueError("time step must be positive")
+        if tol <= 0 or max_iters < 1 or refresh < 1:
+            raise ValueError("invalid Newton configuration")
+        n, m, lo, hi, be = self.n, self.m, self.lo, self.hi, self.backend
+        dev, dtp = x0_full.device, x0_full.dtype
+        x_full = x0_full.clone()
+        x_prev = torch.cat([x0_full[lo:hi], x0_full[n + lo:n + hi]]).contiguous()
+        f_prev = torch.empty(2 * m, dtype=dtp, device=dev)
+        be.velocity_rows(x_full, lo, hi, f_prev)
+        xi = torch.empty_like(x_prev)
+        fxi = torch.empty_like(f_prev)
+        r = torch.empty_like(x_prev)
+        inv = torch.empty((max(m, 1), 4), dtype=dtp, device=dev)
+        norm2 = torch.zeros(1, dtype=torch.float64, device=dev)
+        snaps = torch.empty((n_steps, 2 * m), dtype=dtp, device=dev)
+        iters, conv, rels = [], [], []
+        have_blocks = False
+        x_prev_full = x_full.clone()
+        for s in range(n_steps):
+            xi.copy_(x_prev)
+            fxi.copy_(f_prev)
+            x_full.copy_(x_prev_full)
+            refresh_due = (s % refresh) == 0 or not have_blocks
+            refreshed = False
+            updates, converged, r0, rel = 0, False, 0.0, 0.0
+            while True:
+                be.residual(xi, fxi, x_prev, f_prev, dt, r, norm2, m)
+                nr = self._global_norm(norm2)
+                if updates == 0:
+                    r0 = nr
+                    if r0 == 0.0:
+                        converged, rel = True, 0.0
+                        break
+                rel = nr / r0
+                if rel <= tol:
+                    converged = True
+                    break
+                if updates >= max_iters:
+                    break
+                if refresh_due and not refreshed:
+                    be.newton_blocks(x_full, lo, hi, dt, inv)
+                    refreshed = have_blocks = True
+                be.newton_update(inv, r, xi, m)
+                updates += 1
+                self._gather_positions(xi, x_full)
+                be.velocity_rows(x_full, lo, hi, fxi)
+            x_prev, xi = xi, x_prev
+            f_prev, fxi = fxi, f_prev
+            x_prev_full.copy_(x_full)
+            snaps[s].copy_(x_prev)
+            iters.append(updates)
+            conv.append(int(converged))
+            rels.append(rel)
+        be.check()
+        return ShardedResult(snaps, iters, conv, rels, lo, hi)
+
+
+class PtromInstanceSplit:
+    """μ instances split evenly across ranks; x̂ gathered on every rank."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def local_slice(self, n_inst: int) -> tuple[int, int]:
+        return shard_bounds(n_inst, self.rank, self.world)
+
+    def gather(self, local: torch.Tensor, n_inst: int) -> torch.Tensor:
+        """Concatenate per-rank instance blocks (leading dimension) in rank order."""
+        if self.world == 1:
+            return local
+        counts = [shard_bounds(n_inst, r, self.world)[1] - shard_bounds(n_inst, r, self.world)[0]
+                  for r in range(self.world)]
+        tail = tuple(local.shape[1:])
+        mx = max(counts)
+        buf = torch.zeros((mx,) + tail, dtype=local.dtype, device=local.device)
+        buf[:local.shape[0]] = local
+        out = torch.empty((self.world * mx,) + tail, dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(out, buf, group=self.group)
+        return torch.cat([out[r * mx:r * mx + counts[r]] for r in range(self.world)])

@@ -1,0 +1,150 @@
+"""Multi-rank control logic of the sharded drivers (paper_2103_01983_b200/
+sharded.py) on CPU with gloo, world sizes 2 and 3 (uneven shards). The
+per-rank compute is a CPU test backend over the oracle; on GPUs the same
+driver runs CudaBackend (NCCL). The sharded trajectory must match the
+single-process oracle FOM within 1e-12."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _run(world, target, args, timeout=240):
+    """Spawn `world` gloo ranks; return what rank 0 puts on the queue."""
+    import queue
+    import time
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
+    for p in procs:
+        p.start()
+    t0 = time.time()
+    result = None
+    while time.time() - t0 < timeout:
+        try:
+            result = q.get(timeout=1.0)
+            break
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    assert result is not None, [p.exitcode for p in procs]
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    return result
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class OracleBackend:
+    """CPU backend with the ShardedFom backend interface (test only)."""
+
+    def __init__(self, oracle, gamma, delta, form=0, inflow=None):
+        self.o, self.gamma, self.delta, self.form, self.inflow = oracle, gamma, delta, form, inflow
+        self.n = len(gamma)
+
+    def velocity_rows(self, x_full, lo, hi, out):
+        n, m = self.n, hi - lo
+        f = self.o.pairwise_velocity(x_full.numpy(), self.gamma, self.delta, self.form, self.inflow, lo, hi)
+        out[:m] = torch.from_numpy(f[lo:hi])
+        out[m:] = torch.from_numpy(f[n + lo:n + hi])
+
+    def newton_blocks(self, x_full, lo, hi, dt, out):
+        j = self.o.inexact_kernel_jacobian(x_full.numpy(), self.gamma, self.delta, self.form, lo, hi)[:, lo:hi]
+        h = dt / 2.0
+        b00, b01, b10, b11 = 1.0 - h * j[0], 0.0 - h * j[1], 0.0 - h * j[2], 1.0 - h * j[3]
+        det = b00 * b11 - b01 * b10
+        out[:, 0] = torch.from_numpy(b11 / det)
+        out[:, 1] = torch.from_numpy(-b01 / det)
+        out[:, 2] = torch.from_numpy(-b10 / det)
+        out[:, 3] = torch.from_numpy(b00 / det)
+
+    def residual(self, xi, fxi, xp, fp, dt, r, norm2, m):
+        r.copy_((xi - xp) - (dt / 2.0) * (fxi + fp))
+        norm2[0] = float(np.sum(r.numpy() ** 2))
+
+    def newton_update(self, inv, r, x, m):
+        r0, r1 = -r[:m], -r[m:]
+        x[:m] += inv[:, 0] * r0 + inv[:, 1] * r1
+        x[m:] += inv[:, 2] * r0 + inv[:, 3] * r1
+
+    def check(self):
+        pass
+
+
+def _fom_worker(rank, world, port, n, steps, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import pyoracle
+        from paper_2103_01983_b200 import workloads
+        from paper_2103_01983_b200.sharded import ShardedFom
+        w = workloads.config1(n=n)
+        fom = ShardedFom(n, OracleBackend(pyoracle, w.gamma, w.delta))
+        res = fom.simulate(torch.tensor(w.x0), w.dt, steps)
+        parts = [None] * world
+        dist.all_gather_object(parts, (res.lo, res.hi, res.snapshots_local.numpy(), res.iterations))
+        if rank == 0:
+            out_q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 64), (3, 50)])
+def test_sharded_fom_matches_single_process_oracle(oracle, world, n):
+    from paper_2103_01983_b200 import workloads
+    steps = 4
+    parts = _run(world, _fom_worker, (n, steps))
+    w = workloads.config1(n=n)
+    snaps, iters, _, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps)
+    full = np.zeros((steps, 2 * n))
+    for lo, hi, loc, its in parts:
+        m = hi - lo
+        full[:, lo:hi] = loc[:, :m]
+        full[:, n + lo:n + hi] = loc[:, m:]
+        assert list(its) == list(iters)
+    for s in range(steps):
+        assert np.linalg.norm(full[s] - snaps[:, s]) / np.linalg.norm(snaps[:, s]) <= 1e-12
+
+
+def _split_worker(rank, world, port, n_inst, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_01983_b200.sharded import PtromInstanceSplit
+        sp = PtromInstanceSplit()
+        lo, hi = sp.local_slice(n_inst)
+        local = torch.arange(lo, hi, dtype=torch.float64).reshape(-1, 1).repeat(1, 3) * 10.0 + rank * 0
+        full = sp.gather(local, n_inst)
+        if rank == 0:
+            out_q.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_inst", [(2, 8), (3, 10)])
+def test_ptrom_instance_split_gathers_in_order(world, n_inst):
+    full = _run(world, _split_worker, (n_inst,))
+    np.testing.assert_array_equal(full[:, 0], np.arange(n_inst) * 10.0)
+
+
+def test_shard_bounds_cover_everything():
+    from paper_2103_01983_b200.sharded import shard_bounds
+    for n in (1, 7, 64, 4194304):
+        for g in (1, 2, 3, 8):
+            b = [shard_bounds(n, r, g) for r in range(g)]
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(g - 1))
