@@ -78,6 +78,18 @@ int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const do
                            int form, const double* inflow, double dt, int64_t n_steps, double tol,
                            int max_iters, int jacobian_refresh_period, double* snapshots, int* iterations,
                            uint8_t* converged, double* relative_residual, uint64_t* n_pair_evals);
+/* kernel.hpp:174-191 hamiltonian<double>: Σ_{i<j} Γi Γj log|x_i - x_j| / 2π.
+ * A coincident pair is status 3 "hamiltonian: coincident particles i and j"
+ * (the lexicographically first pair, as the reference's loop order). */
+int ptrom_hamiltonian_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double* out);
+/* kernel.hpp:213-238 velocity_field_grid<double> with LatticeSpec
+ * kernel.hpp:194-208 passed as (x_min, x_max, nx, y_min, y_max, ny): grid is
+ * ny x nx column-major, grid[j + i*ny] = |f(x_i, y_j)| * c_g * l / gamma_bar.
+ * n_pair_evals = nx*ny*n (the reference's kernel_pair counter). */
+int ptrom_velocity_field_grid_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma,
+                                  double delta, int form, double x_min, double x_max, int64_t nx,
+                                  double y_min, double y_max, int64_t ny, double c_g, double l,
+                                  double gamma_bar, double* grid, uint64_t* n_pair_evals);
 
 /* --------------------------------------------- all-pairs (device buffers) -- */
 /* Velocity of targets [t_begin, t_end) against all n sources (j != i):
@@ -95,6 +107,14 @@ int ptrom_dev_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const doubl
                                           const double* d_gamma, double delta, int form, int64_t t_begin,
                                           int64_t t_end, double* d_jxx, double* d_jxy, double* d_jyx,
                                           double* d_jyy);
+/* Device-buffer hamiltonian: d_out is one double (stream-ordered). */
+int ptrom_dev_hamiltonian_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                              double* d_out);
+/* Device-buffer velocity_field_grid: d_grid is ny*nx doubles. */
+int ptrom_dev_velocity_field_grid_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                      double delta, int form, double x_min, double x_max, int64_t nx,
+                                      double y_min, double y_max, int64_t ny, double c_g, double l,
+                                      double gamma_bar, double* d_grid);
 /* Newton-block refactor fused with the Jacobian (integrators.hpp:181-194):
  * inv = (I - dt/2 J_i)^{-1} for rows [t_begin,t_end), row-major 4 per particle.
  * A singular block latches status 3 "singular Newton block for particle i". */

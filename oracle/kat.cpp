@@ -287,6 +287,49 @@ TEST_CASE("test_kernel.cpp:248 hamiltonian two-particle value") {
   CHECK(approx(hamiltonian<double>(Vec{0.0, e, 0.0, 0.0}, sys), 1.0 / (2.0 * M_PI), 1e-14));
 }
 
+TEST_CASE("test_kernel.cpp:257 hamiltonian brute-force and translation invariance") {
+  std::mt19937_64 rng(23);
+  const Index n = 6;
+  const auto sys = random_system(rng, n, 0.0);
+  const Vec x = random_state(rng, n);
+  double ref = 0.0;
+  for (Index j = 0; j < n; ++j)
+    for (Index i = 0; i < n; ++i) {
+      if (i == j) continue;
+      ref += sys.circulation[j] * sys.circulation[i] * std::log(std::hypot(x[i] - x[j], x[i + n] - x[j + n]));
+    }
+  ref /= 4.0 * M_PI;
+  const double h = hamiltonian<double>(x, sys);
+  CHECK(approx(h, ref, 1e-13));
+  Vec shifted = x;
+  for (Index i = 0; i < n; ++i) {
+    shifted[i] += 3.25;
+    shifted[i + n] -= 1.5;
+  }
+  CHECK(approx(hamiltonian<double>(shifted, sys), h, 1e-12));
+  Vec coincident = x;
+  coincident[1] = coincident[0];
+  coincident[1 + n] = coincident[n];
+  CHECK_THROWS_AS((void)hamiltonian<double>(coincident, sys), numerical_error);
+}
+
+TEST_CASE("test_kernel.cpp:287 velocity_field_grid single vortex") {
+  ParticleSystem<double> sys;
+  sys.circulation = {2.0 * M_PI};
+  sys.delta = 0.0;
+  const Vec x{0.0, 0.0};
+  const LatticeSpec<double> lattice{-1.0, 1.0, 2, 0.0, 1.0, 2};
+  const double c_g = 1.25, l = 2.0, gamma_bar = 4.0;
+  const Vec grid = velocity_field_grid<double>(x, sys, lattice, c_g, l, gamma_bar);
+  CHECK(grid.size() == 4);
+  CHECK(approx(grid[0 + 0 * 2], c_g * l / gamma_bar, 1e-13));
+  CHECK(approx(grid[0 + 1 * 2], c_g * l / gamma_bar, 1e-13));
+  CHECK(approx(grid[1 + 0 * 2], c_g * l / gamma_bar / std::sqrt(2.0), 1e-13));
+  CHECK_THROWS_AS((void)velocity_field_grid<double>(x, sys, lattice, c_g, l, 0.0), config_error);
+  const LatticeSpec<double> touching{-1.0, 1.0, 3, -1.0, 1.0, 3};
+  CHECK_THROWS_AS((void)velocity_field_grid<double>(x, sys, touching, c_g, l, gamma_bar), numerical_error);
+}
+
 TEST_CASE("test_kernel.cpp:312 kernel evaluation counter") {
   kernel_eval_counter = 0;
   ParticleSystem<double> sys;

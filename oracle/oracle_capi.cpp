@@ -205,6 +205,18 @@ int oracle_hamiltonian_f64(std::int64_t n, const double* x, const double* gamma,
   });
 }
 
+int oracle_velocity_field_grid_f64(std::int64_t n, const double* x, const double* gamma, double delta, int form,
+                                   double x_min, double x_max, std::int64_t nx, double y_min, double y_max,
+                                   std::int64_t ny, double c_g, double l, double gamma_bar, double* grid) {
+  return guarded([&] {
+    auto sys = make_sys<double>(n, gamma, delta, form, nullptr);
+    std::vector<double> xs(x, x + 2 * n);
+    const LatticeSpec<double> lat{x_min, x_max, nx, y_min, y_max, ny};
+    const auto g = velocity_field_grid<double>(xs, sys, lat, c_g, l, gamma_bar);
+    std::memcpy(grid, g.data(), sizeof(double) * g.size());
+  });
+}
+
 // integrators.hpp:243-272 with the PairwiseModel (optionally target-threaded).
 int oracle_fom_simulate_f64(std::int64_t n, const double* x0, const double* gamma, double delta, int form,
                             const double* inflow, double dt, std::int64_t n_steps, double tol, int max_iters,

@@ -236,6 +236,51 @@ inline S hamiltonian(const std::vector<S>& state, const ParticleSystem<S>& sys) 
   return acc / (S(2) * S(kPiL));
 }
 
+// kernel.hpp:195-208 — rectangular evaluation lattice.
+template <class S>
+struct LatticeSpec {
+  S x_min, x_max;
+  Index nx;
+  S y_min, y_max;
+  Index ny;
+  void validate() const {
+    if (nx < 2 || ny < 2) throw config_error("lattice needs at least 2 points per axis");
+    if (!(x_max > x_min) || !(y_max > y_min)) throw config_error("degenerate lattice extents");
+  }
+  S x_at(Index i) const { return x_min + (x_max - x_min) * S(i) / S(nx - 1); }
+  S y_at(Index j) const { return y_min + (y_max - y_min) * S(j) / S(ny - 1); }
+};
+
+// kernel.hpp:213-238 — |f| * c_g * l / gamma_bar at every lattice vertex;
+// grid is ny x nx column-major (entry (j, i) at j + i * ny).
+template <class S>
+inline std::vector<S> velocity_field_grid(const std::vector<S>& state, const ParticleSystem<S>& sys,
+                                          const LatticeSpec<S>& lattice, S c_g, S l, S gamma_bar) {
+  sys.validate();
+  check_state<S>(state, sys, "velocity_field_grid");
+  lattice.validate();
+  if (!(gamma_bar > S(0))) throw config_error("velocity_field_grid: gamma_bar must be positive");
+  if (!(c_g > S(0)) || !(l > S(0)))
+    throw config_error("velocity_field_grid: characteristic length must be positive");
+  const Index n = sys.size();
+  const S scale = c_g * l / gamma_bar;
+  std::vector<S> grid(static_cast<size_t>(lattice.ny * lattice.nx));
+  for (Index j = 0; j < lattice.ny; ++j) {
+    for (Index i = 0; i < lattice.nx; ++i) {
+      const V2<S> vertex{lattice.x_at(i), lattice.y_at(j)};
+      S fx = S(0), fy = S(0);
+      for (Index p = 0; p < n; ++p) {
+        const V2<S> k = kernel_pair<S>(vertex, V2<S>{state[p], state[p + n]}, sys.circulation[p], sys.delta,
+                                       sys.kernel_form);
+        fx += k.x;
+        fy += k.y;
+      }
+      grid[j + i * lattice.ny] = std::sqrt(fx * fx + fy * fy) * scale;
+    }
+  }
+  return grid;
+}
+
 // Plain ascending Euclidean norm, standing in for Eigen's VectorX::norm()
 // (integrators.hpp:141, rom.hpp:313).
 template <class S>

@@ -91,6 +91,25 @@ def inexact_kernel_jacobian(x, gamma, delta, form=0, t_begin=0, t_end=None, thre
     return out
 
 
+def hamiltonian(x, gamma):
+    """kernel.hpp:174-191."""
+    x, g = _f64(x), _f64(gamma)
+    out = C.c_double()
+    _check(lib().oracle_hamiltonian_f64(C.c_int64(g.shape[0]), _p(x), _p(g), C.byref(out)))
+    return out.value
+
+
+def velocity_field_grid(x, gamma, delta, form, x_min, x_max, nx, y_min, y_max, ny, c_g, l, gamma_bar):
+    """kernel.hpp:213-238 → (ny, nx) array."""
+    x, g = _f64(x), _f64(gamma)
+    grid = np.zeros(nx * ny)
+    d = C.c_double
+    _check(lib().oracle_velocity_field_grid_f64(C.c_int64(g.shape[0]), _p(x), _p(g), d(delta), C.c_int(form),
+                                                d(x_min), d(x_max), C.c_int64(nx), d(y_min), d(y_max),
+                                                C.c_int64(ny), d(c_g), d(l), d(gamma_bar), _p(grid)))
+    return grid.reshape(nx, ny).T
+
+
 def fom_simulate(x0, gamma, delta, dt, n_steps, form=0, inflow=None, tol=1e-10, max_iters=100, refresh=1,
                  threads=1):
     """integrators.hpp:243-272 → (snapshots (2N, steps), iterations, converged, relative_residual)."""

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     Context,
     CudaError,
     KernelForm,
+    LatticeSpec,
     NewtonConfig,
     NumericalError,
     PairwiseModel,
@@ -20,9 +21,11 @@ from .api import (  # noqa: F401
     TimeGrid,
     default_context,
     fom_simulate,
+    hamiltonian,
     inexact_kernel_jacobian,
     kernel_eval_count,
     pairwise_velocity,
     reset_kernel_eval_count,
+    velocity_field_grid,
 )
 from ._lib import LIB_PATH, load as load_library  # noqa: F401

@@ -39,6 +39,14 @@ PROTOTYPES = {
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, c_i64, c_i64, c_dp, c_i64]),
     "ptrom_dev_pairwise_velocity_f32": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_float, C.c_int, c_dp, c_i64, c_i64, c_dp, c_i64]),
+    "ptrom_hamiltonian_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, c_dp]),
+    "ptrom_velocity_field_grid_f64": (
+        C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_double, C.c_double, c_i64, C.c_double,
+                  C.c_double, c_i64, C.c_double, C.c_double, C.c_double, c_dp, c_u64p]),
+    "ptrom_dev_hamiltonian_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, c_dp]),
+    "ptrom_dev_velocity_field_grid_f64": (
+        C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_double, C.c_double, c_i64, C.c_double,
+                  C.c_double, c_i64, C.c_double, C.c_double, C.c_double, c_dp]),
     "ptrom_dev_inexact_kernel_jacobian_f64": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp]),
     "ptrom_dev_newton_blocks_f64": (

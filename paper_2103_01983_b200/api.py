@@ -187,6 +187,55 @@ def inexact_kernel_jacobian(state, sys: ParticleSystem, ctx: Optional[Context] =
     return BlockDiagonalJacobian(*out)
 
 
+def hamiltonian(state, sys: ParticleSystem, ctx: Optional[Context] = None) -> float:
+    """kernel.hpp:174-191 — Kirchhoff–Routh energy Σ_{i<j} Γi Γj log|r_ij| / 2π."""
+    ctx = ctx or default_context()
+    x = _as(state, np.float64)
+    g = _as(sys.circulation, np.float64)
+    n = g.shape[0]
+    if x.shape[0] != 2 * n:
+        raise ConfigError(f"hamiltonian: state dimension {x.shape[0]} does not match particle count {n}")
+    out = C.c_double()
+    ctx.check(ctx.lib.ptrom_hamiltonian_f64(ctx.handle, n, _p(x), _p(g), C.byref(out)))
+    return out.value
+
+
+@dataclass
+class LatticeSpec:  # kernel.hpp:194-208
+    x_min: float
+    x_max: float
+    nx: int
+    y_min: float
+    y_max: float
+    ny: int
+
+    def x_at(self, i: int) -> float:
+        return self.x_min + (self.x_max - self.x_min) * float(i) / float(self.nx - 1)
+
+    def y_at(self, j: int) -> float:
+        return self.y_min + (self.y_max - self.y_min) * float(j) / float(self.ny - 1)
+
+
+def velocity_field_grid(state, sys: ParticleSystem, lattice: LatticeSpec, c_g: float, l: float, gamma_bar: float,
+                        ctx: Optional[Context] = None) -> np.ndarray:
+    """kernel.hpp:213-238 — (ny, nx) array, entry (j, i) = |f(x_i, y_j)|·c_g·l/Γ̄."""
+    ctx = ctx or default_context()
+    x = _as(state, np.float64)
+    g = _as(sys.circulation, np.float64)
+    n = g.shape[0]
+    if x.shape[0] != 2 * n:
+        raise ConfigError(f"velocity_field_grid: state dimension {x.shape[0]} does not match particle count {n}")
+    nx, ny = int(lattice.nx), int(lattice.ny)
+    grid = np.empty(max(nx, 0) * max(ny, 0), dtype=np.float64)
+    cnt = C.c_uint64()
+    ctx.check(ctx.lib.ptrom_velocity_field_grid_f64(
+        ctx.handle, n, _p(x), _p(g), float(sys.delta), int(sys.kernel_form), float(lattice.x_min),
+        float(lattice.x_max), nx, float(lattice.y_min), float(lattice.y_max), ny, float(c_g), float(l),
+        float(gamma_bar), _p(grid) if grid.size else None, C.byref(cnt)))
+    _bump(cnt.value)
+    return grid.reshape(nx, ny).T  # column-major (ny x nx) → [j, i]
+
+
 @dataclass
 class TimeGrid:  # integrators.hpp:15-23
     dt: float

@@ -187,7 +187,12 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
                                                            const double* __restrict__ ys,
                                                            const double* __restrict__ gam, double inv2pi,
                                                            double dp, long long t_begin, long long t_count,
-                                                           long long chunk_len, double* __restrict__ part) {
+                                                           long long chunk_len, double* __restrict__ part,
+                                                           const double* __restrict__ txs,
+                                                           const double* __restrict__ tys, int self_excl) {
+  // Targets are rows of (txs, tys); self_excl = targets are the sources
+  // themselves (txs == xs), so pair (i, i) is skipped. External targets
+  // (lattice vertices, kernel.hpp:213-238) pass self_excl = 0.
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   __shared__ double2 sp[TPB];
   __shared__ double sg[TPB];
@@ -201,8 +206,8 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
     const long long i = tile0 + k * TPB + tid;
     const bool ok = i < t_begin + t_count;
     ti[k] = ok ? i : -1;
-    tx[k] = ok ? xs[i] : 0.0;
-    ty[k] = ok ? ys[i] : 0.0;
+    tx[k] = ok ? txs[i] : 0.0;
+    ty[k] = ok ? tys[i] : 0.0;
     fx[k] = fy[k] = ja[k] = jb[k] = jc[k] = 0.0;
   }
   const long long tile_end = min(tile0 + (long long)TPB * T, t_begin + t_count);
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
       py = ys[jn];
       pg = gam[jn] * inv2pi;
     }
-    const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt);
+    const bool masked = self_excl && (j0 < tile_end) && (tile0 < j0 + cnt);
     if (masked)
       tile_f64<T, UNR, VEL, JAC, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else if (fast4)
@@ -482,7 +487,8 @@ int reduce_grid(ptrom_ctx* ctx, long long count) {
 
 template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC>
 void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
-                           long long t_begin, long long t_count, double** part_out, int* chunks_out) {
+                           long long t_begin, long long t_count, double** part_out, int* chunks_out,
+                           const double* tx, const double* ty) {
   auto kern = allpairs_f64_kernel<TPB, T, UNR, MINB, VEL, JAC>;
   static int occ = resident_blocks(kern, TPB);
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
@@ -496,7 +502,9 @@ void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const d
   const double inv2pi = 1.0 / (2.0 * M_PI);
   {
     ProfScope prof(ctx);
-    kern<<<grid, TPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part);
+    const bool external = tx != nullptr;
+    kern<<<grid, TPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part,
+                                        external ? tx : x, external ? ty : x + n, external ? 0 : 1);
   }
   PTROM_LAUNCH_CHECK();
   *part_out = part;
@@ -504,7 +512,7 @@ void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const d
 }
 
 using LaunchFn = void (*)(ptrom_ctx*, long long, const double*, const double*, double, long long, long long,
-                          double**, int*);
+                          double**, int*, const double*, const double*);
 
 // Velocity-kernel shapes (TPB, targets/thread, source unroll, min blocks/SM);
 // entry 0 is the default, the rest are kept for tools/tune_allpairs.py
@@ -526,14 +534,44 @@ constexpr int kNumVelVariants = sizeof(kVelVariants) / sizeof(kVelVariants[0]);
 // keep several targets per thread in registers to amortize the shared loads.
 template <bool VEL, bool JAC>
 void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
-                         long long t_begin, long long t_count, double** part, int* chunks) {
+                         long long t_begin, long long t_count, double** part, int* chunks,
+                         const double* tx = nullptr, const double* ty = nullptr) {
   if (t_count < 16384) {
-    launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+    launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
   } else if (VEL && !JAC) {
     const int v = (ctx->allpairs_variant >= 0 && ctx->allpairs_variant < kNumVelVariants) ? ctx->allpairs_variant : 0;
-    kVelVariants[v](ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+    kVelVariants[v](ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
   } else {
-    launch_allpairs_f64_t<kTPB, 4, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks);
+    launch_allpairs_f64_t<kTPB, 4, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
+  }
+}
+
+// Lattice speeds (kernel.hpp:213-238): |Σ_p kernel_pair(vertex, p)|·scale per
+// vertex; grid column-major ny x nx (vertex t = i·ny + j).
+__global__ void lattice_vertices_kernel(double x_min, double x_max, long long nx, double y_min, double y_max,
+                                        long long ny, double* __restrict__ vx, double* __restrict__ vy) {
+  const long long count = nx * ny;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / ny, j = t - i * ny;
+    // LatticeSpec::x_at / y_at (kernel.hpp:205-206), reference rounding order
+    vx[t] = __dadd_rn(x_min, __ddiv_rn(__dmul_rn(__dsub_rn(x_max, x_min), (double)i), (double)(nx - 1)));
+    vy[t] = __dadd_rn(y_min, __ddiv_rn(__dmul_rn(__dsub_rn(y_max, y_min), (double)j), (double)(ny - 1)));
+  }
+}
+
+__global__ void lattice_speed_kernel(long long count, int n_chunks, const double* __restrict__ part, double scale,
+                                     double* __restrict__ grid, DeviceStatus* st) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count;
+       t += (long long)gridDim.x * blockDim.x) {
+    double fx = 0.0, fy = 0.0;
+    for (int c = 0; c < n_chunks; ++c) {
+      fx += part[((long long)c * 2 + 0) * count + t];
+      fy += part[((long long)c * 2 + 1) * count + t];
+    }
+    const double speed = __dmul_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(fx, fx), __dmul_rn(fy, fy))), scale);
+    if (!isfinite(speed)) latch_status(st, kStatusNonFiniteVelocity, t);
+    grid[t] = speed;
   }
 }
 
@@ -551,6 +589,137 @@ void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double
   reduce_velocity_f64_kernel<<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
       n, t_begin, t_count, chunks, part, 2, inflow, f, ld, ctx->d_status);
   PTROM_LAUNCH_CHECK();
+}
+
+// Kirchhoff–Routh energy (kernel.hpp:174-191): H = Σ_{i<j} Γi Γj log|r_ij| / 2π.
+// Blocks own TPB·T targets i and a source chunk; only pairs j > i are
+// evaluated (blocks and tiles entirely at or below the diagonal skip). Each
+// target accumulates Σ_j Γj·log(d²) in its registers (log|r| = ½ log d²,
+// within one ulp of the reference's log(sqrt(d²))); the fixed-order reduce
+// below multiplies by Γi and sums targets in a fixed tree, so the result is
+// bit-reproducible. d² == 0 latches the lexicographically first pair
+// (encoded i·n + j), the reference's throw at kernel.hpp:185-187.
+template <int TPB, int T>
+__global__ void __launch_bounds__(TPB) hamiltonian_f64_kernel(long long n, const double* __restrict__ xs,
+                                                              const double* __restrict__ ys,
+                                                              const double* __restrict__ gam, long long chunk_len,
+                                                              double* __restrict__ part, DeviceStatus* st) {
+  __shared__ double2 sp[TPB];
+  __shared__ double sg[TPB];
+  const int tid = threadIdx.x;
+  const long long tile0 = (long long)blockIdx.x * (TPB * T);
+  const long long tile_end = min(tile0 + (long long)TPB * T, n);
+  double tx[T], ty[T], acc[T];
+  long long ti[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const long long i = tile0 + k * TPB + tid;
+    ti[k] = i < n ? i : LLONG_MAX;  // out-of-range rows never see j > i
+    tx[k] = i < n ? xs[i] : 0.0;
+    ty[k] = i < n ? ys[i] : 0.0;
+    acc[k] = 0.0;
+  }
+  const long long cbeg = max((long long)blockIdx.y * chunk_len, tile0 + 1);
+  const long long cend = min(n, (long long)(blockIdx.y + 1) * chunk_len);
+  for (long long j0 = cbeg; j0 < cend; j0 += TPB) {
+    const int cnt = (int)min((long long)TPB, cend - j0);
+    if (tid < cnt) {
+      sp[tid] = make_double2(xs[j0 + tid], ys[j0 + tid]);
+      sg[tid] = gam[j0 + tid];
+    }
+    __syncthreads();
+    const bool full = j0 >= tile_end;  // every source above every target of the block
+    for (int jj = 0; jj < cnt; ++jj) {
+      const double2 p = sp[jj];
+      const double g = sg[jj];
+      const long long j = j0 + jj;
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        const double rx = __dsub_rn(tx[k], p.x), ry = __dsub_rn(ty[k], p.y);
+        double d2 = __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry));
+        const bool use = full || j > ti[k];
+        if (use && d2 == 0.0) latch_status(st, kStatusCoincidentPair, ti[k] * n + j);
+        d2 = use ? d2 : 1.0;
+        acc[k] = fma(use ? g : 0.0, log(d2), acc[k]);
+      }
+    }
+    __syncthreads();
+  }
+  double* out = part + (long long)blockIdx.y * n;
+#pragma unroll
+  for (int k = 0; k < T; ++k)
+    if (ti[k] < n) out[ti[k]] = acc[k];
+}
+
+constexpr int kHamBlocks = 296;
+
+__global__ void hamiltonian_reduce_kernel(long long n, int n_chunks, const double* __restrict__ part,
+                                          const double* __restrict__ gam, double* __restrict__ block_sums) {
+  __shared__ double red[kReduceThreads];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int c = 0; c < n_chunks; ++c) a += part[(long long)c * n + i];
+    s = fma(gam[i], a, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kReduceThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = red[0];
+}
+
+__global__ void hamiltonian_finish_kernel(int nb, const double* __restrict__ block_sums, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += block_sums[b];
+  out[0] = 0.5 * s / (2.0 * M_PI);
+}
+
+void dev_hamiltonian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double* out) {
+  constexpr int TPB = 128, T = 2;
+  auto kern = hamiltonian_f64_kernel<TPB, T>;
+  static int occ = resident_blocks(kern, TPB);
+  const long long tiles = (n + TPB * T - 1) / (TPB * T);
+  // About half of the (tile, chunk) blocks sit below the diagonal and exit at once.
+  const int chunks = choose_source_chunks(ctx, (tiles + 1) / 2, n, occ, 2 * TPB);
+  const long long chunk_len = (n + chunks - 1) / chunks;
+  ctx->scratch.reset();
+  ctx->scratch.reserve(((size_t)chunks * n + kHamBlocks) * sizeof(double) + 4096);
+  double* part = ctx->scratch.take<double>((size_t)chunks * n);
+  double* bs = ctx->scratch.take<double>(kHamBlocks);
+  PTROM_CUDA(cudaMemsetAsync(part, 0, (size_t)chunks * n * sizeof(double), ctx->stream));
+  ctx->status_pair_n = n;
+  {
+    ProfScope prof(ctx);
+    kern<<<dim3((unsigned)tiles, (unsigned)chunks), TPB, 0, ctx->stream>>>(n, x, x + n, gamma, chunk_len, part,
+                                                                           ctx->d_status);
+  }
+  PTROM_LAUNCH_CHECK();
+  hamiltonian_reduce_kernel<<<kHamBlocks, kReduceThreads, 0, ctx->stream>>>(n, chunks, part, gamma, bs);
+  hamiltonian_finish_kernel<<<1, 32, 0, ctx->stream>>>(kHamBlocks, bs, out);
+  PTROM_LAUNCH_CHECK();
+}
+
+void dev_velocity_field_grid_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta,
+                                 int form, double x_min, double x_max, long long nx, double y_min, double y_max,
+                                 long long ny, double scale, double* grid) {
+  const long long count = nx * ny;
+  double* vx;
+  PTROM_CUDA(cudaMallocAsync(&vx, 2 * count * sizeof(double), ctx->stream));
+  double* vy = vx + count;
+  lattice_vertices_kernel<<<reduce_grid(ctx, count), kReduceThreads, 0, ctx->stream>>>(x_min, x_max, nx, y_min,
+                                                                                         y_max, ny, vx, vy);
+  PTROM_LAUNCH_CHECK();
+  double* part;
+  int chunks;
+  launch_allpairs_f64<true, false>(ctx, n, x, gamma, effective_delta(delta, form), 0, count, &part, &chunks, vx, vy);
+  lattice_speed_kernel<<<reduce_grid(ctx, count), kReduceThreads, 0, ctx->stream>>>(count, chunks, part, scale, grid,
+                                                                                     ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+  PTROM_CUDA(cudaFreeAsync(vx, ctx->stream));
 }
 
 void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,

@@ -26,6 +26,11 @@ void check_device_status(ptrom_ctx* ctx) {
     case kStatusZeroClusterCirculation:
       numerical_fail("affine circulation batch: cluster " + std::to_string(st.index) +
                      " has zero net circulation for some mu (use the per-instance ptrom_simulate)");
+    case kStatusCoincidentPair: {  // kernel.hpp:185-187
+      const long long pn = std::max(1LL, ctx->status_pair_n);
+      numerical_fail("hamiltonian: coincident particles " + std::to_string(st.index / pn) + " and " +
+                     std::to_string(st.index % pn));
+    }
     case kStatusNonFiniteJacobian:  // kernel.hpp:55-56 / 64-65
       numerical_fail("kernel_pair_jacobian: coincident target/source with zero desingularization (target " +
                      std::to_string(st.index) + ")");
@@ -249,7 +254,74 @@ int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const do
   });
 }
 
+// kernel.hpp:174-191
+int ptrom_hamiltonian_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double* out) {
+  return guarded(ctx, [&] {
+    validate_system<double>(n, x, gamma, 0.0, PTROM_FORM_STANDARD, nullptr, "hamiltonian");
+    ctx->io.reset();
+    ctx->io.reserve(sizeof(double) * (size_t)(3 * n + 1) + 4096);
+    double* dx = stage_in(ctx, x, 2 * n);
+    double* dg = stage_in(ctx, gamma, n);
+    double* dh = ctx->io.take<double>(1);
+    dev_hamiltonian_f64(ctx, n, dx, dg, dh);
+    PTROM_CUDA(cudaMemcpyAsync(out, dh, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+  });
+}
+
+namespace {
+// kernel.hpp:200-203 LatticeSpec::validate + kernel.hpp:219-222
+double lattice_scale(int64_t nx, int64_t ny, double x_min, double x_max, double y_min, double y_max, double c_g,
+                     double l, double gamma_bar) {
+  if (nx < 2 || ny < 2) config_fail("lattice needs at least 2 points per axis");
+  if (!(x_max > x_min) || !(y_max > y_min)) config_fail("degenerate lattice extents");
+  if (!(gamma_bar > 0)) config_fail("velocity_field_grid: gamma_bar must be positive");
+  if (!(c_g > 0) || !(l > 0)) config_fail("velocity_field_grid: characteristic length must be positive");
+  return c_g * l / gamma_bar;
+}
+}  // namespace
+
+// kernel.hpp:213-238; grid is ny x nx column-major (entry (j, i) at j + i*ny).
+int ptrom_velocity_field_grid_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
+                                  int form, double x_min, double x_max, int64_t nx, double y_min, double y_max,
+                                  int64_t ny, double c_g, double l, double gamma_bar, double* grid,
+                                  uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    validate_system<double>(n, x, gamma, delta, form, nullptr, "velocity_field_grid");
+    const double scale = lattice_scale(nx, ny, x_min, x_max, y_min, y_max, c_g, l, gamma_bar);
+    ctx->io.reset();
+    ctx->io.reserve(sizeof(double) * (size_t)(3 * n + nx * ny) + 4096);
+    double* dx = stage_in(ctx, x, 2 * n);
+    double* dg = stage_in(ctx, gamma, n);
+    double* dgrid = ctx->io.take<double>((size_t)(nx * ny));
+    dev_velocity_field_grid_f64(ctx, n, dx, dg, delta, form, x_min, x_max, nx, y_min, y_max, ny, scale, dgrid);
+    PTROM_CUDA(cudaMemcpyAsync(grid, dgrid, sizeof(double) * nx * ny, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+    if (n_pair_evals) *n_pair_evals = (uint64_t)(nx * ny) * (uint64_t)n;
+  });
+}
+
 // ---------------------------------------------------------- device API ---
+int ptrom_dev_hamiltonian_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma, double* d_out) {
+  return guarded(ctx, [&] {
+    if (n <= 0) config_fail("particle system is empty");
+    dev_hamiltonian_f64(ctx, n, d_x, d_gamma, d_out);
+  });
+}
+
+int ptrom_dev_velocity_field_grid_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                      double delta, int form, double x_min, double x_max, int64_t nx, double y_min,
+                                      double y_max, int64_t ny, double c_g, double l, double gamma_bar,
+                                      double* d_grid) {
+  return guarded(ctx, [&] {
+    if (n <= 0) config_fail("particle system is empty");
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    const double scale = lattice_scale(nx, ny, x_min, x_max, y_min, y_max, c_g, l, gamma_bar);
+    dev_velocity_field_grid_f64(ctx, n, d_x, d_gamma, delta, form, x_min, x_max, nx, y_min, y_max, ny, scale,
+                                d_grid);
+  });
+}
+
 int ptrom_dev_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma, double delta,
                                     int form, const double* d_inflow, int64_t t_begin, int64_t t_end, double* d_f,
                                     int64_t ld_f) {

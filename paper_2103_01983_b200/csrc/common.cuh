@@ -45,6 +45,7 @@ enum : int {
   kStatusSingularBlock = 2,      // integrators.hpp:187-189
   kStatusNonFiniteJacobian = 3,
   kStatusZeroClusterCirculation = 4,  // affine batch: G_A + mu G_B == 0
+  kStatusCoincidentPair = 5,  // hamiltonian d² == 0; index = i·n + j (kernel.hpp:185-187)
 };
 struct DeviceStatus {
   int kind;
@@ -105,6 +106,7 @@ struct ptrom_ctx {
   bool prof_on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
+  long long status_pair_n = 0;  // n for decoding kStatusCoincidentPair (i·n + j)
   int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
   ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)

@@ -16,6 +16,10 @@ void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* 
 void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
                       long long t_begin, long long t_end, double* jxx, double* jxy, double* jyx, double* jyy,
                       double dt_for_inverse, double* inv);
+void dev_hamiltonian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double* out);
+void dev_velocity_field_grid_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta,
+                                 int form, double x_min, double x_max, long long nx, double y_min, double y_max,
+                                 long long ny, double scale, double* grid);
 void dev_residual_f64(ptrom_ctx* ctx, long long m, long long ld, const double* xi, const double* fxi,
                       const double* xp, const double* fp, double dt, double* r, double* norm2, double* block_part);
 void dev_newton_update_f64(ptrom_ctx* ctx, long long m, long long ld, const double* inv, const double* r, double* x);

@@ -91,5 +91,29 @@ def newton_update(inv: torch.Tensor, r: torch.Tensor, x: torch.Tensor, m: int, l
     ctx.check(ctx.lib.ptrom_dev_newton_update_f64(ctx.handle, m, ld, _ptr(inv), _ptr(r), _ptr(x)))
 
 
+def hamiltonian(x: torch.Tensor, gamma: torch.Tensor, out: Optional[torch.Tensor] = None,
+                ctx: Optional[Context] = None) -> torch.Tensor:
+    """kernel.hpp:174-191 on device; out is a 1-element float64 tensor."""
+    n = gamma.shape[0]
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=x.device)
+    ctx = _ctx(ctx, x)
+    ctx.check(ctx.lib.ptrom_dev_hamiltonian_f64(ctx.handle, n, _ptr(x), _ptr(gamma), _ptr(out)))
+    return out
+
+
+def velocity_field_grid(x: torch.Tensor, gamma: torch.Tensor, delta: float, form: int, lattice, c_g: float,
+                        l: float, gamma_bar: float, ctx: Optional[Context] = None) -> torch.Tensor:
+    """kernel.hpp:213-238 on device → (ny, nx) tensor (a transposed view of the column-major grid)."""
+    n = gamma.shape[0]
+    nx, ny = int(lattice.nx), int(lattice.ny)
+    grid = torch.empty(nx, ny, dtype=torch.float64, device=x.device)
+    ctx = _ctx(ctx, x)
+    ctx.check(ctx.lib.ptrom_dev_velocity_field_grid_f64(
+        ctx.handle, n, _ptr(x), _ptr(gamma), float(delta), int(form), float(lattice.x_min), float(lattice.x_max),
+        nx, float(lattice.y_min), float(lattice.y_max), ny, float(c_g), float(l), float(gamma_bar), _ptr(grid)))
+    return grid.t()
+
+
 def synchronize(ctx: Optional[Context] = None, device: int = 0) -> None:
     (ctx or default_context(device)).synchronize()

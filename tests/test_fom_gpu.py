@@ -97,3 +97,21 @@ def test_config_validation(pt):
         pt.fom_simulate(x, s, pt.TimeGrid(0.1, 5), pt.NewtonConfig(tol=0.0))
     with pytest.raises(pt.ConfigError):
         pt.fom_simulate(x, s, pt.TimeGrid(0.1, 5), pt.NewtonConfig(jacobian_refresh_period=0))
+
+
+def test_sharded_driver_single_rank_cuda_backend(oracle):
+    """sharded.py ShardedFom with the CUDA backend (ptrom_dev_* ABI) at world 1:
+    the per-rank control path the multi-GPU run executes, against the oracle."""
+    import torch
+    from paper_2103_01983_b200.sharded import CudaBackend, ShardedFom
+    w = workloads.config1(n=1024)
+    steps = 10
+    dev = torch.device("cuda:0")
+    gamma = torch.tensor(w.gamma, device=dev)
+    fom = ShardedFom(w.n, CudaBackend(gamma, w.delta))
+    res = fom.simulate(torch.tensor(w.x0, device=dev), w.dt, steps)
+    snaps, iters, conv, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps, threads=THREADS)
+    got = res.snapshots_local.cpu().numpy()
+    assert all(res.converged) and conv.all()
+    for s in range(steps):
+        assert rel(got[s], snaps[:, s]) <= 1e-12
