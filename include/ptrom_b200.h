@@ -187,6 +187,15 @@ typedef struct ptrom_basis ptrom_basis;
 int ptrom_basis_create(ptrom_ctx* ctx, int64_t n_dofs, int64_t modes, const double* phi,
                        const double* singular_values /* nullable */, const double* x_ref, ptrom_basis** out);
 void ptrom_basis_free(ptrom_basis* basis);
+/* rom.hpp:45-58 reconstruct_output: out (n_dofs x n_steps, column-major) row k
+ * = x_ref[dofs[k]] + phi.row(dofs[k]) * x_hat; dofs == NULL gives
+ * reconstruct_full (rom.hpp:60-64, all 2n rows). x_hat is modes x n_steps
+ * column-major (RomTrajectory::x_hat). modes <= 32. */
+int ptrom_reconstruct_output_f64(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_steps, const double* x_hat,
+                                 int64_t n_dofs, const int64_t* dofs /* nullable */, double* out);
+int ptrom_dev_reconstruct_output_f64(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_steps,
+                                     const double* d_xhat, int64_t n_dofs, const int64_t* d_dofs,
+                                     double* d_out);
 /* GnatOperator (reduction.hpp:173-180): sorted sample ids and A = pinv(P Φ_r)
  * (m_r x 2 n_samples, column-major); gathers Φ̄, x̄⁰ like GnatSolver's
  * constructor (rom.hpp:264-290). m_r <= 32, modes <= 32. */

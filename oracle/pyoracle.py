@@ -110,6 +110,13 @@ def velocity_field_grid(x, gamma, delta, form, x_min, x_max, nx, y_min, y_max, n
     return grid.reshape(nx, ny).T
 
 
+def reconstruct_output(phi, x_ref, x_hat, dofs=None):
+    """rom.hpp:45-58 (rows dofs) / rom.hpp:60-64 (all rows): x_ref[d] + Φ[d,:]·x̂."""
+    phi, x_ref, x_hat = np.asarray(phi, float), np.asarray(x_ref, float), np.asarray(x_hat, float)
+    rows = np.arange(phi.shape[0]) if dofs is None else np.asarray(dofs, np.int64)
+    return phi[rows, :] @ x_hat + x_ref[rows][:, None]
+
+
 def fom_simulate(x0, gamma, delta, dt, n_steps, form=0, inflow=None, tol=1e-10, max_iters=100, refresh=1,
                  threads=1):
     """integrators.hpp:243-272 → (snapshots (2N, steps), iterations, converged, relative_residual)."""

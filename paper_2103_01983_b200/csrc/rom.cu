@@ -850,7 +850,50 @@ int blocks_for(long long count, int tpb) { return (int)std::max(1LL, (count + tp
 
 }  // namespace
 
+// reconstruct_output / reconstruct_full (rom.hpp:45-64): out(k, s) = x_ref[d_k] + Φ(d_k,:)·x̂(:, s).
+// One thread per output row d_k keeps Φ's row in registers (M ≤ 32; one
+// coalesced read of Φ per column) and walks the steps with x̂ staged in
+// shared memory (≤ 32 steps per stage); writes are coalesced along k.
+template <int MAXM>
+__global__ void __launch_bounds__(128) reconstruct_kernel(DBasis b, long long n_steps, const double* __restrict__ xh,
+                                                          long long n_out, const long long* __restrict__ dofs,
+                                                          double* __restrict__ out) {
+  constexpr int SS = 32;
+  __shared__ double xs[SS * MAXM];
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nd = 2 * b.n;
+  const int m = b.m;
+  long long d = k < n_out ? (dofs ? dofs[k] : k) : 0;
+  double row[MAXM];
+#pragma unroll
+  for (int j = 0; j < MAXM; ++j) row[j] = (j < m && k < n_out) ? b.phi[d + j * nd] : 0.0;
+  const double xr = k < n_out ? b.x_ref[d] : 0.0;
+  for (long long s0 = 0; s0 < n_steps; s0 += SS) {
+    const int cnt = (int)min((long long)SS, n_steps - s0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt * m; e += blockDim.x) xs[e] = xh[s0 * m + e];
+    __syncthreads();
+    if (k < n_out) {
+      for (int s = 0; s < cnt; ++s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < MAXM; ++j)
+          if (j < m) acc = fma(row[j], xs[s * m + j], acc);
+        out[k + (s0 + s) * n_out] = acc + xr;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- drivers ---
+void rom_reconstruct(ptrom_ctx* ctx, const DBasis& b, long long n_steps, const double* d_xhat, long long n_out,
+                     const long long* d_dofs, double* d_out) {
+  if (n_out <= 0 || n_steps <= 0) return;
+  if (b.m > 32) throw status_error(PTROM_CONFIG_ERROR, "reconstruct: at most 32 modes");
+  reconstruct_kernel<32><<<blocks_for(n_out, 128), 128, 0, ctx->stream>>>(b, n_steps, d_xhat, n_out, d_dofs, d_out);
+  PTROM_LAUNCH_CHECK();
+}
+
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma) {
   const long long work = s.n_c * (s.m + 1);
   if (work > 0) reassign_exact_kernel<<<blocks_for(work, 128), 128, 0, ctx->stream>>>(s, b, d_gamma);

@@ -9,6 +9,8 @@
 
 namespace ptrom {
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma);
+void rom_reconstruct(ptrom_ctx* ctx, const DBasis& b, long long n_steps, const double* d_xhat, long long n_out,
+                     const long long* d_dofs, double* d_out);
 void rom_affine_tables(ptrom_ctx* ctx, const DSurrogate& s, const DBasis& b, const double* d_ga, const double* d_gb,
                        AffineTables& t);
 unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGnat* g, const AffineTables* t,
@@ -127,6 +129,45 @@ void ptrom_basis_free(ptrom_basis* b) {
     cudaSetDevice(b->device);
     delete b;
   }
+}
+
+// rom.hpp:45-64 reconstruct_output (dofs != NULL) / reconstruct_full (dofs == NULL).
+int ptrom_reconstruct_output_f64(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_steps, const double* x_hat,
+                                 int64_t n_dofs, const int64_t* dofs, double* out) {
+  return guarded(ctx, [&] {
+    if (!basis) config_fail("reconstruct_output: null basis");
+    if (n_steps < 0) config_fail("reconstruct_output: negative step count");
+    const long long nd = 2 * basis->b.n;
+    const long long n_out = dofs ? n_dofs : nd;
+    if (dofs)
+      for (long long k = 0; k < n_dofs; ++k)
+        if (dofs[k] < 0 || dofs[k] >= nd) config_fail("reconstruct_output: dof out of range");
+    const int m = basis->b.m;
+    double* dx = nullptr;
+    double* dout = nullptr;
+    long long* dd = nullptr;
+    PTROM_CUDA(cudaMallocAsync(&dx, sizeof(double) * std::max<long long>(1, m * n_steps), ctx->stream));
+    PTROM_CUDA(cudaMallocAsync(&dout, sizeof(double) * std::max<long long>(1, n_out * n_steps), ctx->stream));
+    if (dofs) PTROM_CUDA(cudaMallocAsync(&dd, sizeof(long long) * std::max<long long>(1, n_dofs), ctx->stream));
+    PTROM_CUDA(cudaMemcpyAsync(dx, x_hat, sizeof(double) * m * n_steps, cudaMemcpyHostToDevice, ctx->stream));
+    if (dofs)
+      PTROM_CUDA(cudaMemcpyAsync(dd, dofs, sizeof(long long) * n_dofs, cudaMemcpyHostToDevice, ctx->stream));
+    rom_reconstruct(ctx, basis->b, n_steps, dx, n_out, dd, dout);
+    PTROM_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * n_out * n_steps, cudaMemcpyDeviceToHost, ctx->stream));
+    PTROM_CUDA(cudaFreeAsync(dx, ctx->stream));
+    PTROM_CUDA(cudaFreeAsync(dout, ctx->stream));
+    if (dd) PTROM_CUDA(cudaFreeAsync(dd, ctx->stream));
+    PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ptrom_dev_reconstruct_output_f64(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_steps, const double* d_xhat,
+                                     int64_t n_dofs, const int64_t* d_dofs, double* d_out) {
+  return guarded(ctx, [&] {
+    if (!basis) config_fail("reconstruct_output: null basis");
+    const long long n_out = d_dofs ? n_dofs : 2 * basis->b.n;
+    rom_reconstruct(ctx, basis->b, n_steps, d_xhat, n_out, reinterpret_cast<const long long*>(d_dofs), d_out);
+  });
 }
 
 int ptrom_gnat_op_create(ptrom_ctx* ctx, const ptrom_basis* basis, int64_t n_samples, const int64_t* sample_ids,

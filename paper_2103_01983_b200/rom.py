@@ -56,6 +56,23 @@ class PODBasis:  # reduction.hpp:18-26
     def modes(self):
         return self.phi.shape[1]
 
+    def reconstruct_output(self, x_hat, dofs=None) -> np.ndarray:
+        """rom.hpp:45-58 (dofs given) / rom.hpp:60-64 reconstruct_full (dofs None), on the device."""
+        xh = _fortran(x_hat)
+        if xh.ndim == 1:
+            xh = xh.reshape(-1, 1, order="F")
+        if xh.shape[0] != self.modes():
+            raise ConfigError("reconstruct_output: coordinate dimension mismatch")
+        d = None if dofs is None else _i64(dofs)
+        n_out = self.dim() if d is None else d.shape[0]
+        out = np.zeros((n_out, xh.shape[1]), order="F")
+        self.ctx.check(self.ctx.lib.ptrom_reconstruct_output_f64(self.ctx.handle, self._h, xh.shape[1], _p(xh),
+                                                                 0 if d is None else d.shape[0], _p(d), _p(out)))
+        return out
+
+    def reconstruct_full(self, x_hat) -> np.ndarray:
+        return self.reconstruct_output(x_hat, None)
+
     def __del__(self):
         try:
             self.ctx.lib.ptrom_basis_free(self._h)
