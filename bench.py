@@ -175,13 +175,26 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 200 for config2)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--workload", choices=["config2", "config3", "config4"], default="config2",
+                    help="config2 (default, the headline) | config3 Barnes-Hut | config4 PTROM online batch")
+    ap.add_argument("--batch", type=int, default=512, help="config4: instances per step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.steps_given = args.steps is not None
+    if args.steps is None:
+        args.steps = 200
+    if args.workload != "config2":
+        import bench_extra
+        rank = env_int("RANK", 0)
+        world = env_int("WORLD_SIZE", 1)
+        if args.impl == "reference":
+            return bench_extra.run_reference(args, rank, world)
+        return bench_extra.run(args, rank, world)
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)

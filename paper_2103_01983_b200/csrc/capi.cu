@@ -113,6 +113,12 @@ int ptrom_create(int device, void* stream, ptrom_ctx** out) {
     PTROM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
     if (major != 10) throw status_error(PTROM_CUDA_ERROR, "libptrom_b200 requires an sm_100a (B200) device");
     ctx->num_sms = sms;
+    // Keep freed stream-ordered allocations (tree / ROM scratch) in the pool
+    // instead of returning them to the OS at every synchronization.
+    cudaMemPool_t pool;
+    PTROM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    PTROM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     if (const char* v = std::getenv("PTROM_ALLPAIRS_VARIANT")) ctx->allpairs_variant = std::atoi(v);
     if (const char* v = std::getenv("PTROM_TREE_SEQ_MAX")) ctx->tree_seq_max = std::max(1, std::atoi(v));
     PTROM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DeviceStatus)));
