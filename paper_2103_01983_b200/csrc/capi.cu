@@ -123,6 +123,7 @@ int ptrom_create(int device, void* stream, ptrom_ctx** out) {
     if (const char* v = std::getenv("PTROM_TREE_SEQ_MAX")) ctx->tree_seq_max = std::max(1, std::atoi(v));
     PTROM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DeviceStatus)));
     PTROM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DeviceStatus)));
+    PTROM_CUDA(cudaMallocHost(&ctx->h_counts, 16 * sizeof(int)));
     DeviceStatus clear{0, 0, LLONG_MAX};
     PTROM_CUDA(cudaMemcpy(ctx->d_status, &clear, sizeof(clear), cudaMemcpyHostToDevice));
   });
@@ -140,6 +141,7 @@ void ptrom_destroy(ptrom_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_status) cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
   if (ctx->scratch.base) cudaFree(ctx->scratch.base);
   if (ctx->io.base) cudaFree(ctx->io.base);
   for (auto& pr : ctx->prof_events) {

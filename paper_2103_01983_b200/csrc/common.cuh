@@ -106,7 +106,8 @@ struct ptrom_ctx {
   bool prof_on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
-  long long status_pair_n = 0;  // n for decoding kStatusCoincidentPair (i·n + j)
+  long long status_pair_n = 0;
+  int* h_counts = nullptr;  // pinned scratch for small D2H reads (tree level counts)  // n for decoding kStatusCoincidentPair (i·n + j)
   int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
   ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)

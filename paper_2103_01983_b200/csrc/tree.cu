@@ -34,6 +34,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "ops.cuh"
@@ -72,6 +73,31 @@ struct U4Sum {
 
 __device__ __forceinline__ unsigned comp(const uint4& v, int q) {
   return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+// Quadrant prefix counters for the level partition. uint4: one-hot counts of
+// all four quadrants. u64 (n + 1 < 2^21): three 21-bit counts packed into one
+// word (half the scan traffic); inside a splitting node every element is
+// counted, so quadrant 3 = span - (q0 + q1 + q2).
+constexpr int kPackBits = 21;
+__device__ __forceinline__ uint4 quad_one(int q, uint4*) {
+  return make_uint4(q == 0, q == 1, q == 2, q == 3);
+}
+__device__ __forceinline__ unsigned long long quad_one(int q, unsigned long long*) {
+  return q < 3 ? 1ull << (kPackBits * q) : 0ull;
+}
+__device__ __forceinline__ uint4 quad_zero(uint4*) { return make_uint4(0, 0, 0, 0); }
+__device__ __forceinline__ unsigned long long quad_zero(unsigned long long*) { return 0ull; }
+// count of quadrant q among positions [i0, i1) of one splitting node (a = scan[i0], b = scan[i1])
+__device__ __forceinline__ unsigned quad_delta(const uint4& a, const uint4& b, int q, int) {
+  return comp(b, q) - comp(a, q);
+}
+__device__ __forceinline__ unsigned quad_delta(unsigned long long a, unsigned long long b, int q, int span) {
+  constexpr unsigned long long m = (1ull << kPackBits) - 1;
+  const unsigned d0 = (unsigned)(((b >> 0) & m) - ((a >> 0) & m));
+  const unsigned d1 = (unsigned)(((b >> kPackBits) & m) - ((a >> kPackBits) & m));
+  const unsigned d2 = (unsigned)(((b >> (2 * kPackBits)) & m) - ((a >> (2 * kPackBits)) & m));
+  return q == 0 ? d0 : q == 1 ? d1 : q == 2 ? d2 : (unsigned)span - d0 - d1 - d2;
 }
 
 // ---------------------------------------------------------------- hull ---
@@ -113,11 +139,12 @@ __global__ void iota_copy_kernel(long long n, const double* __restrict__ px, con
 
 // ------------------------------------------------------------- levels ---
 // quadtree.hpp:81-86: quadrant digit of each member of a splitting node.
+template <class T>
 __global__ void digit_kernel(long long n, const int* __restrict__ pos_rec, const double* __restrict__ sx,
-                             const double* __restrict__ sy, const double* __restrict__ rec_mid, uint4* __restrict__ flags,
+                             const double* __restrict__ sy, const double* __restrict__ rec_mid, T* __restrict__ flags,
                              unsigned char* __restrict__ digit) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= n; k += (long long)gridDim.x * blockDim.x) {
-    uint4 f = make_uint4(0, 0, 0, 0);
+    T f = quad_zero((T*)nullptr);
     if (k < n) {
       const int r = pos_rec[k];
       if (r >= 0) {
@@ -126,10 +153,7 @@ __global__ void digit_kernel(long long n, const int* __restrict__ pos_rec, const
         const int qy = sy[k] <= cy ? 0 : 1;
         const int q = qy * 2 + qx;
         digit[k] = (unsigned char)q;
-        f.x = q == 0;
-        f.y = q == 1;
-        f.z = q == 2;
-        f.w = q == 3;
+        f = quad_one(q, (T*)nullptr);
       }
     }
     flags[k] = f;
@@ -137,28 +161,32 @@ __global__ void digit_kernel(long long n, const int* __restrict__ pos_rec, const
 }
 
 // Per level node: child counts (from the scan) and number of children.
+template <class T>
 __global__ void child_count_kernel(int L, int lv_base, const int* __restrict__ rec_begin,
                                    const int* __restrict__ rec_end, const unsigned char* __restrict__ rec_split,
-                                   const uint4* __restrict__ scan, int* __restrict__ nchild) {
+                                   const T* __restrict__ scan, int* __restrict__ nchild) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const int r = lv_base + l;
   int c = 0;
   if (rec_split[r]) {
-    const uint4 a = scan[rec_begin[r]], b = scan[rec_end[r]];
-    c = (b.x != a.x) + (b.y != a.y) + (b.z != a.z) + (b.w != a.w);
+    const int span = rec_end[r] - rec_begin[r];
+    const T a = scan[rec_begin[r]], b = scan[rec_end[r]];
+    for (int q = 0; q < 4; ++q) c += quad_delta(a, b, q, span) != 0;
   }
   nchild[l] = c;
 }
 
 // quadtree.hpp:87-116: child records in SW, SE, NW, NE order.
-__global__ void make_children_kernel(int L, int lv_base, int next_base, int leaf_cap, const uint4* __restrict__ scan,
+template <class T>
+__global__ void make_children_kernel(int L, int lv_base, int next_base, int leaf_cap, const T* __restrict__ scan,
                                      const int* __restrict__ child_off, TreeRecords rec, int* __restrict__ n_split_next) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const int r = lv_base + l;
   if (!rec.split[r]) return;
-  const uint4 a = scan[rec.begin[r]], b = scan[rec.end[r]];
+  const int span = rec.end[r] - rec.begin[r];
+  const T a = scan[rec.begin[r]], b = scan[rec.end[r]];
   const double b0 = rec.bounds[4 * r], b1 = rec.bounds[4 * r + 1], b2 = rec.bounds[4 * r + 2], b3 = rec.bounds[4 * r + 3];
   const double cx = rec.mid[2 * r], cy = rec.mid[2 * r + 1];
   const double half = __ddiv_rn(rec.width[r], 2.0);
@@ -166,7 +194,7 @@ __global__ void make_children_kernel(int L, int lv_base, int next_base, int leaf
   int j = 0;
   int splits = 0;
   for (int q = 0; q < 4; ++q) {
-    const int cnt = (int)(comp(b, q) - comp(a, q));
+    const int cnt = (int)quad_delta(a, b, q, span);
     if (cnt == 0) continue;
     const int c = next_base + child_off[l] + (j++);
     rec.children[4 * r + q] = c;
@@ -192,8 +220,9 @@ __global__ void make_children_kernel(int L, int lv_base, int next_base, int leaf
 }
 
 // Stable scatter of the splitting nodes' members into their children.
+template <class T>
 __global__ void scatter_kernel(long long n, const int* __restrict__ pos_rec, const unsigned char* __restrict__ digit,
-                               const uint4* __restrict__ scan, TreeRecords rec, const int* __restrict__ ord,
+                               const T* __restrict__ scan, TreeRecords rec, const int* __restrict__ ord,
                                const double* __restrict__ sx, const double* __restrict__ sy,
                                const double* __restrict__ sg, int* __restrict__ ord_n, double* __restrict__ sx_n,
                                double* __restrict__ sy_n, double* __restrict__ sg_n, int* __restrict__ pos_rec_n) {
@@ -204,7 +233,8 @@ __global__ void scatter_kernel(long long n, const int* __restrict__ pos_rec, con
     if (r >= 0) {
       const int q = digit[k];
       const int c = rec.children[4 * r + q];
-      np = rec.begin[c] + (long long)(comp(scan[k], q) - comp(scan[rec.begin[r]], q));
+      const int b0 = rec.begin[r];
+      np = rec.begin[c] + (long long)quad_delta(scan[b0], scan[k], q, (int)(k - b0));
       nrec = rec.split[c] ? c : -1;
     }
     ord_n[np] = ord[k];
@@ -216,25 +246,47 @@ __global__ void scatter_kernel(long long n, const int* __restrict__ pos_rec, con
 }
 
 // quadtree.hpp:51-67 finish_node for small nodes: sequential, reference order.
-__global__ void sums_small_kernel(int R0, int R1, TreeRecords rec, const double* __restrict__ sx,
-                                  const double* __restrict__ sy, const double* __restrict__ sg, int seq_max,
-                                  int* __restrict__ large_list, int* __restrict__ large_count) {
-  const int r = R0 + blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per node: the lanes stage 32 members at a time (coalesced) in
+// shared memory and lane 0 runs the reference's left-to-right sums over them.
+constexpr int kSumWarps = kThreads / 32;
+__global__ void __launch_bounds__(kThreads) sums_small_kernel(int R0, int R1, TreeRecords rec,
+                                                              const double* __restrict__ sx,
+                                                              const double* __restrict__ sy,
+                                                              const double* __restrict__ sg, int seq_max,
+                                                              int* __restrict__ large_list,
+                                                              int* __restrict__ large_count) {
+  __shared__ double st[kSumWarps][3][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int r = R0 + blockIdx.x * kSumWarps + wib;
   if (r >= R1) return;
   const int b = rec.begin[r], e = rec.end[r];
   if (e - b > seq_max) {
-    large_list[atomicAdd(large_count, 1)] = r;
+    if (lane == 0) large_list[atomicAdd(large_count, 1)] = r;
     return;
   }
   double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
-  for (int k = b; k < e; ++k) {
-    const double g = sg[k], x = sx[k], y = sy[k];
-    gs = __dadd_rn(gs, g);
-    wx = __dadd_rn(wx, __dmul_rn(g, x));
-    wy = __dadd_rn(wy, __dmul_rn(g, y));
-    plx = __dadd_rn(plx, x);
-    ply = __dadd_rn(ply, y);
+  for (int c0 = b; c0 < e; c0 += 32) {
+    const int k = c0 + lane;
+    if (k < e) {
+      st[wib][0][lane] = sg[k];
+      st[wib][1][lane] = sx[k];
+      st[wib][2][lane] = sy[k];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = min(32, e - c0);
+      for (int j = 0; j < cnt; ++j) {
+        const double g = st[wib][0][j], x = st[wib][1][j], y = st[wib][2][j];
+        gs = __dadd_rn(gs, g);
+        wx = __dadd_rn(wx, __dmul_rn(g, x));
+        wy = __dadd_rn(wy, __dmul_rn(g, y));
+        plx = __dadd_rn(plx, x);
+        ply = __dadd_rn(ply, y);
+      }
+    }
+    __syncwarp();
   }
+  if (lane != 0) return;
   rec.gamma_sum[r] = gs;
   const bool fb = gs == 0.0;
   rec.fallback[r] = fb ? 1 : 0;
@@ -245,18 +297,45 @@ __global__ void sums_small_kernel(int R0, int R1, TreeRecords rec, const double*
   rec.cerr[r] = 0.0;
 }
 
-// Large nodes: fixed-order block reduction + rigorous centroid error bound
-// relative to the reference's sequential order.
-__global__ void sums_large_kernel(TreeRecords rec, const double* __restrict__ sx, const double* __restrict__ sy,
-                                  const double* __restrict__ sg, const int* __restrict__ large_list,
-                                  const int* __restrict__ large_count) {
+// Large nodes (> seq_max members): fixed chunks of kChunk members reduced by
+// one CTA each (fixed-order block reduction), then the chunk partials of a
+// node summed in chunk order — deterministic — with a rigorous bound on the
+// centroid's distance from the reference's sequential order.
+constexpr int kChunk = 8192;
+__global__ void large_prefix_kernel(TreeRecords rec, const int* __restrict__ large_list,
+                                    const int* __restrict__ large_count, int* __restrict__ chunk_off) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int total = *large_count;
+  int acc = 0;
+  for (int li = 0; li < total; ++li) {
+    chunk_off[li] = acc;
+    const int r = large_list[li];
+    acc += (rec.end[r] - rec.begin[r] + kChunk - 1) / kChunk;
+  }
+  chunk_off[total] = acc;
+}
+
+__global__ void __launch_bounds__(kThreads) large_partial_kernel(TreeRecords rec, const double* __restrict__ sx,
+                                                                 const double* __restrict__ sy,
+                                                                 const double* __restrict__ sg,
+                                                                 const int* __restrict__ large_list,
+                                                                 const int* __restrict__ large_count,
+                                                                 const int* __restrict__ chunk_off,
+                                                                 double* __restrict__ part) {
   using BR = cub::BlockReduce<double, kThreads>;
   __shared__ typename BR::TempStorage tmp;
-  __shared__ double red[8];
   const int total = *large_count;
-  for (int li = blockIdx.x; li < total; li += gridDim.x) {
-    const int r = large_list[li];
-    const int b = rec.begin[r], e = rec.end[r];
+  const int nchunks = chunk_off[total];
+  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    int lo = 0, hi = total;  // node li with chunk_off[li] <= ci < chunk_off[li + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (chunk_off[mid] <= ci) lo = mid;
+      else hi = mid;
+    }
+    const int r = large_list[lo];
+    const int b = rec.begin[r] + (ci - chunk_off[lo]) * kChunk;
+    const int e = min(rec.end[r], b + kChunk);
     double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // gs wx wy plx ply |g| |gx| |gy|
     for (int k = b + threadIdx.x; k < e; k += kThreads) {
       const double g = sg[k], x = sx[k], y = sy[k];
@@ -272,41 +351,50 @@ __global__ void sums_large_kernel(TreeRecords rec, const double* __restrict__ sx
     }
     for (int c = 0; c < 8; ++c) {
       const double t = BR(tmp).Sum(v[c]);
-      if (threadIdx.x == 0) red[c] = t;
+      if (threadIdx.x == 0) part[8 * (long long)ci + c] = t;
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      const double m = (double)(e - b);
-      const double u = 0x1p-53;
-      // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
-      // sum; their difference within twice that (first order, padded).
-      const double k2 = 2.05 * (m + 1.0) * u;
-      const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
-      const double gs = red[0];
-      rec.gamma_sum[r] = gs;
-      const bool fb = gs == 0.0;
-      rec.fallback[r] = fb ? 1 : 0;
-      double cx, cy, err;
-      if (fb) {
-        cx = __ddiv_rn(red[3], m);
-        cy = __ddiv_rn(red[4], m);
-      } else {
-        cx = __ddiv_rn(red[1], gs);
-        cy = __ddiv_rn(red[2], gs);
-      }
-      if (fabs(gs) <= 2.0 * eg) {
-        err = INFINITY;  // the fallback flag itself is uncertain
-      } else {
-        const double ag = fabs(gs) - eg;
-        err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
-      }
-      rec.centroid[2 * r] = cx;
-      rec.centroid[2 * r + 1] = cy;
-      rec.exact[r] = 0;
-      rec.cerr[r] = err;
-    }
-    __syncthreads();
   }
+}
+
+__global__ void large_finish_kernel(TreeRecords rec, const int* __restrict__ large_list,
+                                    const int* __restrict__ large_count, const int* __restrict__ chunk_off,
+                                    const double* __restrict__ part) {
+  const int li = blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= *large_count) return;
+  const int r = large_list[li];
+  const int b = rec.begin[r], e = rec.end[r];
+  double red[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int ci = chunk_off[li]; ci < chunk_off[li + 1]; ++ci)
+    for (int c = 0; c < 8; ++c) red[c] = __dadd_rn(red[c], part[8 * (long long)ci + c]);
+  const double m = (double)(e - b);
+  const double u = 0x1p-53;
+  // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
+  // sum; their difference within twice that (first order, padded).
+  const double k2 = 2.05 * (m + 1.0) * u;
+  const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
+  const double gs = red[0];
+  rec.gamma_sum[r] = gs;
+  const bool fb = gs == 0.0;
+  rec.fallback[r] = fb ? 1 : 0;
+  double cx, cy, err;
+  if (fb) {
+    cx = __ddiv_rn(red[3], m);
+    cy = __ddiv_rn(red[4], m);
+  } else {
+    cx = __ddiv_rn(red[1], gs);
+    cy = __ddiv_rn(red[2], gs);
+  }
+  if (fabs(gs) <= 2.0 * eg) {
+    err = INFINITY;  // the fallback flag itself is uncertain
+  } else {
+    const double ag = fabs(gs) - eg;
+    err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
+  }
+  rec.centroid[2 * r] = cx;
+  rec.centroid[2 * r + 1] = cy;
+  rec.exact[r] = 0;
+  rec.cerr[r] = err;
 }
 
 // ------------------------------------------------------------ preorder ---
@@ -547,33 +635,53 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   int *ord = dalloc<int>(n), *ord_n = dalloc<int>(n), *pr = dalloc<int>(n), *pr_n = dalloc<int>(n);
   double *sx = dalloc<double>(n), *sy = dalloc<double>(n), *sg = dalloc<double>(n);
   double *sx_n = dalloc<double>(n), *sy_n = dalloc<double>(n), *sg_n = dalloc<double>(n);
-  uint4* flags = dalloc<uint4>(n + 1);
-  uint4* scan = dalloc<uint4>(n + 1);
+  const bool packed = n + 1 < (1LL << kPackBits);  // u64 counters (3 x 21 bits) else uint4
+  void* flags_raw = dalloc<uint4>(n + 1);
+  void* scan_raw = dalloc<uint4>(n + 1);
   unsigned char* digit = dalloc<unsigned char>(n);
   int* dcount = dalloc<int>(4);  // [0] splits at next level, [1] large-node count
-  int* h_counts = nullptr;
-  PTROM_CUDA(cudaMallocHost(&h_counts, 4 * sizeof(int)));
-  size_t scan_tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveScan(nullptr, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0), n + 1, s);
+  int* h_counts = ctx->h_counts;  // pinned, owned by the context
+  size_t scan_tmp_bytes = 0, scan_tmp_u64 = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, scan_tmp_bytes, (uint4*)flags_raw, (uint4*)scan_raw, U4Sum(),
+                                 make_uint4(0, 0, 0, 0), n + 1, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp_u64, (unsigned long long*)flags_raw, (unsigned long long*)scan_raw,
+                                n + 1, s);
+  scan_tmp_bytes = std::max(scan_tmp_bytes, scan_tmp_u64);
   size_t scan2_tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan2_tmp_bytes, (int*)nullptr, (int*)nullptr, (int)std::min<long long>(n, INT_MAX), s);
   void* tmp = dalloc<char>(std::max(scan_tmp_bytes, scan2_tmp_bytes) + 256);
   int* nchild = nullptr;
   int* child_off = nullptr;
   size_t lvl_cap = 0;
-  int* large_list = dalloc<int>(std::max<long long>(1, n / std::max(1, seq_max) * 2 * kMaxDepth + 64));
+  const long long max_large = n / std::max(1, seq_max) + 2;  // nodes > seq_max at one level
+  int* large_list = dalloc<int>(max_large);
+  int* chunk_off = dalloc<int>(max_large + 1);
+  double* large_part = dalloc<double>(8 * (n / kChunk + max_large + 1));
+  auto run_sums = [&](int R0, int R1) {
+    sums_small_kernel<<<(R1 - R0 + kSumWarps - 1) / kSumWarps, kThreads, 0, s>>>(R0, R1, rec, sx, sy, sg, seq_max,
+                                                                                 large_list, dcount + 1);
+    large_prefix_kernel<<<1, 32, 0, s>>>(rec, large_list, dcount + 1, chunk_off);
+    large_partial_kernel<<<ctx->num_sms * 4, kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1, chunk_off,
+                                                               large_part);
+    const long long fl = std::min<long long>(R1 - R0, max_large);
+    large_finish_kernel<<<(int)((fl + 127) / 128), 128, 0, s>>>(rec, large_list, dcount + 1, chunk_off, large_part);
+    PTROM_LAUNCH_CHECK();
+  };
 
   iota_copy_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.px, t.py, t.g, ord, sx, sy, sg, pr, root_split);
   PTROM_LAUNCH_CHECK();
   // root sums
   PTROM_CUDA(cudaMemsetAsync(dcount, 0, 16, s));
-  sums_small_kernel<<<1, 32, 0, s>>>(0, 1, rec, sx, sy, sg, seq_max, large_list, dcount + 1);
-  sums_large_kernel<<<1, kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1);
-  PTROM_LAUNCH_CHECK();
+  run_sums(0, 1);
 
   int lv_base = 0, L = 1, R = 1;
-  bool splitting = root_split;
-  while (splitting) {
+  // One host round trip per level: the child count decides the next level
+  // (no splitting node → no children → done).
+  auto run_levels = [&](auto* tag) {
+  using T = std::remove_pointer_t<decltype(tag)>;
+  T* flags = static_cast<T*>(flags_raw);
+  T* scan = static_cast<T*>(scan_raw);
+  while (root_split) {
     // per-level buffers
     if ((size_t)L > lvl_cap) {
       dfree(nchild);
@@ -584,8 +692,11 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
     }
     digit_kernel<<<grid_for(ctx, n + 1), kThreads, 0, s>>>(n, pr, sx, sy, rec.mid, flags, digit);
     PTROM_LAUNCH_CHECK();
-    PTROM_CUDA(cub::DeviceScan::ExclusiveScan(tmp, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0),
-                                              n + 1, s));
+    if constexpr (std::is_same_v<T, uint4>)
+      PTROM_CUDA(cub::DeviceScan::ExclusiveScan(tmp, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0),
+                                                n + 1, s));
+    else
+      PTROM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp_bytes, flags, scan, n + 1, s));
     child_count_kernel<<<(L + kThreads - 1) / kThreads, kThreads, 0, s>>>(L, lv_base, rec.begin, rec.end, rec.split,
                                                                           scan, nchild);
     PTROM_LAUNCH_CHECK();
@@ -611,16 +722,16 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
     std::swap(sy, sy_n);
     std::swap(sg, sg_n);
     std::swap(pr, pr_n);
-    sums_small_kernel<<<(C + 127) / 128, 128, 0, s>>>(R, R + C, rec, sx, sy, sg, seq_max, large_list, dcount + 1);
-    sums_large_kernel<<<std::min(C, ctx->num_sms * 4), kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1);
-    PTROM_LAUNCH_CHECK();
-    PTROM_CUDA(cudaMemcpyAsync(&h_counts[2], dcount, 4, cudaMemcpyDeviceToHost, s));
-    PTROM_CUDA(cudaStreamSynchronize(s));
-    splitting = h_counts[2] > 0;
+    run_sums(R, R + C);
     lv_base = R;
     L = C;
     R += C;
   }
+  };
+  if (packed)
+    run_levels((unsigned long long*)nullptr);
+  else
+    run_levels((uint4*)nullptr);
 
   // ---- preorder numbering (sort records by (begin, depth))
   unsigned long long *keys = dalloc<unsigned long long>(R), *keys_s = dalloc<unsigned long long>(R);
@@ -657,10 +768,9 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
 
-  void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags, scan, digit, dcount, tmp, nchild, child_off, large_list,
-                   keys, keys_s, vals, order, rec2id, stmp};
+  void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags_raw, scan_raw, digit, dcount, tmp, nchild, child_off, large_list,
+                   chunk_off, large_part, keys, keys_s, vals, order, rec2id, stmp};
   for (void* p : frees) dfree(p);
-  cudaFreeHost(h_counts);
   rec.free();
 }
 

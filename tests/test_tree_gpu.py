@@ -243,3 +243,20 @@ def test_barnes_hut_model_rebuilds(pt, oracle):
     ot = oracle.Tree(w.x0[:n], w.x0[n:], w.gamma, 32)
     ref = ot.bh_velocity(w.x0, w.gamma, w.delta, 0, 0.5, threads=THREADS)
     assert rel(f, ref) <= 1e-12
+
+
+def test_wide_counter_path_above_2pow21(pt, oracle):
+    """n + 1 >= 2^21 takes the uint4 quadrant counters (below, three 21-bit
+    counters packed in a u64): topology still byte-equal, velocities 1e-12."""
+    from paper_2103_01983_b200.tree import ClusterCriterion, QuadTree
+    n = (1 << 21) + 5
+    rng = np.random.default_rng(21)
+    px, py = rng.normal(0, 0.3, n), rng.normal(0, 0.3, n)
+    g = rng.uniform(0.1, 1.0, n) / n
+    gt, ot = QuadTree(px, py, g, 32), oracle.Tree(px, py, g, 32)
+    assert_same_tree(gt, ot)
+    x = np.concatenate([px, py])
+    f = gt.bh_velocity(x, pt.ParticleSystem(g, 1e-6), ClusterCriterion.barnes_hut(0.5))
+    ref = ot.bh_velocity(x, g, 1e-6, 0, 0.5, t_begin=0, t_end=1500, threads=THREADS)
+    rows = np.r_[0:1500, n:n + 1500]
+    assert rel(f[rows], ref[rows]) <= 1e-12
