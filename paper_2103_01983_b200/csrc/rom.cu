@@ -55,36 +55,70 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 // ---------------------------------------------------- table preparation ---
-// reduction.hpp:407-428 for one (cluster, column) pair: column j < m is
-// the Φ̃ mode j, j == m is x̃⁰; sequential member order as the reference.
+// Row-major basis rows (DBasis::rm) for coalesced member gathers.
+__global__ void basis_rowmajor_kernel(DBasis b) {
+  const int W = 2 * (b.m + 1);
+  const long long total = b.n * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / W;
+    const int c = (int)(i % W);
+    const int half = c / (b.m + 1), j = c % (b.m + 1);  // half 0 = x row, 1 = y row
+    const long long row = p + half * b.n;
+    b.rm[i] = j < b.m ? b.phi[row + (long long)j * 2 * b.n] : b.x_ref[row];
+  }
+}
+
+// reduction.hpp:400-431 for one cluster per warp, members in the reference's
+// sequential order: ΣΓ first (each chunk of 32 members gathered in parallel,
+// then added in order via shuffles), then w_p = Γ_p / ΣΓ for 32 members at
+// once (one division per lane), then lane j owns column j (mode j, or x_ref
+// for j == m) of both rows and accumulates w_p·Φ(p, j) member by member.
+// The arithmetic is the reference's, so Φ̃, x̃⁰ and Γ̃ are bit-identical.
 __global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __restrict__ gamma) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int cols = s.m + 1;
-  if (idx >= s.n_c * cols) return;
-  const long long c = idx / cols;
-  const int j = (int)(idx % cols);
+  const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= s.n_c) return;
   const long long b0 = s.mem_off[c], b1 = s.mem_off[c + 1];
   double gsum = 0.0;
-  for (long long k = b0; k < b1; ++k) gsum = __dadd_rn(gsum, gamma[s.mem_ids[k]]);
+  for (long long k0 = b0; k0 < b1; k0 += 32) {
+    const int cnt = (int)min(32LL, b1 - k0);
+    const double gv = lane < cnt ? gamma[s.mem_ids[k0 + lane]] : 0.0;
+    for (int t = 0; t < cnt; ++t) gsum = __dadd_rn(gsum, __shfl_sync(0xffffffffu, gv, t));
+  }
   const bool fb = gsum == 0.0;
   const double inv_count = __ddiv_rn(1.0, (double)(b1 - b0));
-  double ax = 0.0, ay = 0.0;
-  for (long long k = b0; k < b1; ++k) {
-    const long long p = s.mem_ids[k];
-    const double w = fb ? inv_count : __ddiv_rn(gamma[p], gsum);
-    const double vx = j < s.m ? b.phi[p + (long long)j * 2 * b.n] : b.x_ref[p];
-    const double vy = j < s.m ? b.phi[p + b.n + (long long)j * 2 * b.n] : b.x_ref[p + b.n];
-    ax = __dadd_rn(ax, __dmul_rn(w, vx));
-    ay = __dadd_rn(ay, __dmul_rn(w, vy));
-  }
-  if (j < s.m) {
-    s.phi_tilde[c + (long long)j * 2 * s.n_c] = ax;
-    s.phi_tilde[c + s.n_c + (long long)j * 2 * s.n_c] = ay;
-  } else {
-    s.x0_tilde[c] = ax;
-    s.x0_tilde[c + s.n_c] = ay;
-    s.gamma_tilde[c] = gsum;
-    s.zero_gamma[c] = fb ? 1 : 0;
+  const int W = 2 * (b.m + 1);
+  for (int j0 = 0; j0 <= b.m; j0 += 32) {
+    const int j = min(j0 + lane, b.m);  // lanes past m duplicate column m (not stored)
+    double ax = 0.0, ay = 0.0;
+    for (long long k0 = b0; k0 < b1; k0 += 32) {
+      const int cnt = (int)min(32LL, b1 - k0);
+      long long pl = 0;
+      double wl = 0.0;
+      if (lane < cnt) {
+        pl = s.mem_ids[k0 + lane];
+        wl = fb ? inv_count : __ddiv_rn(gamma[pl], gsum);
+      }
+#pragma unroll 8
+      for (int t = 0; t < cnt; ++t) {
+        const long long p = __shfl_sync(0xffffffffu, pl, t);
+        const double w = __shfl_sync(0xffffffffu, wl, t);
+        const double* row = b.rm + p * W;
+        ax = __dadd_rn(ax, __dmul_rn(w, row[j]));
+        ay = __dadd_rn(ay, __dmul_rn(w, row[b.m + 1 + j]));
+      }
+    }
+    if (j0 + lane > b.m) continue;
+    if (j < s.m) {
+      s.phi_tilde[c + (long long)j * 2 * s.n_c] = ax;
+      s.phi_tilde[c + s.n_c + (long long)j * 2 * s.n_c] = ay;
+    } else {
+      s.x0_tilde[c] = ax;
+      s.x0_tilde[c + s.n_c] = ay;
+      s.gamma_tilde[c] = gsum;
+      s.zero_gamma[c] = fb ? 1 : 0;
+    }
   }
 }
 
@@ -95,7 +129,8 @@ __global__ void direct_gamma_kernel(DSurrogate s, const double* __restrict__ gam
 
 // Affine member sums for Γ(μ) = Γa + μΓb: S_A, S_B (Φ rows), X_A, X_B
 // (x_ref), G_A, G_B per cluster — an algebraic reformulation, so any order:
-// one warp per (cluster, column), lanes striding over the members.
+// one warp per (cluster, column), lanes striding over the members (large
+// clusters are split across the lanes; rows come from the row-major basis).
 __global__ void affine_tables_kernel(DSurrogate s, DBasis b, const double* __restrict__ ga,
                                      const double* __restrict__ gb, AffineTables t) {
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -104,11 +139,13 @@ __global__ void affine_tables_kernel(DSurrogate s, DBasis b, const double* __res
   if (wid >= s.n_c * cols) return;
   const long long c = wid / cols;
   const int j = (int)(wid % cols);
+  const int W = 2 * (b.m + 1);
   double v[6] = {0, 0, 0, 0, 0, 0};  // sax say sbx sby ga gb
+#pragma unroll 4
   for (long long k = s.mem_off[c] + lane; k < s.mem_off[c + 1]; k += 32) {
     const long long p = s.mem_ids[k];
-    const double vx = j < s.m ? b.phi[p + (long long)j * 2 * b.n] : b.x_ref[p];
-    const double vy = j < s.m ? b.phi[p + b.n + (long long)j * 2 * b.n] : b.x_ref[p + b.n];
+    const double* row = b.rm + p * W;
+    const double vx = row[j], vy = row[b.m + 1 + j];
     const double a = ga[p], bb = gb[p];
     v[0] = fma(a, vx, v[0]);
     v[1] = fma(a, vy, v[1]);
@@ -213,23 +250,29 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
 // then combines (a + μ b)/(G_A + μ G_B) in the epilogue. Exact mode: 4
 // clusters x (x, y) per tile, x̃⁰ + Φ̃ x̂.
 template <bool AFFINE, int MP>
-__global__ void positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et, int B,
-                                              const double* __restrict__ xhat, const double* __restrict__ mu,
-                                              const unsigned char* __restrict__ active, double* __restrict__ cx,
-                                              double* __restrict__ cy, DeviceStatus* st) {
+__global__ void __launch_bounds__(256) positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et,
+                                                                     int B, const double* __restrict__ xhat,
+                                                                     const double* __restrict__ mu,
+                                                                     const unsigned char* __restrict__ active,
+                                                                     double* __restrict__ cx, double* __restrict__ cy,
+                                                                     DeviceStatus* st) {
   // One warp per cluster tile; its table rows (the A operand) stay in
-  // registers while it sweeps all instance tiles of 8.
+  // registers while it sweeps all instance tiles of 8. x̂ is staged per CTA
+  // in shared memory, IC instances at a time (row stride MP + 4 doubles:
+  // conflict-free B-fragment loads).
   constexpr int CPT = AFFINE ? 2 : 4;
   constexpr int KS = MP / 4;
+  constexpr int IC = 64, SX = MP + 4;
+  __shared__ double sxh[IC * SX];
   const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long ctiles = (s.n_c + CPT - 1) / CPT;
-  if (warp_id >= ctiles) return;
+  const bool w_ok = warp_id < ctiles;
   const long long c0 = warp_id * CPT;
   const int lr = lane >> 2, lc = lane & 3;
   const long long ca = c0 + (AFFINE ? (lr >> 2) : (lr >> 1));
   const int q = AFFINE ? (lr & 3) : (lr & 1);  // 0 ax, 1 ay, 2 bx, 3 by
-  const bool c_ok = ca < s.n_c;
+  const bool c_ok = w_ok && ca < s.n_c;
   const double* trow = et.ct + (ca * (AFFINE ? 4 : 2) + q) * (long long)MP;
   double a[KS];
 #pragma unroll
@@ -246,43 +289,50 @@ __global__ void positions_clusters_mma_kernel(DSurrogate s, AffineTables t, Engi
     }
   }
   double* out = (q & 1) ? cy : cx;
-  for (int b0 = 0; b0 < B; b0 += 8) {
-    double acc[2] = {0.0, 0.0};
-    const int bb = b0 + lr;
+  for (int i0 = 0; i0 < B; i0 += IC) {
+    const int icnt = min(IC, B - i0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < icnt * MP; e += blockDim.x) sxh[(e / MP) * SX + e % MP] = xhat[(long long)i0 * MP + e];
+    __syncthreads();
+    if (!w_ok) continue;
+    for (int b0 = 0; b0 < icnt; b0 += 8) {
+      double acc[2] = {0.0, 0.0};
+      const int bl = b0 + lr;
 #pragma unroll
-    for (int k = 0; k < KS; ++k) {
-      const double x = bb < B ? xhat[(long long)bb * MP + 4 * k + lc] : 0.0;
-      dmma(acc, a[k], x);
-    }
-    if (AFFINE) {
-      const double o0 = __shfl_down_sync(0xffffffffu, acc[0], 8);  // S_B row partner (row + 2)
-      const double o1 = __shfl_down_sync(0xffffffffu, acc[1], 8);
-      if (q < 2 && c_ok) {
-        const int b = b0 + 2 * lc;  // two consecutive instances per lane: one 16-byte store
-        double v[2];
+      for (int k = 0; k < KS; ++k) {
+        const double x = bl < icnt ? sxh[bl * SX + 4 * k + lc] : 0.0;
+        dmma(acc, a[k], x);
+      }
+      const int b = i0 + b0 + 2 * lc;  // two consecutive instances per lane: one 16-byte store
+      if (AFFINE) {
+        const double o0 = __shfl_down_sync(0xffffffffu, acc[0], 8);  // S_B row partner (row + 2)
+        const double o1 = __shfl_down_sync(0xffffffffu, acc[1], 8);
+        if (q < 2 && c_ok) {
+          double v[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double m = b + e < B ? mu[b + e] : 0.0;
-          const double G = fma(m, gb, ga);
-          if (b + e < B && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
-          v[e] = fma(m, base_b + (e ? o1 : o0), base_a + acc[e]) / G;
+          for (int e = 0; e < 2; ++e) {
+            const double m = b + e < B ? mu[b + e] : 0.0;
+            const double G = fma(m, gb, ga);
+            if (b + e < B && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+            // (S_A + μS_B)x̂-part / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times numerator
+            v[e] = fma(m, base_b + (e ? o1 : o0), base_a + acc[e]) * rcp64(G);
+          }
+          if (b + 1 < B && !active && (B % 2 == 0)) {
+            *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(v[0], v[1]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = v[e];
+          }
         }
+      } else if (c_ok) {
         if (b + 1 < B && !active && (B % 2 == 0)) {
-          *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(v[0], v[1]);
+          *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(base_a + acc[0], base_a + acc[1]);
         } else {
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = v[e];
+            if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = base_a + acc[e];
         }
-      }
-    } else if (c_ok) {
-      const int b = b0 + 2 * lc;
-      if (b + 1 < B && !active && (B % 2 == 0)) {
-        *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(base_a + acc[0], base_a + acc[1]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = base_a + acc[e];
       }
     }
   }
@@ -366,6 +416,7 @@ __global__ void positions_targets_kernel(DGnat g, int B, const double* __restric
 // exactly on its target when delta == 0, rom.hpp:129), then direct sources
 // (skipping the target's own id, rom.hpp:136), fused velocity + Jacobian,
 // inflow at the target id. f: [b][2n_t], jac: [b][n_t][4].
+template <int IB>
 __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTables at, const double* __restrict__ mu,
                                                         int B, const double* __restrict__ xbar,
                                                         const double* __restrict__ cx, const double* __restrict__ cy,
@@ -375,18 +426,23 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
                                                         long long n, const unsigned char* __restrict__ active,
                                                         double* __restrict__ f, double* __restrict__ jac,
                                                         unsigned long long* __restrict__ pairs, DeviceStatus* st) {
-  // Work mapping: with B >= 32 a warp is (target, 32-instance chunk) and the
-  // chunk is the slow grid dimension, so concurrently resident warps sweep
-  // spatially adjacent targets (t_order) for the same instances and share
-  // cluster positions in L2; with B < 32 one thread per (target, instance).
+  // Work mapping: with B >= IB a warp is (32/IB targets, IB-instance chunk)
+  // and the chunk is the slow grid dimension, so concurrently resident warps
+  // sweep spatially adjacent targets (t_order) for the same IB instances: the
+  // positions of one chunk (n_c x IB x 16 B per chunk)
+  // stay in L2 while the targets sweep, so each is read from HBM about once.
+  // With B < IB one thread per (target, instance).
   const long long gidx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nt = s.n_t;
   unsigned long long cnt = 0;
   long long tt, bb_;
-  if (B >= 32) {
+  if (B >= IB) {
     const long long wid = gidx >> 5;
-    tt = wid % nt;
-    bb_ = (wid / nt) * 32 + (gidx & 31);
+    const int lane = (int)(gidx & 31);
+    constexpr int TPW = 32 / IB;
+    const long long tgroups = (nt + TPW - 1) / TPW;
+    tt = (wid % tgroups) * TPW + lane / IB;
+    bb_ = (wid / tgroups) * IB + lane % IB;
   } else {
     tt = gidx / B;
     bb_ = gidx % B;
@@ -609,18 +665,23 @@ __global__ void __launch_bounds__(kGnThreads) gn_eval_kernel(DGnat g, int B, dou
 
 
 // Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
-// slice of the sampled rows; A and Φ̄ rows of the slice are shared by the 8
-// warps through L1. Partials [slice][b][32·M + 32 + M] are reduced in slice
-// order by gn_finish_kernel (deterministic).
+// slice of the sampled rows. A warp takes 32 rows at a time with one row per
+// lane (coalesced loads of x̄, x̄_prev, f̄, f̄_prev, the 2x2 Jacobian block and
+// the Φ̄ rows), forms the residual r̄ and C = (I − h·J)Φ̄ rows in registers
+// (rom.hpp:71-84, the reference's rounding order), stages them in shared
+// memory and feeds A·C to DMMA (mma.sync m8n8k4 f64) 4 rows per k-step.
+// Partials [slice][b][32·M + 32 + M] are reduced in slice order by
+// gn_finish_kernel (deterministic).
 template <int M>
-__global__ void __launch_bounds__(256) gn_partial_kernel(DGnat g, EngineTables et, int B, double h,
+__global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat g, EngineTables et, int B, double h,
                                                          const double* __restrict__ xbar,
                                                          const double* __restrict__ xprev,
                                                          const double* __restrict__ fbar,
                                                          const double* __restrict__ fprev,
                                                          const double* __restrict__ jac, GnState st_,
                                                          long long slice_len, double* __restrict__ part) {
-  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M;
+  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M, CS = M + 4;
+  extern __shared__ double gn_smem[];  // per warp: 32 x CS C rows, then 32 residuals
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * 8 + warp;
   if (b >= B || !st_.active[b]) return;
@@ -643,40 +704,55 @@ __global__ void __launch_bounds__(256) gn_partial_kernel(DGnat g, EngineTables e
   }
 #pragma unroll
   for (int j = 0; j < TN; ++j) gr[j] = 0.0;
+  double* swc = gn_smem + warp * (32 * CS + 32);
+  double* swr = swc + 32 * CS;
   const long long k_begin = blockIdx.y * slice_len, k_end = min(rows, k_begin + slice_len);
-  for (long long k0 = k_begin; k0 < k_end; k0 += 4) {
-    const long long r = k0 + lc;
-    double rv = 0.0;
-    double cv[TN];
+  for (long long k0 = k_begin; k0 < k_end; k0 += 32) {
+    const long long r = k0 + lane;
+    __syncwarp();
     if (r < k_end) {
-      rv = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
-      const long long t = r < nt ? r : r - nt;
+      swr[lane] = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
+      const bool xrow = r < nt;
+      const long long t = xrow ? r : r - nt;
       const double4 J = *reinterpret_cast<const double4*>(jb + 4 * t);
+      const double ja = xrow ? J.x : J.z, jb_ = xrow ? J.y : J.w;
+      const double2* pxr = reinterpret_cast<const double2*>(et.pbr + t * M);
+      const double2* pyr = reinterpret_cast<const double2*>(et.pbr + (t + nt) * M);
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int m = j * 8 + lr;
-        const double px = et.pbr[t * M + m], py = et.pbr[(t + nt) * M + m];
-        const double own = r < nt ? px : py;
-        const double inner = r < nt ? __dadd_rn(__dmul_rn(J.x, px), __dmul_rn(J.y, py))
-                                    : __dadd_rn(__dmul_rn(J.z, px), __dmul_rn(J.w, py));
-        cv[j] = __dsub_rn(own, __dmul_rn(h, inner));
-        gr[j] = fma(cv[j], rv, gr[j]);
+      for (int m2 = 0; m2 < M / 2; ++m2) {
+        const double2 px = pxr[m2], py = pyr[m2];
+        const double own0 = xrow ? px.x : py.x, own1 = xrow ? px.y : py.y;
+        swc[lane * CS + 2 * m2] =
+            __dsub_rn(own0, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.x), __dmul_rn(jb_, py.x))));
+        swc[lane * CS + 2 * m2 + 1] =
+            __dsub_rn(own1, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.y), __dmul_rn(jb_, py.y))));
       }
     } else {
+      swr[lane] = 0.0;
 #pragma unroll
-      for (int j = 0; j < TN; ++j) cv[j] = 0.0;
+      for (int m = 0; m < M; ++m) swc[lane * CS + m] = 0.0;
     }
-    double av[TI];
+    __syncwarp();
+    const int steps = (int)min(8LL, (k_end - k0 + 3) / 4);
+    for (int s4 = 0; s4 < steps; ++s4) {
+      const int kk = 4 * s4 + lc;
+      const long long row = k0 + kk;
+      const double rvv = swr[kk];
+      double av[TI];
 #pragma unroll
-    for (int i = 0; i < TI; ++i) {
-      av[i] = r < k_end ? g.A[(i * 8 + lr) + r * MR] : 0.0;
-      ar[i] = fma(av[i], rv, ar[i]);
-    }
-    if (need_ac) {
+      for (int i = 0; i < TI; ++i) {
+        av[i] = row < k_end ? g.A[(i * 8 + lr) + row * MR] : 0.0;
+        ar[i] = fma(av[i], rvv, ar[i]);
+      }
 #pragma unroll
-      for (int i = 0; i < TI; ++i)
+      for (int j = 0; j < TN; ++j) {
+        const double cvv = swc[kk * CS + j * 8 + lr];
+        gr[j] = fma(cvv, rvv, gr[j]);
+        if (need_ac) {
 #pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc[i][j], av[i], cv[j]);
+          for (int i = 0; i < TI; ++i) dmma(acc[i][j], av[i], cvv);
+        }
+      }
     }
   }
   double* out = part + ((long long)blockIdx.y * B + b) * PART;
@@ -894,9 +970,14 @@ void rom_reconstruct(ptrom_ctx* ctx, const DBasis& b, long long n_steps, const d
   PTROM_LAUNCH_CHECK();
 }
 
+void rom_basis_rowmajor(ptrom_ctx* ctx, DBasis& b) {
+  PTROM_CUDA(cudaMalloc(&b.rm, sizeof(double) * std::max<long long>(1, b.n * 2 * (b.m + 1))));
+  basis_rowmajor_kernel<<<std::max(1, ctx->num_sms * 8), 256, 0, ctx->stream>>>(b);
+  PTROM_LAUNCH_CHECK();
+}
+
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma) {
-  const long long work = s.n_c * (s.m + 1);
-  if (work > 0) reassign_exact_kernel<<<blocks_for(work, 128), 128, 0, ctx->stream>>>(s, b, d_gamma);
+  if (s.n_c > 0) reassign_exact_kernel<<<blocks_for(s.n_c * 32, 256), 256, 0, ctx->stream>>>(s, b, d_gamma);
   if (s.u > 0) direct_gamma_kernel<<<blocks_for(s.u, 256), 256, 0, ctx->stream>>>(s, d_gamma);
   PTROM_LAUNCH_CHECK();
 }
@@ -980,11 +1061,13 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
   if (count_pairs) PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
   {
     ProfScope prof(ctx);
-    const long long threads = B >= 32 ? s.n_t * 32 * ((B + 31) / 32) : s.n_t * B;
-    hyperpair_kernel<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg,
-                                                                 w.dx, w.dy, w.dg, effective_delta(delta, form), delta,
-                                                                 d_inflow, n, d_active, d_f, d_jac, w.pairs,
-                                                                 ctx->d_status);
+    // IB = 32: one 256-byte segment per position row and instance chunk (8-instance
+    // chunks doubled the DRAM traffic: half-used L2 lines).
+    constexpr int IB = 32;
+    const long long threads = B >= IB ? ((s.n_t + 32 / IB - 1) / (32 / IB)) * 32 * ((B + IB - 1) / IB) : s.n_t * B;
+    hyperpair_kernel<IB><<<blocks_for(threads, 128), 128, 0, st>>>(
+        s, tt, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy, w.dg, effective_delta(delta, form), delta,
+        d_inflow, n, d_active, d_f, d_jac, w.pairs, ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
@@ -1081,8 +1164,10 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
   }
   // split-K shape: ~4 CTAs per SM over ceil(B/8) instance groups
   const long long groups = (B + 7) / 8;
-  const int S = (int)std::max<long long>(1, std::min<long long>(64, (4LL * ctx->num_sms + groups - 1) / groups));
-  const long long slice_len = ((rows + S - 1) / S + 3) / 4 * 4;
+  const int S = (int)std::max<long long>(1, std::min<long long>(64, (8LL * ctx->num_sms + groups - 1) / groups));
+  const long long slice_len = ((rows + S - 1) / S + 31) / 32 * 32;
+  const size_t gn_smem = (size_t)8 * (32 * (MP + 4) + 32) * sizeof(double);
+  PTROM_CUDA(cudaFuncSetAttribute(gn_partial_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gn_smem));
   double* part = (double*)alloc((size_t)S * B * (32 * MP + 32 + MP) * 8);
   int* h_active = nullptr;
   PTROM_CUDA(cudaMallocHost(&h_active, 4));
@@ -1099,9 +1184,8 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
                   jac, false);
     while (true) {
       PTROM_CUDA(cudaMemsetAsync(gs.n_active, 0, 4, st));
-      gn_partial_kernel<MP><<<dim3((unsigned)((B + 7) / 8), (unsigned)S), 256, 0, st>>>(g, et, B, h, xbar, xprev,
-                                                                                      fbar, fprev, jac, gs,
-                                                                                      slice_len, part);
+      gn_partial_kernel<MP><<<dim3((unsigned)((B + 7) / 8), (unsigned)S), 256, gn_smem, st>>>(
+          g, et, B, h, xbar, xprev, fbar, fprev, jac, gs, slice_len, part);
       gn_finish_kernel<MP><<<B, 128, 0, st>>>(B, S, part, gs);
       PTROM_LAUNCH_CHECK();
       PTROM_CUDA(cudaMemcpyAsync(h_active, gs.n_active, 4, cudaMemcpyDeviceToHost, st));

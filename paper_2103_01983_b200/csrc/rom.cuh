@@ -12,6 +12,9 @@ struct DBasis {
   double* phi = nullptr;
   double* x_ref = nullptr;
   double* sv = nullptr;
+  // Row-major copy for member gathers: particle p owns rm[p·2(m+1) ...]:
+  // x row (Φ(p, 0..m-1), x_ref[p]) then y row (Φ(p+n, ·), x_ref[p+n]).
+  double* rm = nullptr;
 };
 
 // GnatOperator (reduction.hpp:173-180) + the solver's gathered rows

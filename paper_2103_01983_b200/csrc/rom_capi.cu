@@ -9,6 +9,7 @@
 
 namespace ptrom {
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma);
+void rom_basis_rowmajor(ptrom_ctx* ctx, DBasis& b);
 void rom_reconstruct(ptrom_ctx* ctx, const DBasis& b, long long n_steps, const double* d_xhat, long long n_out,
                      const long long* d_dofs, double* d_out);
 void rom_affine_tables(ptrom_ctx* ctx, const DSurrogate& s, const DBasis& b, const double* d_ga, const double* d_gb,
@@ -117,6 +118,8 @@ int ptrom_basis_create(ptrom_ctx* ctx, int64_t n_dofs, int64_t modes, const doub
       h->b.phi = h->mem.up(phi, (size_t)(n_dofs * modes));
       h->b.x_ref = h->mem.up(x_ref, (size_t)n_dofs);
       h->b.sv = h->mem.up(singular_values, singular_values ? (size_t)modes : 0);
+      rom_basis_rowmajor(ctx, h->b);
+      h->mem.p.push_back(h->b.rm);
     } catch (...) {
       delete h;
       throw;
