@@ -468,19 +468,62 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
         ++cnt;
       };
       const double mub = mu ? mu[b] : 0.0;
-      for (long long k = s.cl_off[t]; k < s.cl_off[t + 1]; ++k) {
+      auto cgam = [&](long long ci) { return mu ? fma(mub, at.gb[ci], at.ga[ci]) : s.gamma_tilde[ci]; };
+      // Cluster list, U entries per round: the U list reads, then the 2U
+      // position loads are issued before any arithmetic (memory-level
+      // parallelism for the L2/HBM-latency-bound gathers); order of the
+      // accumulation is unchanged.
+      constexpr int U = 4;
+      long long k = s.cl_off[t];
+      const long long ke = s.cl_off[t + 1];
+      for (; k + U <= ke; k += U) {
+        long long ci[U];
+        double sx[U], sy[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ci[u] = s.cl_list[k + u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          sx[u] = cx[ci[u] * B + b];
+          sy[u] = cy[ci[u] * B + b];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (delta == 0.0 && sx[u] == px && sy[u] == py) continue;
+          add(sx[u], sy[u], cgam(ci[u]));
+        }
+      }
+      for (; k < ke; ++k) {
         const long long ci = s.cl_list[k];
         const long long c = ci * B + b;
         const double sx = cx[c], sy = cy[c];
         if (delta == 0.0 && sx == px && sy == py) continue;
-        add(sx, sy, mu ? fma(mub, at.gb[ci], at.ga[ci]) : s.gamma_tilde[ci]);
+        add(sx, sy, cgam(ci));
       }
       const long long pid = s.target_ids[t];
-      for (long long k = s.d_off[t]; k < s.d_off[t + 1]; ++k) {
-        const long long loc = s.d_list[k];
+      auto dgam = [&](long long loc) { return mu ? fma(mub, at.dgb[loc], at.dga[loc]) : s.direct_gamma[loc]; };
+      long long kd = s.d_off[t];
+      const long long kde = s.d_off[t + 1];
+      for (; kd + 4 <= kde; kd += 4) {
+        long long loc[4];
+        double sx[4], sy[4];
+        bool me[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) loc[u] = s.d_list[kd + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          me[u] = s.direct_ids[loc[u]] == pid;
+          sx[u] = dx[loc[u] * B + b];
+          sy[u] = dy[loc[u] * B + b];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (!me[u]) add(sx[u], sy[u], dgam(loc[u]));
+      }
+      for (; kd < kde; ++kd) {
+        const long long loc = s.d_list[kd];
         if (s.direct_ids[loc] == pid) continue;
         const long long d = loc * B + b;
-        add(dx[d], dy[d], mu ? fma(mub, at.dgb[loc], at.dga[loc]) : s.direct_gamma[loc]);
+        add(dx[d], dy[d], dgam(loc));
       }
       if (inflow) {
         fx = fx + inflow[pid];
