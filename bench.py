@@ -301,7 +301,7 @@ def main():
                     "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_dfma_tflops"],
                     "traffic": ncu_traffic("r01_allpairs_vel64_ncu_summary.json"),
                     "algorithmic_bytes_per_launch": 24 * n,
-                    "kernel": "allpairs_f64_kernel<64,8,2,1,vel> (csrc/allpairs.cu)",
+                    "kernel": "allpairs_f64_kernel<128,8,2,1,vel> (csrc/allpairs.cu)",
                     "peak_source": "measured live: tools/peaks.cu DFMA chain (MEASURED_PEAKS.json has no FP64)",
                     "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": local_pairs,
                     "avg_launch_ms": avg_kernel_s * 1e3, "launches": kern_launches.value,

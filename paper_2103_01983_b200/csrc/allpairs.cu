@@ -102,7 +102,7 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
   for (int jj = 0; jj < cnt; ++jj) {
     const double2 p = sp[jj];
     const double g = sg[jj];
-    if (FAST == 4 && !MASK && (T % 4 == 0)) {
+    if ((FAST == 4 || FAST == 5) && !MASK && (T % 4 == 0)) {
       // four targets share one reciprocal: P = (q1 q2)(q3 q4), q ∈ [2^-31, 2^31]
 #pragma unroll
       for (int k = 0; k < T; k += 4) {
@@ -115,9 +115,17 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
         }
         const double p01 = q[0] * q[1], p23 = q[2] * q[3];
         const double P = p01 * p23;
-        const double y0 = rcp_seed_via_f32(P);
-        const double e = fma(-P, y0, 1.0);
-        const double uP = fma(y0, e, y0);  // 1/P
+        double uP;  // 1/P
+        if (FAST == 5) {  // MUFU.RCP64H seed (~2^-20) + cubic correction
+          const double y0 = rcp_seed(P);
+          double e = fma(-P, y0, 1.0);
+          e = fma(e, e, e);
+          uP = fma(y0, e, y0);
+        } else {  // fp32 seed via exponent rebias (≤ 2^-22) + one Newton step
+          const double y0 = rcp_seed_via_f32(P);
+          const double e = fma(-P, y0, 1.0);
+          uP = fma(y0, e, y0);
+        }
         if (JAC) {
           const double u01 = uP * p23, u23 = uP * p01;  // 1/(q0 q1), 1/(q2 q3)
           const double u[4] = {u01 * q[1], u01 * q[0], u23 * q[3], u23 * q[2]};
@@ -182,7 +190,7 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
   }
 }
 
-template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC>
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4>
 __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, const double* __restrict__ xs,
                                                            const double* __restrict__ ys,
                                                            const double* __restrict__ gam, double inv2pi,
@@ -243,11 +251,14 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
       py = ys[jn];
       pg = gam[jn] * inv2pi;
     }
-    const bool masked = self_excl && (j0 < tile_end) && (tile0 < j0 + cnt);
+    // The self pair (kernel.hpp:118 skips j == i) needs masking only for the
+    // Jacobian or on the safe path: on the fast paths δ' > 0, so for the
+    // velocity it has r = 0, q = δ', s finite and adds exactly ±0 to f.
+    const bool masked = self_excl && (j0 < tile_end) && (tile0 < j0 + cnt) && (JAC || !fast);
     if (masked)
       tile_f64<T, UNR, VEL, JAC, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else if (fast4)
-      tile_f64<T, UNR, VEL, JAC, false, 4>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      tile_f64<T, UNR, VEL, JAC, false, F4>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else if (fast)
       tile_f64<T, UNR, VEL, JAC, false, 2>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
     else
@@ -485,11 +496,11 @@ int reduce_grid(ptrom_ctx* ctx, long long count) {
   return (int)std::max(1LL, std::min(g, (long long)ctx->num_sms * 8));
 }
 
-template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC>
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4>
 void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                            long long t_begin, long long t_count, double** part_out, int* chunks_out,
                            const double* tx, const double* ty) {
-  auto kern = allpairs_f64_kernel<TPB, T, UNR, MINB, VEL, JAC>;
+  auto kern = allpairs_f64_kernel<TPB, T, UNR, MINB, VEL, JAC, F4>;
   static int occ = resident_blocks(kern, TPB);
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   const long long tiles = (t_count + TPB * T - 1) / (TPB * T);
@@ -517,16 +528,27 @@ using LaunchFn = void (*)(ptrom_ctx*, long long, const double*, const double*, d
 // Velocity-kernel shapes (TPB, targets/thread, source unroll, min blocks/SM);
 // entry 0 is the default, the rest are kept for tools/tune_allpairs.py
 // (PTROM_ALLPAIRS_VARIANT selects one at context creation). Sweep on B200 at
-// N = 65,536 (profiles/r01_allpairs_tuning.md): (64,8,2,1) 21.2 TFLOP/s,
-// (128,8,2,1) 21.0, (128,4,8,4) 20.9, (128,8,3,1) 20.4, (64,8,2,6) 20.2.
+// N = 65,536 with the unmasked fast diagonal (profiles/r01_tune_allpairs_sweeps.jsonl):
+// (128,8,2,1) 21.6 TFLOP/s, (64,8,2,1) 21.4, (128,8,4,1) 21.4, (64,8,4,1) 21.2,
+// (128,4,8,4) 21.1, (32,8,2,1) 21.1, (128,8,3,1) 21.0, (64,8,3,1) 20.8.
 #define PTROM_VEL_VARIANTS(X) \
-  X(64, 8, 2, 1)              \
-  X(128, 8, 2, 1)             \
-  X(128, 4, 8, 4)             \
-  X(128, 8, 3, 1)             \
-  X(64, 8, 2, 6)
+  X(128, 8, 2, 1, 4)          \
+  X(64, 8, 2, 1, 4)           \
+  X(128, 4, 8, 4, 4)          \
+  X(128, 8, 3, 1, 4)          \
+  X(64, 8, 2, 6, 4)           \
+  X(64, 8, 4, 1, 4)           \
+  X(64, 8, 3, 1, 4)           \
+  X(128, 8, 4, 1, 4)          \
+  X(64, 12, 2, 1, 4)          \
+  X(96, 8, 2, 1, 4)           \
+  X(32, 8, 2, 1, 4)           \
+  X(64, 16, 1, 1, 4)          \
+  X(128, 8, 2, 1, 5)          \
+  X(64, 8, 2, 1, 5)           \
+  X(128, 8, 4, 1, 5)
 
-#define PTROM_VEL_ENTRY(TPB, T, UNR, MINB) launch_allpairs_f64_t<TPB, T, UNR, MINB, true, false>,
+#define PTROM_VEL_ENTRY(TPB, T, UNR, MINB, F4) launch_allpairs_f64_t<TPB, T, UNR, MINB, true, false, F4>,
 const LaunchFn kVelVariants[] = {PTROM_VEL_VARIANTS(PTROM_VEL_ENTRY)};
 constexpr int kNumVelVariants = sizeof(kVelVariants) / sizeof(kVelVariants[0]);
 
