@@ -285,6 +285,32 @@ def main():
                "h2d_bytes_per_step": int(hx.nbytes + hg.nbytes), "d2h_bytes_per_step": int(hf.nbytes),
                "api": "ptrom_pairwise_velocity_f64 (host buffers)"}
         del sys_
+    else:
+        # Sharded end to end: every step each rank copies its own positions in
+        # from pinned host memory, all-gathers the sources, evaluates its
+        # targets and copies its velocity rows back out (max over ranks).
+        hx_local = x_local.cpu().pin_memory()
+        hf_local = torch.empty(2 * m, dtype=torch.float64).pin_memory()
+        e2e_steps = max(5, min(args.steps, 50))
+
+        def e2e_step():
+            x_local.copy_(hx_local, non_blocking=True)
+            step()
+            hf_local.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(3):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs_per_step * e2e_steps / float(e2e_s.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(hx_local.numel() * 8 * world),
+               "d2h_bytes_per_step": int(hf_local.numel() * 8 * world),
+               "api": "per rank: H2D own positions, NCCL all-gather, ptrom_dev_pairwise_velocity_f64, D2H own rows"}
 
     if rank != 0:
         if world > 1:

@@ -558,7 +558,7 @@ template <bool VEL, bool JAC>
 void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                          long long t_begin, long long t_count, double** part, int* chunks,
                          const double* tx = nullptr, const double* ty = nullptr) {
-  if (t_count < 16384) {
+  if (t_count < 4096) {
     launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
   } else if (VEL && !JAC) {
     const int v = (ctx->allpairs_variant >= 0 && ctx->allpairs_variant < kNumVelVariants) ? ctx->allpairs_variant : 0;
