@@ -224,11 +224,41 @@ def main():
     ctx = pt.default_context(local)
     stream = torch.cuda.current_stream()
 
-    def step():
-        if world > 1:  # per-evaluation exchange: allgather source positions (x then y) over NVLink
+    def step_allgather():  # per-evaluation exchange: NCCL all-gather of the positions, then the local kernel
+        if world > 1:
             dist.all_gather_into_tensor(x_full[:n], x_local[0])
             dist.all_gather_into_tensor(x_full[n:], x_local[1])
         dev.pairwise_velocity(x_full, gamma, w.delta, 0, None, lo, hi, out, ctx=ctx)
+
+    # N > 1: the exchange fused into the kernel — each rank publishes its block
+    # in CUDA-IPC memory and the tile loads read the peers' blocks in place over
+    # NVLink (paper_2103_01983_b200/peer.py). Verified once against the
+    # all-gather path; PTROM_EXCHANGE=nccl selects the all-gather path.
+    exchange = "single-gpu"
+    step = step_allgather
+    if world > 1:
+        exchange = "nccl-allgather"
+        if os.environ.get("PTROM_EXCHANGE", "peer") == "peer":
+            try:
+                from paper_2103_01983_b200.peer import PeerExchange
+                pex = PeerExchange(n, ctx)
+                token = torch.zeros(1, dtype=torch.float32, device="cuda")
+
+                def step_peer():
+                    pex.write_local(x_local)
+                    pex.barrier(token)
+                    pex.velocity(gamma, w.delta, out)
+
+                step_allgather()
+                ref_out = out.clone()
+                step_peer()
+                dev.synchronize(ctx)
+                same = torch.tensor([1.0 if torch.equal(out, ref_out) else 0.0], device="cuda")
+                dist.all_reduce(same, op=dist.ReduceOp.MIN)
+                if float(same.item()) == 1.0:
+                    exchange, step = "peer-ipc (fused into the tile loads)", step_peer
+            except Exception as exc:  # keep the NCCL path; say why in the JSON line
+                exchange = f"nccl-allgather (peer setup failed: {type(exc).__name__})"
 
     for _ in range(args.warmup):
         step()
@@ -344,7 +374,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
         "config": {"workload": w.name, "n": n, "delta": w.delta, "targets_per_rank": m,
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
-                   "parallelism": f"targets sharded x{world}, NCCL allgather of positions per step"
+                   "parallelism": f"targets sharded x{world}, position exchange per step: {exchange}"
                    if world > 1 else "single GPU"},
         "gpu_launches": 2 * args.steps,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),

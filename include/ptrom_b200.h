@@ -101,6 +101,29 @@ int ptrom_dev_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d_x
 int ptrom_dev_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* d_x, const float* d_gamma,
                                     float delta, int form, const float* d_inflow, int64_t t_begin,
                                     int64_t t_end, float* d_f, int64_t ld_f);
+/* Target-sharded velocity with the sources read in place from every rank's
+ * HBM (the per-evaluation position exchange fused into the
+ * tile loads over NVLink instead of an all-gather). Rank r's block of
+ * particles [peer_offsets[r], peer_offsets[r+1]) is SoA (x then y) at device
+ * pointer d_peer_blocks[r] (own block or a CUDA-IPC mapping of a peer's,
+ * see ptrom_ipc_*); d_peer_blocks / peer_offsets are host arrays. Targets are
+ * this rank's rows [t_begin, t_end), SoA at d_local. Γ and the inflow are the
+ * full replicated n- and 2n-vectors. Output as ptrom_dev_pairwise_velocity_f64.
+ * kernel.hpp:107-129 restricted to rows. n_peers <= 8. */
+int ptrom_dev_pairwise_velocity_peers_f64(ptrom_ctx* ctx, int64_t n, int32_t n_peers,
+                                          const double* const* d_peer_blocks, const int64_t* peer_offsets,
+                                          const double* d_gamma, double delta, int form, const double* d_inflow,
+                                          int64_t t_begin, int64_t t_end, const double* d_local, double* d_f,
+                                          int64_t ld_f);
+/* CUDA IPC helpers for the peer exchange: an IPC-shareable device buffer,
+ * its 64-byte handle, mapping a peer's handle into this process, and a
+ * stream-ordered device copy (cudaMemcpyDefault: local or peer memory). */
+int ptrom_ipc_alloc(ptrom_ctx* ctx, uint64_t bytes, void** d_ptr);
+int ptrom_ipc_free(ptrom_ctx* ctx, void* d_ptr);
+int ptrom_ipc_get_handle(ptrom_ctx* ctx, void* d_ptr, uint8_t* handle64);
+int ptrom_ipc_open_handle(ptrom_ctx* ctx, const uint8_t* handle64, void** d_ptr);
+int ptrom_ipc_close_handle(ptrom_ctx* ctx, void* d_ptr);
+int ptrom_dev_memcpy(ptrom_ctx* ctx, void* d_dst, const void* d_src, uint64_t bytes);
 /* kernel.hpp:154-170 restricted to rows [t_begin, t_end); four vectors of
  * length t_end - t_begin. */
 int ptrom_dev_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* d_x,

@@ -39,6 +39,15 @@ PROTOTYPES = {
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, c_i64, c_i64, c_dp, c_i64]),
     "ptrom_dev_pairwise_velocity_f32": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_float, C.c_int, c_dp, c_i64, c_i64, c_dp, c_i64]),
+    "ptrom_dev_pairwise_velocity_peers_f64": (
+        C.c_int, [c_ctxp, c_i64, C.c_int32, C.c_void_p, C.c_void_p, c_dp, C.c_double, C.c_int, c_dp, c_i64, c_i64,
+                  c_dp, c_dp, c_i64]),
+    "ptrom_ipc_alloc": (C.c_int, [c_ctxp, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "ptrom_ipc_free": (C.c_int, [c_ctxp, C.c_void_p]),
+    "ptrom_ipc_get_handle": (C.c_int, [c_ctxp, C.c_void_p, C.c_void_p]),
+    "ptrom_ipc_open_handle": (C.c_int, [c_ctxp, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ptrom_ipc_close_handle": (C.c_int, [c_ctxp, C.c_void_p]),
+    "ptrom_dev_memcpy": (C.c_int, [c_ctxp, C.c_void_p, C.c_void_p, C.c_uint64]),
     "ptrom_hamiltonian_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, c_dp]),
     "ptrom_velocity_field_grid_f64": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_double, C.c_double, c_i64, C.c_double,

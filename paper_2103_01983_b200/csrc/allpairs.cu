@@ -40,6 +40,8 @@
 
 namespace ptrom {
 
+constexpr int kMaxPeers = 8;  // ranks whose source blocks one kernel reads in place
+
 __device__ __forceinline__ double rcp_seed(double q) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
@@ -190,17 +192,45 @@ __device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp
   }
 }
 
-template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4>
-__global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, const double* __restrict__ xs,
-                                                           const double* __restrict__ ys,
+// Source position loaders. SrcFlat: the SoA state of one device.
+// SrcPeers: the sources are split over G ranks (offsets off[0..G]); rank r's
+// SoA block (x then y, off[r+1]-off[r] each) lives in its own HBM and is read
+// in place over NVLink (CUDA IPC mappings) — the per-evaluation exchange of
+// the sharded FOM fused into the tile loads instead of an all-gather.
+struct SrcFlat {
+  const double* xs;
+  const double* ys;
+  __device__ __forceinline__ void load(long long j, double& x, double& y) const {
+    x = xs[j];
+    y = ys[j];
+  }
+};
+struct SrcPeers {
+  const double* base[kMaxPeers];
+  long long off[kMaxPeers + 1];
+  int G;
+  __device__ __forceinline__ void load(long long j, double& x, double& y) const {
+    int r = 0;
+#pragma unroll
+    for (int q = 1; q < kMaxPeers; ++q) r += (q < G && j >= off[q]) ? 1 : 0;
+    const long long jl = j - off[r], m = off[r + 1] - off[r];
+    x = base[r][jl];
+    y = base[r][m + jl];
+  }
+};
+
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4, class Src = SrcFlat>
+__global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, Src src,
                                                            const double* __restrict__ gam, double inv2pi,
                                                            double dp, long long t_begin, long long t_count,
                                                            long long chunk_len, double* __restrict__ part,
                                                            const double* __restrict__ txs,
-                                                           const double* __restrict__ tys, int self_excl) {
-  // Targets are rows of (txs, tys); self_excl = targets are the sources
-  // themselves (txs == xs), so pair (i, i) is skipped. External targets
-  // (lattice vertices, kernel.hpp:213-238) pass self_excl = 0.
+                                                           const double* __restrict__ tys, long long t_base,
+                                                           int self_excl) {
+  // Targets i in [t_begin, t_begin + t_count) are rows i - t_base of
+  // (txs, tys); self_excl = targets are sources with the same global index,
+  // so pair (i, i) is skipped. External targets (lattice vertices,
+  // kernel.hpp:213-238) pass self_excl = 0.
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   __shared__ double2 sp[TPB];
   __shared__ double sg[TPB];
@@ -214,8 +244,8 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
     const long long i = tile0 + k * TPB + tid;
     const bool ok = i < t_begin + t_count;
     ti[k] = ok ? i : -1;
-    tx[k] = ok ? txs[i] : 0.0;
-    ty[k] = ok ? tys[i] : 0.0;
+    tx[k] = ok ? txs[i - t_base] : 0.0;
+    ty[k] = ok ? tys[i - t_base] : 0.0;
     fx[k] = fy[k] = ja[k] = jb[k] = jc[k] = 0.0;
   }
   const long long tile_end = min(tile0 + (long long)TPB * T, t_begin + t_count);
@@ -235,8 +265,7 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
   // Register prefetch of the first source tile.
   double px = 0.0, py = 0.0, pg = 0.0;
   if (cbeg + tid < cend) {
-    px = xs[cbeg + tid];
-    py = ys[cbeg + tid];
+    src.load(cbeg + tid, px, py);
     pg = gam[cbeg + tid] * inv2pi;
   }
   for (long long j0 = cbeg; j0 < cend; j0 += TPB) {
@@ -247,8 +276,7 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, co
     const bool fast = fast4 || (__syncthreads_and(coord_ok(px) && coord_ok(py)) && targets_ok);
     const long long jn = j0 + TPB + tid;  // prefetch the next tile while computing
     if (jn < cend) {
-      px = xs[jn];
-      py = ys[jn];
+      src.load(jn, px, py);
       pg = gam[jn] * inv2pi;
     }
     // The self pair (kernel.hpp:118 skips j == i) needs masking only for the
@@ -496,11 +524,11 @@ int reduce_grid(ptrom_ctx* ctx, long long count) {
   return (int)std::max(1LL, std::min(g, (long long)ctx->num_sms * 8));
 }
 
-template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4>
-void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
-                           long long t_begin, long long t_count, double** part_out, int* chunks_out,
-                           const double* tx, const double* ty) {
-  auto kern = allpairs_f64_kernel<TPB, T, UNR, MINB, VEL, JAC, F4>;
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4, class Src>
+void launch_allpairs_src(ptrom_ctx* ctx, long long n, Src src, const double* gamma, double dp, long long t_begin,
+                         long long t_count, double** part_out, int* chunks_out, const double* tx, const double* ty,
+                         long long t_base, int self_excl) {
+  auto kern = allpairs_f64_kernel<TPB, T, UNR, MINB, VEL, JAC, F4, Src>;
   static int occ = resident_blocks(kern, TPB);
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   const long long tiles = (t_count + TPB * T - 1) / (TPB * T);
@@ -513,17 +541,32 @@ void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const d
   const double inv2pi = 1.0 / (2.0 * M_PI);
   {
     ProfScope prof(ctx);
-    const bool external = tx != nullptr;
-    kern<<<grid, TPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part,
-                                        external ? tx : x, external ? ty : x + n, external ? 0 : 1);
+    kern<<<grid, TPB, 0, ctx->stream>>>(n, src, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part, tx, ty, t_base,
+                                        self_excl);
   }
   PTROM_LAUNCH_CHECK();
   *part_out = part;
   *chunks_out = chunks;
 }
 
+template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4>
+void launch_allpairs_f64_t(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
+                           long long t_begin, long long t_count, double** part_out, int* chunks_out,
+                           const double* tx, const double* ty, const SrcPeers* peers, long long t_base) {
+  if (peers) {
+    launch_allpairs_src<TPB, T, UNR, MINB, VEL, JAC, F4>(ctx, n, *peers, gamma, dp, t_begin, t_count, part_out,
+                                                         chunks_out, tx, ty, t_base, 1);
+    return;
+  }
+  const bool external = tx != nullptr;
+  launch_allpairs_src<TPB, T, UNR, MINB, VEL, JAC, F4>(ctx, n, SrcFlat{x, x + n}, gamma, dp, t_begin, t_count,
+                                                       part_out, chunks_out, external ? tx : x,
+                                                       external ? ty : x + n, external ? t_base : 0,
+                                                       external ? 0 : 1);
+}
+
 using LaunchFn = void (*)(ptrom_ctx*, long long, const double*, const double*, double, long long, long long,
-                          double**, int*, const double*, const double*);
+                          double**, int*, const double*, const double*, const SrcPeers*, long long);
 
 // Velocity-kernel shapes (TPB, targets/thread, source unroll, min blocks/SM);
 // entry 0 is the default, the rest are kept for tools/tune_allpairs.py
@@ -557,14 +600,17 @@ constexpr int kNumVelVariants = sizeof(kVelVariants) / sizeof(kVelVariants[0]);
 template <bool VEL, bool JAC>
 void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                          long long t_begin, long long t_count, double** part, int* chunks,
-                         const double* tx = nullptr, const double* ty = nullptr) {
+                         const double* tx = nullptr, const double* ty = nullptr, const SrcPeers* peers = nullptr,
+                         long long t_base = 0) {
   if (t_count < 4096) {
-    launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
+    launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty,
+                                                   peers, t_base);
   } else if (VEL && !JAC) {
     const int v = (ctx->allpairs_variant >= 0 && ctx->allpairs_variant < kNumVelVariants) ? ctx->allpairs_variant : 0;
-    kVelVariants[v](ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
+    kVelVariants[v](ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty, peers, t_base);
   } else {
-    launch_allpairs_f64_t<kTPB, 4, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty);
+    launch_allpairs_f64_t<kTPB, 4, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty,
+                                                   peers, t_base);
   }
 }
 
@@ -722,6 +768,32 @@ void dev_hamiltonian_f64(ptrom_ctx* ctx, long long n, const double* x, const dou
   PTROM_LAUNCH_CHECK();
   hamiltonian_reduce_kernel<<<kHamBlocks, kReduceThreads, 0, ctx->stream>>>(n, chunks, part, gamma, bs);
   hamiltonian_finish_kernel<<<1, 32, 0, ctx->stream>>>(kHamBlocks, bs, out);
+  PTROM_LAUNCH_CHECK();
+}
+
+// Target-sharded velocity reading the other ranks' source blocks in place
+// (SrcPeers): rows [t_begin, t_end) are this rank's particles, stored at
+// tx/ty (row i at tx[i - t_begin]); Γ and the inflow are full replicated
+// arrays. Result as dev_velocity_f64.
+void dev_velocity_peers_f64(ptrom_ctx* ctx, long long n, int n_peers, const double* const* peer_base,
+                            const long long* peer_off, const double* gamma, double delta, int form,
+                            const double* inflow, long long t_begin, long long t_end, const double* tx,
+                            const double* ty, double* f, long long ld) {
+  const long long t_count = t_end - t_begin;
+  if (t_count <= 0) return;
+  if (n_peers < 1 || n_peers > kMaxPeers) throw status_error(PTROM_CONFIG_ERROR, "peer count outside [1, 8]");
+  SrcPeers sp{};
+  sp.G = n_peers;
+  for (int r = 0; r < n_peers; ++r) sp.base[r] = peer_base[r];
+  for (int r = 0; r <= n_peers; ++r) sp.off[r] = peer_off[r];
+  for (int r = n_peers + 1; r <= kMaxPeers; ++r) sp.off[r] = n;
+  for (int r = n_peers; r < kMaxPeers; ++r) sp.base[r] = nullptr;
+  double* part;
+  int chunks;
+  launch_allpairs_f64<true, false>(ctx, n, nullptr, gamma, effective_delta(delta, form), t_begin, t_count, &part,
+                                   &chunks, tx, ty, &sp, t_begin);
+  reduce_velocity_f64_kernel<<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+      n, t_begin, t_count, chunks, part, 2, inflow, f, ld, ctx->d_status);
   PTROM_LAUNCH_CHECK();
 }
 

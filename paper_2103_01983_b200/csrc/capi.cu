@@ -6,7 +6,9 @@
 #include <climits>
 #include <cstdlib>
 #include <cmath>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "ops.cuh"
 
@@ -350,6 +352,61 @@ int ptrom_dev_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* d_x,
     if (ld_f < t_end - t_begin) config_fail("ld_f smaller than the row count");
     dev_velocity_f32(ctx, n, d_x, d_gamma, delta, form, d_inflow, t_begin, t_end, d_f, ld_f);
   });
+}
+
+int ptrom_dev_pairwise_velocity_peers_f64(ptrom_ctx* ctx, int64_t n, int32_t n_peers,
+                                          const double* const* d_peer_blocks, const int64_t* peer_offsets,
+                                          const double* d_gamma, double delta, int form, const double* d_inflow,
+                                          int64_t t_begin, int64_t t_end, const double* d_local, double* d_f,
+                                          int64_t ld_f) {
+  return guarded(ctx, [&] {
+    check_rows(n, t_begin, t_end);
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    if (n_peers < 1 || n_peers > 8) config_fail("peer count outside [1, 8]");
+    if (!d_peer_blocks || !peer_offsets) config_fail("null peer table");
+    if (peer_offsets[0] != 0 || peer_offsets[n_peers] != n) config_fail("peer offsets must span [0, n]");
+    for (int r = 0; r < n_peers; ++r) {
+      if (peer_offsets[r + 1] < peer_offsets[r]) config_fail("peer offsets must be non-decreasing");
+      if (!d_peer_blocks[r] && peer_offsets[r + 1] > peer_offsets[r]) config_fail("null peer block");
+    }
+    if (ld_f < t_end - t_begin) config_fail("ld_f smaller than the row count");
+    const long long m = t_end - t_begin;
+    std::vector<long long> off(peer_offsets, peer_offsets + n_peers + 1);
+    dev_velocity_peers_f64(ctx, n, n_peers, d_peer_blocks, off.data(), d_gamma, delta, form, d_inflow, t_begin,
+                           t_end, d_local, d_local + m, d_f, ld_f);
+  });
+}
+
+// ---- CUDA IPC for the peer-memory exchange (one process per GPU) ----
+int ptrom_ipc_alloc(ptrom_ctx* ctx, uint64_t bytes, void** d_ptr) {
+  return guarded(ctx, [&] {
+    if (!d_ptr) config_fail("null output pointer");
+    PTROM_CUDA(cudaMalloc(d_ptr, std::max<uint64_t>(bytes, 8)));
+  });
+}
+int ptrom_ipc_free(ptrom_ctx* ctx, void* d_ptr) {
+  return guarded(ctx, [&] { PTROM_CUDA(cudaFree(d_ptr)); });
+}
+int ptrom_ipc_get_handle(ptrom_ctx* ctx, void* d_ptr, uint8_t* handle64) {
+  return guarded(ctx, [&] {
+    cudaIpcMemHandle_t h;
+    PTROM_CUDA(cudaIpcGetMemHandle(&h, d_ptr));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+  });
+}
+int ptrom_ipc_open_handle(ptrom_ctx* ctx, const uint8_t* handle64, void** d_ptr) {
+  return guarded(ctx, [&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    PTROM_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+int ptrom_ipc_close_handle(ptrom_ctx* ctx, void* d_ptr) {
+  return guarded(ctx, [&] { PTROM_CUDA(cudaIpcCloseMemHandle(d_ptr)); });
+}
+int ptrom_dev_memcpy(ptrom_ctx* ctx, void* d_dst, const void* d_src, uint64_t bytes) {
+  return guarded(ctx, [&] { PTROM_CUDA(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDefault, ctx->stream)); });
 }
 
 int ptrom_dev_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,

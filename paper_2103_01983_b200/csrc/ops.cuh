@@ -16,6 +16,10 @@ void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* 
 void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
                       long long t_begin, long long t_end, double* jxx, double* jxy, double* jyx, double* jyy,
                       double dt_for_inverse, double* inv);
+void dev_velocity_peers_f64(ptrom_ctx* ctx, long long n, int n_peers, const double* const* peer_base,
+                            const long long* peer_off, const double* gamma, double delta, int form,
+                            const double* inflow, long long t_begin, long long t_end, const double* tx,
+                            const double* ty, double* f, long long ld);
 void dev_hamiltonian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double* out);
 void dev_velocity_field_grid_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta,
                                  int form, double x_min, double x_max, long long nx, double y_min, double y_max,
