@@ -9,6 +9,7 @@
 
 #include "ptrom_b200.hpp"
 #include "ptrom_oracle.hpp"
+#include "ptrom_oracle_tree.hpp"
 
 struct GpuModel {  // Model concept over the adapter, returning oracle types
   ptrom_b200::PairwiseModelVec m;
@@ -58,5 +59,39 @@ int main() {
     threw = true;
   }
   std::printf("coincident pair -> numerical_error: %s\n", threw ? "yes" : "no");
-  return (worst <= 1e-12 && threw) ? 0 : 1;
+  // BarnesHutModelVec (integrators.hpp:83-102) vs the oracle's BarnesHutModel
+  const int nb = 5000;
+  std::vector<double> xb(2 * nb), gb(nb);
+  for (int i = 0; i < nb; ++i) {
+    const double a = 2.399963 * i, r = std::sqrt((i + 0.5) / nb);
+    xb[i] = r * std::cos(a);
+    xb[i + nb] = r * std::sin(a);
+    gb[i] = 1.0 / nb;
+  }
+  ptrom_b200::BarnesHutModelVec bh(ctx, gb, 1e-4, PTROM_CRIT_BARNES_HUT, 0.5, 16);
+  oracle::ParticleSystem<double> sb;
+  sb.circulation = gb;
+  sb.delta = 1e-4;
+  oracle::BarnesHutModel<double> obh{sb, oracle::ClusterCriterion<double>::barnes_hut(0.5), 16};
+  const auto fv = bh.velocity(xb), ov = obh.velocity(xb);
+  const auto jg = bh.jacobian(xb);
+  const auto jo = obh.jacobian(xb);
+  double num = 0, den = 0, jn = 0, jd = 0;
+  for (int k = 0; k < 2 * nb; ++k) {
+    num += (fv[k] - ov[k]) * (fv[k] - ov[k]);
+    den += ov[k] * ov[k];
+  }
+  for (int k = 0; k < nb; ++k) {
+    const double d[4] = {jg.dfx_dx[k] - jo.dfx_dx[k], jg.dfx_dy[k] - jo.dfx_dy[k], jg.dfy_dx[k] - jo.dfy_dx[k],
+                         jg.dfy_dy[k] - jo.dfy_dy[k]};
+    const double o[4] = {jo.dfx_dx[k], jo.dfx_dy[k], jo.dfy_dx[k], jo.dfy_dy[k]};
+    for (int c = 0; c < 4; ++c) {
+      jn += d[c] * d[c];
+      jd += o[c] * o[c];
+    }
+  }
+  const double bh_rel = std::sqrt(num / den), bhj_rel = std::sqrt(jn / jd);
+  std::printf("BarnesHutModelVec parity: velocity rel %.3e, jacobian rel %.3e, pair evals %llu\n", bh_rel, bhj_rel,
+              (unsigned long long)bh.pair_evals());
+  return (worst <= 1e-12 && threw && bh_rel <= 1e-12 && bhj_rel <= 1e-12) ? 0 : 1;
 }
