@@ -532,7 +532,8 @@ void launch_allpairs_src(ptrom_ctx* ctx, long long n, Src src, const double* gam
   static int occ = resident_blocks(kern, TPB);
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   const long long tiles = (t_count + TPB * T - 1) / (TPB * T);
-  const int chunks = choose_source_chunks(ctx, tiles, n, occ, 2 * TPB);
+  // short source ranges (small N) may split down to one source tile per chunk
+  const int chunks = choose_source_chunks(ctx, tiles, n, occ, T <= 2 ? TPB : 2 * TPB);
   const long long chunk_len = (n + chunks - 1) / chunks;
   ctx->scratch.reset();
   ctx->scratch.reserve((size_t)chunks * NCOMP * t_count * sizeof(double) + 4096);
@@ -602,7 +603,10 @@ void launch_allpairs_f64(ptrom_ctx* ctx, long long n, const double* x, const dou
                          long long t_begin, long long t_count, double** part, int* chunks,
                          const double* tx = nullptr, const double* ty = nullptr, const SrcPeers* peers = nullptr,
                          long long t_base = 0) {
-  if (t_count < 4096) {
+  // Few target tiles x few source chunks would not fill the 148 SMs with
+  // 8 targets per thread (e.g. N = 4,096): use 2 per thread (4x the tiles).
+  const long long wide_blocks = ((t_count + 1023) / 1024) * std::max(1LL, n / 256);
+  if (t_count < 4096 || wide_blocks < 8LL * ctx->num_sms) {
     launch_allpairs_f64_t<kTPB, 2, 4, 1, VEL, JAC>(ctx, n, x, gamma, dp, t_begin, t_count, part, chunks, tx, ty,
                                                    peers, t_base);
   } else if (VEL && !JAC) {

@@ -3,9 +3,17 @@
 // Replaces FomStepper::step / refactor (integrators.hpp:117-201) and
 // fom_simulate (integrators.hpp:243-272) for the PairwiseModel
 // (integrators.hpp:69-79). State, velocity, residual and the per-particle
-// 2x2 inverse blocks stay in HBM for the whole trajectory; the host only
-// sees one 8-byte residual norm per Newton iteration (the convergence test
-// integrators.hpp:140-155 needs it) and the snapshot columns.
+// 2x2 inverse blocks stay in HBM for the whole trajectory.
+//
+// Control flow on the device: one FOM step is a CUDA graph whose Newton loop
+// is a conditional WHILE node; a single-thread decide kernel evaluates the
+// reference's convergence test (integrators.hpp:140-155: ‖r‖/‖r0‖ ≤ tol,
+// update cap, r0 == 0) and sets the loop condition, and a nested IF node runs
+// the Jacobian/Newton-block refresh on the steps it is due. The host enqueues
+// the step graph n_steps times with no synchronization in between; iteration
+// counts, flags, ‖r‖/‖r0‖ and snapshots are recorded on the device and copied
+// out once. (PTROM_FOM_GRAPH=0 selects the host-driven loop, one 8-byte
+// norm read per iteration.)
 //
 // Elementwise arithmetic follows the reference rounding order with explicit
 // _rn intrinsics (no FMA contraction), so given identical velocities the
@@ -13,6 +21,7 @@
 // two-level reduction (per-thread strided sums, warp/block trees in a fixed
 // shape, then the block partials in index order): deterministic run to run.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ops.cuh"
@@ -54,12 +63,20 @@ __global__ void __launch_bounds__(kNormThreads) residual_kernel(long long m, lon
   }
 }
 
+// Fixed-order sum of the block partials by one warp: lane l adds blocks
+// l, l+32, ... in order, then a fixed shuffle tree (deterministic).
+__device__ __forceinline__ double warp_sum_blocks(int nb, const double* __restrict__ block_part) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s = __dadd_rn(s, block_part[b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+  return __shfl_sync(0xffffffffu, s, 0);
+}
+
 __global__ void sum_blocks_kernel(int nb, const double* __restrict__ block_part, double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s = __dadd_rn(s, block_part[b]);
-    *out = s;
-  }
+  const double s = warp_sum_blocks(nb, block_part);
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = s;
 }
 
 // integrators.hpp:161-167: d = inv * (-r); x += d (reference rounding order).
@@ -73,6 +90,78 @@ __global__ void newton_update_kernel(long long m, long long ld, const double* __
     x[k] = __dadd_rn(x[k], d0);
     x[k + ld] = __dadd_rn(x[k + ld], d1);
   }
+}
+
+// Per-trajectory control block of the device-driven Newton loop.
+struct FomCtl {
+  long long step;
+  long long evals;  // velocity evaluations (the reference's counter / N(N-1))
+  double r0, rel;
+  int updates, converged, have_blocks, refreshed, do_refresh;
+};
+
+// integrators.hpp:140-155 on the device: ‖r‖ from the fixed-order block
+// partials, the reference's decisions, and the loop / refresh conditions.
+__global__ void fom_decide_kernel(FomCtl* c, const double* __restrict__ block_part, int nb, double tol,
+                                  int max_iters, int refresh, cudaGraphConditionalHandle h_loop) {
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const double s = warp_sum_blocks(nb, block_part);
+  if (threadIdx.x != 0) return;
+  const double nr = sqrt(s);
+  const int upd = c->updates;
+  bool cont = false, do_ref = false;
+  if (upd == 0) {
+    c->r0 = nr;
+    if (nr == 0.0) {
+      c->converged = 1;
+      c->rel = 0.0;
+      c->do_refresh = 0;
+      cudaGraphSetConditional(h_loop, 0);
+      return;
+    }
+  }
+  const double rel = nr / c->r0;
+  c->rel = rel;
+  if (rel <= tol) {
+    c->converged = 1;
+  } else if (upd < max_iters) {
+    cont = true;
+    const bool due = (c->step % refresh) == 0 || !c->have_blocks;
+    do_ref = due && !c->refreshed;
+    if (do_ref) c->refreshed = c->have_blocks = 1;
+    c->updates = upd + 1;
+    c->evals += 1;
+  }
+  c->do_refresh = do_ref ? 1 : 0;
+  cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
+}
+
+// First node of the loop body: arms the IF node of the Newton-block refresh.
+__global__ void fom_refresh_gate_kernel(const FomCtl* c, cudaGraphConditionalHandle h_refresh) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) cudaGraphSetConditional(h_refresh, c->do_refresh ? 1u : 0u);
+}
+
+// StepResult + snapshot column of the accepted state (integrators.hpp:262-268).
+__global__ void fom_record_kernel(const FomCtl* c, long long dim, const double* __restrict__ x,
+                                  double* __restrict__ snaps, int* __restrict__ iters,
+                                  unsigned char* __restrict__ conv, double* __restrict__ rel) {
+  const long long s = c->step;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < dim; k += (long long)gridDim.x * blockDim.x)
+    snaps[s * dim + k] = x[k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    iters[s] = c->updates;
+    conv[s] = (unsigned char)c->converged;
+    rel[s] = c->rel;
+  }
+}
+
+__global__ void fom_advance_kernel(FomCtl* c) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  c->step += 1;
+  c->updates = 0;
+  c->converged = 0;
+  c->refreshed = 0;
+  c->rel = 0.0;
 }
 
 int grid_for(ptrom_ctx* ctx, long long count, int tpb) {
@@ -98,6 +187,169 @@ void dev_newton_update_f64(ptrom_ctx* ctx, long long m, long long ld, const doub
 
 size_t residual_block_part_count() { return kNormBlocks; }
 
+// Device-driven trajectory: the step graph (see the file comment) launched
+// n_steps times back to back; one synchronization at the end.
+static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d_x0, const double* d_gamma,
+                                    double delta, int form, const double* d_inflow, double dt, long long n_steps,
+                                    double tol, int max_iters, int refresh, double* h_snapshots, int* iters,
+                                    unsigned char* conv, double* rel_out) {
+  FomResult out;
+  // Capture needs a real stream (the caller's may be the legacy default one):
+  // run the whole trajectory on a private stream ordered after ctx->stream.
+  cudaStream_t caller = ctx->stream, st = nullptr;
+  PTROM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    cudaEvent_t ev;
+    PTROM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PTROM_CUDA(cudaEventRecord(ev, caller));
+    PTROM_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    cudaEventDestroy(ev);
+  }
+  struct StreamGuard {
+    ptrom_ctx* c;
+    cudaStream_t caller, own;
+    ~StreamGuard() {
+      c->stream = caller;
+      cudaStreamSynchronize(own);
+      cudaStreamDestroy(own);
+    }
+  } sguard{ctx, caller, st};
+  ctx->stream = st;
+  const long long dim = 2 * n;
+  std::vector<void*> bufs;
+  auto alloc = [&](size_t bytes) {
+    void* p;
+    PTROM_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+    bufs.push_back(p);
+    return p;
+  };
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaStream_t s_body = nullptr, s_ref = nullptr;
+  struct Cleanup {
+    std::vector<void*>* b;
+    cudaGraphExec_t* e;
+    cudaGraph_t* g;
+    cudaStream_t *s1, *s2;
+    ~Cleanup() {
+      if (*e) cudaGraphExecDestroy(*e);
+      if (*g) cudaGraphDestroy(*g);
+      if (*s1) cudaStreamDestroy(*s1);
+      if (*s2) cudaStreamDestroy(*s2);
+      for (void* p : *b) cudaFree(p);
+    }
+  } cleanup{&bufs, &exec, &graph, &s_body, &s_ref};
+  double* x_prev = (double*)alloc(dim * 8);
+  double* f_prev = (double*)alloc(dim * 8);
+  double* xi = (double*)alloc(dim * 8);
+  double* fxi = (double*)alloc(dim * 8);
+  double* r = (double*)alloc(dim * 8);
+  double* inv = (double*)alloc(4 * n * 8);
+  double* block_part = (double*)alloc(kNormBlocks * 8);
+  double* snaps = (double*)alloc((size_t)dim * std::max<long long>(n_steps, 1) * 8);
+  int* d_iters = (int*)alloc(std::max<long long>(n_steps, 1) * 4);
+  unsigned char* d_conv = (unsigned char*)alloc(std::max<long long>(n_steps, 1));
+  double* d_rel = (double*)alloc(std::max<long long>(n_steps, 1) * 8);
+  FomCtl* ctl = (FomCtl*)alloc(sizeof(FomCtl));
+  PTROM_CUDA(cudaMemsetAsync(ctl, 0, sizeof(FomCtl), st));
+
+  // x = x0; f = model.velocity(x0)   (integrators.hpp:257-259); also sizes the scratch
+  PTROM_CUDA(cudaMemcpyAsync(x_prev, d_x0, dim * 8, cudaMemcpyDeviceToDevice, st));
+  dev_jacobian_f64(ctx, n, x_prev, d_gamma, delta, form, 0, n, nullptr, nullptr, nullptr, nullptr, dt, inv);
+  dev_velocity_f64(ctx, n, x_prev, d_gamma, delta, form, d_inflow, 0, n, f_prev, n);
+  ++out.velocity_evals;
+  PTROM_CUDA(cudaStreamSynchronize(st));
+
+  const double h = dt / 2.0;
+  PTROM_CUDA(cudaStreamCreateWithFlags(&s_body, cudaStreamNonBlocking));
+  PTROM_CUDA(cudaStreamCreateWithFlags(&s_ref, cudaStreamNonBlocking));
+  const bool prof = ctx->prof_on;
+  ctx->prof_on = false;  // no event nodes inside conditional bodies
+  cudaGraphConditionalHandle h_loop, h_ref;
+  PTROM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  // pre: ξ = x_prev, f_ξ = f_prev (integrators.hpp:130-131); r; decide
+  PTROM_CUDA(cudaMemcpyAsync(xi, x_prev, dim * 8, cudaMemcpyDeviceToDevice, st));
+  PTROM_CUDA(cudaMemcpyAsync(fxi, f_prev, dim * 8, cudaMemcpyDeviceToDevice, st));
+  residual_kernel<<<kNormBlocks, kNormThreads, 0, st>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part);
+  // the loop node's handle must exist before the decide kernel that sets it
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g_cap;
+  PTROM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g_cap, nullptr, nullptr));
+  PTROM_CUDA(cudaGraphConditionalHandleCreate(&h_loop, g_cap, 0, 0));
+  fom_decide_kernel<<<1, 32, 0, st>>>(ctl, block_part, kNormBlocks, tol, max_iters, refresh, h_loop);
+  {
+    // WHILE (continue): [IF refresh: Newton blocks]; update; velocity; r; decide
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    PTROM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g_cap, &deps, &ndeps));
+    cudaGraphNodeParams prm = {};
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h_loop;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    cudaGraphNode_t loop_node;
+    PTROM_CUDA(cudaGraphAddNode(&loop_node, g_cap, deps, ndeps, &prm));
+    PTROM_CUDA(cudaStreamUpdateCaptureDependencies(st, &loop_node, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = prm.conditional.phGraph_out[0];
+
+    PTROM_CUDA(cudaStreamBeginCaptureToGraph(s_body, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    PTROM_CUDA(cudaGraphConditionalHandleCreate(&h_ref, body, 0, 0));
+    fom_refresh_gate_kernel<<<1, 32, 0, s_body>>>(ctl, h_ref);
+    cudaStream_t saved = ctx->stream;
+    {
+      const cudaGraphNode_t* bdeps = nullptr;
+      size_t nbdeps = 0;
+      cudaGraph_t g_body;
+      PTROM_CUDA(cudaStreamGetCaptureInfo(s_body, &cs, nullptr, &g_body, &bdeps, &nbdeps));
+      cudaGraphNodeParams ip = {};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = h_ref;
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 1;
+      cudaGraphNode_t if_node;
+      PTROM_CUDA(cudaGraphAddNode(&if_node, g_body, bdeps, nbdeps, &ip));
+      PTROM_CUDA(cudaStreamUpdateCaptureDependencies(s_body, &if_node, 1, cudaStreamSetCaptureDependencies));
+      cudaGraph_t ref_body = ip.conditional.phGraph_out[0];
+      PTROM_CUDA(cudaStreamBeginCaptureToGraph(s_ref, ref_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      ctx->stream = s_ref;  // integrators.hpp:181-194 refactor at ξ
+      dev_jacobian_f64(ctx, n, xi, d_gamma, delta, form, 0, n, nullptr, nullptr, nullptr, nullptr, dt, inv);
+      cudaGraph_t tmp;
+      PTROM_CUDA(cudaStreamEndCapture(s_ref, &tmp));
+    }
+    ctx->stream = s_body;
+    newton_update_kernel<<<grid_for(ctx, n, 256), 256, 0, s_body>>>(n, n, inv, r, xi);
+    dev_velocity_f64(ctx, n, xi, d_gamma, delta, form, d_inflow, 0, n, fxi, n);
+    residual_kernel<<<kNormBlocks, kNormThreads, 0, s_body>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part);
+    fom_decide_kernel<<<1, 32, 0, s_body>>>(ctl, block_part, kNormBlocks, tol, max_iters, refresh, h_loop);
+    ctx->stream = saved;
+    cudaGraph_t tmp;
+    PTROM_CUDA(cudaStreamEndCapture(s_body, &tmp));
+  }
+  // post: record the accepted state, it becomes the history (integrators.hpp:262-264)
+  fom_record_kernel<<<grid_for(ctx, dim, 256), 256, 0, st>>>(ctl, dim, xi, snaps, d_iters, d_conv, d_rel);
+  PTROM_CUDA(cudaMemcpyAsync(x_prev, xi, dim * 8, cudaMemcpyDeviceToDevice, st));
+  PTROM_CUDA(cudaMemcpyAsync(f_prev, fxi, dim * 8, cudaMemcpyDeviceToDevice, st));
+  fom_advance_kernel<<<1, 32, 0, st>>>(ctl);
+  PTROM_CUDA(cudaStreamEndCapture(st, &graph));
+  ctx->prof_on = prof;
+  PTROM_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+
+  for (long long s = 0; s < n_steps; ++s) PTROM_CUDA(cudaGraphLaunch(exec, st));
+  FomCtl hc;
+  PTROM_CUDA(cudaMemcpyAsync(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  if (n_steps > 0) {
+    PTROM_CUDA(cudaMemcpyAsync(iters, d_iters, n_steps * 4, cudaMemcpyDeviceToHost, st));
+    PTROM_CUDA(cudaMemcpyAsync(conv, d_conv, n_steps, cudaMemcpyDeviceToHost, st));
+    PTROM_CUDA(cudaMemcpyAsync(rel_out, d_rel, n_steps * 8, cudaMemcpyDeviceToHost, st));
+    if (h_snapshots)
+      PTROM_CUDA(cudaMemcpyAsync(h_snapshots, snaps, (size_t)dim * n_steps * 8, cudaMemcpyDeviceToHost, st));
+  }
+  PTROM_CUDA(cudaStreamSynchronize(st));
+  check_device_status(ctx);
+  out.velocity_evals += hc.evals;
+  return out;
+}
+
 // ----------------------------------------------------------- fom_simulate --
 // integrators.hpp:243-272 + FomStepper::step integrators.hpp:126-178.
 // All buffers are device-resident; host copies only x0 in and snapshots out.
@@ -105,6 +357,10 @@ FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, c
                               int form, const double* d_inflow, double dt, long long n_steps, double tol,
                               int max_iters, int refresh, double* h_snapshots, int* iters, unsigned char* conv,
                               double* rel_out) {
+  const char* mode = std::getenv("PTROM_FOM_GRAPH");
+  if (!(mode && mode[0] == '0'))
+    return fom_simulate_graph(ctx, n, d_x0, d_gamma, delta, form, d_inflow, dt, n_steps, tol, max_iters, refresh,
+                              h_snapshots, iters, conv, rel_out);
   FomResult out;
   const size_t dim = (size_t)2 * n;
   double *x_prev, *f_prev, *xi, *fxi, *r, *inv, *norm2, *block_part;

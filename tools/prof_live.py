@@ -68,6 +68,15 @@ if what == "config4":
         torch.cuda.synchronize()
     print(f"single instance, 2 steps: wall {time.perf_counter() - t0:.3f} s")
     table(prof, "ptrom_simulate single instance")
+elif what == "config1":
+    w = workloads.config1()
+    sysm = pt.ParticleSystem(w.gamma, w.delta)
+    pt.fom_simulate(w.x0, sysm, pt.TimeGrid(w.dt, 3))
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        pt.fom_simulate(w.x0, sysm, pt.TimeGrid(w.dt, w.n_steps))
+        torch.cuda.synchronize()
+    table(prof, "config1 FOM 100 steps")
 elif what == "config3":
     import ctypes
     w = workloads.config3()
