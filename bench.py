@@ -111,8 +111,8 @@ def ncu_traffic(name):
     committed `ncu --set full` summary of the same kernel (profiles/)."""
     path = os.path.join(ROOT, "profiles", name)
     try:
-        d = json.load(open(path))
-        return float(d["dram__bytes_read.sum"]) * 1e6 + float(d["dram__bytes_write.sum"])
+        d = json.load(open(path))  # written by tools/ncu_summary.py (bytes)
+        return float(d["dram_bytes_per_launch"])
     except Exception:
         return None
 
