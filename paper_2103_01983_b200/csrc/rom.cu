@@ -723,19 +723,22 @@ __global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat 
                                                          const double* __restrict__ fprev,
                                                          const double* __restrict__ jac, GnState st_,
                                                          long long slice_len, double* __restrict__ part) {
-  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M, CS = M + 4;
-  extern __shared__ double gn_smem[];  // per warp: 32 x CS C rows, then 32 residuals
+  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M, CS = M + 4, AS = MR + 4;
+  // dynamic shared memory: the CTA's 32-row block of A (32 x AS, shared by
+  // the 8 instance warps), then per warp 32 x CS C rows and 32 residuals
+  extern __shared__ double gn_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * 8 + warp;
-  if (b >= B || !st_.active[b]) return;
+  const bool ok = b < B && st_.active[b];
   const long long nt = g.n_s, rows = 2 * nt;
-  const double* xb = xbar + (long long)b * rows;
-  const double* xp = xprev + (long long)b * rows;
-  const double* fb = fbar + (long long)b * rows;
-  const double* fp = fprev + (long long)b * rows;
-  const double* jb = jac + (long long)b * nt * 4;
+  const long long bb = ok ? b : 0;
+  const double* xb = xbar + bb * rows;
+  const double* xp = xprev + bb * rows;
+  const double* fb = fbar + bb * rows;
+  const double* fp = fprev + bb * rows;
+  const double* jb = jac + bb * nt * 4;
   const int lr = lane >> 2, lc = lane & 3;
-  const bool need_ac = !(st_.evals[b] >= st_.max_iters);
+  const bool need_ac = ok && !(st_.evals[b] >= st_.max_iters);
   double acc[TI][TN][2];
   double ar[TI];
   double gr[TN];
@@ -747,44 +750,52 @@ __global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat 
   }
 #pragma unroll
   for (int j = 0; j < TN; ++j) gr[j] = 0.0;
-  double* swc = gn_smem + warp * (32 * CS + 32);
+  double* sA = gn_smem;
+  double* swc = gn_smem + 32 * AS + warp * (32 * CS + 32);
   double* swr = swc + 32 * CS;
   const long long k_begin = blockIdx.y * slice_len, k_end = min(rows, k_begin + slice_len);
   for (long long k0 = k_begin; k0 < k_end; k0 += 32) {
-    const long long r = k0 + lane;
-    __syncwarp();
-    if (r < k_end) {
-      swr[lane] = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
-      const bool xrow = r < nt;
-      const long long t = xrow ? r : r - nt;
-      const double4 J = *reinterpret_cast<const double4*>(jb + 4 * t);
-      const double ja = xrow ? J.x : J.z, jb_ = xrow ? J.y : J.w;
-      const double2* pxr = reinterpret_cast<const double2*>(et.pbr + t * M);
-      const double2* pyr = reinterpret_cast<const double2*>(et.pbr + (t + nt) * M);
-#pragma unroll
-      for (int m2 = 0; m2 < M / 2; ++m2) {
-        const double2 px = pxr[m2], py = pyr[m2];
-        const double own0 = xrow ? px.x : py.x, own1 = xrow ? px.y : py.y;
-        swc[lane * CS + 2 * m2] =
-            __dsub_rn(own0, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.x), __dmul_rn(jb_, py.x))));
-        swc[lane * CS + 2 * m2 + 1] =
-            __dsub_rn(own1, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.y), __dmul_rn(jb_, py.y))));
-      }
-    } else {
-      swr[lane] = 0.0;
-#pragma unroll
-      for (int m = 0; m < M; ++m) swc[lane * CS + m] = 0.0;
+    __syncthreads();
+    // A columns k0..k0+31 (column-major, 32 rows each) → sA[kk][i] (stride AS)
+    for (int e = threadIdx.x; e < 32 * MR; e += blockDim.x) {
+      const int kk = e / MR, i = e % MR;
+      sA[kk * AS + i] = k0 + kk < k_end ? g.A[i + (k0 + kk) * MR] : 0.0;
     }
-    __syncwarp();
+    const long long r = k0 + lane;
+    if (ok) {
+      if (r < k_end) {
+        swr[lane] = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
+        const bool xrow = r < nt;
+        const long long t = xrow ? r : r - nt;
+        const double4 J = *reinterpret_cast<const double4*>(jb + 4 * t);
+        const double ja = xrow ? J.x : J.z, jb_ = xrow ? J.y : J.w;
+        const double2* pxr = reinterpret_cast<const double2*>(et.pbr + t * M);
+        const double2* pyr = reinterpret_cast<const double2*>(et.pbr + (t + nt) * M);
+#pragma unroll
+        for (int m2 = 0; m2 < M / 2; ++m2) {
+          const double2 px = pxr[m2], py = pyr[m2];
+          const double own0 = xrow ? px.x : py.x, own1 = xrow ? px.y : py.y;
+          swc[lane * CS + 2 * m2] =
+              __dsub_rn(own0, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.x), __dmul_rn(jb_, py.x))));
+          swc[lane * CS + 2 * m2 + 1] =
+              __dsub_rn(own1, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.y), __dmul_rn(jb_, py.y))));
+        }
+      } else {
+        swr[lane] = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) swc[lane * CS + m] = 0.0;
+      }
+    }
+    __syncthreads();
+    if (!ok) continue;
     const int steps = (int)min(8LL, (k_end - k0 + 3) / 4);
     for (int s4 = 0; s4 < steps; ++s4) {
       const int kk = 4 * s4 + lc;
-      const long long row = k0 + kk;
       const double rvv = swr[kk];
       double av[TI];
 #pragma unroll
       for (int i = 0; i < TI; ++i) {
-        av[i] = row < k_end ? g.A[(i * 8 + lr) + row * MR] : 0.0;
+        av[i] = sA[kk * AS + i * 8 + lr];
         ar[i] = fma(av[i], rvv, ar[i]);
       }
 #pragma unroll
@@ -798,6 +809,7 @@ __global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat 
       }
     }
   }
+  if (!ok) return;
   double* out = part + ((long long)blockIdx.y * B + b) * PART;
 #pragma unroll
   for (int i = 0; i < TI; ++i)
@@ -1209,7 +1221,7 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
   const long long groups = (B + 7) / 8;
   const int S = (int)std::max<long long>(1, std::min<long long>(64, (8LL * ctx->num_sms + groups - 1) / groups));
   const long long slice_len = ((rows + S - 1) / S + 31) / 32 * 32;
-  const size_t gn_smem = (size_t)8 * (32 * (MP + 4) + 32) * sizeof(double);
+  const size_t gn_smem = ((size_t)32 * (32 + 4) + (size_t)8 * (32 * (MP + 4) + 32)) * sizeof(double);
   PTROM_CUDA(cudaFuncSetAttribute(gn_partial_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gn_smem));
   double* part = (double*)alloc((size_t)S * B * (32 * MP + 32 + MP) * 8);
   int* h_active = nullptr;
