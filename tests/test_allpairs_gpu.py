@@ -158,3 +158,33 @@ def test_repeatable_bitwise(pt):
     a = pt.pairwise_velocity(w.x0, s)
     b = pt.pairwise_velocity(w.x0, s)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("scale,delta", [(1.0, 0.3), (2.0 ** 15, 1e3), (2.0 ** 30, 1e10), (1.0, 1e-300),
+                                         (1e-3, 1e-9)])
+def test_reciprocal_tiers_match_oracle(pt, oracle, scale, delta):
+    """Exercises the 4-way (|x| < 2^14, δ' >= 2^-31), 2-way (|x| < 2^29) and
+    safe (huge coordinates, tiny δ) reciprocal tiers, incl. the unmasked
+    fast-path diagonal, on a size with ragged tiles."""
+    rng = np.random.default_rng(int(scale) % 1000 + 17)
+    n = 20000 + 37
+    x = rng.uniform(-1.0, 1.0, 2 * n) * scale
+    g = rng.uniform(-1.0, 1.0, n)
+    f = pt.pairwise_velocity(x, pt.ParticleSystem(g, delta))
+    ref = oracle.pairwise_velocity(x, g, delta, t_end=1500, threads=THREADS)
+    rows = np.r_[0:1500, n:n + 1500]
+    assert rel(f[rows], ref[rows]) <= FP64_TOL
+
+
+def test_empty_system_is_a_config_error(pt):
+    with pytest.raises(pt.ConfigError, match="empty"):
+        pt.pairwise_velocity(np.zeros(0), pt.ParticleSystem(np.zeros(0), 0.1))
+    with pytest.raises(pt.ConfigError):
+        pt.hamiltonian(np.zeros(0), pt.ParticleSystem(np.zeros(0), 0.1))
+    with pytest.raises(pt.ConfigError):
+        pt.fom_simulate(np.zeros(0), pt.ParticleSystem(np.zeros(0), 0.1), pt.TimeGrid(1e-3, 2))
+
+
+def test_single_particle_has_only_inflow(pt):
+    f = pt.pairwise_velocity(np.array([0.5, -0.25]), pt.ParticleSystem(np.array([3.0]), 0.0, np.array([0.1, -0.2])))
+    assert f.tolist() == [0.1, -0.2]
