@@ -245,48 +245,9 @@ __global__ void scatter_kernel(long long n, const int* __restrict__ pos_rec, con
   }
 }
 
-// quadtree.hpp:51-67 finish_node for small nodes: sequential, reference order.
-// One warp per node: the lanes stage 32 members at a time (coalesced) in
-// shared memory and lane 0 runs the reference's left-to-right sums over them.
-constexpr int kSumWarps = kThreads / 32;
-__global__ void __launch_bounds__(kThreads) sums_small_kernel(int R0, int R1, TreeRecords rec,
-                                                              const double* __restrict__ sx,
-                                                              const double* __restrict__ sy,
-                                                              const double* __restrict__ sg, int seq_max,
-                                                              int* __restrict__ large_list,
-                                                              int* __restrict__ large_count) {
-  __shared__ double st[kSumWarps][3][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int r = R0 + blockIdx.x * kSumWarps + wib;
-  if (r >= R1) return;
-  const int b = rec.begin[r], e = rec.end[r];
-  if (e - b > seq_max) {
-    if (lane == 0) large_list[atomicAdd(large_count, 1)] = r;
-    return;
-  }
-  double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
-  for (int c0 = b; c0 < e; c0 += 32) {
-    const int k = c0 + lane;
-    if (k < e) {
-      st[wib][0][lane] = sg[k];
-      st[wib][1][lane] = sx[k];
-      st[wib][2][lane] = sy[k];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const int cnt = min(32, e - c0);
-      for (int j = 0; j < cnt; ++j) {
-        const double g = st[wib][0][j], x = st[wib][1][j], y = st[wib][2][j];
-        gs = __dadd_rn(gs, g);
-        wx = __dadd_rn(wx, __dmul_rn(g, x));
-        wy = __dadd_rn(wy, __dmul_rn(g, y));
-        plx = __dadd_rn(plx, x);
-        ply = __dadd_rn(ply, y);
-      }
-    }
-    __syncwarp();
-  }
-  if (lane != 0) return;
+// quadtree.hpp:51-67 finish_node: sequential sums in the reference's order.
+__device__ __forceinline__ void finish_exact(TreeRecords& rec, int r, int b, int e, double gs, double wx, double wy,
+                                             double plx, double ply) {
   rec.gamma_sum[r] = gs;
   const bool fb = gs == 0.0;
   rec.fallback[r] = fb ? 1 : 0;
@@ -297,44 +258,161 @@ __global__ void __launch_bounds__(kThreads) sums_small_kernel(int R0, int R1, Tr
   rec.cerr[r] = 0.0;
 }
 
-// Large nodes (> seq_max members): fixed chunks of kChunk members reduced by
-// one CTA each (fixed-order block reduction), then the chunk partials of a
-// node summed in chunk order — deterministic — with a rigorous bound on the
-// centroid's distance from the reference's sequential order.
-constexpr int kChunk = 8192;
-__global__ void large_prefix_kernel(TreeRecords rec, const int* __restrict__ large_list,
-                                    const int* __restrict__ large_count, int* __restrict__ chunk_off) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int total = *large_count;
-  int acc = 0;
-  for (int li = 0; li < total; ++li) {
-    chunk_off[li] = acc;
-    const int r = large_list[li];
-    acc += (rec.end[r] - rec.begin[r] + kChunk - 1) / kChunk;
+// Nodes [R0, R1) of one level, one lane each. Nodes with at most kLaneSum
+// members are summed by their own lane (short sequential chains, all lanes
+// busy — the many small nodes of the deep levels); larger ones go to the mid
+// list (one warp each, sums_mid_kernel) or, above seq_max, to the large list
+// (multi-CTA, certified).
+constexpr int kSumWarps = kThreads / 32;
+constexpr int kLaneSum = 48;
+__global__ void __launch_bounds__(kThreads) sums_small_kernel(int R0, int R1, TreeRecords rec,
+                                                              const double* __restrict__ sx,
+                                                              const double* __restrict__ sy,
+                                                              const double* __restrict__ sg, int seq_max,
+                                                              int* __restrict__ large_list,
+                                                              int* __restrict__ large_count,
+                                                              int* __restrict__ mid_list,
+                                                              int* __restrict__ mid_count) {
+  const int r = R0 + blockIdx.x * kThreads + threadIdx.x;
+  if (r >= R1) return;
+  const int b = rec.begin[r], e = rec.end[r];
+  const int cnt = e - b;
+  if (cnt > seq_max) {
+    large_list[atomicAdd(large_count, 1)] = r;
+    return;
   }
-  chunk_off[total] = acc;
+  if (cnt > kLaneSum) {
+    mid_list[atomicAdd(mid_count, 1)] = r;
+    return;
+  }
+  double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+  for (int k = b; k < e; ++k) {
+    const double g = sg[k], x = sx[k], y = sy[k];
+    gs = __dadd_rn(gs, g);
+    wx = __dadd_rn(wx, __dmul_rn(g, x));
+    wy = __dadd_rn(wy, __dmul_rn(g, y));
+    plx = __dadd_rn(plx, x);
+    ply = __dadd_rn(ply, y);
+  }
+  finish_exact(rec, r, b, e, gs, wx, wy, plx, ply);
 }
 
-__global__ void __launch_bounds__(kThreads) large_partial_kernel(TreeRecords rec, const double* __restrict__ sx,
-                                                                 const double* __restrict__ sy,
-                                                                 const double* __restrict__ sg,
-                                                                 const int* __restrict__ large_list,
-                                                                 const int* __restrict__ large_count,
-                                                                 const int* __restrict__ chunk_off,
-                                                                 double* __restrict__ part) {
-  using BR = cub::BlockReduce<double, kThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int total = *large_count;
-  const int nchunks = chunk_off[total];
-  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    int lo = 0, hi = total;  // node li with chunk_off[li] <= ci < chunk_off[li + 1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (chunk_off[mid] <= ci) lo = mid;
-      else hi = mid;
+// Mid-size nodes (kLaneSum < members <= seq_max): one warp per node, the
+// lanes stage 32 members at a time (coalesced) in shared memory for lane 0's
+// sequential chain in the reference's order.
+__global__ void __launch_bounds__(kThreads) sums_mid_kernel(TreeRecords rec, const double* __restrict__ sx,
+                                                            const double* __restrict__ sy,
+                                                            const double* __restrict__ sg,
+                                                            const int* __restrict__ mid_list,
+                                                            int* __restrict__ mid_count) {
+  __shared__ double st[kSumWarps][3][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int total = *mid_count;
+  for (int w = blockIdx.x * kSumWarps + wib; w < total; w += gridDim.x * kSumWarps) {
+    const int r = mid_list[w];
+    const int b = rec.begin[r], e = rec.end[r];
+    double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+    for (int c0 = b; c0 < e; c0 += 32) {
+      const int k = c0 + lane;
+      if (k < e) {
+        st[wib][0][lane] = sg[k];
+        st[wib][1][lane] = sx[k];
+        st[wib][2][lane] = sy[k];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int n = min(32, e - c0);
+        for (int j = 0; j < n; ++j) {
+          const double g = st[wib][0][j], x = st[wib][1][j], y = st[wib][2][j];
+          gs = __dadd_rn(gs, g);
+          wx = __dadd_rn(wx, __dmul_rn(g, x));
+          wy = __dadd_rn(wy, __dmul_rn(g, y));
+          plx = __dadd_rn(plx, x);
+          ply = __dadd_rn(ply, y);
+        }
+      }
+      __syncwarp();
     }
-    const int r = large_list[lo];
-    const int b = rec.begin[r] + (ci - chunk_off[lo]) * kChunk;
+    if (lane == 0) finish_exact(rec, r, b, e, gs, wx, wy, plx, ply);
+  }
+}
+
+// Large nodes (> seq_max members) in ONE launch: every CTA finds the node of
+// each of its chunks (kChunk members) from the large list, reduces the chunk
+// with a fixed-order block reduction; the last CTA to finish adds each
+// node's chunk partials in chunk order (deterministic) and finishes the
+// centroid with a rigorous bound on its distance from the reference's
+// sequential order. With no large node at the level the launch is a no-op.
+constexpr int kChunk = 8192;
+__global__ void __launch_bounds__(kThreads) large_sums_kernel(TreeRecords rec, const double* __restrict__ sx,
+                                                              const double* __restrict__ sy,
+                                                              const double* __restrict__ sg,
+                                                              const int* __restrict__ large_list,
+                                                              int* __restrict__ large_count,
+                                                              int* __restrict__ chunk_off,
+                                                              double* __restrict__ part,
+                                                              unsigned* __restrict__ done_ctr) {
+  const int total = *large_count;
+  if (total == 0) return;
+  using BR = cub::BlockReduce<double, kThreads>;
+  using BS = cub::BlockScan<int, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ typename BS::TempStorage stmp;
+  constexpr int kMaxLarge = 4096;  // chunk offsets kept in shared memory
+  __shared__ int s_off[kMaxLarge + 1];
+  __shared__ bool s_last;
+  __shared__ int s_carry;
+  // chunk offsets of the large nodes: block-wide scan, 256 nodes per round
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int l0 = 0; l0 < total; l0 += kThreads) {
+    const int li = l0 + threadIdx.x;
+    int nc = 0;
+    if (li < total) {
+      const int r = large_list[li];
+      nc = (rec.end[r] - rec.begin[r] + kChunk - 1) / kChunk;
+    }
+    int ex = 0, agg = 0;
+    BS(stmp).ExclusiveSum(nc, ex, agg);
+    const int carry = s_carry;
+    if (li < total) {
+      if (li < kMaxLarge) s_off[li] = carry + ex;
+      if (blockIdx.x == 0) chunk_off[li] = carry + ex;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + agg;
+    __syncthreads();
+  }
+  const int nchunks = s_carry;
+  if (total <= kMaxLarge && threadIdx.x == 0) s_off[total] = nchunks;
+  if (blockIdx.x == 0 && threadIdx.x == 0) chunk_off[total] = nchunks;
+  __syncthreads();
+  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    int li = 0, base = 0;
+    if (total <= kMaxLarge) {  // node of chunk ci: last li with s_off[li] <= ci
+      int lo = 0, hi = total;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] <= ci) lo = mid;
+        else hi = mid;
+      }
+      li = lo;
+      base = s_off[lo];
+    } else {  // very long lists: linear walk over the global offsets
+      int acc = 0;
+      for (int q = 0; q < total; ++q) {
+        const int r = large_list[q];
+        const int nc = (rec.end[r] - rec.begin[r] + kChunk - 1) / kChunk;
+        if (ci < acc + nc) {
+          li = q;
+          base = acc;
+          break;
+        }
+        acc += nc;
+      }
+    }
+    const int r = large_list[li];
+    const int b = rec.begin[r] + (ci - base) * kChunk;
     const int e = min(rec.end[r], b + kChunk);
     double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // gs wx wy plx ply |g| |gx| |gy|
     for (int k = b + threadIdx.x; k < e; k += kThreads) {
@@ -355,46 +433,53 @@ __global__ void __launch_bounds__(kThreads) large_partial_kernel(TreeRecords rec
       __syncthreads();
     }
   }
-}
-
-__global__ void large_finish_kernel(TreeRecords rec, const int* __restrict__ large_list,
-                                    const int* __restrict__ large_count, const int* __restrict__ chunk_off,
-                                    const double* __restrict__ part) {
-  const int li = blockIdx.x * blockDim.x + threadIdx.x;
-  if (li >= *large_count) return;
-  const int r = large_list[li];
-  const int b = rec.begin[r], e = rec.end[r];
-  double red[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int ci = chunk_off[li]; ci < chunk_off[li + 1]; ++ci)
-    for (int c = 0; c < 8; ++c) red[c] = __dadd_rn(red[c], part[8 * (long long)ci + c]);
-  const double m = (double)(e - b);
-  const double u = 0x1p-53;
-  // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
-  // sum; their difference within twice that (first order, padded).
-  const double k2 = 2.05 * (m + 1.0) * u;
-  const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
-  const double gs = red[0];
-  rec.gamma_sum[r] = gs;
-  const bool fb = gs == 0.0;
-  rec.fallback[r] = fb ? 1 : 0;
-  double cx, cy, err;
-  if (fb) {
-    cx = __ddiv_rn(red[3], m);
-    cy = __ddiv_rn(red[4], m);
-  } else {
-    cx = __ddiv_rn(red[1], gs);
-    cy = __ddiv_rn(red[2], gs);
+  // last CTA: finish every large node
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int li = threadIdx.x; li < total; li += blockDim.x) {
+    const int r = large_list[li];
+    const int b = rec.begin[r], e = rec.end[r];
+    double red[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int ci = chunk_off[li]; ci < chunk_off[li + 1]; ++ci)
+      for (int c = 0; c < 8; ++c) red[c] = __dadd_rn(red[c], part[8 * (long long)ci + c]);
+    const double m = (double)(e - b);
+    const double u = 0x1p-53;
+    // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
+    // sum; their difference within twice that (first order, padded).
+    const double k2 = 2.05 * (m + 1.0) * u;
+    const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
+    const double gs = red[0];
+    rec.gamma_sum[r] = gs;
+    const bool fb = gs == 0.0;
+    rec.fallback[r] = fb ? 1 : 0;
+    double cx, cy, err;
+    if (fb) {
+      cx = __ddiv_rn(red[3], m);
+      cy = __ddiv_rn(red[4], m);
+    } else {
+      cx = __ddiv_rn(red[1], gs);
+      cy = __ddiv_rn(red[2], gs);
+    }
+    if (fabs(gs) <= 2.0 * eg) {
+      err = INFINITY;  // the fallback flag itself is uncertain
+    } else {
+      const double ag = fabs(gs) - eg;
+      err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
+    }
+    rec.centroid[2 * r] = cx;
+    rec.centroid[2 * r + 1] = cy;
+    rec.exact[r] = 0;
+    rec.cerr[r] = err;
   }
-  if (fabs(gs) <= 2.0 * eg) {
-    err = INFINITY;  // the fallback flag itself is uncertain
-  } else {
-    const double ag = fabs(gs) - eg;
-    err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *done_ctr = 0;  // ready for the next level
+    *large_count = 0;
   }
-  rec.centroid[2 * r] = cx;
-  rec.centroid[2 * r + 1] = cy;
-  rec.exact[r] = 0;
-  rec.cerr[r] = err;
 }
 
 // ------------------------------------------------------------ preorder ---
@@ -639,7 +724,7 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   void* flags_raw = dalloc<uint4>(n + 1);
   void* scan_raw = dalloc<uint4>(n + 1);
   unsigned char* digit = dalloc<unsigned char>(n);
-  int* dcount = dalloc<int>(4);  // [0] splits at next level, [1] large-node count
+  int* dcount = dalloc<int>(4);  // [0] splits at next level, [1] large-node count, [2] mid-node count
   int* h_counts = ctx->h_counts;  // pinned, owned by the context
   size_t scan_tmp_bytes = 0, scan_tmp_u64 = 0;
   cub::DeviceScan::ExclusiveScan(nullptr, scan_tmp_bytes, (uint4*)flags_raw, (uint4*)scan_raw, U4Sum(),
@@ -657,14 +742,17 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   int* large_list = dalloc<int>(max_large);
   int* chunk_off = dalloc<int>(max_large + 1);
   double* large_part = dalloc<double>(8 * (n / kChunk + max_large + 1));
+  unsigned* done_ctr = dalloc<unsigned>(1);
+  PTROM_CUDA(cudaMemsetAsync(done_ctr, 0, sizeof(unsigned), s));
+  int* mid_list = dalloc<int>(std::max<long long>(1, n));
   auto run_sums = [&](int R0, int R1) {
-    sums_small_kernel<<<(R1 - R0 + kSumWarps - 1) / kSumWarps, kThreads, 0, s>>>(R0, R1, rec, sx, sy, sg, seq_max,
-                                                                                 large_list, dcount + 1);
-    large_prefix_kernel<<<1, 32, 0, s>>>(rec, large_list, dcount + 1, chunk_off);
-    large_partial_kernel<<<ctx->num_sms * 4, kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1, chunk_off,
-                                                               large_part);
-    const long long fl = std::min<long long>(R1 - R0, max_large);
-    large_finish_kernel<<<(int)((fl + 127) / 128), 128, 0, s>>>(rec, large_list, dcount + 1, chunk_off, large_part);
+    sums_small_kernel<<<(R1 - R0 + kThreads - 1) / kThreads, kThreads, 0, s>>>(R0, R1, rec, sx, sy, sg, seq_max,
+                                                                               large_list, dcount + 1, mid_list,
+                                                                               dcount + 2);
+    const int mid_blocks = (int)std::min<long long>((R1 - R0 + kSumWarps - 1) / kSumWarps, ctx->num_sms * 16LL);
+    sums_mid_kernel<<<std::max(1, mid_blocks), kThreads, 0, s>>>(rec, sx, sy, sg, mid_list, dcount + 2);
+    large_sums_kernel<<<ctx->num_sms * 2, kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1, chunk_off,
+                                                            large_part, done_ctr);
     PTROM_LAUNCH_CHECK();
   };
 
@@ -769,7 +857,7 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   cudaEventDestroy(ev1);
 
   void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags_raw, scan_raw, digit, dcount, tmp, nchild, child_off, large_list,
-                   chunk_off, large_part, keys, keys_s, vals, order, rec2id, stmp};
+                   chunk_off, large_part, done_ctr, mid_list, keys, keys_s, vals, order, rec2id, stmp};
   for (void* p : frees) dfree(p);
   rec.free();
 }
