@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "ops.cuh"
@@ -416,9 +417,52 @@ __global__ void positions_targets_kernel(DGnat g, int B, const double* __restric
 // exactly on its target when delta == 0, rom.hpp:129), then direct sources
 // (skipping the target's own id, rom.hpp:136), fused velocity + Jacobian,
 // inflow at the target id. f: [b][2n_t], jac: [b][n_t][4].
+// Γ/2π tables for hyperpair (built once per march): exact mode Γ̃_c/2π and
+// Γ_d/2π (bit-identical to the reference's Γ·(1/2π) before the 1/q product),
+// affine mode (G_A, G_B)/2π and (Γa_d, Γb_d)/2π as double2.
+struct HpGamma {
+  const double* gc = nullptr;    // [n_c] exact
+  const double2* gab = nullptr;  // [n_c] affine
+  const double* gd = nullptr;    // [u] exact
+  const double2* gdab = nullptr; // [u] affine
+  const int* self_loc = nullptr; // [n_t] the target's own slot in direct_ids, or -1
+};
+
+// Each target's own slot in the sorted near-field union (rom.hpp:140 skips it).
+__global__ void hp_self_kernel(DSurrogate s, int* __restrict__ self_loc) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= s.n_t) return;
+  const long long pid = s.target_ids[t];
+  long long lo = 0, hi = s.u;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (s.direct_ids[mid] < pid) lo = mid + 1;
+    else hi = mid;
+  }
+  self_loc[t] = (lo < s.u && s.direct_ids[lo] == pid) ? (int)lo : -1;
+}
+
+__global__ void hp_gamma_kernel(DSurrogate s, AffineTables t, bool affine, double* gc, double2* gab, double* gd,
+                                double2* gdab) {
+  const double inv2pi = 1.0 / (2.0 * M_PI);
+  const long long total = s.n_c + s.u;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i < s.n_c) {
+      if (affine) gab[i] = make_double2(t.ga[i] * inv2pi, t.gb[i] * inv2pi);
+      else gc[i] = s.gamma_tilde[i] * inv2pi;
+    } else {
+      const long long d = i - s.n_c;
+      if (affine) gdab[d] = make_double2(t.dga[d] * inv2pi, t.dgb[d] * inv2pi);
+      else gd[d] = s.direct_gamma[d] * inv2pi;
+    }
+  }
+}
+
 template <int IB>
-__global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTables at, const double* __restrict__ mu,
-                                                        int B, const double* __restrict__ xbar,
+__global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTables at, HpGamma hg,
+                                                        const double* __restrict__ mu, int B,
+                                                        const double* __restrict__ xbar,
                                                         const double* __restrict__ cx, const double* __restrict__ cy,
                                                         const double* __restrict__ cg, const double* __restrict__ dx,
                                                         const double* __restrict__ dy, const double* __restrict__ dg,
@@ -428,10 +472,9 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
                                                         unsigned long long* __restrict__ pairs, DeviceStatus* st) {
   // Work mapping: with B >= IB a warp is (32/IB targets, IB-instance chunk)
   // and the chunk is the slow grid dimension, so concurrently resident warps
-  // sweep spatially adjacent targets (t_order) for the same IB instances: the
-  // positions of one chunk (n_c x IB x 16 B per chunk)
-  // stay in L2 while the targets sweep, so each is read from HBM about once.
-  // With B < IB one thread per (target, instance).
+  // sweep spatially adjacent targets (t_order) for the same IB instances and
+  // share the cluster positions in L2. With B < IB one thread per
+  // (target, instance).
   const long long gidx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nt = s.n_t;
   unsigned long long cnt = 0;
@@ -454,76 +497,123 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
       const double px = xbar[(long long)b * 2 * nt + t], py = xbar[(long long)b * 2 * nt + nt + t];
       const double inv2pi = 1.0 / (2.0 * M_PI);
       double fx = 0, fy = 0, ja = 0, jb = 0, jc = 0;
-      auto add = [&](double sx, double sy, double gam) {
+      // gs = Γ/2π: sv = gs·(1/q) is the reference's Γ·(1/2π)·(1/q) (rom.hpp:131-132)
+      auto add = [&](double sx, double sy, double gs) {
         const double rx = px - sx, ry = py - sy;
         const double q = fma(rx, rx, fma(ry, ry, dp));
         const double u = rcp64(q);
-        const double sv = gam * inv2pi * u;
+        const double sv = gs * u;
         fx = fma(-ry, sv, fx);
         fy = fma(rx, sv, fy);
         const double w = sv * u;
         ja = fma(w * rx, ry, ja);
         jb = fma(w, fma(ry, ry, -(rx * rx)), jb);
         jc += w;
-        ++cnt;
       };
       const double mub = mu ? mu[b] : 0.0;
-      auto cgam = [&](long long ci) { return mu ? fma(mub, at.gb[ci], at.ga[ci]) : s.gamma_tilde[ci]; };
+      auto cgam = [&](int ci) -> double {
+        if (mu) {
+          if (hg.gab) {
+            const double2 v = hg.gab[ci];
+            return fma(mub, v.y, v.x);
+          }
+          return fma(mub, at.gb[ci], at.ga[ci]) * inv2pi;
+        }
+        return hg.gc ? hg.gc[ci] : s.gamma_tilde[ci] * inv2pi;
+      };
+      const double* cxb = cx + b;
+      const double* cyb = cy + b;
       // Cluster list, U entries per round: the U list reads, then the 2U
       // position loads are issued before any arithmetic (memory-level
       // parallelism for the L2/HBM-latency-bound gathers); order of the
       // accumulation is unchanged.
       constexpr int U = 4;
-      long long k = s.cl_off[t];
+      const long long k0 = s.cl_off[t];
       const long long ke = s.cl_off[t + 1];
-      for (; k + U <= ke; k += U) {
-        long long ci[U];
-        double sx[U], sy[U];
+      unsigned skipped = 0;
+      cnt = (unsigned long long)(ke - k0);
+      // rom.hpp:129: a centroid coincident with the target is dropped when
+      // delta == 0 (only then can it be singular); the check is hoisted out of
+      // the δ > 0 loop.
+      auto clusters = [&](auto check) {
+        constexpr bool CHECK = decltype(check)::value;
+        long long k = k0;
+        for (; k + U <= ke; k += U) {
+          int ci[U];
+          double sx[U], sy[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ci[u] = s.cl_list[k + u];
+          for (int u = 0; u < U; ++u) ci[u] = s.cl_list[k + u];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          sx[u] = cx[ci[u] * B + b];
-          sy[u] = cy[ci[u] * B + b];
+          for (int u = 0; u < U; ++u) {
+            const long long off = (long long)ci[u] * B;
+            sx[u] = cxb[off];
+            sy[u] = cyb[off];
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (CHECK && sx[u] == px && sy[u] == py) {
+              ++skipped;
+              continue;
+            }
+            add(sx[u], sy[u], cgam(ci[u]));
+          }
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (delta == 0.0 && sx[u] == px && sy[u] == py) continue;
-          add(sx[u], sy[u], cgam(ci[u]));
+        for (; k < ke; ++k) {
+          const int ci = s.cl_list[k];
+          const long long off = (long long)ci * B;
+          const double sx = cxb[off], sy = cyb[off];
+          if (CHECK && sx == px && sy == py) {
+            ++skipped;
+            continue;
+          }
+          add(sx, sy, cgam(ci));
         }
-      }
-      for (; k < ke; ++k) {
-        const long long ci = s.cl_list[k];
-        const long long c = ci * B + b;
-        const double sx = cx[c], sy = cy[c];
-        if (delta == 0.0 && sx == px && sy == py) continue;
-        add(sx, sy, cgam(ci));
-      }
+      };
+      if (delta == 0.0)
+        clusters(std::true_type{});
+      else
+        clusters(std::false_type{});
+      cnt -= skipped;
       const long long pid = s.target_ids[t];
-      auto dgam = [&](long long loc) { return mu ? fma(mub, at.dgb[loc], at.dga[loc]) : s.direct_gamma[loc]; };
+      const int self_loc = hg.self_loc ? hg.self_loc[t] : -1;
+      auto dgam = [&](int loc) -> double {
+        if (mu) {
+          if (hg.gdab) {
+            const double2 v = hg.gdab[loc];
+            return fma(mub, v.y, v.x);
+          }
+          return fma(mub, at.dgb[loc], at.dga[loc]) * inv2pi;
+        }
+        return hg.gd ? hg.gd[loc] : s.direct_gamma[loc] * inv2pi;
+      };
+      const double* dxb = dx + b;
+      const double* dyb = dy + b;
       long long kd = s.d_off[t];
       const long long kde = s.d_off[t + 1];
       for (; kd + 4 <= kde; kd += 4) {
-        long long loc[4];
+        int loc[4];
         double sx[4], sy[4];
-        bool me[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) loc[u] = s.d_list[kd + u];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          me[u] = s.direct_ids[loc[u]] == pid;
-          sx[u] = dx[loc[u] * B + b];
-          sy[u] = dy[loc[u] * B + b];
+          const long long off = (long long)loc[u] * B;
+          sx[u] = dxb[off];
+          sy[u] = dyb[off];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (!me[u]) add(sx[u], sy[u], dgam(loc[u]));
+          if (hg.self_loc ? loc[u] != self_loc : s.direct_ids[loc[u]] != pid) {
+            add(sx[u], sy[u], dgam(loc[u]));
+            ++cnt;
+          }
       }
       for (; kd < kde; ++kd) {
-        const long long loc = s.d_list[kd];
-        if (s.direct_ids[loc] == pid) continue;
-        const long long d = loc * B + b;
-        add(dx[d], dy[d], dgam(loc));
+        const int loc = s.d_list[kd];
+        if (hg.self_loc ? loc == self_loc : s.direct_ids[loc] == pid) continue;
+        const long long off = (long long)loc * B;
+        add(dxb[off], dyb[off], dgam(loc));
+        ++cnt;
       }
       if (inflow) {
         fx = fx + inflow[pid];
@@ -1120,9 +1210,17 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
     // chunks doubled the DRAM traffic: half-used L2 lines).
     constexpr int IB = 32;
     const long long threads = B >= IB ? ((s.n_t + 32 / IB - 1) / (32 / IB)) * 32 * ((B + IB - 1) / IB) : s.n_t * B;
+    HpGamma hg;
+    if (et) {
+      hg.self_loc = et->hself;
+      hg.gc = et->hgc;
+      hg.gab = et->hgab;
+      hg.gd = et->hgd;
+      hg.gdab = et->hgdab;
+    }
     hyperpair_kernel<IB><<<blocks_for(threads, 128), 128, 0, st>>>(
-        s, tt, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy, w.dg, effective_delta(delta, form), delta,
-        d_inflow, n, d_active, d_f, d_jac, w.pairs, ctx->d_status);
+        s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy, w.dg, effective_delta(delta, form),
+        delta, d_inflow, n, d_active, d_f, d_jac, w.pairs, ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
@@ -1215,6 +1313,21 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
     AffineTables empty{};
     const long long total = s.n_c * et.q * MP + s.u * 2 * MP + rows * MP;
     engine_tables_kernel<<<blocks_for(total, 256), 256, 0, st>>>(s, t ? *t : empty, g, et.q, MP, et);
+    PTROM_LAUNCH_CHECK();
+  }
+  if (t) {
+    et.hgab = (double2*)alloc((size_t)std::max<long long>(1, s.n_c) * 16);
+    et.hgdab = (double2*)alloc((size_t)std::max<long long>(1, s.u) * 16);
+  } else {
+    et.hgc = (double*)alloc((size_t)std::max<long long>(1, s.n_c) * 8);
+    et.hgd = (double*)alloc((size_t)std::max<long long>(1, s.u) * 8);
+  }
+  et.hself = (int*)alloc((size_t)std::max<long long>(1, s.n_t) * 4);
+  if (s.n_t > 0) hp_self_kernel<<<blocks_for(s.n_t, 256), 256, 0, st>>>(s, et.hself);
+  {
+    AffineTables empty2{};
+    hp_gamma_kernel<<<std::max(1, ctx->num_sms * 4), 256, 0, st>>>(s, t ? *t : empty2, t != nullptr, et.hgc, et.hgab,
+                                                                   et.hgd, et.hgdab);
     PTROM_LAUNCH_CHECK();
   }
   // split-K shape: ~4 CTAs per SM over ceil(B/8) instance groups

@@ -69,6 +69,12 @@ struct EngineTables {
   double* dt = nullptr;
   double* pbr = nullptr;
   int q = 2;
+  // Γ/2π tables for hyperpair: exact Γ̃/2π, Γ_d/2π; affine (G_A, G_B)/2π, (Γa_d, Γb_d)/2π
+  double* hgc = nullptr;
+  double2* hgab = nullptr;
+  double* hgd = nullptr;
+  double2* hgdab = nullptr;
+  int* hself = nullptr;  // [n_t] each target's slot in direct_ids or -1
 };
 
 // Per-instance Gauss–Newton state.
