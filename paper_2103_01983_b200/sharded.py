@@ -11,6 +11,12 @@ targets split evenly across ranks. Per Newton iteration:
   * all-gather of the updated source positions (x then y, NVLink/NVSwitch),
     then the all-pairs velocity of the rank's targets against all sources.
 
+With `exchange="peer"` (CUDA backend, one GPU per process) the per-iteration
+all-gather is replaced by the peer-memory exchange (peer.py): each rank
+publishes its updated rows in CUDA-IPC memory and the velocity kernel reads
+the other ranks' blocks in place over NVLink; the Newton-block refresh (once
+per refresh period) still gathers the positions.
+
 PtromInstanceSplit — μ instances of the PTROM online path split evenly across
 ranks (no communication during the march); reduced states gathered at the end.
 
@@ -38,9 +44,11 @@ class CudaBackend:
 
     def __init__(self, gamma: torch.Tensor, delta: float, form: int = 0, inflow: Optional[torch.Tensor] = None):
         from . import device as dev
+        from .api import default_context
         self.dev = dev
         self.gamma, self.delta, self.form, self.inflow = gamma, float(delta), int(form), inflow
         self.device = gamma.device
+        self.ctx = default_context(gamma.device.index or 0)
 
     def velocity_rows(self, x_full, lo, hi, out):
         self.dev.pairwise_velocity(x_full, self.gamma, self.delta, self.form, self.inflow, lo, hi, out)
@@ -69,7 +77,7 @@ class ShardedResult:
 
 
 class ShardedFom:
-    def __init__(self, n: int, backend, group=None):
+    def __init__(self, n: int, backend, group=None, exchange: str = "allgather"):
         self.n = n
         self.backend = backend
         self.group = group
@@ -77,6 +85,26 @@ class ShardedFom:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
         self.m = self.hi - self.lo
+        if exchange not in ("allgather", "peer"):
+            raise ValueError("exchange must be 'allgather' or 'peer'")
+        self.exchange = exchange
+        self._peer = None
+        if exchange == "peer":
+            from .peer import PeerExchange
+            self._peer = PeerExchange(n, ctx=getattr(backend, "ctx", None), group=group)
+            self._token = torch.zeros(1, dtype=torch.float32, device=backend.device)
+
+    def _peer_velocity(self, xi, fxi):
+        """Publish this rank's rows, order against the peers, evaluate in place."""
+        self._peer.write_local(xi)
+        if self.world > 1:
+            if dist.get_backend(self.group) == "nccl":
+                self._peer.barrier(self._token)
+            else:  # gloo (tests): host barrier after the copy completed
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)
+        be = self.backend
+        self._peer.velocity(be.gamma, be.delta, fxi, be.form, be.inflow)
 
     def _gather_positions(self, x_local, x_full):
         """Local SoA rows → full SoA state on every rank (the per-iteration exchange)."""
@@ -138,6 +166,7 @@ class ShardedFom:
             x_full.copy_(x_prev_full)
             refresh_due = (s % refresh) == 0 or not have_blocks
             refreshed = False
+            x_stale = False  # peer mode: x_full lags the published rows
             updates, converged, r0, rel = 0, False, 0.0, 0.0
             while True:
                 be.residual(xi, fxi, x_prev, f_prev, dt, r, norm2, m)
@@ -154,12 +183,21 @@ class ShardedFom:
                 if updates >= max_iters:
                     break
                 if refresh_due and not refreshed:
+                    if x_stale:
+                        self._gather_positions(xi, x_full)
+                        x_stale = False
                     be.newton_blocks(x_full, lo, hi, dt, inv)
                     refreshed = have_blocks = True
                 be.newton_update(inv, r, xi, m)
                 updates += 1
+                if self._peer is not None:
+                    self._peer_velocity(xi, fxi)
+                    x_stale = True
+                else:
+                    self._gather_positions(xi, x_full)
+                    be.velocity_rows(x_full, lo, hi, fxi)
+            if x_stale:  # the accepted state is the next step's Jacobian point
                 self._gather_positions(xi, x_full)
-                be.velocity_rows(x_full, lo, hi, fxi)
             x_prev, xi = xi, x_prev
             f_prev, fxi = fxi, f_prev
             x_prev_full.copy_(x_full)
@@ -169,6 +207,11 @@ class ShardedFom:
             rels.append(rel)
         be.check()
         return ShardedResult(snaps, iters, conv, rels, lo, hi)
+
+    def close(self):
+        if self._peer is not None:
+            self._peer.close()
+            self._peer = None
 
 
 class PtromInstanceSplit:

@@ -122,3 +122,62 @@ def test_ipc_exchange_two_processes_one_gpu(oracle):
         full[lo:hi], full[n + lo:n + hi] = o[:m], o[m:]
     ref = oracle.pairwise_velocity(w.x0, w.gamma, w.delta)
     assert rel(full, ref) <= 1e-12
+
+
+def _fom_peer_worker(rank, world, port, n, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2103_01983_b200.sharded import CudaBackend, ShardedFom
+        w = workloads.config1(n=n, seed=5)
+        g = torch.tensor(w.gamma, device="cuda")
+        fom = ShardedFom(n, CudaBackend(g, w.delta), exchange="peer")
+        res = fom.simulate(torch.tensor(w.x0, device="cuda"), w.dt, steps)
+        parts = [None] * world
+        dist.all_gather_object(parts, (res.lo, res.hi, res.snapshots_local.cpu().numpy(), res.iterations))
+        dist.barrier()
+        fom.close()
+        if rank == 0:
+            q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_fom_peer_exchange_two_processes(oracle):
+    """ShardedFom(exchange='peer'): velocity evaluations read the other rank's
+    rows in place (CUDA IPC); trajectory equals the oracle's within 1e-12."""
+    import queue
+    import torch.multiprocessing as mp
+    n, steps = 800, 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_fom_peer_worker, args=(r, 2, port, n, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = None
+    for _ in range(300):
+        try:
+            parts = q.get(timeout=1.0)
+            break
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert parts is not None, [p.exitcode for p in procs]
+    w = workloads.config1(n=n, seed=5)
+    snaps, iters, _, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps)
+    full = np.zeros((steps, 2 * n))
+    for lo, hi, loc, its in parts:
+        m = hi - lo
+        full[:, lo:hi], full[:, n + lo:n + hi] = loc[:, :m], loc[:, m:]
+    for k in range(steps):
+        assert rel(full[k], snaps[:, k]) <= 1e-12
