@@ -363,6 +363,31 @@ def main():
                     "avg_launch_ms": avg_kernel_s * 1e3, "launches": kern_launches.value,
                     "peaks": peaks}
 
+    # config 2's fp32 run (BASELINE configs[1]: "fp64 and fp32"): same workload,
+    # device-timed, L2 flushed; reported beside the fp64 headline
+    fp32 = None
+    if world == 1:
+        x32, g32 = x_full.float(), gamma.float()
+        out32 = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            dev.pairwise_velocity(x32, g32, w.delta, 0, None, 0, n, out32, ctx=ctx)
+        torch.cuda.synchronize()
+        k32 = max(10, min(args.steps, 100))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k32)]
+        for a, b in ev:
+            l2_flush.zero_()
+            a.record(stream)
+            dev.pairwise_velocity(x32, g32, w.delta, 0, None, 0, n, out32, ctx=ctx)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms32 = sum(a.elapsed_time(b) for a, b in ev) / k32
+        v32 = pairs_per_step / (ms32 * 1e-3)
+        fp32 = {"value": v32, "unit": UNIT, "ms_per_step": ms32, "steps": k32,
+                "roofline": {"bound": "fp32", "achieved": FLOPS_PER_PAIR * v32 / 1e12,
+                             "peak": peaks["fp32_ffma_tflops"] if peaks else None, "unit": "TFLOP/s",
+                             "frac": FLOPS_PER_PAIR * v32 / 1e12 / peaks["fp32_ffma_tflops"] if peaks else None,
+                             "kernel": "allpairs_f32_kernel<128,8> (csrc/allpairs.cu), step incl. chunk reduction"}}
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, sample = cpu_baseline_sample(w, 1, args.cpu_seconds)
@@ -378,6 +403,7 @@ def main():
                    if world > 1 else "single GPU"},
         "gpu_launches": 2 * args.steps,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
+        "fp32": fp32,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
