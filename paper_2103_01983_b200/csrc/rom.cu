@@ -76,11 +76,14 @@ __global__ void basis_rowmajor_kernel(DBasis b) {
 // once (one division per lane), then lane j owns column j (mode j, or x_ref
 // for j == m) of both rows and accumulates w_p·Φ(p, j) member by member.
 // The arithmetic is the reference's, so Φ̃, x̃⁰ and Γ̃ are bit-identical.
+constexpr long long kBigCluster = 4096;  // members: above, one CTA per cluster (reassign_big_kernel)
+
 __global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __restrict__ gamma) {
   const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (c >= s.n_c) return;
   const long long b0 = s.mem_off[c], b1 = s.mem_off[c + 1];
+  if (b1 - b0 > kBigCluster) return;
   double gsum = 0.0;
   for (long long k0 = b0; k0 < b1; k0 += 32) {
     const int cnt = (int)min(32LL, b1 - k0);
@@ -120,6 +123,136 @@ __global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __re
       s.gamma_tilde[c] = gsum;
       s.zero_gamma[c] = fb ? 1 : 0;
     }
+  }
+}
+
+__global__ void big_clusters_kernel(DSurrogate s, int* __restrict__ list, int* __restrict__ count) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c < s.n_c && s.mem_off[c + 1] - s.mem_off[c] > kBigCluster) list[atomicAdd(count, 1)] = (int)c;
+}
+
+// reduction.hpp:400-431 for the large clusters, one CTA each. Warps 1..7
+// stage the next chunk of members (ids and w_p = Γ_p/ΣΓ, then the row-major
+// basis rows through cp.async — all loads of a chunk in flight at once) into
+// the other shared-memory buffer while warp 0 runs the reference's sequential
+// chains (lane j owns column j of both rows) over the current chunk. ΣΓ is
+// the same producer/consumer pattern with lane 0 of warp 0 adding in order.
+// Same arithmetic and order as reassign_exact_kernel: bit-identical tables.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void producers_sync(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr)); }
+
+constexpr int kBigGChunk = 2048;  // members per ΣΓ chunk
+__global__ void __launch_bounds__(256) reassign_big_kernel(DSurrogate s, DBasis b, const double* __restrict__ gamma,
+                                                           const int* __restrict__ list,
+                                                           const int* __restrict__ count, int ch) {
+  extern __shared__ double big_smem[];
+  const int W = 2 * (b.m + 1);
+  double* rows = big_smem;                 // [2][ch][W]
+  double* wbuf = big_smem + 2 * ch * W;    // [2][max(ch, kBigGChunk)]
+  const int wcap = max(ch, kBigGChunk);
+  long long* sid = reinterpret_cast<long long*>(wbuf + 2 * wcap);  // [2][ch]
+  __shared__ double s_gsum;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ptid = threadIdx.x - 32, pn = blockDim.x - 32;  // producer threads (warps 1..7)
+  const int total = *count;
+  for (int li = blockIdx.x; li < total; li += gridDim.x) {
+    const long long c = list[li];
+    const long long b0 = s.mem_off[c], b1 = s.mem_off[c + 1];
+    // ---- ΣΓ in member order
+    auto gstage = [&](long long k0, int buf, int tid0, int nthr) {
+      const int cnt = (int)min((long long)kBigGChunk, b1 - k0);
+      double* gb = wbuf + buf * wcap;
+#pragma unroll 4
+      for (int i = tid0; i < cnt; i += nthr) gb[i] = gamma[s.mem_ids[k0 + i]];
+    };
+    gstage(b0, 0, threadIdx.x, blockDim.x);
+    __syncthreads();
+    double gsum = 0.0;
+    int buf = 0;
+    for (long long k0 = b0; k0 < b1; k0 += kBigGChunk) {
+      if (warp != 0) {
+        if (k0 + kBigGChunk < b1) gstage(k0 + kBigGChunk, buf ^ 1, ptid, pn);
+      } else if (lane == 0) {
+        const int cnt = (int)min((long long)kBigGChunk, b1 - k0);
+        const double* gb = wbuf + buf * wcap;
+        for (int i = 0; i < cnt; ++i) gsum = __dadd_rn(gsum, gb[i]);
+      }
+      __syncthreads();
+      buf ^= 1;
+    }
+    if (threadIdx.x == 0) s_gsum = gsum;
+    __syncthreads();
+    gsum = s_gsum;
+    const bool fb = gsum == 0.0;
+    const double inv_count = __ddiv_rn(1.0, (double)(b1 - b0));
+    // ---- weighted rows
+    auto stage = [&](long long k0, int bf, int tid0, int nthr, bool all) {
+      const int cnt = (int)min((long long)ch, b1 - k0);
+      double* rb = rows + (long long)bf * ch * W;
+      for (int i = tid0; i < cnt; i += nthr) {
+        const long long p = s.mem_ids[k0 + i];
+        sid[bf * ch + i] = p;
+        wbuf[bf * wcap + i] = fb ? inv_count : __ddiv_rn(gamma[p], gsum);
+      }
+      if (all) __syncthreads();
+      else producers_sync(nthr);
+      for (int e = tid0; e < cnt * W; e += nthr) {
+        const int i = e / W, j = e - i * W;
+        cp_async8(rb + e, b.rm + sid[bf * ch + i] * W + j);
+      }
+      cp_async_wait_all();
+    };
+    stage(b0, 0, threadIdx.x, blockDim.x, true);
+    __syncthreads();
+    // warp 0, lane l: columns l and l + 32 (mode j, or x_ref for j == m)
+    double ax = 0.0, ay = 0.0, ax2 = 0.0, ay2 = 0.0;
+    const int j = lane, j2 = lane + 32;
+    buf = 0;
+    for (long long k0 = b0; k0 < b1; k0 += ch) {
+      if (warp != 0) {
+        if (k0 + ch < b1) stage(k0 + ch, buf ^ 1, ptid, pn, false);
+      } else if (j <= b.m) {
+        const int cnt = (int)min((long long)ch, b1 - k0);
+        const double* rb = rows + (long long)buf * ch * W;
+        const double* wb = wbuf + buf * wcap;
+        if (j2 <= b.m) {
+          for (int i = 0; i < cnt; ++i) {
+            const double w = wb[i];
+            ax = __dadd_rn(ax, __dmul_rn(w, rb[i * W + j]));
+            ay = __dadd_rn(ay, __dmul_rn(w, rb[i * W + b.m + 1 + j]));
+            ax2 = __dadd_rn(ax2, __dmul_rn(w, rb[i * W + j2]));
+            ay2 = __dadd_rn(ay2, __dmul_rn(w, rb[i * W + b.m + 1 + j2]));
+          }
+        } else {
+#pragma unroll 4
+          for (int i = 0; i < cnt; ++i) {
+            const double w = wb[i];
+            ax = __dadd_rn(ax, __dmul_rn(w, rb[i * W + j]));
+            ay = __dadd_rn(ay, __dmul_rn(w, rb[i * W + b.m + 1 + j]));
+          }
+        }
+      }
+      __syncthreads();
+      buf ^= 1;
+    }
+    auto put = [&](int jj, double vx, double vy) {
+      if (jj < s.m) {
+        s.phi_tilde[c + (long long)jj * 2 * s.n_c] = vx;
+        s.phi_tilde[c + s.n_c + (long long)jj * 2 * s.n_c] = vy;
+      } else {
+        s.x0_tilde[c] = vx;
+        s.x0_tilde[c + s.n_c] = vy;
+        s.gamma_tilde[c] = gsum;
+        s.zero_gamma[c] = fb ? 1 : 0;
+      }
+    };
+    if (warp == 0 && j <= b.m) put(j, ax, ay);
+    if (warp == 0 && j2 <= b.m) put(j2, ax2, ay2);
+    __syncthreads();
   }
 }
 
@@ -1122,7 +1255,20 @@ void rom_basis_rowmajor(ptrom_ctx* ctx, DBasis& b) {
 }
 
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma) {
-  if (s.n_c > 0) reassign_exact_kernel<<<blocks_for(s.n_c * 32, 256), 256, 0, ctx->stream>>>(s, b, d_gamma);
+  if (s.n_c > 0) {
+    if (b.m > 63) throw status_error(PTROM_CONFIG_ERROR, "reassign: at most 63 modes");
+    int* big;  // [0] count, then the list of clusters above kBigCluster members
+    PTROM_CUDA(cudaMallocAsync(&big, sizeof(int) * (s.n_c + 1), ctx->stream));
+    PTROM_CUDA(cudaMemsetAsync(big, 0, sizeof(int), ctx->stream));
+    big_clusters_kernel<<<blocks_for(s.n_c, 256), 256, 0, ctx->stream>>>(s, big + 1, big);
+    const int ch = b.m <= 16 ? 256 : 128;  // members per weighted-pass chunk
+    const size_t smem = sizeof(double) * (2 * (size_t)ch * 2 * (b.m + 1) + 2 * std::max(ch, kBigGChunk)) +
+                        sizeof(long long) * 2 * ch;
+    PTROM_CUDA(cudaFuncSetAttribute(reassign_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    reassign_big_kernel<<<ctx->num_sms, 256, smem, ctx->stream>>>(s, b, d_gamma, big + 1, big, ch);
+    reassign_exact_kernel<<<blocks_for(s.n_c * 32, 256), 256, 0, ctx->stream>>>(s, b, d_gamma);
+    PTROM_CUDA(cudaFreeAsync(big, ctx->stream));
+  }
   if (s.u > 0) direct_gamma_kernel<<<blocks_for(s.u, 256), 256, 0, ctx->stream>>>(s, d_gamma);
   PTROM_LAUNCH_CHECK();
 }
