@@ -697,6 +697,7 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
     config_fail("build_tree: non-finite input");
   double side = std::max(x_hi - x_lo, y_hi - y_lo);
   if (side == 0.0) side = 1.0;
+  t.root_width = side;
   const double cx = (x_lo + x_hi) / 2.0, cy = (y_lo + y_hi) / 2.0;
   const double rb[4] = {cx - side / 2.0, cx + side / 2.0, cy - side / 2.0, cy + side / 2.0};
   const double rmid[2] = {(rb[0] + rb[1]) / 2.0, (rb[2] + rb[3]) / 2.0};

@@ -43,6 +43,7 @@ struct TreeNodes {
 struct Tree {
   long long n = 0;
   long long leaf_cap = 0;
+  double root_width = 0.0;  // node widths are root_width / 2^depth (depth <= 64)
   TreeNodes nodes;
   int* perm = nullptr;       // particle ids grouped by node slices
   int* slot = nullptr;       // perm^-1
