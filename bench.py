@@ -131,7 +131,7 @@ def cpu_baseline_sample(w, threads: int, target_seconds: float):
     pyoracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=0, t_end=rows, threads=threads)
     dt = time.perf_counter() - t0
     pairs = rows * (n - 1)
-    return pairs / dt, f"{rows} targets x {n} sources of config2 (N={n}), {dt:.1f} s"
+    return pairs / dt, f"{rows} targets x {n} sources of {w.name} (N={n}), {dt:.1f} s"
 
 
 def run_reference(args, rank, world):
@@ -139,10 +139,13 @@ def run_reference(args, rank, world):
     reference itself does not build here: Eigen absent)."""
     if rank != 0:
         return 0
+    if args.workload not in ("config2", "config5"):
+        import bench_extra
+        return bench_extra.run_reference(args, rank, world)
     from paper_2103_01983_b200 import workloads
     from oracle import pyoracle
     pyoracle.build()
-    w = workloads.config2()
+    w = workloads.config5() if args.workload == "config5" else workloads.config2()
     threads = os.cpu_count() or 1
     # calibrate one step to ~1.5 s of CPU work
     t0 = time.perf_counter()
@@ -158,7 +161,7 @@ def run_reference(args, rank, world):
         times.append(time.perf_counter() - t0)
     pairs = rows * (w.n - 1)
     value = pairs * len(times) / sum(times)
-    sample = f"{rows} targets x {w.n} sources per step (config2, N={w.n}); oracle port, {threads} threads"
+    sample = f"{rows} targets x {w.n} sources per step ({w.name}, N={w.n}); oracle port, {threads} threads"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
@@ -180,15 +183,16 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--workload", choices=["config2", "config3", "config4"], default="config2",
-                    help="config2 (default, the headline) | config3 Barnes-Hut | config4 PTROM online batch")
+    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5"], default="config2",
+                    help="config2 (default, the headline) | config3 Barnes-Hut | config4 PTROM online batch | "
+                         "config5 all-pairs evaluation at N = 4,194,304 (the 8-GPU sharded config)")
     ap.add_argument("--batch", type=int, default=512, help="config4: instances per step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.steps_given = args.steps is not None
     if args.steps is None:
-        args.steps = 200
-    if args.workload != "config2":
+        args.steps = 3 if args.workload == "config5" else 200
+    if args.workload not in ("config2", "config5"):
         import bench_extra
         rank = env_int("RANK", 0)
         world = env_int("WORLD_SIZE", 1)
@@ -212,7 +216,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = workloads.config2()
+    w = workloads.config5() if args.workload == "config5" else workloads.config2()
     n = w.n
     lo, hi = rank * n // world, (rank + 1) * n // world
     m = hi - lo
@@ -304,9 +308,10 @@ def main():
         fn = lambda: ctx.check(lib.ptrom_pairwise_velocity_f64(ctx.handle, n, hx.ctypes.data, hg.ctypes.data,
                                                                float(w.delta), 0, None, hf.ctypes.data,
                                                                ctypes.byref(cnt)))
-        for _ in range(3):
+        big = args.workload == "config5"  # ~10 s per evaluation
+        for _ in range(1 if big else 3):
             fn()
-        e2e_steps = max(5, min(args.steps, 50))
+        e2e_steps = max(1, args.steps) if big else max(5, min(args.steps, 50))
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             fn()
@@ -355,7 +360,7 @@ def main():
     if peaks:
         roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peaks["fp64_dfma_tflops"],
                     "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_dfma_tflops"],
-                    "traffic": ncu_traffic("r01_allpairs_vel64_ncu_summary.json"),
+                    "traffic": ncu_traffic("r01_allpairs_vel64_ncu_summary.json") if args.workload == "config2" else None,
                     "algorithmic_bytes_per_launch": 24 * n,
                     "kernel": "allpairs_f64_kernel<128,8,2,1,vel> (csrc/allpairs.cu)",
                     "peak_source": "measured live: tools/peaks.cu DFMA chain (MEASURED_PEAKS.json has no FP64)",
@@ -366,7 +371,7 @@ def main():
     # config 2's fp32 run (BASELINE configs[1]: "fp64 and fp32"): same workload,
     # device-timed, L2 flushed; reported beside the fp64 headline
     fp32 = None
-    if world == 1:
+    if world == 1 and args.workload == "config2":
         x32, g32 = x_full.float(), gamma.float()
         out32 = torch.empty(2 * n, dtype=torch.float32, device="cuda")
         for _ in range(3):
