@@ -8,15 +8,16 @@
 //   ptrom_simulate                rom.hpp:404-412
 //
 // Per Gauss–Newton evaluation of instance b:
-//   1. source positions: clusters c (x̃⁰ + Φ̃x̂, Γ̃), direct sources (x⁰_d + Φ_d x̂, Γ_d), sampled
-//      targets x̄ = x̄⁰ + Φ̄x̂ (positions_* kernels; instance-minor layout [source][b] so a warp of
-//      32 instances reads one cluster's 32 positions coalesced).
-//   2. hyperpair: one thread per (target, instance), cluster list then direct list, fused
+//   1. source positions: clusters c (x̃⁰ + Φ̃x̂, or the affine (S_A + μS_B)/(G_A + μG_B) form),
+//      direct sources (x⁰_d + Φ_d x̂), sampled targets x̄ = x̄⁰ + Φ̄x̂, as DMMA GEMMs
+//      (positions_*_mma kernels; instance-minor layout [source][b] so a warp of 32 instances
+//      reads one cluster's 32 positions coalesced).
+//   2. hyperpair: a warp per (target, 32 instances), cluster list then direct list, fused
 //      velocity + self-Jacobian (the reference's two calls kernel.hpp:29-73 per source).
-//   3. gn_eval: one CTA per instance streams the 2n_t sampled rows once: residual r̄, C = (I − h J)Φ̄
-//      formed in registers, A·C on the FP64 tensor cores (mma.sync m8n8k4 DMMA; tcgen05 has no
-//      fp64 kind), A·r̄ and Cᵀr̄ on the FP64 pipe, fixed-order cross-warp reduction, then the
-//      reference's convergence logic on ‖Cᵀr̄‖.
+//   3. gn_partial / gn_finish: split-K over the 2n_t sampled rows, 8 instances per CTA: residual
+//      r̄, C = (I − h J)Φ̄ rows (row per lane, staged in shared memory), A·C on the FP64 tensor
+//      cores (mma.sync m8n8k4 DMMA; tcgen05 has no fp64 kind), A·r̄ and Cᵀr̄; slice-ordered
+//      reduction, then the reference's convergence logic on ‖Cᵀr̄‖.
 //   4. qr_update: one warp per instance solves min‖AC·Δ + A r̄‖ by column-pivoted Householder QR
 //      (lane i owns row i of the 32 x 16 system) and applies x̂ += αΔ.
 //
@@ -39,7 +40,6 @@ namespace ptrom {
 
 namespace {
 
-constexpr int kGnThreads = 256;  // 8 warps per instance in gn_eval
 
 __device__ __forceinline__ double rcp64(double q) {
   double y;
@@ -770,166 +770,7 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(pairs, sum);
 }
 
-// -------------------------------------------------------------- gn_eval ---
-
-// One CTA per instance. Streams rows k of the sampled residual in steps of 4
-// (the DMMA k-extent); each warp owns every 8th step. MR = 32 residual modes
-// (4 row tiles of A), M = 16 modes (2 column tiles of C).
-template <int MR, int M>
-__global__ void __launch_bounds__(kGnThreads) gn_eval_kernel(DGnat g, int B, double h, const double* __restrict__ xbar,
-                                                             const double* __restrict__ xprev,
-                                                             const double* __restrict__ fbar,
-                                                             const double* __restrict__ fprev,
-                                                             const double* __restrict__ jac, GnState st_, int first) {
-  static_assert(MR % 8 == 0 && M % 8 == 0, "DMMA tiles");
-  constexpr int TI = MR / 8, TN = M / 8;
-  const int b = blockIdx.x;
-  if (!st_.active[b]) return;
-  const long long nt = g.n_s, rows = 2 * nt;
-  const double* xb = xbar + (long long)b * rows;
-  const double* xp = xprev + (long long)b * rows;
-  const double* fb = fbar + (long long)b * rows;
-  const double* fp = fprev + (long long)b * rows;
-  const double* jb = jac + (long long)b * nt * 4;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lr = lane >> 2, lc = lane & 3;  // fragment row / column
-  // the update is needed unless this evaluation is the last one allowed
-  const bool need_ac = !(st_.evals[b] + 1 - 1 >= st_.max_iters);
-  double acc[TI][TN][2];
-  double ar[TI];
-  double gr[TN];
-#pragma unroll
-  for (int i = 0; i < TI; ++i) {
-    ar[i] = 0.0;
-#pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  }
-#pragma unroll
-  for (int j = 0; j < TN; ++j) gr[j] = 0.0;
-
-  for (long long k0 = 4LL * warp; k0 < rows; k0 += 4LL * (kGnThreads / 32)) {
-    const long long r = k0 + lc;  // this thread's residual row
-    double rv = 0.0;
-    double cv[TN];
-    if (r < rows) {
-      // rom.hpp:310 residual, integrators.hpp:47-53 evaluation order
-      rv = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
-      const long long t = r < nt ? r : r - nt;
-      const double* J = jb + 4 * t;
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int m = j * 8 + lr;
-        const double px = g.phi_bar[t + m * rows], py = g.phi_bar[t + nt + m * rows];
-        // rom.hpp:79-81: row - h*(J_r0 * row_x + J_r1 * row_y)
-        const double own = r < nt ? px : py;
-        const double inner = r < nt ? __dadd_rn(__dmul_rn(J[0], px), __dmul_rn(J[1], py))
-                                    : __dadd_rn(__dmul_rn(J[2], px), __dmul_rn(J[3], py));
-        cv[j] = __dsub_rn(own, __dmul_rn(h, inner));
-        gr[j] = fma(cv[j], rv, gr[j]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < TN; ++j) cv[j] = 0.0;
-    }
-    double av[TI];
-#pragma unroll
-    for (int i = 0; i < TI; ++i) {
-      const long long ka = k0 + lc;
-      av[i] = ka < rows ? g.A[(i * 8 + lr) + ka * MR] : 0.0;
-      ar[i] = fma(av[i], rv, ar[i]);
-    }
-    if (need_ac) {
-#pragma unroll
-      for (int i = 0; i < TI; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc[i][j], av[i], cv[j]);
-    }
-  }
-  // ---- fixed-order reductions: over lc (lanes of a row group), then a
-  // pairwise tree over the 8 warps (4+4, 2+2, 1+1) through shared memory.
-  constexpr int NW = kGnThreads / 32;
-  __shared__ double red_ac[NW / 2][MR * M];
-  __shared__ double red_ar[NW][MR];
-  __shared__ double red_gr[NW][M];
-#pragma unroll
-  for (int i = 0; i < TI; ++i) {
-    double v = ar[i];
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    if (lc == 0) red_ar[warp][i * 8 + lr] = v;
-  }
-#pragma unroll
-  for (int j = 0; j < TN; ++j) {
-    double v = gr[j];
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    if (lc == 0) red_gr[warp][j * 8 + lr] = v;
-  }
-  for (int half = NW / 2; half >= 1; half >>= 1) {
-    if (warp >= half && warp < 2 * half) {
-#pragma unroll
-      for (int i = 0; i < TI; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          const int row = i * 8 + lr, col = j * 8 + lc * 2;
-          red_ac[warp - half][row + col * MR] = acc[i][j][0];
-          red_ac[warp - half][row + (col + 1) * MR] = acc[i][j][1];
-        }
-    }
-    __syncthreads();
-    if (warp < half) {
-#pragma unroll
-      for (int i = 0; i < TI; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          const int row = i * 8 + lr, col = j * 8 + lc * 2;
-          acc[i][j][0] += red_ac[warp][row + col * MR];
-          acc[i][j][1] += red_ac[warp][row + (col + 1) * MR];
-        }
-    }
-    __syncthreads();
-  }
-  if (warp == 0) {
-#pragma unroll
-    for (int i = 0; i < TI; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int row = i * 8 + lr, col = j * 8 + lc * 2;
-        st_.ac[(long long)b * MR * M + row + col * MR] = acc[i][j][0];
-        st_.ac[(long long)b * MR * M + row + (col + 1) * MR] = acc[i][j][1];
-      }
-  }
-  if (threadIdx.x < MR) {
-    double v = 0.0;
-    for (int w = 0; w < NW; ++w) v += red_ar[w][threadIdx.x];
-    st_.ar[(long long)b * MR + threadIdx.x] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double ss = 0.0;
-    for (int m = 0; m < M; ++m) {
-      double v = 0.0;
-      for (int w = 0; w < NW; ++w) v += red_gr[w][m];
-      ss += v * v;
-    }
-    const double gn = sqrt(ss);
-    // rom.hpp:309-324
-    const int evals = ++st_.evals[b];
-    bool done = false, conv = false;
-    if (evals == 1) {
-      st_.g0[b] = gn;
-      if (gn == 0.0) done = conv = true;
-    } else if (gn / st_.g0[b] <= st_.tol) {
-      done = conv = true;
-    }
-    if (!done && evals - 1 >= st_.max_iters) done = true;
-    st_.converged[b] = conv ? 1 : 0;
-    if (done) st_.active[b] = 0;
-    else atomicAdd(st_.n_active, 1);
-  }
-}
-
-
+// ------------------------------------------------------ Gauss–Newton ---
 // Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
 // slice of the sampled rows. A warp takes 32 rows at a time with one row per
 // lane (coalesced loads of x̄, x̄_prev, f̄, f̄_prev, the 2x2 Jacobian block and
