@@ -406,7 +406,7 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "parallelism": f"targets sharded x{world}, position exchange per step: {exchange}"
                    if world > 1 else "single GPU"},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 2 * args.steps,  # tile kernel + fixed-order chunk reduction
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
         "fp32": fp32,
     }

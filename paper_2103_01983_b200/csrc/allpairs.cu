@@ -219,6 +219,19 @@ struct SrcPeers {
   }
 };
 
+// Velocity epilogue fused into the tile kernel: the last CTA to finish a
+// target tile (arrival counter per tile) adds that tile's chunk partials in
+// chunk order — the same fixed order as reduce_velocity_f64_kernel, so the
+// result is bit-identical — adds the inflow, latches non-finite results and
+// writes f; f == nullptr keeps the separate reduction.
+struct FusedOut {
+  double* f = nullptr;
+  long long ld = 0, n_total = 0;
+  const double* inflow = nullptr;
+  unsigned* tile_ctr = nullptr;
+  DeviceStatus* st = nullptr;
+};
+
 template <int TPB, int T, int UNR, int MINB, bool VEL, bool JAC, int F4 = 4, class Src = SrcFlat>
 __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, Src src,
                                                            const double* __restrict__ gam, double inv2pi,
@@ -226,7 +239,7 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, Sr
                                                            long long chunk_len, double* __restrict__ part,
                                                            const double* __restrict__ txs,
                                                            const double* __restrict__ tys, long long t_base,
-                                                           int self_excl) {
+                                                           int self_excl, FusedOut fo) {
   // Targets i in [t_begin, t_begin + t_count) are rows i - t_base of
   // (txs, tys); self_excl = targets are sources with the same global index,
   // so pair (i, i) is skipped. External targets (lattice vertices,
@@ -309,6 +322,34 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, Sr
       out[(c++) * t_count + li] = jb[k];
       out[(c++) * t_count + li] = jc[k];
     }
+  }
+  if (VEL && !JAC && fo.f) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(fo.tile_ctr + blockIdx.x, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      if (ti[k] < 0) continue;
+      const long long li = ti[k] - t_begin;
+      double sx = 0.0, sy = 0.0;
+      for (unsigned c = 0; c < gridDim.y; ++c) {
+        sx += __ldcg(part + ((long long)c * 2 + 0) * t_count + li);
+        sy += __ldcg(part + ((long long)c * 2 + 1) * t_count + li);
+      }
+      const long long i = ti[k];
+      if (fo.inflow) {
+        sx = sx + fo.inflow[i];
+        sy = sy + fo.inflow[i + fo.n_total];
+      }
+      if (!isfinite(sx) || !isfinite(sy)) latch_status(fo.st, kStatusNonFiniteVelocity, i);
+      fo.f[li] = sx;
+      fo.f[li + fo.ld] = sy;
+    }
+    if (tid == 0) fo.tile_ctr[blockIdx.x] = 0;  // ready for the next launch
   }
 }
 
@@ -558,6 +599,9 @@ namespace {
 
 constexpr int kTPB = 128;
 constexpr int kReduceThreads = 256;
+// Set by dev_velocity_* for the duration of one launch: fuse the chunk
+// reduction into the tile kernel (FusedOut).
+thread_local const FusedOut* g_fuse = nullptr;
 
 template <class K>
 int resident_blocks(K kernel, int tpb) {
@@ -589,8 +633,20 @@ void launch_allpairs_src(ptrom_ctx* ctx, long long n, Src src, const double* gam
   const double inv2pi = 1.0 / (2.0 * M_PI);
   {
     ProfScope prof(ctx);
+    FusedOut fo{};
+    if (VEL && !JAC && g_fuse) {
+      fo = *g_fuse;
+      if (ctx->tile_ctr_cap < (size_t)tiles) {  // zero-initialised once; the kernel leaves it zeroed
+        if (ctx->tile_ctr) PTROM_CUDA(cudaFree(ctx->tile_ctr));
+        const size_t cap = std::max<size_t>((size_t)tiles, 4096);
+        PTROM_CUDA(cudaMalloc(&ctx->tile_ctr, cap * sizeof(unsigned)));
+        PTROM_CUDA(cudaMemset(ctx->tile_ctr, 0, cap * sizeof(unsigned)));
+        ctx->tile_ctr_cap = cap;
+      }
+      fo.tile_ctr = ctx->tile_ctr;
+    }
     kern<<<grid, TPB, 0, ctx->stream>>>(n, src, gamma, inv2pi, dp, t_begin, t_count, chunk_len, part, tx, ty, t_base,
-                                        self_excl);
+                                        self_excl, fo);
   }
   PTROM_LAUNCH_CHECK();
   *part_out = part;
@@ -704,10 +760,30 @@ void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double
   if (t_count <= 0) return;
   double* part;
   int chunks;
-  launch_allpairs_f64<true, false>(ctx, n, x, gamma, effective_delta(delta, form), t_begin, t_count, &part, &chunks);
-  reduce_velocity_f64_kernel<<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
-      n, t_begin, t_count, chunks, part, 2, inflow, f, ld, ctx->d_status);
-  PTROM_LAUNCH_CHECK();
+  if ((double)n * (double)t_count > 268435456.0) {  // large: the separate reduction is cheaper than a serial tail
+    launch_allpairs_f64<true, false>(ctx, n, x, gamma, effective_delta(delta, form), t_begin, t_count, &part,
+                                     &chunks);
+    reduce_velocity_f64_kernel<<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+        n, t_begin, t_count, chunks, part, 2, inflow, f, ld, ctx->d_status);
+    PTROM_LAUNCH_CHECK();
+    return;
+  }
+  // small (launch-bound, e.g. the N = 4,096 FOM): one launch, reduction fused
+  FusedOut fo;
+  fo.f = f;
+  fo.ld = ld;
+  fo.n_total = n;
+  fo.inflow = inflow;
+  fo.st = ctx->d_status;
+  g_fuse = &fo;
+  try {
+    launch_allpairs_f64<true, false>(ctx, n, x, gamma, effective_delta(delta, form), t_begin, t_count, &part,
+                                     &chunks);
+  } catch (...) {
+    g_fuse = nullptr;
+    throw;
+  }
+  g_fuse = nullptr;
 }
 
 // Kirchhoff–Routh energy (kernel.hpp:174-191): H = Σ_{i<j} Γi Γj log|r_ij| / 2π.

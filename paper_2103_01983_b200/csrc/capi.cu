@@ -144,6 +144,7 @@ void ptrom_destroy(ptrom_ctx* ctx) {
   if (ctx->d_status) cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+  if (ctx->tile_ctr) cudaFree(ctx->tile_ctr);
   if (ctx->scratch.base) cudaFree(ctx->scratch.base);
   if (ctx->io.base) cudaFree(ctx->io.base);
   for (auto& pr : ctx->prof_events) {

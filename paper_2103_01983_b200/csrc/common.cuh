@@ -107,7 +107,9 @@ struct ptrom_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   long long status_pair_n = 0;
-  int* h_counts = nullptr;  // pinned scratch for small D2H reads (tree level counts)  // n for decoding kStatusCoincidentPair (i·n + j)
+  int* h_counts = nullptr;  // pinned scratch for small D2H reads (tree level counts)
+  unsigned* tile_ctr = nullptr;  // per-target-tile arrival counters of the fused chunk reduction (kept zeroed)
+  size_t tile_ctr_cap = 0;  // n for decoding kStatusCoincidentPair (i·n + j)
   int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
   ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)
