@@ -161,15 +161,18 @@ __global__ void digit_kernel(long long n, const int* __restrict__ pos_rec, const
 }
 
 // Per level node: child counts (from the scan) and number of children.
+// Level descriptors live on the device: lv = {first record, node count,
+// records so far}; the host only holds upper bounds (Lub), so several levels
+// run back to back without a host round trip.
 template <class T>
-__global__ void child_count_kernel(int L, int lv_base, const int* __restrict__ rec_begin,
+__global__ void child_count_kernel(const int* __restrict__ lv, int Lub, const int* __restrict__ rec_begin,
                                    const int* __restrict__ rec_end, const unsigned char* __restrict__ rec_split,
                                    const T* __restrict__ scan, int* __restrict__ nchild) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= L) return;
-  const int r = lv_base + l;
+  if (l > Lub) return;
+  const int L = lv[1], r = lv[0] + l;
   int c = 0;
-  if (rec_split[r]) {
+  if (l < L && rec_split[r]) {
     const int span = rec_end[r] - rec_begin[r];
     const T a = scan[rec_begin[r]], b = scan[rec_end[r]];
     for (int q = 0; q < 4; ++q) c += quad_delta(a, b, q, span) != 0;
@@ -178,12 +181,23 @@ __global__ void child_count_kernel(int L, int lv_base, const int* __restrict__ r
 }
 
 // quadtree.hpp:87-116: child records in SW, SE, NW, NE order.
+// lv_next = {R, C, R + C} for the children level (C = total child count).
+__global__ void level_advance_kernel(const int* __restrict__ lv, const int* __restrict__ child_off, int Lub,
+                                     int* __restrict__ lv_next) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int C = child_off[Lub];
+    lv_next[0] = lv[2];
+    lv_next[1] = C;
+    lv_next[2] = lv[2] + C;
+  }
+}
+
 template <class T>
-__global__ void make_children_kernel(int L, int lv_base, int next_base, int leaf_cap, const T* __restrict__ scan,
+__global__ void make_children_kernel(const int* __restrict__ lv, int leaf_cap, const T* __restrict__ scan,
                                      const int* __restrict__ child_off, TreeRecords rec, int* __restrict__ n_split_next) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= L) return;
-  const int r = lv_base + l;
+  if (l >= lv[1]) return;
+  const int r = lv[0] + l, next_base = lv[2];
   if (!rec.split[r]) return;
   const int span = rec.end[r] - rec.begin[r];
   const T a = scan[rec.begin[r]], b = scan[rec.end[r]];
@@ -265,7 +279,7 @@ __device__ __forceinline__ void finish_exact(TreeRecords& rec, int r, int b, int
 // (multi-CTA, certified).
 constexpr int kSumWarps = kThreads / 32;
 constexpr int kLaneSum = 48;
-__global__ void __launch_bounds__(kThreads) sums_small_kernel(int R0, int R1, TreeRecords rec,
+__global__ void __launch_bounds__(kThreads) sums_small_kernel(const int* __restrict__ lv, TreeRecords rec,
                                                               const double* __restrict__ sx,
                                                               const double* __restrict__ sy,
                                                               const double* __restrict__ sg, int seq_max,
@@ -273,8 +287,9 @@ __global__ void __launch_bounds__(kThreads) sums_small_kernel(int R0, int R1, Tr
                                                               int* __restrict__ large_count,
                                                               int* __restrict__ mid_list,
                                                               int* __restrict__ mid_count) {
-  const int r = R0 + blockIdx.x * kThreads + threadIdx.x;
-  if (r >= R1) return;
+  const int i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= lv[1]) return;
+  const int r = lv[0] + i;
   const int b = rec.begin[r], e = rec.end[r];
   const int cnt = e - b;
   if (cnt > seq_max) {
@@ -703,7 +718,13 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   const double rmid[2] = {(rb[0] + rb[1]) / 2.0, (rb[2] + rb[3]) / 2.0};
 
   TreeRecords rec;
-  rec.alloc(std::max<size_t>(1024, (size_t)(n / std::max<long long>(1, leaf_cap)) * 2 + 16));
+  {
+    // room for the tree plus the speculative look-ahead of the level batches
+    // (see run_levels) so that the records rarely need to grow
+    const long long lcap = std::min<long long>(n + 1, 4 * (n / (leaf_cap + 1)) + 4);
+    const long long est = (n / std::max<long long>(1, leaf_cap)) * 2 + 16;
+    rec.alloc((size_t)std::max<long long>(1024, lcap > 524288 ? est : std::max(est, 5 * lcap)));
+  }
   const int zero = 0, one = 1, neg[4] = {-1, -1, -1, -1};
   const int nn32 = (int)n, d0 = 0;
   const unsigned char root_split = (n > leaf_cap) ? 1 : 0;
@@ -746,11 +767,14 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   unsigned* done_ctr = dalloc<unsigned>(1);
   PTROM_CUDA(cudaMemsetAsync(done_ctr, 0, sizeof(unsigned), s));
   int* mid_list = dalloc<int>(std::max<long long>(1, n));
-  auto run_sums = [&](int R0, int R1) {
-    sums_small_kernel<<<(R1 - R0 + kThreads - 1) / kThreads, kThreads, 0, s>>>(R0, R1, rec, sx, sy, sg, seq_max,
-                                                                               large_list, dcount + 1, mid_list,
-                                                                               dcount + 2);
-    const int mid_blocks = (int)std::min<long long>((R1 - R0 + kSumWarps - 1) / kSumWarps, ctx->num_sms * 16LL);
+  // level descriptors {first record, nodes, records so far}, ping-pong
+  int* lv_buf = dalloc<int>(8);
+  int* lv_cur = lv_buf;
+  int* lv_next = lv_buf + 4;
+  auto run_sums = [&](const int* lv, long long nodes_ub) {
+    sums_small_kernel<<<(int)std::max<long long>(1, (nodes_ub + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+        lv, rec, sx, sy, sg, seq_max, large_list, dcount + 1, mid_list, dcount + 2);
+    const int mid_blocks = (int)std::min<long long>((nodes_ub + kSumWarps - 1) / kSumWarps, ctx->num_sms * 16LL);
     sums_mid_kernel<<<std::max(1, mid_blocks), kThreads, 0, s>>>(rec, sx, sy, sg, mid_list, dcount + 2);
     large_sums_kernel<<<ctx->num_sms * 2, kThreads, 0, s>>>(rec, sx, sy, sg, large_list, dcount + 1, chunk_off,
                                                             large_part, done_ctr);
@@ -759,62 +783,71 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
 
   iota_copy_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.px, t.py, t.g, ord, sx, sy, sg, pr, root_split);
   PTROM_LAUNCH_CHECK();
+  {
+    const int lv0[4] = {0, 1, 1, 0};
+    PTROM_CUDA(cudaMemcpyAsync(lv_cur, lv0, sizeof(lv0), cudaMemcpyHostToDevice, s));
+  }
   // root sums
   PTROM_CUDA(cudaMemsetAsync(dcount, 0, 16, s));
-  run_sums(0, 1);
+  run_sums(lv_cur, 1);
 
-  int lv_base = 0, L = 1, R = 1;
-  // One host round trip per level: the child count decides the next level
-  // (no splitting node → no children → done).
+  int R = 1;
+  // Nodes per level are bounded by 4 x (splitting nodes) <= 4 n / (leaf_cap + 1):
+  // levels run in batches of K on upper bounds, one host round trip per batch
+  // (speculative levels past the last split are empty no-ops).
+  const long long Lcap = std::min<long long>(n + 1, 4 * (n / (leaf_cap + 1)) + 4);
+  const int K = Lcap > 524288 ? 1 : 4;
   auto run_levels = [&](auto* tag) {
   using T = std::remove_pointer_t<decltype(tag)>;
   T* flags = static_cast<T*>(flags_raw);
   T* scan = static_cast<T*>(scan_raw);
+  long long Lub = 1, R_ub = 1;
   while (root_split) {
-    // per-level buffers
-    if ((size_t)L > lvl_cap) {
-      dfree(nchild);
-      dfree(child_off);
-      lvl_cap = std::max<size_t>(L, lvl_cap * 2);
-      nchild = dalloc<int>(lvl_cap);
-      child_off = dalloc<int>(lvl_cap);
+    for (int lvl = 0; lvl < K; ++lvl) {
+      const long long Cub = std::min(Lcap, 4 * Lub);
+      rec.grow((size_t)(R_ub + Cub), (size_t)R_ub, s);
+      if ((size_t)(Lub + 1) > lvl_cap) {
+        dfree(nchild);
+        dfree(child_off);
+        lvl_cap = std::max<size_t>(Lub + 1, lvl_cap * 2);
+        nchild = dalloc<int>(lvl_cap);
+        child_off = dalloc<int>(lvl_cap);
+      }
+      digit_kernel<<<grid_for(ctx, n + 1), kThreads, 0, s>>>(n, pr, sx, sy, rec.mid, flags, digit);
+      PTROM_LAUNCH_CHECK();
+      if constexpr (std::is_same_v<T, uint4>)
+        PTROM_CUDA(cub::DeviceScan::ExclusiveScan(tmp, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0),
+                                                  n + 1, s));
+      else
+        PTROM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp_bytes, flags, scan, n + 1, s));
+      child_count_kernel<<<(int)((Lub + 1 + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+          lv_cur, (int)Lub, rec.begin, rec.end, rec.split, scan, nchild);
+      PTROM_LAUNCH_CHECK();
+      PTROM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan2_tmp_bytes, nchild, child_off, (int)(Lub + 1), s));
+      level_advance_kernel<<<1, 32, 0, s>>>(lv_cur, child_off, (int)Lub, lv_next);
+      PTROM_CUDA(cudaMemsetAsync(dcount, 0, 16, s));
+      make_children_kernel<<<(int)((Lub + kThreads - 1) / kThreads), kThreads, 0, s>>>(lv_cur, (int)leaf_cap, scan,
+                                                                                      child_off, rec, dcount);
+      PTROM_LAUNCH_CHECK();
+      scatter_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, pr, digit, scan, rec, ord, sx, sy, sg, ord_n, sx_n,
+                                                           sy_n, sg_n, pr_n);
+      PTROM_LAUNCH_CHECK();
+      std::swap(ord, ord_n);
+      std::swap(sx, sx_n);
+      std::swap(sy, sy_n);
+      std::swap(sg, sg_n);
+      std::swap(pr, pr_n);
+      run_sums(lv_next, Cub);
+      std::swap(lv_cur, lv_next);
+      Lub = Cub;
+      R_ub += Cub;
     }
-    digit_kernel<<<grid_for(ctx, n + 1), kThreads, 0, s>>>(n, pr, sx, sy, rec.mid, flags, digit);
-    PTROM_LAUNCH_CHECK();
-    if constexpr (std::is_same_v<T, uint4>)
-      PTROM_CUDA(cub::DeviceScan::ExclusiveScan(tmp, scan_tmp_bytes, flags, scan, U4Sum(), make_uint4(0, 0, 0, 0),
-                                                n + 1, s));
-    else
-      PTROM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp_bytes, flags, scan, n + 1, s));
-    child_count_kernel<<<(L + kThreads - 1) / kThreads, kThreads, 0, s>>>(L, lv_base, rec.begin, rec.end, rec.split,
-                                                                          scan, nchild);
-    PTROM_LAUNCH_CHECK();
-    PTROM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan2_tmp_bytes, nchild, child_off, L, s));
-    int last_off = 0, last_cnt = 0;
-    PTROM_CUDA(cudaMemcpyAsync(&h_counts[0], child_off + (L - 1), 4, cudaMemcpyDeviceToHost, s));
-    PTROM_CUDA(cudaMemcpyAsync(&h_counts[1], nchild + (L - 1), 4, cudaMemcpyDeviceToHost, s));
+    PTROM_CUDA(cudaMemcpyAsync(h_counts, lv_cur, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
     PTROM_CUDA(cudaStreamSynchronize(s));
-    last_off = h_counts[0];
-    last_cnt = h_counts[1];
-    const int C = last_off + last_cnt;
-    if (C == 0) break;
-    rec.grow((size_t)R + C, (size_t)R, s);
-    PTROM_CUDA(cudaMemsetAsync(dcount, 0, 16, s));
-    make_children_kernel<<<(L + kThreads - 1) / kThreads, kThreads, 0, s>>>(L, lv_base, R, (int)leaf_cap, scan,
-                                                                            child_off, rec, dcount);
-    PTROM_LAUNCH_CHECK();
-    scatter_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, pr, digit, scan, rec, ord, sx, sy, sg, ord_n, sx_n, sy_n,
-                                                         sg_n, pr_n);
-    PTROM_LAUNCH_CHECK();
-    std::swap(ord, ord_n);
-    std::swap(sx, sx_n);
-    std::swap(sy, sy_n);
-    std::swap(sg, sg_n);
-    std::swap(pr, pr_n);
-    run_sums(R, R + C);
-    lv_base = R;
-    L = C;
-    R += C;
+    R = h_counts[2];
+    if (h_counts[1] == 0) break;
+    Lub = h_counts[1];
+    R_ub = R;
   }
   };
   if (packed)
@@ -858,7 +891,7 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   cudaEventDestroy(ev1);
 
   void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags_raw, scan_raw, digit, dcount, tmp, nchild, child_off, large_list,
-                   chunk_off, large_part, done_ctr, mid_list, keys, keys_s, vals, order, rec2id, stmp};
+                   chunk_off, large_part, done_ctr, mid_list, lv_buf, keys, keys_s, vals, order, rec2id, stmp};
   for (void* p : frees) dfree(p);
   rec.free();
 }
