@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kThreads) sums_small_kernel(const int* __restr
     return;
   }
   double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+#pragma unroll 4
   for (int k = b; k < e; ++k) {
     const double g = sg[k], x = sx[k], y = sy[k];
     gs = __dadd_rn(gs, g);
@@ -312,42 +313,81 @@ __global__ void __launch_bounds__(kThreads) sums_small_kernel(const int* __restr
   finish_exact(rec, r, b, e, gs, wx, wy, plx, ply);
 }
 
-// Mid-size nodes (kLaneSum < members <= seq_max): one warp per node, the
-// lanes stage 32 members at a time (coalesced) in shared memory for lane 0's
-// sequential chain in the reference's order.
+// Mid-size nodes (kLaneSum < members <= seq_max): one warp per node. The
+// lanes stage kMidChunk members at a time in shared memory (coalesced, 4 per
+// lane) and prefetch the next chunk into registers while lane 0 runs the
+// reference's sequential chain over the current one (the chain, not the
+// load latency, bounds the node).
+constexpr int kMidChunk = 128;
 __global__ void __launch_bounds__(kThreads) sums_mid_kernel(TreeRecords rec, const double* __restrict__ sx,
                                                             const double* __restrict__ sy,
                                                             const double* __restrict__ sg,
                                                             const int* __restrict__ mid_list,
                                                             int* __restrict__ mid_count) {
-  __shared__ double st[kSumWarps][3][32];
+  __shared__ double st[kSumWarps][2][3][kMidChunk];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int total = *mid_count;
+  constexpr int PER = kMidChunk / 32;
   for (int w = blockIdx.x * kSumWarps + wib; w < total; w += gridDim.x * kSumWarps) {
     const int r = mid_list[w];
     const int b = rec.begin[r], e = rec.end[r];
-    double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
-    for (int c0 = b; c0 < e; c0 += 32) {
-      const int k = c0 + lane;
-      if (k < e) {
-        st[wib][0][lane] = sg[k];
-        st[wib][1][lane] = sx[k];
-        st[wib][2][lane] = sy[k];
+    double pg[PER], px[PER], py[PER];
+    auto fetch = [&](int c0) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int k = c0 + u * 32 + lane;
+        pg[u] = k < e ? sg[k] : 0.0;
+        px[u] = k < e ? sx[k] : 0.0;
+        py[u] = k < e ? sy[k] : 0.0;
       }
-      __syncwarp();
-      if (lane == 0) {
-        const int n = min(32, e - c0);
-        for (int j = 0; j < n; ++j) {
-          const double g = st[wib][0][j], x = st[wib][1][j], y = st[wib][2][j];
-          gs = __dadd_rn(gs, g);
-          wx = __dadd_rn(wx, __dmul_rn(g, x));
-          wy = __dadd_rn(wy, __dmul_rn(g, y));
-          plx = __dadd_rn(plx, x);
-          ply = __dadd_rn(ply, y);
+    };
+    auto put = [&](int buf) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        st[wib][buf][0][u * 32 + lane] = pg[u];
+        st[wib][buf][1][u * 32 + lane] = px[u];
+        st[wib][buf][2][u * 32 + lane] = py[u];
+      }
+    };
+    fetch(b);
+    put(0);
+    __syncwarp();
+    // The five chains run on lanes 0..4 (same instructions, one term each):
+    // lane 0 Σg, 1 Σg·x, 2 Σg·y, 3 Σx, 4 Σy — term = a·b with b = 1 where the
+    // reference adds a plain value (exact), so every chain is the reference's.
+    const int ia = lane == 3 ? 1 : lane == 4 ? 2 : 0;  // operand a: g, x or y
+    const int ib = lane == 1 ? 1 : lane == 2 ? 2 : -1;  // operand b: x, y or 1
+    double acc = 0.0;
+    int buf = 0;
+    for (int c0 = b; c0 < e; c0 += kMidChunk) {
+      const bool more = c0 + kMidChunk < e;
+      if (more) fetch(c0 + kMidChunk);  // in flight while lanes 0..4 add
+      if (lane < 5) {
+        const int n = min(kMidChunk, e - c0);
+        const double* A = st[wib][buf][ia];
+        const double* Bv = st[wib][buf][ib < 0 ? 0 : ib];
+        const double* Bp = ib < 0 ? nullptr : Bv;
+        int j = 0;
+        for (; j + 8 <= n; j += 8) {  // loads of 8 members issued ahead of the chain
+          double a8[8], b8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            a8[u] = A[j + u];
+            b8[u] = Bp ? Bp[j + u] : 1.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(a8[u], b8[u]));
         }
+        for (; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(A[j], Bp ? Bp[j] : 1.0));
       }
       __syncwarp();
+      if (more) put(buf ^ 1);
+      __syncwarp();
+      buf ^= 1;
     }
+    const double gs = __shfl_sync(0xffffffffu, acc, 0), wx = __shfl_sync(0xffffffffu, acc, 1),
+                 wy = __shfl_sync(0xffffffffu, acc, 2), plx = __shfl_sync(0xffffffffu, acc, 3),
+                 ply = __shfl_sync(0xffffffffu, acc, 4);
     if (lane == 0) finish_exact(rec, r, b, e, gs, wx, wy, plx, ply);
   }
 }
@@ -430,6 +470,7 @@ __global__ void __launch_bounds__(kThreads) large_sums_kernel(TreeRecords rec, c
     const int b = rec.begin[r] + (ci - base) * kChunk;
     const int e = min(rec.end[r], b + kChunk);
     double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // gs wx wy plx ply |g| |gx| |gy|
+#pragma unroll 4
     for (int k = b + threadIdx.x; k < e; k += kThreads) {
       const double g = sg[k], x = sx[k], y = sy[k];
       const double gx = __dmul_rn(g, x), gy = __dmul_rn(g, y);
