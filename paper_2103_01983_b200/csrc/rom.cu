@@ -179,7 +179,15 @@ __global__ void __launch_bounds__(256) reassign_big_kernel(DSurrogate s, DBasis 
       } else if (lane == 0) {
         const int cnt = (int)min((long long)kBigGChunk, b1 - k0);
         const double* gb = wbuf + buf * wcap;
-        for (int i = 0; i < cnt; ++i) gsum = __dadd_rn(gsum, gb[i]);
+        int i = 0;
+        for (; i + 8 <= cnt; i += 8) {  // loads issued ahead of the chain
+          double v8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v8[u] = gb[i + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) gsum = __dadd_rn(gsum, v8[u]);
+        }
+        for (; i < cnt; ++i) gsum = __dadd_rn(gsum, gb[i]);
       }
       __syncthreads();
       buf ^= 1;
@@ -228,8 +236,22 @@ __global__ void __launch_bounds__(256) reassign_big_kernel(DSurrogate s, DBasis 
             ay2 = __dadd_rn(ay2, __dmul_rn(w, rb[i * W + b.m + 1 + j2]));
           }
         } else {
-#pragma unroll 4
-          for (int i = 0; i < cnt; ++i) {
+          int i = 0;
+          for (; i + 4 <= cnt; i += 4) {  // loads issued ahead of the chains
+            double w4[4], vx4[4], vy4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              w4[u] = wb[i + u];
+              vx4[u] = rb[(i + u) * W + j];
+              vy4[u] = rb[(i + u) * W + b.m + 1 + j];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              ax = __dadd_rn(ax, __dmul_rn(w4[u], vx4[u]));
+              ay = __dadd_rn(ay, __dmul_rn(w4[u], vy4[u]));
+            }
+          }
+          for (; i < cnt; ++i) {
             const double w = wb[i];
             ax = __dadd_rn(ax, __dmul_rn(w, rb[i * W + j]));
             ay = __dadd_rn(ay, __dmul_rn(w, rb[i * W + b.m + 1 + j]));
