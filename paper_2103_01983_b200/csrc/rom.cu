@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(256) positions_clusters_mma_kernel(DSurrogate 
   constexpr int KS = MP / 4;
   constexpr int IC = 64, SX = MP + 4;
   __shared__ double sxh[IC * SX];
+  __shared__ double smu[IC];
   const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long ctiles = (s.n_c + CPT - 1) / CPT;
@@ -449,6 +450,8 @@ __global__ void __launch_bounds__(256) positions_clusters_mma_kernel(DSurrogate 
     const int icnt = min(IC, B - i0);
     __syncthreads();
     for (int e = threadIdx.x; e < icnt * MP; e += blockDim.x) sxh[(e / MP) * SX + e % MP] = xhat[(long long)i0 * MP + e];
+    if (AFFINE)
+      for (int e = threadIdx.x; e < icnt; e += blockDim.x) smu[e] = mu[i0 + e];
     __syncthreads();
     if (!w_ok) continue;
     for (int b0 = 0; b0 < icnt; b0 += 8) {
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(256) positions_clusters_mma_kernel(DSurrogate 
           double v[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const double m = b + e < B ? mu[b + e] : 0.0;
+            const double m = b + e < B ? smu[b + e - i0] : 0.0;
             const double G = fma(m, gb, ga);
             if (b + e < B && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
             // (S_A + μS_B)x̂-part / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times numerator
@@ -1154,16 +1157,18 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
     if (t) {
       const long long warps = (s.n_c + 1) / 2;
       positions_clusters_mma_kernel<true, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
-          s, tt, et, B, d_xhat, d_mu, d_active, w.cx, w.cy, ctx->d_status);
+          s, tt, et, B, d_xhat, d_mu, nullptr, w.cx, w.cy, ctx->d_status);
     } else {
       const long long warps = (s.n_c + 3) / 4;
       positions_clusters_mma_kernel<false, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
-          s, tt, et, B, d_xhat, d_mu, d_active, w.cx, w.cy, ctx->d_status);
+          s, tt, et, B, d_xhat, d_mu, nullptr, w.cx, w.cy, ctx->d_status);
     }
   }
   if (s.u > 0) {
     const long long warps = ((s.u + 3) / 4) * btiles;
-    positions_direct_mma_kernel<MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(s, et, B, d_xhat, d_active, w.dx,
+    // source positions are written for every instance: hyperpair skips the
+    // inactive ones (their x̂ is frozen), so the stores stay vectorised
+    positions_direct_mma_kernel<MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(s, et, B, d_xhat, nullptr, w.dx,
                                                                                 w.dy);
   }
   PTROM_LAUNCH_CHECK();
