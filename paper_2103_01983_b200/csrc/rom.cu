@@ -617,7 +617,7 @@ __global__ void hp_gamma_kernel(DSurrogate s, AffineTables t, bool affine, doubl
   }
 }
 
-template <int IB>
+template <int IB, bool OFF32>
 __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTables at, HpGamma hg,
                                                         const double* __restrict__ mu, int B,
                                                         const double* __restrict__ xbar,
@@ -703,9 +703,16 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
           for (int u = 0; u < U; ++u) ci[u] = s.cl_list[k + u];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const long long off = (long long)ci[u] * B;
-            sx[u] = cxb[off];
-            sy[u] = cyb[off];
+            // n_c·B < 2^32 (host-checked): 32-bit offsets, one IMAD.WIDE per gather
+            if (OFF32) {
+              const unsigned off = (unsigned)ci[u] * (unsigned)B;
+              sx[u] = cxb[off];
+              sy[u] = cyb[off];
+            } else {
+              const long long off = (long long)ci[u] * B;
+              sx[u] = cxb[off];
+              sy[u] = cyb[off];
+            }
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -755,9 +762,15 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
         for (int u = 0; u < 4; ++u) loc[u] = s.d_list[kd + u];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const long long off = (long long)loc[u] * B;
-          sx[u] = dxb[off];
-          sy[u] = dyb[off];
+          if (OFF32) {
+            const unsigned off = (unsigned)loc[u] * (unsigned)B;
+            sx[u] = dxb[off];
+            sy[u] = dyb[off];
+          } else {
+            const long long off = (long long)loc[u] * B;
+            sx[u] = dxb[off];
+            sy[u] = dyb[off];
+          }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -1232,9 +1245,11 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
       hg.gd = et->hgd;
       hg.gdab = et->hgdab;
     }
-    hyperpair_kernel<IB><<<blocks_for(threads, 128), 128, 0, st>>>(
-        s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy, w.dg, effective_delta(delta, form),
-        delta, d_inflow, n, d_active, d_f, d_jac, w.pairs, ctx->d_status);
+    const bool off32 = (double)std::max(s.n_c, s.u) * (double)B < 4294967296.0;
+    auto hk = off32 ? hyperpair_kernel<IB, true> : hyperpair_kernel<IB, false>;
+    hk<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy,
+                                                 w.dg, effective_delta(delta, form), delta, d_inflow, n, d_active, d_f,
+                                                 d_jac, w.pairs, ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
