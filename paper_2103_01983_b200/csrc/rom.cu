@@ -810,13 +810,31 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
 
 // ------------------------------------------------------ Gauss–Newton ---
 // Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
-// slice of the sampled rows. A warp takes 32 rows at a time with one row per
-// lane (coalesced loads of x̄, x̄_prev, f̄, f̄_prev, the 2x2 Jacobian block and
-// the Φ̄ rows), forms the residual r̄ and C = (I − h·J)Φ̄ rows in registers
-// (rom.hpp:71-84, the reference's rounding order), stages them in shared
-// memory and feeds A·C to DMMA (mma.sync m8n8k4 f64) 4 rows per k-step.
-// Partials [slice][b][32·M + 32 + M] are reduced in slice order by
-// gn_finish_kernel (deterministic).
+// slice of the sampled rows, 32 rows per chunk. Each chunk's operands are
+// staged by cp.async into a two-stage shared-memory ring while the previous
+// chunk computes: the A columns and the Φ̄ rows (x and y rows of each
+// sampled particle) once per CTA, and per instance warp the x̄, x̄_prev, f̄,
+// f̄_prev slices plus the row's half of the 2x2 Jacobian block. Lane l forms
+// the residual r̄ and C-row coefficients for row l (rom.hpp:71-84):
+// C = Φ̄_own − h·(J_a Φ̄_x + J_b Φ̄_y) = α Φ̄_x + β Φ̄_y; A·C goes to DMMA
+// (mma.sync m8n8k4 f64), 4 rows per k-step. Partials [slice][b][32·M + 32 +
+// M] are reduced in slice order by gn_finish_kernel (deterministic).
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int M>
+struct GnSmem {
+  static constexpr int AS = 36;         // A chunk row stride (doubles), kk-major
+  static constexpr int PS = 2 * M + 8;  // Φ̄ chunk row stride: [Φ̄_x (M) | Φ̄_y (M)], ≡ 8 mod 16
+  static constexpr int WS = 2 * 32 + 4 * 32;  // per warp: J halves (32 x 2), x̄ x̄p f̄ f̄p (4 x 32)
+  static constexpr int STAGE = 32 * AS + 32 * PS + 8 * WS;
+  static constexpr int BYTES = (2 * STAGE + 8 * 3 * 32) * 8;
+};
+
 template <int M>
 __global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat g, EngineTables et, int B, double h,
                                                          const double* __restrict__ xbar,
@@ -825,22 +843,57 @@ __global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat 
                                                          const double* __restrict__ fprev,
                                                          const double* __restrict__ jac, GnState st_,
                                                          long long slice_len, double* __restrict__ part) {
-  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M, CS = M + 4, AS = MR + 4;
-  // dynamic shared memory: the CTA's 32-row block of A (32 x AS, shared by
-  // the 8 instance warps), then per warp 32 x CS C rows and 32 residuals
-  extern __shared__ double gn_smem[];
+  using L = GnSmem<M>;
+  constexpr int MR = 32, TI = MR / 8, TN = M / 8, PART = MR * M + MR + M, AS = L::AS, PS = L::PS;
+  extern __shared__ __align__(16) double gn_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * 8 + warp;
   const bool ok = b < B && st_.active[b];
   const long long nt = g.n_s, rows = 2 * nt;
   const long long bb = ok ? b : 0;
-  const double* xb = xbar + bb * rows;
-  const double* xp = xprev + bb * rows;
-  const double* fb = fbar + bb * rows;
-  const double* fp = fprev + bb * rows;
+  // lanes 0-15 stage x̄ (f̄), lanes 16-31 x̄_prev (f̄_prev)
+  const double* wsrc0 = (lane < 16 ? xbar : xprev) + bb * rows;
+  const double* wsrc1 = (lane < 16 ? fbar : fprev) + bb * rows;
   const double* jb = jac + bb * nt * 4;
   const int lr = lane >> 2, lc = lane & 3;
   const bool need_ac = ok && !(st_.evals[b] >= st_.max_iters);
+  double* coef = gn_smem + 2 * L::STAGE + warp * 3 * 32;  // r̄, α, β per row of the chunk
+  const long long k_begin = blockIdx.y * slice_len, k_end = min(rows, k_begin + slice_len);
+  const int n_chunks = (int)((k_end - k_begin + 31) / 32);
+
+  auto issue = [&](int c) {
+    double* st = gn_smem + (c & 1) * L::STAGE;
+    const long long k0 = k_begin + 32LL * c;
+    // A: 32 columns x 32 rows = 512 16-byte units
+    for (int u = threadIdx.x; u < 512; u += 256) {
+      const int kk = u >> 4, i2 = u & 15;
+      const bool v = k0 + kk < k_end;
+      cp_async16z(st + kk * AS + 2 * i2, g.A + (v ? (k0 + kk) * MR + 2 * i2 : 0), v);
+    }
+    // Φ̄ rows of the chunk's particles: 32 x 2M doubles = 32·M units
+    double* sp = st + 32 * AS;
+    for (int u = threadIdx.x; u < 32 * M; u += 256) {
+      const int kk = u / M, q = u % M, half = q / (M / 2), c2 = q % (M / 2);
+      const long long r = k0 + kk;
+      const bool v = r < k_end;
+      const long long t = r < nt ? r : r - nt;
+      cp_async16z(sp + kk * PS + half * M + 2 * c2, et.pbr + (v ? (t + half * nt) * M + 2 * c2 : 0), v);
+    }
+    if (ok) {
+      double* sw = st + 32 * AS + 32 * PS + warp * L::WS;
+      const long long r = k0 + lane;
+      const bool v = r < k_end;
+      const long long t = r < nt ? r : r - nt;
+      cp_async16z(sw + 2 * lane, jb + (v ? 4 * t + (r < nt ? 0 : 2) : 0), v);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int uu = lane + 32 * e, arr = uu >> 4, q = uu & 15;
+        const bool vv = k0 + 2 * q < k_end;
+        cp_async16z(sw + 64 + arr * 32 + 2 * q, (e ? wsrc1 : wsrc0) + (vv ? k0 + 2 * q : 0), vv);
+      }
+    }
+  };
+
   double acc[TI][TN][2];
   double ar[TI];
   double gr[TN];
@@ -852,64 +905,51 @@ __global__ void __launch_bounds__(256, M <= 16 ? 3 : 2) gn_partial_kernel(DGnat 
   }
 #pragma unroll
   for (int j = 0; j < TN; ++j) gr[j] = 0.0;
-  double* sA = gn_smem;
-  double* swc = gn_smem + 32 * AS + warp * (32 * CS + 32);
-  double* swr = swc + 32 * CS;
-  const long long k_begin = blockIdx.y * slice_len, k_end = min(rows, k_begin + slice_len);
-  for (long long k0 = k_begin; k0 < k_end; k0 += 32) {
+
+  if (n_chunks > 0) issue(0);
+  cp_async_commit();
+  for (int c = 0; c < n_chunks; ++c) {
+    if (c + 1 < n_chunks) issue(c + 1);
+    cp_async_commit();
+    cp_async_wait1();
     __syncthreads();
-    // A columns k0..k0+31 (column-major, 32 rows each) → sA[kk][i] (stride AS)
-    for (int e = threadIdx.x; e < 32 * MR; e += blockDim.x) {
-      const int kk = e / MR, i = e % MR;
-      sA[kk * AS + i] = k0 + kk < k_end ? g.A[i + (k0 + kk) * MR] : 0.0;
-    }
-    const long long r = k0 + lane;
+    const double* st = gn_smem + (c & 1) * L::STAGE;
+    const double* sA = st;
+    const double* sp = st + 32 * AS;
     if (ok) {
-      if (r < k_end) {
-        swr[lane] = __dsub_rn(__dsub_rn(xb[r], xp[r]), __dmul_rn(h, __dadd_rn(fb[r], fp[r])));
-        const bool xrow = r < nt;
-        const long long t = xrow ? r : r - nt;
-        const double4 J = *reinterpret_cast<const double4*>(jb + 4 * t);
-        const double ja = xrow ? J.x : J.z, jb_ = xrow ? J.y : J.w;
-        const double2* pxr = reinterpret_cast<const double2*>(et.pbr + t * M);
-        const double2* pyr = reinterpret_cast<const double2*>(et.pbr + (t + nt) * M);
+      const double* sw = st + 32 * AS + 32 * PS + warp * L::WS;
+      const long long r = k_begin + 32LL * c + lane;
+      const double ja = sw[2 * lane], jbv = sw[2 * lane + 1];
+      const double x = sw[64 + lane], xp = sw[96 + lane], f = sw[128 + lane], fp = sw[160 + lane];
+      const bool xrow = r < nt;
+      const double hja = __dmul_rn(h, ja), hjb = __dmul_rn(h, jbv);
+      coef[lane] = __dsub_rn(__dsub_rn(x, xp), __dmul_rn(h, __dadd_rn(f, fp)));
+      coef[32 + lane] = xrow ? 1.0 - hja : -hja;
+      coef[64 + lane] = xrow ? -hjb : 1.0 - hjb;
+      __syncwarp();
 #pragma unroll
-        for (int m2 = 0; m2 < M / 2; ++m2) {
-          const double2 px = pxr[m2], py = pyr[m2];
-          const double own0 = xrow ? px.x : py.x, own1 = xrow ? px.y : py.y;
-          swc[lane * CS + 2 * m2] =
-              __dsub_rn(own0, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.x), __dmul_rn(jb_, py.x))));
-          swc[lane * CS + 2 * m2 + 1] =
-              __dsub_rn(own1, __dmul_rn(h, __dadd_rn(__dmul_rn(ja, px.y), __dmul_rn(jb_, py.y))));
+      for (int s4 = 0; s4 < 8; ++s4) {
+        const int kk = 4 * s4 + lc;
+        const double rvv = coef[kk], al = coef[32 + kk], be = coef[64 + kk];
+        double av[TI];
+#pragma unroll
+        for (int i = 0; i < TI; ++i) {
+          av[i] = sA[kk * AS + i * 8 + lr];
+          ar[i] = fma(av[i], rvv, ar[i]);
         }
-      } else {
-        swr[lane] = 0.0;
 #pragma unroll
-        for (int m = 0; m < M; ++m) swc[lane * CS + m] = 0.0;
+        for (int j = 0; j < TN; ++j) {
+          const double cvv = fma(al, sp[kk * PS + j * 8 + lr], be * sp[kk * PS + M + j * 8 + lr]);
+          gr[j] = fma(cvv, rvv, gr[j]);
+          if (need_ac) {
+#pragma unroll
+            for (int i = 0; i < TI; ++i) dmma(acc[i][j], av[i], cvv);
+          }
+        }
       }
+      __syncwarp();
     }
     __syncthreads();
-    if (!ok) continue;
-    const int steps = (int)min(8LL, (k_end - k0 + 3) / 4);
-    for (int s4 = 0; s4 < steps; ++s4) {
-      const int kk = 4 * s4 + lc;
-      const double rvv = swr[kk];
-      double av[TI];
-#pragma unroll
-      for (int i = 0; i < TI; ++i) {
-        av[i] = sA[kk * AS + i * 8 + lr];
-        ar[i] = fma(av[i], rvv, ar[i]);
-      }
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const double cvv = swc[kk * CS + j * 8 + lr];
-        gr[j] = fma(cvv, rvv, gr[j]);
-        if (need_ac) {
-#pragma unroll
-          for (int i = 0; i < TI; ++i) dmma(acc[i][j], av[i], cvv);
-        }
-      }
-    }
   }
   if (!ok) return;
   double* out = part + ((long long)blockIdx.y * B + b) * PART;
@@ -1363,7 +1403,7 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
   const long long groups = (B + 7) / 8;
   const int S = (int)std::max<long long>(1, std::min<long long>(64, (8LL * ctx->num_sms + groups - 1) / groups));
   const long long slice_len = ((rows + S - 1) / S + 31) / 32 * 32;
-  const size_t gn_smem = ((size_t)32 * (32 + 4) + (size_t)8 * (32 * (MP + 4) + 32)) * sizeof(double);
+  const size_t gn_smem = GnSmem<MP>::BYTES;
   PTROM_CUDA(cudaFuncSetAttribute(gn_partial_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gn_smem));
   double* part = (double*)alloc((size_t)S * B * (32 * MP + 32 + MP) * 8);
   int* h_active = nullptr;
