@@ -400,97 +400,106 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
 }
 
 
-// Cluster positions as a DMMA GEMM: one warp computes a tile of 2 clusters x
-// 4 quantities (X_A+S_A x̂ and X_B+S_B x̂ for x and y) x 8 instances with
-// K = MP modes (tables are the A operand, x̂ of 8 instances the B operand),
-// then combines (a + μ b)/(G_A + μ G_B) in the epilogue. Exact mode: 4
-// clusters x (x, y) per tile, x̃⁰ + Φ̃ x̂.
-template <bool AFFINE, int MP>
-__global__ void __launch_bounds__(256) positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et,
-                                                                     int B, const double* __restrict__ xhat,
-                                                                     const double* __restrict__ mu,
-                                                                     const unsigned char* __restrict__ active,
-                                                                     double* __restrict__ cx, double* __restrict__ cy,
-                                                                     DeviceStatus* st) {
-  // One warp per cluster tile; its table rows (the A operand) stay in
-  // registers while it sweeps all instance tiles of 8. x̂ is staged per CTA
-  // in shared memory, IC instances at a time (row stride MP + 4 doubles:
-  // conflict-free B-fragment loads).
-  constexpr int CPT = AFFINE ? 2 : 4;
-  constexpr int KS = MP / 4;
-  constexpr int IC = 64, SX = MP + 4;
-  __shared__ double sxh[IC * SX];
-  __shared__ double smu[IC];
-  const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long ctiles = (s.n_c + CPT - 1) / CPT;
-  const bool w_ok = warp_id < ctiles;
-  const long long c0 = warp_id * CPT;
-  const int lr = lane >> 2, lc = lane & 3;
-  const long long ca = c0 + (AFFINE ? (lr >> 2) : (lr >> 1));
-  const int q = AFFINE ? (lr & 3) : (lr & 1);  // 0 ax, 1 ay, 2 bx, 3 by
-  const bool c_ok = w_ok && ca < s.n_c;
-  const double* trow = et.ct + (ca * (AFFINE ? 4 : 2) + q) * (long long)MP;
-  double a[KS];
-#pragma unroll
-  for (int k = 0; k < KS; ++k) a[k] = c_ok ? trow[4 * k + lc] : 0.0;
-  double base_a = 0, base_b = 0, ga = 0, gb = 0;
-  if (c_ok) {
-    if (AFFINE) {
-      base_a = (q & 1) ? t.xa[ca + s.n_c] : t.xa[ca];
-      base_b = (q & 1) ? t.xb[ca + s.n_c] : t.xb[ca];
-      ga = t.ga[ca];
-      gb = t.gb[ca];
-    } else {
-      base_a = s.x0_tilde[ca + (q ? s.n_c : 0)];
-    }
+// Cluster positions as a DMMA GEMM. A warp tile is 4 clusters x (x, y) rows
+// x 8 instances with K = MP modes: the table rows are the A operand, x̂ of 8
+// instances the B operand. Affine mode runs two accumulator chains per tile
+// (X_A + S_A x̂ and X_B + S_B x̂ land in the same lane), and the epilogue
+// forms (a + μ b)/(G_A + μ G_B) on all 32 lanes. Exact mode is one chain,
+// x̃⁰ + Φ̃ x̂. The CTA stages x̂ (and μ) of up to `ic` instances in shared
+// memory once (row stride MP + 4 doubles: conflict-free B fragments), and its
+// 16 warps then sweep cluster tiles grid-stride.
+template <int MP>
+struct PosSmem {
+  static constexpr int SX = MP + 4;
+  static int ic(int B) {  // instances staged per pass: ≤ 96 KB of x̂
+    const int cap = (12288 / SX) / 8 * 8;
+    return std::min(cap, (B + 7) / 8 * 8);
   }
-  double* out = (q & 1) ? cy : cx;
-  for (int i0 = 0; i0 < B; i0 += IC) {
-    const int icnt = min(IC, B - i0);
+  static size_t bytes(int ic) { return (size_t)ic * (SX + 1) * 8; }
+};
+
+template <bool AFFINE, int MP>
+__global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et,
+                                                                        int B, int ic, const double* __restrict__ xhat,
+                                                                        const double* __restrict__ mu,
+                                                                        const unsigned char* __restrict__ active,
+                                                                        double* __restrict__ cx,
+                                                                        double* __restrict__ cy, DeviceStatus* st) {
+  constexpr int KS = MP / 4, SX = PosSmem<MP>::SX;
+  extern __shared__ __align__(16) double pos_smem[];
+  double* sxh = pos_smem;
+  double* smu = pos_smem + (size_t)ic * SX;
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  const long long ctiles = (s.n_c + 3) / 4;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long w0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int xy = lr & 1;
+  double* out = xy ? cy : cx;
+  const bool vec_store = !active && (B % 2 == 0);
+  for (int i0 = 0; i0 < B; i0 += ic) {
+    const int icnt = min(ic, B - i0), ipad = (icnt + 7) & ~7;
     __syncthreads();
-    for (int e = threadIdx.x; e < icnt * MP; e += blockDim.x) sxh[(e / MP) * SX + e % MP] = xhat[(long long)i0 * MP + e];
+    for (int e = threadIdx.x; e < ipad * (MP / 2); e += blockDim.x) {
+      const int r = e / (MP / 2), c2 = e % (MP / 2);
+      const double2 v = r < icnt ? reinterpret_cast<const double2*>(xhat + (long long)(i0 + r) * MP)[c2]
+                                 : make_double2(0.0, 0.0);
+      *reinterpret_cast<double2*>(sxh + r * SX + 2 * c2) = v;
+    }
     if (AFFINE)
       for (int e = threadIdx.x; e < icnt; e += blockDim.x) smu[e] = mu[i0 + e];
     __syncthreads();
-    if (!w_ok) continue;
-    for (int b0 = 0; b0 < icnt; b0 += 8) {
-      double acc[2] = {0.0, 0.0};
-      const int bl = b0 + lr;
+    for (long long tile = w0; tile < ctiles; tile += wstride) {
+      const long long ca = tile * 4 + (lr >> 1);
+      const bool c_ok = ca < s.n_c;
+      const double* trow = et.ct + (ca * (AFFINE ? 4 : 2) + xy) * (long long)MP;
+      double a0[KS], a1[KS];
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
-        const double x = bl < icnt ? sxh[bl * SX + 4 * k + lc] : 0.0;
-        dmma(acc, a[k], x);
+        a0[k] = c_ok ? trow[4 * k + lc] : 0.0;
+        a1[k] = (AFFINE && c_ok) ? trow[2 * MP + 4 * k + lc] : 0.0;
       }
-      const int b = i0 + b0 + 2 * lc;  // two consecutive instances per lane: one 16-byte store
-      if (AFFINE) {
-        const double o0 = __shfl_down_sync(0xffffffffu, acc[0], 8);  // S_B row partner (row + 2)
-        const double o1 = __shfl_down_sync(0xffffffffu, acc[1], 8);
-        if (q < 2 && c_ok) {
-          double v[2];
+      double base_a = 0, base_b = 0, ga = 0, gb = 0;
+      if (c_ok) {
+        if (AFFINE) {
+          base_a = t.xa[ca + (xy ? s.n_c : 0)];
+          base_b = t.xb[ca + (xy ? s.n_c : 0)];
+          ga = t.ga[ca];
+          gb = t.gb[ca];
+        } else {
+          base_a = s.x0_tilde[ca + (xy ? s.n_c : 0)];
+        }
+      }
+      for (int b0 = 0; b0 < icnt; b0 += 8) {
+        double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
+        const double* xrow = sxh + (b0 + lr) * SX + lc;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+          const double x = xrow[4 * k];
+          dmma(acc0, a0[k], x);
+          if (AFFINE) dmma(acc1, a1[k], x);
+        }
+        if (!c_ok) continue;
+        const int bl = b0 + 2 * lc, b = i0 + bl;  // two consecutive instances per lane: one 16-byte store
+        double v[2];
+        if (AFFINE) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const double m = b + e < B ? smu[b + e - i0] : 0.0;
+            const double m = bl + e < icnt ? smu[bl + e] : 0.0;
             const double G = fma(m, gb, ga);
-            if (b + e < B && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
-            // (S_A + μS_B)x̂-part / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times numerator
-            v[e] = fma(m, base_b + (e ? o1 : o0), base_a + acc[e]) * rcp64(G);
+            if (bl + e < icnt && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+            // (a + μ b) / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times numerator
+            v[e] = fma(m, base_b + acc1[e], base_a + acc0[e]) * rcp64(G);
           }
-          if (b + 1 < B && !active && (B % 2 == 0)) {
-            *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(v[0], v[1]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-              if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = v[e];
-          }
+        } else {
+          v[0] = base_a + acc0[0];
+          v[1] = base_a + acc0[1];
         }
-      } else if (c_ok) {
-        if (b + 1 < B && !active && (B % 2 == 0)) {
-          *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(base_a + acc[0], base_a + acc[1]);
+        if (vec_store && bl < icnt) {
+          *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(v[0], v[1]);
         } else {
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            if (b + e < B && (!active || active[b + e])) out[ca * B + b + e] = base_a + acc[e];
+            if (bl + e < icnt && (!active || active[b + e])) out[ca * B + b + e] = v[e];
         }
       }
     }
@@ -1207,14 +1216,20 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
   const AffineTables& tt = t ? *t : empty;
   const long long btiles = (B + 7) / 8;
   if (s.n_c > 0) {
+    const int ic = PosSmem<MP>::ic(B);
+    const size_t smem = PosSmem<MP>::bytes(ic);
+    const long long ctiles = (s.n_c + 3) / 4;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(2LL * ctx->num_sms, (ctiles + 15) / 16));
     if (t) {
-      const long long warps = (s.n_c + 1) / 2;
-      positions_clusters_mma_kernel<true, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
-          s, tt, et, B, d_xhat, d_mu, nullptr, w.cx, w.cy, ctx->d_status);
+      PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<true, MP>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      positions_clusters_mma_kernel<true, MP><<<grid, 512, smem, st>>>(s, tt, et, B, ic, d_xhat, d_mu, nullptr, w.cx,
+                                                                      w.cy, ctx->d_status);
     } else {
-      const long long warps = (s.n_c + 3) / 4;
-      positions_clusters_mma_kernel<false, MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(
-          s, tt, et, B, d_xhat, d_mu, nullptr, w.cx, w.cy, ctx->d_status);
+      PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<false, MP>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s, tt, et, B, ic, d_xhat, d_mu, nullptr,
+                                                                       w.cx, w.cy, ctx->d_status);
     }
   }
   if (s.u > 0) {
