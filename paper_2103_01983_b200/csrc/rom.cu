@@ -405,7 +405,8 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
 // instances the B operand. Affine mode runs two accumulator chains per tile
 // (X_A + S_A x̂ and X_B + S_B x̂ land in the same lane), and the epilogue
 // forms (a + μ b)/(G_A + μ G_B) on all 32 lanes. Exact mode is one chain,
-// x̃⁰ + Φ̃ x̂. The CTA stages x̂ (and μ) of up to `ic` instances in shared
+// x̃⁰ + Φ̃ x̂, and it also serves the direct sources (x⁰_d + Φ_d x̂, table
+// [u][2][mp]). The CTA stages x̂ (and μ) of up to `ic` instances in shared
 // memory once (row stride MP + 4 doubles: conflict-free B fragments), and its
 // 16 warps then sweep cluster tiles grid-stride.
 template <int MP>
@@ -419,7 +420,8 @@ struct PosSmem {
 };
 
 template <bool AFFINE, int MP>
-__global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(DSurrogate s, AffineTables t, EngineTables et,
+__global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long long nc, const double* __restrict__ tab,
+                                                                        const double* __restrict__ x0, AffineTables t,
                                                                         int B, int ic, const double* __restrict__ xhat,
                                                                         const double* __restrict__ mu,
                                                                         const unsigned char* __restrict__ active,
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(DSurroga
   double* sxh = pos_smem;
   double* smu = pos_smem + (size_t)ic * SX;
   const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
-  const long long ctiles = (s.n_c + 3) / 4;
+  const long long ctiles = (nc + 3) / 4;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
   const long long w0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int xy = lr & 1;
@@ -450,8 +452,8 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(DSurroga
     __syncthreads();
     for (long long tile = w0; tile < ctiles; tile += wstride) {
       const long long ca = tile * 4 + (lr >> 1);
-      const bool c_ok = ca < s.n_c;
-      const double* trow = et.ct + (ca * (AFFINE ? 4 : 2) + xy) * (long long)MP;
+      const bool c_ok = ca < nc;
+      const double* trow = tab + (ca * (AFFINE ? 4 : 2) + xy) * (long long)MP;
       double a0[KS], a1[KS];
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
@@ -461,12 +463,12 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(DSurroga
       double base_a = 0, base_b = 0, ga = 0, gb = 0;
       if (c_ok) {
         if (AFFINE) {
-          base_a = t.xa[ca + (xy ? s.n_c : 0)];
-          base_b = t.xb[ca + (xy ? s.n_c : 0)];
+          base_a = t.xa[ca + (xy ? nc : 0)];
+          base_b = t.xb[ca + (xy ? nc : 0)];
           ga = t.ga[ca];
           gb = t.gb[ca];
         } else {
-          base_a = s.x0_tilde[ca + (xy ? s.n_c : 0)];
+          base_a = x0[ca + (xy ? nc : 0)];
         }
       }
       for (int b0 = 0; b0 < icnt; b0 += 8) {
@@ -503,42 +505,6 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(DSurroga
         }
       }
     }
-  }
-}
-
-// Direct-source positions x⁰_d + Φ_d x̂ as a DMMA GEMM (4 sources x (x, y)
-// x 8 instances per warp tile).
-template <int MP>
-__global__ void positions_direct_mma_kernel(DSurrogate s, EngineTables et, int B, const double* __restrict__ xhat,
-                                            const unsigned char* __restrict__ active, double* __restrict__ dx,
-                                            double* __restrict__ dy) {
-  const long long warp_id = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long dtiles = (s.u + 3) / 4;
-  const int btiles = (B + 7) / 8;
-  if (warp_id >= dtiles * btiles) return;
-  const long long d0 = (warp_id / btiles) * 4;
-  const int b0 = (int)(warp_id % btiles) * 8;
-  const int lr = lane >> 2, lc = lane & 3;
-  const long long d = d0 + (lr >> 1);
-  const int q = lr & 1;
-  const bool ok = d < s.u;
-  const double* trow = et.dt + (d * 2 + q) * (long long)MP;
-  double acc[2] = {0.0, 0.0};
-  const int bb = b0 + lr;
-#pragma unroll
-  for (int k0 = 0; k0 < MP; k0 += 4) {
-    const int k = k0 + lc;
-    const double a = ok ? trow[k] : 0.0;
-    const double x = bb < B ? xhat[(long long)bb * MP + k] : 0.0;
-    dmma(acc, a, x);
-  }
-  if (!ok) return;
-  const double base = s.direct_x0[d + (q ? s.u : 0)];
-  for (int e = 0; e < 2; ++e) {
-    const int b = b0 + 2 * lc + e;
-    if (b >= B || (active && !active[b])) continue;
-    (q == 0 ? dx : dy)[d * B + b] = base + acc[e];
   }
 }
 
@@ -1214,7 +1180,6 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
   cudaStream_t st = ctx->stream;
   AffineTables empty{};
   const AffineTables& tt = t ? *t : empty;
-  const long long btiles = (B + 7) / 8;
   if (s.n_c > 0) {
     const int ic = PosSmem<MP>::ic(B);
     const size_t smem = PosSmem<MP>::bytes(ic);
@@ -1223,21 +1188,26 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
     if (t) {
       PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<true, MP>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      positions_clusters_mma_kernel<true, MP><<<grid, 512, smem, st>>>(s, tt, et, B, ic, d_xhat, d_mu, nullptr, w.cx,
+      positions_clusters_mma_kernel<true, MP><<<grid, 512, smem, st>>>(s.n_c, et.ct, nullptr, tt, B, ic, d_xhat, d_mu, nullptr, w.cx,
                                                                       w.cy, ctx->d_status);
     } else {
       PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<false, MP>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s, tt, et, B, ic, d_xhat, d_mu, nullptr,
+      positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s.n_c, et.ct, s.x0_tilde, tt, B, ic, d_xhat, d_mu, nullptr,
                                                                        w.cx, w.cy, ctx->d_status);
     }
   }
   if (s.u > 0) {
-    const long long warps = ((s.u + 3) / 4) * btiles;
     // source positions are written for every instance: hyperpair skips the
     // inactive ones (their x̂ is frozen), so the stores stay vectorised
-    positions_direct_mma_kernel<MP><<<blocks_for(warps * 32, 256), 256, 0, st>>>(s, et, B, d_xhat, nullptr, w.dx,
-                                                                                w.dy);
+    const int ic = PosSmem<MP>::ic(B);
+    const size_t smem = PosSmem<MP>::bytes(ic);
+    const long long dtiles = (s.u + 3) / 4;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(2LL * ctx->num_sms, (dtiles + 15) / 16));
+    PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<false, MP>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s.u, et.dt, s.direct_x0, tt, B, ic, d_xhat,
+                                                                     nullptr, nullptr, w.dx, w.dy, ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
 }
