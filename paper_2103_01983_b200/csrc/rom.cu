@@ -531,18 +531,35 @@ __global__ void positions_direct_kernel(DSurrogate s, AffineTables t, int B, int
 }
 
 // Sampled targets x̄ = x̄⁰ + Φ̄ x̂ (rom.hpp:306, 329); instance-major [b][row].
-__global__ void positions_targets_kernel(DGnat g, int B, const double* __restrict__ xhat,
-                                         const unsigned char* __restrict__ active, double* __restrict__ xbar) {
+// A thread keeps one row of Φ̄ in registers and sweeps 32 instances (x̂
+// staged in shared memory); stores are coalesced along the rows. Same
+// sequential fma chain over the modes as the reference's dot product.
+template <int MP>
+__global__ void __launch_bounds__(256) positions_targets_kernel(DGnat g, int B, const double* __restrict__ xhat,
+                                                               const unsigned char* __restrict__ active,
+                                                               double* __restrict__ xbar) {
+  constexpr int IB = 32;
+  __shared__ double sx[IB * MP];
+  __shared__ unsigned char sact[IB];
   const long long rows = 2 * g.n_s;
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= rows * B) return;
-  const int b = (int)(idx / rows);
-  const long long r = idx % rows;
-  if (active && !active[b]) return;
-  const double* xh = xhat + (long long)b * g.mp;
-  double a = 0.0;
-  for (int j = 0; j < g.m; ++j) a = fma(g.phi_bar[r + j * rows], xh[j], a);
-  xbar[idx] = g.x0_bar[r] + a;
+  const int b0 = blockIdx.y * IB, nb = min(IB, B - b0);
+  for (int e = threadIdx.x; e < nb * MP; e += blockDim.x) sx[e] = xhat[(long long)b0 * MP + e];
+  if (threadIdx.x < nb) sact[threadIdx.x] = active ? active[b0 + threadIdx.x] : 1;
+  __syncthreads();
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double ph[MP];
+#pragma unroll
+  for (int j = 0; j < MP; ++j) ph[j] = j < g.m ? g.phi_bar[r + j * rows] : 0.0;
+  const double x0 = g.x0_bar[r];
+  for (int i = 0; i < nb; ++i) {
+    if (!sact[i]) continue;
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < MP; ++j)
+      if (j < g.m) a = fma(ph[j], sx[i * MP + j], a);
+    xbar[(long long)(b0 + i) * rows + r] = x0 + a;
+  }
 }
 
 // ------------------------------------------------------------- hyperpair ---
@@ -1251,7 +1268,13 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
   }
   const double* xbar = d_xbar_in;
   if (g) {
-    positions_targets_kernel<<<blocks_for(2 * g->n_s * B, 256), 256, 0, st>>>(*g, B, d_xhat, d_active, d_xbar_out);
+    const dim3 grid((unsigned)((2 * g->n_s + 255) / 256), (unsigned)((B + 31) / 32));
+    switch (g->mp) {
+      case 8: positions_targets_kernel<8><<<grid, 256, 0, st>>>(*g, B, d_xhat, d_active, d_xbar_out); break;
+      case 16: positions_targets_kernel<16><<<grid, 256, 0, st>>>(*g, B, d_xhat, d_active, d_xbar_out); break;
+      case 24: positions_targets_kernel<24><<<grid, 256, 0, st>>>(*g, B, d_xhat, d_active, d_xbar_out); break;
+      default: positions_targets_kernel<32><<<grid, 256, 0, st>>>(*g, B, d_xhat, d_active, d_xbar_out); break;
+    }
     xbar = d_xbar_out;
   }
   PTROM_LAUNCH_CHECK();
