@@ -143,6 +143,23 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// L1-allocating variants (data reused by neighbouring warps)
+__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem, bool) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8_ca(void* smem, const void* gmem, bool) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void producers_sync(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr)); }
 
 constexpr int kBigGChunk = 2048;  // members per ΣΓ chunk
@@ -362,8 +379,7 @@ __global__ void engine_tables_kernel(DSurrogate s, AffineTables t, DGnat g, int 
 template <bool AFFINE>
 __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, int xs, const double* __restrict__ xhat,
                                           const double* __restrict__ mu, const unsigned char* __restrict__ active,
-                                          double* __restrict__ cx, double* __restrict__ cy, double* __restrict__ cg,
-                                          DeviceStatus* st) {
+                                          double2* __restrict__ cxy, DeviceStatus* st) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= s.n_c * B) return;
   const long long c = idx / B;
@@ -377,9 +393,7 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
       ax = fma(s.phi_tilde[c + j * ld], xh[j], ax);
       ay = fma(s.phi_tilde[c + s.n_c + j * ld], xh[j], ay);
     }
-    cx[idx] = s.x0_tilde[c] + ax;
-    cy[idx] = s.x0_tilde[c + s.n_c] + ay;
-    cg[idx] = s.gamma_tilde[c];
+    cxy[idx] = make_double2(s.x0_tilde[c] + ax, s.x0_tilde[c + s.n_c] + ay);
   } else {
     double ax = t.xa[c], ay = t.xa[c + s.n_c], bx = t.xb[c], by = t.xb[c + s.n_c];
     for (int j = 0; j < s.m; ++j) {
@@ -393,9 +407,7 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
     const double g = t.ga[c] + m * t.gb[c];
     if (g == 0.0) latch_status(st, kStatusZeroClusterCirculation, c);
     const double ig = 1.0 / g;
-    cx[idx] = fma(m, bx, ax) * ig;
-    cy[idx] = fma(m, by, ay) * ig;
-    cg[idx] = g;
+    cxy[idx] = make_double2(fma(m, bx, ax) * ig, fma(m, by, ay) * ig);
   }
 }
 
@@ -425,8 +437,8 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long lon
                                                                         int B, int ic, const double* __restrict__ xhat,
                                                                         const double* __restrict__ mu,
                                                                         const unsigned char* __restrict__ active,
-                                                                        double* __restrict__ cx,
-                                                                        double* __restrict__ cy, DeviceStatus* st) {
+                                                                        double2* __restrict__ out,
+                                                                        DeviceStatus* st) {
   constexpr int KS = MP / 4, SX = PosSmem<MP>::SX;
   extern __shared__ __align__(16) double pos_smem[];
   double* sxh = pos_smem;
@@ -436,8 +448,6 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long lon
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
   const long long w0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int xy = lr & 1;
-  double* out = xy ? cy : cx;
-  const bool vec_store = !active && (B % 2 == 0);
   for (int i0 = 0; i0 < B; i0 += ic) {
     const int icnt = min(ic, B - i0), ipad = (icnt + 7) & ~7;
     __syncthreads();
@@ -480,15 +490,14 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long lon
           dmma(acc0, a0[k], x);
           if (AFFINE) dmma(acc1, a1[k], x);
         }
-        if (!c_ok) continue;
-        const int bl = b0 + 2 * lc, b = i0 + bl;  // two consecutive instances per lane: one 16-byte store
+        const int bl = b0 + 2 * lc, b = i0 + bl;  // lane holds instances b, b+1 of its row
         double v[2];
         if (AFFINE) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double m = bl + e < icnt ? smu[bl + e] : 0.0;
             const double G = fma(m, gb, ga);
-            if (bl + e < icnt && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+            if (c_ok && bl + e < icnt && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
             // (a + μ b) / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times numerator
             v[e] = fma(m, base_b + acc1[e], base_a + acc0[e]) * rcp64(G);
           }
@@ -496,23 +505,20 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long lon
           v[0] = base_a + acc0[0];
           v[1] = base_a + acc0[1];
         }
-        if (vec_store && bl < icnt) {
-          *reinterpret_cast<double2*>(out + ca * B + b) = make_double2(v[0], v[1]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (bl + e < icnt && (!active || active[b + e])) out[ca * B + b + e] = v[e];
-        }
+        // the x-row lane and the y-row lane (lane ^ 4) swap one value: the
+        // x lane stores (x, y) of instance b, the y lane that of b + 1
+        const double other = __shfl_xor_sync(0xffffffffu, xy ? v[0] : v[1], 4);
+        const int e = xy;
+        if (c_ok && bl + e < icnt && (!active || active[b + e]))
+          out[ca * B + b + e] = xy ? make_double2(other, v[1]) : make_double2(v[0], other);
       }
     }
   }
 }
 
-// Direct sources: x⁰_d + Φ_d x̂ (rom.hpp:114), Γ_d(μ).
-template <bool AFFINE>
-__global__ void positions_direct_kernel(DSurrogate s, AffineTables t, int B, int xs, const double* __restrict__ xhat,
-                                        const double* __restrict__ mu, const unsigned char* __restrict__ active,
-                                        double* __restrict__ dx, double* __restrict__ dy, double* __restrict__ dg) {
+// Direct sources: x⁰_d + Φ_d x̂ (rom.hpp:114); Γ_d(μ) comes from the Γ tables.
+__global__ void positions_direct_kernel(DSurrogate s, int B, int xs, const double* __restrict__ xhat,
+                                        const unsigned char* __restrict__ active, double2* __restrict__ dxy) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= s.u * B) return;
   const long long k = idx / B;
@@ -525,9 +531,7 @@ __global__ void positions_direct_kernel(DSurrogate s, AffineTables t, int B, int
     ax = fma(s.direct_phi[k + j * ld], xh[j], ax);
     ay = fma(s.direct_phi[k + s.u + j * ld], xh[j], ay);
   }
-  dx[idx] = s.direct_x0[k] + ax;
-  dy[idx] = s.direct_x0[k + s.u] + ay;
-  dg[idx] = AFFINE ? t.dga[k] + mu[b] * t.dgb[k] : s.direct_gamma[k];
+  dxy[idx] = make_double2(s.direct_x0[k] + ax, s.direct_x0[k + s.u] + ay);
 }
 
 // Sampled targets x̄ = x̄⁰ + Φ̄ x̂ (rom.hpp:306, 329); instance-major [b][row].
@@ -613,10 +617,8 @@ template <int IB, bool OFF32>
 __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTables at, HpGamma hg,
                                                         const double* __restrict__ mu, int B,
                                                         const double* __restrict__ xbar,
-                                                        const double* __restrict__ cx, const double* __restrict__ cy,
-                                                        const double* __restrict__ cg, const double* __restrict__ dx,
-                                                        const double* __restrict__ dy, const double* __restrict__ dg,
-                                                        double dp, double delta, const double* __restrict__ inflow,
+                                                        const double2* __restrict__ cxy,
+                                                        const double2* __restrict__ dxy, double dp, double delta, const double* __restrict__ inflow,
                                                         long long n, const unsigned char* __restrict__ active,
                                                         double* __restrict__ f, double* __restrict__ jac,
                                                         unsigned long long* __restrict__ pairs, DeviceStatus* st) {
@@ -671,8 +673,7 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
         }
         return hg.gc ? hg.gc[ci] : s.gamma_tilde[ci] * inv2pi;
       };
-      const double* cxb = cx + b;
-      const double* cyb = cy + b;
+      const double2* cpb = cxy + b;
       // Cluster list, U entries per round: the U list reads, then the 2U
       // position loads are issued before any arithmetic (memory-level
       // parallelism for the L2/HBM-latency-bound gathers); order of the
@@ -696,15 +697,9 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             // n_c·B < 2^32 (host-checked): 32-bit offsets, one IMAD.WIDE per gather
-            if (OFF32) {
-              const unsigned off = (unsigned)ci[u] * (unsigned)B;
-              sx[u] = cxb[off];
-              sy[u] = cyb[off];
-            } else {
-              const long long off = (long long)ci[u] * B;
-              sx[u] = cxb[off];
-              sy[u] = cyb[off];
-            }
+            const double2 p = OFF32 ? cpb[(unsigned)ci[u] * (unsigned)B] : cpb[(long long)ci[u] * B];
+            sx[u] = p.x;
+            sy[u] = p.y;
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -717,8 +712,8 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
         }
         for (; k < ke; ++k) {
           const int ci = s.cl_list[k];
-          const long long off = (long long)ci * B;
-          const double sx = cxb[off], sy = cyb[off];
+          const double2 p = cpb[(long long)ci * B];
+          const double sx = p.x, sy = p.y;
           if (CHECK && sx == px && sy == py) {
             ++skipped;
             continue;
@@ -743,8 +738,7 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
         }
         return hg.gd ? hg.gd[loc] : s.direct_gamma[loc] * inv2pi;
       };
-      const double* dxb = dx + b;
-      const double* dyb = dy + b;
+      const double2* dpb = dxy + b;
       long long kd = s.d_off[t];
       const long long kde = s.d_off[t + 1];
       for (; kd + 4 <= kde; kd += 4) {
@@ -754,15 +748,9 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
         for (int u = 0; u < 4; ++u) loc[u] = s.d_list[kd + u];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (OFF32) {
-            const unsigned off = (unsigned)loc[u] * (unsigned)B;
-            sx[u] = dxb[off];
-            sy[u] = dyb[off];
-          } else {
-            const long long off = (long long)loc[u] * B;
-            sx[u] = dxb[off];
-            sy[u] = dyb[off];
-          }
+          const double2 p = OFF32 ? dpb[(unsigned)loc[u] * (unsigned)B] : dpb[(long long)loc[u] * B];
+          sx[u] = p.x;
+          sy[u] = p.y;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -774,8 +762,8 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
       for (; kd < kde; ++kd) {
         const int loc = s.d_list[kd];
         if (hg.self_loc ? loc == self_loc : s.direct_ids[loc] == pid) continue;
-        const long long off = (long long)loc * B;
-        add(dxb[off], dyb[off], dgam(loc));
+        const double2 p = dpb[(long long)loc * B];
+        add(p.x, p.y, dgam(loc));
         ++cnt;
       }
       if (inflow) {
@@ -800,6 +788,267 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(pairs, sum);
 }
 
+// Batched form (B >= 32): a warp is one target x 32 consecutive instances,
+// so the target's cluster and near-field lists are warp-uniform. The warp
+// reads 32 list entries with one coalesced load (the next 32 prefetched while
+// the current ones are consumed) and broadcasts each with a shuffle; per
+// round of U entries the 2U position gathers (32 instances = 256 contiguous
+// bytes each) and the U Γ loads are all in flight before any arithmetic.
+// Every lane walks the lists (lanes past B or of inactive instances gather a
+// valid row and drop the result), so the shuffles see the full warp.
+// Same per-lane accumulation order as hyperpair_kernel. Needs the engine
+// tables (Γ/2π tables, self slots).
+struct HpAcc {
+  double px, py, dp;
+  double fx = 0, fy = 0, ja = 0, jb = 0, jc = 0;
+  __device__ __forceinline__ void add(double sx, double sy, double gs) {
+    const double rx = px - sx, ry = py - sy;
+    const double q = fma(rx, rx, fma(ry, ry, dp));
+    const double u = rcp64(q);
+    const double sv = gs * u;
+    fx = fma(-ry, sv, fx);
+    fy = fma(rx, sv, fy);
+    const double w = sv * u;
+    ja = fma(w * rx, ry, ja);
+    jb = fma(w, fma(ry, ry, -(rx * rx)), jb);
+    jc += w;
+  }
+};
+
+// SKIP: 0 none, 1 coincident position (clusters, δ = 0), 2 the target's own slot (near field)
+template <bool OFF32, int U, bool AFF, int SKIP>
+__device__ __forceinline__ long long hp_walk(HpAcc& acc, const int* __restrict__ list, long long k0, long long ke,
+                                             const double2* __restrict__ ps, const double* __restrict__ g1, const double2* __restrict__ g2, double mub,
+                                             int B, int self_loc, int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  // per-lane base address; a gather is one IMAD.WIDE.U32 off from it
+  const unsigned long long pbase = reinterpret_cast<unsigned long long>(ps);
+  long long used = 0;
+  int my = k0 + lane < ke ? list[k0 + lane] : 0;
+  for (long long kc = k0; kc < ke; kc += 32) {
+    const int nk = (int)min(32LL, ke - kc);
+    const int my_next = kc + 32 + lane < ke ? list[kc + 32 + lane] : 0;
+    auto entry = [&](int ci, double& sx, double& sy, double& gs) {
+      const double2 p =
+          OFF32 ? __ldg(reinterpret_cast<const double2*>(pbase + (unsigned long long)((unsigned)ci * (unsigned)B) * 16u))
+                : ps[(long long)ci * B];
+      sx = p.x;
+      sy = p.y;
+      if (AFF) {
+        const double2 v = g2[ci];
+        gs = fma(mub, v.y, v.x);
+      } else {
+        gs = g1[ci];
+      }
+    };
+    int u0 = 0;
+    for (; u0 + U <= nk; u0 += U) {  // full rounds: the U interactions interleave
+      int ci[U];
+      double sx[U], sy[U], gs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) ci[u] = __shfl_sync(FULL, my, u0 + u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) entry(ci[u], sx[u], sy[u], gs[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (SKIP == 1 && sx[u] == acc.px && sy[u] == acc.py) continue;
+        if (SKIP == 2 && ci[u] == self_loc) continue;
+        acc.add(sx[u], sy[u], gs[u]);
+        ++used;
+      }
+    }
+    for (; u0 < nk; ++u0) {
+      const int ci = __shfl_sync(FULL, my, u0);
+      double sx, sy, gs;
+      entry(ci, sx, sy, gs);
+      if (SKIP == 1 && sx == acc.px && sy == acc.py) continue;
+      if (SKIP == 2 && ci == self_loc) continue;
+      acc.add(sx, sy, gs);
+      ++used;
+    }
+    my = my_next;
+  }
+  return used;
+}
+
+// Pipelined walk: the warp stages the positions (one 16-byte (x, y) per lane)
+// and Γ entries of round r + D into a D-slot shared-memory ring with
+// cp.async while it computes round r, so D·U gathers per warp are in flight
+// without holding registers. U = 4 entries per round, D = 4 slots; the round
+// loop is unrolled by D so ring slots are compile-time, and a 32-entry list
+// chunk (one coalesced load, broadcast by shuffles) covers two unrolled
+// iterations.
+template <int U, int D>
+struct HpRing {
+  double2 pos[D][U][32];
+  double2 gam[D][U];
+  int idx[D][U];
+};
+
+template <bool OFF32, int U, int D, bool AFF, int SKIP>
+__device__ __forceinline__ int hp_walk_async(HpAcc& acc, const int* __restrict__ list, long long k0, long long ke,
+                                             const double2* __restrict__ ps, const double* __restrict__ g1,
+                                             const double2* __restrict__ g2, double mub, int B, int self_loc,
+                                             int lane, HpRing<U, D>& ring) {
+  constexpr unsigned FULL = 0xffffffffu;
+  static_assert(U * D == 16 && 32 % (U * D) == 0, "a list chunk spans 32 / (U·D) unrolled iterations");
+  const int n = (int)(ke - k0);
+  if (n <= 0) return 0;
+  const int rounds = (n + U - 1) / U;
+  list += k0;
+  const unsigned long long pbase = reinterpret_cast<unsigned long long>(ps);
+  int my = lane < n ? list[lane] : 0;          // chunk of the issue pointer
+  int my_next = 32 + lane < n ? list[32 + lane] : 0;
+  int chunk0 = 0;
+  auto issue = [&](int r, int slot) {
+    const int e0 = r * U;
+    if (e0 >= chunk0 + 32) {
+      chunk0 += 32;
+      my = my_next;
+      my_next = chunk0 + 32 + lane < n ? list[chunk0 + 32 + lane] : 0;
+    }
+    const int base = e0 - chunk0;
+    // entries past the list end carry id 0 (a valid row): their copies land
+    // but the partial-round code never reads them
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ci = __shfl_sync(FULL, my, base + u);
+      const unsigned long long src =
+          OFF32 ? pbase + (unsigned long long)((unsigned)ci * (unsigned)B) * 16u
+                : reinterpret_cast<unsigned long long>(ps + (long long)ci * B);
+      cp_async16_ca(&ring.pos[slot][u][lane], reinterpret_cast<const void*>(src), true);
+    }
+    const int cl = __shfl_sync(FULL, my, base + (lane & (U - 1)));
+    if (lane < U) {
+      if (AFF) cp_async16_ca(&ring.gam[slot][lane], g2 + cl, true);
+      else cp_async8_ca(&ring.gam[slot][lane], g1 + cl, true);
+      if (SKIP == 2) ring.idx[slot][lane] = cl;
+    }
+  };
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (j < rounds) issue(j, j);
+    cp_async_commit();
+  }
+  int used = 0;
+  for (int r = 0; r < rounds; r += D) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int rr = r + j;
+      if (rr < rounds) {
+        cp_async_wait_n<D - 1>();
+        __syncwarp();
+        const int e0 = rr * U;
+        if (e0 + U <= n) {
+          double2 p[U];
+          double gs[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            p[u] = ring.pos[j][u][lane];
+            const double2 g = ring.gam[j][u];
+            gs[u] = AFF ? fma(mub, g.y, g.x) : g.x;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (SKIP == 1 && p[u].x == acc.px && p[u].y == acc.py) continue;
+            if (SKIP == 2 && ring.idx[j][u] == self_loc) continue;
+            acc.add(p[u].x, p[u].y, gs[u]);
+            ++used;
+          }
+        } else {
+          for (int u = 0; u < U && e0 + u < n; ++u) {
+            const double2 pu = ring.pos[j][u][lane];
+            const double2 g = ring.gam[j][u];
+            if (SKIP == 1 && pu.x == acc.px && pu.y == acc.py) continue;
+            if (SKIP == 2 && ring.idx[j][u] == self_loc) continue;
+            acc.add(pu.x, pu.y, AFF ? fma(mub, g.y, g.x) : g.x);
+            ++used;
+          }
+        }
+        __syncwarp();
+        if (rr + D < rounds) issue(rr + D, j);
+      }
+      cp_async_commit();
+    }
+  }
+  return used;
+}
+
+template <bool OFF32, int U, bool AFF, int D>
+__global__ void __launch_bounds__(128) hyperpair_warp_kernel(DSurrogate s, HpGamma hg, const double* __restrict__ mu,
+                                                             int B, const double* __restrict__ xbar,
+                                                             const double2* __restrict__ cxy,
+                                                             const double2* __restrict__ dxy, double dp, double delta,
+                                                             const double* __restrict__ inflow, long long n,
+                                                             const unsigned char* __restrict__ active,
+                                                             double* __restrict__ f, double* __restrict__ jac,
+                                                             unsigned long long* __restrict__ pairs,
+                                                             DeviceStatus* st) {
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nt = s.n_t;
+  const long long tt = wid % nt, chunk = wid / nt;
+  const int b = (int)(chunk * 32 + lane);
+  unsigned long long cnt = 0;
+  const bool lane_ok = chunk * 32 < B && b < B && (!active || active[b]);
+  if (chunk * 32 < B && __any_sync(0xffffffffu, lane_ok)) {
+    const int bl = min(b, B - 1);
+    const long long t = s.t_order ? s.t_order[tt] : tt;
+    HpAcc acc;
+    acc.px = xbar[(long long)bl * 2 * nt + t];
+    acc.py = xbar[(long long)bl * 2 * nt + nt + t];
+    acc.dp = dp;
+    const double mub = AFF ? mu[bl] : 0.0;
+    long long used;
+    // rom.hpp:129: a centroid coincident with the target is dropped when
+    // delta == 0 (only then can it be singular); rom.hpp:136-140: the near
+    // field skips the target's own id
+    const long long c0 = s.cl_off[t], c1 = s.cl_off[t + 1], d0 = s.d_off[t], d1 = s.d_off[t + 1];
+    if constexpr (D > 0) {
+      __shared__ HpRing<U, (D > 0 ? D : 1)> rings[4];
+      auto& ring = rings[threadIdx.x >> 5];
+      if (delta == 0.0)
+        used = hp_walk_async<OFF32, U, D, AFF, 1>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane,
+                                                  ring);
+      else
+        used = hp_walk_async<OFF32, U, D, AFF, 0>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane,
+                                                  ring);
+      used += hp_walk_async<OFF32, U, D, AFF, 2>(acc, s.d_list, d0, d1, dxy + bl, hg.gd, hg.gdab, mub, B,
+                                                 hg.self_loc[t], lane, ring);
+    } else {
+      if (delta == 0.0)
+        used = hp_walk<OFF32, U, AFF, 1>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane);
+      else
+        used = hp_walk<OFF32, U, AFF, 0>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane);
+      used += hp_walk<OFF32, U, AFF, 2>(acc, s.d_list, d0, d1, dxy + bl, hg.gd, hg.gdab, mub, B, hg.self_loc[t],
+                                        lane);
+    }
+    if (lane_ok) {
+      const long long pid = s.target_ids[t];
+      cnt = (unsigned long long)used;
+      double fx = acc.fx, fy = acc.fy;
+      if (inflow) {
+        fx = fx + inflow[pid];
+        fy = fy + inflow[pid + n];
+      }
+      const double j00 = 2.0 * acc.ja, j01 = acc.jb - dp * acc.jc, j10 = acc.jb + dp * acc.jc;
+      if (!isfinite(fx) || !isfinite(fy) || !isfinite(j00) || !isfinite(j01) || !isfinite(j10))
+        latch_status(st, kStatusNonFiniteVelocity, pid);
+      f[(long long)b * 2 * nt + t] = fx;
+      f[(long long)b * 2 * nt + nt + t] = fy;
+      double* jj = jac + ((long long)b * nt + t) * 4;
+      jj[0] = j00;
+      jj[1] = j01;
+      jj[2] = j10;
+      jj[3] = -j00;
+    }
+  }
+  using WR = cub::WarpReduce<unsigned long long>;
+  __shared__ typename WR::TempStorage wt[4];
+  const unsigned long long sum = WR(wt[threadIdx.x / 32]).Sum(cnt);
+  if (lane == 0 && sum) atomicAdd(pairs, sum);
+}
+
 // ------------------------------------------------------ Gauss–Newton ---
 // Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
 // slice of the sampled rows, 32 rows per chunk. Each chunk's operands are
@@ -811,12 +1060,6 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
 // C = Φ̄_own − h·(J_a Φ̄_x + J_b Φ̄_y) = α Φ̄_x + β Φ̄_y; A·C goes to DMMA
 // (mma.sync m8n8k4 f64), 4 rows per k-step. Partials [slice][b][32·M + 32 +
 // M] are reduced in slice order by gn_finish_kernel (deterministic).
-__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int M>
 struct GnSmem {
@@ -1205,13 +1448,13 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
     if (t) {
       PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<true, MP>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      positions_clusters_mma_kernel<true, MP><<<grid, 512, smem, st>>>(s.n_c, et.ct, nullptr, tt, B, ic, d_xhat, d_mu, nullptr, w.cx,
-                                                                      w.cy, ctx->d_status);
+      positions_clusters_mma_kernel<true, MP><<<grid, 512, smem, st>>>(s.n_c, et.ct, nullptr, tt, B, ic, d_xhat, d_mu,
+                                                                      nullptr, w.cxy, ctx->d_status);
     } else {
       PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<false, MP>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s.n_c, et.ct, s.x0_tilde, tt, B, ic, d_xhat, d_mu, nullptr,
-                                                                       w.cx, w.cy, ctx->d_status);
+      positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s.n_c, et.ct, s.x0_tilde, tt, B, ic, d_xhat,
+                                                                       d_mu, nullptr, w.cxy, ctx->d_status);
     }
   }
   if (s.u > 0) {
@@ -1224,7 +1467,7 @@ void launch_positions_mma(ptrom_ctx* ctx, const DSurrogate& s, const AffineTable
     PTROM_CUDA(cudaFuncSetAttribute(positions_clusters_mma_kernel<false, MP>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     positions_clusters_mma_kernel<false, MP><<<grid, 512, smem, st>>>(s.u, et.dt, s.direct_x0, tt, B, ic, d_xhat,
-                                                                     nullptr, nullptr, w.dx, w.dy, ctx->d_status);
+                                                                     nullptr, nullptr, w.dxy, ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
 }
@@ -1251,20 +1494,13 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
     if (s.n_c > 0) {
       if (t)
         positions_clusters_kernel<true><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
-                                                                                   w.cx, w.cy, w.cg, ctx->d_status);
+                                                                                   w.cxy, ctx->d_status);
       else
         positions_clusters_kernel<false><<<blocks_for(s.n_c * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu,
-                                                                                    d_active, w.cx, w.cy, w.cg,
-                                                                                    ctx->d_status);
+                                                                                    d_active, w.cxy, ctx->d_status);
     }
-    if (s.u > 0) {
-      if (t)
-        positions_direct_kernel<true><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
-                                                                               w.dx, w.dy, w.dg);
-      else
-        positions_direct_kernel<false><<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, tt, B, xs, d_xhat, d_mu, d_active,
-                                                                                w.dx, w.dy, w.dg);
-    }
+    if (s.u > 0)
+      positions_direct_kernel<<<blocks_for(s.u * B, 256), 256, 0, st>>>(s, B, xs, d_xhat, d_active, w.dxy);
   }
   const double* xbar = d_xbar_in;
   if (g) {
@@ -1294,10 +1530,27 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
       hg.gdab = et->hgdab;
     }
     const bool off32 = (double)std::max(s.n_c, s.u) * (double)B < 4294967296.0;
+    // PTROM_HP_WARP=D selects the warp-uniform-list kernel (D-slot cp.async ring,
+    // 0 = register rounds); the per-lane kernel measures faster on config 4
+    static const char* hp_warp = getenv("PTROM_HP_WARP");
+    if (B >= IB && et && hp_warp) {
+      const bool aff = t != nullptr;
+      const int hp_d = atoi(hp_warp);
+      auto wk = off32 ? (aff ? hyperpair_warp_kernel<true, 4, true, 4> : hyperpair_warp_kernel<true, 4, false, 4>)
+                      : (aff ? hyperpair_warp_kernel<false, 4, true, 4> : hyperpair_warp_kernel<false, 4, false, 4>);
+      if (off32 && aff) {
+        if (hp_d == 0) wk = hyperpair_warp_kernel<true, 4, true, 0>;
+        if (hp_d == 2) wk = hyperpair_warp_kernel<true, 8, true, 2>;
+      }
+      wk<<<blocks_for(s.n_t * 32 * ((B + 31) / 32), 128), 128, 0, st>>>(
+          s, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy, effective_delta(delta, form), delta, d_inflow, n,
+          d_active, d_f, d_jac, w.pairs, ctx->d_status);
+    } else {
     auto hk = off32 ? hyperpair_kernel<IB, true> : hyperpair_kernel<IB, false>;
-    hk<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cx, w.cy, w.cg, w.dx, w.dy,
-                                                 w.dg, effective_delta(delta, form), delta, d_inflow, n, d_active, d_f,
+    hk<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy,
+                                                 effective_delta(delta, form), delta, d_inflow, n, d_active, d_f,
                                                  d_jac, w.pairs, ctx->d_status);
+    }
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
@@ -1311,28 +1564,20 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
 void RomScratch::ensure(const DSurrogate& s, long long nt, int B) {
   const size_t need_c = (size_t)std::max<long long>(1, s.n_c) * B, need_d = (size_t)std::max<long long>(1, s.u) * B;
   if (need_c > cap_c) {
-    cudaFree(cx);
-    cudaFree(cy);
-    cudaFree(cg);
-    PTROM_CUDA(cudaMalloc(&cx, need_c * 8));
-    PTROM_CUDA(cudaMalloc(&cy, need_c * 8));
-    PTROM_CUDA(cudaMalloc(&cg, need_c * 8));
+    cudaFree(cxy);
+    PTROM_CUDA(cudaMalloc(&cxy, need_c * 16));
     cap_c = need_c;
   }
   if (need_d > cap_d) {
-    cudaFree(dx);
-    cudaFree(dy);
-    cudaFree(dg);
-    PTROM_CUDA(cudaMalloc(&dx, need_d * 8));
-    PTROM_CUDA(cudaMalloc(&dy, need_d * 8));
-    PTROM_CUDA(cudaMalloc(&dg, need_d * 8));
+    cudaFree(dxy);
+    PTROM_CUDA(cudaMalloc(&dxy, need_d * 16));
     cap_d = need_d;
   }
   if (!pairs) PTROM_CUDA(cudaMalloc(&pairs, 16));
   (void)nt;
 }
 void RomScratch::release() {
-  void* ps[] = {cx, cy, cg, dx, dy, dg, pairs};
+  void* ps[] = {cxy, dxy, pairs};
   for (void* p : ps)
     if (p) cudaFree(p);
   *this = RomScratch{};

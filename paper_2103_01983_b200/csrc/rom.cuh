@@ -92,8 +92,8 @@ struct GnState {
 
 // Source positions per instance ([source][b]) and the pair counter.
 struct RomScratch {
-  double *cx = nullptr, *cy = nullptr, *cg = nullptr;
-  double *dx = nullptr, *dy = nullptr, *dg = nullptr;
+  // source positions, (x, y) interleaved: [cluster][instance], [direct][instance]
+  double2 *cxy = nullptr, *dxy = nullptr;
   unsigned long long* pairs = nullptr;
   size_t cap_c = 0, cap_d = 0;
   void ensure(const DSurrogate& s, long long nt, int B);

@@ -346,12 +346,15 @@ int ptrom_hyperpair_f64(ptrom_ctx* ctx, const ptrom_surrogate* sur, const double
       for (long long t = 0; t < nt; ++t)
         for (int k = 0; k < 4; ++k) jac[k * nt + t] = jh[4 * t + k];
       if (cluster_positions) {
-        PTROM_CUDA(cudaMemcpy(cluster_positions, w.cx, 8 * s.n_c, cudaMemcpyDeviceToHost));
-        PTROM_CUDA(cudaMemcpy(cluster_positions + s.n_c, w.cy, 8 * s.n_c, cudaMemcpyDeviceToHost));
+        // de-interleave (x, y) pairs into the reference's [x..., y...]
+        PTROM_CUDA(cudaMemcpy2D(cluster_positions, 8, w.cxy, 16, 8, s.n_c, cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy2D(cluster_positions + s.n_c, 8, reinterpret_cast<const double*>(w.cxy) + 1, 16, 8,
+                                s.n_c, cudaMemcpyDeviceToHost));
       }
       if (direct_positions) {
-        PTROM_CUDA(cudaMemcpy(direct_positions, w.dx, 8 * s.u, cudaMemcpyDeviceToHost));
-        PTROM_CUDA(cudaMemcpy(direct_positions + s.u, w.dy, 8 * s.u, cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy2D(direct_positions, 8, w.dxy, 16, 8, s.u, cudaMemcpyDeviceToHost));
+        PTROM_CUDA(cudaMemcpy2D(direct_positions + s.u, 8, reinterpret_cast<const double*>(w.dxy) + 1, 16, 8, s.u,
+                                cudaMemcpyDeviceToHost));
       }
     } catch (...) {
       w.release();
