@@ -149,17 +149,6 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool v
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-// L1-allocating variants (data reused by neighbouring warps)
-__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem, bool) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8_ca(void* smem, const void* gmem, bool) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void producers_sync(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr)); }
 
 constexpr int kBigGChunk = 2048;  // members per ΣΓ chunk
@@ -788,267 +777,6 @@ __global__ void __launch_bounds__(128) hyperpair_kernel(DSurrogate s, AffineTabl
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(pairs, sum);
 }
 
-// Batched form (B >= 32): a warp is one target x 32 consecutive instances,
-// so the target's cluster and near-field lists are warp-uniform. The warp
-// reads 32 list entries with one coalesced load (the next 32 prefetched while
-// the current ones are consumed) and broadcasts each with a shuffle; per
-// round of U entries the 2U position gathers (32 instances = 256 contiguous
-// bytes each) and the U Γ loads are all in flight before any arithmetic.
-// Every lane walks the lists (lanes past B or of inactive instances gather a
-// valid row and drop the result), so the shuffles see the full warp.
-// Same per-lane accumulation order as hyperpair_kernel. Needs the engine
-// tables (Γ/2π tables, self slots).
-struct HpAcc {
-  double px, py, dp;
-  double fx = 0, fy = 0, ja = 0, jb = 0, jc = 0;
-  __device__ __forceinline__ void add(double sx, double sy, double gs) {
-    const double rx = px - sx, ry = py - sy;
-    const double q = fma(rx, rx, fma(ry, ry, dp));
-    const double u = rcp64(q);
-    const double sv = gs * u;
-    fx = fma(-ry, sv, fx);
-    fy = fma(rx, sv, fy);
-    const double w = sv * u;
-    ja = fma(w * rx, ry, ja);
-    jb = fma(w, fma(ry, ry, -(rx * rx)), jb);
-    jc += w;
-  }
-};
-
-// SKIP: 0 none, 1 coincident position (clusters, δ = 0), 2 the target's own slot (near field)
-template <bool OFF32, int U, bool AFF, int SKIP>
-__device__ __forceinline__ long long hp_walk(HpAcc& acc, const int* __restrict__ list, long long k0, long long ke,
-                                             const double2* __restrict__ ps, const double* __restrict__ g1, const double2* __restrict__ g2, double mub,
-                                             int B, int self_loc, int lane) {
-  constexpr unsigned FULL = 0xffffffffu;
-  // per-lane base address; a gather is one IMAD.WIDE.U32 off from it
-  const unsigned long long pbase = reinterpret_cast<unsigned long long>(ps);
-  long long used = 0;
-  int my = k0 + lane < ke ? list[k0 + lane] : 0;
-  for (long long kc = k0; kc < ke; kc += 32) {
-    const int nk = (int)min(32LL, ke - kc);
-    const int my_next = kc + 32 + lane < ke ? list[kc + 32 + lane] : 0;
-    auto entry = [&](int ci, double& sx, double& sy, double& gs) {
-      const double2 p =
-          OFF32 ? __ldg(reinterpret_cast<const double2*>(pbase + (unsigned long long)((unsigned)ci * (unsigned)B) * 16u))
-                : ps[(long long)ci * B];
-      sx = p.x;
-      sy = p.y;
-      if (AFF) {
-        const double2 v = g2[ci];
-        gs = fma(mub, v.y, v.x);
-      } else {
-        gs = g1[ci];
-      }
-    };
-    int u0 = 0;
-    for (; u0 + U <= nk; u0 += U) {  // full rounds: the U interactions interleave
-      int ci[U];
-      double sx[U], sy[U], gs[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) ci[u] = __shfl_sync(FULL, my, u0 + u);
-#pragma unroll
-      for (int u = 0; u < U; ++u) entry(ci[u], sx[u], sy[u], gs[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (SKIP == 1 && sx[u] == acc.px && sy[u] == acc.py) continue;
-        if (SKIP == 2 && ci[u] == self_loc) continue;
-        acc.add(sx[u], sy[u], gs[u]);
-        ++used;
-      }
-    }
-    for (; u0 < nk; ++u0) {
-      const int ci = __shfl_sync(FULL, my, u0);
-      double sx, sy, gs;
-      entry(ci, sx, sy, gs);
-      if (SKIP == 1 && sx == acc.px && sy == acc.py) continue;
-      if (SKIP == 2 && ci == self_loc) continue;
-      acc.add(sx, sy, gs);
-      ++used;
-    }
-    my = my_next;
-  }
-  return used;
-}
-
-// Pipelined walk: the warp stages the positions (one 16-byte (x, y) per lane)
-// and Γ entries of round r + D into a D-slot shared-memory ring with
-// cp.async while it computes round r, so D·U gathers per warp are in flight
-// without holding registers. U = 4 entries per round, D = 4 slots; the round
-// loop is unrolled by D so ring slots are compile-time, and a 32-entry list
-// chunk (one coalesced load, broadcast by shuffles) covers two unrolled
-// iterations.
-template <int U, int D>
-struct HpRing {
-  double2 pos[D][U][32];
-  double2 gam[D][U];
-  int idx[D][U];
-};
-
-template <bool OFF32, int U, int D, bool AFF, int SKIP>
-__device__ __forceinline__ int hp_walk_async(HpAcc& acc, const int* __restrict__ list, long long k0, long long ke,
-                                             const double2* __restrict__ ps, const double* __restrict__ g1,
-                                             const double2* __restrict__ g2, double mub, int B, int self_loc,
-                                             int lane, HpRing<U, D>& ring) {
-  constexpr unsigned FULL = 0xffffffffu;
-  static_assert(U * D == 16 && 32 % (U * D) == 0, "a list chunk spans 32 / (U·D) unrolled iterations");
-  const int n = (int)(ke - k0);
-  if (n <= 0) return 0;
-  const int rounds = (n + U - 1) / U;
-  list += k0;
-  const unsigned long long pbase = reinterpret_cast<unsigned long long>(ps);
-  int my = lane < n ? list[lane] : 0;          // chunk of the issue pointer
-  int my_next = 32 + lane < n ? list[32 + lane] : 0;
-  int chunk0 = 0;
-  auto issue = [&](int r, int slot) {
-    const int e0 = r * U;
-    if (e0 >= chunk0 + 32) {
-      chunk0 += 32;
-      my = my_next;
-      my_next = chunk0 + 32 + lane < n ? list[chunk0 + 32 + lane] : 0;
-    }
-    const int base = e0 - chunk0;
-    // entries past the list end carry id 0 (a valid row): their copies land
-    // but the partial-round code never reads them
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ci = __shfl_sync(FULL, my, base + u);
-      const unsigned long long src =
-          OFF32 ? pbase + (unsigned long long)((unsigned)ci * (unsigned)B) * 16u
-                : reinterpret_cast<unsigned long long>(ps + (long long)ci * B);
-      cp_async16_ca(&ring.pos[slot][u][lane], reinterpret_cast<const void*>(src), true);
-    }
-    const int cl = __shfl_sync(FULL, my, base + (lane & (U - 1)));
-    if (lane < U) {
-      if (AFF) cp_async16_ca(&ring.gam[slot][lane], g2 + cl, true);
-      else cp_async8_ca(&ring.gam[slot][lane], g1 + cl, true);
-      if (SKIP == 2) ring.idx[slot][lane] = cl;
-    }
-  };
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    if (j < rounds) issue(j, j);
-    cp_async_commit();
-  }
-  int used = 0;
-  for (int r = 0; r < rounds; r += D) {
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const int rr = r + j;
-      if (rr < rounds) {
-        cp_async_wait_n<D - 1>();
-        __syncwarp();
-        const int e0 = rr * U;
-        if (e0 + U <= n) {
-          double2 p[U];
-          double gs[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            p[u] = ring.pos[j][u][lane];
-            const double2 g = ring.gam[j][u];
-            gs[u] = AFF ? fma(mub, g.y, g.x) : g.x;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (SKIP == 1 && p[u].x == acc.px && p[u].y == acc.py) continue;
-            if (SKIP == 2 && ring.idx[j][u] == self_loc) continue;
-            acc.add(p[u].x, p[u].y, gs[u]);
-            ++used;
-          }
-        } else {
-          for (int u = 0; u < U && e0 + u < n; ++u) {
-            const double2 pu = ring.pos[j][u][lane];
-            const double2 g = ring.gam[j][u];
-            if (SKIP == 1 && pu.x == acc.px && pu.y == acc.py) continue;
-            if (SKIP == 2 && ring.idx[j][u] == self_loc) continue;
-            acc.add(pu.x, pu.y, AFF ? fma(mub, g.y, g.x) : g.x);
-            ++used;
-          }
-        }
-        __syncwarp();
-        if (rr + D < rounds) issue(rr + D, j);
-      }
-      cp_async_commit();
-    }
-  }
-  return used;
-}
-
-template <bool OFF32, int U, bool AFF, int D>
-__global__ void __launch_bounds__(128) hyperpair_warp_kernel(DSurrogate s, HpGamma hg, const double* __restrict__ mu,
-                                                             int B, const double* __restrict__ xbar,
-                                                             const double2* __restrict__ cxy,
-                                                             const double2* __restrict__ dxy, double dp, double delta,
-                                                             const double* __restrict__ inflow, long long n,
-                                                             const unsigned char* __restrict__ active,
-                                                             double* __restrict__ f, double* __restrict__ jac,
-                                                             unsigned long long* __restrict__ pairs,
-                                                             DeviceStatus* st) {
-  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long nt = s.n_t;
-  const long long tt = wid % nt, chunk = wid / nt;
-  const int b = (int)(chunk * 32 + lane);
-  unsigned long long cnt = 0;
-  const bool lane_ok = chunk * 32 < B && b < B && (!active || active[b]);
-  if (chunk * 32 < B && __any_sync(0xffffffffu, lane_ok)) {
-    const int bl = min(b, B - 1);
-    const long long t = s.t_order ? s.t_order[tt] : tt;
-    HpAcc acc;
-    acc.px = xbar[(long long)bl * 2 * nt + t];
-    acc.py = xbar[(long long)bl * 2 * nt + nt + t];
-    acc.dp = dp;
-    const double mub = AFF ? mu[bl] : 0.0;
-    long long used;
-    // rom.hpp:129: a centroid coincident with the target is dropped when
-    // delta == 0 (only then can it be singular); rom.hpp:136-140: the near
-    // field skips the target's own id
-    const long long c0 = s.cl_off[t], c1 = s.cl_off[t + 1], d0 = s.d_off[t], d1 = s.d_off[t + 1];
-    if constexpr (D > 0) {
-      __shared__ HpRing<U, (D > 0 ? D : 1)> rings[4];
-      auto& ring = rings[threadIdx.x >> 5];
-      if (delta == 0.0)
-        used = hp_walk_async<OFF32, U, D, AFF, 1>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane,
-                                                  ring);
-      else
-        used = hp_walk_async<OFF32, U, D, AFF, 0>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane,
-                                                  ring);
-      used += hp_walk_async<OFF32, U, D, AFF, 2>(acc, s.d_list, d0, d1, dxy + bl, hg.gd, hg.gdab, mub, B,
-                                                 hg.self_loc[t], lane, ring);
-    } else {
-      if (delta == 0.0)
-        used = hp_walk<OFF32, U, AFF, 1>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane);
-      else
-        used = hp_walk<OFF32, U, AFF, 0>(acc, s.cl_list, c0, c1, cxy + bl, hg.gc, hg.gab, mub, B, -1, lane);
-      used += hp_walk<OFF32, U, AFF, 2>(acc, s.d_list, d0, d1, dxy + bl, hg.gd, hg.gdab, mub, B, hg.self_loc[t],
-                                        lane);
-    }
-    if (lane_ok) {
-      const long long pid = s.target_ids[t];
-      cnt = (unsigned long long)used;
-      double fx = acc.fx, fy = acc.fy;
-      if (inflow) {
-        fx = fx + inflow[pid];
-        fy = fy + inflow[pid + n];
-      }
-      const double j00 = 2.0 * acc.ja, j01 = acc.jb - dp * acc.jc, j10 = acc.jb + dp * acc.jc;
-      if (!isfinite(fx) || !isfinite(fy) || !isfinite(j00) || !isfinite(j01) || !isfinite(j10))
-        latch_status(st, kStatusNonFiniteVelocity, pid);
-      f[(long long)b * 2 * nt + t] = fx;
-      f[(long long)b * 2 * nt + nt + t] = fy;
-      double* jj = jac + ((long long)b * nt + t) * 4;
-      jj[0] = j00;
-      jj[1] = j01;
-      jj[2] = j10;
-      jj[3] = -j00;
-    }
-  }
-  using WR = cub::WarpReduce<unsigned long long>;
-  __shared__ typename WR::TempStorage wt[4];
-  const unsigned long long sum = WR(wt[threadIdx.x / 32]).Sum(cnt);
-  if (lane == 0 && sum) atomicAdd(pairs, sum);
-}
-
 // ------------------------------------------------------ Gauss–Newton ---
 // Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
 // slice of the sampled rows, 32 rows per chunk. Each chunk's operands are
@@ -1530,27 +1258,10 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
       hg.gdab = et->hgdab;
     }
     const bool off32 = (double)std::max(s.n_c, s.u) * (double)B < 4294967296.0;
-    // PTROM_HP_WARP=D selects the warp-uniform-list kernel (D-slot cp.async ring,
-    // 0 = register rounds); the per-lane kernel measures faster on config 4
-    static const char* hp_warp = getenv("PTROM_HP_WARP");
-    if (B >= IB && et && hp_warp) {
-      const bool aff = t != nullptr;
-      const int hp_d = atoi(hp_warp);
-      auto wk = off32 ? (aff ? hyperpair_warp_kernel<true, 4, true, 4> : hyperpair_warp_kernel<true, 4, false, 4>)
-                      : (aff ? hyperpair_warp_kernel<false, 4, true, 4> : hyperpair_warp_kernel<false, 4, false, 4>);
-      if (off32 && aff) {
-        if (hp_d == 0) wk = hyperpair_warp_kernel<true, 4, true, 0>;
-        if (hp_d == 2) wk = hyperpair_warp_kernel<true, 8, true, 2>;
-      }
-      wk<<<blocks_for(s.n_t * 32 * ((B + 31) / 32), 128), 128, 0, st>>>(
-          s, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy, effective_delta(delta, form), delta, d_inflow, n,
-          d_active, d_f, d_jac, w.pairs, ctx->d_status);
-    } else {
     auto hk = off32 ? hyperpair_kernel<IB, true> : hyperpair_kernel<IB, false>;
     hk<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy,
                                                  effective_delta(delta, form), delta, d_inflow, n, d_active, d_f,
                                                  d_jac, w.pairs, ctx->d_status);
-    }
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
