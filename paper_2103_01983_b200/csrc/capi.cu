@@ -61,20 +61,12 @@ int guarded(ptrom_ctx* ctx, F&& fn) {
   }
 }
 
-// kernel.hpp:84-93 ParticleSystem::validate + kernel.hpp:96-103 check_state.
-template <class S>
-void validate_system(long long n, const S* x, const S* gamma, S delta, int form, const S* inflow, const char* who) {
+// kernel.hpp:84-93 ParticleSystem::validate: the host-side part (size and
+// form). The finiteness and δ checks run on the uploaded copies
+// (validate_uploaded, validate.cu) in the reference's order.
+void validate_shape(long long n, int form) {
   if (n <= 0) config_fail("particle system is empty");
   if (form != PTROM_FORM_STANDARD && form != PTROM_FORM_DENOMINATOR_SCALED) config_fail("unknown kernel form");
-  for (long long i = 0; i < n; ++i)
-    if (!std::isfinite(gamma[i])) config_fail("non-finite circulation");
-  if (!(delta >= S(0))) config_fail("negative desingularization constant");
-  if (inflow)
-    for (long long i = 0; i < 2 * n; ++i)
-      if (!std::isfinite(inflow[i])) config_fail("non-finite inflow");
-  if (x)
-    for (long long i = 0; i < 2 * n; ++i)
-      if (!std::isfinite(x[i])) config_fail(std::string(who) + ": non-finite state");
 }
 
 void check_rows(long long n, long long b, long long e) {
@@ -191,12 +183,13 @@ int ptrom_profile_end(ptrom_ctx* ctx, double* total_ms, int64_t* launches) {
 int ptrom_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
                                 int form, const double* inflow, double* f, uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    validate_system<double>(n, x, gamma, delta, form, inflow, "pairwise_velocity");
+    validate_shape(n, form);
     ctx->io.reset();
     ctx->io.reserve(sizeof(double) * (size_t)(2 * n + n + (inflow ? 2 * n : 0) + 2 * n) + 4096);
     double* dx = stage_in(ctx, x, 2 * n);
     double* dg = stage_in(ctx, gamma, n);
     double* di = stage_in(ctx, inflow, inflow ? 2 * n : 0);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, di, "pairwise_velocity");
     double* df = ctx->io.take<double>(2 * n);
     dev_velocity_f64(ctx, n, dx, dg, delta, form, di, 0, n, df, n);
     PTROM_CUDA(cudaMemcpyAsync(f, df, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -208,12 +201,13 @@ int ptrom_pairwise_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, cons
 int ptrom_pairwise_velocity_f32(ptrom_ctx* ctx, int64_t n, const float* x, const float* gamma, float delta, int form,
                                 const float* inflow, float* f, uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    validate_system<float>(n, x, gamma, delta, form, inflow, "pairwise_velocity");
+    validate_shape(n, form);
     ctx->io.reset();
     ctx->io.reserve(sizeof(float) * (size_t)(2 * n + n + (inflow ? 2 * n : 0) + 2 * n) + 4096);
     float* dx = stage_in(ctx, x, 2 * n);
     float* dg = stage_in(ctx, gamma, n);
     float* di = stage_in(ctx, inflow, inflow ? 2 * n : 0);
+    validate_uploaded<float>(ctx, n, dx, dg, delta, di, "pairwise_velocity");
     float* df = ctx->io.take<float>(2 * n);
     dev_velocity_f32(ctx, n, dx, dg, delta, form, di, 0, n, df, n);
     PTROM_CUDA(cudaMemcpyAsync(f, df, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -226,11 +220,12 @@ int ptrom_inexact_kernel_jacobian_f64(ptrom_ctx* ctx, int64_t n, const double* x
                                       int form, double* jxx, double* jxy, double* jyx, double* jyy,
                                       uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    validate_system<double>(n, x, gamma, delta, form, nullptr, "inexact_kernel_jacobian");
+    validate_shape(n, form);
     ctx->io.reset();
     ctx->io.reserve(sizeof(double) * (size_t)(3 * n + 4 * n) + 4096);
     double* dx = stage_in(ctx, x, 2 * n);
     double* dg = stage_in(ctx, gamma, n);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, (const double*)nullptr, "inexact_kernel_jacobian");
     double* dj = ctx->io.take<double>(4 * n);
     dev_jacobian_f64(ctx, n, dx, dg, delta, form, 0, n, dj, dj + n, dj + 2 * n, dj + 3 * n, 0.0, nullptr);
     double* outs[4] = {jxx, jxy, jyx, jyy};
@@ -253,12 +248,13 @@ int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const do
     if (!(tol > 0)) config_fail("Newton tolerance must be positive");
     if (max_iters < 1) config_fail("Newton max_iters must be >= 1");
     if (jacobian_refresh_period < 1) config_fail("Jacobian refresh period must be >= 1");
-    validate_system<double>(n, x0, gamma, delta, form, inflow, "pairwise_velocity");
+    validate_shape(n, form);
     ctx->io.reset();
     ctx->io.reserve(sizeof(double) * (size_t)(2 * n + n + (inflow ? 2 * n : 0)) + 4096);
     double* dx = stage_in(ctx, x0, 2 * n);
     double* dg = stage_in(ctx, gamma, n);
     double* di = stage_in(ctx, inflow, inflow ? 2 * n : 0);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, di, "pairwise_velocity");
     FomResult r = fom_simulate_device(ctx, n, dx, dg, delta, form, di, dt, n_steps, tol, max_iters,
                                       jacobian_refresh_period, snapshots, iterations, converged, relative_residual);
     if (n_pair_evals) *n_pair_evals = (uint64_t)r.velocity_evals * (uint64_t)n * (uint64_t)(n - 1);
@@ -268,11 +264,12 @@ int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const do
 // kernel.hpp:174-191
 int ptrom_hamiltonian_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double* out) {
   return guarded(ctx, [&] {
-    validate_system<double>(n, x, gamma, 0.0, PTROM_FORM_STANDARD, nullptr, "hamiltonian");
+    validate_shape(n, PTROM_FORM_STANDARD);
     ctx->io.reset();
     ctx->io.reserve(sizeof(double) * (size_t)(3 * n + 1) + 4096);
     double* dx = stage_in(ctx, x, 2 * n);
     double* dg = stage_in(ctx, gamma, n);
+    validate_uploaded<double>(ctx, n, dx, dg, 0.0, (const double*)nullptr, "hamiltonian");
     double* dh = ctx->io.take<double>(1);
     dev_hamiltonian_f64(ctx, n, dx, dg, dh);
     PTROM_CUDA(cudaMemcpyAsync(out, dh, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -298,12 +295,14 @@ int ptrom_velocity_field_grid_f64(ptrom_ctx* ctx, int64_t n, const double* x, co
                                   int64_t ny, double c_g, double l, double gamma_bar, double* grid,
                                   uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    validate_system<double>(n, x, gamma, delta, form, nullptr, "velocity_field_grid");
-    const double scale = lattice_scale(nx, ny, x_min, x_max, y_min, y_max, c_g, l, gamma_bar);
+    validate_shape(n, form);
     ctx->io.reset();
-    ctx->io.reserve(sizeof(double) * (size_t)(3 * n + nx * ny) + 4096);
+    const size_t cells = nx >= 2 && ny >= 2 ? (size_t)(nx * ny) : 0;  // lattice_scale validates below
+    ctx->io.reserve(sizeof(double) * ((size_t)(3 * n) + cells) + 4096);
     double* dx = stage_in(ctx, x, 2 * n);
     double* dg = stage_in(ctx, gamma, n);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, (const double*)nullptr, "velocity_field_grid");
+    const double scale = lattice_scale(nx, ny, x_min, x_max, y_min, y_max, c_g, l, gamma_bar);
     double* dgrid = ctx->io.take<double>((size_t)(nx * ny));
     dev_velocity_field_grid_f64(ctx, n, dx, dg, delta, form, x_min, x_max, nx, y_min, y_max, ny, scale, dgrid);
     PTROM_CUDA(cudaMemcpyAsync(grid, dgrid, sizeof(double) * nx * ny, cudaMemcpyDeviceToHost, ctx->stream));

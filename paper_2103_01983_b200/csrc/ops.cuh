@@ -7,6 +7,10 @@
 namespace ptrom {
 
 double effective_delta(double delta, int form);
+// kernel.hpp:84-103 finiteness / δ checks on the device copies of host-API
+// inputs (null arrays skipped); raises the reference's config errors in order.
+template <class S>
+void validate_uploaded(ptrom_ctx* ctx, long long n, const S* dx, const S* dg, S delta, const S* di, const char* who);
 void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
                       const double* inflow, long long t_begin, long long t_end, double* f, long long ld);
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,

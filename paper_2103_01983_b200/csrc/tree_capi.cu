@@ -56,18 +56,11 @@ void check_criterion(int kind, double value) {
 }
 
 // kernel.hpp:84-103 (sys.validate + check_state) for the tree evaluators.
-void validate_eval(long long n, const double* x, const double* gamma, double delta, int form, const double* inflow,
-                   const char* who) {
+// kernel.hpp:84-93 validate, host part (size, form); the finiteness and δ
+// checks run on the uploaded copies (validate_uploaded, validate.cu).
+void validate_eval_shape(long long n, int form) {
   if (n <= 0) config_fail("particle system is empty");
   if (form != PTROM_FORM_STANDARD && form != PTROM_FORM_DENOMINATOR_SCALED) config_fail("unknown kernel form");
-  for (long long i = 0; i < n; ++i)
-    if (!std::isfinite(gamma[i])) config_fail("non-finite circulation");
-  if (!(delta >= 0)) config_fail("negative desingularization constant");
-  if (inflow)
-    for (long long i = 0; i < 2 * n; ++i)
-      if (!std::isfinite(inflow[i])) config_fail("non-finite inflow");
-  for (long long i = 0; i < 2 * n; ++i)
-    if (!std::isfinite(x[i])) config_fail(std::string(who) + ": non-finite state");
 }
 
 struct DevBuf {
@@ -214,13 +207,14 @@ int ptrom_bh_velocity_f64(ptrom_ctx* ctx, ptrom_tree* tree, int64_t n, const dou
                           double delta, int form, int crit_kind, double crit_value, const double* inflow, double* f,
                           uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    validate_eval(n, x, gamma, delta, form, inflow, "bh_velocity");
-    if (!tree || tree->t.n != n) config_fail("bh_velocity: tree size mismatch");
-    check_criterion(crit_kind, crit_value);
+    validate_eval_shape(n, form);
     DevBuf b{ctx->stream};
     const double* dx = b.up(x, 2 * n);
     const double* dg = b.up(gamma, n);
     const double* di = b.up(inflow, inflow ? 2 * n : 0);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, di, "bh_velocity");
+    if (!tree || tree->t.n != n) config_fail("bh_velocity: tree size mismatch");
+    check_criterion(crit_kind, crit_value);
     double* df = b.alloc<double>(2 * n);
     const unsigned long long pairs =
         tree_eval(ctx, tree->t, dx, dg, delta, form, crit_kind, crit_value, di, df, nullptr, nullptr, nullptr, nullptr);
@@ -234,12 +228,13 @@ int ptrom_bh_jacobian_f64(ptrom_ctx* ctx, ptrom_tree* tree, int64_t n, const dou
                           double delta, int form, int crit_kind, double crit_value, double* dfx_dx, double* dfx_dy,
                           double* dfy_dx, double* dfy_dy) {
   return guarded(ctx, [&] {
-    validate_eval(n, x, gamma, delta, form, nullptr, "bh_jacobian");
-    if (!tree || tree->t.n != n) config_fail("bh_jacobian: tree size mismatch");
-    check_criterion(crit_kind, crit_value);
+    validate_eval_shape(n, form);
     DevBuf b{ctx->stream};
     const double* dx = b.up(x, 2 * n);
     const double* dg = b.up(gamma, n);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, (const double*)nullptr, "bh_jacobian");
+    if (!tree || tree->t.n != n) config_fail("bh_jacobian: tree size mismatch");
+    check_criterion(crit_kind, crit_value);
     double* dj = b.alloc<double>(4 * n);
     tree_eval(ctx, tree->t, dx, dg, delta, form, crit_kind, crit_value, nullptr, nullptr, dj, dj + n, dj + 2 * n,
               dj + 3 * n);
@@ -274,13 +269,14 @@ int ptrom_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, co
                                   int form, int crit_kind, double crit_value, int64_t leaf_capacity,
                                   const double* inflow, double* f, uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    validate_eval(n, x, gamma, delta, form, inflow, "bh_velocity");
-    check_criterion(crit_kind, crit_value);
-    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+    validate_eval_shape(n, form);
     DevBuf b{ctx->stream};
     const double* dx = b.up(x, 2 * n);
     const double* dg = b.up(gamma, n);
     const double* di = b.up(inflow, inflow ? 2 * n : 0);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, di, "bh_velocity");
+    check_criterion(crit_kind, crit_value);
+    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
     double* df = b.alloc<double>(2 * n);
     Tree t;
     try {
