@@ -188,3 +188,34 @@ def test_empty_system_is_a_config_error(pt):
 def test_single_particle_has_only_inflow(pt):
     f = pt.pairwise_velocity(np.array([0.5, -0.25]), pt.ParticleSystem(np.array([3.0]), 0.0, np.array([0.1, -0.2])))
     assert f.tolist() == [0.1, -0.2]
+
+
+def test_device_validation_order_and_messages(pt):
+    """kernel.hpp:84-103 order on the uploaded copies: circulation, δ, inflow, state."""
+    import ctypes as C
+    ctx = pt.default_context()
+    lib = ctx.lib
+    n = 300
+    rng = np.random.default_rng(9)
+    x, g, inf_ = rng.uniform(-1, 1, 2 * n), np.ones(n), np.zeros(2 * n)
+    f = np.empty(2 * n)
+
+    def call(x, g, delta, inflow):
+        p = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None
+        rc = lib.ptrom_pairwise_velocity_f64(ctx.handle, n, p(x), p(g), delta, 0, p(inflow), p(f), None)
+        return rc, lib.ptrom_last_error(ctx.handle).decode()
+
+    bad_g, bad_x, bad_i = g.copy(), x.copy(), inf_.copy()
+    bad_g[n - 1] = np.nan
+    bad_x[2 * n - 1] = np.inf
+    bad_i[7] = -np.inf
+    rc, msg = call(x, bad_g, -1.0, bad_i)
+    assert rc != 0 and "non-finite circulation" in msg
+    rc, msg = call(bad_x, g, -1.0, bad_i)
+    assert rc != 0 and "negative desingularization" in msg
+    rc, msg = call(bad_x, g, 0.1, bad_i)
+    assert rc != 0 and "non-finite inflow" in msg
+    rc, msg = call(bad_x, g, 0.1, inf_)
+    assert rc != 0 and "pairwise_velocity: non-finite state" in msg
+    rc, msg = call(x, g, 0.1, inf_)
+    assert rc == 0, msg
