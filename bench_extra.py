@@ -60,8 +60,8 @@ def run(args, rank, world):
     import torch
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     if world > 1:
-        # Barnes-Hut and PTROM shard by targets / μ instances with no data-path
-        # exchange; this secondary bench runs replicas per rank.
+        # Barnes-Hut shards the far field by target (one all-gather per
+        # evaluation); PTROM splits μ instances (no data-path exchange).
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     if args.workload == "config3":
@@ -73,8 +73,10 @@ def run(args, rank, world):
         t = torch.tensor([line["ms_per_step"]], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         line["ms_per_step"] = float(t.item())
-        line["value"] = line["units_per_step"] * world * 1e3 / line["ms_per_step"]
-        line["scaling"] = "weak"
+        # config 3: one N-body evaluation split across ranks (strong scaling);
+        # config 4: every rank marches its own μ block (weak scaling)
+        strong = line.get("scaling") == "strong"
+        line["value"] = line["units_per_step"] * (1 if strong else world) * 1e3 / line["ms_per_step"]
         dist.destroy_process_group()
     line.pop("units_per_step", None)
     if rank == 0:
@@ -100,9 +102,18 @@ def bench_config3(args, world):
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     cnt = ctypes.c_uint64()
 
-    def step():
-        ctx.check(lib.ptrom_dev_barnes_hut_velocity_f64(ctx.handle, n, x.data_ptr(), g.data_ptr(), w.delta, 0, 0,
-                                                        theta, leaf, None, f.data_ptr(), ctypes.byref(cnt)))
+    if world == 1:
+        def step():
+            ctx.check(lib.ptrom_dev_barnes_hut_velocity_f64(ctx.handle, n, x.data_ptr(), g.data_ptr(), w.delta, 0,
+                                                            0, theta, leaf, None, f.data_ptr(), ctypes.byref(cnt)))
+    else:
+        # replicated build, far field split by tree slot, shards
+        # all-gathered over NCCL and scattered back to particle order
+        from paper_2103_01983_b200.sharded import CudaBhBackend, ShardedBarnesHut
+        sharded = ShardedBarnesHut(n, CudaBhBackend(torch.cuda.current_device()))
+
+        def step():
+            f.copy_(sharded.velocity(x, g, w.delta, 0, theta, leaf))
 
     for _ in range(args.warmup):
         step()
@@ -148,32 +159,48 @@ def bench_config3(args, world):
                   "achieved_gbs": build_bytes / (build_ms * 1e-3) / 1e9, "peak_gbs": hbm,
                   "frac": (build_bytes / (build_ms * 1e-3) / 1e9) / hbm if hbm else None, "nodes": nodes}
 
-    # e2e: host buffers through the drop-in ptrom_barnes_hut_velocity_f64
-    hx = torch.tensor(w.x0).pin_memory().numpy()
+    # e2e: host buffers through the drop-in ptrom_barnes_hut_velocity_f64 (one
+    # GPU), or pinned host state -> every rank, sharded evaluation, result ->
+    # host (N GPUs)
+    hx_t = torch.tensor(w.x0).pin_memory()
+    hx = hx_t.numpy()
     hg = torch.tensor(w.gamma).pin_memory().numpy()
-    hf = torch.empty(2 * n, dtype=torch.float64).pin_memory().numpy()
-    fn = lambda: ctx.check(lib.ptrom_barnes_hut_velocity_f64(ctx.handle, n, hx.ctypes.data, hg.ctypes.data, w.delta,
-                                                             0, 0, theta, leaf, None, hf.ctypes.data,
-                                                             ctypes.byref(cnt)))
+    hf_t = torch.empty(2 * n, dtype=torch.float64).pin_memory()
+    hf = hf_t.numpy()
+    if world == 1:
+        fn = lambda: ctx.check(lib.ptrom_barnes_hut_velocity_f64(ctx.handle, n, hx.ctypes.data, hg.ctypes.data,
+                                                                 w.delta, 0, 0, theta, leaf, None, hf.ctypes.data,
+                                                                 ctypes.byref(cnt)))
+        api = "ptrom_barnes_hut_velocity_f64 (host buffers)"
+    else:
+        def fn():
+            x.copy_(hx_t, non_blocking=True)
+            step()
+            hf_t.copy_(f, non_blocking=True)
+            torch.cuda.synchronize()
+        api = "ShardedBarnesHut.velocity (pinned state in, velocities out on every rank)"
     fn()
     ke = max(3, min(K, 10))
     t0 = time.perf_counter()
     for _ in range(ke):
         fn()
     e2e_s = time.perf_counter() - t0
-    e2e = {"value": n * ke / e2e_s, "unit": "bodies/s", "h2d_bytes_per_step": int(hx.nbytes + hg.nbytes),
-           "d2h_bytes_per_step": int(hf.nbytes), "api": "ptrom_barnes_hut_velocity_f64 (host buffers)"}
+    e2e = {"value": n * ke / e2e_s, "unit": "bodies/s",
+           "h2d_bytes_per_step": int(hx.nbytes + (hg.nbytes if world == 1 else 0)),
+           "d2h_bytes_per_step": int(hf.nbytes), "api": api}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_config3(w, theta, leaf, args.cpu_seconds)
     return {
         "metric": "Barnes-Hut velocity evaluation bodies/s (fp64; build + aggregation + far field)",
         "value": value, "unit": "bodies/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": total_ms / K, "units_per_step": n, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": total_ms / K, "units_per_step": n, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
         "config": {"workload": w.name, "n": n, "leaf_capacity": leaf, "theta": theta, "delta": w.delta,
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
-                   "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
+                   "parallelism": "single GPU" if world == 1 else
+                   f"replicated build, far field split by tree slot x{world} (NCCL all-gather)"},
         "gpu_launches": ours * K if ours is not None else None,
         "e2e": e2e, "roofline": roofline, "build_roofline": build_roof, "cpu_baseline": cpu,
         "clocks": clocks.summary(),

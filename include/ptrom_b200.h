@@ -196,6 +196,18 @@ int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d
                                       double delta, int form, int crit_kind, double crit_value,
                                       int64_t leaf_capacity, const double* d_inflow, double* d_f,
                                       uint64_t* n_pair_evals);
+/* Target-sharded form (replicated build, far field split by
+ * target): builds the same tree as ptrom_dev_barnes_hut_velocity_f64 and
+ * evaluates only the targets in tree slots [k_begin, k_end) (slot k holds
+ * particle perm[k]; slots are spatially contiguous). Velocities go to
+ * d_f_slots in slot order, x then y (2·(k_end − k_begin) doubles); the
+ * permutation is written to d_perm (n int32, may be null) so ranks can
+ * scatter the gathered shards back to particle order. */
+int ptrom_dev_barnes_hut_velocity_slots_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                            double delta, int form, int crit_kind, double crit_value,
+                                            int64_t leaf_capacity, const double* d_inflow, int64_t k_begin,
+                                            int64_t k_end, double* d_f_slots, int32_t* d_perm,
+                                            uint64_t* n_pair_evals);
 
 /* Statistics of the last tree build / evaluation on this context: device
  * time of the build (T1+T2) and of the final traversal pass (T3), kernel

@@ -78,6 +78,9 @@ PROTOTYPES = {
                                                 c_i64, c_dp, c_dp, c_u64p]),
     "ptrom_dev_barnes_hut_velocity_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int,
                                                     C.c_double, c_i64, c_dp, c_dp, c_u64p]),
+    "ptrom_dev_barnes_hut_velocity_slots_f64": (C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int,
+                                                          C.c_double, c_i64, c_dp, c_i64, c_i64, c_dp, C.c_void_p,
+                                                          c_u64p]),
     "ptrom_tree_stats": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_double), c_u64p, c_u64p, c_u64p,
                                    c_u64p]),
     "ptrom_basis_create": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_dp, c_dp, C.POINTER(C.c_void_p)]),

@@ -45,8 +45,12 @@ struct Tree;
 void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const double* d_py, const double* d_g,
                 long long leaf_cap, int seq_max);
 int tree_resolve_uncertain(ptrom_ctx* ctx, Tree& t, const int* d_flag_count);
+// Targets are the tree slots [k_begin, k_end) (k_end < 0: all n). With
+// f_slots != nullptr the velocities go there in slot order, x then y
+// (2·(k_end − k_begin)), instead of d_f in particle order.
 unsigned long long tree_eval(ptrom_ctx* ctx, Tree& t, const double* d_x, const double* d_gamma, double delta,
                              int form, int crit_kind, double crit_value, const double* d_inflow, double* d_f,
-                             double* jxx, double* jxy, double* jyx, double* jyy);
+                             double* jxx, double* jxy, double* jyx, double* jyy, long long k_begin = 0,
+                             long long k_end = -1, double* f_slots = nullptr);
 
 }  // namespace ptrom

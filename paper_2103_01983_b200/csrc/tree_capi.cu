@@ -265,6 +265,33 @@ int ptrom_dev_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* d
   });
 }
 
+int ptrom_dev_barnes_hut_velocity_slots_f64(ptrom_ctx* ctx, int64_t n, const double* d_x, const double* d_gamma,
+                                            double delta, int form, int crit_kind, double crit_value,
+                                            int64_t leaf_capacity, const double* d_inflow, int64_t k_begin,
+                                            int64_t k_end, double* d_f_slots, int32_t* d_perm,
+                                            uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    check_criterion(crit_kind, crit_value);
+    if (!(delta >= 0)) config_fail("negative desingularization constant");
+    if (n <= 0) config_fail("particle system is empty");
+    if (k_begin < 0 || k_end > n || k_begin > k_end) config_fail("target slot range outside [0, n]");
+    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+    Tree t;
+    try {
+      tree_build(ctx, t, n, d_x, d_x + n, d_gamma, leaf_capacity, ctx->tree_seq_max);
+      const unsigned long long pairs = tree_eval(ctx, t, d_x, d_gamma, delta, form, crit_kind, crit_value, d_inflow,
+                                                 nullptr, nullptr, nullptr, nullptr, nullptr, k_begin, k_end,
+                                                 d_f_slots);
+      if (d_perm) PTROM_CUDA(cudaMemcpyAsync(d_perm, t.perm, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (n_pair_evals) *n_pair_evals = pairs;
+    } catch (...) {
+      t.free_all(ctx->stream);
+      throw;
+    }
+    t.free_all(ctx->stream);
+  });
+}
+
 int ptrom_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, const double* gamma, double delta,
                                   int form, int crit_kind, double crit_value, int64_t leaf_capacity,
                                   const double* inflow, double* f, uint64_t* n_pair_evals) {

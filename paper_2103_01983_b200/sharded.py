@@ -20,6 +20,13 @@ per refresh period) still gathers the positions.
 PtromInstanceSplit — μ instances of the PTROM online path split evenly across
 ranks (no communication during the march); reduced states gathered at the end.
 
+ShardedBarnesHut — BarnesHutModel::velocity (integrators.hpp:83-102) with the
+build replicated and the far field split by target: every rank
+builds the identical tree from the replicated state (the build is
+deterministic), evaluates the targets of its contiguous range of tree slots
+(spatially coherent), and the slot-ordered shards are all-gathered and
+scattered back to particle order through the tree permutation.
+
 The compute backend is pluggable: CudaBackend (libptrom_b200.so through the
 device C ABI) is the product; tests drive the same control logic with a CPU
 backend over gloo.
@@ -238,3 +245,60 @@ class PtromInstanceSplit:
         out = torch.empty((self.world * mx,) + tail, dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(out, buf, group=self.group)
         return torch.cat([out[r * mx:r * mx + counts[r]] for r in range(self.world)])
+
+
+class CudaBhBackend:
+    """Replicated build + slot-range far field through ptrom_dev_barnes_hut_velocity_slots_f64."""
+
+    def __init__(self, device_index: int = 0):
+        from .api import default_context
+        self.ctx = default_context(device_index)
+        self.pairs = 0
+
+    def slots(self, x_full, gamma, delta, form, crit_kind, crit_value, leaf, inflow, lo, hi):
+        import ctypes as C
+        n = gamma.shape[0]
+        out = torch.empty(2 * max(hi - lo, 0), dtype=torch.float64, device=x_full.device)
+        perm = torch.empty(n, dtype=torch.int32, device=x_full.device)
+        cnt = C.c_uint64()
+        self.ctx.check(self.ctx.lib.ptrom_dev_barnes_hut_velocity_slots_f64(
+            self.ctx.handle, n, x_full.data_ptr(), gamma.data_ptr(), float(delta), int(form), int(crit_kind),
+            float(crit_value), int(leaf), inflow.data_ptr() if inflow is not None else None, lo, hi,
+            out.data_ptr() if out.numel() else None, perm.data_ptr(), C.byref(cnt)))
+        self.pairs = cnt.value
+        return out, perm
+
+
+class ShardedBarnesHut:
+    """Target-sharded Barnes–Hut velocity (see the module docstring)."""
+
+    def __init__(self, n: int, backend, group=None):
+        self.n, self.be, self.group = n, backend, group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.lo, self.hi = shard_bounds(n, self.rank, self.world)
+
+    def velocity(self, x_full: torch.Tensor, gamma: torch.Tensor, delta: float, crit_kind: int = 0,
+                 crit_value: float = 0.5, leaf: int = 32, form: int = 0,
+                 inflow: Optional[torch.Tensor] = None) -> torch.Tensor:
+        n, lo, hi = self.n, self.lo, self.hi
+        f_loc, perm = self.be.slots(x_full, gamma, delta, form, crit_kind, crit_value, leaf, inflow, lo, hi)
+        m = hi - lo
+        if self.world == 1:
+            fxs, fys = f_loc[:m], f_loc[m:]
+        else:
+            counts = [shard_bounds(n, r, self.world)[1] - shard_bounds(n, r, self.world)[0]
+                      for r in range(self.world)]
+            mx = max(counts)
+            buf = torch.zeros(2 * mx, dtype=torch.float64, device=x_full.device)
+            buf[:m] = f_loc[:m]
+            buf[mx:mx + m] = f_loc[m:]
+            outs = [torch.empty_like(buf) for _ in range(self.world)]
+            dist.all_gather(outs, buf, group=self.group)
+            fxs = torch.cat([outs[r][:counts[r]] for r in range(self.world)])
+            fys = torch.cat([outs[r][mx:mx + counts[r]] for r in range(self.world)])
+        idx = perm.long()
+        f = torch.empty(2 * n, dtype=torch.float64, device=x_full.device)
+        f[idx] = fxs
+        f[n + idx] = fys
+        return f

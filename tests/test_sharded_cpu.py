@@ -148,3 +148,50 @@ def test_shard_bounds_cover_everything():
             b = [shard_bounds(n, r, g) for r in range(g)]
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(g - 1))
+
+
+class OracleBhBackend:
+    """CPU backend with the ShardedBarnesHut interface: the oracle's build_tree and
+    per-target bh_velocity (quadtree.hpp:124-162, 257-281), slots [lo, hi)."""
+
+    def __init__(self, oracle):
+        self.o = oracle
+
+    def slots(self, x_full, gamma, delta, form, crit_kind, crit_value, leaf, inflow, lo, hi):
+        x, g = x_full.numpy(), gamma.numpy()
+        n = g.shape[0]
+        tree = self.o.Tree(x[:n], x[n:], g, leaf)
+        out = torch.zeros(2 * (hi - lo), dtype=torch.float64)
+        for k in range(lo, hi):
+            i = int(tree.perm[k])
+            f = tree.bh_velocity(x, g, delta, crit_kind, crit_value, form=form, t_begin=i, t_end=i + 1)
+            out[k - lo] = f[i]
+            out[(hi - lo) + k - lo] = f[n + i]
+        return out, torch.from_numpy(tree.perm.astype(np.int32))
+
+
+def _bh_worker(rank, world, port, n, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import pyoracle
+        from paper_2103_01983_b200 import workloads
+        from paper_2103_01983_b200.sharded import ShardedBarnesHut
+        w = workloads.config3(n=n)
+        bh = ShardedBarnesHut(n, OracleBhBackend(pyoracle))
+        f = bh.velocity(torch.tensor(w.x0), torch.tensor(w.gamma), w.delta, 0, 0.5, 4)
+        if rank == 0:
+            out_q.put(f.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 160), (3, 101)])
+def test_sharded_barnes_hut_matches_single_process_oracle(oracle, world, n):
+    """Replicated build, far field split by tree slot, shards gathered back to
+    particle order: bit-identical to the oracle's single-process bh_velocity."""
+    from paper_2103_01983_b200 import workloads
+    f = _run(world, _bh_worker, (n,))
+    w = workloads.config3(n=n)
+    tree = oracle.Tree(w.x0[:n], w.x0[n:], w.gamma, 4)
+    np.testing.assert_array_equal(f, tree.bh_velocity(w.x0, w.gamma, w.delta, 0, 0.5))

@@ -260,3 +260,40 @@ def test_wide_counter_path_above_2pow21(pt, oracle):
     ref = ot.bh_velocity(x, g, 1e-6, 0, 0.5, t_begin=0, t_end=1500, threads=THREADS)
     rows = np.r_[0:1500, n:n + 1500]
     assert rel(f[rows], ref[rows]) <= 1e-12
+
+
+@pytest.mark.parametrize("n,shards", [(5000, 3), (65536, 8)])
+def test_sharded_barnes_hut_slots_equal_full_evaluation(pt, oracle, n, shards):
+    """Replicated build + slot-range far field (ShardedBarnesHut's per-rank call,
+    SURVEY.md §8e): the slot shards, scattered through perm, are bit-identical
+    to the single-call evaluation, and perm is the oracle's."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2103_01983_b200.sharded import CudaBhBackend, ShardedBarnesHut, shard_bounds
+    w = workloads.config3(n=n)
+    x = torch.tensor(w.x0, device="cuda")
+    g = torch.tensor(w.gamma, device="cuda")
+    ctx = pt.default_context()
+    full = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    cnt = C.c_uint64()
+    ctx.check(ctx.lib.ptrom_dev_barnes_hut_velocity_f64(ctx.handle, n, x.data_ptr(), g.data_ptr(), w.delta, 0, 0,
+                                                        0.5, 32, None, full.data_ptr(), C.byref(cnt)))
+    be = CudaBhBackend()
+    fx, fy = torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.float64, device="cuda")
+    perm = None
+    for r in range(shards):
+        lo, hi = shard_bounds(n, r, shards)
+        loc, perm = be.slots(x, g, w.delta, 0, 0, 0.5, 32, None, lo, hi)
+        fx[lo:hi], fy[lo:hi] = loc[:hi - lo], loc[hi - lo:]
+    f = torch.empty_like(full)
+    f[perm.long()] = fx
+    f[n + perm.long()] = fy
+    np.testing.assert_array_equal(f.cpu().numpy(), full.cpu().numpy())
+    f1 = ShardedBarnesHut(n, be).velocity(x, g, w.delta, 0, 0.5, 32)
+    np.testing.assert_array_equal(f1.cpu().numpy(), full.cpu().numpy())
+    if n <= 5000:
+        ot = oracle.Tree(w.x0[:n], w.x0[n:], w.gamma, 32)
+        np.testing.assert_array_equal(perm.cpu().numpy(), ot.perm)
+        assert rel(full.cpu().numpy(), ot.bh_velocity(w.x0, w.gamma, w.delta, 0, 0.5)) <= 1e-12
