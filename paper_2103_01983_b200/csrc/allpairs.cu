@@ -331,15 +331,47 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, Sr
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    // chunk partials summed in ascending chunk order (bit-identical to the
+    // separate reduction); U chunks of every target are loaded before they
+    // are added, so the tail is ~nch/U L2 round trips, not nch
+    constexpr int U = T <= 2 ? 8 : (T <= 4 ? 4 : 2);
+    const int nch = (int)gridDim.y;
+    double sxs[T], sys[T];
+    long long lis[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      sxs[k] = sys[k] = 0.0;
+      lis[k] = ti[k] >= 0 ? ti[k] - t_begin : 0;
+    }
+    int c = 0;
+    for (; c + U <= nch; c += U) {
+      double vx[T][U], vy[T][U];
+#pragma unroll
+      for (int k = 0; k < T; ++k)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          vx[k][u] = __ldcg(part + ((long long)(c + u) * 2 + 0) * t_count + lis[k]);
+          vy[k][u] = __ldcg(part + ((long long)(c + u) * 2 + 1) * t_count + lis[k]);
+        }
+#pragma unroll
+      for (int k = 0; k < T; ++k)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          sxs[k] += vx[k][u];
+          sys[k] += vy[k][u];
+        }
+    }
+    for (; c < nch; ++c)
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        sxs[k] += __ldcg(part + ((long long)c * 2 + 0) * t_count + lis[k]);
+        sys[k] += __ldcg(part + ((long long)c * 2 + 1) * t_count + lis[k]);
+      }
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       if (ti[k] < 0) continue;
-      const long long li = ti[k] - t_begin;
-      double sx = 0.0, sy = 0.0;
-      for (unsigned c = 0; c < gridDim.y; ++c) {
-        sx += __ldcg(part + ((long long)c * 2 + 0) * t_count + li);
-        sy += __ldcg(part + ((long long)c * 2 + 1) * t_count + li);
-      }
+      const long long li = lis[k];
+      double sx = sxs[k], sy = sys[k];
       const long long i = ti[k];
       if (fo.inflow) {
         sx = sx + fo.inflow[i];
@@ -360,8 +392,23 @@ __global__ void reduce_velocity_f64_kernel(long long n, long long t_begin, long 
                                            DeviceStatus* st) {
   for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < t_count;
        li += (long long)gridDim.x * blockDim.x) {
+    // ascending chunk order; 8 chunks loaded ahead of their adds
     double fx = 0.0, fy = 0.0;
-    for (int c = 0; c < n_chunks; ++c) {
+    int c = 0;
+    for (; c + 8 <= n_chunks; c += 8) {
+      double vx[8], vy[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        vx[u] = part[((long long)(c + u) * ncomp + 0) * t_count + li];
+        vy[u] = part[((long long)(c + u) * ncomp + 1) * t_count + li];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        fx += vx[u];
+        fy += vy[u];
+      }
+    }
+    for (; c < n_chunks; ++c) {
       fx += part[((long long)c * ncomp + 0) * t_count + li];
       fy += part[((long long)c * ncomp + 1) * t_count + li];
     }
@@ -386,8 +433,26 @@ __global__ void reduce_jacobian_f64_kernel(long long t_begin, long long t_count,
                                            double* __restrict__ inv, DeviceStatus* st) {
   for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < t_count;
        li += (long long)gridDim.x * blockDim.x) {
+    // ascending chunk order; 8 chunks loaded ahead of their adds
     double a = 0.0, b = 0.0, c = 0.0;
-    for (int ch = 0; ch < n_chunks; ++ch) {
+    int ch = 0;
+    for (; ch + 8 <= n_chunks; ch += 8) {
+      double va[8], vb[8], vc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double* pc = part + (long long)(ch + u) * ncomp * t_count + li;
+        va[u] = pc[(off + 0) * t_count];
+        vb[u] = pc[(off + 1) * t_count];
+        vc[u] = pc[(off + 2) * t_count];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a += va[u];
+        b += vb[u];
+        c += vc[u];
+      }
+    }
+    for (; ch < n_chunks; ++ch) {
       const double* pc = part + (long long)ch * ncomp * t_count + li;
       a += pc[(off + 0) * t_count];
       b += pc[(off + 1) * t_count];
@@ -623,8 +688,8 @@ void launch_allpairs_src(ptrom_ctx* ctx, long long n, Src src, const double* gam
   static int occ = resident_blocks(kern, TPB);
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   const long long tiles = (t_count + TPB * T - 1) / (TPB * T);
-  // short source ranges (small N) may split down to one source tile per chunk
-  const int chunks = choose_source_chunks(ctx, tiles, n, occ, T <= 2 ? TPB : 2 * TPB);
+  // short source ranges (small N) may split into chunks of 32 sources
+  const int chunks = choose_source_chunks(ctx, tiles, n, occ, T <= 2 ? 32 : 2 * TPB);
   const long long chunk_len = (n + chunks - 1) / chunks;
   ctx->scratch.reset();
   ctx->scratch.reserve((size_t)chunks * NCOMP * t_count * sizeof(double) + 4096);
