@@ -215,6 +215,11 @@ int ptrom_dev_barnes_hut_velocity_slots_f64(ptrom_ctx* ctx, int64_t n, const dou
  * hit an uncertain (certified-then-resolved) prune test. */
 int ptrom_tree_stats(ptrom_ctx* ctx, double* build_ms, double* eval_ms, uint64_t* interactions,
                      uint64_t* prune_tests, uint64_t* nodes, uint64_t* resolved_targets);
+/* Which build produced the last tree on this context: *morton = 1 for the
+ * Morton-key sort build, 0 for the level-by-level partition (chosen when the
+ * tree needs more than 32 levels, leaf_capacity > 256, or PTROM_TREE_BUILD=levels);
+ * *levels = tree levels walked by the Morton build. Same tree either way. */
+int ptrom_tree_build_info(ptrom_ctx* ctx, int* morton, int* levels);
 
 /* ----------------------------------------------------------- PTROM online -- */
 /* PODBasis (reduction.hpp:18-26): phi is n_dofs x modes column-major. */

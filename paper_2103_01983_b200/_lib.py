@@ -83,6 +83,7 @@ PROTOTYPES = {
                                                           c_u64p]),
     "ptrom_tree_stats": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_double), c_u64p, c_u64p, c_u64p,
                                    c_u64p]),
+    "ptrom_tree_build_info": (C.c_int, [c_ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ptrom_basis_create": (C.c_int, [c_ctxp, c_i64, c_i64, c_dp, c_dp, c_dp, C.POINTER(C.c_void_p)]),
     "ptrom_reconstruct_output_f64": (C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_i64, c_dp, c_dp]),
     "ptrom_dev_reconstruct_output_f64": (C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_i64, c_dp, c_dp]),

@@ -115,9 +115,10 @@ int ptrom_create(int device, void* stream, ptrom_ctx** out) {
     PTROM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     if (const char* v = std::getenv("PTROM_ALLPAIRS_VARIANT")) ctx->allpairs_variant = std::atoi(v);
     if (const char* v = std::getenv("PTROM_TREE_SEQ_MAX")) ctx->tree_seq_max = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("PTROM_TREE_BUILD")) ctx->tree_build_mode = std::string(v) == "levels" ? 1 : 0;
     PTROM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DeviceStatus)));
     PTROM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DeviceStatus)));
-    PTROM_CUDA(cudaMallocHost(&ctx->h_counts, 16 * sizeof(int)));
+    PTROM_CUDA(cudaMallocHost(&ctx->h_counts, 128 * sizeof(int)));  // also holds the Morton build state
     DeviceStatus clear{0, 0, LLONG_MAX};
     PTROM_CUDA(cudaMemcpy(ctx->d_status, &clear, sizeof(clear), cudaMemcpyHostToDevice));
   });

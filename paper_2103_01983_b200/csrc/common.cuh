@@ -90,6 +90,7 @@ namespace ptrom {
 struct TreeStats {  // last tree build / evaluation on this context (ptrom_tree_stats)
   double build_ms = 0, eval_ms = 0;
   unsigned long long interactions = 0, prune_tests = 0, nodes = 0, levels = 0, resolved_targets = 0;
+  int morton = 0;  // 1 when the last build used the Morton-key path
 };
 }  // namespace ptrom
 
@@ -113,6 +114,7 @@ struct ptrom_ctx {
   int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
   ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)
+  int tree_build_mode = 0;   // 0: Morton-key build (level build when it does not apply), 1: level build (PTROM_TREE_BUILD=levels)
 };
 
 namespace ptrom {

@@ -392,6 +392,40 @@ __global__ void __launch_bounds__(kThreads) sums_mid_kernel(TreeRecords rec, con
   }
 }
 
+// Large-node finish: centroid from block/child-reduced sums red = {Σg, Σgx,
+// Σgy, Σx, Σy, Σ|g|, Σ|gx|, Σ|gy|}, with a rigorous bound on its distance from
+// the reference's sequential order (quadtree.hpp:51-67).
+__device__ void finish_certified(TreeRecords& rec, int r, int b, int e, const double (&red)[8]) {
+  const double m = (double)(e - b);
+  const double u = 0x1p-53;
+  // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
+  // sum; their difference within twice that (first order, padded).
+  const double k2 = 2.05 * (m + 1.0) * u;
+  const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
+  const double gs = red[0];
+  rec.gamma_sum[r] = gs;
+  const bool fb = gs == 0.0;
+  rec.fallback[r] = fb ? 1 : 0;
+  double cx, cy, err;
+  if (fb) {
+    cx = __ddiv_rn(red[3], m);
+    cy = __ddiv_rn(red[4], m);
+  } else {
+    cx = __ddiv_rn(red[1], gs);
+    cy = __ddiv_rn(red[2], gs);
+  }
+  if (fabs(gs) <= 2.0 * eg) {
+    err = INFINITY;  // the fallback flag itself is uncertain
+  } else {
+    const double ag = fabs(gs) - eg;
+    err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
+  }
+  rec.centroid[2 * r] = cx;
+  rec.centroid[2 * r + 1] = cy;
+  rec.exact[r] = 0;
+  rec.cerr[r] = err;
+}
+
 // Large nodes (> seq_max members) in ONE launch: every CTA finds the node of
 // each of its chunks (kChunk members) from the large list, reduces the chunk
 // with a fixed-order block reduction; the last CTA to finish adds each
@@ -502,34 +536,7 @@ __global__ void __launch_bounds__(kThreads) large_sums_kernel(TreeRecords rec, c
     double red[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int ci = chunk_off[li]; ci < chunk_off[li + 1]; ++ci)
       for (int c = 0; c < 8; ++c) red[c] = __dadd_rn(red[c], part[8 * (long long)ci + c]);
-    const double m = (double)(e - b);
-    const double u = 0x1p-53;
-    // both orders are within (m-1)u·Σ|a| (+ product rounding) of the exact
-    // sum; their difference within twice that (first order, padded).
-    const double k2 = 2.05 * (m + 1.0) * u;
-    const double eg = k2 * red[5], ex = k2 * (red[6] * 1.0001), ey = k2 * (red[7] * 1.0001);
-    const double gs = red[0];
-    rec.gamma_sum[r] = gs;
-    const bool fb = gs == 0.0;
-    rec.fallback[r] = fb ? 1 : 0;
-    double cx, cy, err;
-    if (fb) {
-      cx = __ddiv_rn(red[3], m);
-      cy = __ddiv_rn(red[4], m);
-    } else {
-      cx = __ddiv_rn(red[1], gs);
-      cy = __ddiv_rn(red[2], gs);
-    }
-    if (fabs(gs) <= 2.0 * eg) {
-      err = INFINITY;  // the fallback flag itself is uncertain
-    } else {
-      const double ag = fabs(gs) - eg;
-      err = (ex + fabs(cx) * eg) / ag + (ey + fabs(cy) * eg) / ag + 8.0 * u * (fabs(cx) + fabs(cy));
-    }
-    rec.centroid[2 * r] = cx;
-    rec.centroid[2 * r + 1] = cy;
-    rec.exact[r] = 0;
-    rec.cerr[r] = err;
+    finish_certified(rec, r, b, e, red);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -539,21 +546,33 @@ __global__ void __launch_bounds__(kThreads) large_sums_kernel(TreeRecords rec, c
 }
 
 // ------------------------------------------------------------ preorder ---
-__global__ void preorder_keys_kernel(int R, const int* __restrict__ rbegin, const int* __restrict__ rdepth,
-                                     unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+// Preorder (quadtree.hpp:97-116 numbers a child, then recurses) sorts nodes by
+// (begin, depth); the nodes sharing a begin are one ancestor chain with
+// consecutive depths, so id = #(nodes with a smaller begin) + depth - (the
+// chain's smallest depth): a histogram over begin, one scan, no sort.
+__global__ void begin_hist_kernel(int R, const int* __restrict__ rbegin, const int* __restrict__ rdepth,
+                                  int* __restrict__ cnt, int* __restrict__ mind) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
-  keys[r] = ((unsigned long long)rbegin[r] << 7) | (unsigned long long)rdepth[r];
-  vals[r] = r;
+  const int b = rbegin[r];
+  atomicAdd(cnt + b, 1);
+  atomicMin(mind + b, rdepth[r]);
 }
 
-__global__ void rec2id_kernel(int R, const int* __restrict__ order, int* __restrict__ rec2id) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < R) rec2id[order[i]] = i;
+__global__ void preorder_ids_kernel(int R, const int* __restrict__ rbegin, const int* __restrict__ rdepth,
+                                    const int* __restrict__ base, const int* __restrict__ mind,
+                                    int* __restrict__ rec2id, int* __restrict__ order) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int b = rbegin[r];
+  const int id = base[b] + rdepth[r] - mind[b];
+  rec2id[r] = id;
+  order[id] = r;
 }
+
 
 __global__ void emit_nodes_kernel(int R, const int* __restrict__ order, const int* __restrict__ rec2id,
-                                  const unsigned long long* __restrict__ sorted_keys, TreeRecords rec, TreeNodes nd) {
+                                  const int* __restrict__ begin_base, TreeRecords rec, TreeNodes nd) {
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= R) return;
   const int r = order[id];
@@ -566,15 +585,7 @@ __global__ void emit_nodes_kernel(int R, const int* __restrict__ order, const in
   const bool leaf = rec.children[4 * r] < 0 && rec.children[4 * r + 1] < 0 && rec.children[4 * r + 2] < 0 &&
                     rec.children[4 * r + 3] < 0;
   // skip: first node in preorder with begin >= e
-  const unsigned long long key = (unsigned long long)e << 7;
-  int lo = id + 1, hi = R;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sorted_keys[mid] < key)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
+  const int lo = begin_base[e];
   nd.width[id] = rec.width[r];
   nd.centroid[2 * id] = rec.centroid[2 * r];
   nd.centroid[2 * id + 1] = rec.centroid[2 * r + 1];
@@ -710,6 +721,44 @@ void Tree::free_all(cudaStream_t s) {
   sx = sy = sg = px = py = g = nullptr;
 }
 
+// Preorder numbering and the final tables, shared by both builds: records
+// [0, R) with perm-order members (ord, sx, sy, sg become the tree's).
+void finish_tree(ptrom_ctx* ctx, Tree& t, TreeRecords& rec, int R, int* ord, double* sx, double* sy, double* sg) {
+  cudaStream_t s = ctx->stream;
+  const long long n = t.n;
+  // ---- preorder numbering
+  int *cnt = dalloc<int>(n + 1), *base = dalloc<int>(n + 1), *mind = dalloc<int>(n + 1);
+  int *order = dalloc<int>(R), *rec2id = dalloc<int>(R);
+  PTROM_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), s));
+  PTROM_CUDA(cudaMemsetAsync(mind, 0x7f, (n + 1) * sizeof(int), s));
+  begin_hist_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, rec.begin, rec.depth, cnt, mind);
+  PTROM_LAUNCH_CHECK();
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, base, (int)(n + 1), s);
+  void* stmp = dalloc<char>(scan_bytes + 256);
+  PTROM_CUDA(cub::DeviceScan::ExclusiveSum(stmp, scan_bytes, cnt, base, (int)(n + 1), s));
+  preorder_ids_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, rec.begin, rec.depth, base, mind, rec2id,
+                                                                         order);
+  t.nodes.alloc(R);
+  emit_nodes_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, order, rec2id, base, rec, t.nodes);
+  PTROM_LAUNCH_CHECK();
+  PTROM_CUDA(cudaMemsetAsync(t.nodes.need_exact, 0, R, s));
+
+  t.perm = ord;
+  t.sx = sx;
+  t.sy = sy;
+  t.sg = sg;
+  t.slot = dalloc<int>(n);
+  t.leaf_node = dalloc<int>(n);
+  particle_maps_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.perm, t.slot);
+  leaf_node_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, t.nodes, t.perm, t.leaf_node);
+  PTROM_LAUNCH_CHECK();
+  void* frees[] = {cnt, base, mind, order, rec2id, stmp};
+  for (void* p : frees) dfree(p);
+}
+
+bool tree_build_morton(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max);
+
 // quadtree.hpp:124-162 build_tree over device points (px, py) and weights g.
 void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const double* d_py, const double* d_g,
                 long long leaf_cap, int seq_max) {
@@ -732,6 +781,20 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   PTROM_CUDA(cudaMemcpyAsync(t.px, d_px, n * 8, cudaMemcpyDeviceToDevice, s));
   PTROM_CUDA(cudaMemcpyAsync(t.py, d_py, n * 8, cudaMemcpyDeviceToDevice, s));
   PTROM_CUDA(cudaMemcpyAsync(t.g, d_g, n * 8, cudaMemcpyDeviceToDevice, s));
+
+  ctx->tree_stats = TreeStats{};
+  if (ctx->tree_build_mode == 0 && tree_build_morton(ctx, t, leaf_cap, seq_max)) {
+    cudaEventRecord(ev1, s);
+    PTROM_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    ctx->tree_stats.build_ms = ms;
+    ctx->tree_stats.nodes = t.nodes.count;
+    ctx->tree_stats.morton = 1;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return;
+  }
 
   // ---- root: tight square hull (quadtree.hpp:139-151)
   const int hb = std::min<long long>((n + kThreads - 1) / kThreads, 256);
@@ -896,35 +959,11 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   else
     run_levels((uint4*)nullptr);
 
-  // ---- preorder numbering (sort records by (begin, depth))
-  unsigned long long *keys = dalloc<unsigned long long>(R), *keys_s = dalloc<unsigned long long>(R);
-  int *vals = dalloc<int>(R), *order = dalloc<int>(R), *rec2id = dalloc<int>(R);
-  preorder_keys_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, rec.begin, rec.depth, keys, vals);
-  PTROM_LAUNCH_CHECK();
-  size_t sort_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys, keys_s, vals, order, R, 0, 7 + 31, s);
-  void* stmp = dalloc<char>(sort_bytes + 256);
-  PTROM_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sort_bytes, keys, keys_s, vals, order, R, 0, 7 + 31, s));
-  rec2id_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, order, rec2id);
-  t.nodes.alloc(R);
-  emit_nodes_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, order, rec2id, keys_s, rec, t.nodes);
-  PTROM_LAUNCH_CHECK();
-  PTROM_CUDA(cudaMemsetAsync(t.nodes.need_exact, 0, R, s));
-
-  t.perm = ord;
-  t.sx = sx;
-  t.sy = sy;
-  t.sg = sg;
-  t.slot = dalloc<int>(n);
-  t.leaf_node = dalloc<int>(n);
-  particle_maps_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.perm, t.slot);
-  leaf_node_kernel<<<(R + kThreads - 1) / kThreads, kThreads, 0, s>>>(R, t.nodes, t.perm, t.leaf_node);
-  PTROM_LAUNCH_CHECK();
+  finish_tree(ctx, t, rec, R, ord, sx, sy, sg);
   cudaEventRecord(ev1, s);
   PTROM_CUDA(cudaStreamSynchronize(s));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
-  ctx->tree_stats = TreeStats{};
   ctx->tree_stats.build_ms = ms;
   ctx->tree_stats.nodes = R;
   ctx->tree_stats.levels = 0;
@@ -932,9 +971,761 @@ void tree_build(ptrom_ctx* ctx, Tree& t, long long n, const double* d_px, const 
   cudaEventDestroy(ev1);
 
   void* frees[] = {ord_n, pr, pr_n, sx_n, sy_n, sg_n, flags_raw, scan_raw, digit, dcount, tmp, nchild, child_off, large_list,
-                   chunk_off, large_part, done_ctr, mid_list, lv_buf, keys, keys_s, vals, order, rec2id, stmp};
+                   chunk_off, large_part, done_ctr, mid_list, lv_buf};
   for (void* p : frees) dfree(p);
   rec.free();
+}
+
+
+// ========================================================= Morton build ===
+// The same tree from one sort. Node bounds depend only on the path from the
+// root (child bounds = parent bounds cut at the parent's midpoint,
+// quadtree.hpp:87-93), so each point replays the reference's midpoint
+// arithmetic down its path on its own and records the 2-bit quadrant of each
+// level in a 64-bit key (level 0 in the top bits). A stable radix sort of
+// (key, id) puts every node's members in one contiguous range, children in
+// SW, SE, NW, NE order. Then:
+//  * nodes above seq_max members (the certified-sum "large" nodes) are split
+//    level by level in one cooperative launch (grid barrier per level): the
+//    child boundaries are the digit changes inside the node's key range;
+//  * every node of at most seq_max members whose parent is large roots a
+//    subtree that one CTA finishes in shared memory: its keys, ids and
+//    (Γ, x, y) are loaded once; the CTA splits it level by level, then walks
+//    the levels back up: a leaf sorts its members by id (the reference's
+//    bucket order, quadtree.hpp:81-105, giving perm / sx / sy / sg), an
+//    internal node merges its children's ascending-id runs, and finish_node's
+//    five sequential chains (quadtree.hpp:51-67) run over that order, so the
+//    sums are bit-identical;
+//  * the large nodes take the certified chunked reduction (large_sums_kernel).
+// A split needed below the key's levels, a subtree with more local nodes than
+// the CTA holds, or a record-capacity overflow makes the host rebuild with the
+// level build (same tree).
+namespace {
+
+constexpr int kMortonLevels = 32;
+constexpr int kSubMax = 2048;     // members of a subtree (seq_max <= kSubMax)
+constexpr int kSubNodes = 2048;   // local nodes of a subtree
+constexpr int kSubThreads = 256;
+constexpr int kSubLevels = 64;
+constexpr int kMergeChunk = 128;
+
+struct MortonState {
+  int lvl_cnt[kMaxDepth + 2];  // records per level of the large-node pass (level 0 = root)
+  int overflow;                // split needed below the key's levels / capacity exceeded
+  int finite;                  // hull finite
+  int levels_used;
+  int large_count, sub_count;
+  int rec_extra;               // records created by the subtree CTAs
+  unsigned bar_count, bar_gen;
+  double width;
+};
+
+__device__ __forceinline__ void grid_barrier(MortonState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &st->bar_gen;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
+      st->bar_count = 0;
+      __threadfence();
+      atomicAdd(&st->bar_gen, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Root record from the hull partials (quadtree.hpp:139-151), on the device.
+__global__ void morton_root_kernel(int hb, const double* __restrict__ hull, long long n, long long leaf_cap,
+                                   TreeRecords rec, MortonState* st) {
+  if (blockIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
+  double xl = DBL_MAX, xh = -DBL_MAX, yl = DBL_MAX, yh = -DBL_MAX;
+  for (int b = lane; b < hb; b += 32) {
+    xl = fmin(xl, hull[4 * b]);
+    xh = fmax(xh, hull[4 * b + 1]);
+    yl = fmin(yl, hull[4 * b + 2]);
+    yh = fmax(yh, hull[4 * b + 3]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    xl = fmin(xl, __shfl_xor_sync(0xffffffffu, xl, o));
+    xh = fmax(xh, __shfl_xor_sync(0xffffffffu, xh, o));
+    yl = fmin(yl, __shfl_xor_sync(0xffffffffu, yl, o));
+    yh = fmax(yh, __shfl_xor_sync(0xffffffffu, yh, o));
+  }
+  if (lane != 0) return;
+  st->finite = isfinite(xl) && isfinite(xh) && isfinite(yl) && isfinite(yh);
+  double side = fmax(__dsub_rn(xh, xl), __dsub_rn(yh, yl));
+  if (side == 0.0) side = 1.0;
+  const double cx = __dmul_rn(__dadd_rn(xl, xh), 0.5), cy = __dmul_rn(__dadd_rn(yl, yh), 0.5);
+  const double hs = __dmul_rn(side, 0.5);
+  const double b0 = __dsub_rn(cx, hs), b1 = __dadd_rn(cx, hs), b2 = __dsub_rn(cy, hs), b3 = __dadd_rn(cy, hs);
+  rec.begin[0] = 0;
+  rec.end[0] = (int)n;
+  rec.depth[0] = 0;
+  for (int q = 0; q < 4; ++q) rec.children[q] = -1;
+  rec.split[0] = n > leaf_cap ? 1 : 0;
+  rec.bounds[0] = b0;
+  rec.bounds[1] = b1;
+  rec.bounds[2] = b2;
+  rec.bounds[3] = b3;
+  rec.mid[0] = __dmul_rn(__dadd_rn(b0, b1), 0.5);
+  rec.mid[1] = __dmul_rn(__dadd_rn(b2, b3), 0.5);
+  rec.width[0] = side;
+  st->width = side;
+  st->lvl_cnt[0] = 1;
+}
+
+// Path key of every point: the quadrant chosen at each of `levels` levels
+// with the reference's midpoint and `<=` rule (quadtree.hpp:77-85).
+__global__ void morton_keys_kernel(long long n, const double* __restrict__ px, const double* __restrict__ py,
+                                   const TreeRecords rec, int levels, unsigned long long* __restrict__ key,
+                                   int* __restrict__ ids) {
+  const double r0 = rec.bounds[0], r1 = rec.bounds[1], r2 = rec.bounds[2], r3 = rec.bounds[3];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double x = px[i], y = py[i];
+    double b0 = r0, b1 = r1, b2 = r2, b3 = r3;
+    unsigned long long k = 0;
+    for (int l = 0; l < levels; ++l) {
+      const double cx = __dmul_rn(__dadd_rn(b0, b1), 0.5), cy = __dmul_rn(__dadd_rn(b2, b3), 0.5);
+      const bool qx = !(x <= cx), qy = !(y <= cy);
+      k = (k << 2) | (unsigned long long)((qy ? 2 : 0) | (qx ? 1 : 0));
+      if (qx) b0 = cx; else b1 = cx;
+      if (qy) b2 = cy; else b3 = cy;
+    }
+    key[i] = k;
+    ids[i] = (int)i;
+  }
+}
+
+__device__ __forceinline__ int key_digit(const unsigned long long* __restrict__ skey, int k, int shift) {
+  return (int)((__ldg(skey + k) >> shift) & 3ull);
+}
+
+// Child geometry of record r (quadtree.hpp:87-105) into record c for quadrant q.
+__device__ __forceinline__ void morton_child_geometry(TreeRecords& rec, int r, int c, int q, int d, bool l2) {
+  double b0, b1, b2, b3, cx, cy, w;
+  if (l2) {  // parent written by another CTA of this launch
+    b0 = __ldcg(rec.bounds + 4 * r);
+    b1 = __ldcg(rec.bounds + 4 * r + 1);
+    b2 = __ldcg(rec.bounds + 4 * r + 2);
+    b3 = __ldcg(rec.bounds + 4 * r + 3);
+    cx = __ldcg(rec.mid + 2 * r);
+    cy = __ldcg(rec.mid + 2 * r + 1);
+    w = __ldcg(rec.width + r);
+  } else {
+    b0 = rec.bounds[4 * r];
+    b1 = rec.bounds[4 * r + 1];
+    b2 = rec.bounds[4 * r + 2];
+    b3 = rec.bounds[4 * r + 3];
+    cx = rec.mid[2 * r];
+    cy = rec.mid[2 * r + 1];
+    w = rec.width[r];
+  }
+  const double cb0 = (q & 1) ? cx : b0, cb1 = (q & 1) ? b1 : cx;
+  const double cb2 = (q & 2) ? cy : b2, cb3 = (q & 2) ? b3 : cy;
+  rec.bounds[4 * c] = cb0;
+  rec.bounds[4 * c + 1] = cb1;
+  rec.bounds[4 * c + 2] = cb2;
+  rec.bounds[4 * c + 3] = cb3;
+  rec.mid[2 * c] = __dmul_rn(__dadd_rn(cb0, cb1), 0.5);
+  rec.mid[2 * c + 1] = __dmul_rn(__dadd_rn(cb2, cb3), 0.5);
+  rec.width[c] = __ddiv_rn(w, 2.0);
+  rec.depth[c] = d + 1;
+  rec.children[4 * c] = rec.children[4 * c + 1] = rec.children[4 * c + 2] = rec.children[4 * c + 3] = -1;
+}
+
+// Large nodes (> seq_max members), level by level (quadtree.hpp:70-116): one
+// cooperative launch, a grid barrier between levels, a warp per node with a
+// grouped 11-ary search for the three digit boundaries. Children of at most
+// seq_max members are subtree roots for morton_subtree_kernel.
+__global__ void __launch_bounds__(kThreads) morton_levels_kernel(const unsigned long long* __restrict__ skey,
+                                                                 int levels, long long leaf_cap, int seq_max,
+                                                                 TreeRecords rec, int rec_cap, MortonState* st,
+                                                                 int* __restrict__ sub_list,
+                                                                 int* __restrict__ large_list) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int nwarps = gridDim.x * (kThreads / 32);
+  int base = 0, cnt = 1;
+  int d = 0;
+  for (;; ++d) {
+    const int next_base = base + cnt;
+    const int shift = 2 * (levels - 1 - d);
+    for (int w = gwarp; w < cnt; w += nwarps) {
+      const int r = base + w;
+      const int b = __ldcg(rec.begin + r), e = __ldcg(rec.end + r);
+      if (e - b <= seq_max) {
+        if (lane == 0) sub_list[atomicAdd(&st->sub_count, 1)] = r;
+        continue;
+      }
+      if (lane == 0) large_list[atomicAdd(&st->large_count, 1)] = r;
+      if (d >= levels) {  // a large node always splits (count > seq_max >= leaf_capacity)
+        if (lane == 0) st->overflow = 1;
+        continue;
+      }
+      const int g = lane < 11 ? 0 : (lane < 22 ? 1 : 2);
+      const int g0 = g * 11, gsz = g == 2 ? 10 : 11, gl = lane - g0;
+      const int q = g + 1;
+      int lo = b, hi = e;  // first k in [lo, hi] with digit >= q (hi = e: none)
+      while (__any_sync(0xffffffffu, hi > lo)) {
+        const long long span = hi - lo;
+        const int p = lo + (int)((span * gl) / gsz);
+        const bool pred = hi > lo && key_digit(skey, p, shift) >= q;
+        const unsigned bits = (__ballot_sync(0xffffffffu, pred) >> g0) & ((1u << gsz) - 1u);
+        if (hi > lo) {
+          const int J = bits ? __ffs(bits) - 1 : gsz;
+          const int pJ = J < gsz ? lo + (int)((span * J) / gsz) : hi;
+          const int pJm = J > 0 ? lo + (int)((span * (J - 1)) / gsz) + 1 : lo;
+          lo = pJm;
+          hi = pJ;
+        }
+      }
+      const int s1 = __shfl_sync(0xffffffffu, lo, 0), s2 = __shfl_sync(0xffffffffu, lo, 11),
+                s3 = __shfl_sync(0xffffffffu, lo, 22);
+      if (lane == 0) {
+        const int sb[5] = {b, s1, s2, s3, e};
+        int nch = 0;
+        for (int k = 0; k < 4; ++k) nch += sb[k + 1] > sb[k];
+        const int first = next_base + atomicAdd(&st->lvl_cnt[d + 1], nch);
+        if (first + nch > rec_cap) {
+          st->overflow = 1;
+        } else {
+          int j = 0;
+          for (int k = 0; k < 4; ++k) {
+            if (sb[k + 1] == sb[k]) {
+              rec.children[4 * r + k] = -1;
+              continue;
+            }
+            const int c = first + (j++);
+            rec.children[4 * r + k] = c;
+            rec.begin[c] = sb[k];
+            rec.end[c] = sb[k + 1];
+            rec.split[c] = (sb[k + 1] - sb[k] > leaf_cap && d + 1 < kMaxDepth) ? 1 : 0;
+            morton_child_geometry(rec, r, c, k, d, true);
+          }
+        }
+      }
+    }
+    grid_barrier(st);
+    const int ncnt = *(volatile int*)&st->lvl_cnt[d + 1];
+    const int ovf = *(volatile int*)&st->overflow;
+    base = next_base;
+    cnt = ncnt;
+    if (cnt == 0 || ovf || d + 1 > kMaxDepth) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->levels_used = d + 1;
+}
+
+// Shared-memory layout of one subtree CTA.
+struct SubSmem {
+  unsigned long long keys[kSubMax];  // topology phase; aid[] in the sums phase
+  int ids[kSubMax];
+  double g[kSubMax], x[kSubMax], y[kSubMax];
+  short ord[2][kSubMax];             // ascending-id order (local member index), ping-pong by level
+  short lb[kSubNodes], le[kSubNodes];
+  int lrec[kSubNodes];
+  short lfirst[kSubNodes];
+  unsigned char ldep[kSubNodes], lsplit[kSubNodes], lmask[kSubNodes];
+  short lvl_start[kSubLevels + 2];
+  short cpre[kSubNodes + 1];         // merge work list: chunk prefix over one level's nodes
+  int nloc, nlvl, base, ovf;
+};
+
+// One CTA per subtree root (see the section comment).
+__global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
+    const unsigned long long* __restrict__ skey, const int* __restrict__ sid, const double* __restrict__ px,
+    const double* __restrict__ py, const double* __restrict__ pg, const int* __restrict__ sub_list,
+    MortonState* st, TreeRecords rec, int rec_cap, int rec_top, int levels, long long leaf_cap, int* __restrict__ perm,
+    double* __restrict__ sx, double* __restrict__ sy, double* __restrict__ sg, double* __restrict__ aux) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double s_abs[kSubThreads / 32][3];
+  SubSmem& S = *reinterpret_cast<SubSmem*>(smem_raw);
+  int* const aid_base = reinterpret_cast<int*>(S.keys);  // two kSubMax id buffers
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarp = kSubThreads / 32;
+  const int n_sub = st->sub_count;
+  for (int si = blockIdx.x; si < n_sub; si += gridDim.x) {
+    const int r = sub_list[si];
+    const int b = rec.begin[r], e = rec.end[r], m = e - b;
+    const int d0 = rec.depth[r];
+    for (int k = tid; k < m; k += kSubThreads) {
+      S.keys[k] = skey[b + k];
+      const int v = sid[b + k];
+      S.ids[k] = v;
+      S.g[k] = pg[v];
+      S.x[k] = px[v];
+      S.y[k] = py[v];
+    }
+    if (tid == 0) {
+      S.lb[0] = 0;
+      S.le[0] = (short)m;
+      S.ldep[0] = 0;
+      S.lrec[0] = r;
+      S.lsplit[0] = rec.split[r];
+      S.nloc = 1;
+      S.nlvl = 0;
+      S.lvl_start[0] = 0;
+      S.lvl_start[1] = 1;
+      S.ovf = 0;
+    }
+    __syncthreads();
+    // ---- topology, level by level inside the subtree
+    for (int L = 0;; ++L) {
+      const int lo = S.lvl_start[L], hi = S.lvl_start[L + 1];
+      if (lo == hi || S.ovf) break;
+      for (int j = lo + tid; j < hi; j += kSubThreads) {
+        S.lmask[j] = 0;
+        if (!S.lsplit[j]) continue;
+        const int d = d0 + S.ldep[j];
+        if (d >= levels) {
+          S.ovf = 1;
+          continue;
+        }
+        const int shift = 2 * (levels - 1 - d);
+        const int jb = S.lb[j], je = S.le[j];
+        int sb[5] = {jb, jb, jb, jb, je};
+#pragma unroll
+        for (int q = 1; q <= 3; ++q) {
+          int l = jb, h = je;
+          while (l < h) {
+            const int md = (l + h) >> 1;
+            if ((int)((S.keys[md] >> shift) & 3ull) >= q) h = md;
+            else l = md + 1;
+          }
+          sb[q] = l;
+        }
+        int nch = 0;
+        unsigned char mask = 0;
+        for (int q = 0; q < 4; ++q)
+          if (sb[q + 1] > sb[q]) {
+            ++nch;
+            mask |= (unsigned char)(1u << q);
+          }
+        const int first = atomicAdd(&S.nloc, nch);
+        if (first + nch > kSubNodes) {
+          S.ovf = 1;
+          continue;
+        }
+        S.lfirst[j] = (short)first;
+        S.lmask[j] = mask;
+        int c = first;
+        for (int q = 0; q < 4; ++q) {
+          if (!(mask & (1u << q))) continue;
+          const int cnt = sb[q + 1] - sb[q];
+          S.lb[c] = (short)sb[q];
+          S.le[c] = (short)sb[q + 1];
+          S.ldep[c] = (unsigned char)(S.ldep[j] + 1);
+          S.lsplit[c] = (cnt > leaf_cap && d + 1 < kMaxDepth) ? 1 : 0;
+          ++c;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const int nn = min(S.nloc, kSubNodes);
+        S.lvl_start[L + 2] = (short)nn;
+        S.nlvl = L + 1;
+        const int cnt = nn - hi;
+        S.base = cnt ? rec_top + atomicAdd(&st->rec_extra, cnt) : 0;
+        if (S.base + cnt > rec_cap || L + 2 > kSubLevels) S.ovf = 1;
+      }
+      __syncthreads();
+      if (S.ovf) break;
+      // records of the new level; the parents' child pointers
+      for (int j = lo + tid; j < hi; j += kSubThreads) {
+        const int pr = S.lrec[j];
+        const unsigned mask = S.lmask[j];
+        int c = S.lfirst[j];
+        for (int q = 0; q < 4; ++q) {
+          if (!(mask & (1u << q))) {
+            if (S.lsplit[j]) rec.children[4 * pr + q] = -1;
+            continue;
+          }
+          const int cr = S.base + (c - hi);
+          S.lrec[c] = cr;
+          rec.begin[cr] = b + S.lb[c];
+          rec.end[cr] = b + S.le[c];
+          rec.split[cr] = S.lsplit[c];
+          morton_child_geometry(rec, pr, cr, q, d0 + S.ldep[j], false);
+          rec.children[4 * pr + q] = cr;
+          ++c;
+        }
+      }
+      __syncthreads();
+    }
+    if (S.ovf) {
+      if (tid == 0) st->overflow = 1;
+      __syncthreads();
+      continue;
+    }
+    // ---- sums, deepest level first (ids now in aid[], keys no longer needed)
+    for (int L = S.nlvl - 1; L >= 0; --L) {
+      const int lo = S.lvl_start[L], hi = S.lvl_start[L + 1];
+      const int o = L & 1, i = o ^ 1;
+      int* const aid_o = aid_base + o * kSubMax;
+      const int* const aid_i = aid_base + i * kSubMax;
+      // leaves: members by ascending id (a warp per leaf, at most 32 members)
+      for (int j = lo + warp; j < hi; j += nwarp) {
+        if (S.lsplit[j]) continue;
+        const int jb = S.lb[j], jm = S.le[j] - jb;
+        const bool act = lane < jm;
+        const int v = act ? S.ids[jb + lane] : INT_MAX;
+        int rank = 0;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) rank += __shfl_sync(0xffffffffu, v, t) < v;
+        if (act) {
+          aid_o[jb + rank] = v;
+          S.ord[o][jb + rank] = (short)(jb + lane);
+          const int gk = b + jb + rank;
+          perm[gk] = v;
+          sx[gk] = S.x[jb + lane];
+          sy[gk] = S.y[jb + lane];
+          sg[gk] = S.g[jb + lane];
+        }
+      }
+      // internal nodes: merge the children's ascending runs by rank. Work
+      // items are 128-member chunks of the level's internal nodes (so a big
+      // node is spread over all warps); a lane ranks 4 members at once.
+      if (warp == 0) {
+        int carry = 0;
+        for (int j0 = lo; j0 < hi; j0 += 32) {
+          const int j = j0 + lane;
+          const int c = (j < hi && S.lsplit[j]) ? (S.le[j] - S.lb[j] + kMergeChunk - 1) / kMergeChunk : 0;
+          int incl = c;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += t;
+          }
+          if (j < hi) S.cpre[j - lo] = (short)(carry + incl - c);
+          carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) S.cpre[hi - lo] = (short)carry;
+      }
+      __syncthreads();
+      const int n_chunks = S.cpre[hi - lo];
+      for (int w = warp; w < n_chunks; w += nwarp) {
+        int l = 0, h = hi - lo;  // node: last jj with cpre[jj] <= w
+        while (h - l > 1) {
+          const int md = (l + h) >> 1;
+          if (S.cpre[md] <= w) l = md;
+          else h = md;
+        }
+        const int j = lo + l;
+        const int jb = S.lb[j], je = S.le[j];
+        const unsigned mask = S.lmask[j];
+        int rs0, rs1, rs2, rs3, rs4;
+        {
+          int c = S.lfirst[j], cur = jb;
+          rs0 = jb;
+          if (mask & 1u) cur = S.le[c++];
+          rs1 = cur;
+          if (mask & 2u) cur = S.le[c++];
+          rs2 = cur;
+          if (mask & 4u) cur = S.le[c++];
+          rs3 = cur;
+          rs4 = je;
+        }
+        const int t0 = jb + (w - S.cpre[l]) * kMergeChunk;
+        int v[4], tt[4], pos[4], lo4[4][4], len4[4][4];
+        int maxlen = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * 32 + lane;
+          const bool act = t < je && t < t0 + kMergeChunk;
+          tt[u] = act ? t : -1;
+          v[u] = act ? aid_i[t] : 0;
+          const int own = (t >= rs1) + (t >= rs2) + (t >= rs3);
+          const int rb[5] = {rs0, rs1, rs2, rs3, rs4};
+          pos[u] = act ? t - (own == 0 ? rs0 : own == 1 ? rs1 : own == 2 ? rs2 : rs3) : 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            lo4[u][q] = rb[q];
+            len4[u][q] = (act && q != own) ? rb[q + 1] - rb[q] : 0;
+            maxlen = max(maxlen, len4[u][q]);
+          }
+        }
+        while (maxlen > 0) {  // lower bounds of v in the other runs, all searches in step
+          maxlen = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int L4 = len4[u][q];
+              if (L4 > 0) {
+                const int half = L4 >> 1;
+                const bool lt = aid_i[lo4[u][q] + half] < v[u];
+                lo4[u][q] = lt ? lo4[u][q] + half + 1 : lo4[u][q];
+                len4[u][q] = lt ? L4 - half - 1 : half;
+              }
+              maxlen = max(maxlen, len4[u][q]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (tt[u] < 0) continue;
+          const int t = tt[u];
+          const int own = (t >= rs1) + (t >= rs2) + (t >= rs3);
+          const int rb[4] = {rs0, rs1, rs2, rs3};
+          int p = pos[u];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q != own) p += lo4[u][q] - rb[q];
+          aid_o[jb + p] = v[u];
+          S.ord[o][jb + p] = S.ord[i][t];
+        }
+      }
+      __syncthreads();
+      // finish_node chains: small nodes one thread each, large ones lanes 0..4 of a warp
+      for (int j = lo + tid; j < hi; j += kSubThreads) {
+        const int jb = S.lb[j], je = S.le[j];
+        if (je - jb > 64) continue;
+        double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+        for (int t = jb; t < je; ++t) {
+          const int k = S.ord[o][t];
+          const double g = S.g[k], x = S.x[k], y = S.y[k];
+          gs = __dadd_rn(gs, g);
+          wx = __dadd_rn(wx, __dmul_rn(g, x));
+          wy = __dadd_rn(wy, __dmul_rn(g, y));
+          plx = __dadd_rn(plx, x);
+          ply = __dadd_rn(ply, y);
+        }
+        finish_exact(rec, S.lrec[j], b + jb, b + je, gs, wx, wy, plx, ply);
+        if (j == 0) {  // subtree root: raw sums for the large nodes above
+          aux[8 * r] = gs;
+          aux[8 * r + 1] = wx;
+          aux[8 * r + 2] = wy;
+          aux[8 * r + 3] = plx;
+          aux[8 * r + 4] = ply;
+        }
+      }
+      for (int j = lo + warp; j < hi; j += nwarp) {
+        const int jb = S.lb[j], je = S.le[j];
+        if (je - jb <= 64) continue;
+        const double* A = lane == 3 ? S.x : lane == 4 ? S.y : S.g;
+        const double* B = lane == 1 ? S.x : lane == 2 ? S.y : nullptr;
+        double acc = 0.0;
+        if (lane < 5) {
+          int t = jb;
+          for (; t + 8 <= je; t += 8) {
+            double a8[8], b8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int k = S.ord[o][t + u];
+              a8[u] = A[k];
+              b8[u] = B ? B[k] : 1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(a8[u], b8[u]));
+          }
+          for (; t < je; ++t) {
+            const int k = S.ord[o][t];
+            acc = __dadd_rn(acc, __dmul_rn(A[k], B ? B[k] : 1.0));
+          }
+        }
+        const double gs = __shfl_sync(0xffffffffu, acc, 0), wx = __shfl_sync(0xffffffffu, acc, 1),
+                     wy = __shfl_sync(0xffffffffu, acc, 2), plx = __shfl_sync(0xffffffffu, acc, 3),
+                     ply = __shfl_sync(0xffffffffu, acc, 4);
+        if (lane == 0) {
+          finish_exact(rec, S.lrec[j], b + jb, b + je, gs, wx, wy, plx, ply);
+          if (j == 0) {
+            aux[8 * r] = gs;
+            aux[8 * r + 1] = wx;
+            aux[8 * r + 2] = wy;
+            aux[8 * r + 3] = plx;
+            aux[8 * r + 4] = ply;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // Σ|Γ|, Σ|Γx|, Σ|Γy| of the subtree (any fixed order: they only bound
+    // the rounding of the large nodes' sums)
+    {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int k = tid; k < m; k += kSubThreads) {
+        const double g = S.g[k];
+        a0 += fabs(g);
+        a1 += fabs(__dmul_rn(g, S.x[k]));
+        a2 += fabs(__dmul_rn(g, S.y[k]));
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        a0 += __shfl_down_sync(0xffffffffu, a0, off);
+        a1 += __shfl_down_sync(0xffffffffu, a1, off);
+        a2 += __shfl_down_sync(0xffffffffu, a2, off);
+      }
+      if (lane == 0) {
+        s_abs[warp][0] = a0;
+        s_abs[warp][1] = a1;
+        s_abs[warp][2] = a2;
+      }
+      __syncthreads();
+      if (tid < 3) {
+        double t = 0.0;
+        for (int w = 0; w < nwarp; ++w) t += s_abs[w][tid];
+        aux[8 * r + 5 + tid] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Large nodes (> seq_max members) bottom-up from their children's raw sums,
+// one CTA, deepest large level first. Any summation order is within
+// (m-1)u·Σ|a| of the exact sum, as is the reference's sequential order, so the
+// node carries the same certified centroid bound as large_sums_kernel.
+__global__ void __launch_bounds__(1024) morton_large_kernel(TreeRecords rec, const MortonState* __restrict__ st,
+                                                            int seq_max, double* __restrict__ aux) {
+  __shared__ int base[kMaxDepth + 3];
+  if (threadIdx.x == 0) {
+    base[0] = 0;
+    for (int d = 0; d <= kMaxDepth + 1; ++d) base[d + 1] = base[d] + st->lvl_cnt[d];
+  }
+  __syncthreads();
+  for (int d = st->levels_used - 1; d >= 0; --d) {
+    for (int r = base[d] + threadIdx.x; r < base[d + 1]; r += blockDim.x) {
+      const int b = rec.begin[r], e = rec.end[r];
+      if (e - b <= seq_max) continue;
+      double red[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int q = 0; q < 4; ++q) {
+        const int c = rec.children[4 * r + q];
+        if (c < 0) continue;
+        for (int k = 0; k < 8; ++k) red[k] = __dadd_rn(red[k], aux[8 * c + k]);
+      }
+      for (int k = 0; k < 8; ++k) aux[8 * r + k] = red[k];
+      finish_certified(rec, r, b, e, red);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+// Returns false (nothing built) when the Morton path does not apply or
+// overflowed; the caller then runs the level build.
+bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels);
+bool tree_build_morton(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max) {
+  const long long n = t.n;
+  if (leaf_cap > 32 || seq_max > kSubMax || seq_max < leaf_cap) return false;
+  // key depth: the uniform-density depth plus a margin (fewer radix passes);
+  // a tree that needs more levels is rebuilt once with all 32
+  int lg4 = 0;
+  while (lg4 < kMortonLevels && (1LL << (2 * lg4)) * leaf_cap < n) ++lg4;
+  const int levels = std::min(kMortonLevels, std::max(8, lg4 + 10));
+  return tree_build_morton_levels(ctx, t, leaf_cap, seq_max, levels) ||
+         (levels < kMortonLevels && tree_build_morton_levels(ctx, t, leaf_cap, seq_max, kMortonLevels));
+}
+
+bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels) {
+  const long long n = t.n;
+  cudaStream_t s = ctx->stream;
+
+  // ---- root (device-side hull finish, no host round trip)
+  const int hb = std::min<long long>((n + kThreads - 1) / kThreads, 256);
+  double* hull = dalloc<double>(4 * hb);
+  hull_kernel<<<hb, kThreads, 0, s>>>(n, t.px, t.py, hull);
+  PTROM_LAUNCH_CHECK();
+  const long long est = 4 * ((2 * n) / std::max<long long>(1, leaf_cap) + 64);
+  const int rec_cap = (int)std::min<long long>(est, INT_MAX / 8);
+  TreeRecords rec;
+  rec.alloc((size_t)rec_cap);
+  MortonState* st = dalloc<MortonState>(1);
+  PTROM_CUDA(cudaMemsetAsync(st, 0, sizeof(MortonState), s));
+  morton_root_kernel<<<1, 32, 0, s>>>(hb, hull, n, leaf_cap, rec, st);
+  PTROM_LAUNCH_CHECK();
+
+  // ---- keys and the stable sort
+  unsigned long long *key = dalloc<unsigned long long>(n), *skey = dalloc<unsigned long long>(n);
+  int *ids = dalloc<int>(n), *sid = dalloc<int>(n);
+  morton_keys_kernel<<<grid_for(ctx, n), kThreads, 0, s>>>(n, t.px, t.py, rec, levels, key, ids);
+  PTROM_LAUNCH_CHECK();
+  size_t sort_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, skey, ids, sid, (int)n, 0, 2 * levels, s);
+  void* stmp = dalloc<char>(sort_bytes + 256);
+  PTROM_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sort_bytes, key, skey, ids, sid, (int)n, 0, 2 * levels, s));
+
+  // ---- large nodes level by level
+  const long long max_large = (long long)(kMaxDepth + 1) * (n / std::max(1, seq_max) + 2);
+  int* sub_list = dalloc<int>(std::min<long long>(rec_cap, 4 * max_large + 4));
+  int* large_list = dalloc<int>(max_large);
+  {
+    int occ = 0;
+    PTROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, morton_levels_kernel, kThreads, 0));
+    // few large nodes per level: a small grid keeps the grid barrier cheap
+    const int grid = std::min(ctx->num_sms * std::max(1, occ), 32);
+    void* args[] = {(void*)&skey, (void*)&levels, (void*)&leaf_cap, (void*)&seq_max, (void*)&rec,
+                    (void*)&rec_cap, (void*)&st, (void*)&sub_list, (void*)&large_list};
+    PTROM_CUDA(cudaLaunchCooperativeKernel((void*)morton_levels_kernel, grid, kThreads, args, 0, s));
+  }
+  double* aux = nullptr;
+  MortonState* h_st = reinterpret_cast<MortonState*>(ctx->h_counts);
+  static_assert(sizeof(MortonState) <= 512, "pinned scratch");
+  auto read_state = [&]() {
+    PTROM_CUDA(cudaMemcpyAsync(h_st, st, sizeof(MortonState), cudaMemcpyDeviceToHost, s));
+    PTROM_CUDA(cudaStreamSynchronize(s));
+    return *h_st;
+  };
+  MortonState hs = read_state();
+  auto release = [&]() {
+    void* frees[] = {hull, st, key, skey, ids, sid, stmp, sub_list, large_list, aux};
+    for (void* p : frees) dfree(p);
+  };
+  if (!hs.finite) {
+    release();
+    rec.free();
+    config_fail("build_tree: non-finite input");
+  }
+  if (hs.overflow) {
+    release();
+    rec.free();
+    return false;
+  }
+  int R_top = 0;
+  for (int d = 0; d <= kMaxDepth + 1; ++d) R_top += hs.lvl_cnt[d];
+  t.root_width = hs.width;
+
+  // ---- subtrees of at most seq_max members: topology, leaf order, exact sums
+  int* perm = dalloc<int>(n);
+  double *sx = dalloc<double>(n), *sy = dalloc<double>(n), *sg = dalloc<double>(n);
+  aux = dalloc<double>(8 * (size_t)R_top);  // raw sums of the subtree roots and large nodes
+  {
+    static bool attr = false;
+    if (!attr) {
+      PTROM_CUDA(cudaFuncSetAttribute(morton_subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(SubSmem)));
+      attr = true;
+    }
+    const int nb = std::max(1, std::min(hs.sub_count, ctx->num_sms * 2));
+    morton_subtree_kernel<<<nb, kSubThreads, sizeof(SubSmem), s>>>(skey, sid, t.px, t.py, t.g, sub_list, st, rec,
+                                                                   rec_cap, R_top, levels, leaf_cap, perm, sx, sy,
+                                                                   sg, aux);
+    PTROM_LAUNCH_CHECK();
+  }
+  if (hs.large_count > 0) {
+    morton_large_kernel<<<1, 1024, 0, s>>>(rec, st, seq_max, aux);
+    PTROM_LAUNCH_CHECK();
+  }
+  hs = read_state();
+  if (hs.overflow) {
+    dfree(perm);
+    dfree(sx);
+    dfree(sy);
+    dfree(sg);
+    release();
+    rec.free();
+    return false;
+  }
+  const int R = R_top + hs.rec_extra;
+  finish_tree(ctx, t, rec, R, perm, sx, sy, sg);
+  ctx->tree_stats.levels = hs.levels_used;
+  release();
+  rec.free();
+  return true;
 }
 
 // Computes exact sums for nodes flagged need_exact; returns how many.

@@ -147,6 +147,13 @@ int ptrom_tree_stats(ptrom_ctx* ctx, double* build_ms, double* eval_ms, uint64_t
   });
 }
 
+int ptrom_tree_build_info(ptrom_ctx* ctx, int* morton, int* levels) {
+  return guarded(ctx, [&] {
+    if (morton) *morton = ctx->tree_stats.morton;
+    if (levels) *levels = (int)ctx->tree_stats.levels;
+  });
+}
+
 int64_t ptrom_tree_num_nodes(const ptrom_tree* tree) { return tree ? (int64_t)tree->t.nodes.count : 0; }
 
 int ptrom_tree_export(ptrom_ctx* ctx, const ptrom_tree* tree, double* bounds, double* width, double* centroid,

@@ -297,3 +297,86 @@ def test_sharded_barnes_hut_slots_equal_full_evaluation(pt, oracle, n, shards):
         ot = oracle.Tree(w.x0[:n], w.x0[n:], w.gamma, 32)
         np.testing.assert_array_equal(perm.cpu().numpy(), ot.perm)
         assert rel(full.cpu().numpy(), ot.bh_velocity(w.x0, w.gamma, w.delta, 0, 0.5)) <= 1e-12
+
+
+def build_info(ctx):
+    import ctypes
+    m, lv = ctypes.c_int(), ctypes.c_int()
+    ctx.check(ctx.lib.ptrom_tree_build_info(ctx.handle, ctypes.byref(m), ctypes.byref(lv)))
+    return m.value, lv.value
+
+
+@pytest.mark.parametrize("case", ["config3", "uniform", "clustered", "cap4_distinct", "seq64"])
+def test_morton_build_equals_level_build(pt, case):
+    """The Morton-key build and the level-by-level build produce the same
+    tree bit for bit (every exported array, sums included), and the Morton
+    path is the one taken for these inputs."""
+    import paper_2103_01983_b200 as ptm
+    from paper_2103_01983_b200.tree import QuadTree
+    rng = np.random.default_rng(7)
+    cap = 32
+    if case == "config3":
+        w = workloads.config3(n=200_000)
+        px, py, g = w.x0[:w.n], w.x0[w.n:], w.gamma
+    elif case == "uniform":
+        n = 100_003
+        px, py, g = rng.uniform(-3, 5, n), rng.uniform(-1, 1, n), rng.normal(0, 1, n)
+    elif case == "clustered":
+        n = 150_000
+        c = rng.integers(0, 6, n)
+        px = rng.normal(0, 0.02, n) + c * 0.3
+        py = rng.normal(0, 0.02, n) - c * 0.1
+        g = rng.uniform(-1, 1, n)
+    elif case == "cap4_distinct":
+        n, cap = 20_000, 4
+        px, py, g = rng.uniform(0, 1, n), rng.uniform(0, 1, n), rng.uniform(0.5, 1.5, n)
+    else:  # small exact-sum threshold: many large (certified) levels
+        n, cap = 50_000, 8
+        px, py, g = rng.normal(0, 1, n), rng.normal(0, 1, n), rng.uniform(0.5, 1.5, n)
+    seq = "64" if case == "seq64" else None
+    if seq:
+        os.environ["PTROM_TREE_SEQ_MAX"] = seq
+    try:
+        ctx_m = ptm.Context(0)
+    finally:
+        os.environ.pop("PTROM_TREE_SEQ_MAX", None)
+    tm = QuadTree(px, py, g, cap, ctx=ctx_m)
+    morton, levels = build_info(ctx_m)
+    assert morton == 1 and levels > 1
+    os.environ["PTROM_TREE_BUILD"] = "levels"
+    if seq:
+        os.environ["PTROM_TREE_SEQ_MAX"] = seq
+    try:
+        ctx_l = ptm.Context(0)
+    finally:
+        del os.environ["PTROM_TREE_BUILD"]
+        os.environ.pop("PTROM_TREE_SEQ_MAX", None)
+    tl = QuadTree(px, py, g, cap, ctx=ctx_l)
+    assert build_info(ctx_l)[0] == 0
+    em, el = tm.export(), tl.export()
+    assert tm.num_nodes == tl.num_nodes
+    assert set(em) == set(el)
+    # nodes above seq_max take certified block sums whose order follows each
+    # build's member layout: equal within the certified bound, not bitwise
+    small = (el["end"] - el["begin"]) <= int(seq or 2048)
+    for k in em:
+        if k in ("gamma_sum", "centroid"):
+            np.testing.assert_array_equal(em[k][small], el[k][small], err_msg=k)
+            np.testing.assert_allclose(em[k][~small], el[k][~small], rtol=1e-12, atol=1e-15, err_msg=k)
+        else:
+            np.testing.assert_array_equal(em[k], el[k], err_msg=k)
+
+
+def test_morton_build_falls_back_on_deep_trees(pt, oracle):
+    """Coincident points with leaf_capacity 1 need the depth-64 guard, deeper
+    than the 32 key levels: the level build takes over, same tree."""
+    from paper_2103_01983_b200.tree import QuadTree
+    rng = np.random.default_rng(3)
+    n = 300
+    px, py = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+    px[10:14] = px[9]
+    py[10:14] = py[9]
+    g = rng.uniform(0.5, 1.5, n)
+    gt = QuadTree(px, py, g, 1)
+    assert build_info(gt.ctx)[0] == 0
+    assert_same_tree(gt, oracle.Tree(px, py, g, 1))
