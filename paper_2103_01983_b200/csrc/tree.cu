@@ -31,6 +31,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -1004,10 +1006,11 @@ namespace {
 
 constexpr int kMortonLevels = 32;
 constexpr int kSubMax = 2048;     // members of a subtree (seq_max <= kSubMax)
-constexpr int kSubNodes = 2048;   // local nodes of a subtree
+constexpr int kSubNodes = 1024;   // local nodes of a subtree
 constexpr int kSubThreads = 256;
 constexpr int kSubLevels = 64;
-constexpr int kMergeChunk = 128;
+constexpr int kListShorts = 25600;  // ascending-id lists of all local levels, level L at L*m (shared memory)
+constexpr int kThreadChain = 256;  // chains of nodes up to this size run in one thread
 
 struct MortonState {
   int lvl_cnt[kMaxDepth + 2];  // records per level of the large-node pass (level 0 = root)
@@ -1222,30 +1225,43 @@ __global__ void __launch_bounds__(kThreads) morton_levels_kernel(const unsigned 
 }
 
 // Shared-memory layout of one subtree CTA.
+using SubIdSort = cub::BlockRadixSort<unsigned, kSubThreads, kSubMax / kSubThreads, short>;
 struct SubSmem {
-  unsigned long long keys[kSubMax];  // topology phase; aid[] in the sums phase
-  int ids[kSubMax];
+  union {
+    unsigned long long keys[kSubMax];     // topology phase
+    typename SubIdSort::TempStorage sort;  // member ids -> ascending order
+    short lists[kListShorts];             // ascending-id member list of every node, level L at L*m
+  } u;
   double g[kSubMax], x[kSubMax], y[kSubMax];
-  short ord[2][kSubMax];             // ascending-id order (local member index), ping-pong by level
-  short lb[kSubNodes], le[kSubNodes];
-  int lrec[kSubNodes];
-  short lfirst[kSubNodes];
-  unsigned char ldep[kSubNodes], lsplit[kSubNodes], lmask[kSubNodes];
+  short lb[kSubNodes], le[kSubNodes];  // local node ranges (member positions in key order)
+  short lfirst[kSubNodes], lpar[kSubNodes];
+  unsigned char ldep[kSubNodes], lsplit[kSubNodes], lmask[kSubNodes], lq[kSubNodes];
   short lvl_start[kSubLevels + 2];
-  short cpre[kSubNodes + 1];         // merge work list: chunk prefix over one level's nodes
   int nloc, nlvl, base, ovf;
 };
 
-// One CTA per subtree root (see the section comment).
+// One CTA per subtree root (see the section comment). Phases:
+//  1. members (key, id, Γ, x, y) into shared memory;
+//  2. local topology level by level (binary searches for the digit changes);
+//  3. one record allocation for the subtree, records written in parallel
+//     (geometry replayed from the subtree root down each node's path);
+//  4. members sorted by id (bitonic, shared memory): the root's ascending-id
+//     list; each level's lists are stably partitioned into the children's
+//     (ballots), kept per level in global scratch `lists`;
+//  5. finish_node's chains for every node over its list in one parallel pass
+//     (a thread per node up to 64 members, lanes 0..4 of a warp above), and
+//     the leaves' members into perm / sx / sy / sg.
 __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
     const unsigned long long* __restrict__ skey, const int* __restrict__ sid, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pg, const int* __restrict__ sub_list,
-    MortonState* st, TreeRecords rec, int rec_cap, int rec_top, int levels, long long leaf_cap, int* __restrict__ perm,
-    double* __restrict__ sx, double* __restrict__ sy, double* __restrict__ sg, double* __restrict__ aux) {
+    MortonState* st, TreeRecords rec, int rec_cap, int rec_top, int levels, long long leaf_cap, int id_bits,
+    int* __restrict__ perm, double* __restrict__ sx, double* __restrict__ sy,
+    double* __restrict__ sg, double* __restrict__ aux, long long* __restrict__ prof) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_abs[kSubThreads / 32][3];
   SubSmem& S = *reinterpret_cast<SubSmem*>(smem_raw);
-  int* const aid_base = reinterpret_cast<int*>(S.keys);  // two kSubMax id buffers
+#define SUBPROF(ph)                                                          \
+  if (prof && tid == 0) prof[(long long)si * 10 + (ph)] = clock64();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarp = kSubThreads / 32;
   const int n_sub = st->sub_count;
@@ -1253,20 +1269,34 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
     const int r = sub_list[si];
     const int b = rec.begin[r], e = rec.end[r], m = e - b;
     const int d0 = rec.depth[r];
-    for (int k = tid; k < m; k += kSubThreads) {
-      S.keys[k] = skey[b + k];
-      const int v = sid[b + k];
-      S.ids[k] = v;
-      S.g[k] = pg[v];
-      S.x[k] = px[v];
-      S.y[k] = py[v];
+    SUBPROF(0)
+    // ---- 1. members
+    {
+      constexpr int IPT = kSubMax / kSubThreads;
+      int v[IPT];
+#pragma unroll
+      for (int u = 0; u < IPT; ++u) {
+        const int k = u * kSubThreads + tid;
+        v[u] = k < m ? sid[b + k] : -1;
+        if (k < m) S.u.keys[k] = skey[b + k];
+      }
+#pragma unroll
+      for (int u = 0; u < IPT; ++u) {
+        const int k = u * kSubThreads + tid;
+        if (v[u] >= 0) {
+          S.g[k] = pg[v[u]];
+          S.x[k] = px[v[u]];
+          S.y[k] = py[v[u]];
+        }
+      }
     }
     if (tid == 0) {
       S.lb[0] = 0;
       S.le[0] = (short)m;
       S.ldep[0] = 0;
-      S.lrec[0] = r;
       S.lsplit[0] = rec.split[r];
+      S.lpar[0] = -1;
+      S.lq[0] = 0;
       S.nloc = 1;
       S.nlvl = 0;
       S.lvl_start[0] = 0;
@@ -1274,7 +1304,8 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
       S.ovf = 0;
     }
     __syncthreads();
-    // ---- topology, level by level inside the subtree
+    SUBPROF(1)
+    // ---- 2. topology, level by level inside the subtree
     for (int L = 0;; ++L) {
       const int lo = S.lvl_start[L], hi = S.lvl_start[L + 1];
       if (lo == hi || S.ovf) break;
@@ -1294,13 +1325,14 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
           int l = jb, h = je;
           while (l < h) {
             const int md = (l + h) >> 1;
-            if ((int)((S.keys[md] >> shift) & 3ull) >= q) h = md;
+            if ((int)((S.u.keys[md] >> shift) & 3ull) >= q) h = md;
             else l = md + 1;
           }
           sb[q] = l;
         }
         int nch = 0;
         unsigned char mask = 0;
+#pragma unroll
         for (int q = 0; q < 4; ++q)
           if (sb[q + 1] > sb[q]) {
             ++nch;
@@ -1314,6 +1346,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
         S.lfirst[j] = (short)first;
         S.lmask[j] = mask;
         int c = first;
+#pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (!(mask & (1u << q))) continue;
           const int cnt = sb[q + 1] - sb[q];
@@ -1321,6 +1354,8 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
           S.le[c] = (short)sb[q + 1];
           S.ldep[c] = (unsigned char)(S.ldep[j] + 1);
           S.lsplit[c] = (cnt > leaf_cap && d + 1 < kMaxDepth) ? 1 : 0;
+          S.lpar[c] = (short)j;
+          S.lq[c] = (unsigned char)q;
           ++c;
         }
       }
@@ -1329,185 +1364,163 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
         const int nn = min(S.nloc, kSubNodes);
         S.lvl_start[L + 2] = (short)nn;
         S.nlvl = L + 1;
-        const int cnt = nn - hi;
-        S.base = cnt ? rec_top + atomicAdd(&st->rec_extra, cnt) : 0;
-        if (S.base + cnt > rec_cap || L + 2 > kSubLevels) S.ovf = 1;
-      }
-      __syncthreads();
-      if (S.ovf) break;
-      // records of the new level; the parents' child pointers
-      for (int j = lo + tid; j < hi; j += kSubThreads) {
-        const int pr = S.lrec[j];
-        const unsigned mask = S.lmask[j];
-        int c = S.lfirst[j];
-        for (int q = 0; q < 4; ++q) {
-          if (!(mask & (1u << q))) {
-            if (S.lsplit[j]) rec.children[4 * pr + q] = -1;
-            continue;
-          }
-          const int cr = S.base + (c - hi);
-          S.lrec[c] = cr;
-          rec.begin[cr] = b + S.lb[c];
-          rec.end[cr] = b + S.le[c];
-          rec.split[cr] = S.lsplit[c];
-          morton_child_geometry(rec, pr, cr, q, d0 + S.ldep[j], false);
-          rec.children[4 * pr + q] = cr;
-          ++c;
-        }
+        if (L + 2 > kSubLevels || (long long)(L + 2) * m > kListShorts) S.ovf = 1;
       }
       __syncthreads();
     }
+    SUBPROF(2)
+    // ---- 3. records
+    if (tid == 0 && !S.ovf) {
+      const int extra = S.nloc - 1;
+      S.base = extra ? rec_top + atomicAdd(&st->rec_extra, extra) : 0;
+      if (S.base + extra > rec_cap) S.ovf = 1;
+    }
+    __syncthreads();
     if (S.ovf) {
       if (tid == 0) st->overflow = 1;
       __syncthreads();
       continue;
     }
-    // ---- sums, deepest level first (ids now in aid[], keys no longer needed)
-    for (int L = S.nlvl - 1; L >= 0; --L) {
-      const int lo = S.lvl_start[L], hi = S.lvl_start[L + 1];
-      const int o = L & 1, i = o ^ 1;
-      int* const aid_o = aid_base + o * kSubMax;
-      const int* const aid_i = aid_base + i * kSubMax;
-      // leaves: members by ascending id (a warp per leaf, at most 32 members)
-      for (int j = lo + warp; j < hi; j += nwarp) {
-        if (S.lsplit[j]) continue;
-        const int jb = S.lb[j], jm = S.le[j] - jb;
-        const bool act = lane < jm;
-        const int v = act ? S.ids[jb + lane] : INT_MAX;
-        int rank = 0;
-#pragma unroll
-        for (int t = 0; t < 32; ++t) rank += __shfl_sync(0xffffffffu, v, t) < v;
-        if (act) {
-          aid_o[jb + rank] = v;
-          S.ord[o][jb + rank] = (short)(jb + lane);
-          const int gk = b + jb + rank;
-          perm[gk] = v;
-          sx[gk] = S.x[jb + lane];
-          sy[gk] = S.y[jb + lane];
-          sg[gk] = S.g[jb + lane];
-        }
-      }
-      // internal nodes: merge the children's ascending runs by rank. Work
-      // items are 128-member chunks of the level's internal nodes (so a big
-      // node is spread over all warps); a lane ranks 4 members at once.
-      if (warp == 0) {
-        int carry = 0;
-        for (int j0 = lo; j0 < hi; j0 += 32) {
-          const int j = j0 + lane;
-          const int c = (j < hi && S.lsplit[j]) ? (S.le[j] - S.lb[j] + kMergeChunk - 1) / kMergeChunk : 0;
-          int incl = c;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += t;
+    const int nloc = S.nloc, base = S.base;
+    auto rid = [&](int j) { return j == 0 ? r : base + j - 1; };
+    {
+      const double r0 = rec.bounds[4 * r], r1 = rec.bounds[4 * r + 1], r2 = rec.bounds[4 * r + 2],
+                   r3 = rec.bounds[4 * r + 3], rw = rec.width[r];
+      for (int j = tid; j < nloc; j += kSubThreads) {
+        const int me = rid(j);
+        if (j > 0) {
+          // path quadrants from the subtree root, then the reference's halvings
+          unsigned long long path = 0;
+          int depth = 0;
+          for (int c = j; c > 0; c = S.lpar[c]) {
+            path |= (unsigned long long)S.lq[c] << (2 * depth);
+            ++depth;
           }
-          if (j < hi) S.cpre[j - lo] = (short)(carry + incl - c);
-          carry += __shfl_sync(0xffffffffu, incl, 31);
+          double b0 = r0, b1 = r1, b2 = r2, b3 = r3, w = rw;
+          for (int l = depth - 1; l >= 0; --l) {
+            const int q = (int)((path >> (2 * l)) & 3ull);
+            const double cx = __dmul_rn(__dadd_rn(b0, b1), 0.5), cy = __dmul_rn(__dadd_rn(b2, b3), 0.5);
+            if (q & 1) b0 = cx; else b1 = cx;
+            if (q & 2) b2 = cy; else b3 = cy;
+            w = __ddiv_rn(w, 2.0);
+          }
+          rec.bounds[4 * me] = b0;
+          rec.bounds[4 * me + 1] = b1;
+          rec.bounds[4 * me + 2] = b2;
+          rec.bounds[4 * me + 3] = b3;
+          rec.mid[2 * me] = __dmul_rn(__dadd_rn(b0, b1), 0.5);
+          rec.mid[2 * me + 1] = __dmul_rn(__dadd_rn(b2, b3), 0.5);
+          rec.width[me] = w;
+          rec.depth[me] = d0 + S.ldep[j];
+          rec.begin[me] = b + S.lb[j];
+          rec.end[me] = b + S.le[j];
+          rec.split[me] = S.lsplit[j];
         }
-        if (lane == 0) S.cpre[hi - lo] = (short)carry;
-      }
-      __syncthreads();
-      const int n_chunks = S.cpre[hi - lo];
-      for (int w = warp; w < n_chunks; w += nwarp) {
-        int l = 0, h = hi - lo;  // node: last jj with cpre[jj] <= w
-        while (h - l > 1) {
-          const int md = (l + h) >> 1;
-          if (S.cpre[md] <= w) l = md;
-          else h = md;
-        }
-        const int j = lo + l;
-        const int jb = S.lb[j], je = S.le[j];
-        const unsigned mask = S.lmask[j];
-        int rs0, rs1, rs2, rs3, rs4;
-        {
-          int c = S.lfirst[j], cur = jb;
-          rs0 = jb;
-          if (mask & 1u) cur = S.le[c++];
-          rs1 = cur;
-          if (mask & 2u) cur = S.le[c++];
-          rs2 = cur;
-          if (mask & 4u) cur = S.le[c++];
-          rs3 = cur;
-          rs4 = je;
-        }
-        const int t0 = jb + (w - S.cpre[l]) * kMergeChunk;
-        int v[4], tt[4], pos[4], lo4[4][4], len4[4][4];
-        int maxlen = 0;
+        const unsigned mask = S.lsplit[j] ? S.lmask[j] : 0u;
+        int c = S.lfirst[j];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int t = t0 + u * 32 + lane;
-          const bool act = t < je && t < t0 + kMergeChunk;
-          tt[u] = act ? t : -1;
-          v[u] = act ? aid_i[t] : 0;
-          const int own = (t >= rs1) + (t >= rs2) + (t >= rs3);
-          const int rb[5] = {rs0, rs1, rs2, rs3, rs4};
-          pos[u] = act ? t - (own == 0 ? rs0 : own == 1 ? rs1 : own == 2 ? rs2 : rs3) : 0;
+        for (int q = 0; q < 4; ++q) rec.children[4 * me + q] = (mask & (1u << q)) ? rid(c++) : -1;
+      }
+    }
+    SUBPROF(3)
+    // ---- 4. ascending-id lists: radix sort of the member ids (block-wide),
+    // then stable partitions level by level into the children's ranges
+    {
+      constexpr int IPT = kSubMax / kSubThreads;
+      unsigned kk[IPT];
+      short vv[IPT];
+      const unsigned pad = id_bits >= 32 ? 0xffffffffu : ((1u << id_bits) - 1u);
+#pragma unroll
+      for (int u = 0; u < IPT; ++u) {
+        const int k = tid * IPT + u;
+        kk[u] = k < m ? (unsigned)sid[b + k] : pad;  // pads sort after every member (stable)
+        vv[u] = (short)k;
+      }
+      __syncthreads();  // keys of the topology phase are dead
+      SubIdSort(S.u.sort).Sort(kk, vv, 0, id_bits);
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < IPT; ++u)
+        if (tid * IPT + u < m) S.u.lists[tid * IPT + u] = vv[u];
+    }
+    __syncthreads();
+    SUBPROF(4)
+    for (int L = 0; L + 1 < S.nlvl; ++L) {
+      const short* src = S.u.lists + L * m;
+      short* dst = S.u.lists + (L + 1) * m;
+      for (int j = S.lvl_start[L] + warp; j < S.lvl_start[L + 1]; j += nwarp) {
+        if (!S.lsplit[j]) continue;
+        const unsigned mask = S.lmask[j];
+        int rs1 = 0, rs2 = 0, rs3 = 0, cb[4];
+        {
+          int c = S.lfirst[j], cur = S.lb[j];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            lo4[u][q] = rb[q];
-            len4[u][q] = (act && q != own) ? rb[q + 1] - rb[q] : 0;
-            maxlen = max(maxlen, len4[u][q]);
+            cb[q] = cur;
+            if (mask & (1u << q)) cur = S.le[c++];
+            if (q == 0) rs1 = cur;
+            if (q == 1) rs2 = cur;
+            if (q == 2) rs3 = cur;
           }
         }
-        while (maxlen > 0) {  // lower bounds of v in the other runs, all searches in step
-          maxlen = 0;
+        const int jb = S.lb[j], je = S.le[j];
+        for (int t0 = jb; t0 < je; t0 += 32) {
+          const int t = t0 + lane;
+          const bool act = t < je;
+          const int k = act ? src[t] : 0;
+          const int q = (k >= rs1) + (k >= rs2) + (k >= rs3);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int L4 = len4[u][q];
-              if (L4 > 0) {
-                const int half = L4 >> 1;
-                const bool lt = aid_i[lo4[u][q] + half] < v[u];
-                lo4[u][q] = lt ? lo4[u][q] + half + 1 : lo4[u][q];
-                len4[u][q] = lt ? L4 - half - 1 : half;
-              }
-              maxlen = max(maxlen, len4[u][q]);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (tt[u] < 0) continue;
-          const int t = tt[u];
-          const int own = (t >= rs1) + (t >= rs2) + (t >= rs3);
-          const int rb[4] = {rs0, rs1, rs2, rs3};
-          int p = pos[u];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q != own) p += lo4[u][q] - rb[q];
-          aid_o[jb + p] = v[u];
-          S.ord[o][jb + p] = S.ord[i][t];
+          for (int qq = 0; qq < 4; ++qq) {
+            const unsigned bal = __ballot_sync(0xffffffffu, act && q == qq);
+            if (act && q == qq) dst[cb[qq] + __popc(bal & ((1u << lane) - 1u))] = (short)k;
+            cb[qq] += __popc(bal);
+          }
         }
       }
       __syncthreads();
-      // finish_node chains: small nodes one thread each, large ones lanes 0..4 of a warp
-      for (int j = lo + tid; j < hi; j += kSubThreads) {
-        const int jb = S.lb[j], je = S.le[j];
-        if (je - jb > 64) continue;
-        double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
-        for (int t = jb; t < je; ++t) {
-          const int k = S.ord[o][t];
-          const double g = S.g[k], x = S.x[k], y = S.y[k];
-          gs = __dadd_rn(gs, g);
-          wx = __dadd_rn(wx, __dmul_rn(g, x));
-          wy = __dadd_rn(wy, __dmul_rn(g, y));
-          plx = __dadd_rn(plx, x);
-          ply = __dadd_rn(ply, y);
-        }
-        finish_exact(rec, S.lrec[j], b + jb, b + je, gs, wx, wy, plx, ply);
-        if (j == 0) {  // subtree root: raw sums for the large nodes above
-          aux[8 * r] = gs;
-          aux[8 * r + 1] = wx;
-          aux[8 * r + 2] = wy;
-          aux[8 * r + 3] = plx;
-          aux[8 * r + 4] = ply;
+    }
+    SUBPROF(5)
+    // ---- 5. finish_node chains over the ascending lists: a thread per node
+    // up to kThreadChain members (the five chains interleaved), lanes 0..4 of
+    // a warp above; leaves' members into perm / sx / sy / sg
+    for (int j = tid; j < nloc; j += kSubThreads) {
+      const int jb = S.lb[j], je = S.le[j];
+      if (je - jb > kThreadChain) continue;
+      const short* l = S.u.lists + S.ldep[j] * m;
+      const bool leaf = !S.lsplit[j];
+      double gs = 0.0, wx = 0.0, wy = 0.0, plx = 0.0, ply = 0.0;
+#pragma unroll 4
+      for (int t = jb; t < je; ++t) {
+        const int k = l[t];
+        const double g = S.g[k], x = S.x[k], y = S.y[k];
+        gs = __dadd_rn(gs, g);
+        wx = __dadd_rn(wx, __dmul_rn(g, x));
+        wy = __dadd_rn(wy, __dmul_rn(g, y));
+        plx = __dadd_rn(plx, x);
+        ply = __dadd_rn(ply, y);
+        if (leaf) {
+          perm[b + t] = sid[b + k];
+          sx[b + t] = x;
+          sy[b + t] = y;
+          sg[b + t] = g;
         }
       }
-      for (int j = lo + warp; j < hi; j += nwarp) {
+      finish_exact(rec, rid(j), b + jb, b + je, gs, wx, wy, plx, ply);
+      if (j == 0) {  // subtree root: raw sums for the large nodes above
+        aux[8 * r] = gs;
+        aux[8 * r + 1] = wx;
+        aux[8 * r + 2] = wy;
+        aux[8 * r + 3] = plx;
+        aux[8 * r + 4] = ply;
+      }
+    }
+    {
+      const double* A = lane == 3 ? S.x : lane == 4 ? S.y : S.g;
+      const double* B = lane == 1 ? S.x : lane == 2 ? S.y : nullptr;
+      for (int j = warp; j < nloc; j += nwarp) {
         const int jb = S.lb[j], je = S.le[j];
-        if (je - jb <= 64) continue;
-        const double* A = lane == 3 ? S.x : lane == 4 ? S.y : S.g;
-        const double* B = lane == 1 ? S.x : lane == 2 ? S.y : nullptr;
+        if (je - jb <= kThreadChain) continue;
+        const short* l = S.u.lists + S.ldep[j] * m;
         double acc = 0.0;
         if (lane < 5) {
           int t = jb;
@@ -1515,7 +1528,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
             double a8[8], b8[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              const int k = S.ord[o][t + u];
+              const int k = l[t + u];
               a8[u] = A[k];
               b8[u] = B ? B[k] : 1.0;
             }
@@ -1523,7 +1536,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
             for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(a8[u], b8[u]));
           }
           for (; t < je; ++t) {
-            const int k = S.ord[o][t];
+            const int k = l[t];
             acc = __dadd_rn(acc, __dmul_rn(A[k], B ? B[k] : 1.0));
           }
         }
@@ -1531,7 +1544,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
                      wy = __shfl_sync(0xffffffffu, acc, 2), plx = __shfl_sync(0xffffffffu, acc, 3),
                      ply = __shfl_sync(0xffffffffu, acc, 4);
         if (lane == 0) {
-          finish_exact(rec, S.lrec[j], b + jb, b + je, gs, wx, wy, plx, ply);
+          finish_exact(rec, rid(j), b + jb, b + je, gs, wx, wy, plx, ply);
           if (j == 0) {
             aux[8 * r] = gs;
             aux[8 * r + 1] = wx;
@@ -1541,8 +1554,9 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
           }
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
+    SUBPROF(6)
     // Σ|Γ|, Σ|Γx|, Σ|Γy| of the subtree (any fixed order: they only bound
     // the rounding of the large nodes' sums)
     {
@@ -1572,7 +1586,13 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
       }
       __syncthreads();
     }
+    SUBPROF(7)
+    if (prof && tid == 0) {
+      prof[(long long)si * 10 + 8] = m;
+      prof[(long long)si * 10 + 9] = (long long)S.nloc * 100 + S.nlvl;
+    }
   }
+#undef SUBPROF
 }
 
 // Large nodes (> seq_max members) bottom-up from their children's raw sums,
@@ -1701,10 +1721,26 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
       attr = true;
     }
     const int nb = std::max(1, std::min(hs.sub_count, ctx->num_sms * 2));
+    int id_bits = 1;
+    while (id_bits < 31 && (1LL << id_bits) <= n) ++id_bits;
+    static const bool sub_prof = std::getenv("PTROM_SUBTREE_PROFILE") != nullptr;
+    long long* prof = sub_prof ? dalloc<long long>((size_t)hs.sub_count * 10) : nullptr;
     morton_subtree_kernel<<<nb, kSubThreads, sizeof(SubSmem), s>>>(skey, sid, t.px, t.py, t.g, sub_list, st, rec,
-                                                                   rec_cap, R_top, levels, leaf_cap, perm, sx, sy,
-                                                                   sg, aux);
+                                                                   rec_cap, R_top, levels, leaf_cap, id_bits, perm,
+                                                                   sx, sy, sg, aux, prof);
     PTROM_LAUNCH_CHECK();
+    if (prof) {
+      std::vector<long long> hp((size_t)hs.sub_count * 10);
+      PTROM_CUDA(cudaMemcpyAsync(hp.data(), prof, hp.size() * 8, cudaMemcpyDeviceToHost, s));
+      PTROM_CUDA(cudaStreamSynchronize(s));
+      if (FILE* f = std::fopen("gpurun_out/subtree_prof.csv", "w")) {
+        for (int i = 0; i < hs.sub_count; ++i) {
+          for (int k = 0; k < 10; ++k) std::fprintf(f, "%lld%c", hp[10 * i + k], k == 9 ? '\n' : ',');
+        }
+        std::fclose(f);
+      }
+      dfree(prof);
+    }
   }
   if (hs.large_count > 0) {
     morton_large_kernel<<<1, 1024, 0, s>>>(rec, st, seq_max, aux);
