@@ -1254,7 +1254,7 @@ struct SubSmem {
 __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
     const unsigned long long* __restrict__ skey, const int* __restrict__ sid, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pg, const int* __restrict__ sub_list,
-    MortonState* st, TreeRecords rec, int rec_cap, int rec_top, int levels, long long leaf_cap, int id_bits,
+    MortonState* st, TreeRecords rec, int rec_cap, int levels, long long leaf_cap, int id_bits,
     int* __restrict__ perm, double* __restrict__ sx, double* __restrict__ sy,
     double* __restrict__ sg, double* __restrict__ aux, long long* __restrict__ prof) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1264,6 +1264,16 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
   if (prof && tid == 0) prof[(long long)si * 10 + (ph)] = clock64();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarp = kSubThreads / 32;
+  __shared__ int s_top, s_skip;
+  if (tid == 0) {  // records of the large-node pass come first
+    int t = 0;
+    for (int d = 0; d <= kMaxDepth + 1; ++d) t += st->lvl_cnt[d];
+    s_top = t;
+    s_skip = st->overflow || !st->finite;
+  }
+  __syncthreads();
+  if (s_skip) return;
+  const int rec_top = s_top;
   const int n_sub = st->sub_count;
   for (int si = blockIdx.x; si < n_sub; si += gridDim.x) {
     const int r = sub_list[si];
@@ -1602,6 +1612,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
 __global__ void __launch_bounds__(1024) morton_large_kernel(TreeRecords rec, const MortonState* __restrict__ st,
                                                             int seq_max, double* __restrict__ aux) {
   __shared__ int base[kMaxDepth + 3];
+  if (st->overflow || !st->finite) return;
   if (threadIdx.x == 0) {
     base[0] = 0;
     for (int d = 0; d <= kMaxDepth + 1; ++d) base[d + 1] = base[d] + st->lvl_cnt[d];
@@ -1636,7 +1647,7 @@ bool tree_build_morton(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max)
   // a tree that needs more levels is rebuilt once with all 32
   int lg4 = 0;
   while (lg4 < kMortonLevels && (1LL << (2 * lg4)) * leaf_cap < n) ++lg4;
-  const int levels = std::min(kMortonLevels, std::max(8, lg4 + 10));
+  const int levels = std::min(kMortonLevels, std::max(8, lg4 + 8));
   return tree_build_morton_levels(ctx, t, leaf_cap, seq_max, levels) ||
          (levels < kMortonLevels && tree_build_morton_levels(ctx, t, leaf_cap, seq_max, kMortonLevels));
 }
@@ -1690,29 +1701,16 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
     PTROM_CUDA(cudaStreamSynchronize(s));
     return *h_st;
   };
-  MortonState hs = read_state();
   auto release = [&]() {
     void* frees[] = {hull, st, key, skey, ids, sid, stmp, sub_list, large_list, aux};
     for (void* p : frees) dfree(p);
   };
-  if (!hs.finite) {
-    release();
-    rec.free();
-    config_fail("build_tree: non-finite input");
-  }
-  if (hs.overflow) {
-    release();
-    rec.free();
-    return false;
-  }
-  int R_top = 0;
-  for (int d = 0; d <= kMaxDepth + 1; ++d) R_top += hs.lvl_cnt[d];
-  t.root_width = hs.width;
 
-  // ---- subtrees of at most seq_max members: topology, leaf order, exact sums
+  // ---- subtrees of at most seq_max members: topology, leaf order, exact
+  // sums (no host round trip: the kernels read the level counts on the device)
   int* perm = dalloc<int>(n);
   double *sx = dalloc<double>(n), *sy = dalloc<double>(n), *sg = dalloc<double>(n);
-  aux = dalloc<double>(8 * (size_t)R_top);  // raw sums of the subtree roots and large nodes
+  aux = dalloc<double>(8 * (size_t)rec_cap);  // raw sums of the subtree roots and large nodes
   {
     static bool attr = false;
     if (!attr) {
@@ -1720,21 +1718,23 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
                                       (int)sizeof(SubSmem)));
       attr = true;
     }
-    const int nb = std::max(1, std::min(hs.sub_count, ctx->num_sms * 2));
+    const int nb = ctx->num_sms * 2;
     int id_bits = 1;
     while (id_bits < 31 && (1LL << id_bits) <= n) ++id_bits;
     static const bool sub_prof = std::getenv("PTROM_SUBTREE_PROFILE") != nullptr;
-    long long* prof = sub_prof ? dalloc<long long>((size_t)hs.sub_count * 10) : nullptr;
+    const int max_sub = (int)std::min<long long>(rec_cap, 4 * max_large + 4);
+    long long* prof = sub_prof ? dalloc<long long>((size_t)max_sub * 10) : nullptr;
     morton_subtree_kernel<<<nb, kSubThreads, sizeof(SubSmem), s>>>(skey, sid, t.px, t.py, t.g, sub_list, st, rec,
-                                                                   rec_cap, R_top, levels, leaf_cap, id_bits, perm,
+                                                                   rec_cap, levels, leaf_cap, id_bits, perm,
                                                                    sx, sy, sg, aux, prof);
     PTROM_LAUNCH_CHECK();
     if (prof) {
-      std::vector<long long> hp((size_t)hs.sub_count * 10);
+      const MortonState h1 = read_state();
+      std::vector<long long> hp((size_t)h1.sub_count * 10);
       PTROM_CUDA(cudaMemcpyAsync(hp.data(), prof, hp.size() * 8, cudaMemcpyDeviceToHost, s));
       PTROM_CUDA(cudaStreamSynchronize(s));
       if (FILE* f = std::fopen("gpurun_out/subtree_prof.csv", "w")) {
-        for (int i = 0; i < hs.sub_count; ++i) {
+        for (int i = 0; i < h1.sub_count; ++i) {
           for (int k = 0; k < 10; ++k) std::fprintf(f, "%lld%c", hp[10 * i + k], k == 9 ? '\n' : ',');
         }
         std::fclose(f);
@@ -1742,11 +1742,18 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
       dfree(prof);
     }
   }
-  if (hs.large_count > 0) {
-    morton_large_kernel<<<1, 1024, 0, s>>>(rec, st, seq_max, aux);
-    PTROM_LAUNCH_CHECK();
+  morton_large_kernel<<<1, 1024, 0, s>>>(rec, st, seq_max, aux);
+  PTROM_LAUNCH_CHECK();
+  const MortonState hs = read_state();
+  if (!hs.finite) {
+    dfree(perm);
+    dfree(sx);
+    dfree(sy);
+    dfree(sg);
+    release();
+    rec.free();
+    config_fail("build_tree: non-finite input");
   }
-  hs = read_state();
   if (hs.overflow) {
     dfree(perm);
     dfree(sx);
@@ -1756,7 +1763,9 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
     rec.free();
     return false;
   }
-  const int R = R_top + hs.rec_extra;
+  int R = hs.rec_extra;
+  for (int d = 0; d <= kMaxDepth + 1; ++d) R += hs.lvl_cnt[d];
+  t.root_width = hs.width;
   finish_tree(ctx, t, rec, R, perm, sx, sy, sg);
   ctx->tree_stats.levels = hs.levels_used;
   release();
