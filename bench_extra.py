@@ -151,13 +151,18 @@ def bench_config3(args, world):
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_dfma_tflops"] if peaks else None,
                 "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"] if peaks else None,
                 "traffic": _ncu_traffic("r01_bh_eval_ncu_summary.json"),
-                "kernel": "bh_eval_kernel (csrc/tree_eval.cu)", "avg_launch_ms": eval_ms,
+                "kernel": "bh_eval_warp_kernel (csrc/tree_eval.cu)", "avg_launch_ms": eval_ms,
                 "interactions_per_launch": inter, "prune_tests_per_launch": prune,
                 "flops_convention": "12/interaction + 7/prune test (BASELINE.md §2)",
                 "peak_source": "measured live: tools/peaks.cu DFMA chain"}
     build_roof = {"bound": "hbm", "median_build_ms": build_ms, "algorithmic_bytes": build_bytes,
                   "achieved_gbs": build_bytes / (build_ms * 1e-3) / 1e9, "peak_gbs": hbm,
                   "frac": (build_bytes / (build_ms * 1e-3) / 1e9) / hbm if hbm else None, "nodes": nodes}
+    mi, lv = ctypes.c_int(), ctypes.c_int()
+    ctx.check(lib.ptrom_tree_build_info(ctx.handle, ctypes.byref(mi), ctypes.byref(lv)))
+    build_roof["build"] = "morton-key sort" if mi.value else "level partition"
+    build_roof["note"] = ("latency-bound, not HBM-bound: sequential finish_node chains of the <=2048-member "
+                          "nodes, radix passes and level barriers (DESIGN.md section 6)")
 
     # e2e: host buffers through the drop-in ptrom_barnes_hut_velocity_f64 (one
     # GPU), or pinned host state -> every rank, sharded evaluation, result ->
