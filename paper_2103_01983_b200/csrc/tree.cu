@@ -1008,8 +1008,9 @@ constexpr int kMortonLevels = 32;
 constexpr int kSubMax = 2048;     // members of a subtree (seq_max <= kSubMax)
 constexpr int kSubNodes = 1024;   // local nodes of a subtree
 constexpr int kSubThreads = 256;
+constexpr int kSubBig = 1024;
 constexpr int kSubLevels = 64;
-constexpr int kListShorts = 25600;  // ascending-id lists of all local levels, level L at L*m (shared memory)
+constexpr int kListShorts = 22016;  // ascending-id lists of all local levels, level L at L*m (shared memory)
 constexpr int kThreadChain = 256;  // chains of nodes up to this size run in one thread
 
 struct MortonState {
@@ -1018,7 +1019,9 @@ struct MortonState {
   int finite;                  // hull finite
   int levels_used;
   int large_count, sub_count;
+  int sub_big, sub_small;      // subtrees above / at most kSubBig members (big ones scheduled first)
   int rec_extra;               // records created by the subtree CTAs
+  int sub_next;                // subtree work counter (dynamic scheduling)
   unsigned bar_count, bar_gen;
   double width;
 };
@@ -1149,7 +1152,7 @@ __device__ __forceinline__ void morton_child_geometry(TreeRecords& rec, int r, i
 __global__ void __launch_bounds__(kThreads) morton_levels_kernel(const unsigned long long* __restrict__ skey,
                                                                  int levels, long long leaf_cap, int seq_max,
                                                                  TreeRecords rec, int rec_cap, MortonState* st,
-                                                                 int* __restrict__ sub_list,
+                                                                 int* __restrict__ sub_list, int sub_half,
                                                                  int* __restrict__ large_list) {
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -1163,7 +1166,11 @@ __global__ void __launch_bounds__(kThreads) morton_levels_kernel(const unsigned 
       const int r = base + w;
       const int b = __ldcg(rec.begin + r), e = __ldcg(rec.end + r);
       if (e - b <= seq_max) {
-        if (lane == 0) sub_list[atomicAdd(&st->sub_count, 1)] = r;
+        if (lane == 0) {  // big subtrees at the front, the rest from sub_cap/2 on
+          atomicAdd(&st->sub_count, 1);
+          if (e - b > kSubBig) sub_list[atomicAdd(&st->sub_big, 1)] = r;
+          else sub_list[sub_half + atomicAdd(&st->sub_small, 1)] = r;
+        }
         continue;
       }
       if (lane == 0) large_list[atomicAdd(&st->large_count, 1)] = r;
@@ -1233,12 +1240,15 @@ struct SubSmem {
     short lists[kListShorts];             // ascending-id member list of every node, level L at L*m
   } u;
   double g[kSubMax], x[kSubMax], y[kSubMax];
+  int ids[kSubMax];                    // particle id of each member
   short lb[kSubNodes], le[kSubNodes];  // local node ranges (member positions in key order)
   short lfirst[kSubNodes], lpar[kSubNodes];
   unsigned char ldep[kSubNodes], lsplit[kSubNodes], lmask[kSubNodes], lq[kSubNodes];
   short lvl_start[kSubLevels + 2];
   int nloc, nlvl, base, ovf;
 };
+
+static_assert(sizeof(SubSmem) <= 112 * 1024, "two subtree CTAs per SM (228 KB shared memory)");
 
 // One CTA per subtree root (see the section comment). Phases:
 //  1. members (key, id, Γ, x, y) into shared memory;
@@ -1253,7 +1263,7 @@ struct SubSmem {
 //     the leaves' members into perm / sx / sy / sg.
 __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
     const unsigned long long* __restrict__ skey, const int* __restrict__ sid, const double* __restrict__ px,
-    const double* __restrict__ py, const double* __restrict__ pg, const int* __restrict__ sub_list,
+    const double* __restrict__ py, const double* __restrict__ pg, const int* __restrict__ sub_list, int sub_half,
     MortonState* st, TreeRecords rec, int rec_cap, int levels, long long leaf_cap, int id_bits,
     int* __restrict__ perm, double* __restrict__ sx, double* __restrict__ sy,
     double* __restrict__ sg, double* __restrict__ aux, long long* __restrict__ prof) {
@@ -1275,8 +1285,15 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
   if (s_skip) return;
   const int rec_top = s_top;
   const int n_sub = st->sub_count;
-  for (int si = blockIdx.x; si < n_sub; si += gridDim.x) {
-    const int r = sub_list[si];
+  __shared__ int s_si;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_si = atomicAdd(&st->sub_next, 1);  // CTAs take subtrees as they free up
+    __syncthreads();
+    const int si = s_si;
+    if (si >= n_sub) break;
+    const int nbig = st->sub_big;
+    const int r = si < nbig ? sub_list[si] : sub_list[sub_half + (si - nbig)];
     const int b = rec.begin[r], e = rec.end[r], m = e - b;
     const int d0 = rec.depth[r];
     SUBPROF(0)
@@ -1288,7 +1305,10 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
       for (int u = 0; u < IPT; ++u) {
         const int k = u * kSubThreads + tid;
         v[u] = k < m ? sid[b + k] : -1;
-        if (k < m) S.u.keys[k] = skey[b + k];
+        if (k < m) {
+          S.u.keys[k] = skey[b + k];
+          S.ids[k] = v[u];
+        }
       }
 #pragma unroll
       for (int u = 0; u < IPT; ++u) {
@@ -1443,7 +1463,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
 #pragma unroll
       for (int u = 0; u < IPT; ++u) {
         const int k = tid * IPT + u;
-        kk[u] = k < m ? (unsigned)sid[b + k] : pad;  // pads sort after every member (stable)
+        kk[u] = k < m ? (unsigned)S.ids[k] : pad;  // pads sort after every member (stable)
         vv[u] = (short)k;
       }
       __syncthreads();  // keys of the topology phase are dead
@@ -1509,7 +1529,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
         plx = __dadd_rn(plx, x);
         ply = __dadd_rn(ply, y);
         if (leaf) {
-          perm[b + t] = sid[b + k];
+          perm[b + t] = S.ids[k];
           sx[b + t] = x;
           sy[b + t] = y;
           sg[b + t] = g;
@@ -1682,7 +1702,8 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
 
   // ---- large nodes level by level
   const long long max_large = (long long)(kMaxDepth + 1) * (n / std::max(1, seq_max) + 2);
-  int* sub_list = dalloc<int>(std::min<long long>(rec_cap, 4 * max_large + 4));
+  const int sub_half = (int)std::min<long long>(rec_cap, 4 * max_large + 4);
+  int* sub_list = dalloc<int>(2 * (size_t)sub_half);
   int* large_list = dalloc<int>(max_large);
   {
     int occ = 0;
@@ -1690,7 +1711,7 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
     // few large nodes per level: a small grid keeps the grid barrier cheap
     const int grid = std::min(ctx->num_sms * std::max(1, occ), 32);
     void* args[] = {(void*)&skey, (void*)&levels, (void*)&leaf_cap, (void*)&seq_max, (void*)&rec,
-                    (void*)&rec_cap, (void*)&st, (void*)&sub_list, (void*)&large_list};
+                    (void*)&rec_cap, (void*)&st, (void*)&sub_list, (void*)&sub_half, (void*)&large_list};
     PTROM_CUDA(cudaLaunchCooperativeKernel((void*)morton_levels_kernel, grid, kThreads, args, 0, s));
   }
   double* aux = nullptr;
@@ -1724,7 +1745,7 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
     static const bool sub_prof = std::getenv("PTROM_SUBTREE_PROFILE") != nullptr;
     const int max_sub = (int)std::min<long long>(rec_cap, 4 * max_large + 4);
     long long* prof = sub_prof ? dalloc<long long>((size_t)max_sub * 10) : nullptr;
-    morton_subtree_kernel<<<nb, kSubThreads, sizeof(SubSmem), s>>>(skey, sid, t.px, t.py, t.g, sub_list, st, rec,
+    morton_subtree_kernel<<<nb, kSubThreads, sizeof(SubSmem), s>>>(skey, sid, t.px, t.py, t.g, sub_list, sub_half, st, rec,
                                                                    rec_cap, levels, leaf_cap, id_bits, perm,
                                                                    sx, sy, sg, aux, prof);
     PTROM_LAUNCH_CHECK();
