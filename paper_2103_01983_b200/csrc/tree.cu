@@ -1742,7 +1742,9 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
     const int nb = ctx->num_sms * 2;
     int id_bits = 1;
     while (id_bits < 31 && (1LL << id_bits) <= n) ++id_bits;
-    static const bool sub_prof = std::getenv("PTROM_SUBTREE_PROFILE") != nullptr;
+    // PTROM_SUBTREE_PROFILE=<csv path>: per-subtree phase clocks (tools/, not the product path)
+    static const char* sub_prof_path = std::getenv("PTROM_SUBTREE_PROFILE");
+    const bool sub_prof = sub_prof_path != nullptr;
     const int max_sub = (int)std::min<long long>(rec_cap, 4 * max_large + 4);
     long long* prof = sub_prof ? dalloc<long long>((size_t)max_sub * 10) : nullptr;
     morton_subtree_kernel<<<nb, kSubThreads, sizeof(SubSmem), s>>>(skey, sid, t.px, t.py, t.g, sub_list, sub_half, st, rec,
@@ -1754,7 +1756,7 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
       std::vector<long long> hp((size_t)h1.sub_count * 10);
       PTROM_CUDA(cudaMemcpyAsync(hp.data(), prof, hp.size() * 8, cudaMemcpyDeviceToHost, s));
       PTROM_CUDA(cudaStreamSynchronize(s));
-      if (FILE* f = std::fopen("gpurun_out/subtree_prof.csv", "w")) {
+      if (FILE* f = std::fopen(sub_prof_path, "w")) {
         for (int i = 0; i < h1.sub_count; ++i) {
           for (int k = 0; k < 10; ++k) std::fprintf(f, "%lld%c", hp[10 * i + k], k == 9 ? '\n' : ',');
         }
