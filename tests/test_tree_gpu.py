@@ -334,12 +334,15 @@ def test_morton_build_equals_level_build(pt, case):
         n, cap = 50_000, 8
         px, py, g = rng.normal(0, 1, n), rng.normal(0, 1, n), rng.uniform(0.5, 1.5, n)
     seq = "64" if case == "seq64" else None
+    forced = os.environ.pop("PTROM_TREE_BUILD", None)  # this test picks the build itself
     if seq:
         os.environ["PTROM_TREE_SEQ_MAX"] = seq
     try:
         ctx_m = ptm.Context(0)
     finally:
         os.environ.pop("PTROM_TREE_SEQ_MAX", None)
+        if forced is not None:
+            os.environ["PTROM_TREE_BUILD"] = forced
     tm = QuadTree(px, py, g, cap, ctx=ctx_m)
     morton, levels = build_info(ctx_m)
     assert morton == 1 and levels > 1
@@ -349,8 +352,10 @@ def test_morton_build_equals_level_build(pt, case):
     try:
         ctx_l = ptm.Context(0)
     finally:
-        del os.environ["PTROM_TREE_BUILD"]
+        os.environ.pop("PTROM_TREE_BUILD", None)
         os.environ.pop("PTROM_TREE_SEQ_MAX", None)
+        if forced is not None:
+            os.environ["PTROM_TREE_BUILD"] = forced
     tl = QuadTree(px, py, g, cap, ctx=ctx_l)
     assert build_info(ctx_l)[0] == 0
     em, el = tm.export(), tl.export()
@@ -380,3 +385,19 @@ def test_morton_build_falls_back_on_deep_trees(pt, oracle):
     gt = QuadTree(px, py, g, 1)
     assert build_info(gt.ctx)[0] == 0
     assert_same_tree(gt, oracle.Tree(px, py, g, 1))
+
+
+def test_morton_build_deterministic_and_small_sizes(pt, oracle):
+    """Two Morton builds of the same input are identical array for array, and
+    sizes around the subtree / leaf thresholds (1, 33, 2047..2049, 4097)
+    still equal the reference."""
+    from paper_2103_01983_b200.tree import QuadTree
+    rng = np.random.default_rng(99)
+    for n in (1, 33, 2047, 2048, 2049, 4097):
+        px, py = rng.normal(0, 1, n), rng.normal(0, 1, n)
+        g = rng.uniform(0.5, 1.5, n)
+        a, b = QuadTree(px, py, g, 32), QuadTree(px, py, g, 32)
+        ea, eb = a.export(), b.export()
+        for k in ea:
+            np.testing.assert_array_equal(ea[k], eb[k], err_msg=f"{k} n={n}")
+        assert_same_tree(a, oracle.Tree(px, py, g, 32))
