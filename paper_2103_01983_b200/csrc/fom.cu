@@ -6,7 +6,7 @@
 // 2x2 inverse blocks stay in HBM for the whole trajectory.
 //
 // Control flow on the device: one FOM step is a CUDA graph whose Newton loop
-// is a conditional WHILE node; a single-thread decide kernel evaluates the
+// is a conditional WHILE node; the residual kernel's last block evaluates the
 // reference's convergence test (integrators.hpp:140-155: ‖r‖/‖r0‖ ≤ tol,
 // update cap, r0 == 0) and sets the loop condition, and a nested IF node runs
 // the Jacobian/Newton-block refresh on the steps it is due. The host enqueues
@@ -98,15 +98,13 @@ struct FomCtl {
   long long evals;  // velocity evaluations (the reference's counter / N(N-1))
   double r0, rel;
   int updates, converged, have_blocks, refreshed, do_refresh;
+  unsigned ticket;  // residual blocks done (the last one decides)
 };
 
 // integrators.hpp:140-155 on the device: ‖r‖ from the fixed-order block
 // partials, the reference's decisions, and the loop / refresh conditions.
-__global__ void fom_decide_kernel(FomCtl* c, const double* __restrict__ block_part, int nb, double tol,
-                                  int max_iters, int refresh, cudaGraphConditionalHandle h_loop) {
-  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
-  const double s = warp_sum_blocks(nb, block_part);
-  if (threadIdx.x != 0) return;
+__device__ void fom_decide(FomCtl* c, double s, double tol, int max_iters, int refresh,
+                           cudaGraphConditionalHandle h_loop) {
   const double nr = sqrt(s);
   const int upd = c->updates;
   bool cont = false, do_ref = false;
@@ -134,6 +132,49 @@ __global__ void fom_decide_kernel(FomCtl* c, const double* __restrict__ block_pa
   }
   c->do_refresh = do_ref ? 1 : 0;
   cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
+}
+
+// residual_kernel + fom_decide in one launch: the last block to finish sums
+// the block partials (same fixed order) and decides.
+__global__ void __launch_bounds__(kNormThreads) residual_decide_kernel(
+    long long m, long long ld, const double* __restrict__ xi, const double* __restrict__ fxi,
+    const double* __restrict__ xp, const double* __restrict__ fp, double h, double* __restrict__ r,
+    double* __restrict__ block_part, FomCtl* c, double tol, int max_iters, int refresh,
+    cudaGraphConditionalHandle h_loop) {
+  double acc = 0.0;
+  const long long rows = 2 * m;
+  for (long long e = blockIdx.x * (long long)kNormThreads + threadIdx.x; e < rows;
+       e += (long long)gridDim.x * kNormThreads) {
+    const long long k = e < m ? e : (e - m) + ld;
+    const double v = __dsub_rn(__dsub_rn(xi[k], xp[k]), __dmul_rn(h, __dadd_rn(fxi[k], fp[k])));
+    r[k] = v;
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  __shared__ double warp_sum[kNormThreads / 32];
+  __shared__ bool s_last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sb = 0.0;
+    for (int w = 0; w < kNormThreads / 32; ++w) sb = __dadd_rn(sb, warp_sum[w]);
+    block_part[blockIdx.x] = sb;
+    __threadfence();
+    s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  double sum = 0.0;
+  for (int b = lane; b < (int)gridDim.x; b += 32) sum = __dadd_rn(sum, __ldcg(block_part + b));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, o));
+  if (lane == 0) {
+    c->ticket = 0;
+    fom_decide(c, sum, tol, max_iters, refresh, h_loop);
+  }
 }
 
 // First node of the loop body: arms the IF node of the Newton-block refresh.
@@ -270,13 +311,13 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
   // pre: ξ = x_prev, f_ξ = f_prev (integrators.hpp:130-131); r; decide
   PTROM_CUDA(cudaMemcpyAsync(xi, x_prev, dim * 8, cudaMemcpyDeviceToDevice, st));
   PTROM_CUDA(cudaMemcpyAsync(fxi, f_prev, dim * 8, cudaMemcpyDeviceToDevice, st));
-  residual_kernel<<<kNormBlocks, kNormThreads, 0, st>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part);
-  // the loop node's handle must exist before the decide kernel that sets it
+  // the loop node's handle must exist before the kernel that sets it
   cudaStreamCaptureStatus cs;
   cudaGraph_t g_cap;
   PTROM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g_cap, nullptr, nullptr));
   PTROM_CUDA(cudaGraphConditionalHandleCreate(&h_loop, g_cap, 0, 0));
-  fom_decide_kernel<<<1, 32, 0, st>>>(ctl, block_part, kNormBlocks, tol, max_iters, refresh, h_loop);
+  residual_decide_kernel<<<kNormBlocks, kNormThreads, 0, st>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part, ctl,
+                                                                tol, max_iters, refresh, h_loop);
   {
     // WHILE (continue): [IF refresh: Newton blocks]; update; velocity; r; decide
     const cudaGraphNode_t* deps = nullptr;
@@ -319,8 +360,9 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
     ctx->stream = s_body;
     newton_update_kernel<<<grid_for(ctx, n, 256), 256, 0, s_body>>>(n, n, inv, r, xi);
     dev_velocity_f64(ctx, n, xi, d_gamma, delta, form, d_inflow, 0, n, fxi, n);
-    residual_kernel<<<kNormBlocks, kNormThreads, 0, s_body>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part);
-    fom_decide_kernel<<<1, 32, 0, s_body>>>(ctl, block_part, kNormBlocks, tol, max_iters, refresh, h_loop);
+    residual_decide_kernel<<<kNormBlocks, kNormThreads, 0, s_body>>>(n, n, xi, fxi, x_prev, f_prev, h, r,
+                                                                      block_part, ctl, tol, max_iters, refresh,
+                                                                      h_loop);
     ctx->stream = saved;
     cudaGraph_t tmp;
     PTROM_CUDA(cudaStreamEndCapture(s_body, &tmp));
