@@ -183,6 +183,8 @@ def test_config3_two_patches_full_size(pt, oracle):
     n = w.n
     px, py = w.x0[:n], w.x0[n:]
     gt, ot = QuadTree(px, py, w.gamma, 32), oracle.Tree(px, py, w.gamma, 32)
+    if "PTROM_TREE_BUILD" not in os.environ:  # the measured path: no silent fall back to the level build
+        assert build_info(gt.ctx)[0] == 1
     assert_same_tree(gt, ot)
     crit = ClusterCriterion.barnes_hut(0.5)
     rng = np.random.default_rng(3)
