@@ -1733,12 +1733,9 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
   double *sx = dalloc<double>(n), *sy = dalloc<double>(n), *sg = dalloc<double>(n);
   aux = dalloc<double>(8 * (size_t)rec_cap);  // raw sums of the subtree roots and large nodes
   {
-    static bool attr = false;
-    if (!attr) {
-      PTROM_CUDA(cudaFuncSetAttribute(morton_subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(SubSmem)));
-      attr = true;
-    }
+    // per call: the attribute belongs to the current device's context
+    PTROM_CUDA(cudaFuncSetAttribute(morton_subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(SubSmem)));
     const int nb = ctx->num_sms * 2;
     int id_bits = 1;
     while (id_bits < 31 && (1LL << id_bits) <= n) ++id_bits;
