@@ -1662,7 +1662,9 @@ __global__ void __launch_bounds__(1024) morton_large_kernel(TreeRecords rec, con
 bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels);
 bool tree_build_morton(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max) {
   const long long n = t.n;
-  if (leaf_cap > 32 || seq_max > kSubMax || seq_max < leaf_cap) return false;
+  // leaf_capacity < 4 gives subtrees with more local nodes than a CTA holds
+  // (kSubNodes): the level build, without a wasted attempt
+  if (leaf_cap > 32 || leaf_cap < 4 || seq_max > kSubMax || seq_max < leaf_cap) return false;
   // key depth: the uniform-density depth plus a margin (fewer radix passes);
   // a tree that needs more levels is rebuilt once with all 32
   int lg4 = 0;
