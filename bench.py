@@ -1,20 +1,29 @@
 #!/usr/bin/env python3
 """bench.py — Biot–Savart pair interactions/s (fp64) on B200.
 
-Workload (BASELINE.json configs[1]): one all-pairs velocity evaluation of the
-N = 65,536 Gaussian vortex patch (δ = 0.005 → reference delta 2.5e-5) per
-step, fp64, SURVEY.md §8d. With --gpus G > 1 (torchrun, one rank per GPU)
-the targets are split evenly across ranks and every step all-gathers the
-source positions over NCCL first (the per-evaluation exchange of the sharded
-FOM) — strong scaling: total work per step is fixed.
+Default workload (BASELINE.json's metric configuration, configs[4]): one
+all-pairs velocity evaluation of the N = 4,194,304 uniform-square system
+(δ = 1e-3 → reference delta 1e-6) per step, fp64, SURVEY.md §8d config 5.
+With --gpus G > 1 (torchrun, one rank per GPU) the targets are split evenly
+across ranks and every step exchanges the source positions first (peer-memory
+reads fused into the tile loads, or an NCCL all-gather) —
+strong scaling: total work per step is fixed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+At G = 1 the line also carries the other BASELINE configs under "extra",
+each with its own value, e2e, roofline, cpu_baseline and clocks:
+  config1  FOM trajectory (N = 4,096, 100 steps; integrators.hpp:243-272)
+  config2  single evaluation at N = 65,536, fp64 and fp32
+  config3  Barnes–Hut build + aggregation + far field at N = 1,048,576
+  config4  PTROM online, 4,096 μ instances x 50 steps (rom.hpp:404-412)
+(--no-extras skips them; --workload configK runs one of them as the headline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload configK]
 
 `value` is device-timed (CUDA events, max over ranks) with inputs resident in
-HBM; `e2e` times the drop-in host C-ABI call (ptrom_pairwise_velocity_f64:
-pinned host buffers in, H2D + kernels + D2H inside the timed region).
-`--impl reference` times the reference's CPU algorithm (the oracle port in
-oracle/, all host threads) on a bounded sample of the same workload.
+HBM; `e2e` times the drop-in host C-ABI call (pinned host buffers in, H2D +
+kernels + D2H inside the timed region). `--impl reference` times the
+reference's CPU algorithm (the oracle port in oracle/, all host threads) on a
+bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -117,21 +126,24 @@ def ncu_traffic(name):
         return None
 
 
-def cpu_baseline_sample(w, threads: int, target_seconds: float):
+def cpu_baseline_sample(w, threads: int, target_seconds: float, fp32: bool = False):
     """Oracle (the reference's serial loop, kernel.hpp:107-129) on a bounded
     target sample × all sources; returns pairs/s and the sample description."""
     from oracle import pyoracle
     n = w.n
+    x = w.x0.astype(np.float32) if fp32 else w.x0
+    g = w.gamma.astype(np.float32) if fp32 else w.gamma
     t0 = time.perf_counter()
     probe = max(8, 64 * threads)
-    pyoracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=0, t_end=probe, threads=threads)
+    pyoracle.pairwise_velocity(x, g, w.delta, t_begin=0, t_end=probe, threads=threads)
     dt = time.perf_counter() - t0
     rows = int(min(n, max(probe, probe * target_seconds / max(dt, 1e-6))))
     t0 = time.perf_counter()
-    pyoracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=0, t_end=rows, threads=threads)
+    pyoracle.pairwise_velocity(x, g, w.delta, t_begin=0, t_end=rows, threads=threads)
     dt = time.perf_counter() - t0
     pairs = rows * (n - 1)
-    return pairs / dt, f"{rows} targets x {n} sources of {w.name} (N={n}), {dt:.1f} s"
+    return pairs / dt, (f"{rows} targets x {n} sources of {w.name} (N={n}){' in fp32' if fp32 else ''}, "
+                        f"{dt:.1f} s, {threads} thread(s)")
 
 
 def run_reference(args, rank, world):
@@ -139,6 +151,8 @@ def run_reference(args, rank, world):
     reference itself does not build here: Eigen absent)."""
     if rank != 0:
         return 0
+    if args.workload == "config1":
+        return run_reference_config1(args)
     if args.workload not in ("config2", "config5"):
         import bench_extra
         return bench_extra.run_reference(args, rank, world)
@@ -175,48 +189,15 @@ def run_reference(args, rank, world):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 200 for config2)")
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--workload", choices=["config2", "config3", "config4", "config5"], default="config2",
-                    help="config2 (default, the headline) | config3 Barnes-Hut | config4 PTROM online batch | "
-                         "config5 all-pairs evaluation at N = 4,194,304 (the 8-GPU sharded config)")
-    ap.add_argument("--batch", type=int, default=512, help="config4: instances per step")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    args.steps_given = args.steps is not None
-    if args.steps is None:
-        args.steps = 3 if args.workload == "config5" else 200
-    if args.workload not in ("config2", "config5"):
-        import bench_extra
-        rank = env_int("RANK", 0)
-        world = env_int("WORLD_SIZE", 1)
-        if args.impl == "reference":
-            return bench_extra.run_reference(args, rank, world)
-        return bench_extra.run(args, rank, world)
-
-    rank = env_int("RANK", 0)
-    world = env_int("WORLD_SIZE", 1)
-    local = env_int("LOCAL_RANK", 0)
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
-
+def allpairs_line(args, w, K, W, rank, world, local, e2e_steps, cpu_seconds, with_fp32, traffic_file=None):
+    """One all-pairs velocity evaluation per step (kernel.hpp:107-129) of
+    workload w; K timed steps after W warm-up steps (L2 flushed between)."""
     import torch
     import torch.distributed as dist
 
     import paper_2103_01983_b200 as pt
     from paper_2103_01983_b200 import device as dev
-    from paper_2103_01983_b200 import workloads
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = workloads.config5() if args.workload == "config5" else workloads.config2()
     n = w.n
     lo, hi = rank * n // world, (rank + 1) * n // world
     m = hi - lo
@@ -227,6 +208,7 @@ def main():
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     ctx = pt.default_context(local)
     stream = torch.cuda.current_stream()
+    lib = ctx.lib
 
     def step_allgather():  # per-evaluation exchange: NCCL all-gather of the positions, then the local kernel
         if world > 1:
@@ -250,8 +232,9 @@ def main():
 
                 def step_peer():
                     pex.write_local(x_local)
-                    pex.barrier(token)
+                    pex.barrier(token)  # every rank published before any rank reads
                     pex.velocity(gamma, w.delta, out)
+                    pex.barrier(token)  # every rank's reads done before any rank's next write (WAR)
 
                 step_allgather()
                 ref_out = out.clone()
@@ -264,7 +247,7 @@ def main():
             except Exception as exc:  # keep the NCCL path; say why in the JSON line
                 exchange = f"nccl-allgather (peer setup failed: {type(exc).__name__})"
 
-    for _ in range(args.warmup):
+    for _ in range(W):
         step()
     dev.synchronize(ctx)
     if world > 1:
@@ -272,17 +255,16 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    lib = ctx.lib
+    import ctypes
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     with ClockSampler(local) as clocks:
         lib.ptrom_profile_begin(ctx.handle)
-        for k in range(args.steps):
+        for k in range(K):
             l2_flush.zero_()
             starts[k].record(stream)
             step()
             ends[k].record(stream)
-        import ctypes
         kern_ms, kern_launches = ctypes.c_double(), ctypes.c_int64()
         ctx.check(lib.ptrom_profile_end(ctx.handle, ctypes.byref(kern_ms), ctypes.byref(kern_launches)))
         torch.cuda.synchronize()
@@ -294,39 +276,31 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     pairs_per_step = n * (n - 1)
-    value = pairs_per_step * args.steps / (total_ms * 1e-3)
+    value = pairs_per_step * K / (total_ms * 1e-3)
 
     # ---- e2e through the drop-in host C-ABI (pinned host buffers, H2D + D2H inside)
-    e2e = None
     if world == 1:
         hx = torch.tensor(w.x0).pin_memory().numpy()
         hg = torch.tensor(w.gamma).pin_memory().numpy()
         hf = torch.empty(2 * n, dtype=torch.float64).pin_memory().numpy()
-        sys_ = pt.ParticleSystem(hg, w.delta)
-        import ctypes
         cnt = ctypes.c_uint64()
         fn = lambda: ctx.check(lib.ptrom_pairwise_velocity_f64(ctx.handle, n, hx.ctypes.data, hg.ctypes.data,
                                                                float(w.delta), 0, None, hf.ctypes.data,
                                                                ctypes.byref(cnt)))
-        big = args.workload == "config5"  # ~10 s per evaluation
-        for _ in range(1 if big else 3):
-            fn()
-        e2e_steps = max(1, args.steps) if big else max(5, min(args.steps, 50))
+        fn()  # first host-API call sizes the staging buffers
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             fn()
         e2e_s = time.perf_counter() - t0
-        e2e = {"value": pairs_per_step * e2e_steps / e2e_s, "unit": UNIT,
+        e2e = {"value": pairs_per_step * e2e_steps / e2e_s, "unit": UNIT, "steps": e2e_steps,
                "h2d_bytes_per_step": int(hx.nbytes + hg.nbytes), "d2h_bytes_per_step": int(hf.nbytes),
                "api": "ptrom_pairwise_velocity_f64 (host buffers)"}
-        del sys_
     else:
         # Sharded end to end: every step each rank copies its own positions in
-        # from pinned host memory, all-gathers the sources, evaluates its
+        # from pinned host memory, exchanges the sources, evaluates its
         # targets and copies its velocity rows back out (max over ranks).
         hx_local = x_local.cpu().pin_memory()
         hf_local = torch.empty(2 * m, dtype=torch.float64).pin_memory()
-        e2e_steps = max(5, min(args.steps, 50))
 
         def e2e_step():
             x_local.copy_(hx_local, non_blocking=True)
@@ -334,23 +308,20 @@ def main():
             hf_local.copy_(out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
 
-        for _ in range(3):
-            e2e_step()
+        e2e_step()
         dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
         e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        e2e = {"value": pairs_per_step * e2e_steps / float(e2e_s.item()), "unit": UNIT,
+        e2e = {"value": pairs_per_step * e2e_steps / float(e2e_s.item()), "unit": UNIT, "steps": e2e_steps,
                "h2d_bytes_per_step": int(hx_local.numel() * 8 * world),
                "d2h_bytes_per_step": int(hf_local.numel() * 8 * world),
-               "api": "per rank: H2D own positions, NCCL all-gather, ptrom_dev_pairwise_velocity_f64, D2H own rows"}
+               "api": f"per rank: H2D own positions, {exchange}, ptrom_dev_pairwise_velocity_f64, D2H own rows"}
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return 0
+        return None
 
     peaks = measured_peaks(local)
     avg_kernel_s = (kern_ms.value * 1e-3) / max(1, kern_launches.value)
@@ -360,57 +331,300 @@ def main():
     if peaks:
         roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peaks["fp64_dfma_tflops"],
                     "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_dfma_tflops"],
-                    "traffic": ncu_traffic("r01_allpairs_vel64_ncu_summary.json") if args.workload == "config2" else None,
+                    "traffic": ncu_traffic(traffic_file) if traffic_file else None,
                     "algorithmic_bytes_per_launch": 24 * n,
                     "kernel": "allpairs_f64_kernel<128,8,2,1,vel> (csrc/allpairs.cu)",
                     "peak_source": "measured live: tools/peaks.cu DFMA chain (MEASURED_PEAKS.json has no FP64)",
                     "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": local_pairs,
                     "avg_launch_ms": avg_kernel_s * 1e3, "launches": kern_launches.value,
+                    "share_of_step": (kern_ms.value / max(1, kern_launches.value)) / (total_ms / K),
                     "peaks": peaks}
 
     # config 2's fp32 run (BASELINE configs[1]: "fp64 and fp32"): same workload,
-    # device-timed, L2 flushed; reported beside the fp64 headline
+    # device-timed, L2 flushed; reported beside the fp64 line
     fp32 = None
-    if world == 1 and args.workload == "config2":
+    if world == 1 and with_fp32:
         x32, g32 = x_full.float(), gamma.float()
         out32 = torch.empty(2 * n, dtype=torch.float32, device="cuda")
         for _ in range(3):
             dev.pairwise_velocity(x32, g32, w.delta, 0, None, 0, n, out32, ctx=ctx)
         torch.cuda.synchronize()
-        k32 = max(10, min(args.steps, 100))
+        k32 = max(10, min(K, 100))
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k32)]
-        for a, b in ev:
-            l2_flush.zero_()
-            a.record(stream)
-            dev.pairwise_velocity(x32, g32, w.delta, 0, None, 0, n, out32, ctx=ctx)
-            b.record(stream)
-        torch.cuda.synchronize()
+        with ClockSampler(local) as clocks32:
+            for a, b in ev:
+                l2_flush.zero_()
+                a.record(stream)
+                dev.pairwise_velocity(x32, g32, w.delta, 0, None, 0, n, out32, ctx=ctx)
+                b.record(stream)
+            torch.cuda.synchronize()
         ms32 = sum(a.elapsed_time(b) for a, b in ev) / k32
         v32 = pairs_per_step / (ms32 * 1e-3)
-        fp32 = {"value": v32, "unit": UNIT, "ms_per_step": ms32, "steps": k32,
+        hx32 = torch.tensor(w.x0, dtype=torch.float32).pin_memory().numpy()
+        hg32 = torch.tensor(w.gamma, dtype=torch.float32).pin_memory().numpy()
+        hf32 = torch.empty(2 * n, dtype=torch.float32).pin_memory().numpy()
+        fn32 = lambda: ctx.check(lib.ptrom_pairwise_velocity_f32(ctx.handle, n, hx32.ctypes.data, hg32.ctypes.data,
+                                                                 float(w.delta), 0, None, hf32.ctypes.data, None))
+        fn32()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            fn32()
+        e32 = time.perf_counter() - t0
+        cpu32 = None
+        if not args.no_cpu_baseline:
+            v_cpu, sample = cpu_baseline_sample(w, 1, cpu_seconds / 2, fp32=True)
+            cpu32 = {"value": v_cpu, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
+        fp32 = {"value": v32, "unit": UNIT, "ms_per_step": ms32, "steps": k32, "dtype": "f32",
+                "e2e": {"value": pairs_per_step * e2e_steps / e32, "unit": UNIT, "steps": e2e_steps,
+                        "h2d_bytes_per_step": int(hx32.nbytes + hg32.nbytes), "d2h_bytes_per_step": int(hf32.nbytes),
+                        "api": "ptrom_pairwise_velocity_f32 (host buffers)"},
                 "roofline": {"bound": "fp32", "achieved": FLOPS_PER_PAIR * v32 / 1e12,
                              "peak": peaks["fp32_ffma_tflops"] if peaks else None, "unit": "TFLOP/s",
                              "frac": FLOPS_PER_PAIR * v32 / 1e12 / peaks["fp32_ffma_tflops"] if peaks else None,
-                             "kernel": "allpairs_f32_kernel<128,8> (csrc/allpairs.cu), step incl. chunk reduction"}}
+                             "traffic": None,
+                             "kernel": "allpairs_f32_kernel<128,8> (csrc/allpairs.cu), step incl. chunk reduction"},
+                "cpu_baseline": cpu32, "clocks": clocks32.summary(),
+                "parity": "judged against the fp64 oracle at 1e-5 (tests/test_allpairs_gpu.py)"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, sample = cpu_baseline_sample(w, 1, args.cpu_seconds)
+        v, sample = cpu_baseline_sample(w, 1, cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
 
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
         "config": {"workload": w.name, "n": n, "delta": w.delta, "targets_per_rank": m,
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "parallelism": f"targets sharded x{world}, position exchange per step: {exchange}"
                    if world > 1 else "single GPU"},
-        "gpu_launches": 2 * args.steps,  # tile kernel + fixed-order chunk reduction
+        "gpu_launches": (kern_launches.value if world == 1 else K) * (1 if n * m <= 268435456 else 2),
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
         "fp32": fp32,
     }
-    print(json.dumps(line), flush=True)
+
+
+def config1_line(args, K, W, local, cpu_seconds):
+    """BASELINE configs[0]: the implicit-trapezoidal FOM trajectory
+    (integrators.hpp:243-272) at N = 4,096, 100 steps, dt = 1e-3,
+    NewtonConfig{1e-10, 100, 1}; one step = one whole trajectory through
+    ptrom_dev_fom_simulate_f64 (device-side Newton control, CUDA graph).
+    Unit: pair interactions/s counting velocity pairs (12 flops) and
+    Jacobian pairs (21 flops), N(N-1) per evaluation."""
+    import torch
+
+    import paper_2103_01983_b200 as pt
+    from paper_2103_01983_b200 import device as dev
+    from paper_2103_01983_b200 import workloads
+    w = workloads.config1()
+    n = w.n
+    ctx = pt.default_context(local)
+    stream = torch.cuda.current_stream()
+    x0 = torch.tensor(w.x0, device="cuda")
+    g = torch.tensor(w.gamma, device="cuda")
+    snaps = torch.empty(w.n_steps, 2 * n, dtype=torch.float64, device="cuda")
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    res = {}
+
+    def step():
+        res["r"] = dev.fom_simulate(x0, g, w.delta, w.dt, w.n_steps, snapshots=snaps, ctx=ctx)
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    import bench_extra
+    ours, _ = bench_extra._count_launches(step)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    nv = nj = 0
+    with ClockSampler(local) as clocks:
+        for k in range(K):
+            l2_flush.zero_()
+            starts[k].record(stream)
+            step()
+            ends[k].record(stream)
+            nv += res["r"][4]
+            nj += res["r"][5]
+        torch.cuda.synchronize()
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    pairs = n * (n - 1)
+    value = (nv + nj) * pairs / (total_ms * 1e-3)
+    flops = (12 * nv + 21 * nj) * pairs
+    peaks = measured_peaks(local)
+    achieved = flops / (total_ms * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_dfma_tflops"] if peaks else None,
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"] if peaks else None, "traffic": None,
+                "scope": "whole trajectory (launch/latency-bound at N = 4,096: ~900 small graph-launched kernels)",
+                "flops_convention": "12 per velocity pair + 21 per Jacobian pair (BASELINE.md §2)",
+                "velocity_evals_per_trajectory": nv / K, "jacobian_evals_per_trajectory": nj / K,
+                "peak_source": "measured live: tools/peaks.cu DFMA chain"}
+    # e2e: the drop-in host entry point (x0, Γ in; snapshots, iterations out)
+    sys_ = pt.ParticleSystem(w.gamma, w.delta)
+    grid = pt.TimeGrid(w.dt, w.n_steps)
+    pt.fom_simulate(w.x0, sys_, grid)
+    ke = max(3, min(K, 10))
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        run = pt.fom_simulate(w.x0, sys_, grid)
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": (nv + nj) / K * pairs * ke / e2e_s, "unit": UNIT, "steps": ke,
+           "h2d_bytes_per_step": int(w.x0.nbytes + w.gamma.nbytes),
+           "d2h_bytes_per_step": int(run.snapshots.nbytes + 13 * w.n_steps),
+           "api": "ptrom_fom_simulate_f64 (host x0, Γ in; snapshots, iterations, converged, residuals out)"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import pyoracle
+        steps_cpu = w.n_steps
+        t0 = time.perf_counter()
+        _, it_o, _, _ = pyoracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, 10, threads=1)
+        dt10 = time.perf_counter() - t0
+        steps_cpu = int(min(w.n_steps, max(10, 10 * cpu_seconds / max(dt10, 1e-6))))
+        t0 = time.perf_counter()
+        _, it_o, _, _ = pyoracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps_cpu, threads=1)
+        dtc = time.perf_counter() - t0
+        evals = 1 + int(np.sum(it_o)) + int(np.sum(np.asarray(it_o) > 0))
+        cpu = {"value": evals * pairs / dtc, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"oracle fom_simulate, {steps_cpu} of {w.n_steps} steps of {w.name} "
+                         f"({evals} velocity+Jacobian evaluations, {dtc:.1f} s, 1 thread)"}
+    return {
+        "metric": "Biot-Savart pair interactions/s (fp64), FOM trajectory (velocity + Jacobian pairs)",
+        "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": total_ms / K,
+        "higher_is_better": True, "scaling": "weak", "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
+        "config": {"workload": w.name, "n": n, "delta": w.delta, "dt": w.dt, "n_steps": w.n_steps,
+                   "newton": "tol 1e-10, max_iters 100, refresh 1 (integrators.hpp:55-58)",
+                   "unit_of_step": "one 100-step trajectory", "l2": "flushed between trajectories"},
+        "trajectory_ms": total_ms / K, "newton_updates_per_trajectory": float(np.sum(res["r"][1])),
+        "gpu_launches": ours * K if ours is not None else None,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
+    }
+
+
+def extras(args, local):
+    """The other BASELINE configs at one GPU, compact runs (bounded time)."""
+    import copy
+
+    import bench_extra
+    from paper_2103_01983_b200 import workloads
+    out = {}
+    small = copy.copy(args)
+    small.cpu_seconds = min(args.cpu_seconds, 8.0)
+
+    def guard(name, fn):
+        t0 = time.perf_counter()
+        try:
+            out[name] = fn()
+        except Exception as exc:  # an extra never hides the headline; say what failed
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        if isinstance(out[name], dict):
+            out[name]["bench_seconds"] = time.perf_counter() - t0
+
+    guard("config1", lambda: config1_line(small, 10, 3, local, small.cpu_seconds))
+    guard("config2", lambda: allpairs_line(small, workloads.config2(), 20, 3, 0, 1, local, 10,
+                                           small.cpu_seconds, True, "r01_allpairs_vel64_ncu_summary.json"))
+
+    def c3():
+        a = copy.copy(small)
+        a.steps, a.steps_given, a.warmup = 10, True, 3
+        line = bench_extra.bench_config3(a, 1)
+        line.pop("units_per_step", None)
+        return line
+
+    def c4():
+        a = copy.copy(small)
+        a.steps, a.steps_given, a.warmup, a.batch = 8, True, 3, 512
+        line = bench_extra.bench_config4(a, 1)
+        line.pop("units_per_step", None)
+        return line
+
+    guard("config3", c3)
+    guard("config4", c4)
+    return out
+
+
+def run_reference_config1(args):
+    """--impl reference --workload config1: the oracle's fom_simulate
+    (integrators.hpp:243-272) on all host threads, a bounded number of steps
+    of the config-1 trajectory per step."""
+    from oracle import pyoracle
+    from paper_2103_01983_b200 import workloads
+    pyoracle.build()
+    w = workloads.config1()
+    threads = os.cpu_count() or 1
+    pairs = w.n * (w.n - 1)
+    vals, times = [], []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, it, _, _ = pyoracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, 10, threads=threads)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            evals = 1 + int(np.sum(it)) + int(np.sum(np.asarray(it) > 0))
+            vals.append(evals * pairs)
+            times.append(dt)
+    value = sum(vals) / sum(times)
+    sample = f"oracle fom_simulate, 10 of {w.n_steps} steps of {w.name} per step, {threads} threads"
+    print(json.dumps({
+        "metric": "Biot-Savart pair interactions/s (fp64), FOM trajectory (velocity + Jacobian pairs)",
+        "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)", "impl": "reference",
+        "config": {"workload": w.name, "n": w.n, "steps_per_sample": 10},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 3 for config5, 200 for config2)")
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="config5: skip the other configs' keys")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--workload", choices=["config1", "config2", "config3", "config4", "config5"], default="config5",
+                    help="config5 (default: the metric's N = 4,194,304 evaluation) | config1 FOM trajectory | "
+                         "config2 N = 65,536 evaluation | config3 Barnes-Hut | config4 PTROM online batch")
+    ap.add_argument("--batch", type=int, default=512, help="config4: instances per step")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    args.steps_given = args.steps is not None
+    if args.steps is None:
+        args.steps = {"config5": 3, "config1": 20}.get(args.workload, 200)
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if args.workload in ("config3", "config4"):
+        import bench_extra
+        if args.impl == "reference":
+            return bench_extra.run_reference(args, rank, world)
+        return bench_extra.run(args, rank, world)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_01983_b200 import workloads
+
+    torch.cuda.set_device(local)
+    if args.workload == "config1":
+        if rank == 0:
+            line = config1_line(args, args.steps, args.warmup, local, args.cpu_seconds)
+            print(json.dumps(line), flush=True)
+        return 0
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    big = args.workload == "config5"
+    w = workloads.config5() if big else workloads.config2()
+    line = allpairs_line(args, w, args.steps, args.warmup, rank, world, local,
+                         2 if big else max(5, min(args.steps, 50)), args.cpu_seconds, not big,
+                         None if big else "r01_allpairs_vel64_ncu_summary.json")
+    if rank == 0:
+        if big and world == 1 and not args.no_extras:
+            line["extra"] = extras(args, local)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

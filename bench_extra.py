@@ -349,11 +349,13 @@ def bench_config4(args, world):
         "metric": "PTROM online instance-steps/s (fp64)", "value": value, "unit": "instance-steps/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K, "units_per_step": units,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded SplitMix64; Fourier-mode basis stands in for the offline POD)",
+        "data": "synthetic (seeded SplitMix64; Φ = 16-mode POD of 200 seeded snapshots, SURVEY.md §8d)",
         "config": {"workload": w.name, "n": w.n, "instances_per_step": B, "mu_instances": len(mu_all),
                    "steps_per_instance": n_steps, "gn_updates_per_step": 5, "modes": basis.modes(),
                    "modes_r": w.phi_r.shape[1], "n_samples": nt, "n_clusters": sur.n_clusters,
-                   "n_direct": sur.n_direct, "offline": offline,
+                   "n_direct": sur.n_direct, "membership_entries": int(len(L["mem_ids"])),
+                   "cluster_list_entries": int(len(L["cl_list"])), "direct_list_entries": int(len(L["d_list"])),
+                   "offline": offline,
                    "l2": "working set (positions of 768k sources x B instances) exceeds L2",
                    "parallelism": "single GPU" if world == 1 else f"mu instances split x{world}"},
         "gpu_launches": ours * K * n_steps if ours is not None else None,

@@ -53,6 +53,13 @@ int ptrom_set_stream(ptrom_ctx* ctx, void* cuda_stream);
 /* Synchronizes the context stream; returns and clears any latched device
  * status (3 with the reference's message when a kernel saw a singularity). */
 int ptrom_synchronize(ptrom_ctx* ctx);
+/* Engine tuning knobs (no reference counterpart; results do not depend on
+ * them). Keys: "reassign_big_members" (clusters above this size take the
+ * one-CTA-per-cluster reassign path, default 4096, min 32), "tree_seq_max"
+ * (tree nodes up to this size get bit-exact sequential sums in the subtree
+ * CTAs, default 2048), "tree_build_mode" (0 Morton, 1 level build),
+ * "allpairs_variant" (tile shape). Unknown keys are status 2. */
+int ptrom_set_tuning(ptrom_ctx* ctx, const char* key, int64_t value);
 /* Library/kernel identification for provenance checks. */
 const char* ptrom_build_info(void);
 
@@ -78,6 +85,15 @@ int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const do
                            int form, const double* inflow, double dt, int64_t n_steps, double tol,
                            int max_iters, int jacobian_refresh_period, double* snapshots, int* iterations,
                            uint8_t* converged, double* relative_residual, uint64_t* n_pair_evals);
+/* ptrom_fom_simulate_f64 on DEVICE buffers (x0 2n, gamma n, inflow 2n or
+ * NULL, snapshots 2n x n_steps column-major or NULL); iterations / converged /
+ * relative_residual are HOST arrays of n_steps. Synchronizes. Reports the
+ * number of velocity and Jacobian (Newton-block refresh) evaluations, each
+ * N(N-1) pairs. */
+int ptrom_dev_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* d_x0, const double* d_gamma, double delta,
+                               int form, const double* d_inflow, double dt, int64_t n_steps, double tol, int max_iters,
+                               int jacobian_refresh_period, double* d_snapshots, int* iterations, uint8_t* converged,
+                               double* relative_residual, uint64_t* n_velocity_evals, uint64_t* n_jacobian_evals);
 /* kernel.hpp:174-191 hamiltonian<double>: Σ_{i<j} Γi Γj log|x_i - x_j| / 2π.
  * A coincident pair is status 3 "hamiltonian: coincident particles i and j"
  * (the lexicographically first pair, as the reference's loop order). */

@@ -25,6 +25,7 @@ PROTOTYPES = {
     "ptrom_last_error": (C.c_char_p, [c_ctxp]),
     "ptrom_set_stream": (C.c_int, [c_ctxp, C.c_void_p]),
     "ptrom_synchronize": (C.c_int, [c_ctxp]),
+    "ptrom_set_tuning": (C.c_int, [c_ctxp, C.c_char_p, c_i64]),
     "ptrom_build_info": (C.c_char_p, []),
     "ptrom_pairwise_velocity_f64": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, c_dp, c_u64p]),
@@ -35,6 +36,9 @@ PROTOTYPES = {
     "ptrom_fom_simulate_f64": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, C.c_double, c_i64, C.c_double,
                   C.c_int, C.c_int, c_dp, c_dp, c_dp, c_dp, c_u64p]),
+    "ptrom_dev_fom_simulate_f64": (
+        C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, C.c_double, c_i64, C.c_double,
+                  C.c_int, C.c_int, c_dp, c_dp, c_dp, c_dp, c_u64p, c_u64p]),
     "ptrom_dev_pairwise_velocity_f64": (
         C.c_int, [c_ctxp, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, c_i64, c_i64, c_dp, c_i64]),
     "ptrom_dev_pairwise_velocity_f32": (

@@ -98,6 +98,10 @@ class Context:
             raise NumericalError(msg)
         raise CudaError(msg)
 
+    def set_tuning(self, key: str, value: int) -> None:
+        """Engine knobs (ptrom_set_tuning); results do not depend on them."""
+        self.check(self.lib.ptrom_set_tuning(self._h, key.encode(), int(value)))
+
     def close(self) -> None:
         if self._h:
             self.lib.ptrom_destroy(self._h)

@@ -24,8 +24,8 @@
 //   (a coincident pair with δ = 0, the reference's throw at kernel.hpp:38-39).
 //
 // Reciprocal (the FP64 pipe is the bound):
-//  * fast path (δ' ≥ 2^-62 and every coordinate of the tile and of the
-//    block's targets below 2^29, so q ∈ [2^-62, 2^61]): two targets share one
+//  * fast path (δ' ∈ [2^-62, 2^60] and every coordinate of the tile and of the
+//    block's targets below 2^29, so q ∈ [2^-62, 2^62)): two targets share one
 //    reciprocal of P = q1·q2 (Montgomery); the double P is re-biased into an
 //    fp32 bit pattern with integer ops (ALU pipe), seeded with MUFU.RCP (fp32,
 //    ≤ 2^-22 rel incl. truncation) and refined by one fp64 Newton step:
@@ -47,8 +47,10 @@ __device__ __forceinline__ double rcp_seed(double q) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
   return y;
 }
-// fp32 reciprocal seed of a double q ∈ [2^-100, 2^122] through integer
-// exponent re-biasing (no FP64-pipe conversion instructions).
+// fp32 reciprocal seed of a double q ∈ [2^-126, 2^126) through integer
+// exponent re-biasing (no FP64-pipe conversion instructions); outside that
+// range the re-biased exponent wraps or the fp32 reciprocal flushes, so every
+// caller guards the range (allpairs_f64_kernel targets_ok / targets_ok4).
 __device__ __forceinline__ double rcp_seed_via_f32(double q) {
   const int hi = __double2hiint(q), lo = __double2loint(q);
   const unsigned fb = __funnelshift_l((unsigned)lo, (unsigned)hi, 3) - (896u << 23);
@@ -272,8 +274,13 @@ __global__ void __launch_bounds__(TPB, MINB) allpairs_f64_kernel(long long n, Sr
     my_ok = my_ok && coord_ok(tx[k]) && coord_ok(ty[k]);
     my_ok4 = my_ok4 && coord_ok4(tx[k]) && coord_ok4(ty[k]);
   }
-  const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62;
-  const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31;
+  // δ' bounded on both sides so the Montgomery product stays inside the fp32
+  // seed's range (rcp_seed_via_f32 needs P ∈ [2^-126, 2^126)):
+  //   2-way: q ∈ [2^-62, 2^61 + 2^60]  → P = q1 q2 < 2^124
+  //   4-way: q ∈ [2^-31, 2^31 + 2^29]  → P = q1 q2 q3 q4 < 2^125.3
+  // (also false for δ' = inf / NaN); otherwise the tile takes the safe path.
+  const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62 && dp <= 0x1p60;
+  const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
 
   // Register prefetch of the first source tile.
   double px = 0.0, py = 0.0, pg = 0.0;
@@ -667,6 +674,9 @@ constexpr int kReduceThreads = 256;
 // Set by dev_velocity_* for the duration of one launch: fuse the chunk
 // reduction into the tile kernel (FusedOut).
 thread_local const FusedOut* g_fuse = nullptr;
+// dev_jacobian_reserve_f64: size the scratch arena of a launch without
+// launching it (graph capture cannot allocate)
+thread_local bool g_size_only = false;
 
 template <class K>
 int resident_blocks(K kernel, int tpb) {
@@ -694,6 +704,11 @@ void launch_allpairs_src(ptrom_ctx* ctx, long long n, Src src, const double* gam
   ctx->scratch.reset();
   ctx->scratch.reserve((size_t)chunks * NCOMP * t_count * sizeof(double) + 4096);
   double* part = ctx->scratch.take<double>((size_t)chunks * NCOMP * t_count);
+  if (g_size_only) {
+    *part_out = part;
+    *chunks_out = chunks;
+    return;
+  }
   dim3 grid((unsigned)tiles, (unsigned)chunks);
   const double inv2pi = 1.0 / (2.0 * M_PI);
   {
@@ -1026,6 +1041,20 @@ void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double
         t_begin, t_count, chunks, part, 3, 0, dp, 0.0, jxx, jxy, jyx, jyy, nullptr, ctx->d_status);
   }
   PTROM_LAUNCH_CHECK();
+}
+
+void dev_jacobian_reserve_f64(ptrom_ctx* ctx, long long n, long long t_count) {
+  if (t_count <= 0) return;
+  double* part;
+  int chunks;
+  g_size_only = true;
+  try {
+    launch_allpairs_f64<false, true>(ctx, n, nullptr, nullptr, 1.0, 0, t_count, &part, &chunks);
+  } catch (...) {
+    g_size_only = false;
+    throw;
+  }
+  g_size_only = false;
 }
 
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,

@@ -116,6 +116,8 @@ int ptrom_create(int device, void* stream, ptrom_ctx** out) {
     if (const char* v = std::getenv("PTROM_ALLPAIRS_VARIANT")) ctx->allpairs_variant = std::atoi(v);
     if (const char* v = std::getenv("PTROM_TREE_SEQ_MAX")) ctx->tree_seq_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("PTROM_TREE_BUILD")) ctx->tree_build_mode = std::string(v) == "levels" ? 1 : 0;
+    if (const char* v = std::getenv("PTROM_REASSIGN_BIG")) ctx->reassign_big = std::max(32LL, std::atoll(v));
+    PTROM_CUDA(cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     PTROM_CUDA(cudaMalloc(&ctx->d_status, sizeof(DeviceStatus)));
     PTROM_CUDA(cudaMallocHost(&ctx->h_status, sizeof(DeviceStatus)));
     PTROM_CUDA(cudaMallocHost(&ctx->h_counts, 128 * sizeof(int)));  // also holds the Morton build state
@@ -151,6 +153,17 @@ const char* ptrom_last_error(const ptrom_ctx* ctx) { return ctx ? ctx->err.c_str
 
 int ptrom_set_stream(ptrom_ctx* ctx, void* stream) {
   return guarded(ctx, [&] { ctx->stream = static_cast<cudaStream_t>(stream); });
+}
+
+int ptrom_set_tuning(ptrom_ctx* ctx, const char* key, int64_t value) {
+  return guarded(ctx, [&] {
+    const std::string k = key ? key : "";
+    if (k == "reassign_big_members") ctx->reassign_big = std::max<long long>(32, value);
+    else if (k == "tree_seq_max") ctx->tree_seq_max = (int)std::max<int64_t>(1, value);
+    else if (k == "tree_build_mode") ctx->tree_build_mode = value ? 1 : 0;
+    else if (k == "allpairs_variant") ctx->allpairs_variant = (int)value;
+    else throw status_error(PTROM_CONFIG_ERROR, "ptrom_set_tuning: unknown key '" + k + "'");
+  });
 }
 
 int ptrom_synchronize(ptrom_ctx* ctx) {
@@ -259,6 +272,27 @@ int ptrom_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* x0, const do
     FomResult r = fom_simulate_device(ctx, n, dx, dg, delta, form, di, dt, n_steps, tol, max_iters,
                                       jacobian_refresh_period, snapshots, iterations, converged, relative_residual);
     if (n_pair_evals) *n_pair_evals = (uint64_t)r.velocity_evals * (uint64_t)n * (uint64_t)(n - 1);
+  });
+}
+
+// integrators.hpp:243-272 on device-resident inputs (x0, gamma, inflow and
+// the snapshot matrix in HBM); step statistics are written to host arrays.
+int ptrom_dev_fom_simulate_f64(ptrom_ctx* ctx, int64_t n, const double* d_x0, const double* d_gamma, double delta,
+                               int form, const double* d_inflow, double dt, int64_t n_steps, double tol, int max_iters,
+                               int jacobian_refresh_period, double* d_snapshots, int* iterations, uint8_t* converged,
+                               double* relative_residual, uint64_t* n_velocity_evals, uint64_t* n_jacobian_evals) {
+  return guarded(ctx, [&] {
+    if (!(dt > 0)) config_fail("time step must be positive");
+    if (n_steps < 0) config_fail("negative step count");
+    if (!(tol > 0)) config_fail("Newton tolerance must be positive");
+    if (max_iters < 1) config_fail("Newton max_iters must be >= 1");
+    if (jacobian_refresh_period < 1) config_fail("Jacobian refresh period must be >= 1");
+    validate_shape(n, form);
+    validate_uploaded<double>(ctx, n, d_x0, d_gamma, delta, d_inflow, "pairwise_velocity");
+    FomResult r = fom_simulate_device(ctx, n, d_x0, d_gamma, delta, form, d_inflow, dt, n_steps, tol, max_iters,
+                                      jacobian_refresh_period, d_snapshots, iterations, converged, relative_residual);
+    if (n_velocity_evals) *n_velocity_evals = (uint64_t)r.velocity_evals;
+    if (n_jacobian_evals) *n_jacobian_evals = (uint64_t)r.jacobian_evals;
   });
 }
 

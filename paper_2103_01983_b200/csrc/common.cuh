@@ -114,6 +114,8 @@ struct ptrom_ctx {
   int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
   ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)
+  long long reassign_big = 4096;  // clusters above this many members take reassign_big_kernel (PTROM_REASSIGN_BIG)
+  int smem_optin = 232448;   // cudaDevAttrMaxSharedMemoryPerBlockOptin
   int tree_build_mode = 0;   // 0: Morton-key build (level build when it does not apply), 1: level build (PTROM_TREE_BUILD=levels)
 };
 

@@ -96,6 +96,7 @@ __global__ void newton_update_kernel(long long m, long long ld, const double* __
 struct FomCtl {
   long long step;
   long long evals;  // velocity evaluations (the reference's counter / N(N-1))
+  long long jac_evals;  // Newton-block refreshes (inexact_kernel_jacobian evaluations)
   double r0, rel;
   int updates, converged, have_blocks, refreshed, do_refresh;
   unsigned ticket;  // residual blocks done (the last one decides)
@@ -178,8 +179,11 @@ __global__ void __launch_bounds__(kNormThreads) residual_decide_kernel(
 }
 
 // First node of the loop body: arms the IF node of the Newton-block refresh.
-__global__ void fom_refresh_gate_kernel(const FomCtl* c, cudaGraphConditionalHandle h_refresh) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) cudaGraphSetConditional(h_refresh, c->do_refresh ? 1u : 0u);
+__global__ void fom_refresh_gate_kernel(FomCtl* c, cudaGraphConditionalHandle h_refresh) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    cudaGraphSetConditional(h_refresh, c->do_refresh ? 1u : 0u);
+    if (c->do_refresh) c->jac_evals += 1;
+  }
 }
 
 // StepResult + snapshot column of the accepted state (integrators.hpp:262-268).
@@ -294,9 +298,10 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
   FomCtl* ctl = (FomCtl*)alloc(sizeof(FomCtl));
   PTROM_CUDA(cudaMemsetAsync(ctl, 0, sizeof(FomCtl), st));
 
-  // x = x0; f = model.velocity(x0)   (integrators.hpp:257-259); also sizes the scratch
+  // x = x0; f = model.velocity(x0)   (integrators.hpp:257-259); the Jacobian
+  // path's scratch is sized without evaluating it (capture cannot allocate)
   PTROM_CUDA(cudaMemcpyAsync(x_prev, d_x0, dim * 8, cudaMemcpyDeviceToDevice, st));
-  dev_jacobian_f64(ctx, n, x_prev, d_gamma, delta, form, 0, n, nullptr, nullptr, nullptr, nullptr, dt, inv);
+  dev_jacobian_reserve_f64(ctx, n, n);
   dev_velocity_f64(ctx, n, x_prev, d_gamma, delta, form, d_inflow, 0, n, f_prev, n);
   ++out.velocity_evals;
   PTROM_CUDA(cudaStreamSynchronize(st));
@@ -384,11 +389,12 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
     PTROM_CUDA(cudaMemcpyAsync(conv, d_conv, n_steps, cudaMemcpyDeviceToHost, st));
     PTROM_CUDA(cudaMemcpyAsync(rel_out, d_rel, n_steps * 8, cudaMemcpyDeviceToHost, st));
     if (h_snapshots)
-      PTROM_CUDA(cudaMemcpyAsync(h_snapshots, snaps, (size_t)dim * n_steps * 8, cudaMemcpyDeviceToHost, st));
+      PTROM_CUDA(cudaMemcpyAsync(h_snapshots, snaps, (size_t)dim * n_steps * 8, cudaMemcpyDefault, st));
   }
   PTROM_CUDA(cudaStreamSynchronize(st));
   check_device_status(ctx);
   out.velocity_evals += hc.evals;
+  out.jacobian_evals += hc.jac_evals;
   return out;
 }
 
@@ -466,6 +472,7 @@ FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, c
       if (updates >= max_iters) break;
       if (refresh_due && !refreshed) {
         dev_jacobian_f64(ctx, n, xi, d_gamma, delta, form, 0, n, nullptr, nullptr, nullptr, nullptr, dt, inv);
+        ++out.jacobian_evals;
         refreshed = true;
         have_blocks = true;
       }
@@ -479,7 +486,7 @@ FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, c
     std::swap(f_prev, fxi);
     if (h_snapshots)
       PTROM_CUDA(cudaMemcpyAsync(h_snapshots + (size_t)s * dim, x_prev, dim * sizeof(double),
-                                 cudaMemcpyDeviceToHost, ctx->stream));
+                                 cudaMemcpyDefault, ctx->stream));
     iters[s] = updates;
     conv[s] = converged ? 1 : 0;
     rel_out[s] = rel;

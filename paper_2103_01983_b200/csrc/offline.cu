@@ -398,6 +398,7 @@ void offline_cluster_pod(ptrom_ctx* ctx, const DBasis& b, const double* d_gamma,
   s.n_c = nc;
   s.u = u;
   s.n_t = nt;
+  for (long long c = 0; c < nc; ++c) s.max_members = std::max(s.max_members, mem_off[c + 1] - mem_off[c]);
   auto up = [&](const void* h, size_t bytes) {
     void* d = dalloc(bytes);
     if (bytes) PTROM_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));

@@ -17,6 +17,9 @@ void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* 
                       const float* inflow, long long t_begin, long long t_end, float* f, long long ld);
 // jxx..jyy (may be null when inv is given) or the Newton-block inverse of
 // (I - dt/2 J) into inv (4 per row) when inv != nullptr.
+// Sizes the context's scratch for dev_jacobian_f64 over t_count targets
+// without launching (before a graph capture).
+void dev_jacobian_reserve_f64(ptrom_ctx* ctx, long long n, long long t_count);
 void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
                       long long t_begin, long long t_end, double* jxx, double* jxy, double* jyx, double* jyy,
                       double dt_for_inverse, double* inv);
@@ -35,6 +38,7 @@ size_t residual_block_part_count();
 
 struct FomResult {
   long long velocity_evals = 0;
+  long long jacobian_evals = 0;
 };
 FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, const double* d_gamma, double delta,
                               int form, const double* d_inflow, double dt, long long n_steps, double tol,

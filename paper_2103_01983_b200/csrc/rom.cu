@@ -76,14 +76,14 @@ __global__ void basis_rowmajor_kernel(DBasis b) {
 // once (one division per lane), then lane j owns column j (mode j, or x_ref
 // for j == m) of both rows and accumulates w_p·Φ(p, j) member by member.
 // The arithmetic is the reference's, so Φ̃, x̃⁰ and Γ̃ are bit-identical.
-constexpr long long kBigCluster = 4096;  // members: above, one CTA per cluster (reassign_big_kernel)
-
-__global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __restrict__ gamma) {
+// Clusters above `big` members (ctx->reassign_big, default 4096) take one CTA
+// each (reassign_big_kernel); the rest a warp each.
+__global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __restrict__ gamma, long long big) {
   const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (c >= s.n_c) return;
   const long long b0 = s.mem_off[c], b1 = s.mem_off[c + 1];
-  if (b1 - b0 > kBigCluster) return;
+  if (b1 - b0 > big) return;
   double gsum = 0.0;
   for (long long k0 = b0; k0 < b1; k0 += 32) {
     const int cnt = (int)min(32LL, b1 - k0);
@@ -126,9 +126,9 @@ __global__ void reassign_exact_kernel(DSurrogate s, DBasis b, const double* __re
   }
 }
 
-__global__ void big_clusters_kernel(DSurrogate s, int* __restrict__ list, int* __restrict__ count) {
+__global__ void big_clusters_kernel(DSurrogate s, long long big, int* __restrict__ list, int* __restrict__ count) {
   const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (c < s.n_c && s.mem_off[c + 1] - s.mem_off[c] > kBigCluster) list[atomicAdd(count, 1)] = (int)c;
+  if (c < s.n_c && s.mem_off[c + 1] - s.mem_off[c] > big) list[atomicAdd(count, 1)] = (int)c;
 }
 
 // reduction.hpp:400-431 for the large clusters, one CTA each. Warps 1..7
@@ -1139,17 +1139,33 @@ void rom_basis_rowmajor(ptrom_ctx* ctx, DBasis& b) {
 void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const double* d_gamma) {
   if (s.n_c > 0) {
     if (b.m > 63) throw status_error(PTROM_CONFIG_ERROR, "reassign: at most 63 modes");
-    int* big;  // [0] count, then the list of clusters above kBigCluster members
-    PTROM_CUDA(cudaMallocAsync(&big, sizeof(int) * (s.n_c + 1), ctx->stream));
-    PTROM_CUDA(cudaMemsetAsync(big, 0, sizeof(int), ctx->stream));
-    big_clusters_kernel<<<blocks_for(s.n_c, 256), 256, 0, ctx->stream>>>(s, big + 1, big);
-    const int ch = b.m <= 16 ? 256 : 128;  // members per weighted-pass chunk
-    const size_t smem = sizeof(double) * (2 * (size_t)ch * 2 * (b.m + 1) + 2 * std::max(ch, kBigGChunk)) +
-                        sizeof(long long) * 2 * ch;
-    PTROM_CUDA(cudaFuncSetAttribute(reassign_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    reassign_big_kernel<<<ctx->num_sms, 256, smem, ctx->stream>>>(s, b, d_gamma, big + 1, big, ch);
-    reassign_exact_kernel<<<blocks_for(s.n_c * 32, 256), 256, 0, ctx->stream>>>(s, b, d_gamma);
-    PTROM_CUDA(cudaFreeAsync(big, ctx->stream));
+    const long long big_thr = std::max<long long>(32, ctx->reassign_big);
+    // Clusters above big_thr members: one CTA each. Their count is known on
+    // the host from the membership offsets' maximum, which the surrogate
+    // records when it is built (max_members); the CTA path is launched only
+    // when some cluster needs it.
+    if (s.max_members > big_thr) {
+      int* big;  // [0] count, then the list of clusters above big_thr members
+      PTROM_CUDA(cudaMallocAsync(&big, sizeof(int) * (s.n_c + 1), ctx->stream));
+      PTROM_CUDA(cudaMemsetAsync(big, 0, sizeof(int), ctx->stream));
+      big_clusters_kernel<<<blocks_for(s.n_c, 256), 256, 0, ctx->stream>>>(s, big_thr, big + 1, big);
+      // members per weighted-pass chunk: the largest multiple of 32 (<= 256)
+      // whose double-buffered rows fit the opt-in shared memory of one CTA
+      const size_t row = sizeof(double) * 2 * (b.m + 1);
+      const size_t fixed_b = sizeof(double) * 2 * kBigGChunk;
+      int ch = 256;
+      auto bytes = [&](int c) {
+        return 2 * (size_t)c * row + sizeof(double) * 2 * (size_t)std::max(c, kBigGChunk) +
+               sizeof(long long) * 2 * (size_t)c;
+      };
+      while (ch > 32 && bytes(ch) > (size_t)ctx->smem_optin) ch -= 32;
+      (void)fixed_b;
+      const size_t smem = bytes(ch);
+      PTROM_CUDA(cudaFuncSetAttribute(reassign_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      reassign_big_kernel<<<ctx->num_sms, 256, smem, ctx->stream>>>(s, b, d_gamma, big + 1, big, ch);
+      PTROM_CUDA(cudaFreeAsync(big, ctx->stream));
+    }
+    reassign_exact_kernel<<<blocks_for(s.n_c * 32, 256), 256, 0, ctx->stream>>>(s, b, d_gamma, big_thr);
   }
   if (s.u > 0) direct_gamma_kernel<<<blocks_for(s.u, 256), 256, 0, ctx->stream>>>(s, d_gamma);
   PTROM_LAUNCH_CHECK();

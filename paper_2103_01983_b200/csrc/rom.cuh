@@ -39,6 +39,7 @@ struct DSurrogate {
   unsigned char* zero_gamma = nullptr;
   long long* mem_off = nullptr;  // n_c + 1
   long long* mem_ids = nullptr;  // ascending particle ids per cluster
+  long long max_members = 0;     // largest cluster (host-side; picks the reassign path)
   long long* target_ids = nullptr;
   int* t_order = nullptr;  // processing order of the targets (spatial; null = identity)
   long long* cl_off = nullptr;  // n_t + 1

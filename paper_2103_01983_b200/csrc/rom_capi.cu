@@ -260,6 +260,8 @@ int ptrom_surrogate_create(ptrom_ctx* ctx, int64_t modes, int64_t n_clusters, co
       s.gamma_tilde = h->mem.up(gamma_tilde, nc);
       s.zero_gamma = h->mem.up(zero_gamma, zero_gamma ? nc : 0);
       s.mem_off = h->mem.up(reinterpret_cast<const long long*>(membership_offsets), nc + 1);
+      for (size_t c = 0; c < nc; ++c)
+        s.max_members = std::max<long long>(s.max_members, membership_offsets[c + 1] - membership_offsets[c]);
       s.mem_ids = h->mem.up(reinterpret_cast<const long long*>(membership_ids), (size_t)membership_offsets[nc]);
       h->target_ids.assign(target_ids, target_ids + nt);
       s.target_ids = h->mem.up(reinterpret_cast<const long long*>(target_ids), nt);

@@ -51,6 +51,30 @@ def pairwise_velocity(x: torch.Tensor, gamma: torch.Tensor, delta: float, form: 
     return out
 
 
+def fom_simulate(x0: torch.Tensor, gamma: torch.Tensor, delta: float, dt: float, n_steps: int, form: int = 0,
+                 inflow: Optional[torch.Tensor] = None, tol: float = 1e-10, max_iters: int = 100, refresh: int = 1,
+                 snapshots: Optional[torch.Tensor] = None, ctx: Optional[Context] = None):
+    """integrators.hpp:243-272 on device-resident state (ptrom_dev_fom_simulate_f64):
+    returns (snapshots (n_steps, 2n) on the device, iterations, converged,
+    relative_residual, velocity evaluations, Jacobian evaluations). Synchronizes."""
+    import ctypes as C
+
+    import numpy as np
+    n = gamma.shape[0]
+    if snapshots is None:
+        snapshots = torch.empty(max(n_steps, 1), 2 * n, dtype=torch.float64, device=x0.device)
+    it = np.zeros(max(n_steps, 1), np.int32)
+    cv = np.zeros(max(n_steps, 1), np.uint8)
+    rr = np.zeros(max(n_steps, 1), np.float64)
+    nv, nj = C.c_uint64(), C.c_uint64()
+    ctx = _ctx(ctx, x0)
+    ctx.check(ctx.lib.ptrom_dev_fom_simulate_f64(ctx.handle, n, _ptr(x0), _ptr(gamma), float(delta), int(form),
+                                                 _ptr(inflow), float(dt), int(n_steps), float(tol), int(max_iters),
+                                                 int(refresh), _ptr(snapshots), it.ctypes.data, cv.ctypes.data,
+                                                 rr.ctypes.data, C.byref(nv), C.byref(nj)))
+    return snapshots[:n_steps], it[:n_steps], cv[:n_steps], rr[:n_steps], nv.value, nj.value
+
+
 def inexact_kernel_jacobian(x: torch.Tensor, gamma: torch.Tensor, delta: float, form: int = 0, t_begin: int = 0,
                             t_end: Optional[int] = None, ctx: Optional[Context] = None) -> torch.Tensor:
     """kernel.hpp:154-170 rows [t_begin, t_end) → (4, m): dfx_dx, dfx_dy, dfy_dx, dfy_dy."""

@@ -131,14 +131,46 @@ def _orthonormal(a: np.ndarray) -> np.ndarray:
     return np.asfortranarray(q)
 
 
+N_FIELDS = 24      # smooth Fourier displacement fields in the snapshot family
+N_SNAPSHOTS = 200
+
+
+def pod_of_snapshots(x0: np.ndarray, fields: np.ndarray, amps: np.ndarray, modes: int):
+    """build_pod (reduction.hpp:32-66) of the snapshot matrix
+    S = x0·1ᵀ + 1e-2·F·Aᵀ (columns s = x0 + 1e-2·Σ_k a_ks F_k), computed
+    without forming the 2N x n_s matrix: S = B Cᵀ with B = [x0, F] and
+    C = [1, 1e-2·A], so with B = Q_B R_B, S = Q_B (R_B Cᵀ) and the thin SVD of
+    the small (K+1) x n_s factor gives U = Q_B Û and σ. The numerical-rank
+    check and the sign rule (largest-magnitude entry positive, first on ties)
+    are the reference's."""
+    b = np.concatenate([x0[:, None], fields], axis=1)
+    c = np.concatenate([np.ones((amps.shape[0], 1)), 1e-2 * amps], axis=1)
+    qb, rb = np.linalg.qr(b)
+    uh, sv, _ = np.linalg.svd(rb @ c.T, full_matrices=False)
+    cutoff = max(x0.shape[0], amps.shape[0]) * np.finfo(np.float64).eps * sv[0]
+    rank = int(np.sum(sv > cutoff))
+    if modes > rank:
+        raise ValueError(f"build_pod: requested {modes} modes but snapshots have numerical rank {rank}")
+    phi = qb @ uh[:, :modes]
+    for c_ in range(modes):
+        arg = int(np.argmax(np.abs(phi[:, c_])))
+        if phi[arg, c_] < 0:
+            phi[:, c_] = -phi[:, c_]
+    return np.asfortranarray(phi), sv[:modes].copy()
+
+
 def config4(n: int = 1 << 20, n_inst: int = 4096, modes: int = 16, modes_r: int = 32, n_steps: int = 50,
             seed: int = 4) -> PtromWorkload:
     """Two patches as config 3; Γ(μ) = 2/N on patch A and μ·2/N on patch B, μ ~ U[0.5, 2] (seeded).
 
-    Φ: M smooth Fourier displacement fields (seeded wavenumbers/phases) evaluated at the bodies and
-    orthonormalized — it stands in for the offline POD of seeded random snapshots (build_pod is an
-    offline producer, out of scope), with singular values 2^{-k/2}. Φ_r: seeded
-    random orthonormal 2N x M_r (as test_rom.cpp:50-58). Samples n = ceil(0.02 N)."""
+    Φ: the M-mode POD (build_pod, reduction.hpp:32-66)
+    of 200 seeded snapshots x0 + 1e-2·Σ_k a_ks·F_k over 24 smooth Fourier
+    displacement fields F_k = (cos(a·x + b·y + φ), sin(c·x + e·y + ψ)) with
+    seeded wavenumbers in [-3π, 3π] and seeded phases, amplitudes
+    a_ks ~ N(0, 1)/k (a decaying spectrum); σ are the snapshot matrix's own
+    singular values (they weight the POD space W = Φσ the surrogate tree is
+    built on, reduction.hpp:74-77). Φ_r: seeded random orthonormal 2N x M_r
+    (as test_rom.cpp:50-58). Samples n = ceil(0.02 N)."""
     base = config3(n, seed=3)
     rng = SplitMix64(seed)
     x, y = base.x0[:n], base.x0[n:]
@@ -147,15 +179,16 @@ def config4(n: int = 1 << 20, n_inst: int = 4096, modes: int = 16, modes_r: int 
     gb = np.zeros(n)
     ga[:half] = 2.0 / n
     gb[half:] = 2.0 / n
-    waves = rng.uniform(4 * modes) * 6.0 - 3.0
-    phases = rng.uniform(2 * modes) * 2.0 * np.pi
-    fields = np.empty((2 * n, modes))
-    for k in range(modes):
+    nf = max(N_FIELDS, modes + 8)
+    waves = rng.uniform(4 * nf) * 6.0 - 3.0
+    phases = rng.uniform(2 * nf) * 2.0 * np.pi
+    fields = np.empty((2 * n, nf))
+    for k in range(nf):
         a, b, c, e = waves[4 * k:4 * k + 4] * np.pi
         fields[:n, k] = np.cos(a * x + b * y + phases[2 * k])
         fields[n:, k] = np.sin(c * x + e * y + phases[2 * k + 1])
-    phi = _orthonormal(fields)
-    sv = 2.0 ** (-0.5 * np.arange(1, modes + 1))
+    amps = rng.normal(N_SNAPSHOTS * nf).reshape(N_SNAPSHOTS, nf) / np.arange(1, nf + 1)[None, :]
+    phi, sv = pod_of_snapshots(base.x0, fields, amps, modes)
     phi_r = _orthonormal(rng.normal(2 * n * modes_r).reshape(modes_r, 2 * n).T)
     mu = 0.5 + 1.5 * rng.uniform(n_inst)
     return PtromWorkload("config4_ptrom_n%d" % n, n, base.x0.copy(), ga, gb, phi, sv, phi_r, mu, 0.005 ** 2, 1e-3,

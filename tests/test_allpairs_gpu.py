@@ -50,6 +50,20 @@ def test_velocity_config2_full_size_rows(pt, oracle):
         assert rel(f[rows], ref[rows]) <= FP64_TOL
 
 
+def test_velocity_config5_full_size_rows(pt, oracle):
+    """BASELINE configs[4] at its full size, N = 4,194,304 (δ = 1e-3): one
+    evaluation through the host C ABI (17.6e12 pairs), then 3 x 512 target
+    rows (start, middle, end) against every source on the oracle."""
+    w = workloads.config5()
+    n = w.n
+    f = pt.pairwise_velocity(w.x0, pt.ParticleSystem(w.gamma, w.delta))
+    assert np.all(np.isfinite(f))
+    for b in (0, n // 2 - 256, n - 512):
+        ref = oracle.pairwise_velocity(w.x0, w.gamma, w.delta, t_begin=b, t_end=b + 512, threads=THREADS)
+        rows = np.r_[b:b + 512, n + b:n + b + 512]
+        assert rel(f[rows], ref[rows]) <= FP64_TOL, b
+
+
 def test_velocity_config2_fp32(pt, oracle):
     w = workloads.config2()
     x32 = w.x0.astype(np.float32)
@@ -174,6 +188,30 @@ def test_reciprocal_tiers_match_oracle(pt, oracle, scale, delta):
     ref = oracle.pairwise_velocity(x, g, delta, t_end=1500, threads=THREADS)
     rows = np.r_[0:1500, n:n + 1500]
     assert rel(f[rows], ref[rows]) <= FP64_TOL
+
+
+@pytest.mark.parametrize("scale,delta", [(1.0, 1e9), (1.0, 5e9), (1.0, 1e10), (1e3, 1e12), (1.0, 1e20),
+                                         (2.0 ** 13, 2.0 ** 29), (2.0 ** 13, 2.0 ** 29 * 1.0000001),
+                                         (2.0 ** 28, 2.0 ** 60), (2.0 ** 28, 2.0 ** 61), (1.0, 1e200)])
+def test_reciprocal_tiers_large_delta_small_coordinates(pt, oracle, scale, delta):
+    """δ' above the fast tiers' product range: the 4-way tier needs δ' ≤ 2^29
+    and the 2-way tier δ' ≤ 2^60 (the fp32 seed of P = Π q must stay inside
+    [2^-126, 2^126)); beyond that the tile must take the safe per-pair tier
+    and still match the reference (kernel.hpp:29-42)."""
+    rng = np.random.default_rng(int(np.log2(delta)) + 3)
+    n = 4096 + 19
+    x = rng.uniform(-1.0, 1.0, 2 * n) * scale
+    g = rng.uniform(-1.0, 1.0, n)
+    for form in (0, 1):
+        f = pt.pairwise_velocity(x, pt.ParticleSystem(g, delta, None, form))
+        ref = oracle.pairwise_velocity(x, g, delta, form, t_end=700, threads=THREADS)
+        rows = np.r_[0:700, n:n + 700]
+        assert np.all(np.isfinite(f))
+        assert rel(f[rows], ref[rows]) <= FP64_TOL, (form, delta)
+    jac = pt.inexact_kernel_jacobian(x[np.r_[0:600, n:n + 600]], pt.ParticleSystem(g[:600], delta))
+    refj = oracle.inexact_kernel_jacobian(x[np.r_[0:600, n:n + 600]], g[:600], delta, 0, threads=THREADS)
+    got = np.stack([jac.dfx_dx, jac.dfx_dy, jac.dfy_dx, jac.dfy_dy])
+    assert rel(got, refj) <= FP64_TOL
 
 
 def test_empty_system_is_a_config_error(pt):

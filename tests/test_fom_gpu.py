@@ -30,6 +30,27 @@ def test_config1_full_trajectory_parity(pt, oracle):
     assert mismatch <= w.n_steps // 10
 
 
+def test_device_resident_fom_simulate(pt, oracle):
+    """ptrom_dev_fom_simulate_f64 (device x0/Γ/snapshots): same trajectory as
+    the host entry point, bit for bit, and the evaluation counters add up
+    (one velocity evaluation per Newton update plus the initial one; one
+    Newton-block refresh per step that updates, refresh period 1)."""
+    import torch
+    from paper_2103_01983_b200 import device as dev
+    w = workloads.config1(n=1000)
+    steps = 12
+    run = pt.fom_simulate(w.x0, pt.ParticleSystem(w.gamma, w.delta), pt.TimeGrid(w.dt, steps))
+    snaps, it, cv, rr, nv, nj = dev.fom_simulate(torch.tensor(w.x0, device="cuda"),
+                                                 torch.tensor(w.gamma, device="cuda"), w.delta, w.dt, steps)
+    got = snaps.cpu().numpy().T
+    assert np.array_equal(got, run.snapshots)
+    assert list(it) == list(run.iterations)
+    assert nv == 1 + int(np.sum(it))
+    assert nj == int(np.sum(np.asarray(it) > 0))
+    ref, _, _, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps)
+    assert max(rel(got[:, s], ref[:, s]) for s in range(steps)) <= 1e-12
+
+
 def co_rotation(gamma, d, cx, cy, t):
     omega = gamma / (np.pi * d * d)
     phi = omega * t

@@ -56,6 +56,45 @@ def test_reassign_is_bit_exact(pt, prob):
     np.testing.assert_array_equal(e["direct_gamma"], os_.direct_gamma)
 
 
+@pytest.mark.parametrize("modes,big", [(16, 32), (16, 100), (5, 64), (48, 32), (63, 40), (63, 4096)])
+def test_reassign_big_cluster_path_bit_exact(pt, oracle, modes, big):
+    """reduction.hpp:400-431 through the one-CTA-per-cluster path
+    (reassign_big_kernel): the threshold is lowered so clusters of this
+    N = 4,096 problem take it (config 4's largest cluster has ~2e5 members),
+    and the mode count reaches the 63-mode limit, where the chunk of staged
+    rows is sized from the opt-in shared memory. Tables bitwise."""
+    from paper_2103_01983_b200 import rom
+    from paper_2103_01983_b200.api import Context
+    p = Problem(oracle, n=4096, modes=modes, modes_r=max(32, modes + 1), n_inst=2, seed=7)
+    w = p.w
+    ctx = Context(0)
+    ctx.set_tuning("reassign_big_members", big)
+    os_ = p.surrogate()
+    sizes = np.diff(np.asarray(os_.mem_off))
+    assert sizes.max() > big or big == 4096
+    basis = rom.PODBasis(w.phi, w.sv, w.x0, ctx=ctx)
+    # device-built surrogate (cluster_pod runs the same reassign at μ = 1;
+    # the host-table constructor is limited to the online engine's 32 modes)
+    from paper_2103_01983_b200.tree import ClusterCriterion
+    ds = rom.SurrogateSourceBasis.cluster_pod(basis, p.g1, p.ids, ClusterCriterion.neighbor(1.0), 1)
+    e = ds.export()
+    np.testing.assert_array_equal(e["phi_tilde"], os_.phi_tilde)
+    np.testing.assert_array_equal(e["x0_tilde"], os_.x0_tilde)
+    for mu in (1.37, 0.0):  # μ = 0 zeroes patch B: zero-circulation clusters take the 1/|c| fallback
+        g = w.gamma_a + mu * w.gamma_b
+        os_.reassign(g)
+        ds.reassign_cluster_circulation(g, basis)
+        e = ds.export()
+        np.testing.assert_array_equal(e["phi_tilde"], os_.phi_tilde)
+        np.testing.assert_array_equal(e["x0_tilde"], os_.x0_tilde)
+        np.testing.assert_array_equal(e["gamma_tilde"], os_.gamma_tilde)
+        np.testing.assert_array_equal(e["direct_gamma"], os_.direct_gamma)
+    del ds, basis
+    with pytest.raises(pt.ConfigError):
+        ctx.set_tuning("no_such_knob", 1)
+    ctx.close()
+
+
 @pytest.mark.parametrize("delta,form", [(2.5e-5, 0), (0.01, 1)])
 def test_hyperpair_parity(pt, prob, delta, form):
     from paper_2103_01983_b200 import rom
@@ -253,3 +292,90 @@ def test_config4_pipeline_built_on_device(pt, oracle):
         xo, it_o, _ = oracle.ptrom_simulate(os_, w.phi, w.sv, w.x0, ids, A_o, w.gamma_a + m * w.gamma_b, w.delta,
                                             w.dt, steps, 1e-300, 5)
         assert max(rel(tr.x_hat[i, s], xo[:, s]) for s in range(steps)) <= 1e-12
+
+
+@pytest.fixture(scope="module")
+def config4_full(pt, oracle):
+    """BASELINE configs[3] at its full size, N = 1,048,576:
+    Φ the 16-mode POD of 200 seeded snapshots, M_r = 32, n_t = 20,972.
+    Sample ids and A come from the product (the oracle's greedy scan at this
+    N is ~2e10 score evaluations; ids are pinned byte-equal at smaller N), so
+    both sides consume identical bytes."""
+    from paper_2103_01983_b200 import rom
+    from paper_2103_01983_b200.tree import ClusterCriterion
+    w = workloads.config4(n_inst=4)
+    ids = rom.greedy_sample(w.phi_r, w.n_samples)
+    A = rom.build_gnat_operator(w.phi_r, ids)
+    g1 = w.gamma_a + w.gamma_b
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, ids, A)
+    ds = rom.SurrogateSourceBasis.cluster_pod(basis, g1, ids, ClusterCriterion.neighbor(1.0), 1)
+    os_ = oracle.Surrogate(w.phi, w.sv, w.x0, g1, ids, 1, 1.0, 1)
+    return w, ids, A, g1, basis, op, ds, os_
+
+
+def test_config4_full_size_surrogate_equals_oracle(pt, config4_full):
+    """Full-N weighted POD tree (leaf 1) + cluster_pod(neighbor p_c = 1):
+    every list byte-equal and every table bitwise (reduction.hpp:236-385),
+    including the > 4,096-member clusters (reassign_big_kernel)."""
+    w, ids, A, g1, basis, op, ds, os_ = config4_full
+    L = ds.export_lists()
+    sizes = np.diff(os_.mem_off)
+    assert sizes.max() > 4096  # the one-CTA-per-cluster reassign path is exercised
+    np.testing.assert_array_equal(L["cluster_node_ids"], os_.cluster_node_ids)
+    for k, ok in (("mem_off", os_.mem_off), ("mem_ids", os_.mem_ids), ("cl_off", os_.cl_off),
+                  ("cl_list", os_.cl_list), ("direct_ids", os_.direct_ids), ("d_off", os_.d_off),
+                  ("d_list", os_.d_list)):
+        np.testing.assert_array_equal(L[k], ok, err_msg=k)
+    e = ds.export()
+    for k in ("phi_tilde", "x0_tilde", "gamma_tilde", "direct_gamma"):
+        np.testing.assert_array_equal(e[k], getattr(os_, k), err_msg=k)
+
+
+def test_config4_full_size_reassign_bit_exact(pt, config4_full):
+    """reduction.hpp:400-431 at N = 1M for μ = 1.37: the 203 clusters above
+    4,096 members (largest ~2.4e5) go through reassign_big_kernel."""
+    w, ids, A, g1, basis, op, ds, os_ = config4_full
+    g = w.gamma_a + 1.37 * w.gamma_b
+    from paper_2103_01983_b200 import rom
+    from oracle import pyoracle
+    o2 = pyoracle.Surrogate(w.phi, w.sv, w.x0, g1, ids, 1, 1.0, 1)
+    o2.reassign(g)
+    d2 = rom.SurrogateSourceBasis.from_tables(
+        os_.phi_tilde, os_.gamma_tilde, os_.x0_tilde, os_.zero_gamma, os_.mem_off, os_.mem_ids, os_.targets,
+        os_.cl_off, os_.cl_list, os_.direct_ids, os_.direct_phi, os_.direct_x0, os_.direct_gamma, os_.d_off,
+        os_.d_list)
+    d2.reassign_cluster_circulation(g, basis)
+    e = d2.export()
+    for k in ("phi_tilde", "x0_tilde", "gamma_tilde", "direct_gamma"):
+        np.testing.assert_array_equal(e[k], getattr(o2, k), err_msg=k)
+
+
+def test_config4_full_size_ptrom_simulate(pt, oracle, config4_full):
+    """rom.hpp:404-412 at N = 1M: the single-instance drop-in (exact
+    reassign, 1 instance x 2 steps) and the batched affine path (2 instances
+    x 2 steps), both against the oracle's ptrom_simulate; RomConfig{1e-300,
+    5, 1} as the §8d config (5 GN updates, 6 hyperpair calls per step)."""
+    from paper_2103_01983_b200 import rom
+    w, ids, A, g1, basis, op, ds, os_ = config4_full
+    steps = 2
+    mu0 = float(w.mu[0])
+    g = w.gamma_a + mu0 * w.gamma_b
+    xo, it_o, cv_o = oracle.ptrom_simulate(oracle.Surrogate(w.phi, w.sv, w.x0, g1, ids, 1, 1.0, 1), w.phi, w.sv,
+                                           w.x0, ids, A, g, w.delta, w.dt, steps, 1e-300, 5)
+    d1 = rom.SurrogateSourceBasis.from_tables(
+        os_.phi_tilde, os_.gamma_tilde, os_.x0_tilde, os_.zero_gamma, os_.mem_off, os_.mem_ids, os_.targets,
+        os_.cl_off, os_.cl_list, os_.direct_ids, os_.direct_phi, os_.direct_x0, os_.direct_gamma, os_.d_off,
+        os_.d_list)
+    tr = rom.ptrom_simulate(basis, op, d1, pt.ParticleSystem(g, w.delta), pt.TimeGrid(w.dt, steps),
+                            rom.RomConfig(1e-300, 5, 1.0))
+    np.testing.assert_array_equal(tr.iterations, it_o)
+    assert max(rel(tr.x_hat[:, s], xo[:, s]) for s in range(steps)) <= 1e-12
+    mus = np.array([w.mu[1], w.mu[2]])
+    tb = rom.ptrom_simulate_batch(basis, op, ds, w.gamma_a, w.gamma_b, mus, pt.ParticleSystem(g1, w.delta),
+                                  pt.TimeGrid(w.dt, steps), rom.RomConfig(1e-300, 5, 1.0))
+    for i, m in enumerate(mus):
+        xo, it_o, _ = oracle.ptrom_simulate(oracle.Surrogate(w.phi, w.sv, w.x0, g1, ids, 1, 1.0, 1), w.phi, w.sv,
+                                            w.x0, ids, A, w.gamma_a + m * w.gamma_b, w.delta, w.dt, steps, 1e-300, 5)
+        np.testing.assert_array_equal(tb.iterations[i], it_o)
+        assert max(rel(tb.x_hat[i, s], xo[:, s]) for s in range(steps)) <= 1e-12, m
