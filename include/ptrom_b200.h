@@ -323,6 +323,75 @@ int ptrom_surrogate_export_lists(ptrom_ctx* ctx, const ptrom_surrogate* sur, int
                                  int64_t* direct_ids, int64_t* d_off, int64_t* d_list, double* direct_phi,
                                  double* direct_x0);
 
+/* ---------------------------------------------------- multi-GPU -- */
+/* SURVEY.md §8b "Multi-GPU: ptrom_comm_init + *_sharded variants". One
+ * process (or host thread) per GPU, one ptrom_ctx and one ptrom_comm per rank.
+ * Collectives run on the context's stream.
+ *
+ * NCCL transport: rank 0 calls ptrom_comm_unique_id, the host distributes the
+ * 128 bytes to every rank by its own means (MPI_Bcast, a file, a TCP store),
+ * and every rank calls ptrom_comm_init. libnccl.so.2 is loaded at run time.
+ *
+ * Host transport: the caller supplies the two collectives on HOST buffers
+ * (an MPI / gloo / shared-memory host already has them); device data is
+ * staged through the host and each collective synchronizes. Callbacks return
+ * 0 on success. all_gather receives `bytes` from every rank into
+ * recv[r * bytes ...] in rank order. */
+typedef struct ptrom_comm ptrom_comm;
+typedef struct {
+  int (*all_gather)(void* user, const void* send, void* recv, uint64_t bytes);
+  int (*broadcast)(void* user, void* buf, uint64_t bytes, int root);
+} ptrom_host_collectives;
+int ptrom_comm_unique_id(uint8_t id_out[128]);
+int ptrom_comm_init(ptrom_ctx* ctx, int rank, int world, const uint8_t id[128], ptrom_comm** out);
+int ptrom_comm_init_host(ptrom_ctx* ctx, int rank, int world, const ptrom_host_collectives* ops, void* user,
+                         ptrom_comm** out);
+void ptrom_comm_destroy(ptrom_comm* comm);
+/* 1 for the NCCL transport, 0 for host callbacks. */
+int ptrom_comm_transport(const ptrom_comm* comm);
+
+/* Target-sharded velocity (kernel.hpp:107-129 for this rank's rows): rank r
+ * owns particles [r*n/G, (r+1)*n/G) (m of them). d_x_local is its 2m SoA rows
+ * [x..., y...]; the positions of all ranks are exchanged into d_x_full (2n,
+ * workspace) and d_f_local (2m) receives this rank's velocities (+ inflow,
+ * d_inflow 2n or NULL). NCCL: stream-ordered; host transport: synchronous. */
+int ptrom_dev_pairwise_velocity_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int64_t n, const double* d_x_local,
+                                            double* d_x_full, const double* d_gamma, double delta, int form,
+                                            const double* d_inflow, double* d_f_local);
+/* integrators.hpp:243-272 fom_simulate with the targets split across the
+ * communicator. Every rank passes the full x0 (2n),
+ * gamma (n) and inflow (2n or NULL) as the reference's fom_simulate does and
+ * receives its own rows: snapshots_local is 2m x n_steps column-major
+ * (column s = [x_lo..x_hi-1, y_lo..y_hi-1] after step s); iterations /
+ * converged / relative_residual are identical on every rank. Per Newton
+ * iteration: the partial |r|^2 of every rank are all-gathered and summed in
+ * rank order (the same decision on every rank, independent of NCCL's
+ * reduction order), the Newton update runs on the local rows (the 2x2
+ * self-blocks are local) and the updated rows are all-gathered before the
+ * velocity of the local targets. n_pair_evals: this rank's share,
+ * velocity evaluations x m x (n-1). */
+int ptrom_fom_simulate_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int64_t n, const double* x0,
+                                   const double* gamma, double delta, int form, const double* inflow, double dt,
+                                   int64_t n_steps, double tol, int max_iters, int jacobian_refresh_period,
+                                   double* snapshots_local, int* iterations, uint8_t* converged,
+                                   double* relative_residual, uint64_t* n_pair_evals);
+/* ptrom_ptrom_simulate_batch_f64 with the n_inst instances split evenly
+ * across the communicator. The tables are needed on
+ * `root` only: basis, op, sur, gamma_a, gamma_b, mu and inflow may be NULL on
+ * the other ranks. One grouped broadcast replicates the shared tables (row-
+ * major basis, GNAT operator and gathered rows, the surrogate's CSR lists and
+ * per-cluster tables) and the parameters; every rank then marches its
+ * instances with no communication, and x_hat / iterations / converged are
+ * all-gathered in instance order on every rank that passes non-NULL outputs.
+ * n_pair_evals: this rank's share. */
+int ptrom_ptrom_simulate_batch_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int root, const ptrom_basis* basis,
+                                           const ptrom_gnat_op* op, const ptrom_surrogate* sur, int64_t n,
+                                           const double* gamma_a, const double* gamma_b, int64_t n_inst,
+                                           const double* mu, int64_t batch, double delta, int form,
+                                           const double* inflow, double dt, int64_t n_steps, double tol,
+                                           int max_iters, double step_length, double* x_hat, int* iterations,
+                                           uint8_t* converged, uint64_t* n_pair_evals);
+
 /* --------------------------------------------------------- instrumentation -- */
 /* bench.py support: while enabled, the context records CUDA events on its own
  * stream around every launch of the dominant kernel of each call (the

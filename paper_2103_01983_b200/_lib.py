@@ -113,6 +113,20 @@ PROTOTYPES = {
                                         C.POINTER(C.c_void_p)]),
     "ptrom_surrogate_sizes": (C.c_int, [C.c_void_p, c_dp]),
     "ptrom_surrogate_export_lists": (C.c_int, [c_ctxp, C.c_void_p] + [c_dp] * 10),
+    "ptrom_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "ptrom_comm_init": (C.c_int, [c_ctxp, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ptrom_comm_init_host": (C.c_int, [c_ctxp, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ptrom_comm_destroy": (None, [C.c_void_p]),
+    "ptrom_comm_transport": (C.c_int, [C.c_void_p]),
+    "ptrom_dev_pairwise_velocity_sharded_f64": (
+        C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_dp, c_dp, C.c_double, C.c_int, c_dp, c_dp]),
+    "ptrom_fom_simulate_sharded_f64": (
+        C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_dp, C.c_double, C.c_int, c_dp, C.c_double, c_i64, C.c_double,
+                  C.c_int, C.c_int, c_dp, c_dp, c_dp, c_dp, c_u64p]),
+    "ptrom_ptrom_simulate_batch_sharded_f64": (
+        C.c_int, [c_ctxp, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_dp, c_dp, c_i64, c_dp,
+                  c_i64, C.c_double, C.c_int, c_dp, C.c_double, c_i64, C.c_double, C.c_int, C.c_double, c_dp, c_dp,
+                  c_dp, c_u64p]),
     "ptrom_profile_begin": (C.c_int, [c_ctxp]),
     "ptrom_profile_end": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

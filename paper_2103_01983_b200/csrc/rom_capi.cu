@@ -1,9 +1,11 @@
 // rom_capi.cu — C ABI for the PTROM online path (include/ptrom_b200.h "ptrom").
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "ops.cuh"
 #include "rom.cuh"
 
@@ -100,6 +102,83 @@ struct ptrom_surrogate {
   long long n_membership = 0, n_cluster_list = 0, n_direct_list = 0;
   DevAllocs mem;
 };
+
+namespace {
+
+// Shared argument checks of the batched entry points (rom.hpp:264-273,
+// RomConfig::validate).
+void validate_batch(const ptrom_basis* basis, const ptrom_gnat_op* op, const ptrom_surrogate* sur, int64_t n,
+                    const double* gamma_a, const double* gamma_b, int64_t n_inst, const double* mu, double dt,
+                    int64_t n_steps, double tol, int max_iters, double step_length) {
+  if (!basis || !op || !sur) config_fail("null basis / operator / surrogate");
+  if (!(dt > 0)) config_fail("time step must be positive");
+  if (n_steps < 0) config_fail("negative step count");
+  if (!(tol > 0)) config_fail("ROM tolerance must be positive");
+  if (max_iters < 1) config_fail("ROM max_iters must be >= 1");
+  if (!(step_length > 0)) config_fail("ROM step length must be positive");
+  if (n != basis->b.n) config_fail("GnatSolver: basis dimension does not match particle count");
+  if (sur->target_ids != op->ids) config_fail("GnatSolver: surrogate targets must equal the sampled particle ids");
+  if (n_inst < 1) config_fail("batch needs at least one instance");
+  check_finite(gamma_a, (size_t)n, "non-finite circulation");
+  check_finite(gamma_b, (size_t)n, "non-finite circulation");
+  check_finite(mu, (size_t)n_inst, "non-finite parameter");
+}
+
+// Batched affine march over host μ / Γa / Γb (SURVEY.md §8b
+// ptrom_gnat_simulate_batch): affine member sums once, then batches of B
+// instances; x_hat [n_inst][n_steps][M], iterations / converged
+// [n_inst][n_steps] on the host. Returns the pair count.
+unsigned long long batch_march(ptrom_ctx* ctx, const DBasis& b, const DGnat& g, const DSurrogate& s, long long n,
+                               const double* gamma_a, const double* gamma_b, long long n_inst, const double* mu,
+                               long long batch, double delta, int form, const double* inflow, double dt,
+                               long long n_steps, double tol, int max_iters, double step_length, double* x_hat,
+                               int* iterations, uint8_t* converged) {
+  DevAllocs tmp;
+  const double* dga = tmp.up(gamma_a, (size_t)n);
+  const double* dgb = tmp.up(gamma_b, (size_t)n);
+  const double* dinf = inflow ? tmp.up(inflow, (size_t)2 * n) : nullptr;
+  AffineTables t;
+  t.pa = tmp.zeros<double>((size_t)2 * s.n_c * s.m);
+  t.pb = tmp.zeros<double>((size_t)2 * s.n_c * s.m);
+  t.xa = tmp.zeros<double>((size_t)2 * s.n_c);
+  t.xb = tmp.zeros<double>((size_t)2 * s.n_c);
+  t.ga = tmp.zeros<double>((size_t)s.n_c);
+  t.gb = tmp.zeros<double>((size_t)s.n_c);
+  // direct circulations Γa[id], Γb[id]
+  std::vector<long long> dids((size_t)s.u);
+  PTROM_CUDA(cudaMemcpy(dids.data(), s.direct_ids, dids.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<double> dga_h(dids.size()), dgb_h(dids.size());
+  for (size_t k = 0; k < dids.size(); ++k) {
+    dga_h[k] = gamma_a[dids[k]];
+    dgb_h[k] = gamma_b[dids[k]];
+  }
+  t.dga = tmp.up(dga_h.data(), dga_h.size());
+  t.dgb = tmp.up(dgb_h.data(), dgb_h.size());
+  rom_affine_tables(ctx, s, b, dga, dgb, t);
+  const int m = b.m;
+  const long long B = std::max<long long>(1, std::min<long long>(batch > 0 ? batch : 256, n_inst));
+  const long long steps = std::max<long long>(n_steps, 1);
+  double* dmu = tmp.up(mu, (size_t)n_inst);
+  double* dxh = tmp.zeros<double>((size_t)B * m * steps);
+  int* dit = tmp.zeros<int>((size_t)B * steps);
+  unsigned char* dcv = tmp.zeros<unsigned char>((size_t)B * steps);
+  unsigned long long pairs = 0;
+  for (long long b0 = 0; b0 < n_inst; b0 += B) {
+    const int nb = (int)std::min<long long>(B, n_inst - b0);
+    pairs += rom_gnat_simulate(ctx, s, g, &t, nb, dmu + b0, delta, form, dinf, n, dt, n_steps, tol, max_iters,
+                               step_length, dxh, dit, dcv);
+    if (n_steps > 0) {
+      PTROM_CUDA(cudaMemcpy(x_hat + (size_t)b0 * n_steps * m, dxh, (size_t)nb * n_steps * m * 8,
+                            cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(iterations + (size_t)b0 * n_steps, dit, (size_t)nb * n_steps * 4,
+                            cudaMemcpyDeviceToHost));
+      PTROM_CUDA(cudaMemcpy(converged + (size_t)b0 * n_steps, dcv, (size_t)nb * n_steps, cudaMemcpyDeviceToHost));
+    }
+  }
+  return pairs;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -415,61 +494,10 @@ int ptrom_ptrom_simulate_batch_f64(ptrom_ctx* ctx, const ptrom_basis* basis, con
                                    double tol, int max_iters, double step_length, double* x_hat, int* iterations,
                                    uint8_t* converged, uint64_t* n_pair_evals) {
   return guarded(ctx, [&] {
-    if (!basis || !op || !sur) config_fail("null basis / operator / surrogate");
-    if (!(dt > 0)) config_fail("time step must be positive");
-    if (n_steps < 0) config_fail("negative step count");
-    if (!(tol > 0)) config_fail("ROM tolerance must be positive");
-    if (max_iters < 1) config_fail("ROM max_iters must be >= 1");
-    if (!(step_length > 0)) config_fail("ROM step length must be positive");
-    if (n != basis->b.n) config_fail("GnatSolver: basis dimension does not match particle count");
-    if (sur->target_ids != op->ids) config_fail("GnatSolver: surrogate targets must equal the sampled particle ids");
-    if (n_inst < 1) config_fail("batch needs at least one instance");
-    check_finite(gamma_a, (size_t)n, "non-finite circulation");
-    check_finite(gamma_b, (size_t)n, "non-finite circulation");
-    check_finite(mu, (size_t)n_inst, "non-finite parameter");
-    DevAllocs tmp;
-    const double* dga = tmp.up(gamma_a, (size_t)n);
-    const double* dgb = tmp.up(gamma_b, (size_t)n);
-    const double* dinf = inflow ? tmp.up(inflow, (size_t)2 * n) : nullptr;
-    const DSurrogate& s = sur->s;
-    AffineTables t;
-    t.pa = tmp.zeros<double>((size_t)2 * s.n_c * s.m);
-    t.pb = tmp.zeros<double>((size_t)2 * s.n_c * s.m);
-    t.xa = tmp.zeros<double>((size_t)2 * s.n_c);
-    t.xb = tmp.zeros<double>((size_t)2 * s.n_c);
-    t.ga = tmp.zeros<double>((size_t)s.n_c);
-    t.gb = tmp.zeros<double>((size_t)s.n_c);
-    // direct circulations Γa[id], Γb[id]
-    std::vector<long long> dids((size_t)s.u);
-    PTROM_CUDA(cudaMemcpy(dids.data(), s.direct_ids, dids.size() * 8, cudaMemcpyDeviceToHost));
-    std::vector<double> dga_h(dids.size()), dgb_h(dids.size());
-    for (size_t k = 0; k < dids.size(); ++k) {
-      dga_h[k] = gamma_a[dids[k]];
-      dgb_h[k] = gamma_b[dids[k]];
-    }
-    t.dga = tmp.up(dga_h.data(), dga_h.size());
-    t.dgb = tmp.up(dgb_h.data(), dgb_h.size());
-    rom_affine_tables(ctx, s, basis->b, dga, dgb, t);
-    const int m = basis->b.m;
-    const int64_t B = std::max<int64_t>(1, std::min<int64_t>(batch > 0 ? batch : 256, n_inst));
-    const int64_t steps = std::max<int64_t>(n_steps, 1);
-    double* dmu = tmp.up(mu, (size_t)n_inst);
-    double* dxh = tmp.zeros<double>((size_t)B * m * steps);
-    int* dit = tmp.zeros<int>((size_t)B * steps);
-    unsigned char* dcv = tmp.zeros<unsigned char>((size_t)B * steps);
-    unsigned long long pairs = 0;
-    for (int64_t b0 = 0; b0 < n_inst; b0 += B) {
-      const int nb = (int)std::min<int64_t>(B, n_inst - b0);
-      pairs += rom_gnat_simulate(ctx, s, op->g, &t, nb, dmu + b0, delta, form, dinf, n, dt, n_steps, tol, max_iters,
-                                 step_length, dxh, dit, dcv);
-      if (n_steps > 0) {
-        PTROM_CUDA(cudaMemcpy(x_hat + (size_t)b0 * n_steps * m, dxh, (size_t)nb * n_steps * m * 8,
-                              cudaMemcpyDeviceToHost));
-        PTROM_CUDA(cudaMemcpy(iterations + (size_t)b0 * n_steps, dit, (size_t)nb * n_steps * 4,
-                              cudaMemcpyDeviceToHost));
-        PTROM_CUDA(cudaMemcpy(converged + (size_t)b0 * n_steps, dcv, (size_t)nb * n_steps, cudaMemcpyDeviceToHost));
-      }
-    }
+    validate_batch(basis, op, sur, n, gamma_a, gamma_b, n_inst, mu, dt, n_steps, tol, max_iters, step_length);
+    const unsigned long long pairs =
+        batch_march(ctx, basis->b, op->g, sur->s, n, gamma_a, gamma_b, n_inst, mu, batch, delta, form, inflow, dt,
+                    n_steps, tol, max_iters, step_length, x_hat, iterations, converged);
     if (n_pair_evals) *n_pair_evals = pairs;
   });
 }
@@ -559,6 +587,185 @@ int ptrom_surrogate_export_lists(ptrom_ctx* ctx, const ptrom_surrogate* sur, int
     };
     widen(cl_list, s.cl_list, (size_t)sur->n_cluster_list);
     widen(d_list, s.d_list, (size_t)sur->n_direct_list);
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- multi-GPU (§8e) --
+namespace {
+
+// Root's sizes and scalars, broadcast first so every rank can allocate its
+// copies of the shared tables.
+struct ShardHeader {
+  long long n, n_inst, batch, n_steps;
+  long long n_c, u, n_t, n_mem, n_cl, n_dl, n_s, max_members;
+  double delta, dt, tol, step;
+  int m, m_r, mp, form, max_iters, has_inflow, has_order, ok;
+  char why[256];
+};
+
+// Device arrays of the online engine's shared tables (the row-major basis,
+// the GNAT operator with its gathered rows, the surrogate): (member, bytes).
+std::vector<std::pair<void**, size_t>> shared_fields(DBasis& b, DGnat& g, DSurrogate& s, const ShardHeader& h) {
+  const size_t nc = (size_t)h.n_c, u = (size_t)h.u, nt = (size_t)h.n_t, m = (size_t)h.m;
+  std::vector<std::pair<void**, size_t>> f = {
+      {reinterpret_cast<void**>(&b.rm), (size_t)h.n * 2 * (m + 1) * 8},
+      {reinterpret_cast<void**>(&g.ids), (size_t)h.n_s * 8},
+      {reinterpret_cast<void**>(&g.A), (size_t)32 * 2 * h.n_s * 8},
+      {reinterpret_cast<void**>(&g.phi_bar), (size_t)2 * h.n_s * h.mp * 8},
+      {reinterpret_cast<void**>(&g.x0_bar), (size_t)2 * h.n_s * 8},
+      {reinterpret_cast<void**>(&s.phi_tilde), 2 * nc * m * 8},
+      {reinterpret_cast<void**>(&s.x0_tilde), 2 * nc * 8},
+      {reinterpret_cast<void**>(&s.gamma_tilde), nc * 8},
+      {reinterpret_cast<void**>(&s.zero_gamma), nc},
+      {reinterpret_cast<void**>(&s.mem_off), (nc + 1) * 8},
+      {reinterpret_cast<void**>(&s.mem_ids), (size_t)h.n_mem * 8},
+      {reinterpret_cast<void**>(&s.target_ids), nt * 8},
+      {reinterpret_cast<void**>(&s.cl_off), (nt + 1) * 8},
+      {reinterpret_cast<void**>(&s.cl_list), (size_t)h.n_cl * 4},
+      {reinterpret_cast<void**>(&s.d_off), (nt + 1) * 8},
+      {reinterpret_cast<void**>(&s.d_list), (size_t)h.n_dl * 4},
+      {reinterpret_cast<void**>(&s.direct_ids), u * 8},
+      {reinterpret_cast<void**>(&s.direct_phi), 2 * u * m * 8},
+      {reinterpret_cast<void**>(&s.direct_x0), 2 * u * 8},
+      {reinterpret_cast<void**>(&s.direct_gamma), u * 8},
+  };
+  if (h.has_order) f.push_back({reinterpret_cast<void**>(&s.t_order), nt * 4});
+  return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ptrom_ptrom_simulate_batch_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int root, const ptrom_basis* basis,
+                                           const ptrom_gnat_op* op, const ptrom_surrogate* sur, int64_t n,
+                                           const double* gamma_a, const double* gamma_b, int64_t n_inst,
+                                           const double* mu, int64_t batch, double delta, int form,
+                                           const double* inflow, double dt, int64_t n_steps, double tol,
+                                           int max_iters, double step_length, double* x_hat, int* iterations,
+                                           uint8_t* converged, uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    if (!comm) config_fail("null communicator");
+    if (comm->device != ctx->device) config_fail("communicator and context are on different devices");
+    if (root < 0 || root >= comm->world) config_fail("sharded batch: root outside [0, world)");
+    const bool is_root = comm->rank == root;
+    ShardHeader h{};
+    if (is_root) {
+      h.ok = 1;
+      try {
+        validate_batch(basis, op, sur, n, gamma_a, gamma_b, n_inst, mu, dt, n_steps, tol, max_iters, step_length);
+        if (inflow) check_finite(inflow, (size_t)2 * n, "non-finite inflow");
+      } catch (const status_error& e) {  // every rank must learn it before the collectives below
+        h.ok = 0;
+        std::strncpy(h.why, e.what(), sizeof(h.why) - 1);
+      }
+      if (h.ok) {
+        const DSurrogate& s = sur->s;
+        h.n = n;
+        h.n_inst = n_inst;
+        h.batch = batch;
+        h.n_steps = n_steps;
+        h.n_c = s.n_c;
+        h.u = s.u;
+        h.n_t = s.n_t;
+        h.n_mem = sur->n_membership;
+        h.n_cl = sur->n_cluster_list;
+        h.n_dl = sur->n_direct_list;
+        h.n_s = op->g.n_s;
+        h.max_members = s.max_members;
+        h.delta = delta;
+        h.dt = dt;
+        h.tol = tol;
+        h.step = step_length;
+        h.m = basis->b.m;
+        h.m_r = op->g.m_r;
+        h.mp = op->g.mp;
+        h.form = form;
+        h.max_iters = max_iters;
+        h.has_inflow = inflow ? 1 : 0;
+        h.has_order = s.t_order ? 1 : 0;
+      }
+    }
+    comm_bcast_host(ctx, comm, &h, sizeof(h), root);
+    if (!h.ok) config_fail(std::string("sharded batch: root rejected the arguments: ") + h.why);
+    // host parameters (Γa, Γb, μ, inflow) in one broadcast
+    const size_t np = (size_t)(2 * h.n + h.n_inst + (h.has_inflow ? 2 * h.n : 0));
+    std::vector<double> par(np);
+    if (is_root) {
+      std::copy(gamma_a, gamma_a + h.n, par.begin());
+      std::copy(gamma_b, gamma_b + h.n, par.begin() + h.n);
+      std::copy(mu, mu + h.n_inst, par.begin() + 2 * h.n);
+      if (h.has_inflow) std::copy(inflow, inflow + 2 * h.n, par.begin() + 2 * h.n + h.n_inst);
+    }
+    comm_bcast_host(ctx, comm, par.data(), np * 8, root);
+    // shared device tables: root's own, a broadcast copy elsewhere
+    DBasis b;
+    DGnat g;
+    DSurrogate s;
+    DevAllocs copies;
+    if (is_root) {
+      b = basis->b;
+      g = op->g;
+      s = sur->s;
+    } else {
+      b.n = h.n;
+      b.m = h.m;
+      g.n_s = h.n_s;
+      g.m_r = h.m_r;
+      g.m = h.m;
+      g.mp = h.mp;
+      s.m = h.m;
+      s.n_c = h.n_c;
+      s.u = h.u;
+      s.n_t = h.n_t;
+      s.max_members = h.max_members;
+      for (auto& [ptr, bytes] : shared_fields(b, g, s, h)) *ptr = copies.up<char>(nullptr, bytes);
+    }
+    std::vector<std::pair<void*, size_t>> bufs;
+    for (auto& [ptr, bytes] : shared_fields(b, g, s, h)) bufs.push_back({*ptr, bytes});
+    comm_bcast_many(ctx, comm, bufs, root);
+    // this rank's instances, no communication during the march
+    long long lo, hi;
+    shard_bounds(h.n_inst, comm->rank, comm->world, lo, hi);
+    const long long cnt = hi - lo, steps = h.n_steps, m = h.m;
+    std::vector<double> xl((size_t)std::max<long long>(cnt * steps * m, 1));
+    std::vector<int> il((size_t)std::max<long long>(cnt * steps, 1));
+    std::vector<uint8_t> cl((size_t)std::max<long long>(cnt * steps, 1));
+    unsigned long long pairs = 0;
+    if (cnt > 0)
+      pairs = batch_march(ctx, b, g, s, h.n, par.data(), par.data() + h.n, cnt, par.data() + 2 * h.n + lo, h.batch,
+                          h.delta, h.form, h.has_inflow ? par.data() + 2 * h.n + h.n_inst : nullptr, h.dt, steps,
+                          h.tol, h.max_iters, h.step, xl.data(), il.data(), cl.data());
+    // gather in instance order: one record per instance (x̂, iterations, converged)
+    long long max_cnt = 0;
+    for (int r = 0; r < comm->world; ++r) {
+      long long a, z;
+      shard_bounds(h.n_inst, r, comm->world, a, z);
+      max_cnt = std::max(max_cnt, z - a);
+    }
+    const size_t rec = (size_t)steps * (m * 8 + 4 + 1);
+    std::vector<char> send((size_t)std::max<long long>(max_cnt, 1) * std::max<size_t>(rec, 1));
+    for (long long i = 0; i < cnt; ++i) {
+      char* p = send.data() + i * rec;
+      std::memcpy(p, xl.data() + i * steps * m, steps * m * 8);
+      std::memcpy(p + steps * m * 8, il.data() + i * steps, steps * 4);
+      std::memcpy(p + steps * m * 8 + steps * 4, cl.data() + i * steps, steps);
+    }
+    std::vector<char> all(send.size() * comm->world);
+    comm_allgather_host(ctx, comm, send.data(), all.data(), send.size());
+    for (int r = 0; r < comm->world; ++r) {
+      long long a, z;
+      shard_bounds(h.n_inst, r, comm->world, a, z);
+      for (long long i = a; i < z; ++i) {
+        const char* p = all.data() + (size_t)r * send.size() + (i - a) * rec;
+        if (x_hat) std::memcpy(x_hat + i * steps * m, p, steps * m * 8);
+        if (iterations) std::memcpy(iterations + i * steps, p + steps * m * 8, steps * 4);
+        if (converged) std::memcpy(converged + i * steps, p + steps * m * 8 + steps * 4, steps);
+      }
+    }
+    if (n_pair_evals) *n_pair_evals = pairs;
   });
 }
 

@@ -1,5 +1,13 @@
 """Multi-GPU drivers, one process per GPU over torch.distributed.
 
+The product's sharded FOM and PTROM batch are C ABI entry points
+(ptrom_fom_simulate_sharded_f64, ptrom_ptrom_simulate_batch_sharded_f64 over a
+ptrom_comm; Python mirror in comm.py) so a C++ host shards without Python.
+This module holds the torch.distributed restatements of the same control
+flow with pluggable per-rank backends — exercised on CPU with gloo, where
+the C ABI (CUDA-only) cannot run — plus the peer-memory FOM variant and the
+Barnes–Hut target split.
+
 ShardedFom — the implicit-trapezoidal FOM (integrators.hpp:117-272) with the
 targets split evenly across ranks. Per Newton iteration:
   * residual on the rank's rows and its squared norm; the G partial norms are
@@ -37,6 +45,7 @@ import math
 from dataclasses import dataclass
 from typing import Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -222,7 +231,13 @@ class ShardedFom:
 
 
 class PtromInstanceSplit:
-    """μ instances split evenly across ranks; x̂ gathered on every rank."""
+    """μ instances split evenly across ranks: the shared
+    tables live on the root only and are broadcast once, every rank marches
+    its block of instances with no communication, and the reduced states are
+    gathered in instance order on every rank. The product path is the C ABI's
+    ptrom_ptrom_simulate_batch_sharded_f64 (comm.py); this is the same
+    control flow over torch.distributed with a pluggable per-rank `march`, so
+    the split / broadcast / gather logic is tested on CPU with gloo."""
 
     def __init__(self, group=None):
         self.group = group
@@ -231,6 +246,24 @@ class PtromInstanceSplit:
 
     def local_slice(self, n_inst: int) -> tuple[int, int]:
         return shard_bounds(n_inst, self.rank, self.world)
+
+    def broadcast_tables(self, tables: Optional[dict], root: int = 0) -> dict:
+        """One broadcast of the root's table dict (numpy arrays and scalars)."""
+        if self.world == 1:
+            return tables
+        box = [tables if self.rank == root else None]
+        dist.broadcast_object_list(box, src=root, group=self.group)
+        return box[0]
+
+    def run(self, tables: Optional[dict], march, root: int = 0):
+        """tables (root only) must hold 'mu'; march(tables, mu_block) returns
+        (x_hat [k][n_steps][M], iterations [k][n_steps]) for its k instances."""
+        tables = self.broadcast_tables(tables, root)
+        mu = np.asarray(tables["mu"])
+        lo, hi = self.local_slice(mu.shape[0])
+        xh, it = march(tables, mu[lo:hi])
+        return (self.gather(torch.as_tensor(np.asarray(xh)), mu.shape[0]).numpy(),
+                self.gather(torch.as_tensor(np.asarray(it)), mu.shape[0]).numpy())
 
     def gather(self, local: torch.Tensor, n_inst: int) -> torch.Tensor:
         """Concatenate per-rank instance blocks (leading dimension) in rank order."""

@@ -120,25 +120,62 @@ def test_sharded_fom_matches_single_process_oracle(oracle, world, n):
         assert np.linalg.norm(full[s] - snaps[:, s]) / np.linalg.norm(snaps[:, s]) <= 1e-12
 
 
-def _split_worker(rank, world, port, n_inst, out_q):
+def _oracle_march(oracle):
+    """Per-rank march of the CPU test: the oracle's ptrom_simulate
+    (rom.hpp:404-412) for each instance of the block, from the broadcast tables."""
+    def march(t, mu_block):
+        xs, its = [], []
+        for m in mu_block:
+            sur = oracle.Surrogate(t["phi"], t["sv"], t["x0"], t["g1"], t["ids"], 1, 1.0, 1)
+            xo, it, _ = oracle.ptrom_simulate(sur, t["phi"], t["sv"], t["x0"], t["ids"], t["A"],
+                                              t["gamma_a"] + m * t["gamma_b"], t["delta"], t["dt"], t["steps"],
+                                              1e-300, 5)
+            xs.append(xo.T.copy())
+            its.append(np.asarray(it, np.int32))
+        m_ = t["phi"].shape[1]
+        return (np.array(xs).reshape(len(mu_block), t["steps"], m_),
+                np.array(its, np.int32).reshape(len(mu_block), t["steps"]))
+    return march
+
+
+def _ptrom_tables(oracle, n=512, n_inst=7, steps=3):
+    from paper_2103_01983_b200 import workloads
+    w = workloads.config4(n=n, n_inst=n_inst, modes=6, modes_r=12)
+    ids = oracle.greedy_sample(w.phi_r, w.n_samples)
+    A = oracle.build_gnat_operator(w.phi_r, ids)
+    return {"phi": w.phi, "sv": w.sv, "x0": w.x0, "g1": w.gamma_a + w.gamma_b, "ids": ids, "A": A,
+            "gamma_a": w.gamma_a, "gamma_b": w.gamma_b, "delta": w.delta, "dt": w.dt, "steps": steps, "mu": w.mu}
+
+
+def _split_worker(rank, world, port, root, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from oracle import pyoracle
         from paper_2103_01983_b200.sharded import PtromInstanceSplit
+        pyoracle.build()
         sp = PtromInstanceSplit()
-        lo, hi = sp.local_slice(n_inst)
-        local = torch.arange(lo, hi, dtype=torch.float64).reshape(-1, 1).repeat(1, 3) * 10.0 + rank * 0
-        full = sp.gather(local, n_inst)
+        tables = _ptrom_tables(pyoracle) if rank == root else None  # the root alone holds the tables
+        xh, it = sp.run(tables, _oracle_march(pyoracle), root=root)
+        parts = [None] * world
+        dist.all_gather_object(parts, (xh, it))
         if rank == 0:
-            out_q.put(full.numpy())
+            out_q.put(parts)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_inst", [(2, 8), (3, 10)])
-def test_ptrom_instance_split_gathers_in_order(world, n_inst):
-    full = _run(world, _split_worker, (n_inst,))
-    np.testing.assert_array_equal(full[:, 0], np.arange(n_inst) * 10.0)
+@pytest.mark.parametrize("world,root", [(2, 0), (3, 2)])
+def test_ptrom_instance_split_march_matches_single_process_oracle(oracle, world, root):
+    """μ split across gloo ranks: tables broadcast from the root once, each
+    rank marches its block, x̂ gathered in instance order on every rank —
+    identical to the single-process per-instance oracle."""
+    parts = _run(world, _split_worker, (root,))
+    t = _ptrom_tables(oracle)
+    want_x, want_it = _oracle_march(oracle)(t, t["mu"])
+    for xh, it in parts:
+        np.testing.assert_array_equal(xh, want_x)
+        np.testing.assert_array_equal(it, want_it)
 
 
 def test_shard_bounds_cover_everything():
@@ -195,3 +232,37 @@ def test_sharded_barnes_hut_matches_single_process_oracle(oracle, world, n):
     w = workloads.config3(n=n)
     tree = oracle.Tree(w.x0[:n], w.x0[n:], w.gamma, 4)
     np.testing.assert_array_equal(f, tree.bh_velocity(w.x0, w.gamma, w.delta, 0, 0.5))
+
+
+def _host_coll_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes as C
+        from paper_2103_01983_b200.comm import torch_host_collectives
+        ops, _keep = torch_host_collectives()
+        # what the C library does: raw host pointers, rank-ordered all-gather,
+        # broadcast from a root, zero-byte calls
+        send = (C.c_double * 3)(rank, rank + 0.5, -rank)
+        recv = (C.c_double * (3 * world))()
+        assert ops.all_gather(None, C.addressof(send), C.addressof(recv), 24) == 0
+        assert ops.all_gather(None, C.addressof(send), C.addressof(recv), 0) == 0
+        buf = (C.c_int64 * 4)(*([7, 8, 9, 10] if rank == world - 1 else [0, 0, 0, 0]))
+        assert ops.broadcast(None, C.addressof(buf), 32, world - 1) == 0
+        parts = [None] * world
+        dist.all_gather_object(parts, (list(recv), list(buf)))
+        if rank == 0:
+            out_q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_transport_callbacks_over_gloo(world):
+    """The ptrom_host_collectives callbacks (comm.py) the C ABI's host
+    transport calls: rank-ordered all-gather and broadcast on raw buffers."""
+    parts = _run(world, _host_coll_worker, ())
+    want = [v for r in range(world) for v in (r, r + 0.5, -r)]
+    for recv, buf in parts:
+        assert recv == want
+        assert buf == [7, 8, 9, 10]
