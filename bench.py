@@ -210,7 +210,24 @@ def allpairs_line(args, w, K, W, rank, world, local, e2e_steps, cpu_seconds, wit
     stream = torch.cuda.current_stream()
     lib = ctx.lib
 
-    def step_allgather():  # per-evaluation exchange: NCCL all-gather of the positions, then the local kernel
+    ctx.set_stream(stream.cuda_stream)
+    comm = None
+    if world > 1:
+        # the C ABI's communicator (NCCL over NVLink / NVSwitch): the exchange
+        # is one grouped broadcast per rank block, then the local tile kernel
+        try:
+            from paper_2103_01983_b200.comm import Comm
+            comm = Comm.nccl(ctx)
+        except Exception as exc:  # keep torch's all-gather; the line says so
+            comm_error = f"{type(exc).__name__}: {exc}"
+        x_ws = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+
+    def step_allgather():  # per-evaluation exchange + local kernel (ptrom_dev_pairwise_velocity_sharded_f64)
+        if comm is not None:
+            ctx.check(lib.ptrom_dev_pairwise_velocity_sharded_f64(ctx.handle, comm.handle, n, x_local.data_ptr(),
+                                                                  x_ws.data_ptr(), gamma.data_ptr(), w.delta, 0,
+                                                                  None, out.data_ptr()))
+            return
         if world > 1:
             dist.all_gather_into_tensor(x_full[:n], x_local[0])
             dist.all_gather_into_tensor(x_full[n:], x_local[1])
@@ -220,10 +237,26 @@ def allpairs_line(args, w, K, W, rank, world, local, e2e_steps, cpu_seconds, wit
     # in CUDA-IPC memory and the tile loads read the peers' blocks in place over
     # NVLink (paper_2103_01983_b200/peer.py). Verified once against the
     # all-gather path; PTROM_EXCHANGE=nccl selects the all-gather path.
+    if comm is not None:  # check the C-ABI exchange once against torch's all-gather + the flat kernel
+        try:
+            step_allgather()
+            got = out.clone()
+            dist.all_gather_into_tensor(x_full[:n], x_local[0])
+            dist.all_gather_into_tensor(x_full[n:], x_local[1])
+            dev.pairwise_velocity(x_full, gamma, w.delta, 0, None, lo, hi, out, ctx=ctx)
+            dev.synchronize(ctx)
+            ok = torch.tensor([1.0 if torch.equal(got, out) else 0.0], device="cuda")
+        except Exception as exc:
+            comm_error = f"{type(exc).__name__}: {exc}"
+            ok = torch.tensor([0.0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if float(ok.item()) != 1.0:
+            comm_error = locals().get("comm_error", "sharded C-ABI result differs from the all-gather path")
+            comm = None
     exchange = "single-gpu"
     step = step_allgather
     if world > 1:
-        exchange = "nccl-allgather"
+        exchange = "ptrom_comm NCCL all-gather-v" if comm is not None else f"torch NCCL all-gather ({comm_error})"
         if os.environ.get("PTROM_EXCHANGE", "peer") == "peer":
             try:
                 from paper_2103_01983_b200.peer import PeerExchange
@@ -245,7 +278,7 @@ def allpairs_line(args, w, K, W, rank, world, local, e2e_steps, cpu_seconds, wit
                 if float(same.item()) == 1.0:
                     exchange, step = "peer-ipc (fused into the tile loads)", step_peer
             except Exception as exc:  # keep the NCCL path; say why in the JSON line
-                exchange = f"nccl-allgather (peer setup failed: {type(exc).__name__})"
+                exchange = f"ptrom_comm NCCL all-gather-v (peer setup failed: {type(exc).__name__})"
 
     for _ in range(W):
         step()

@@ -323,6 +323,42 @@ int ptrom_surrogate_export_lists(ptrom_ctx* ctx, const ptrom_surrogate* sur, int
                                  int64_t* direct_ids, int64_t* d_off, int64_t* d_list, double* direct_phi,
                                  double* direct_x0);
 
+/* --------------------------------------- PTMX / OfflineBundle I/O (§8f-4) -- */
+/* Host I/O in the reference's on-disk layout; no GPU needed except for
+ * ptrom_bundle_to_device. ctx may be NULL: the message is then available from
+ * ptrom_io_last_error() (thread-local). I/O and format errors are status 2
+ * (the reference throws config_error) with the reference's messages. */
+typedef struct ptrom_bundle ptrom_bundle;
+const char* ptrom_io_last_error(void);
+/* io.hpp:53-75 read_matrix: rows, cols, dt, t0 (each nullable); data = NULL
+ * reads the header only, else rows*cols column-major doubles (capacity in
+ * doubles). */
+int ptrom_ptmx_read(ptrom_ctx* ctx, const char* path, uint64_t* rows, uint64_t* cols, double* dt, double* t0,
+                    double* data, uint64_t capacity);
+/* io.hpp:35-51 write_matrix (a time series when dt/t0 are set, e.g. an x_hat
+ * trajectory M x n_steps). */
+int ptrom_ptmx_write(ptrom_ctx* ctx, const char* path, uint64_t rows, uint64_t cols, double dt, double t0,
+                     const double* data);
+/* bundle.cpp:96-141 OfflineBundle::load: index.json + the twelve PTMX files. */
+int ptrom_bundle_open(ptrom_ctx* ctx, const char* dir, ptrom_bundle** out);
+void ptrom_bundle_free(ptrom_bundle* bundle);
+/* sizes[11]: n_dofs, modes, residual modes, n_samples, GNAT rows, n_clusters,
+ * n_direct, n_targets, membership entries, cluster-list entries, direct-list
+ * entries. */
+int ptrom_bundle_sizes(const ptrom_bundle* bundle, int64_t* sizes);
+/* The ExperimentConfig object verbatim (JSON text); returns its length. */
+int64_t ptrom_bundle_config_json(const ptrom_bundle* bundle, char* buf, int64_t cap);
+/* Host copies of every array (NULL skips), column-major matrices, CSR lists. */
+int ptrom_bundle_export(const ptrom_bundle* bundle, double* basis_phi, double* basis_sv, double* basis_xref,
+                        double* residual_phi, double* residual_sv, double* gnat_a, int64_t* sample_ids,
+                        double* phi_tilde, double* x0_tilde, double* gamma_tilde, int32_t* cluster_node_ids,
+                        int64_t* mem_off, int64_t* mem_ids, uint8_t* zero_gamma, int64_t* target_ids,
+                        int64_t* cl_off, int64_t* cl_list, int64_t* d_off, int64_t* d_list, int64_t* direct_ids,
+                        double* direct_phi, double* direct_x0, double* direct_gamma);
+/* → the device basis, GNAT operator and surrogate (rom.hpp:264-290 inputs). */
+int ptrom_bundle_to_device(ptrom_ctx* ctx, const ptrom_bundle* bundle, ptrom_basis** basis, ptrom_gnat_op** op,
+                           ptrom_surrogate** sur);
+
 /* ---------------------------------------------------- multi-GPU -- */
 /* SURVEY.md §8b "Multi-GPU: ptrom_comm_init + *_sharded variants". One
  * process (or host thread) per GPU, one ptrom_ctx and one ptrom_comm per rank.

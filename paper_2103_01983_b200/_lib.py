@@ -113,6 +113,16 @@ PROTOTYPES = {
                                         C.POINTER(C.c_void_p)]),
     "ptrom_surrogate_sizes": (C.c_int, [C.c_void_p, c_dp]),
     "ptrom_surrogate_export_lists": (C.c_int, [c_ctxp, C.c_void_p] + [c_dp] * 10),
+    "ptrom_io_last_error": (C.c_char_p, []),
+    "ptrom_ptmx_read": (C.c_int, [c_ctxp, C.c_char_p, c_dp, c_dp, c_dp, c_dp, c_dp, C.c_uint64]),
+    "ptrom_ptmx_write": (C.c_int, [c_ctxp, C.c_char_p, C.c_uint64, C.c_uint64, C.c_double, C.c_double, c_dp]),
+    "ptrom_bundle_open": (C.c_int, [c_ctxp, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ptrom_bundle_free": (None, [C.c_void_p]),
+    "ptrom_bundle_sizes": (C.c_int, [C.c_void_p, c_dp]),
+    "ptrom_bundle_config_json": (c_i64, [C.c_void_p, C.c_char_p, c_i64]),
+    "ptrom_bundle_export": (C.c_int, [C.c_void_p] + [c_dp] * 23),
+    "ptrom_bundle_to_device": (C.c_int, [c_ctxp, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                         C.POINTER(C.c_void_p)]),
     "ptrom_comm_unique_id": (C.c_int, [C.c_void_p]),
     "ptrom_comm_init": (C.c_int, [c_ctxp, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ptrom_comm_init_host": (C.c_int, [c_ctxp, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -261,3 +261,103 @@ class OfflineBundle:  # bundle.hpp:15-27
 def write_trajectory(path, x_hat, dt: float, t0: float = 0.0) -> None:
     """x̂ (M x n_steps) as a time-series PTMX (io.hpp:23-26: dt/t0 set)."""
     write_matrix(path, x_hat, dt, t0)
+
+
+# ------------------------------------------------------------------ native --
+def _native_lib():
+    from . import _lib
+    return _lib.load()
+
+
+def _native_check(rc, ctx=None):
+    if rc == 0:
+        return
+    msg = (ctx.lib.ptrom_last_error(ctx.handle) if ctx is not None else _native_lib().ptrom_io_last_error()).decode()
+    if rc == 2:
+        raise ConfigError(msg)
+    from .api import CudaError, NumericalError
+    raise (NumericalError if rc == 3 else CudaError)(msg)
+
+
+def read_matrix_native(path) -> MatrixFile:
+    """io.hpp:53-75 through the C ABI (ptrom_ptmx_read; no GPU needed)."""
+    import ctypes as C
+    lib = _native_lib()
+    rows, cols, dt, t0 = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_double()
+    p = os.fsencode(path)
+    _native_check(lib.ptrom_ptmx_read(None, p, C.addressof(rows), C.addressof(cols), C.addressof(dt),
+                                      C.addressof(t0), None, 0))
+    data = np.zeros(max(rows.value * cols.value, 1))
+    _native_check(lib.ptrom_ptmx_read(None, p, None, None, None, None, data.ctypes.data, data.shape[0]))
+    return MatrixFile(data[:rows.value * cols.value].reshape((rows.value, cols.value), order="F"), dt.value, t0.value)
+
+
+def write_matrix_native(path, mat, dt: float = 0.0, t0: float = 0.0) -> None:
+    """io.hpp:35-51 through the C ABI (ptrom_ptmx_write)."""
+    a = np.asarray(mat, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    a = np.asfortranarray(a)
+    _native_check(_native_lib().ptrom_ptmx_write(None, os.fsencode(path), a.shape[0], a.shape[1], float(dt),
+                                                 float(t0), a.ctypes.data))
+
+
+def load_native(directory) -> OfflineBundle:
+    """bundle.cpp:96-141 through the C ABI (ptrom_bundle_open + _export): the
+    loader a C++ host links; returns the same OfflineBundle as load()."""
+    import ctypes as C
+    lib = _native_lib()
+    h = C.c_void_p()
+    _native_check(lib.ptrom_bundle_open(None, os.fsencode(directory), C.byref(h)))
+    try:
+        sz = np.zeros(11, np.int64)
+        lib.ptrom_bundle_sizes(h, sz.ctypes.data)
+        nd, m, mr, ns, ar, nc, u, nt, nmem, ncl, ndl = (int(v) for v in sz)
+        F = lambda r, c: np.zeros((r, c), order="F")
+        out = dict(basis_phi=F(nd, m), basis_sv=np.zeros(m), basis_xref=np.zeros(nd), residual_phi=F(nd, mr),
+                   residual_sv=np.zeros(mr), gnat_a=F(ar, 2 * ns), sample_ids=np.zeros(ns, np.int64),
+                   phi_tilde=F(2 * nc, m), x0_tilde=np.zeros(2 * nc), gamma_tilde=np.zeros(nc),
+                   cluster_node_ids=np.zeros(nc, np.int32), mem_off=np.zeros(nc + 1, np.int64),
+                   mem_ids=np.zeros(nmem, np.int64), zero_gamma=np.zeros(nc, np.uint8),
+                   target_ids=np.zeros(nt, np.int64), cl_off=np.zeros(nt + 1, np.int64),
+                   cl_list=np.zeros(ncl, np.int64), d_off=np.zeros(nt + 1, np.int64), d_list=np.zeros(ndl, np.int64),
+                   direct_ids=np.zeros(u, np.int64), direct_phi=F(2 * u, m), direct_x0=np.zeros(2 * u),
+                   direct_gamma=np.zeros(u))
+        order = ["basis_phi", "basis_sv", "basis_xref", "residual_phi", "residual_sv", "gnat_a", "sample_ids",
+                 "phi_tilde", "x0_tilde", "gamma_tilde", "cluster_node_ids", "mem_off", "mem_ids", "zero_gamma",
+                 "target_ids", "cl_off", "cl_list", "d_off", "d_list", "direct_ids", "direct_phi", "direct_x0",
+                 "direct_gamma"]
+        _native_check(lib.ptrom_bundle_export(h, *(out[k].ctypes.data if out[k].size else None for k in order)))
+        n = lib.ptrom_bundle_config_json(h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        lib.ptrom_bundle_config_json(h, buf, n + 1)
+        config = json.loads(buf.value.decode()) if n > 0 else None
+    finally:
+        lib.ptrom_bundle_free(h)
+    return OfflineBundle(config=config, **out)
+
+
+def to_device_native(directory, ctx=None):
+    """ptrom_bundle_open + ptrom_bundle_to_device: (PODBasis, GnatOperator,
+    SurrogateSourceBasis) built by the C loader, no Python table handling."""
+    import ctypes as C
+
+    from .api import default_context
+    from .rom import GnatOperator, PODBasis, SurrogateSourceBasis
+    ctx = ctx or default_context()
+    lib = ctx.lib
+    h = C.c_void_p()
+    _native_check(lib.ptrom_bundle_open(ctx.handle, os.fsencode(directory), C.byref(h)), ctx)
+    try:
+        sz = np.zeros(11, np.int64)
+        lib.ptrom_bundle_sizes(h, sz.ctypes.data)
+        nd, m, mr, ns, ar, nc, u, nt = (int(v) for v in sz[:8])
+        hb, ho, hs = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _native_check(lib.ptrom_bundle_to_device(ctx.handle, h, C.byref(hb), C.byref(ho), C.byref(hs)), ctx)
+        tid = np.zeros(nt, np.int64)
+        ids = np.zeros(ns, np.int64)
+        lib.ptrom_bundle_export(h, *([None] * 6), ids.ctypes.data, *([None] * 7), tid.ctypes.data, *([None] * 8))
+    finally:
+        lib.ptrom_bundle_free(h)
+    return (PODBasis.adopt(ctx, hb, nd, m), GnatOperator.adopt(ctx, ho, ids),
+            SurrogateSourceBasis(ctx, hs, m, nc, u, nt, tid))

@@ -49,12 +49,21 @@ class PODBasis:  # reduction.hpp:18-26
                                                        _p(self.phi), _p(self.singular_values), _p(self.x_ref),
                                                        C.byref(h)))
         self._h = h
+        self._shape = self.phi.shape
+
+    @classmethod
+    def adopt(cls, ctx: Context, handle, n_dofs: int, modes: int) -> "PODBasis":
+        """Wraps a device basis the library built (ptrom_bundle_to_device); no host copy."""
+        b = cls.__new__(cls)
+        b.ctx, b._h, b._shape = ctx, handle, (int(n_dofs), int(modes))
+        b.phi = b.singular_values = b.x_ref = None
+        return b
 
     def dim(self):
-        return self.phi.shape[0]
+        return self._shape[0]
 
     def modes(self):
-        return self.phi.shape[1]
+        return self._shape[1]
 
     def reconstruct_output(self, x_hat, dofs=None) -> np.ndarray:
         """rom.hpp:45-58 (dofs given) / rom.hpp:60-64 reconstruct_full (dofs None), on the device."""
@@ -90,6 +99,13 @@ class GnatOperator:  # reduction.hpp:173-180
                                                          _p(self.sample_ids), self.A.shape[0], _p(self.A),
                                                          C.byref(h)))
         self._h = h
+
+    @classmethod
+    def adopt(cls, ctx: Context, handle, sample_ids) -> "GnatOperator":
+        """Wraps a device operator the library built (ptrom_bundle_to_device)."""
+        g = cls.__new__(cls)
+        g.ctx, g._h, g.sample_ids, g.A = ctx, handle, _i64(sample_ids), None
+        return g
 
     def __del__(self):
         try:

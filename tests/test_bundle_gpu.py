@@ -29,6 +29,12 @@ def test_bundle_to_device_simulate_equals_in_memory(pt, oracle, tmp_path):
     gm = w.gamma_a + 1.3 * w.gamma_b
     tr = rom.ptrom_simulate(basis, op, sur, pt.ParticleSystem(gm, w.delta), pt.TimeGrid(w.dt, steps),
                             rom.RomConfig(1e-8, 20, 1.0))
+    # the C loader (ptrom_bundle_open + ptrom_bundle_to_device) drives the same march bit for bit
+    nb, no, ns = bundle.to_device_native(tmp_path / "b")
+    tn = rom.ptrom_simulate(nb, no, ns, pt.ParticleSystem(gm, w.delta), pt.TimeGrid(w.dt, steps),
+                            rom.RomConfig(1e-8, 20, 1.0))
+    np.testing.assert_array_equal(tn.x_hat, tr.x_hat)
+    np.testing.assert_array_equal(tn.iterations, tr.iterations)
     xo, it_o, _ = oracle.ptrom_simulate(oracle.Surrogate(w.phi, w.sv, w.x0, g, ids, 1, 1.0, 1), w.phi, w.sv, w.x0,
                                         ids, A, gm, w.delta, w.dt, steps, 1e-8, 20)
     np.testing.assert_array_equal(tr.iterations, it_o)
