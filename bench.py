@@ -466,8 +466,6 @@ def config1_line(args, K, W, local, cpu_seconds):
     for _ in range(W):
         step()
     torch.cuda.synchronize()
-    import bench_extra
-    ours, _ = bench_extra._count_launches(step)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     nv = nj = 0
@@ -520,7 +518,7 @@ def config1_line(args, K, W, local, cpu_seconds):
         cpu = {"value": evals * pairs / dtc, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"oracle fom_simulate, {steps_cpu} of {w.n_steps} steps of {w.name} "
                          f"({evals} velocity+Jacobian evaluations, {dtc:.1f} s, 1 thread)"}
-    return {
+    line = {
         "metric": "Biot-Savart pair interactions/s (fp64), FOM trajectory (velocity + Jacobian pairs)",
         "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": total_ms / K,
         "higher_is_better": True, "scaling": "weak", "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
@@ -528,9 +526,11 @@ def config1_line(args, K, W, local, cpu_seconds):
                    "newton": "tol 1e-10, max_iters 100, refresh 1 (integrators.hpp:55-58)",
                    "unit_of_step": "one 100-step trajectory", "l2": "flushed between trajectories"},
         "trajectory_ms": total_ms / K, "newton_updates_per_trajectory": float(np.sum(res["r"][1])),
-        "gpu_launches": ours * K if ours is not None else None,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
     }
+    import bench_extra
+    bench_extra.defer_count(line, step, K)
+    return line
 
 
 def extras(args, local):
@@ -572,6 +572,7 @@ def extras(args, local):
 
     guard("config3", c3)
     guard("config4", c4)
+    bench_extra.run_deferred_counts()
     return out
 
 
@@ -644,7 +645,9 @@ def main():
     torch.cuda.set_device(local)
     if args.workload == "config1":
         if rank == 0:
+            import bench_extra
             line = config1_line(args, args.steps, args.warmup, local, args.cpu_seconds)
+            bench_extra.run_deferred_counts()
             print(json.dumps(line), flush=True)
         return 0
     if world > 1:

@@ -52,6 +52,25 @@ def _count_launches(fn):
         return None, None
 
 
+# Launch counting runs the torch profiler (CUPTI), which stays attached to the
+# process afterwards; every count is therefore deferred until all timed
+# regions of the run are done (run_deferred_counts).
+_DEFERRED = []
+
+
+def defer_count(line, fn, mult):
+    """line["gpu_launches"] = (our kernels launched by one fn()) * mult, later."""
+    line["gpu_launches"] = None
+    _DEFERRED.append((line, fn, mult))
+
+
+def run_deferred_counts():
+    while _DEFERRED:
+        line, fn, mult = _DEFERRED.pop(0)
+        ours, _ = _count_launches(fn)
+        line["gpu_launches"] = ours * mult if ours is not None else None
+
+
 def _steps(args, default):
     return args.steps if args.steps_given else default
 
@@ -77,6 +96,9 @@ def run(args, rank, world):
         # config 4: every rank marches its own μ block (weak scaling)
         strong = line.get("scaling") == "strong"
         line["value"] = line["units_per_step"] * (1 if strong else world) * 1e3 / line["ms_per_step"]
+    run_deferred_counts()  # every rank (the sharded step has collectives)
+    if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
     line.pop("units_per_step", None)
     if rank == 0:
@@ -118,7 +140,6 @@ def bench_config3(args, world):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    ours, total = _count_launches(step)
     K = _steps(args, 20)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -196,7 +217,7 @@ def bench_config3(args, world):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_config3(w, theta, leaf, args.cpu_seconds)
-    return {
+    line = {
         "metric": "Barnes-Hut velocity evaluation bodies/s (fp64; build + aggregation + far field)",
         "value": value, "unit": "bodies/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": total_ms / K, "units_per_step": n, "higher_is_better": True,
@@ -206,11 +227,12 @@ def bench_config3(args, world):
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "parallelism": "single GPU" if world == 1 else
                    f"replicated build, far field split by tree slot x{world} (NCCL all-gather)"},
-        "gpu_launches": ours * K if ours is not None else None,
         "e2e": e2e, "roofline": roofline, "build_roofline": build_roof, "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "phase_ms": {"build_median": build_ms, "far_field_avg": eval_ms},
     }
+    defer_count(line, step, K)
+    return line
 
 
 def _measured_hbm():
@@ -337,15 +359,13 @@ def bench_config4(args, world):
                 "hbm_view": {"algorithmic_bytes_per_launch": alg_bytes,
                              "achieved_gbs": alg_bytes / (avg_hp_ms * 1e-3) / 1e9, "peak_gbs": hbm},
                 "peak_source": "measured live: tools/peaks.cu DFMA chain"}
-    ours, _ = _count_launches(lambda: rom.ptrom_simulate_batch(basis, op, sur, w.gamma_a, w.gamma_b, mu_rank[:B],
-                                                               sys_, pt.TimeGrid(w.dt, 1), cfg, batch=B))
     e2e = {"value": units * K / wall, "unit": "instance-steps/s",
            "h2d_bytes_per_step": int(8 * B + 16 * w.n), "d2h_bytes_per_step": int(B * n_steps * (8 * basis.modes() + 5)),
            "api": "ptrom_ptrom_simulate_batch_f64 (host μ, Γa, Γb in; host x̂, iterations, converged out)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_config4(w, ids, A, args.cpu_seconds)
-    return {
+    line = {
         "metric": "PTROM online instance-steps/s (fp64)", "value": value, "unit": "instance-steps/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K, "units_per_step": units,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -358,10 +378,12 @@ def bench_config4(args, world):
                    "offline": offline,
                    "l2": "working set (positions of 768k sources x B instances) exceeds L2",
                    "parallelism": "single GPU" if world == 1 else f"mu instances split x{world}"},
-        "gpu_launches": ours * K * n_steps if ours is not None else None,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
         "finite": finite, "interactions_per_instance_step": interactions / (units * K),
     }
+    defer_count(line, lambda: rom.ptrom_simulate_batch(basis, op, sur, w.gamma_a, w.gamma_b, mu_rank[:B], sys_,
+                                                       pt.TimeGrid(w.dt, 1), cfg, batch=B), K * n_steps)
+    return line
 
 
 def _cpu_config4(w, ids, A, seconds):

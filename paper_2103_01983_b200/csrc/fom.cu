@@ -20,6 +20,7 @@
 // residual and update are bit-identical to the oracle. ‖r‖ is a fixed-order
 // two-level reduction (per-thread strided sums, warp/block trees in a fixed
 // shape, then the block partials in index order): deterministic run to run.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -31,7 +32,13 @@ namespace ptrom {
 namespace {
 
 constexpr int kNormThreads = 256;
-constexpr int kNormBlocks = 296;  // 2 x 148 SMs; fixed so the reduction shape is fixed
+constexpr int kNormBlocks = 296;  // 2 x 148 SMs: the most blocks a residual reduction uses
+// Residual blocks for m rows of each half: one block per 1,024 of the 2m rows,
+// capped at kNormBlocks. A function of m alone, so every entry point (graph,
+// host loop, sharded ranks of the same m) reduces in the same fixed shape.
+inline int norm_blocks(long long m) {
+  return (int)std::max(1LL, std::min<long long>(kNormBlocks, (2 * m + 1023) / 1024));
+}
 
 // r = (xi - x_prev) - h*(f_xi + f_prev) on rows k and k+ld, k < m
 // (integrators.hpp:47-53), with fixed-order partial sums of r².
@@ -187,12 +194,20 @@ __global__ void fom_refresh_gate_kernel(FomCtl* c, cudaGraphConditionalHandle h_
 }
 
 // StepResult + snapshot column of the accepted state (integrators.hpp:262-268).
+// The accepted state also becomes the history (integrators.hpp:262-264):
+// x_prev ← ξ, f_prev ← f_ξ; ξ and f_ξ already hold the next step's initial
+// guess (integrators.hpp:130-131), so no copies run at the start of a step.
 __global__ void fom_record_kernel(const FomCtl* c, long long dim, const double* __restrict__ x,
-                                  double* __restrict__ snaps, int* __restrict__ iters,
+                                  const double* __restrict__ fx, double* __restrict__ x_prev,
+                                  double* __restrict__ f_prev, double* __restrict__ snaps, int* __restrict__ iters,
                                   unsigned char* __restrict__ conv, double* __restrict__ rel) {
   const long long s = c->step;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < dim; k += (long long)gridDim.x * blockDim.x)
-    snaps[s * dim + k] = x[k];
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < dim; k += (long long)gridDim.x * blockDim.x) {
+    const double v = x[k];
+    snaps[s * dim + k] = v;
+    x_prev[k] = v;
+    f_prev[k] = fx[k];
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     iters[s] = c->updates;
     conv[s] = (unsigned char)c->converged;
@@ -218,9 +233,10 @@ int grid_for(ptrom_ctx* ctx, long long count, int tpb) {
 
 void dev_residual_f64(ptrom_ctx* ctx, long long m, long long ld, const double* xi, const double* fxi,
                       const double* xp, const double* fp, double dt, double* r, double* norm2, double* block_part) {
-  residual_kernel<<<kNormBlocks, kNormThreads, 0, ctx->stream>>>(m, ld, xi, fxi, xp, fp, dt / 2.0, r, block_part);
+  const int nb = norm_blocks(m);
+  residual_kernel<<<nb, kNormThreads, 0, ctx->stream>>>(m, ld, xi, fxi, xp, fp, dt / 2.0, r, block_part);
   PTROM_LAUNCH_CHECK();
-  sum_blocks_kernel<<<1, 32, 0, ctx->stream>>>(kNormBlocks, block_part, norm2);
+  sum_blocks_kernel<<<1, 32, 0, ctx->stream>>>(nb, block_part, norm2);
   PTROM_LAUNCH_CHECK();
 }
 
@@ -312,16 +328,18 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
   const bool prof = ctx->prof_on;
   ctx->prof_on = false;  // no event nodes inside conditional bodies
   cudaGraphConditionalHandle h_loop, h_ref;
-  PTROM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
-  // pre: ξ = x_prev, f_ξ = f_prev (integrators.hpp:130-131); r; decide
+  // ξ = x_prev, f_ξ = f_prev (integrators.hpp:130-131) for the first step;
+  // later steps inherit them from fom_record_kernel
   PTROM_CUDA(cudaMemcpyAsync(xi, x_prev, dim * 8, cudaMemcpyDeviceToDevice, st));
   PTROM_CUDA(cudaMemcpyAsync(fxi, f_prev, dim * 8, cudaMemcpyDeviceToDevice, st));
+  PTROM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  // pre: r; decide
   // the loop node's handle must exist before the kernel that sets it
   cudaStreamCaptureStatus cs;
   cudaGraph_t g_cap;
   PTROM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g_cap, nullptr, nullptr));
   PTROM_CUDA(cudaGraphConditionalHandleCreate(&h_loop, g_cap, 0, 0));
-  residual_decide_kernel<<<kNormBlocks, kNormThreads, 0, st>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part, ctl,
+  residual_decide_kernel<<<norm_blocks(n), kNormThreads, 0, st>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part, ctl,
                                                                 tol, max_iters, refresh, h_loop);
   {
     // WHILE (continue): [IF refresh: Newton blocks]; update; velocity; r; decide
@@ -365,7 +383,7 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
     ctx->stream = s_body;
     newton_update_kernel<<<grid_for(ctx, n, 256), 256, 0, s_body>>>(n, n, inv, r, xi);
     dev_velocity_f64(ctx, n, xi, d_gamma, delta, form, d_inflow, 0, n, fxi, n);
-    residual_decide_kernel<<<kNormBlocks, kNormThreads, 0, s_body>>>(n, n, xi, fxi, x_prev, f_prev, h, r,
+    residual_decide_kernel<<<norm_blocks(n), kNormThreads, 0, s_body>>>(n, n, xi, fxi, x_prev, f_prev, h, r,
                                                                       block_part, ctl, tol, max_iters, refresh,
                                                                       h_loop);
     ctx->stream = saved;
@@ -373,9 +391,8 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
     PTROM_CUDA(cudaStreamEndCapture(s_body, &tmp));
   }
   // post: record the accepted state, it becomes the history (integrators.hpp:262-264)
-  fom_record_kernel<<<grid_for(ctx, dim, 256), 256, 0, st>>>(ctl, dim, xi, snaps, d_iters, d_conv, d_rel);
-  PTROM_CUDA(cudaMemcpyAsync(x_prev, xi, dim * 8, cudaMemcpyDeviceToDevice, st));
-  PTROM_CUDA(cudaMemcpyAsync(f_prev, fxi, dim * 8, cudaMemcpyDeviceToDevice, st));
+  fom_record_kernel<<<grid_for(ctx, dim, 256), 256, 0, st>>>(ctl, dim, xi, fxi, x_prev, f_prev, snaps, d_iters, d_conv,
+                                                             d_rel);
   fom_advance_kernel<<<1, 32, 0, st>>>(ctl);
   PTROM_CUDA(cudaStreamEndCapture(st, &graph));
   ctx->prof_on = prof;
