@@ -224,6 +224,46 @@ __global__ void fom_advance_kernel(FomCtl* c) {
   c->rel = 0.0;
 }
 
+// Small systems (2m ≤ kOneBlockRows rows, e.g. config 1's 8,192): the
+// residual, its fixed-order norm and (DECIDE) the Newton decision in one
+// block of 1,024 threads — no block partials, fence or arrival ticket on the
+// per-iteration critical path. Every entry point uses this shape for such m.
+constexpr int kOneBlockThreads = 1024;
+constexpr int kOneBlockPer = 8;  // rows per thread, all loads issued before the sums
+constexpr long long kOneBlockRows = (long long)kOneBlockThreads * kOneBlockPer;
+template <bool DECIDE>
+__global__ void __launch_bounds__(kOneBlockThreads) residual_one_block_kernel(
+    long long m, long long ld, const double* __restrict__ xi, const double* __restrict__ fxi,
+    const double* __restrict__ xp, const double* __restrict__ fp, double h, double* __restrict__ r,
+    double* __restrict__ norm2, FomCtl* c, double tol, int max_iters, int refresh, cudaGraphConditionalHandle h_loop) {
+  const long long rows = 2 * m;
+  double v[kOneBlockPer];
+#pragma unroll
+  for (int i = 0; i < kOneBlockPer; ++i) {
+    const long long e = threadIdx.x + (long long)i * kOneBlockThreads;
+    v[i] = 0.0;
+    if (e < rows) {
+      const long long k = e < m ? e : (e - m) + ld;
+      v[i] = __dsub_rn(__dsub_rn(xi[k], xp[k]), __dmul_rn(h, __dadd_rn(fxi[k], fp[k])));
+      r[k] = v[i];
+    }
+  }
+  double acc = 0.0;  // the same per-thread order as the strided loop
+#pragma unroll
+  for (int i = 0; i < kOneBlockPer; ++i) acc = __dadd_rn(acc, __dmul_rn(v[i], v[i]));
+  __shared__ double warp_sum[kOneBlockThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kOneBlockThreads / 32; ++w) sum = __dadd_rn(sum, warp_sum[w]);
+    if (DECIDE) fom_decide(c, sum, tol, max_iters, refresh, h_loop);
+    else *norm2 = sum;
+  }
+}
+
 int grid_for(ptrom_ctx* ctx, long long count, int tpb) {
   long long g = (count + tpb - 1) / tpb;
   return (int)std::max(1LL, std::min(g, (long long)ctx->num_sms * 8));
@@ -233,6 +273,12 @@ int grid_for(ptrom_ctx* ctx, long long count, int tpb) {
 
 void dev_residual_f64(ptrom_ctx* ctx, long long m, long long ld, const double* xi, const double* fxi,
                       const double* xp, const double* fp, double dt, double* r, double* norm2, double* block_part) {
+  if (2 * m <= kOneBlockRows) {
+    residual_one_block_kernel<false><<<1, kOneBlockThreads, 0, ctx->stream>>>(m, ld, xi, fxi, xp, fp, dt / 2.0, r,
+                                                                             norm2, nullptr, 0.0, 0, 1, 0);
+    PTROM_LAUNCH_CHECK();
+    return;
+  }
   const int nb = norm_blocks(m);
   residual_kernel<<<nb, kNormThreads, 0, ctx->stream>>>(m, ld, xi, fxi, xp, fp, dt / 2.0, r, block_part);
   PTROM_LAUNCH_CHECK();
@@ -339,8 +385,15 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
   cudaGraph_t g_cap;
   PTROM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g_cap, nullptr, nullptr));
   PTROM_CUDA(cudaGraphConditionalHandleCreate(&h_loop, g_cap, 0, 0));
-  residual_decide_kernel<<<norm_blocks(n), kNormThreads, 0, st>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part, ctl,
-                                                                tol, max_iters, refresh, h_loop);
+  auto residual_decide = [&](cudaStream_t on) {
+    if (2 * n <= kOneBlockRows)
+      residual_one_block_kernel<true><<<1, kOneBlockThreads, 0, on>>>(n, n, xi, fxi, x_prev, f_prev, h, r, nullptr,
+                                                                       ctl, tol, max_iters, refresh, h_loop);
+    else
+      residual_decide_kernel<<<norm_blocks(n), kNormThreads, 0, on>>>(n, n, xi, fxi, x_prev, f_prev, h, r, block_part,
+                                                                      ctl, tol, max_iters, refresh, h_loop);
+  };
+  residual_decide(st);
   {
     // WHILE (continue): [IF refresh: Newton blocks]; update; velocity; r; decide
     const cudaGraphNode_t* deps = nullptr;
@@ -383,9 +436,7 @@ static FomResult fom_simulate_graph(ptrom_ctx* ctx, long long n, const double* d
     ctx->stream = s_body;
     newton_update_kernel<<<grid_for(ctx, n, 256), 256, 0, s_body>>>(n, n, inv, r, xi);
     dev_velocity_f64(ctx, n, xi, d_gamma, delta, form, d_inflow, 0, n, fxi, n);
-    residual_decide_kernel<<<norm_blocks(n), kNormThreads, 0, s_body>>>(n, n, xi, fxi, x_prev, f_prev, h, r,
-                                                                      block_part, ctl, tol, max_iters, refresh,
-                                                                      h_loop);
+    residual_decide(s_body);
     ctx->stream = saved;
     cudaGraph_t tmp;
     PTROM_CUDA(cudaStreamEndCapture(s_body, &tmp));
