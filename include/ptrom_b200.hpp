@@ -147,6 +147,153 @@ class BarnesHutModelVec {
   mutable uint64_t pair_evals_ = 0;
 };
 
+// ------------------------------------------------------ PTROM online path --
+// Drop-in for ptrom::ptrom_simulate<double> (rom.hpp:404-412) on the
+// reference's own offline types: PODBasis {phi, singular_values, x_ref},
+// GnatOperator {sample_ids, A}, SurrogateSourceBasis {phi_tilde, gamma_tilde,
+// x0_tilde, cluster_membership, zero_gamma, target_ids, per_target_clusters,
+// per_target_direct, direct_ids, direct_phi, direct_x0, direct_gamma},
+// ParticleSystem {circulation, delta, kernel_form, inflow}, RomConfig {tol,
+// max_iters, step_length}, RomTrajectory {x_hat, iterations, converged}.
+// Matrices may be Eigen (data(), rows(), cols(), resize()) or any column-major
+// type with the fields {rows, cols, a}; nested index lists become the C ABI's
+// CSR arrays here, so the caller writes no marshalling. As in the reference
+// the surrogate is reassigned in place: its tables are written back.
+namespace detail {
+template <class M>
+const double* mat_data(const M& m) {
+  if constexpr (requires { m.data(); }) return m.data();
+  else return m.a.data();
+}
+template <class M>
+double* mat_data(M& m) {
+  if constexpr (requires { m.data(); }) return m.data();
+  else return m.a.data();
+}
+template <class M>
+int64_t mat_rows(const M& m) {
+  if constexpr (requires { m.rows(); }) return static_cast<int64_t>(m.rows());
+  else return static_cast<int64_t>(m.rows);
+}
+template <class M>
+int64_t mat_cols(const M& m) {
+  if constexpr (requires { m.cols(); }) return static_cast<int64_t>(m.cols());
+  else return static_cast<int64_t>(m.cols);
+}
+template <class M>
+void mat_resize(M& m, int64_t r, int64_t c) {
+  if constexpr (requires { m.resize(r, c); }) m.resize(r, c);
+  else m = M(r, c);
+}
+template <class L>
+void to_csr(const L& nested, std::vector<int64_t>& off, std::vector<int64_t>& flat) {
+  off.assign(1, 0);
+  flat.clear();
+  for (const auto& l : nested) {
+    for (const auto v : l) flat.push_back(static_cast<int64_t>(v));
+    off.push_back(static_cast<int64_t>(flat.size()));
+  }
+}
+template <class V>
+std::vector<int64_t> to_i64(const V& v) {
+  return std::vector<int64_t>(v.begin(), v.end());
+}
+template <class Sys>
+const double* inflow_ptr(const Sys& sys) {
+  if constexpr (requires { sys.has_inflow; }) return sys.has_inflow ? sys.inflow.data() : nullptr;
+  else if constexpr (requires { sys.inflow->data(); }) return sys.inflow ? sys.inflow->data() : nullptr;
+  else return sys.inflow.empty() ? nullptr : sys.inflow.data();
+}
+}  // namespace detail
+
+// Device-resident copies of the offline products (basis, operator,
+// surrogate) for repeated online queries; `simulate` is rom.hpp:404-412.
+class DevicePtrom {
+ public:
+  template <class Basis, class Op, class Sur>
+  DevicePtrom(const Context& ctx, const Basis& basis, const Op& op, const Sur& sur) : ctx_(ctx) {
+    const int64_t nd = detail::mat_rows(basis.phi), m = detail::mat_cols(basis.phi);
+    n_ = nd / 2;
+    m_ = m;
+    ctx_.check(ptrom_basis_create(ctx_.get(), nd, m, detail::mat_data(basis.phi), basis.singular_values.data(),
+                                  basis.x_ref.data(), &basis_));
+    const std::vector<int64_t> ids = detail::to_i64(op.sample_ids);
+    check_or_free(ptrom_gnat_op_create(ctx_.get(), basis_, static_cast<int64_t>(ids.size()), ids.data(),
+                                       detail::mat_rows(op.A), detail::mat_data(op.A), &op_));
+    std::vector<int64_t> mem_off, mem_ids, cl_off, cl_list, d_off, d_list;
+    detail::to_csr(sur.cluster_membership, mem_off, mem_ids);
+    detail::to_csr(sur.per_target_clusters, cl_off, cl_list);
+    detail::to_csr(sur.per_target_direct, d_off, d_list);
+    const std::vector<int64_t> tid = detail::to_i64(sur.target_ids), did = detail::to_i64(sur.direct_ids);
+    std::vector<uint8_t> zg(sur.zero_gamma.begin(), sur.zero_gamma.end());
+    const int64_t nc = static_cast<int64_t>(sur.gamma_tilde.size());
+    check_or_free(ptrom_surrogate_create(
+        ctx_.get(), detail::mat_cols(sur.phi_tilde), nc, detail::mat_data(sur.phi_tilde), sur.gamma_tilde.data(),
+        sur.x0_tilde.data(), zg.data(), mem_off.data(), mem_ids.data(), static_cast<int64_t>(tid.size()), tid.data(),
+        cl_off.data(), cl_list.data(), static_cast<int64_t>(did.size()), did.data(), detail::mat_data(sur.direct_phi),
+        sur.direct_x0.data(), sur.direct_gamma.data(), d_off.data(), d_list.data(), &sur_));
+  }
+  ~DevicePtrom() {
+    ptrom_surrogate_free(sur_);
+    ptrom_gnat_op_free(op_);
+    ptrom_basis_free(basis_);
+  }
+  DevicePtrom(const DevicePtrom&) = delete;
+  DevicePtrom& operator=(const DevicePtrom&) = delete;
+
+  // rom.hpp:404-412: reassign the surrogate to sys.circulation (on the device
+  // and in `sur`, the reference's in-place mutation) and march n_steps.
+  template <class Sur, class Sys, class Cfg, class Traj>
+  void simulate(Sur& sur, const Sys& sys, double dt, int64_t n_steps, const Cfg& cfg, Traj& out,
+                uint64_t* pair_evals = nullptr) {
+    detail::mat_resize(out.x_hat, m_, n_steps);
+    out.iterations.assign(static_cast<size_t>(n_steps), 0);
+    std::vector<uint8_t> conv(static_cast<size_t>(n_steps), 0);
+    uint64_t pairs = 0;
+    ctx_.check(ptrom_ptrom_simulate_f64(ctx_.get(), basis_, op_, sur_, n_, sys.circulation.data(), sys.delta,
+                                        static_cast<int>(sys.kernel_form), detail::inflow_ptr(sys), dt, n_steps,
+                                        cfg.tol, cfg.max_iters, cfg.step_length, detail::mat_data(out.x_hat),
+                                        out.iterations.data(), conv.data(), &pairs));
+    out.converged.assign(conv.begin(), conv.end());
+    std::vector<uint8_t> zg(sur.zero_gamma.size());
+    ctx_.check(ptrom_surrogate_export(ctx_.get(), sur_, detail::mat_data(sur.phi_tilde), sur.gamma_tilde.data(),
+                                      sur.x0_tilde.data(), zg.data(), sur.direct_gamma.data()));
+    for (size_t c = 0; c < zg.size(); ++c) sur.zero_gamma[c] = static_cast<char>(zg[c]);
+    if (pair_evals) *pair_evals = pairs;
+  }
+
+  ptrom_basis* basis() const { return basis_; }
+  ptrom_gnat_op* op() const { return op_; }
+  ptrom_surrogate* surrogate() const { return sur_; }
+
+ private:
+  void check_or_free(int rc) {
+    if (rc == PTROM_OK) return;
+    const std::string msg = ptrom_last_error(ctx_.get());
+    ptrom_gnat_op_free(op_);
+    ptrom_basis_free(basis_);
+    op_ = nullptr;
+    basis_ = nullptr;
+    if (rc == PTROM_CONFIG_ERROR) throw config_error(msg);
+    if (rc == PTROM_NUMERICAL_ERROR) throw numerical_error(msg);
+    throw std::runtime_error(msg);
+  }
+  const Context& ctx_;
+  int64_t n_ = 0, m_ = 0;
+  ptrom_basis* basis_ = nullptr;
+  ptrom_gnat_op* op_ = nullptr;
+  ptrom_surrogate* sur_ = nullptr;
+};
+
+// One-shot form with the reference's signature shape:
+//   ptrom_simulate(basis, op, surrogate&, sys, grid.dt, grid.n_steps, cfg, traj)
+template <class Basis, class Op, class Sur, class Sys, class Cfg, class Traj>
+void ptrom_simulate(const Context& ctx, const Basis& basis, const Op& op, Sur& sur, const Sys& sys, double dt,
+                    int64_t n_steps, const Cfg& cfg, Traj& out) {
+  DevicePtrom d(ctx, basis, op, sur);
+  d.simulate(sur, sys, dt, n_steps, cfg, out);
+}
+
 }  // namespace ptrom_b200
 
 #if __has_include(<Eigen/Dense>) && __has_include("ptrom/kernel.hpp")
