@@ -37,162 +37,11 @@
 #include <cmath>
 
 #include "ops.cuh"
+#include "pair_tile.cuh"
 
 namespace ptrom {
 
 constexpr int kMaxPeers = 8;  // ranks whose source blocks one kernel reads in place
-
-__device__ __forceinline__ double rcp_seed(double q) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
-  return y;
-}
-// fp32 reciprocal seed of a double q ∈ [2^-126, 2^126) through integer
-// exponent re-biasing (no FP64-pipe conversion instructions); outside that
-// range the re-biased exponent wraps or the fp32 reciprocal flushes, so every
-// caller guards the range (allpairs_f64_kernel targets_ok / targets_ok4).
-__device__ __forceinline__ double rcp_seed_via_f32(double q) {
-  const int hi = __double2hiint(q), lo = __double2loint(q);
-  const unsigned fb = __funnelshift_l((unsigned)lo, (unsigned)hi, 3) - (896u << 23);
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__uint_as_float(fb)));
-  const unsigned rb = __float_as_uint(r);
-  return __hiloint2double((int)((rb >> 3) + (896u << 20)), (int)(rb << 29));
-}
-__device__ __forceinline__ bool coord_ok(double v) {  // |v| < 2^29 (also false for inf/NaN)
-  return (__double2hiint(v) & 0x7fffffff) < 0x41C00000;
-}
-__device__ __forceinline__ bool coord_ok4(double v) {  // |v| < 2^14: q ∈ [δ', 2^31]
-  return (__double2hiint(v) & 0x7fffffff) < 0x40D00000;
-}
-__device__ __forceinline__ float rcp_approx(float q) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(q));
-  return y;
-}
-
-// ----------------------------------------------------------------- fp64 ---
-// Per-pair accumulation given s = Γ'/q and u = 1/q (u only used for JAC).
-template <bool VEL, bool JAC>
-__device__ __forceinline__ void accumulate(double rx, double ry, double s, double u, double& fx, double& fy,
-                                           double& ja, double& jb, double& jc) {
-  if (JAC) {
-    const double w = s * u;  // Γ'/q²
-    const double t = w * rx;
-    ja = fma(t, ry, ja);
-    const double rx2 = rx * rx;
-    jb = fma(w, fma(ry, ry, -rx2), jb);
-    jc += w;
-  }
-  if (VEL) {
-    fx = fma(-ry, s, fx);
-    fy = fma(rx, s, fy);
-  }
-}
-
-// One source tile against T register-resident targets of this thread.
-//  FAST: targets are taken two at a time and share one reciprocal
-//        (Montgomery): u = 1/(q1·q2) from the fp32 seed + one Newton step,
-//        then 1/q1 = q2·u, 1/q2 = q1·u. Per pair 9 FP64 ops and 2 ALU/MUFU
-//        ops instead of 9 + 4 (the SMSP dispatch, not the FP64 pipe, is the
-//        limit: tools/fp64mix.cu). Needs q ∈ [2^-62, 2^61] (tile guard).
-//  safe: MUFU.RCP64H + cubic correction per pair (propagates q = 0 as inf/NaN).
-template <int T, int UNR, bool VEL, bool JAC, bool MASK, int FAST>
-__device__ __forceinline__ void tile_f64(int cnt, const double2* __restrict__ sp, const double* __restrict__ sg,
-                                         long long j0, const double (&tx)[T], const double (&ty)[T],
-                                         const long long (&ti)[T], double dp, double (&fx)[T], double (&fy)[T],
-                                         double (&ja)[T], double (&jb)[T], double (&jc)[T]) {
-#pragma unroll UNR
-  for (int jj = 0; jj < cnt; ++jj) {
-    const double2 p = sp[jj];
-    const double g = sg[jj];
-    if ((FAST == 4 || FAST == 5) && !MASK && (T % 4 == 0)) {
-      // four targets share one reciprocal: P = (q1 q2)(q3 q4), q ∈ [2^-31, 2^31]
-#pragma unroll
-      for (int k = 0; k < T; k += 4) {
-        double rx[4], ry[4], q[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          rx[m] = tx[k + m] - p.x;
-          ry[m] = ty[k + m] - p.y;
-          q[m] = fma(rx[m], rx[m], fma(ry[m], ry[m], dp));
-        }
-        const double p01 = q[0] * q[1], p23 = q[2] * q[3];
-        const double P = p01 * p23;
-        double uP;  // 1/P
-        if (FAST == 5) {  // MUFU.RCP64H seed (~2^-20) + cubic correction
-          const double y0 = rcp_seed(P);
-          double e = fma(-P, y0, 1.0);
-          e = fma(e, e, e);
-          uP = fma(y0, e, y0);
-        } else {  // fp32 seed via exponent rebias (≤ 2^-22) + one Newton step
-          const double y0 = rcp_seed_via_f32(P);
-          const double e = fma(-P, y0, 1.0);
-          uP = fma(y0, e, y0);
-        }
-        if (JAC) {
-          const double u01 = uP * p23, u23 = uP * p01;  // 1/(q0 q1), 1/(q2 q3)
-          const double u[4] = {u01 * q[1], u01 * q[0], u23 * q[3], u23 * q[2]};
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-            accumulate<VEL, JAC>(rx[m], ry[m], g * u[m], u[m], fx[k + m], fy[k + m], ja[k + m], jb[k + m],
-                                 jc[k + m]);
-        } else {
-          const double gu = g * uP;
-          const double g01 = gu * p23, g23 = gu * p01;  // Γ'/(q0 q1), Γ'/(q2 q3)
-          const double sv[4] = {g01 * q[1], g01 * q[0], g23 * q[3], g23 * q[2]};
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-            accumulate<VEL, JAC>(rx[m], ry[m], sv[m], 0.0, fx[k + m], fy[k + m], ja[k + m], jb[k + m], jc[k + m]);
-        }
-      }
-    } else if (FAST >= 2 && !MASK && (T % 2 == 0)) {
-#pragma unroll
-      for (int k = 0; k < T; k += 2) {
-        const double rx1 = tx[k] - p.x, ry1 = ty[k] - p.y;
-        const double rx2 = tx[k + 1] - p.x, ry2 = ty[k + 1] - p.y;
-        const double q1 = fma(rx1, rx1, fma(ry1, ry1, dp));
-        const double q2 = fma(rx2, rx2, fma(ry2, ry2, dp));
-        const double P = q1 * q2;
-        const double y0 = rcp_seed_via_f32(P);
-        const double e = fma(-P, y0, 1.0);
-        if (JAC) {
-          const double uP = fma(y0, e, y0);  // 1/(q1 q2)
-          const double u1 = q2 * uP, u2 = q1 * uP;
-          accumulate<VEL, JAC>(rx1, ry1, g * u1, u1, fx[k], fy[k], ja[k], jb[k], jc[k]);
-          accumulate<VEL, JAC>(rx2, ry2, g * u2, u2, fx[k + 1], fy[k + 1], ja[k + 1], jb[k + 1], jc[k + 1]);
-        } else {
-          const double gu = g * fma(y0, e, y0);  // Γ'/(q1 q2)
-          accumulate<VEL, JAC>(rx1, ry1, gu * q2, 0.0, fx[k], fy[k], ja[k], jb[k], jc[k]);
-          accumulate<VEL, JAC>(rx2, ry2, gu * q1, 0.0, fx[k + 1], fy[k + 1], ja[k + 1], jb[k + 1], jc[k + 1]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < T; ++k) {
-        const double rx = tx[k] - p.x;
-        const double ry = ty[k] - p.y;
-        double q = fma(rx, rx, fma(ry, ry, dp));
-        double gs = g;
-        if (MASK) {
-          const bool self = (j0 + jj) == ti[k];  // kernel.hpp:118 `if (j == i) continue;`
-          q = self ? 1.0 : q;
-          gs = self ? 0.0 : gs;
-        }
-        const double y0 = rcp_seed(q);
-        double e = fma(-q, y0, 1.0);
-        e = fma(e, e, e);
-        if (JAC) {
-          const double u = fma(y0, e, y0);  // 1/q
-          accumulate<VEL, JAC>(rx, ry, gs * u, u, fx[k], fy[k], ja[k], jb[k], jc[k]);
-        } else {
-          const double g0 = gs * y0;
-          accumulate<VEL, JAC>(rx, ry, fma(g0, e, g0), 0.0, fx[k], fy[k], ja[k], jb[k], jc[k]);
-        }
-      }
-    }
-  }
-}
 
 // Source position loaders. SrcFlat: the SoA state of one device.
 // SrcPeers: the sources are split over G ranks (offsets off[0..G]); rank r's

@@ -474,6 +474,9 @@ FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, c
                               int max_iters, int refresh, double* h_snapshots, int* iters, unsigned char* conv,
                               double* rel_out) {
   const char* mode = std::getenv("PTROM_FOM_GRAPH");
+  if (!(mode && mode[0] == '0') && fom_persistent_applies(ctx, n))  // small systems: one persistent kernel
+    return fom_simulate_persistent(ctx, n, d_x0, d_gamma, delta, form, d_inflow, dt, n_steps, tol, max_iters, refresh,
+                                   h_snapshots, iters, conv, rel_out);
   if (!(mode && mode[0] == '0'))
     return fom_simulate_graph(ctx, n, d_x0, d_gamma, delta, form, d_inflow, dt, n_steps, tol, max_iters, refresh,
                               h_snapshots, iters, conv, rel_out);

@@ -1,0 +1,495 @@
+// fom_persistent.cu — the implicit-trapezoidal FOM (FomStepper::step +
+// fom_simulate, integrators.hpp:117-201, 243-272) for small systems as ONE
+// cooperative persistent kernel: the whole trajectory, every Newton
+// iteration and every decision, without a host round trip or a kernel
+// launch (config 1, N = 4,096: ~400 velocity/Jacobian evaluations of 16.7M
+// pairs each, which as separate launches are bound by launch latency and
+// graph-node overhead, not by the FP64 pipe).
+//
+// Work of one evaluation: items = target tiles (256 targets: 128 threads x 2
+// in registers) x source chunks, taken grid-stride by the resident CTAs, each
+// writing its partials part[chunk][comp][target] (the same tile arithmetic as
+// allpairs.cu, pair_tile.cuh). Between phases a grid barrier; per-target
+// phases (chunk reduction, residual, Newton blocks, update, record) use one
+// fixed thread→target mapping, so they need no barrier among themselves.
+// ‖r‖: per-CTA fixed-order partials, then every CTA sums them in the same
+// fixed order, so all CTAs take the reference's decision (integrators.hpp:
+// 140-155) identically; the partials are double-buffered by call parity.
+// Residual, Newton blocks and update use the reference's rounding order
+// (_rn intrinsics), as fom.cu.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "ops.cuh"
+#include "pair_tile.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ptrom {
+namespace {
+
+constexpr int kPTPB = 128;               // threads per CTA
+constexpr int kPT = 2;                   // targets per thread in a tile item
+constexpr int kPTile = kPTPB * kPT;      // targets per item
+constexpr long long kPersistentMaxN = 16384;
+
+struct PFom {
+  long long n;
+  const double* g;       // Γ (n)
+  const double* inflow;  // 2n or null
+  double dp;             // effective delta
+  double h;              // dt / 2
+  double* xp;            // x_prev (2n); holds x0 on entry
+  double* fp;            // f_prev (2n)
+  double* xi;            // ξ
+  double* fxi;           // f_ξ
+  double* r;             // residual
+  double* inv;           // 4n Newton blocks
+  double* part;          // [nch][3][n]
+  double* block_part;    // [2][gridDim] per-CTA partial ‖r‖² (double-buffered by parity)
+  double* snaps;         // 2n x n_steps
+  int* iters;
+  unsigned char* conv;
+  double* rel_out;
+  long long n_steps;
+  double tol;
+  int max_iters, refresh;
+  int nch, n_tiles;
+  long long chunk_len;
+  long long* counters;  // [0] velocity evaluations, [1] Jacobian evaluations
+  DeviceStatus* st;
+  unsigned long long* prof;  // PTROM_FOM_PROFILE phase times, or null
+};
+
+// Fixed-order block sum of one double per thread (warp shuffles, then the
+// warps in order); the result in every thread.
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kPTPB / 32; ++w) s = __dadd_rn(s, red[w]);
+  return s;
+}
+
+// One tile item's partials (allpairs_f64_kernel's tile loop on SrcFlat).
+template <bool VEL, bool JAC>
+__device__ void pair_items(const PFom& P, const double* __restrict__ x, double2* sp, double* sg) {
+  constexpr int T = kPT, TPB = kPTPB, NCOMP = VEL ? 2 : 3;
+  const double inv2pi = 1.0 / (2.0 * M_PI);
+  const long long n = P.n;
+  const int tid = threadIdx.x;
+  const int n_items = P.n_tiles * P.nch;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int tile = item % P.n_tiles, chunk = item / P.n_tiles;
+    const long long tile0 = (long long)tile * kPTile;
+    double tx[T], ty[T], fx[T], fy[T], ja[T], jb[T], jc[T];
+    long long ti[T];
+    bool my_ok = true, my_ok4 = true;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const long long i = tile0 + k * TPB + tid;
+      const bool ok = i < n;
+      ti[k] = ok ? i : -1;
+      tx[k] = ok ? x[i] : 0.0;
+      ty[k] = ok ? x[n + i] : 0.0;
+      fx[k] = fy[k] = ja[k] = jb[k] = jc[k] = 0.0;
+      my_ok = my_ok && coord_ok(tx[k]) && coord_ok(ty[k]);
+      my_ok4 = my_ok4 && coord_ok4(tx[k]) && coord_ok4(ty[k]);
+    }
+    const long long tile_end = min(tile0 + (long long)kPTile, n);
+    const long long cbeg = (long long)chunk * P.chunk_len, cend = min(n, cbeg + P.chunk_len);
+    const double dp = P.dp;
+    const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62 && dp <= 0x1p60;
+    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
+    double px = 0.0, py = 0.0, pg = 0.0;
+    if (cbeg + tid < cend) {
+      px = x[cbeg + tid];
+      py = x[n + cbeg + tid];
+      pg = P.g[cbeg + tid] * inv2pi;
+    }
+    for (long long j0 = cbeg; j0 < cend; j0 += TPB) {
+      const int cnt = (int)min((long long)TPB, cend - j0);
+      sp[tid] = make_double2(px, py);
+      sg[tid] = pg;
+      const bool fast4 = __syncthreads_and(coord_ok4(px) && coord_ok4(py)) && targets_ok4;
+      const bool fast = fast4 || (__syncthreads_and(coord_ok(px) && coord_ok(py)) && targets_ok);
+      const long long jn = j0 + TPB + tid;
+      if (jn < cend) {
+        px = x[jn];
+        py = x[n + jn];
+        pg = P.g[jn] * inv2pi;
+      }
+      const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt) && (JAC || !fast);
+      if (masked)
+        tile_f64<T, 4, VEL, JAC, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      else if (fast)
+        tile_f64<T, 4, VEL, JAC, false, 2>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      else
+        tile_f64<T, 4, VEL, JAC, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      __syncthreads();
+    }
+    double* out = P.part + (long long)chunk * NCOMP * n;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      if (ti[k] < 0) continue;
+      if (VEL) {
+        out[ti[k]] = fx[k];
+        out[n + ti[k]] = fy[k];
+      } else {
+        out[ti[k]] = ja[k];
+        out[n + ti[k]] = jb[k];
+        out[2 * n + ti[k]] = jc[k];
+      }
+    }
+  }
+}
+
+// [velocity chunk reduction →] residual r = ξ − x_prev − h(f_ξ + f_prev)
+// (integrators.hpp:47-53) → ‖r‖ (every CTA, same fixed order). One fixed
+// thread→target mapping for every per-target phase.
+__device__ double residual_norm(const PFom& P, bool with_velocity, int parity, double* red, cg::grid_group& grid) {
+  const long long n = P.n;
+  const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (long long i = g0; i < n; i += gs) {
+    if (with_velocity) {  // chunk partials in ascending chunk order (fixed), + inflow
+      double sx = 0.0, sy = 0.0;
+      int c = 0;
+      for (; c + 16 <= P.nch; c += 16) {  // 16 chunks loaded ahead of their adds
+        double vx[16], vy[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          vx[u] = __ldcg(P.part + (long long)(c + u) * 2 * n + i);
+          vy[u] = __ldcg(P.part + ((long long)(c + u) * 2 + 1) * n + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          sx += vx[u];
+          sy += vy[u];
+        }
+      }
+      for (; c < P.nch; ++c) {
+        sx += __ldcg(P.part + (long long)c * 2 * n + i);
+        sy += __ldcg(P.part + ((long long)c * 2 + 1) * n + i);
+      }
+      if (P.inflow) {
+        sx = sx + P.inflow[i];
+        sy = sy + P.inflow[n + i];
+      }
+      if (!isfinite(sx) || !isfinite(sy)) latch_status(P.st, kStatusNonFiniteVelocity, i);
+      P.fxi[i] = sx;
+      P.fxi[n + i] = sy;
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const long long k = i + half * n;
+      const double v = __dsub_rn(__dsub_rn(P.xi[k], P.xp[k]), __dmul_rn(P.h, __dadd_rn(P.fxi[k], P.fp[k])));
+      P.r[k] = v;
+      acc = __dadd_rn(acc, __dmul_rn(v, v));
+    }
+  }
+  double* bp = P.block_part + (long long)parity * gridDim.x;
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) bp[blockIdx.x] = s;
+  grid.sync();
+  // every CTA: the same partials in the same order; only the CTAs that own
+  // targets under the grid-stride mapping contributed, and their partials
+  // are loaded together (one L2 round trip, not one per partial)
+  const int nb = (int)min((long long)gridDim.x, (n + blockDim.x - 1) / blockDim.x);
+  const int lane = threadIdx.x & 31;
+  double v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = lane + 32 * u < nb ? __ldcg(bp + lane + 32 * u) : 0.0;
+  double tot = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) tot = __dadd_rn(tot, v[u]);
+  for (int b = lane + 256; b < nb; b += 32) tot = __dadd_rn(tot, __ldcg(bp + b));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot = __dadd_rn(tot, __shfl_down_sync(0xffffffffu, tot, o));
+  tot = __shfl_sync(0xffffffffu, tot, 0);
+  return sqrt(tot);
+}
+
+// Newton blocks (I − h·J)^-1 at ξ from the Jacobian partials
+// (integrators.hpp:181-194, reduce_jacobian_f64_kernel<true>'s rounding).
+__device__ void newton_blocks(const PFom& P) {
+  const long long n = P.n;
+  const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = g0; i < n; i += gs) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    int ch = 0;
+    for (; ch + 8 <= P.nch; ch += 8) {  // ascending chunks, 8 loaded ahead of their adds
+      double va[8], vb[8], vc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double* pc = P.part + (long long)(ch + u) * 3 * n + i;
+        va[u] = __ldcg(pc);
+        vb[u] = __ldcg(pc + n);
+        vc[u] = __ldcg(pc + 2 * n);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a += va[u];
+        b += vb[u];
+        c += vc[u];
+      }
+    }
+    for (; ch < P.nch; ++ch) {
+      const double* pc = P.part + (long long)ch * 3 * n + i;
+      a += __ldcg(pc);
+      b += __ldcg(pc + n);
+      c += __ldcg(pc + 2 * n);
+    }
+    const double j00 = 2.0 * a, j11 = -2.0 * a;
+    const double j01 = b - P.dp * c, j10 = b + P.dp * c;
+    const double b00 = __dsub_rn(1.0, __dmul_rn(P.h, j00));
+    const double b01 = __dsub_rn(0.0, __dmul_rn(P.h, j01));
+    const double b10 = __dsub_rn(0.0, __dmul_rn(P.h, j10));
+    const double b11 = __dsub_rn(1.0, __dmul_rn(P.h, j11));
+    const double det = __dsub_rn(__dmul_rn(b00, b11), __dmul_rn(b01, b10));
+    if (det == 0.0 || !isfinite(det)) latch_status(P.st, kStatusSingularBlock, i);
+    double* o = P.inv + 4 * i;
+    o[0] = __ddiv_rn(b11, det);
+    o[1] = __ddiv_rn(-b01, det);
+    o[2] = __ddiv_rn(-b10, det);
+    o[3] = __ddiv_rn(b00, det);
+  }
+}
+
+// ξ += blocks · (−r) (integrators.hpp:161-167, newton_update_kernel's rounding).
+__device__ void newton_update(const PFom& P) {
+  const long long n = P.n;
+  const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = g0; i < n; i += gs) {
+    const double* b = P.inv + 4 * i;
+    const double rhs0 = -P.r[i], rhs1 = -P.r[n + i];
+    const double d0 = __dadd_rn(__dmul_rn(b[0], rhs0), __dmul_rn(b[1], rhs1));
+    const double d1 = __dadd_rn(__dmul_rn(b[2], rhs0), __dmul_rn(b[3], rhs1));
+    P.xi[i] = __dadd_rn(P.xi[i], d0);
+    P.xi[n + i] = __dadd_rn(P.xi[n + i], d1);
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// PTROM_FOM_PROFILE: CTA 0 accumulates the wall time (ns) of each phase
+// kind into P.prof[0..7]: 0 velocity tiles, 1 barrier after them, 2 reduction
+// + residual + norm, 3 Jacobian tiles, 4 barrier after them, 5 blocks +
+// update, 6 barrier after the update, 7 record.
+#define PF_MARK(k)                                          \
+  if (P.prof && threadIdx.x == 0 && blockIdx.x == 0) {      \
+    const unsigned long long t_ = gtimer();                 \
+    P.prof[k] += t_ - t_last;                               \
+    t_last = t_;                                            \
+  }
+
+__global__ void __launch_bounds__(kPTPB) fom_persistent_kernel(PFom P) {
+  unsigned long long t_last = P.prof ? gtimer() : 0;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double2 sp[kPTPB];
+  __shared__ double sg[kPTPB];
+  __shared__ double red[kPTPB / 32];
+  const long long n = P.n;
+  const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  // f = velocity(x0) (integrators.hpp:257-259); ξ = x_prev, f_ξ = f_prev
+  pair_items<true, false>(P, P.xp, sp, sg);
+  grid.sync();
+  for (long long i = g0; i < n; i += gs) {
+    double sx = 0.0, sy = 0.0;
+    for (int c = 0; c < P.nch; ++c) {
+      sx += __ldcg(P.part + (long long)c * 2 * n + i);
+      sy += __ldcg(P.part + ((long long)c * 2 + 1) * n + i);
+    }
+    if (P.inflow) {
+      sx = sx + P.inflow[i];
+      sy = sy + P.inflow[n + i];
+    }
+    if (!isfinite(sx) || !isfinite(sy)) latch_status(P.st, kStatusNonFiniteVelocity, i);
+    P.fp[i] = P.fxi[i] = sx;
+    P.fp[n + i] = P.fxi[n + i] = sy;
+    P.xi[i] = P.xp[i];
+    P.xi[n + i] = P.xp[n + i];
+  }
+  long long evals = 1, jevals = 0;
+  int parity = 0;
+  bool have_blocks = false;
+  for (long long s = 0; s < P.n_steps; ++s) {
+    const bool refresh_due = (s % P.refresh) == 0 || !have_blocks;
+    bool refreshed = false, converged = false;
+    int updates = 0;
+    double r0 = 0.0, rel = 0.0;
+    double nr = residual_norm(P, false, parity, red, grid);  // f_ξ = f_prev: no evaluation
+    parity ^= 1;
+    while (true) {  // integrators.hpp:140-178
+      if (updates == 0) {
+        r0 = nr;
+        if (r0 == 0.0) {
+          converged = true;
+          rel = 0.0;
+          break;
+        }
+      }
+      rel = nr / r0;
+      if (rel <= P.tol) {
+        converged = true;
+        break;
+      }
+      if (updates >= P.max_iters) break;
+      PF_MARK(7);
+      if (refresh_due && !refreshed) {
+        pair_items<false, true>(P, P.xi, sp, sg);
+        PF_MARK(3);
+        grid.sync();
+        PF_MARK(4);
+        newton_blocks(P);  // same thread→target mapping as the update below
+        refreshed = have_blocks = true;
+        ++jevals;
+      }
+      newton_update(P);
+      ++updates;
+      PF_MARK(5);
+      grid.sync();  // every ξ updated before any tile reads the sources
+      PF_MARK(6);
+      pair_items<true, false>(P, P.xi, sp, sg);
+      ++evals;
+      PF_MARK(0);
+      grid.sync();
+      PF_MARK(1);
+      nr = residual_norm(P, true, parity, red, grid);
+      parity ^= 1;
+      PF_MARK(2);
+    }
+    // the accepted state is the next step's history and initial guess
+    // (integrators.hpp:262-264, 130-131), recorded as a snapshot column
+    double* col = P.snaps + s * 2 * n;
+    for (long long i = g0; i < n; i += gs) {
+      const double x0 = P.xi[i], x1 = P.xi[n + i];
+      col[i] = x0;
+      col[n + i] = x1;
+      P.xp[i] = x0;
+      P.xp[n + i] = x1;
+      P.fp[i] = P.fxi[i];
+      P.fp[n + i] = P.fxi[n + i];
+    }
+    if (lead) {
+      P.iters[s] = updates;
+      P.conv[s] = converged ? 1 : 0;
+      P.rel_out[s] = rel;
+    }
+  }
+  if (lead) {
+    P.counters[0] = evals;
+    P.counters[1] = jevals;
+  }
+}
+
+}  // namespace
+
+bool fom_persistent_applies(ptrom_ctx* ctx, long long n) {
+  if (n > kPersistentMaxN || n < 2) return false;
+  const char* v = std::getenv("PTROM_FOM_PERSISTENT");
+  if (v && v[0] == '0') return false;
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+  return coop != 0;
+}
+
+FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x0, const double* d_gamma,
+                                  double delta, int form, const double* d_inflow, double dt, long long n_steps,
+                                  double tol, int max_iters, int refresh, double* snapshots_out, int* iters,
+                                  unsigned char* conv, double* rel_out) {
+  cudaStream_t st = ctx->stream;
+  int occ = 0;
+  PTROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fom_persistent_kernel, kPTPB, 0));
+  int per_sm = 4;  // CTAs per SM (tuning knob PTROM_FOM_PCTAS)
+  if (const char* v = std::getenv("PTROM_FOM_PCTAS")) per_sm = std::max(1, std::atoi(v));
+  const int grid = ctx->num_sms * std::max(1, std::min(occ, per_sm));
+  PFom P{};
+  P.n = n;
+  P.g = d_gamma;
+  P.inflow = d_inflow;
+  P.dp = effective_delta(delta, form);
+  P.h = dt / 2.0;
+  P.n_steps = n_steps;
+  P.tol = tol;
+  P.max_iters = max_iters;
+  P.refresh = refresh;
+  P.n_tiles = (int)((n + kPTile - 1) / kPTile);
+  P.nch = (int)std::max(1LL, std::min<long long>(grid / P.n_tiles, n / 32));
+  P.chunk_len = (n + P.nch - 1) / P.nch;
+  P.st = ctx->d_status;
+  std::vector<void*> bufs;
+  struct Free {
+    std::vector<void*>* b;
+    cudaStream_t s;
+    ~Free() {
+      for (void* p : *b) cudaFreeAsync(p, s);
+    }
+  } guard{&bufs, st};
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    PTROM_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 8), st));
+    bufs.push_back(p);
+    return p;
+  };
+  const size_t dim = 2 * (size_t)n;
+  P.xp = (double*)alloc(dim * 8);
+  P.fp = (double*)alloc(dim * 8);
+  P.xi = (double*)alloc(dim * 8);
+  P.fxi = (double*)alloc(dim * 8);
+  P.r = (double*)alloc(dim * 8);
+  P.inv = (double*)alloc(4 * (size_t)n * 8);
+  P.part = (double*)alloc((size_t)P.nch * 3 * n * 8);
+  P.block_part = (double*)alloc(2 * (size_t)grid * 8);
+  const bool own_snaps = snapshots_out == nullptr;
+  P.snaps = (double*)alloc(dim * std::max<long long>(n_steps, 1) * 8);
+  P.iters = (int*)alloc(std::max<long long>(n_steps, 1) * 4);
+  P.conv = (unsigned char*)alloc(std::max<long long>(n_steps, 1));
+  P.rel_out = (double*)alloc(std::max<long long>(n_steps, 1) * 8);
+  P.counters = (long long*)alloc(16);
+  const bool prof = std::getenv("PTROM_FOM_PROFILE") != nullptr;
+  if (prof) {
+    P.prof = (unsigned long long*)alloc(64);
+    PTROM_CUDA(cudaMemsetAsync(P.prof, 0, 64, st));
+  }
+  PTROM_CUDA(cudaMemcpyAsync(P.xp, d_x0, dim * 8, cudaMemcpyDeviceToDevice, st));
+  void* args[] = {&P};
+  PTROM_CUDA(cudaLaunchCooperativeKernel((const void*)fom_persistent_kernel, dim3(grid), dim3(kPTPB), args, 0, st));
+  PTROM_LAUNCH_CHECK();
+  long long cnt[2] = {0, 0};
+  if (n_steps > 0) {
+    PTROM_CUDA(cudaMemcpyAsync(iters, P.iters, n_steps * 4, cudaMemcpyDeviceToHost, st));
+    PTROM_CUDA(cudaMemcpyAsync(conv, P.conv, n_steps, cudaMemcpyDeviceToHost, st));
+    PTROM_CUDA(cudaMemcpyAsync(rel_out, P.rel_out, n_steps * 8, cudaMemcpyDeviceToHost, st));
+    if (!own_snaps)
+      PTROM_CUDA(cudaMemcpyAsync(snapshots_out, P.snaps, dim * n_steps * 8, cudaMemcpyDefault, st));
+  }
+  PTROM_CUDA(cudaMemcpyAsync(cnt, P.counters, 16, cudaMemcpyDeviceToHost, st));
+  unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (prof) PTROM_CUDA(cudaMemcpyAsync(pr, P.prof, 64, cudaMemcpyDeviceToHost, st));
+  PTROM_CUDA(cudaStreamSynchronize(st));
+  if (prof)
+    fprintf(stderr, "fom_persistent grid %d nch %d: vel %.3f ms, sync %.3f, reduce+norm %.3f, jac %.3f, sync %.3f, "
+                    "blocks+update %.3f, sync %.3f, other %.3f\n",
+            grid, P.nch, pr[0] * 1e-6, pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6, pr[4] * 1e-6, pr[5] * 1e-6,
+            pr[6] * 1e-6, pr[7] * 1e-6);
+  check_device_status(ctx);
+  FomResult out;
+  out.velocity_evals = cnt[0];
+  out.jacobian_evals = cnt[1];
+  return out;
+}
+
+}  // namespace ptrom

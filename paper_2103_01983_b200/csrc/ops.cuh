@@ -40,6 +40,14 @@ struct FomResult {
   long long velocity_evals = 0;
   long long jacobian_evals = 0;
 };
+// Small systems (n ≤ 16,384, cooperative launch available, unless
+// PTROM_FOM_PERSISTENT=0): the whole trajectory as one persistent kernel
+// (fom_persistent.cu).
+bool fom_persistent_applies(ptrom_ctx* ctx, long long n);
+FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x0, const double* d_gamma,
+                                  double delta, int form, const double* d_inflow, double dt, long long n_steps,
+                                  double tol, int max_iters, int refresh, double* snapshots_out, int* iters,
+                                  unsigned char* conv, double* rel_out);
 FomResult fom_simulate_device(ptrom_ctx* ctx, long long n, const double* d_x0, const double* d_gamma, double delta,
                               int form, const double* d_inflow, double dt, long long n_steps, double tol,
                               int max_iters, int refresh, double* h_snapshots, int* iters, unsigned char* conv,
