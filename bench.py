@@ -656,7 +656,7 @@ def main():
     w = workloads.config5() if big else workloads.config2()
     line = allpairs_line(args, w, args.steps, args.warmup, rank, world, local,
                          2 if big else max(5, min(args.steps, 50)), args.cpu_seconds, not big,
-                         None if big else "r01_allpairs_vel64_ncu_summary.json")
+                         "r02_allpairs_c5_ncu_summary.json" if big else "r01_allpairs_vel64_ncu_summary.json")
     if rank == 0:
         if big and world == 1 and not args.no_extras:
             line["extra"] = extras(args, local)

@@ -171,7 +171,7 @@ def bench_config3(args, world):
     hbm = _measured_hbm()
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_dfma_tflops"] if peaks else None,
                 "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"] if peaks else None,
-                "traffic": _ncu_traffic("r01_bh_eval_ncu_summary.json"),
+                "traffic": _ncu_traffic("r02_bh_eval_ncu_summary.json"),
                 "kernel": "bh_eval_warp_kernel (csrc/tree_eval.cu)", "avg_launch_ms": eval_ms,
                 "interactions_per_launch": inter, "prune_tests_per_launch": prune,
                 "flops_convention": "12/interaction + 7/prune test (BASELINE.md §2)",
@@ -352,7 +352,7 @@ def bench_config4(args, world):
     hbm = _measured_hbm()
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_dfma_tflops"] if peaks else None,
                 "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"] if peaks else None,
-                "traffic": _ncu_traffic("r01_hyperpair_ncu_summary.json"),
+                "traffic": _ncu_traffic("r02_hyperpair_ncu_summary.json"),
                 "kernel": "hyperpair_kernel (csrc/rom.cu)", "avg_launch_ms": avg_hp_ms, "launches": hp_n,
                 "interactions_per_launch": inter_per_launch,
                 "flops_convention": "25 per fused velocity+Jacobian interaction (BASELINE.md §2)",

@@ -548,7 +548,13 @@ void launch_allpairs_src(ptrom_ctx* ctx, long long n, Src src, const double* gam
   constexpr int NCOMP = (VEL ? 2 : 0) + (JAC ? 3 : 0);
   const long long tiles = (t_count + TPB * T - 1) / (TPB * T);
   // short source ranges (small N) may split into chunks of 32 sources
-  const int chunks = choose_source_chunks(ctx, tiles, n, occ, T <= 2 ? 32 : 2 * TPB);
+  int chunks = choose_source_chunks(ctx, tiles, n, occ, T <= 2 ? 32 : 2 * TPB);
+  // Sources beyond a third of L2 (x, y, Γ: 24 B each): split them into chunks
+  // of ≤ 40 MB. CTAs are scheduled tile-fastest, so the resident waves stream
+  // one chunk at a time and keep it L2-resident instead of re-reading the
+  // whole source set from HBM per wave (config 5: 100 MB of sources).
+  constexpr long long kL2ChunkBytes = 40ll << 20;
+  chunks = (int)std::min<long long>(512, std::max<long long>(chunks, (n * 24 + kL2ChunkBytes - 1) / kL2ChunkBytes));
   const long long chunk_len = (n + chunks - 1) / chunks;
   ctx->scratch.reset();
   ctx->scratch.reserve((size_t)chunks * NCOMP * t_count * sizeof(double) + 4096);
