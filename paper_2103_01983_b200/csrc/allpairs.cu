@@ -693,6 +693,10 @@ void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double
                       const double* inflow, long long t_begin, long long t_end, double* f, long long ld) {
   const long long t_count = t_end - t_begin;
   if (t_count <= 0) return;
+  if (t_begin == 0 && t_count == n && ld == n && sym_velocity_applies(ctx, n)) {  // every target: unordered pairs
+    dev_velocity_sym_f64(ctx, n, x, gamma, delta, form, inflow, f);
+    return;
+  }
   double* part;
   int chunks;
   if ((double)n * (double)t_count > 268435456.0) {  // large: the separate reduction is cheaper than a serial tail

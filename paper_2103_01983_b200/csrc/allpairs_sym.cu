@@ -1,0 +1,355 @@
+// allpairs_sym.cu — the full self-evaluation f = pairwise_velocity(x)
+// (kernel.hpp:107-129, every target against every source) computed once per
+// UNORDERED pair. Pair (i, j) and pair (j, i) share d² (r_ji = −r_ij
+// exactly, so q = d² + δ' has the same bits) and one reciprocal u = 1/q;
+// they differ only in the weight (Γ'_j for target i, Γ'_i for target j) and
+// the sign of r. Per unordered pair the FP64 pipe executes ~12.75 ops
+// against 2 × 9 for the two ordered pairs of allpairs_f64_kernel.
+//
+// Decomposition (fixed-order, deterministic): the particles are cut into nb
+// blocks of B (a multiple of 1,024). A CTA takes one block pair (I, J),
+// I ≤ J, and walks block I in passes of 1,024 targets (128 threads x 8 in
+// registers, with Γ'_i) against block J's sources staged through shared
+// memory in tiles of 128:
+//  * I side: each thread accumulates its 8 targets in registers over the
+//    whole block J and writes part[J][·][i] once;
+//  * J side: within a warp the sources of a 32-source batch rotate over the
+//    lanes (lane l takes source (l + s) mod 32 at sub-step s) and the
+//    per-source accumulator travels with them — after the FMA it moves one
+//    lane down (one shuffle), so after 32 sub-steps lane l holds the warp's
+//    sum for source l with no reduction tree. The 4 warps' sums are added in
+//    warp order and accumulated over the passes into part[I][·][j], which
+//    only this CTA touches.
+//  * diagonal blocks (I = J) are evaluated one-sided (tile_f64, self pair
+//    excluded) — 1/nb of the work.
+// part[K][c][i] is thus written by exactly one CTA for every (K, i), and
+// f_i = Σ_K part[K][·][i] (ascending K) + inflow in a fixed order.
+// The reciprocal tiers are allpairs.cu's: 4-way Montgomery with an fp32 seed
+// and one Newton step on range-guarded tiles, MUFU.RCP64H + cubic correction
+// otherwise (which also propagates q = 0 as inf/NaN for a coincident pair
+// with δ = 0, the reference's throw at kernel.hpp:38-39).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "ops.cuh"
+#include "pair_tile.cuh"
+
+namespace ptrom {
+namespace {
+
+constexpr int kSTPB = 128;                 // threads per CTA
+constexpr int kST = 8;                     // targets per thread
+constexpr int kSPass = kSTPB * kST;        // targets per pass (1,024)
+constexpr long long kSymMinN = 16384;      // below: the one-sided kernels (launch-bound sizes)
+
+__device__ __forceinline__ double rcp_cubic(double q) {
+  const double y0 = rcp_seed(q);
+  double e = fma(-q, y0, 1.0);
+  e = fma(e, e, e);
+  return fma(y0, e, y0);
+}
+
+__device__ __forceinline__ void decode_pair(long long k, int& I, int& J) {
+  int j = (int)((sqrt(8.0 * (double)k + 1.0) - 1.0) * 0.5);
+  while ((long long)(j + 1) * (j + 2) / 2 <= k) ++j;
+  while ((long long)j * (j + 1) / 2 > k) --j;
+  J = j;
+  I = (int)(k - (long long)j * (j + 1) / 2);
+}
+
+// One rotated source against the thread's 8 targets: I-side into (fx, fy),
+// J-side into (wx, wy). Off-diagonal items always have a full target block
+// (only the last block can be ragged and I < J); TAIL: a source beyond n
+// adds exactly 0 to the targets (selected, so its dummy position can never
+// inject inf/NaN), and its own accumulator is never stored.
+template <bool FAST4, bool TAIL>
+__device__ __forceinline__ void sym_pairs(double px, double py, double g, bool vj, const double (&tx)[kST],
+                                          const double (&ty)[kST], const double (&gi)[kST], double dp,
+                                          double (&fx)[kST], double (&fy)[kST], double& wx, double& wy) {
+#pragma unroll
+  for (int k = 0; k < kST; k += 4) {
+    double rx[4], ry[4], q[4], u[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      rx[m] = tx[k + m] - px;
+      ry[m] = ty[k + m] - py;
+      q[m] = fma(rx[m], rx[m], fma(ry[m], ry[m], dp));
+    }
+    if (FAST4) {  // u_m = 1/q_m from one reciprocal of (q0 q1)(q2 q3)
+      const double p01 = q[0] * q[1], p23 = q[2] * q[3];
+      const double P = p01 * p23;
+      const double y0 = rcp_seed_via_f32(P);
+      const double e = fma(-P, y0, 1.0);
+      const double uP = fma(y0, e, y0);
+      const double u01 = uP * p23, u23 = uP * p01;
+      u[0] = u01 * q[1];
+      u[1] = u01 * q[0];
+      u[2] = u23 * q[3];
+      u[3] = u23 * q[2];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) u[m] = rcp_cubic(q[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      double a = g * u[m];                // Γ'_j / q: target i's weight (kernel.hpp:37-41)
+      const double b = gi[k + m] * u[m];  // Γ'_i / q: source j's weight, r_ji = −r_ij
+      if (TAIL) a = vj ? a : 0.0;         // a source beyond n (its own sum is discarded)
+      fx[k + m] = fma(-ry[m], a, fx[k + m]);
+      fy[k + m] = fma(rx[m], a, fy[k + m]);
+      wx = fma(ry[m], b, wx);
+      wy = fma(-rx[m], b, wy);
+    }
+  }
+}
+
+template <bool TAIL>
+__device__ void sym_item(long long n, const double* __restrict__ xs, const double* __restrict__ ys,
+                         const double* __restrict__ gam, double inv2pi, double dp, long long B, int I, int J,
+                         double* __restrict__ part, double2* sp, double* sg, double2 (*sj)[kSTPB]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i_blk = (long long)I * B, j_blk = (long long)J * B;
+  const long long j_end = min(j_blk + B, n);
+  const int passes = (int)((min(i_blk + B, n) - i_blk + kSPass - 1) / kSPass);
+  for (int pass = 0; pass < passes; ++pass) {
+    const long long i0 = i_blk + (long long)pass * kSPass;
+    double tx[kST], ty[kST], gi[kST], fx[kST], fy[kST];
+    bool my_ok4 = true;
+#pragma unroll
+    for (int k = 0; k < kST; ++k) {
+      const long long i = i0 + k * kSTPB + tid;
+      const bool ok = i < n;
+      tx[k] = ok ? xs[i] : 0.0;
+      ty[k] = ok ? ys[i] : 0.0;
+      gi[k] = ok ? gam[i] * inv2pi : 0.0;
+      fx[k] = fy[k] = 0.0;
+      my_ok4 = my_ok4 && coord_ok4(tx[k]) && coord_ok4(ty[k]);
+    }
+    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
+    for (long long t0 = j_blk; t0 < j_end; t0 += kSTPB) {
+      const long long j = t0 + tid;
+      const bool vj = j < n;
+      const double px = vj ? xs[j] : 0.0, py = vj ? ys[j] : 0.0;
+      sp[tid] = make_double2(px, py);
+      sg[tid] = vj ? gam[j] * inv2pi : 0.0;
+      const bool fast4 = __syncthreads_and(coord_ok4(px) && coord_ok4(py)) && targets_ok4;
+      const int cnt = (int)min((long long)kSTPB, j_end - t0);
+      for (int b0 = 0; b0 < kSTPB; b0 += 32) {
+        double wx = 0.0, wy = 0.0;
+        if (b0 < cnt) {  // CTA-uniform
+#pragma unroll 2
+          for (int s = 0; s < 32; ++s) {
+            const int src = b0 + ((lane + s) & 31);
+            const double2 p = sp[src];
+            const double g = sg[src];
+            const bool v = !TAIL || src < cnt;
+            if (fast4)
+              sym_pairs<true, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, fx, fy, wx, wy);
+            else
+              sym_pairs<false, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, fx, fy, wx, wy);
+            // the accumulator follows its source one lane down
+            wx = __shfl_sync(0xffffffffu, wx, (lane + 1) & 31);
+            wy = __shfl_sync(0xffffffffu, wy, (lane + 1) & 31);
+          }
+        }
+        sj[warp][b0 + lane] = make_double2(wx, wy);  // lane holds source b0 + lane
+      }
+      __syncthreads();
+      if (vj) {  // the 4 warps in order, accumulated over the passes
+        double2 acc = sj[0][tid];
+#pragma unroll
+        for (int w = 1; w < kSTPB / 32; ++w) {
+          acc.x += sj[w][tid].x;
+          acc.y += sj[w][tid].y;
+        }
+        double* px_ = part + (long long)I * 2 * n + j;
+        if (pass == 0) {
+          px_[0] = acc.x;
+          px_[n] = acc.y;
+        } else {
+          px_[0] = px_[0] + acc.x;
+          px_[n] = px_[n] + acc.y;
+        }
+      }
+      __syncthreads();
+    }
+    double* out = part + (long long)J * 2 * n;
+#pragma unroll
+    for (int k = 0; k < kST; ++k) {
+      const long long i = i0 + k * kSTPB + tid;
+      if (i < n) {
+        out[i] = fx[k];
+        out[n + i] = fy[k];
+      }
+    }
+  }
+}
+
+// Diagonal block: one-sided, self pair excluded (allpairs_f64_kernel's tile loop).
+__device__ void diag_item(long long n, const double* __restrict__ xs, const double* __restrict__ ys,
+                          const double* __restrict__ gam, double inv2pi, double dp, long long B, int I,
+                          double* __restrict__ part, double2* sp, double* sg) {
+  constexpr int T = kST, TPB = kSTPB;
+  const int tid = threadIdx.x;
+  const long long blk = (long long)I * B, blk_end = min(blk + B, n);
+  const int passes = (int)((blk_end - blk + kSPass - 1) / kSPass);
+  for (int pass = 0; pass < passes; ++pass) {
+    const long long tile0 = blk + (long long)pass * kSPass;
+    double tx[T], ty[T], fx[T], fy[T], ja[T], jb[T], jc[T];
+    long long ti[T];
+    bool my_ok = true, my_ok4 = true;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const long long i = tile0 + k * TPB + tid;
+      const bool ok = i < blk_end;
+      ti[k] = ok ? i : -1;
+      tx[k] = ok ? xs[i] : 0.0;
+      ty[k] = ok ? ys[i] : 0.0;
+      fx[k] = fy[k] = ja[k] = jb[k] = jc[k] = 0.0;
+      my_ok = my_ok && coord_ok(tx[k]) && coord_ok(ty[k]);
+      my_ok4 = my_ok4 && coord_ok4(tx[k]) && coord_ok4(ty[k]);
+    }
+    const long long tile_end = min(tile0 + (long long)kSPass, blk_end);
+    const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62 && dp <= 0x1p60;
+    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
+    for (long long j0 = blk; j0 < blk_end; j0 += TPB) {
+      const int cnt = (int)min((long long)TPB, blk_end - j0);
+      const long long j = j0 + tid;
+      const double px = j < blk_end ? xs[j] : 0.0, py = j < blk_end ? ys[j] : 0.0;
+      sp[tid] = make_double2(px, py);
+      sg[tid] = j < blk_end ? gam[j] * inv2pi : 0.0;
+      const bool fast4 = __syncthreads_and(coord_ok4(px) && coord_ok4(py)) && targets_ok4;
+      const bool fast = fast4 || (__syncthreads_and(coord_ok(px) && coord_ok(py)) && targets_ok);
+      const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt) && !fast;
+      if (masked)
+        tile_f64<T, 2, true, false, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      else if (fast4)
+        tile_f64<T, 2, true, false, false, 4>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      else if (fast)
+        tile_f64<T, 2, true, false, false, 2>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      else
+        tile_f64<T, 2, true, false, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      __syncthreads();
+    }
+    double* out = part + (long long)I * 2 * n;
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+      if (ti[k] >= 0) {
+        out[ti[k]] = fx[k];
+        out[n + ti[k]] = fy[k];
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kSTPB, 2) allpairs_sym_kernel(long long n, const double* __restrict__ xs,
+                                                                const double* __restrict__ ys,
+                                                                const double* __restrict__ gam, double inv2pi,
+                                                                double dp, long long B, double* __restrict__ part) {
+  __shared__ double2 sp[kSTPB];
+  __shared__ double sg[kSTPB];
+  __shared__ double2 sj[kSTPB / 32][kSTPB];
+  int I, J;
+  decode_pair(blockIdx.x, I, J);
+  if (I == J) {
+    diag_item(n, xs, ys, gam, inv2pi, dp, B, I, part, sp, sg);
+    return;
+  }
+  const bool tail = (long long)(J + 1) * B > n;  // only the last block can be ragged (I < J)
+  if (tail)
+    sym_item<true>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, sp, sg, sj);
+  else
+    sym_item<false>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, sp, sg, sj);
+}
+
+// f_i = Σ_K part[K][·][i] in ascending K (fixed order) + inflow.
+__global__ void reduce_sym_kernel(long long n, int nb, const double* __restrict__ part,
+                                  const double* __restrict__ inflow, double* __restrict__ f, DeviceStatus* st) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double sx = 0.0, sy = 0.0;
+    int k = 0;
+    for (; k + 8 <= nb; k += 8) {
+      double vx[8], vy[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        vx[u] = part[(long long)(k + u) * 2 * n + i];
+        vy[u] = part[((long long)(k + u) * 2 + 1) * n + i];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        sx += vx[u];
+        sy += vy[u];
+      }
+    }
+    for (; k < nb; ++k) {
+      sx += part[(long long)k * 2 * n + i];
+      sy += part[((long long)k * 2 + 1) * n + i];
+    }
+    if (inflow) {
+      sx = sx + inflow[i];
+      sy = sy + inflow[i + n];
+    }
+    if (!isfinite(sx) || !isfinite(sy)) latch_status(st, kStatusNonFiniteVelocity, i);
+    f[i] = sx;
+    f[i + n] = sy;
+  }
+}
+
+}  // namespace
+
+bool sym_velocity_applies(ptrom_ctx* ctx, long long n) {
+  if (n < kSymMinN) return false;
+  const char* v = std::getenv("PTROM_ALLPAIRS_SYM");
+  if (v && v[0] == '0') return false;
+  (void)ctx;
+  return true;
+}
+
+// Block size: a multiple of 1,024 whose block pairs fill the resident CTAs
+// in whole waves best, with the partial buffer (nb x 2 x n doubles) ≤ 12 GB.
+static long long choose_sym_block(ptrom_ctx* ctx, long long n, int resident) {
+  long long best = 0;
+  double best_eff = -1.0;
+  for (long long B = kSPass; B <= std::max<long long>(kSPass, n); B *= 2) {
+    const long long nb = (n + B - 1) / B;
+    if ((double)nb * 2.0 * (double)n * 8.0 > 12e9) continue;
+    const long long items = nb * (nb + 1) / 2;
+    const double waves = (double)items / resident;
+    double eff = waves / std::ceil(waves);
+    if (items < 2LL * resident) eff *= (double)items / (2.0 * resident);  // too few items to balance
+    if (eff > best_eff + 0.01) {
+      best_eff = eff;
+      best = B;
+    }
+  }
+  (void)ctx;
+  return best ? best : kSPass;
+}
+
+void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                          const double* inflow, double* f) {
+  static int occ = [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, allpairs_sym_kernel, kSTPB, 0);
+    return std::max(o, 1);
+  }();
+  const long long B = choose_sym_block(ctx, n, ctx->num_sms * occ);
+  const long long nb = (n + B - 1) / B;
+  const long long items = nb * (nb + 1) / 2;
+  ctx->scratch.reset();
+  ctx->scratch.reserve((size_t)nb * 2 * n * sizeof(double) + 4096);
+  double* part = ctx->scratch.take<double>((size_t)nb * 2 * n);
+  const double inv2pi = 1.0 / (2.0 * M_PI);
+  {
+    ProfScope prof(ctx);
+    allpairs_sym_kernel<<<(unsigned)items, kSTPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi,
+                                                                     effective_delta(delta, form), B, part);
+  }
+  PTROM_LAUNCH_CHECK();
+  const long long rg = std::min<long long>((n + 255) / 256, (long long)ctx->num_sms * 8);
+  reduce_sym_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(n, (int)nb, part, inflow, f,
+                                                                                  ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
+}  // namespace ptrom

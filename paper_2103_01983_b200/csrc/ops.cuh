@@ -13,6 +13,11 @@ template <class S>
 void validate_uploaded(ptrom_ctx* ctx, long long n, const S* dx, const S* dg, S delta, const S* di, const char* who);
 void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
                       const double* inflow, long long t_begin, long long t_end, double* f, long long ld);
+// Full self-evaluation (every target, every source) over unordered pairs
+// (allpairs_sym.cu); applies for n ≥ 16,384 unless PTROM_ALLPAIRS_SYM=0.
+bool sym_velocity_applies(ptrom_ctx* ctx, long long n);
+void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                          const double* inflow, double* f);
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
                       const float* inflow, long long t_begin, long long t_end, float* f, long long ld);
 // jxx..jyy (may be null when inv is given) or the Newton-block inverse of

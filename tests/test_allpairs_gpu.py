@@ -257,3 +257,43 @@ def test_device_validation_order_and_messages(pt):
     assert rc != 0 and "pairwise_velocity: non-finite state" in msg
     rc, msg = call(x, g, 0.1, inf_)
     assert rc == 0, msg
+
+
+@pytest.mark.parametrize("n,scale,delta,form,inflow", [(16384, 1.0, 2.5e-5, 0, False), (20037, 1.0, 0.3, 1, True),
+                                                       (40000, 2.0 ** 15, 1e3, 0, False), (33000, 1.0, 0.0, 0, True),
+                                                       (65536, 0.25, 2.5e-5, 0, False)])
+def test_unordered_pair_kernel_matches_one_sided_and_oracle(pt, oracle, monkeypatch, n, scale, delta, form, inflow):
+    """Full self-evaluations (n ≥ 16,384) run over unordered pairs
+    (allpairs_sym.cu: one reciprocal per pair (i, j) for both directions,
+    rotating per-source accumulators, fixed-order block partials). Against the
+    one-sided kernel (PTROM_ALLPAIRS_SYM=0) and the oracle, ragged blocks,
+    inflow, both forms, the safe tier (|x| ≥ 2^14) and δ = 0; run to run
+    bit-identical."""
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-1.0, 1.0, 2 * n) * scale
+    g = rng.normal(0.0, 1.0, n) / n
+    infl = rng.uniform(-1, 1, 2 * n) if inflow else None
+    sys_ = pt.ParticleSystem(g, delta, infl, form)
+    f = pt.pairwise_velocity(x, sys_)
+    f2 = pt.pairwise_velocity(x, sys_)
+    assert np.array_equal(f, f2)
+    monkeypatch.setenv("PTROM_ALLPAIRS_SYM", "0")
+    one_sided = pt.pairwise_velocity(x, sys_)
+    monkeypatch.delenv("PTROM_ALLPAIRS_SYM")
+    assert rel(f, one_sided) <= FP64_TOL
+    rows_b = [0, n // 2, n - 700]
+    for b in rows_b:
+        ref = oracle.pairwise_velocity(x, g, delta, form, infl, t_begin=b, t_end=b + 700, threads=THREADS)
+        rows = np.r_[b:b + 700, n + b:n + b + 700]
+        assert rel(f[rows], ref[rows]) <= FP64_TOL, b
+
+
+def test_unordered_pair_kernel_flags_coincident_pair(pt):
+    """δ = 0 and two coincident particles: the reference throws
+    (kernel.hpp:38-39); the unordered-pair kernel must report it too."""
+    n = 20000
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, 2 * n)
+    x[17], x[n + 17] = x[15000], x[n + 15000]
+    with pytest.raises(pt.NumericalError):
+        pt.pairwise_velocity(x, pt.ParticleSystem(np.ones(n), 0.0))
