@@ -32,6 +32,7 @@
 #include <cmath>
 #include <cstdlib>
 
+#include "comm.cuh"
 #include "ops.cuh"
 #include "pair_tile.cuh"
 
@@ -107,7 +108,7 @@ __device__ __forceinline__ void sym_pairs(double px, double py, double g, bool v
 template <bool TAIL>
 __device__ void sym_item(long long n, const double* __restrict__ xs, const double* __restrict__ ys,
                          const double* __restrict__ gam, double inv2pi, double dp, long long B, int I, int J,
-                         double* __restrict__ part, double2* sp, double* sg, double2 (*sj)[kSTPB]) {
+                         double* __restrict__ part, long long ps, double2* sp, double* sg, double2 (*sj)[kSTPB]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long i_blk = (long long)I * B, j_blk = (long long)J * B;
   const long long j_end = min(j_blk + B, n);
@@ -169,24 +170,24 @@ __device__ void sym_item(long long n, const double* __restrict__ xs, const doubl
           acc.x += sj[w][tid].x;
           acc.y += sj[w][tid].y;
         }
-        double* px_ = part + (long long)I * 2 * n + j;
+        double* px_ = part + (long long)I * 2 * ps + j;
         if (pass == 0) {
           px_[0] = acc.x;
-          px_[n] = acc.y;
+          px_[ps] = acc.y;
         } else {
           px_[0] = px_[0] + acc.x;
-          px_[n] = px_[n] + acc.y;
+          px_[ps] = px_[ps] + acc.y;
         }
       }
       __syncthreads();
     }
-    double* out = part + (long long)J * 2 * n;
+    double* out = part + (long long)J * 2 * ps;
 #pragma unroll
     for (int k = 0; k < kST; ++k) {
       const long long i = i0 + k * kSTPB + tid;
       if (i < n) {
         out[i] = fx[k];
-        out[n + i] = fy[k];
+        out[ps + i] = fy[k];
       }
     }
   }
@@ -195,7 +196,7 @@ __device__ void sym_item(long long n, const double* __restrict__ xs, const doubl
 // Diagonal block: one-sided, self pair excluded (allpairs_f64_kernel's tile loop).
 __device__ void diag_item(long long n, const double* __restrict__ xs, const double* __restrict__ ys,
                           const double* __restrict__ gam, double inv2pi, double dp, long long B, int I,
-                          double* __restrict__ part, double2* sp, double* sg) {
+                          double* __restrict__ part, long long ps, double2* sp, double* sg) {
   constexpr int T = kST, TPB = kSTPB;
   const int tid = threadIdx.x;
   const long long blk = (long long)I * B, blk_end = min(blk + B, n);
@@ -238,48 +239,55 @@ __device__ void diag_item(long long n, const double* __restrict__ xs, const doub
         tile_f64<T, 2, true, false, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
       __syncthreads();
     }
-    double* out = part + (long long)I * 2 * n;
+    double* out = part + (long long)I * 2 * ps;
 #pragma unroll
     for (int k = 0; k < T; ++k)
       if (ti[k] >= 0) {
         out[ti[k]] = fx[k];
-        out[n + ti[k]] = fy[k];
+        out[ps + ti[k]] = fy[k];
       }
   }
 }
 
+// part rows have stride ps (≥ n); the grid covers items [k0, k0 + gridDim.x)
+// of the nb(nb+1)/2 block pairs (a rank's share in the sharded evaluation).
 __global__ void __launch_bounds__(kSTPB, 4) allpairs_sym_kernel(long long n, const double* __restrict__ xs,
                                                                 const double* __restrict__ ys,
                                                                 const double* __restrict__ gam, double inv2pi,
-                                                                double dp, long long B, double* __restrict__ part) {
+                                                                double dp, long long B, double* __restrict__ part,
+                                                                long long ps, long long k0) {
   __shared__ double2 sp[2 * kSTPB];  // sym items: each batch twice; diagonal items: the first kSTPB
   __shared__ double sg[2 * kSTPB];
   __shared__ double2 sj[kSTPB / 32][kSTPB];
   int I, J;
-  decode_pair(blockIdx.x, I, J);
+  decode_pair(k0 + blockIdx.x, I, J);
   if (I == J) {
-    diag_item(n, xs, ys, gam, inv2pi, dp, B, I, part, sp, sg);
+    diag_item(n, xs, ys, gam, inv2pi, dp, B, I, part, ps, sp, sg);
     return;
   }
   const bool tail = (long long)(J + 1) * B > n;  // only the last block can be ragged (I < J)
   if (tail)
-    sym_item<true>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, sp, sg, sj);
+    sym_item<true>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, ps, sp, sg, sj);
   else
-    sym_item<false>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, sp, sg, sj);
+    sym_item<false>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, ps, sp, sg, sj);
 }
 
-// f_i = Σ_K part[K][·][i] in ascending K (fixed order) + inflow.
-__global__ void reduce_sym_kernel(long long n, int nb, const double* __restrict__ part,
-                                  const double* __restrict__ inflow, double* __restrict__ f, DeviceStatus* st) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+// f_i = Σ_K part[K][·][i] in ascending K (fixed order) + inflow, for the
+// rows [r0, r0 + m) of part (row stride ps) → f (ld m); target ids t0 + row.
+__global__ void reduce_sym_kernel(long long n, int nb, const double* __restrict__ part, long long ps, long long r0,
+                                  long long m, long long t0, const double* __restrict__ inflow,
+                                  double* __restrict__ f, DeviceStatus* st) {
+  for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < m;
+       li += (long long)gridDim.x * blockDim.x) {
+    const long long r = r0 + li;
     double sx = 0.0, sy = 0.0;
     int k = 0;
     for (; k + 8 <= nb; k += 8) {
       double vx[8], vy[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        vx[u] = part[(long long)(k + u) * 2 * n + i];
-        vy[u] = part[((long long)(k + u) * 2 + 1) * n + i];
+        vx[u] = part[(long long)(k + u) * 2 * ps + r];
+        vy[u] = part[((long long)(k + u) * 2 + 1) * ps + r];
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -288,16 +296,17 @@ __global__ void reduce_sym_kernel(long long n, int nb, const double* __restrict_
       }
     }
     for (; k < nb; ++k) {
-      sx += part[(long long)k * 2 * n + i];
-      sy += part[((long long)k * 2 + 1) * n + i];
+      sx += part[(long long)k * 2 * ps + r];
+      sy += part[((long long)k * 2 + 1) * ps + r];
     }
+    const long long i = t0 + li;
     if (inflow) {
       sx = sx + inflow[i];
       sy = sy + inflow[i + n];
     }
     if (!isfinite(sx) || !isfinite(sy)) latch_status(st, kStatusNonFiniteVelocity, i);
-    f[i] = sx;
-    f[i + n] = sy;
+    f[li] = sx;
+    f[li + m] = sy;
   }
 }
 
@@ -311,50 +320,90 @@ bool sym_velocity_applies(ptrom_ctx* ctx, long long n) {
   return true;
 }
 
-// Block size: a multiple of 1,024 whose block pairs fill the resident CTAs
-// in whole waves best, with the partial buffer (nb x 2 x n doubles) ≤ 12 GB.
-static long long choose_sym_block(ptrom_ctx* ctx, long long n, int resident) {
+// Block size: a multiple of 1,024 whose block pairs (split over `world`
+// ranks) fill the resident CTAs in whole waves best, with the partial buffer
+// (nb x 2 x n doubles) ≤ 12 GB (24 GB when sharded).
+static long long choose_sym_block(long long n, int resident, int world) {
   long long best = 0;
   double best_eff = -1.0;
+  const double cap = world > 1 ? 24e9 : 12e9;
   for (long long B = kSPass; B <= std::max<long long>(kSPass, n); B *= 2) {
     const long long nb = (n + B - 1) / B;
-    if ((double)nb * 2.0 * (double)n * 8.0 > 12e9) continue;
-    const long long items = nb * (nb + 1) / 2;
-    const double waves = (double)items / resident;
+    if ((double)nb * 2.0 * (double)n * 8.0 > cap) continue;
+    const double items = (double)(nb * (nb + 1) / 2) / world;
+    const double waves = items / resident;
     double eff = waves / std::ceil(waves);
-    if (items < 2LL * resident) eff *= (double)items / (2.0 * resident);  // too few items to balance
+    if (items < 2.0 * resident) eff *= items / (2.0 * resident);  // too few items to balance
     if (eff > best_eff + 0.01) {
       best_eff = eff;
       best = B;
     }
   }
-  (void)ctx;
   return best ? best : kSPass;
 }
 
-void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
-                          const double* inflow, double* f) {
+static int sym_occupancy() {
   static int occ = [] {
     int o = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, allpairs_sym_kernel, kSTPB, 0);
     return std::max(o, 1);
   }();
-  const long long B = choose_sym_block(ctx, n, ctx->num_sms * occ);
+  return occ;
+}
+
+static void launch_sym_items(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
+                             long long B, double* part, long long ps, long long k0, long long count) {
+  if (count <= 0) return;
+  ProfScope prof(ctx);
+  allpairs_sym_kernel<<<(unsigned)count, kSTPB, 0, ctx->stream>>>(n, x, x + n, gamma, 1.0 / (2.0 * M_PI), dp, B, part,
+                                                                   ps, k0);
+}
+
+void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
+                          const double* inflow, double* f) {
+  const long long B = choose_sym_block(n, ctx->num_sms * sym_occupancy(), 1);
   const long long nb = (n + B - 1) / B;
   const long long items = nb * (nb + 1) / 2;
   ctx->scratch.reset();
   ctx->scratch.reserve((size_t)nb * 2 * n * sizeof(double) + 4096);
   double* part = ctx->scratch.take<double>((size_t)nb * 2 * n);
-  const double inv2pi = 1.0 / (2.0 * M_PI);
-  {
-    ProfScope prof(ctx);
-    allpairs_sym_kernel<<<(unsigned)items, kSTPB, 0, ctx->stream>>>(n, x, x + n, gamma, inv2pi,
-                                                                     effective_delta(delta, form), B, part);
-  }
+  launch_sym_items(ctx, n, x, gamma, effective_delta(delta, form), B, part, n, 0, items);
   PTROM_LAUNCH_CHECK();
   const long long rg = std::min<long long>((n + 255) / 256, (long long)ctx->num_sms * 8);
-  reduce_sym_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(n, (int)nb, part, inflow, f,
-                                                                                  ctx->d_status);
+  reduce_sym_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(n, (int)nb, part, n, 0, n, 0,
+                                                                                  inflow, f, ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
+bool sym_sharded_applies(ptrom_ctx* ctx, long long n, int world) {
+  return world > 1 && n % world == 0 && sym_velocity_applies(ctx, n);
+}
+
+// Target-sharded full evaluation over unordered pairs: every rank holds all
+// positions (x_full), computes its contiguous share of the block pairs into a
+// zeroed partial buffer, and one reduce-scatter (row by row) hands each rank
+// the partial rows of its own targets — every element has exactly one
+// non-zero contributor, so the sum is exact and the result is bit-identical
+// to the single-GPU evaluation; then the same fixed-order reduction.
+void dev_velocity_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
+                                  const double* gamma, double delta, int form, const double* inflow, double* f_local) {
+  const int G = comm->world;
+  const long long B = choose_sym_block(n, ctx->num_sms * sym_occupancy(), G);
+  const long long nb = (n + B - 1) / B;
+  const long long items = nb * (nb + 1) / 2;
+  const long long m = n / G;
+  ctx->scratch.reset();
+  ctx->scratch.reserve(((size_t)nb * 2 * n + (size_t)nb * 2 * m) * sizeof(double) + 8192);
+  double* part = ctx->scratch.take<double>((size_t)nb * 2 * n);
+  double* mine = ctx->scratch.take<double>((size_t)nb * 2 * m);
+  PTROM_CUDA(cudaMemsetAsync(part, 0, (size_t)nb * 2 * n * sizeof(double), ctx->stream));
+  const long long k_lo = items * comm->rank / G, k_hi = items * (comm->rank + 1) / G;
+  launch_sym_items(ctx, n, x_full, gamma, effective_delta(delta, form), B, part, n, k_lo, k_hi - k_lo);
+  PTROM_LAUNCH_CHECK();
+  comm_reduce_scatter_rows(ctx, comm, part, 2 * nb, n, mine);
+  const long long rg = std::min<long long>((m + 255) / 256, (long long)ctx->num_sms * 8);
+  reduce_sym_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(
+      n, (int)nb, mine, m, 0, m, (long long)comm->rank * m, inflow, f_local, ctx->d_status);
   PTROM_LAUNCH_CHECK();
 }
 

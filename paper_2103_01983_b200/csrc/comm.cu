@@ -25,6 +25,7 @@ struct NcclApi {
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
   decltype(&ncclBroadcast) broadcast = nullptr;
   decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclReduceScatter) reduce_scatter = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
@@ -46,10 +47,12 @@ const NcclApi& nccl() {
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
     api.broadcast = reinterpret_cast<decltype(api.broadcast)>(sym("ncclBroadcast"));
     api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
+    api.reduce_scatter = reinterpret_cast<decltype(api.reduce_scatter)>(sym("ncclReduceScatter"));
     api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
     api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
     api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.broadcast && api.all_gather &&
+             api.reduce_scatter &&
              api.group_start && api.group_end && api.error_string;
     if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
   });
@@ -95,6 +98,38 @@ void comm_allgatherv(ptrom_ctx* ctx, ptrom_comm* c, void* d_buf, const std::vect
     if (r != c->rank && cnt[r])
       PTROM_CUDA(cudaMemcpyAsync(b + off[r], recv.data() + (size_t)r * mx, cnt[r], cudaMemcpyHostToDevice,
                                  ctx->stream));
+  PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void comm_reduce_scatter_rows(ptrom_ctx* ctx, ptrom_comm* c, const double* d_in, long long rows, long long row_len,
+                              double* d_out) {
+  const long long chunk = row_len / c->world;
+  if (c->world == 1) {
+    PTROM_CUDA(cudaMemcpyAsync(d_out, d_in, (size_t)rows * row_len * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
+  if (c->nccl) {
+    const NcclApi& api = nccl();
+    nccl_check(api.group_start(), "ncclGroupStart");
+    for (long long r = 0; r < rows; ++r)
+      nccl_check(api.reduce_scatter(d_in + r * row_len, d_out + r * chunk, (size_t)chunk, ncclFloat64, ncclSum,
+                                    as_nccl(c), ctx->stream),
+                 "ncclReduceScatter");
+    nccl_check(api.group_end(), "ncclGroupEnd");
+    return;
+  }
+  // host transport: gather every rank's rows, sum the own chunk in rank order
+  const size_t bytes = (size_t)rows * row_len * 8;
+  std::vector<double> mine((size_t)rows * row_len), all((size_t)rows * row_len * c->world);
+  PTROM_CUDA(cudaMemcpyAsync(mine.data(), d_in, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
+  host_check(c->ops.all_gather(c->user, mine.data(), all.data(), bytes), "all_gather");
+  std::vector<double> out((size_t)rows * chunk, 0.0);
+  for (int q = 0; q < c->world; ++q)
+    for (long long r = 0; r < rows; ++r)
+      for (long long k = 0; k < chunk; ++k)
+        out[r * chunk + k] += all[(size_t)q * rows * row_len + r * row_len + c->rank * chunk + k];
+  PTROM_CUDA(cudaMemcpyAsync(d_out, out.data(), out.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
   PTROM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -301,7 +336,10 @@ int ptrom_dev_pairwise_velocity_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, in
       PTROM_CUDA(cudaMemcpyAsync(d_x_full + n + lo, d_x_local + m, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     exchange_positions(ctx, comm, n, d_x_full);
-    dev_velocity_f64(ctx, n, d_x_full, d_gamma, delta, form, d_inflow, lo, hi, d_f_local, m);
+    if (sym_sharded_applies(ctx, n, comm->world))  // unordered pairs + one reduce-scatter
+      dev_velocity_sym_sharded_f64(ctx, comm, n, d_x_full, d_gamma, delta, form, d_inflow, d_f_local);
+    else
+      dev_velocity_f64(ctx, n, d_x_full, d_gamma, delta, form, d_inflow, lo, hi, d_f_local, m);
   });
 }
 
@@ -351,8 +389,12 @@ int ptrom_fom_simulate_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int64_t n, 
       PTROM_CUDA(cudaMemcpyAsync(x_prev + m, x_full + n + lo, m * 8, cudaMemcpyDeviceToDevice, st));
     }
     long long evals = 0;
+    const bool sym = sym_sharded_applies(ctx, n, comm->world);
     auto velocity = [&](double* f_out) {  // f = velocity(x_full) on the local rows (integrators.hpp:257-259)
-      dev_velocity_f64(ctx, n, x_full, g, delta, form, inf, lo, hi, f_out, m);
+      if (sym)
+        dev_velocity_sym_sharded_f64(ctx, comm, n, x_full, g, delta, form, inf, f_out);
+      else
+        dev_velocity_f64(ctx, n, x_full, g, delta, form, inf, lo, hi, f_out, m);
       ++evals;
     };
     auto global_norm = [&]() -> double {  // partials all-gathered, summed in rank order

@@ -41,6 +41,12 @@ void comm_bcast_many(ptrom_ctx* ctx, ptrom_comm* c, const std::vector<std::pair<
 // Host buffer broadcast / rank-ordered all-gather (synchronous).
 void comm_bcast_host(ptrom_ctx* ctx, ptrom_comm* c, void* h_buf, size_t bytes, int root);
 void comm_allgather_host(ptrom_ctx* ctx, ptrom_comm* c, const void* h_send, void* h_recv, size_t bytes);
+// `rows` rows of row_len doubles (row_len divisible by world): rank r gets,
+// for every row, the element-wise sum over the ranks of the row's r-th
+// chunk (row_len / world doubles) in d_out[row][·]. Used where every element
+// has at most one non-zero contributor, so the sum is exact.
+void comm_reduce_scatter_rows(ptrom_ctx* ctx, ptrom_comm* c, const double* d_in, long long rows, long long row_len,
+                              double* d_out);
 // Waits for the context stream (and, for NCCL, the communicator's work on it).
 void comm_sync(ptrom_ctx* ctx, ptrom_comm* c);
 

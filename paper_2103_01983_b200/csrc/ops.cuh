@@ -18,6 +18,12 @@ void dev_velocity_f64(ptrom_ctx* ctx, long long n, const double* x, const double
 bool sym_velocity_applies(ptrom_ctx* ctx, long long n);
 void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double delta, int form,
                           const double* inflow, double* f);
+// The same split over a communicator (n divisible by the world size): rank r
+// gets rows [r·n/G, (r+1)·n/G) of f (ld n/G), bit-identical to the single-GPU
+// evaluation (allpairs_sym.cu).
+bool sym_sharded_applies(ptrom_ctx* ctx, long long n, int world);
+void dev_velocity_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
+                                  const double* gamma, double delta, int form, const double* inflow, double* f_local);
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
                       const float* inflow, long long t_begin, long long t_end, float* f, long long ld);
 // jxx..jyy (may be null when inv is given) or the Newton-block inverse of

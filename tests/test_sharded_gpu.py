@@ -216,3 +216,55 @@ def test_host_transport_ptrom_batch_sharded(pt, oracle, world, root):
         xo, it_o, _ = oracle.ptrom_simulate(oracle.Surrogate(w.phi, w.sv, w.x0, g1, ids, 1, 1.0, 1), w.phi, w.sv,
                                             w.x0, ids, A, w.gamma_a + m * w.gamma_b, w.delta, w.dt, 4, 1e-300, 5)
         assert max(rel(parts[0][0][i, s], xo[:, s]) for s in range(4)) <= 1e-12
+
+
+def _sym_velocity_worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2103_01983_b200.comm import Comm
+        rng = np.random.default_rng(n)
+        x = rng.uniform(-1, 1, 2 * n)
+        g = rng.normal(0, 1, n) / n
+        inflow = rng.uniform(-1, 1, 2 * n)
+        comm = Comm.host()
+        ctx = comm.ctx
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        lo, hi = comm.bounds(n)
+        m = hi - lo
+        xd = torch.tensor(x, device="cuda")
+        x_local = torch.cat([xd[lo:hi], xd[n + lo:n + hi]]).contiguous()
+        x_ws = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        gd = torch.tensor(g, device="cuda")
+        infd = torch.tensor(inflow, device="cuda")
+        f = torch.empty(2 * m, dtype=torch.float64, device="cuda")
+        ctx.check(ctx.lib.ptrom_dev_pairwise_velocity_sharded_f64(ctx.handle, comm.handle, n, x_local.data_ptr(),
+                                                                  x_ws.data_ptr(), gd.data_ptr(), 2.5e-5, 0,
+                                                                  infd.data_ptr(), f.data_ptr()))
+        ctx.check(ctx.lib.ptrom_synchronize(ctx.handle))
+        parts = [None] * world
+        dist.all_gather_object(parts, (lo, hi, f.cpu().numpy()))
+        comm.close()
+        if rank == 0:
+            q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 20480), (3, 20481)])
+def test_host_transport_unordered_pair_sharded_velocity_bitwise(pt, world, n):
+    """Sharded full evaluation over unordered pairs (allpairs_sym.cu): each
+    rank computes its share of the block pairs, one reduce-scatter of the
+    partial rows (a single non-zero contributor per element: exact) and the
+    same fixed-order reduction — bit-identical to the single-GPU call."""
+    parts = _spawn(_sym_velocity_worker, world, (n,))
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-1, 1, 2 * n)
+    g = rng.normal(0, 1, n) / n
+    inflow = rng.uniform(-1, 1, 2 * n)
+    single = pt.pairwise_velocity(x, pt.ParticleSystem(g, 2.5e-5, inflow))
+    for lo, hi, f in parts:
+        m = hi - lo
+        assert np.array_equal(f[:m], single[lo:hi]) and np.array_equal(f[m:], single[n + lo:n + hi])
