@@ -108,14 +108,16 @@ void comm_reduce_scatter_rows(ptrom_ctx* ctx, ptrom_comm* c, const double* d_in,
     PTROM_CUDA(cudaMemcpyAsync(d_out, d_in, (size_t)rows * row_len * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     return;
   }
-  if (c->nccl) {
+  if (c->nccl) {  // grouped, at most 64 collectives per group
     const NcclApi& api = nccl();
-    nccl_check(api.group_start(), "ncclGroupStart");
-    for (long long r = 0; r < rows; ++r)
-      nccl_check(api.reduce_scatter(d_in + r * row_len, d_out + r * chunk, (size_t)chunk, ncclFloat64, ncclSum,
-                                    as_nccl(c), ctx->stream),
-                 "ncclReduceScatter");
-    nccl_check(api.group_end(), "ncclGroupEnd");
+    for (long long r0 = 0; r0 < rows; r0 += 64) {
+      nccl_check(api.group_start(), "ncclGroupStart");
+      for (long long r = r0; r < std::min(rows, r0 + 64); ++r)
+        nccl_check(api.reduce_scatter(d_in + r * row_len, d_out + r * chunk, (size_t)chunk, ncclFloat64, ncclSum,
+                                      as_nccl(c), ctx->stream),
+                   "ncclReduceScatter");
+      nccl_check(api.group_end(), "ncclGroupEnd");
+    }
     return;
   }
   // host transport: gather every rank's rows, sum the own chunk in rank order
