@@ -370,7 +370,9 @@ def allpairs_line(args, w, K, W, rank, world, local, e2e_steps, cpu_seconds, wit
                     "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_dfma_tflops"],
                     "traffic": ncu_traffic(traffic_file) if traffic_file else None,
                     "algorithmic_bytes_per_launch": 24 * n,
-                    "kernel": "allpairs_f64_kernel<128,8,2,1,vel> (csrc/allpairs.cu)",
+                    "kernel": ("allpairs_sym_kernel (csrc/allpairs_sym.cu: unordered pairs, one reciprocal per pair "
+                               "for both directions)" if n >= 16384 and (world == 1 or n % world == 0)
+                               else "allpairs_f64_kernel<128,8,2,1,vel> (csrc/allpairs.cu)"),
                     "peak_source": "measured live: tools/peaks.cu DFMA chain (MEASURED_PEAKS.json has no FP64)",
                     "flops_per_pair": FLOPS_PER_PAIR, "pairs_per_launch": local_pairs,
                     "avg_launch_ms": avg_kernel_s * 1e3, "launches": kern_launches.value,
@@ -558,7 +560,7 @@ def extras(args, local):
 
     guard("config1", lambda: config1_line(small, 10, 3, local, small.cpu_seconds))
     guard("config2", lambda: allpairs_line(small, workloads.config2(), 20, 3, 0, 1, local, 10,
-                                           small.cpu_seconds, True, "r01_allpairs_vel64_ncu_summary.json"))
+                                           small.cpu_seconds, True, "r02_allpairs_sym_c2_ncu_summary.json"))
 
     def c3():
         a = copy.copy(small)
@@ -660,7 +662,7 @@ def main():
     w = workloads.config5() if big else workloads.config2()
     line = allpairs_line(args, w, args.steps, args.warmup, rank, world, local,
                          2 if big else max(5, min(args.steps, 50)), args.cpu_seconds, not big,
-                         "r02_allpairs_c5_ncu_summary.json" if big else "r01_allpairs_vel64_ncu_summary.json")
+                         "r02_allpairs_sym_c5_ncu_summary.json" if big else "r02_allpairs_sym_c2_ncu_summary.json")
     if rank == 0:
         if big and world == 1 and not args.no_extras:
             line["extra"] = extras(args, local)
