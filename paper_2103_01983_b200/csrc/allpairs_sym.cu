@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "comm.cuh"
 #include "ops.cuh"
@@ -146,19 +147,25 @@ __device__ void sym_item(long long n, const double* __restrict__ xs, const doubl
         if (b0 < cnt) {  // CTA-uniform
           const double2* bp = sp + 2 * b0 + lane;
           const double* bg = sg + 2 * b0 + lane;
+          const int nxt = (lane + 1) & 31;
+          // the tier is uniform over the tile: one loop per tier, no branch per sub-step
+          auto batch = [&](auto fast_tag) {
+            constexpr bool F = decltype(fast_tag)::value;
 #pragma unroll 4
-          for (int s = 0; s < 32; ++s) {
-            const double2 p = bp[s];
-            const double g = bg[s];
-            const bool v = !TAIL || b0 + ((lane + s) & 31) < cnt;
-            if (fast4)
-              sym_pairs<true, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, fx, fy, wx, wy);
-            else
-              sym_pairs<false, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, fx, fy, wx, wy);
-            // the accumulator follows its source one lane down
-            wx = __shfl_sync(0xffffffffu, wx, (lane + 1) & 31);
-            wy = __shfl_sync(0xffffffffu, wy, (lane + 1) & 31);
-          }
+            for (int s = 0; s < 32; ++s) {
+              const double2 p = bp[s];
+              const double g = bg[s];
+              const bool v = !TAIL || b0 + ((lane + s) & 31) < cnt;
+              sym_pairs<F, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, fx, fy, wx, wy);
+              // the accumulator follows its source one lane down
+              wx = __shfl_sync(0xffffffffu, wx, nxt);
+              wy = __shfl_sync(0xffffffffu, wy, nxt);
+            }
+          };
+          if (fast4)
+            batch(std::true_type{});
+          else
+            batch(std::false_type{});
         }
         sj[warp][b0 + lane] = make_double2(wx, wy);  // lane holds source b0 + lane
       }
