@@ -151,7 +151,7 @@ __device__ void sym_item(long long n, const double* __restrict__ xs, const doubl
           // the tier is uniform over the tile: one loop per tier, no branch per sub-step
           auto batch = [&](auto fast_tag) {
             constexpr bool F = decltype(fast_tag)::value;
-#pragma unroll 4
+#pragma unroll 16
             for (int s = 0; s < 32; ++s) {
               const double2 p = bp[s];
               const double g = bg[s];
