@@ -159,3 +159,15 @@ def test_persistent_kernel_equals_graph_path(pt, oracle, n, steps, refresh, monk
     assert max(rel(persistent.snapshots[:, s], graph.snapshots[:, s]) for s in range(steps)) <= 1e-12
     snaps, iters, _, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps, refresh=refresh, threads=THREADS)
     assert max(rel(persistent.snapshots[:, s], snaps[:, s]) for s in range(steps)) <= 1e-12
+
+
+def test_graph_path_with_unordered_pair_velocity(pt, oracle):
+    """Above the persistent kernel's size the CUDA-graph FOM runs its velocity
+    evaluations through the unordered-pair kernel (allpairs_sym.cu, scratch
+    sized before the capture): 3 steps at N = 20,000 against the oracle."""
+    w = workloads.config1(n=20000, seed=9)
+    steps = 3
+    run = pt.fom_simulate(w.x0, pt.ParticleSystem(w.gamma, w.delta), pt.TimeGrid(w.dt, steps))
+    snaps, iters, _, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps, threads=THREADS)
+    assert max(rel(run.snapshots[:, s], snaps[:, s]) for s in range(steps)) <= 1e-12
+    assert int(np.sum(np.asarray(run.iterations) != iters)) <= 1
