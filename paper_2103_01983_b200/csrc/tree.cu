@@ -1016,6 +1016,7 @@ constexpr int kThreadChain = 256;  // chains of nodes up to this size run in one
 struct MortonState {
   int lvl_cnt[kMaxDepth + 2];  // records per level of the large-node pass (level 0 = root)
   int overflow;                // split needed below the key's levels / capacity exceeded
+  int overflow_depth;          // ... because of the key's levels (a 32-level key may fix it)
   int finite;                  // hull finite
   int levels_used;
   int large_count, sub_count;
@@ -1175,7 +1176,10 @@ __global__ void __launch_bounds__(kThreads) morton_levels_kernel(const unsigned 
       }
       if (lane == 0) large_list[atomicAdd(&st->large_count, 1)] = r;
       if (d >= levels) {  // a large node always splits (count > seq_max >= leaf_capacity)
-        if (lane == 0) st->overflow = 1;
+        if (lane == 0) {
+          st->overflow = 1;
+          st->overflow_depth = 1;
+        }
         continue;
       }
       const int g = lane < 11 ? 0 : (lane < 22 ? 1 : 2);
@@ -1345,6 +1349,7 @@ __global__ void __launch_bounds__(kSubThreads, 2) morton_subtree_kernel(
         const int d = d0 + S.ldep[j];
         if (d >= levels) {
           S.ovf = 1;
+          st->overflow_depth = 1;
           continue;
         }
         const int shift = 2 * (levels - 1 - d);
@@ -1659,7 +1664,7 @@ __global__ void __launch_bounds__(1024) morton_large_kernel(TreeRecords rec, con
 
 // Returns false (nothing built) when the Morton path does not apply or
 // overflowed; the caller then runs the level build.
-bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels);
+int tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels);
 bool tree_build_morton(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max) {
   const long long n = t.n;
   // leaf_capacity < 4 gives subtrees with more local nodes than a CTA holds
@@ -1670,11 +1675,15 @@ bool tree_build_morton(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max)
   int lg4 = 0;
   while (lg4 < kMortonLevels && (1LL << (2 * lg4)) * leaf_cap < n) ++lg4;
   const int levels = std::min(kMortonLevels, std::max(8, lg4 + 8));
-  return tree_build_morton_levels(ctx, t, leaf_cap, seq_max, levels) ||
-         (levels < kMortonLevels && tree_build_morton_levels(ctx, t, leaf_cap, seq_max, kMortonLevels));
+  const int r = tree_build_morton_levels(ctx, t, leaf_cap, seq_max, levels);
+  if (r == 0) return true;
+  // only a key-depth overflow can be fixed by more levels; a capacity
+  // overflow (subtree nodes, list storage, records) goes to the level build
+  return r == 1 && levels < kMortonLevels && tree_build_morton_levels(ctx, t, leaf_cap, seq_max, kMortonLevels) == 0;
 }
 
-bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels) {
+// 0: built; 1: a split was needed below the key's levels; 2: another capacity overflow.
+int tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int seq_max, const int levels) {
   const long long n = t.n;
   cudaStream_t s = ctx->stream;
 
@@ -1783,7 +1792,7 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
     dfree(sg);
     release();
     rec.free();
-    return false;
+    return hs.overflow_depth ? 1 : 2;
   }
   int R = hs.rec_extra;
   for (int d = 0; d <= kMaxDepth + 1; ++d) R += hs.lvl_cnt[d];
@@ -1792,7 +1801,7 @@ bool tree_build_morton_levels(ptrom_ctx* ctx, Tree& t, long long leaf_cap, int s
   ctx->tree_stats.levels = hs.levels_used;
   release();
   rec.free();
-  return true;
+  return 0;
 }
 
 // Computes exact sums for nodes flagged need_exact; returns how many.
