@@ -603,7 +603,7 @@ __global__ void hp_gamma_kernel(DSurrogate s, AffineTables t, bool affine, doubl
 }
 
 template <int IB, bool OFF32>
-__global__ void __launch_bounds__(128, 8) hyperpair_kernel(DSurrogate s, AffineTables at, HpGamma hg,
+__global__ void __launch_bounds__(128, 7) hyperpair_kernel(DSurrogate s, AffineTables at, HpGamma hg,
                                                         const double* __restrict__ mu, int B,
                                                         const double* __restrict__ xbar,
                                                         const double2* __restrict__ cxy,
@@ -684,11 +684,22 @@ __global__ void __launch_bounds__(128, 8) hyperpair_kernel(DSurrogate s, AffineT
       auto clusters = [&](auto check) {
         constexpr bool CHECK = decltype(check)::value;
         long long k = k0;
+        // The next round's list entries are read one round ahead (clamped to
+        // the list), so a round waits on the position gathers only.
+        int cn[U] = {};
+        if (k + U <= ke) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) cn[u] = s.cl_list[k + u];
+        }
         for (; k + U <= ke; k += U) {
           int ci[U];
           double sx[U], sy[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) ci[u] = s.cl_list[k + u];
+          for (int u = 0; u < U; ++u) {
+            ci[u] = cn[u];
+            const long long kn = k + U + u;
+            cn[u] = s.cl_list[kn < ke ? kn : k];
+          }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             // n_c·B < 2^32 (host-checked): 32-bit offsets, one IMAD.WIDE per gather
