@@ -482,13 +482,19 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long lon
         const int bl = b0 + 2 * lc, b = i0 + bl;  // lane holds instances b, b+1 of its row
         double v[2];
         if (AFFINE) {
+          // (a + μ b) / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times
+          // numerator. The x-row lane and the y-row lane (lane ^ 4) hold the
+          // same two instances: each forms the reciprocal of one of them
+          // (the x lane instance b, the y lane b + 1) and they swap.
+          const double mo = bl + xy < icnt ? smu[bl + xy] : 0.0;
+          const double Go = fma(mo, gb, ga);
+          if (c_ok && bl + xy < icnt && Go == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+          const double ro = rcp64(Go);
+          const double rs = __shfl_xor_sync(0xffffffffu, ro, 4);
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double m = bl + e < icnt ? smu[bl + e] : 0.0;
-            const double G = fma(m, gb, ga);
-            if (c_ok && bl + e < icnt && G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
-            // (a + μ b) / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times numerator
-            v[e] = fma(m, base_b + acc1[e], base_a + acc0[e]) * rcp64(G);
+            v[e] = fma(m, base_b + acc1[e], base_a + acc0[e]) * (e == xy ? ro : rs);
           }
         } else {
           v[0] = base_a + acc0[0];
@@ -1409,14 +1415,21 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
   PTROM_CUDA(cudaMemsetAsync(xhat, 0, (size_t)B * MP * 8, st));
   PTROM_CUDA(cudaMemsetAsync(w.pairs, 0, 8, st));
   const double h = dt / 2.0;
-  // rom.hpp:298-300: x̄_prev = x̄⁰, f̄_prev = hyperpair(x̄⁰, 0); jac scratch is overwritten below
-  rom_hyperpair(ctx, s, &g, t, &et, B, MP, xhat, d_mu, nullptr, nullptr, xprev, delta, form, d_inflow, n, w, fprev,
+  // rom.hpp:298-300: x̄_prev = x̄⁰, f̄_prev = hyperpair(x̄⁰, 0). The step-start
+  // evaluation of rom.hpp:306-307 (x̄ = x̄⁰ + Φ̄x̂, (f̄, J) = hyperpair(x̄, x̂))
+  // is at the x̂ of the previous evaluation of every instance, so it is the
+  // same deterministic computation on the same inputs: its result is already
+  // in (x̄, f̄, J) — at step 0 from this call (x̂ = 0 gives x̄ = x̄⁰ exactly, and
+  // the fused kernel returns the velocity-only call's f̄ bit for bit), later
+  // from the last evaluation of the previous step (inactive instances keep
+  // theirs). It is reused instead of recomputed; x̄_prev/f̄_prev get copies.
+  rom_hyperpair(ctx, s, &g, t, &et, B, MP, xhat, d_mu, nullptr, nullptr, xbar, delta, form, d_inflow, n, w, fbar,
                 jac, false);
+  const size_t row_bytes = (size_t)B * rows * 8;
+  PTROM_CUDA(cudaMemcpyAsync(xprev, xbar, row_bytes, cudaMemcpyDeviceToDevice, st));
+  PTROM_CUDA(cudaMemcpyAsync(fprev, fbar, row_bytes, cudaMemcpyDeviceToDevice, st));
   for (long long step = 0; step < n_steps; ++step) {
     reset_step_kernel<<<blocks_for(B, 256), 256, 0, st>>>(B, gs);
-    // x̄ = x̄⁰ + Φ̄ x̂; (f̄, J) = hyperpair(x̄, x̂)   (rom.hpp:306-307)
-    rom_hyperpair(ctx, s, &g, t, &et, B, MP, xhat, d_mu, nullptr, nullptr, xbar, delta, form, d_inflow, n, w, fbar,
-                  jac, false);
     while (true) {
       PTROM_CUDA(cudaMemsetAsync(gs.n_active, 0, 4, st));
       gn_partial_kernel<MP><<<dim3((unsigned)((B + 7) / 8), (unsigned)S), 256, gn_smem, st>>>(
@@ -1434,9 +1447,10 @@ unsigned long long gnat_simulate_t(ptrom_ctx* ctx, const DSurrogate& s, const DG
     record_step_kernel<<<blocks_for(B, 128), 128, 0, st>>>(B, g.m, MP, step, n_steps, xhat, gs, d_xhat_out, d_iters,
                                                             d_conv);
     PTROM_LAUNCH_CHECK();
-    // rom.hpp:336-337: history <- accepted state
-    std::swap(xprev, xbar);
-    std::swap(fprev, fbar);
+    // rom.hpp:336-337: history <- accepted state; (x̄, f̄, J) stay as the next
+    // step's start evaluation
+    PTROM_CUDA(cudaMemcpyAsync(xprev, xbar, row_bytes, cudaMemcpyDeviceToDevice, st));
+    PTROM_CUDA(cudaMemcpyAsync(fprev, fbar, row_bytes, cudaMemcpyDeviceToDevice, st));
   }
   unsigned long long pairs = 0;
   PTROM_CUDA(cudaMemcpyAsync(&pairs, w.pairs, 8, cudaMemcpyDeviceToHost, st));
