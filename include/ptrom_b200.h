@@ -58,7 +58,10 @@ int ptrom_synchronize(ptrom_ctx* ctx);
  * one-CTA-per-cluster reassign path, default 4096, min 32), "tree_seq_max"
  * (tree nodes up to this size get bit-exact sequential sums in the subtree
  * CTAs, default 2048), "tree_build_mode" (0 Morton, 1 level build),
- * "allpairs_variant" (tile shape). Unknown keys are status 2. */
+ * "allpairs_variant" (tile shape), "hyperpair_variant" (PTROM batched-march
+ * hyperpair kernel: 0 default, 1 generic kernel, 2 four-entry rounds at 32
+ * warps per SM, 3 per-SM target ranges).
+ * Unknown keys are status 2. */
 int ptrom_set_tuning(ptrom_ctx* ctx, const char* key, int64_t value);
 /* Library/kernel identification for provenance checks. */
 const char* ptrom_build_info(void);

@@ -162,6 +162,7 @@ int ptrom_set_tuning(ptrom_ctx* ctx, const char* key, int64_t value) {
     else if (k == "tree_seq_max") ctx->tree_seq_max = (int)std::max<int64_t>(1, value);
     else if (k == "tree_build_mode") ctx->tree_build_mode = value ? 1 : 0;
     else if (k == "allpairs_variant") ctx->allpairs_variant = (int)value;
+    else if (k == "hyperpair_variant") ctx->hp_variant = (int)value;
     else throw status_error(PTROM_CONFIG_ERROR, "ptrom_set_tuning: unknown key '" + k + "'");
   });
 }

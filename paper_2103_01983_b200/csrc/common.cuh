@@ -111,7 +111,8 @@ struct ptrom_ctx {
   int* h_counts = nullptr;  // pinned scratch for small D2H reads (tree level counts)
   unsigned* tile_ctr = nullptr;  // per-target-tile arrival counters of the fused chunk reduction (kept zeroed)
   size_t tile_ctr_cap = 0;  // n for decoding kStatusCoincidentPair (i·n + j)
-  int allpairs_variant = 0;  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
+  int allpairs_variant = 0;
+  int hp_variant = 0;         // PTROM hyperpair kernel (tuning: hyperpair_variant; 1 = generic kernel)  // tuning knob (PTROM_ALLPAIRS_VARIANT), 0 = default shape
   ptrom::TreeStats tree_stats;
   int tree_seq_max = 2048;   // nodes up to this size get bit-exact sequential sums (PTROM_TREE_SEQ_MAX)
   long long reassign_big = 4096;  // clusters above this many members take reassign_big_kernel (PTROM_REASSIGN_BIG)

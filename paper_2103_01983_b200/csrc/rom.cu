@@ -801,6 +801,233 @@ __global__ void __launch_bounds__(128, 7) hyperpair_kernel(DSurrogate s, AffineT
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(pairs, sum);
 }
 
+// hyperpair for the batched march (engine Γ/2π tables present, n_c·B and
+// u·B < 2^32): the same arithmetic and per-target summation order as
+// hyperpair_kernel, with the table mode (affine (G_A, G_B)/2π or exact Γ̃/2π)
+// and the δ = 0 coincidence check as template arguments, 32-bit list
+// offsets, and the next round's list entries read without a clamp (the last
+// round is peeled), so a round issues only its loads and the pair arithmetic.
+// Warp = one target × 32 instances; the instance chunk is the slow index, and
+// a CTA's WPC warps take WPC consecutive targets of t_order (they share most
+// cluster positions in L1).
+struct HpArgs {
+  DSurrogate s;
+  HpGamma hg;
+  const double* mu;
+  int B;
+  const double* xbar;
+  const double2* cxy;
+  const double2* dxy;
+  double dp;
+  const double* inflow;
+  long long n;
+  const unsigned char* active;
+  double* f;
+  double* jac;
+  unsigned long long* pairs;
+  DeviceStatus* st;
+  int* sm_ctr;  // per-SM work counters (hyperpair_engine_sm_kernel), zeroed before the launch
+};
+
+// One warp's item: target tt of t_order, instances [32·chunk, 32·chunk + 32).
+// Returns the lane's interaction count.
+template <bool AFFINE, bool CHECK, int U>
+__device__ __forceinline__ unsigned long long hp_engine_item(const HpArgs& a, long long tt, long long chunk, int lane) {
+  const DSurrogate& s = a.s;
+  const HpGamma& hg = a.hg;
+  const int B = a.B;
+  const double dp = a.dp;
+  const long long nt = s.n_t, n = a.n;
+  const int b = (int)(chunk * 32 + lane);
+  unsigned long long cnt = 0;
+  const double* __restrict__ xbar = a.xbar;
+  const double* __restrict__ mu = a.mu;
+  const double* __restrict__ inflow = a.inflow;
+  const double2* __restrict__ cxy = a.cxy;
+  const double2* __restrict__ dxy = a.dxy;
+  double* __restrict__ f = a.f;
+  double* __restrict__ jac = a.jac;
+  DeviceStatus* st = a.st;
+  if (b < B && (!a.active || a.active[b])) {
+    const long long t = s.t_order ? s.t_order[tt] : tt;
+    const double px = xbar[(long long)b * 2 * nt + t], py = xbar[(long long)b * 2 * nt + nt + t];
+    double fx = 0, fy = 0, ja = 0, jd = 0, jc = 0, js = 0;
+    // the pair law of hyperpair_kernel (Jacobian B term as S − δ'C − 2D)
+    auto add = [&](double sx, double sy, double gs) {
+      const double rx = px - sx, ry = py - sy;
+      const double q = fma(rx, rx, fma(ry, ry, dp));
+      const double u = rcp64(q);
+      const double sv = gs * u;
+      fx = fma(-ry, sv, fx);
+      fy = fma(rx, sv, fy);
+      const double w = sv * u;
+      const double wrx = w * rx;
+      ja = fma(wrx, ry, ja);
+      jd = fma(wrx, rx, jd);
+      jc += w;
+      js += sv;
+    };
+    const double mub = AFFINE ? mu[b] : 0.0;
+    auto cgam = [&](unsigned ci) -> double {
+      if (AFFINE) {
+        const double2 v = __ldg(hg.gab + ci);
+        return fma(mub, v.y, v.x);
+      }
+      return __ldg(hg.gc + ci);
+    };
+    const double2* cpb = cxy + b;
+    const unsigned ub = (unsigned)B;
+    const long long k0 = s.cl_off[t];
+    const int* lp = s.cl_list + k0;
+    const int nk = (int)(s.cl_off[t + 1] - k0);
+    unsigned skipped = 0;
+    cnt = (unsigned long long)nk;
+    int i = 0;
+    unsigned cn[U];
+    if (nk >= U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) cn[u] = (unsigned)lp[u];
+    }
+    auto round = [&](const unsigned (&ci)[U]) {
+      double2 p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) p[u] = __ldg(cpb + ci[u] * ub);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (CHECK && p[u].x == px && p[u].y == py) {  // rom.hpp:129 (δ = 0 only)
+          ++skipped;
+          continue;
+        }
+        add(p[u].x, p[u].y, cgam(ci[u]));
+      }
+    };
+    const int* lq = lp + U;  // the next round's entries (immediate offsets)
+    for (; i + 2 * U <= nk; i += U, lq += U) {
+      unsigned ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ci[u] = cn[u];
+        cn[u] = (unsigned)lq[u];
+      }
+      round(ci);
+    }
+    if (i + U <= nk) {
+      round(cn);
+      i += U;
+    }
+    for (; i < nk; ++i) {
+      const unsigned ci = (unsigned)lp[i];
+      const double2 p = cpb[ci * ub];
+      if (CHECK && p.x == px && p.y == py) {
+        ++skipped;
+        continue;
+      }
+      add(p.x, p.y, cgam(ci));
+    }
+    cnt -= skipped;
+    const int self_loc = hg.self_loc[t];
+    const double2* dpb = dxy + b;
+    const long long kd0 = s.d_off[t];
+    const int* dl = s.d_list + kd0;
+    const int nd = (int)(s.d_off[t + 1] - kd0);
+    auto dgam = [&](unsigned loc) -> double {
+      if (AFFINE) {
+        const double2 v = hg.gdab[loc];
+        return fma(mub, v.y, v.x);
+      }
+      return hg.gd[loc];
+    };
+    int j = 0;
+    for (; j + 4 <= nd; j += 4) {
+      unsigned loc[4];
+      double2 p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) loc[u] = (unsigned)dl[j + u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] = dpb[loc[u] * ub];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if ((int)loc[u] != self_loc) {  // rom.hpp:140
+          add(p[u].x, p[u].y, dgam(loc[u]));
+          ++cnt;
+        }
+    }
+    for (; j < nd; ++j) {
+      const unsigned loc = (unsigned)dl[j];
+      if ((int)loc == self_loc) continue;
+      const double2 p = dpb[loc * ub];
+      add(p.x, p.y, dgam(loc));
+      ++cnt;
+    }
+    const long long pid = s.target_ids[t];
+    if (inflow) {
+      fx = fx + inflow[pid];
+      fy = fy + inflow[pid + n];
+    }
+    const double jb = fma(-2.0, jd, fma(-dp, jc, js));  // Σ w·(ry² − rx²)
+    const double j00 = 2.0 * ja, j01 = jb - dp * jc, j10 = jb + dp * jc;
+    if (!isfinite(fx) || !isfinite(fy) || !isfinite(j00) || !isfinite(j01) || !isfinite(j10))
+      latch_status(st, kStatusNonFiniteVelocity, pid);
+    f[(long long)b * 2 * nt + t] = fx;
+    f[(long long)b * 2 * nt + nt + t] = fy;
+    double* jj = jac + ((long long)b * nt + t) * 4;
+    jj[0] = j00;
+    jj[1] = j01;
+    jj[2] = j10;
+    jj[3] = -j00;
+  }
+  return cnt;
+}
+
+__device__ __forceinline__ void hp_count(unsigned long long cnt, int lane, unsigned long long* pairs) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(pairs, cnt);
+}
+
+// Static mapping: warp w → (target w mod n_t, chunk w / n_t); a CTA's WPC
+// warps take WPC consecutive targets of t_order.
+template <bool AFFINE, bool CHECK, int WPC, int MINB, int U>
+__global__ void __launch_bounds__(WPC * 32, MINB) hyperpair_engine_kernel(const __grid_constant__ HpArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = blockIdx.x * (long long)WPC + (threadIdx.x >> 5);
+  const long long nt = a.s.n_t;
+  const long long tt = wid % nt, chunk = wid / nt;
+  if (chunk * 32 >= a.B) return;
+  hp_count(hp_engine_item<AFFINE, CHECK, U>(a, tt, chunk, lane), lane, a.pairs);
+}
+
+// Per-SM mapping (persistent CTAs): SM i owns the targets
+// [i·n_t/S, (i+1)·n_t/S) of t_order for every chunk (S = %nsmid), and its
+// warps pull items chunk-major from the SM's counter, so all warps resident
+// on one SM sweep neighbouring targets of one chunk together (their cluster
+// positions meet in the SM's L1). A warp whose SM range is exhausted moves on
+// to the next SM's counter (load balance at the tail).
+template <bool AFFINE, bool CHECK, int WPC, int MINB, int U>
+__global__ void __launch_bounds__(WPC * 32, MINB) hyperpair_engine_sm_kernel(const __grid_constant__ HpArgs a) {
+  const int lane = threadIdx.x & 31;
+  unsigned smid, nsm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+  const long long nt = a.s.n_t;
+  const long long chunks = (a.B + 31) / 32;
+  unsigned long long cnt = 0;
+  for (unsigned v = 0; v < nsm; ++v) {
+    const unsigned sm = (smid + v) % nsm;
+    const long long lo = nt * sm / nsm, hi = nt * (sm + 1) / nsm, len = hi - lo;
+    if (len == 0) continue;
+    const long long items = len * chunks;
+    while (true) {
+      int item = 0;
+      if (lane == 0) item = atomicAdd(a.sm_ctr + sm, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= items) break;
+      cnt += hp_engine_item<AFFINE, CHECK, U>(a, lo + item % len, item / len, lane);
+    }
+  }
+  hp_count(cnt, lane, a.pairs);
+}
+
 // ------------------------------------------------------ Gauss–Newton ---
 // Split-K Gauss–Newton projections: CTA = 8 instances (one warp each) x one
 // slice of the sampled rows, 32 rows per chunk. Each chunk's operands are
@@ -1298,10 +1525,50 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
       hg.gdab = et->hgdab;
     }
     const bool off32 = (double)std::max(s.n_c, s.u) * (double)B < 4294967296.0;
-    auto hk = off32 ? hyperpair_kernel<IB, true> : hyperpair_kernel<IB, false>;
-    hk<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy,
-                                                 effective_delta(delta, form), delta, d_inflow, n, d_active, d_f,
-                                                 d_jac, w.pairs, ctx->d_status);
+    const int var = ctx->hp_variant;
+    if (et && off32 && s.n_t > 0 && var != 1) {
+      // batched march: hyperpair_engine_kernel (template table mode, no clamps)
+      HpArgs ha{s, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy, effective_delta(delta, form), d_inflow, n,
+                d_active, d_f, d_jac, w.pairs, ctx->d_status, w.sm_ctr};
+      const long long warps = s.n_t * ((B + 31) / 32);
+      const bool chk = delta == 0.0;
+      auto launch = [&](auto wpc_tag, auto minb_tag, auto u_tag, auto per_sm_tag) {
+        constexpr int WPC = decltype(wpc_tag)::value, MINB = decltype(minb_tag)::value, UU = decltype(u_tag)::value;
+        if constexpr (decltype(per_sm_tag)::value) {
+          PTROM_CUDA(cudaMemsetAsync(w.sm_ctr, 0, sizeof(int) * RomScratch::kSmCtr, st));
+          const unsigned blocks = (unsigned)(ctx->num_sms * MINB);
+          auto k = t ? (chk ? hyperpair_engine_sm_kernel<true, true, WPC, MINB, UU>
+                            : hyperpair_engine_sm_kernel<true, false, WPC, MINB, UU>)
+                     : (chk ? hyperpair_engine_sm_kernel<false, true, WPC, MINB, UU>
+                            : hyperpair_engine_sm_kernel<false, false, WPC, MINB, UU>);
+          k<<<blocks, WPC * 32, 0, st>>>(ha);
+        } else {
+          const unsigned blocks = (unsigned)((warps + WPC - 1) / WPC);
+          auto k = t ? (chk ? hyperpair_engine_kernel<true, true, WPC, MINB, UU>
+                            : hyperpair_engine_kernel<true, false, WPC, MINB, UU>)
+                     : (chk ? hyperpair_engine_kernel<false, true, WPC, MINB, UU>
+                            : hyperpair_engine_kernel<false, false, WPC, MINB, UU>);
+          k<<<blocks, WPC * 32, 0, st>>>(ha);
+        }
+      };
+      // Measured on config 4 (B = 512, tools/sweep_hp.py, profiles/r02_sweep_hyperpair.jsonl):
+      // generic kernel 4.92 ms; engine U = 4 at 28 / 32 / 36 warps per SM 5.01 / 4.55 / 4.42 ms;
+      // U = 3 at 36 warps (56 registers) 4.40 ms (default); fewer registers spill (U = 2/3 at
+      // 40-44 warps: 4.7-9.0 ms); per-SM target ranges 4.84 ms.
+      using C4 = std::integral_constant<int, 4>;
+      using C3 = std::integral_constant<int, 3>;
+      using C9 = std::integral_constant<int, 9>;
+      switch (var) {
+        case 2: launch(C4{}, std::integral_constant<int, 8>{}, C4{}, std::false_type{}); break;  // U = 4, 32 warps/SM
+        case 3: launch(C4{}, std::integral_constant<int, 8>{}, C4{}, std::true_type{}); break;   // per-SM target ranges
+        default: launch(C4{}, C9{}, C3{}, std::false_type{}); break;                 // U = 3, 36 warps/SM
+      }
+    } else {
+      auto hk = off32 ? hyperpair_kernel<IB, true> : hyperpair_kernel<IB, false>;
+      hk<<<blocks_for(threads, 128), 128, 0, st>>>(s, tt, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy,
+                                                   effective_delta(delta, form), delta, d_inflow, n, d_active, d_f,
+                                                   d_jac, w.pairs, ctx->d_status);
+    }
   }
   PTROM_LAUNCH_CHECK();
   unsigned long long h = 0;
@@ -1325,10 +1592,11 @@ void RomScratch::ensure(const DSurrogate& s, long long nt, int B) {
     cap_d = need_d;
   }
   if (!pairs) PTROM_CUDA(cudaMalloc(&pairs, 16));
+  if (!sm_ctr) PTROM_CUDA(cudaMalloc(&sm_ctr, sizeof(int) * kSmCtr));
   (void)nt;
 }
 void RomScratch::release() {
-  void* ps[] = {cxy, dxy, pairs};
+  void* ps[] = {cxy, dxy, pairs, sm_ctr};
   for (void* p : ps)
     if (p) cudaFree(p);
   *this = RomScratch{};

@@ -96,6 +96,8 @@ struct RomScratch {
   // source positions, (x, y) interleaved: [cluster][instance], [direct][instance]
   double2 *cxy = nullptr, *dxy = nullptr;
   unsigned long long* pairs = nullptr;
+  int* sm_ctr = nullptr;  // per-SM work counters of the per-SM hyperpair mapping
+  static constexpr int kSmCtr = 1024;
   size_t cap_c = 0, cap_d = 0;
   void ensure(const DSurrogate& s, long long nt, int B);
   void release();

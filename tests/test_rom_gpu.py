@@ -379,3 +379,36 @@ def test_config4_full_size_ptrom_simulate(pt, oracle, config4_full):
                                             w.x0, ids, A, w.gamma_a + m * w.gamma_b, w.delta, w.dt, steps, 1e-300, 5)
         np.testing.assert_array_equal(tb.iterations[i], it_o)
         assert max(rel(tb.x_hat[i, s], xo[:, s]) for s in range(steps)) <= 1e-12, m
+
+
+@pytest.mark.parametrize("delta", [None, 0.0])
+def test_hyperpair_kernel_variants_bitwise(pt, prob, delta):
+    """The batched march's hyperpair kernels (ptrom_set_tuning
+    "hyperpair_variant": engine U = 3 default, U = 4, per-SM target ranges,
+    and the generic kernel) give bit-identical x̂ — same per-target summation
+    order — with a partial 32-instance chunk (B = 40), δ = 0 included (the
+    coincident-centroid check path), and match the oracle."""
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    d = w.delta if delta is None else delta
+    steps = 4
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, prob.ids, prob.A)
+    ds = to_device(rom, prob.surrogate())
+    mu = np.linspace(0.5, 2.0, 40)
+    ctx = ds.ctx
+    out = {}
+    try:
+        for v in (1, 0, 2, 3):
+            ctx.set_tuning("hyperpair_variant", v)
+            tr = rom.ptrom_simulate_batch(basis, op, ds, w.gamma_a, w.gamma_b, mu, pt.ParticleSystem(prob.g1, d),
+                                          pt.TimeGrid(w.dt, steps), rom.RomConfig(1e-300, 5, 1.0), batch=40)
+            out[v] = np.asarray(tr.x_hat).copy()
+    finally:
+        ctx.set_tuning("hyperpair_variant", 0)
+    for v in (0, 2, 3):
+        np.testing.assert_array_equal(out[v], out[1])
+    for i in (0, 17, 39):
+        xo, _, _ = prob.oracle.ptrom_simulate(prob.surrogate(), w.phi, w.sv, w.x0, prob.ids, prob.A,
+                                              w.gamma_a + mu[i] * w.gamma_b, d, w.dt, steps, 1e-300, 5)
+        assert max(rel(out[0][i, s], xo[:, s]) for s in range(steps)) <= 1e-12
