@@ -421,7 +421,8 @@ def allpairs_line(args, w, K, W, rank, world, local, e2e_steps, cpu_seconds, wit
                              "peak": peaks["fp32_ffma_tflops"] if peaks else None, "unit": "TFLOP/s",
                              "frac": FLOPS_PER_PAIR * v32 / 1e12 / peaks["fp32_ffma_tflops"] if peaks else None,
                              "traffic": None,
-                             "kernel": "allpairs_f32_kernel<128,8> (csrc/allpairs.cu), step incl. chunk reduction"},
+                             "kernel": "allpairs_sym_f32_kernel (csrc/allpairs_sym.cu, unordered pairs), step incl. "
+                                       "the block-partial reduction"},
                 "cpu_baseline": cpu32, "clocks": clocks32.summary(),
                 "parity": "judged against the fp64 oracle at 1e-5 (tests/test_allpairs_gpu.py)"}
 

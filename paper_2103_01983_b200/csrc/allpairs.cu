@@ -340,64 +340,9 @@ __global__ void reduce_jacobian_f64_kernel(long long t_begin, long long t_count,
 }
 
 // ----------------------------------------------------------------- fp32 ---
-// fp32 pairs; each shared-memory tile is summed in fp32 and promoted into
-// fp64 accumulators (blocked summation keeps the fp32 result within 1e-5 of
-// the fp64 oracle at N = 65,536).
-// MUFU.RCP (16/clk/SM) would bound a reciprocal per pair at 1/8 of the FMA
-// rate, so on the fast path four targets share one reciprocal of
-// P = (q0 q1)(q2 q3) (tile guard: |coords| < 2^13 and δ' in [2^-30, 2^28]
-// keep P inside the normal fp32 range); the safe path (and the masked
-// diagonal tiles) keep one MUFU.RCP per pair.
-__device__ __forceinline__ bool coord_ok_f32(float v) { return fabsf(v) < 8192.f; }
-
-template <int T, bool MASK, bool FAST>
-__device__ __forceinline__ void tile_f32(int cnt, const float2* __restrict__ sp, const float* __restrict__ sg,
-                                         long long j0, const float (&tx)[T], const float (&ty)[T],
-                                         const long long (&ti)[T], float dp, float (&ax)[T], float (&ay)[T]) {
-#pragma unroll 4
-  for (int jj = 0; jj < cnt; ++jj) {
-    const float2 p = sp[jj];
-    const float g = sg[jj];
-    if (FAST && !MASK && (T % 4 == 0)) {
-#pragma unroll
-      for (int k = 0; k < T; k += 4) {
-        float rx[4], ry[4], q[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          rx[m] = tx[k + m] - p.x;
-          ry[m] = ty[k + m] - p.y;
-          q[m] = fmaf(rx[m], rx[m], fmaf(ry[m], ry[m], dp));
-        }
-        const float p01 = q[0] * q[1], p23 = q[2] * q[3];
-        const float gu = g * rcp_approx(p01 * p23);  // Γ'/(q0 q1 q2 q3)
-        const float g01 = gu * p23, g23 = gu * p01;  // Γ'/(q0 q1), Γ'/(q2 q3)
-        const float sv[4] = {g01 * q[1], g01 * q[0], g23 * q[3], g23 * q[2]};
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          ax[k + m] = fmaf(-ry[m], sv[m], ax[k + m]);
-          ay[k + m] = fmaf(rx[m], sv[m], ay[k + m]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < T; ++k) {
-        const float rx = tx[k] - p.x;
-        const float ry = ty[k] - p.y;
-        float q = fmaf(rx, rx, fmaf(ry, ry, dp));
-        float gs = g;
-        if (MASK) {
-          const bool self = (j0 + jj) == ti[k];
-          q = self ? 1.f : q;
-          gs = self ? 0.f : gs;
-        }
-        const float s = gs * rcp_approx(q);
-        ax[k] = fmaf(-ry, s, ax[k]);
-        ay[k] = fmaf(rx, s, ay[k]);
-      }
-    }
-  }
-}
-
+// fp32 pairs (tile_f32, pair_tile.cuh); each shared-memory tile is summed in
+// fp32 and promoted into fp64 accumulators (blocked summation keeps the fp32
+// result within 1e-5 of the fp64 oracle at N = 65,536).
 template <int TPB, int T>
 __global__ void __launch_bounds__(TPB) allpairs_f32_kernel(long long n, const float* __restrict__ xs,
                                                            const float* __restrict__ ys,
@@ -920,6 +865,10 @@ void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* 
                       const float* inflow, long long t_begin, long long t_end, float* f, long long ld) {
   const long long t_count = t_end - t_begin;
   if (t_count <= 0) return;
+  if (t_begin == 0 && t_count == n && ld == n && sym_velocity_applies(ctx, n)) {  // every target: unordered pairs
+    dev_velocity_sym_f32(ctx, n, x, gamma, delta, form, inflow, f);
+    return;
+  }
   constexpr int T = 8;
   auto kern = allpairs_f32_kernel<kTPB, T>;
   static int occ = resident_blocks(kern, kTPB);

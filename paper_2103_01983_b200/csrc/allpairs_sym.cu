@@ -317,6 +317,254 @@ __global__ void reduce_sym_kernel(long long n, int nb, const double* __restrict_
   }
 }
 
+// ----------------------------------------------------------------- fp32 ---
+// The same unordered-pair decomposition at S = float (kernel.hpp:107-129
+// instantiated for float): fp32 pair arithmetic, four targets sharing one
+// MUFU.RCP of (q0 q1)(q2 q3) on range-guarded tiles (tile_f32's guard), one
+// MUFU.RCP per pair otherwise. Blocked summation as in allpairs_f32_kernel:
+// the I side is summed in fp32 per 128-source tile and promoted into fp64
+// accumulators; the J side per 32-source batch (32 lanes x 8 targets) in
+// fp32, the warps' batch sums and the passes in fp64; part rows are fp64.
+template <bool FAST4, bool TAIL>
+__device__ __forceinline__ void sym_pairs_f32(float px, float py, float g, bool vj, const float (&tx)[kST],
+                                              const float (&ty)[kST], const float (&gi)[kST], float dp,
+                                              float (&fx)[kST], float (&fy)[kST], float& wx, float& wy) {
+#pragma unroll
+  for (int k = 0; k < kST; k += 4) {
+    float rx[4], ry[4], q[4], u[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      rx[m] = tx[k + m] - px;
+      ry[m] = ty[k + m] - py;
+      q[m] = fmaf(rx[m], rx[m], fmaf(ry[m], ry[m], dp));
+    }
+    if (FAST4) {  // u_m = 1/q_m from one reciprocal of (q0 q1)(q2 q3)
+      const float p01 = q[0] * q[1], p23 = q[2] * q[3];
+      const float uP = rcp_approx(p01 * p23);
+      const float u01 = uP * p23, u23 = uP * p01;
+      u[0] = u01 * q[1];
+      u[1] = u01 * q[0];
+      u[2] = u23 * q[3];
+      u[3] = u23 * q[2];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) u[m] = rcp_approx(q[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      float a = g * u[m];                // Γ'_j / q: target i's weight
+      const float b = gi[k + m] * u[m];  // Γ'_i / q: source j's weight, r_ji = −r_ij
+      if (TAIL) a = vj ? a : 0.f;        // a source beyond n (its own sum is discarded)
+      fx[k + m] = fmaf(-ry[m], a, fx[k + m]);
+      fy[k + m] = fmaf(rx[m], a, fy[k + m]);
+      wx = fmaf(ry[m], b, wx);
+      wy = fmaf(-rx[m], b, wy);
+    }
+  }
+}
+
+template <bool TAIL>
+__device__ void sym_item_f32(long long n, const float* __restrict__ xs, const float* __restrict__ ys,
+                             const float* __restrict__ gam, float inv2pi, float dp, long long B, int I, int J,
+                             double* __restrict__ part, long long ps, float2* sp, float* sg, double2 (*sj)[kSTPB]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i_blk = (long long)I * B, j_blk = (long long)J * B;
+  const long long j_end = min(j_blk + B, n);
+  const int passes = (int)((min(i_blk + B, n) - i_blk + kSPass - 1) / kSPass);
+  for (int pass = 0; pass < passes; ++pass) {
+    const long long i0 = i_blk + (long long)pass * kSPass;
+    float tx[kST], ty[kST], gi[kST];
+    double dfx[kST], dfy[kST];
+    bool my_ok4 = true;
+#pragma unroll
+    for (int k = 0; k < kST; ++k) {
+      const long long i = i0 + k * kSTPB + tid;
+      const bool ok = i < n;
+      tx[k] = ok ? xs[i] : 0.f;
+      ty[k] = ok ? ys[i] : 0.f;
+      gi[k] = ok ? gam[i] * inv2pi : 0.f;
+      dfx[k] = dfy[k] = 0.0;
+      my_ok4 = my_ok4 && coord_ok_f32(tx[k]) && coord_ok_f32(ty[k]);
+    }
+    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-30f && dp <= 0x1p28f;
+    for (long long t0 = j_blk; t0 < j_end; t0 += kSTPB) {
+      const long long j = t0 + tid;
+      const bool vj = j < n;
+      const float px = vj ? xs[j] : 0.f, py = vj ? ys[j] : 0.f;
+      const float pg = vj ? gam[j] * inv2pi : 0.f;
+      sp[2 * tid - lane] = make_float2(px, py);  // each 32-source batch twice (rotated linear reads)
+      sp[2 * tid - lane + 32] = make_float2(px, py);
+      sg[2 * tid - lane] = pg;
+      sg[2 * tid - lane + 32] = pg;
+      const bool fast4 = __syncthreads_and(coord_ok_f32(px) && coord_ok_f32(py)) && targets_ok4;
+      const int cnt = (int)min((long long)kSTPB, j_end - t0);
+      float fx[kST], fy[kST];
+#pragma unroll
+      for (int k = 0; k < kST; ++k) fx[k] = fy[k] = 0.f;
+      for (int b0 = 0; b0 < kSTPB; b0 += 32) {
+        float wx = 0.f, wy = 0.f;
+        if (b0 < cnt) {  // CTA-uniform
+          const float2* bp = sp + 2 * b0 + lane;
+          const float* bg = sg + 2 * b0 + lane;
+          const int nxt = (lane + 1) & 31;
+          auto batch = [&](auto fast_tag) {
+            constexpr bool F = decltype(fast_tag)::value;
+#pragma unroll 16
+            for (int s = 0; s < 32; ++s) {
+              const float2 p = bp[s];
+              const float g = bg[s];
+              const bool v = !TAIL || b0 + ((lane + s) & 31) < cnt;
+              sym_pairs_f32<F, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, fx, fy, wx, wy);
+              wx = __shfl_sync(0xffffffffu, wx, nxt);  // the accumulator follows its source one lane down
+              wy = __shfl_sync(0xffffffffu, wy, nxt);
+            }
+          };
+          if (fast4)
+            batch(std::true_type{});
+          else
+            batch(std::false_type{});
+        }
+        sj[warp][b0 + lane] = make_double2((double)wx, (double)wy);
+      }
+#pragma unroll
+      for (int k = 0; k < kST; ++k) {
+        dfx[k] += (double)fx[k];
+        dfy[k] += (double)fy[k];
+      }
+      __syncthreads();
+      if (vj) {
+        double2 acc = sj[0][tid];
+#pragma unroll
+        for (int w = 1; w < kSTPB / 32; ++w) {
+          acc.x += sj[w][tid].x;
+          acc.y += sj[w][tid].y;
+        }
+        double* px_ = part + (long long)I * 2 * ps + j;
+        if (pass == 0) {
+          px_[0] = acc.x;
+          px_[ps] = acc.y;
+        } else {
+          px_[0] = px_[0] + acc.x;
+          px_[ps] = px_[ps] + acc.y;
+        }
+      }
+      __syncthreads();
+    }
+    double* out = part + (long long)J * 2 * ps;
+#pragma unroll
+    for (int k = 0; k < kST; ++k) {
+      const long long i = i0 + k * kSTPB + tid;
+      if (i < n) {
+        out[i] = dfx[k];
+        out[ps + i] = dfy[k];
+      }
+    }
+  }
+}
+
+// Diagonal block, fp32: one-sided (allpairs_f32_kernel's tile loop). On the
+// fast path the self pair adds exactly ±0 (δ' > 0); the safe path masks it.
+__device__ void diag_item_f32(long long n, const float* __restrict__ xs, const float* __restrict__ ys,
+                              const float* __restrict__ gam, float inv2pi, float dp, long long B, int I,
+                              double* __restrict__ part, long long ps, float2* sp, float* sg) {
+  constexpr int T = kST, TPB = kSTPB;
+  const int tid = threadIdx.x;
+  const long long blk = (long long)I * B, blk_end = min(blk + B, n);
+  const int passes = (int)((blk_end - blk + kSPass - 1) / kSPass);
+  for (int pass = 0; pass < passes; ++pass) {
+    const long long tile0 = blk + (long long)pass * kSPass;
+    float tx[T], ty[T];
+    double dfx[T], dfy[T];
+    long long ti[T];
+    bool my_ok = true;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const long long i = tile0 + k * TPB + tid;
+      const bool ok = i < blk_end;
+      ti[k] = ok ? i : -1;
+      tx[k] = ok ? xs[i] : 0.f;
+      ty[k] = ok ? ys[i] : 0.f;
+      dfx[k] = dfy[k] = 0.0;
+      my_ok = my_ok && coord_ok_f32(tx[k]) && coord_ok_f32(ty[k]);
+    }
+    const long long tile_end = min(tile0 + (long long)kSPass, blk_end);
+    const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-30f && dp <= 0x1p28f;
+    for (long long j0 = blk; j0 < blk_end; j0 += TPB) {
+      const int cnt = (int)min((long long)TPB, blk_end - j0);
+      const long long j = j0 + tid;
+      const float px = j < blk_end ? xs[j] : 0.f, py = j < blk_end ? ys[j] : 0.f;
+      sp[tid] = make_float2(px, py);
+      sg[tid] = j < blk_end ? gam[j] * inv2pi : 0.f;
+      const bool fast = __syncthreads_and(coord_ok_f32(px) && coord_ok_f32(py)) && targets_ok;
+      const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt) && !fast;
+      float ax[T], ay[T];
+#pragma unroll
+      for (int k = 0; k < T; ++k) ax[k] = ay[k] = 0.f;
+      if (masked)
+        tile_f32<T, true, false>(cnt, sp, sg, j0, tx, ty, ti, dp, ax, ay);
+      else if (fast)
+        tile_f32<T, false, true>(cnt, sp, sg, j0, tx, ty, ti, dp, ax, ay);
+      else
+        tile_f32<T, false, false>(cnt, sp, sg, j0, tx, ty, ti, dp, ax, ay);
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        dfx[k] += (double)ax[k];
+        dfy[k] += (double)ay[k];
+      }
+      __syncthreads();
+    }
+    double* out = part + (long long)I * 2 * ps;
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+      if (ti[k] >= 0) {
+        out[ti[k]] = dfx[k];
+        out[ps + ti[k]] = dfy[k];
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kSTPB, 4) allpairs_sym_f32_kernel(long long n, const float* __restrict__ xs,
+                                                                    const float* __restrict__ ys,
+                                                                    const float* __restrict__ gam, float inv2pi,
+                                                                    float dp, long long B,
+                                                                    double* __restrict__ part, long long ps,
+                                                                    long long k0) {
+  __shared__ float2 sp[2 * kSTPB];
+  __shared__ float sg[2 * kSTPB];
+  __shared__ double2 sj[kSTPB / 32][kSTPB];
+  int I, J;
+  decode_pair(k0 + blockIdx.x, I, J);
+  if (I == J) {
+    diag_item_f32(n, xs, ys, gam, inv2pi, dp, B, I, part, ps, sp, sg);
+    return;
+  }
+  if ((long long)(J + 1) * B > n)
+    sym_item_f32<true>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, ps, sp, sg, sj);
+  else
+    sym_item_f32<false>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, ps, sp, sg, sj);
+}
+
+// f_i = (float)(Σ_K part[K][·][i], ascending K) + inflow (the rounding of
+// reduce_velocity_f32_kernel).
+__global__ void reduce_sym_f32_kernel(long long n, int nb, const double* __restrict__ part,
+                                      const float* __restrict__ inflow, float* __restrict__ f, DeviceStatus* st) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double sx = 0.0, sy = 0.0;
+    for (int k = 0; k < nb; ++k) {
+      sx += part[(long long)k * 2 * n + i];
+      sy += part[((long long)k * 2 + 1) * n + i];
+    }
+    float ox = (float)sx, oy = (float)sy;
+    if (inflow) {
+      ox = ox + inflow[i];
+      oy = oy + inflow[i + n];
+    }
+    if (!isfinite(ox) || !isfinite(oy)) latch_status(st, kStatusNonFiniteVelocity, i);
+    f[i] = ox;
+    f[i + n] = oy;
+  }
+}
+
 }  // namespace
 
 bool sym_velocity_applies(ptrom_ctx* ctx, long long n) {
@@ -379,6 +627,36 @@ void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const do
   const long long rg = std::min<long long>((n + 255) / 256, (long long)ctx->num_sms * 8);
   reduce_sym_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(n, (int)nb, part, n, 0, n, 0,
                                                                                   inflow, f, ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
+static int sym_f32_occupancy() {
+  static int occ = [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, allpairs_sym_f32_kernel, kSTPB, 0);
+    return std::max(o, 1);
+  }();
+  return occ;
+}
+
+void dev_velocity_sym_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
+                          const float* inflow, float* f) {
+  const long long B = choose_sym_block(n, ctx->num_sms * sym_f32_occupancy(), 1);
+  const long long nb = (n + B - 1) / B;
+  const long long items = nb * (nb + 1) / 2;
+  ctx->scratch.reset();
+  ctx->scratch.reserve((size_t)nb * 2 * n * sizeof(double) + 4096);
+  double* part = ctx->scratch.take<double>((size_t)nb * 2 * n);
+  const float dp = (float)effective_delta((double)delta, form);
+  {
+    ProfScope prof(ctx);
+    allpairs_sym_f32_kernel<<<(unsigned)items, kSTPB, 0, ctx->stream>>>(n, x, x + n, gamma,
+                                                                        (float)(1.0 / (2.0 * M_PI)), dp, B, part, n, 0);
+  }
+  PTROM_LAUNCH_CHECK();
+  const long long rg = std::min<long long>((n + 255) / 256, (long long)ctx->num_sms * 8);
+  reduce_sym_f32_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(n, (int)nb, part, inflow, f,
+                                                                                      ctx->d_status);
   PTROM_LAUNCH_CHECK();
 }
 

@@ -24,6 +24,8 @@ void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const do
 bool sym_sharded_applies(ptrom_ctx* ctx, long long n, int world);
 void dev_velocity_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
                                   const double* gamma, double delta, int form, const double* inflow, double* f_local);
+void dev_velocity_sym_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
+                          const float* inflow, float* f);
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
                       const float* inflow, long long t_begin, long long t_end, float* f, long long ld);
 // jxx..jyy (may be null when inv is given) or the Newton-block inverse of

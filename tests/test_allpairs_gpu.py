@@ -297,3 +297,42 @@ def test_unordered_pair_kernel_flags_coincident_pair(pt):
     x[17], x[n + 17] = x[15000], x[n + 15000]
     with pytest.raises(pt.NumericalError):
         pt.pairwise_velocity(x, pt.ParticleSystem(np.ones(n), 0.0))
+
+
+@pytest.mark.parametrize("n,scale,delta,form,inflow", [(16384, 1.0, 2.5e-5, 0, False), (20037, 1.0, 0.3, 1, True),
+                                                       (40000, 2.0 ** 14, 1e3, 0, False), (33000, 1.0, 0.0, 0, True),
+                                                       (65536, 0.25, 0.005, 0, False)])
+def test_unordered_pair_kernel_fp32(pt, oracle, monkeypatch, n, scale, delta, form, inflow):
+    """fp32 full self-evaluations over unordered pairs (allpairs_sym.cu,
+    allpairs_sym_f32_kernel): against the one-sided fp32 kernel
+    (PTROM_ALLPAIRS_SYM=0) and the fp64 oracle at the fp32 tolerance, ragged
+    blocks, inflow, both forms, the safe tier (|x| ≥ 2^13) and δ = 0; run to
+    run bit-identical."""
+    rng = np.random.default_rng(n + 1)
+    x = (rng.uniform(-1.0, 1.0, 2 * n) * scale).astype(np.float32)
+    g = (rng.normal(0.0, 1.0, n) / n).astype(np.float32)
+    infl = rng.uniform(-1, 1, 2 * n).astype(np.float32) if inflow else None
+    sys_ = pt.ParticleSystem(g, np.float32(delta), infl, form)
+    f = pt.pairwise_velocity(x, sys_)
+    assert f.dtype == np.float32
+    assert np.array_equal(f, pt.pairwise_velocity(x, sys_))
+    monkeypatch.setenv("PTROM_ALLPAIRS_SYM", "0")
+    one_sided = pt.pairwise_velocity(x, sys_)
+    monkeypatch.delenv("PTROM_ALLPAIRS_SYM")
+    assert rel(f.astype(np.float64), one_sided.astype(np.float64)) <= FP32_TOL
+    x64, g64 = x.astype(np.float64), g.astype(np.float64)
+    i64 = infl.astype(np.float64) if inflow else None
+    d64 = float(np.float32(delta))
+    for b in (0, n // 2, n - 700):
+        ref = oracle.pairwise_velocity(x64, g64, d64, form, i64, t_begin=b, t_end=b + 700, threads=THREADS)
+        rows = np.r_[b:b + 700, n + b:n + b + 700]
+        assert rel(f[rows].astype(np.float64), ref[rows]) <= FP32_TOL, b
+
+
+def test_unordered_pair_kernel_fp32_flags_coincident_pair(pt):
+    n = 20000
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, 2 * n).astype(np.float32)
+    x[17], x[n + 17] = x[15000], x[n + 15000]
+    with pytest.raises(pt.NumericalError):
+        pt.pairwise_velocity(x, pt.ParticleSystem(np.ones(n, np.float32), np.float32(0.0)))
