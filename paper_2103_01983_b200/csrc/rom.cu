@@ -1009,6 +1009,8 @@ __global__ void __launch_bounds__(WPC * 32, MINB) hyperpair_engine_sm_kernel(con
   unsigned smid, nsm;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+  nsm = min(nsm, (unsigned)RomScratch::kSmCtr);  // counters allocated (smid >= kSmCtr folds below)
+  smid %= nsm;
   const long long nt = a.s.n_t;
   const long long chunks = (a.B + 31) / 32;
   unsigned long long cnt = 0;
