@@ -401,15 +401,17 @@ __global__ void positions_clusters_kernel(DSurrogate s, AffineTables t, int B, i
 }
 
 
-// Cluster positions as a DMMA GEMM. A warp tile is 4 clusters x (x, y) rows
-// x 8 instances with K = MP modes: the table rows are the A operand, x̂ of 8
-// instances the B operand. Affine mode runs two accumulator chains per tile
-// (X_A + S_A x̂ and X_B + S_B x̂ land in the same lane), and the epilogue
-// forms (a + μ b)/(G_A + μ G_B) on all 32 lanes. Exact mode is one chain,
-// x̃⁰ + Φ̃ x̂, and it also serves the direct sources (x⁰_d + Φ_d x̂, table
-// [u][2][mp]). The CTA stages x̂ (and μ) of up to `ic` instances in shared
-// memory once (row stride MP + 4 doubles: conflict-free B fragments), and its
-// 16 warps then sweep cluster tiles grid-stride.
+// Cluster positions as a DMMA GEMM. A warp tile is 8 instances x 4 clusters
+// x (x, y) with K = MP modes: x̂ of 8 instances is the A operand, the table
+// rows the B operand, so each lane's two accumulators are the (x, y) of one
+// (instance, cluster) and the epilogue needs no exchange: one G(μ) and one
+// reciprocal per lane, one 16-byte store. The bases (X_A, X_B or x̃⁰) seed
+// the accumulators. Affine mode runs two chains (X_A + S_A x̂ and X_B + S_B x̂
+// land in the same lane) and forms (a + μ b)/(G_A + μ G_B). Exact mode is one
+// chain, x̃⁰ + Φ̃ x̂, and it also serves the direct sources (x⁰_d + Φ_d x̂,
+// table [u][2][mp]). The CTA stages x̂ (and μ) of up to `ic` instances in
+// shared memory once (row stride MP + 4 doubles: conflict-free fragments),
+// and its 16 warps then sweep cluster tiles grid-stride.
 template <int MP>
 struct PosSmem {
   static constexpr int SX = MP + 4;
@@ -450,62 +452,56 @@ __global__ void __launch_bounds__(512, 2) positions_clusters_mma_kernel(long lon
       for (int e = threadIdx.x; e < icnt; e += blockDim.x) smu[e] = mu[i0 + e];
     __syncthreads();
     for (long long tile = w0; tile < ctiles; tile += wstride) {
-      const long long ca = tile * 4 + (lr >> 1);
-      const bool c_ok = ca < nc;
-      const double* trow = tab + (ca * (AFFINE ? 4 : 2) + xy) * (long long)MP;
+      // B operand (k = lc, column n = lr): the table row of cluster
+      // tile·4 + (lr >> 1), coordinate lr & 1, loaded once per tile
+      const long long cb = tile * 4 + (lr >> 1);
+      const double* trow = tab + (cb * (AFFINE ? 4 : 2) + xy) * (long long)MP;
       double a0[KS], a1[KS];
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
-        a0[k] = c_ok ? trow[4 * k + lc] : 0.0;
-        a1[k] = (AFFINE && c_ok) ? trow[2 * MP + 4 * k + lc] : 0.0;
+        a0[k] = cb < nc ? trow[4 * k + lc] : 0.0;
+        a1[k] = (AFFINE && cb < nc) ? trow[2 * MP + 4 * k + lc] : 0.0;
       }
-      double base_a = 0, base_b = 0, ga = 0, gb = 0;
+      // accumulator owner: instance b0 + lr, cluster tile·4 + lc, (x, y) in
+      // (d0, d1) — the x and y rows of one cluster are adjacent columns
+      const long long ca = tile * 4 + lc;
+      const bool c_ok = ca < nc;
+      double bax = 0, bay = 0, bbx = 0, bby = 0;
       if (c_ok) {
         if (AFFINE) {
-          base_a = t.xa[ca + (xy ? nc : 0)];
-          base_b = t.xb[ca + (xy ? nc : 0)];
-          ga = t.ga[ca];
-          gb = t.gb[ca];
+          bax = t.xa[ca];
+          bay = t.xa[ca + nc];
+          bbx = t.xb[ca];
+          bby = t.xb[ca + nc];
         } else {
-          base_a = x0[ca + (xy ? nc : 0)];
+          bax = x0[ca];
+          bay = x0[ca + nc];
         }
       }
       for (int b0 = 0; b0 < icnt; b0 += 8) {
-        double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
-        const double* xrow = sxh + (b0 + lr) * SX + lc;
+        // D = X̂ · Tᵀ + base: the bases seed the accumulators
+        double acc0[2] = {bax, bay}, acc1[2] = {bbx, bby};
+        const double* xrow = sxh + (b0 + lr) * SX + lc;  // A operand: instance b0 + lr, k = lc
 #pragma unroll
         for (int k = 0; k < KS; ++k) {
           const double x = xrow[4 * k];
-          dmma(acc0, a0[k], x);
-          if (AFFINE) dmma(acc1, a1[k], x);
+          dmma(acc0, x, a0[k]);
+          if (AFFINE) dmma(acc1, x, a1[k]);
         }
-        const int bl = b0 + 2 * lc, b = i0 + bl;  // lane holds instances b, b+1 of its row
-        double v[2];
+        const int bl = b0 + lr, b = i0 + bl;
+        if (!c_ok || bl >= icnt || (active && !active[b])) continue;
+        double2 v;
         if (AFFINE) {
-          // (a + μ b) / G(μ): reciprocal (≤ 1 ulp, MUFU seed + cubic) times
-          // numerator. The x-row lane and the y-row lane (lane ^ 4) hold the
-          // same two instances: each forms the reciprocal of one of them
-          // (the x lane instance b, the y lane b + 1) and they swap.
-          const double mo = bl + xy < icnt ? smu[bl + xy] : 0.0;
-          const double Go = fma(mo, gb, ga);
-          if (c_ok && bl + xy < icnt && Go == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
-          const double ro = rcp64(Go);
-          const double rs = __shfl_xor_sync(0xffffffffu, ro, 4);
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double m = bl + e < icnt ? smu[bl + e] : 0.0;
-            v[e] = fma(m, base_b + acc1[e], base_a + acc0[e]) * (e == xy ? ro : rs);
-          }
+          // (a + μ b) / G(μ): one reciprocal (≤ 1 ulp, MUFU seed + cubic) for both coordinates
+          const double m = smu[bl];
+          const double G = fma(m, __ldg(t.gb + ca), __ldg(t.ga + ca));  // L1-resident across the tile
+          if (G == 0.0) latch_status(st, kStatusZeroClusterCirculation, ca);
+          const double ig = rcp64(G);
+          v = make_double2(fma(m, acc1[0], acc0[0]) * ig, fma(m, acc1[1], acc0[1]) * ig);
         } else {
-          v[0] = base_a + acc0[0];
-          v[1] = base_a + acc0[1];
+          v = make_double2(acc0[0], acc0[1]);
         }
-        // the x-row lane and the y-row lane (lane ^ 4) swap one value: the
-        // x lane stores (x, y) of instance b, the y lane that of b + 1
-        const double other = __shfl_xor_sync(0xffffffffu, xy ? v[0] : v[1], 4);
-        const int e = xy;
-        if (c_ok && bl + e < icnt && (!active || active[b + e]))
-          out[ca * B + b + e] = xy ? make_double2(other, v[1]) : make_double2(v[0], other);
+        out[ca * B + b] = v;
       }
     }
   }
