@@ -32,6 +32,10 @@ def table(prof, title):
 
 
 what = sys.argv[1]
+# PTROM_TUNING="key=value,...": ptrom_set_tuning on the default context (A/B of engine variants)
+for kv in filter(None, os.environ.get("PTROM_TUNING", "").split(",")):
+    k_, v_ = kv.split("=")
+    pt.default_context().set_tuning(k_, int(v_))
 if what == "config4":
     from paper_2103_01983_b200 import rom
     from paper_2103_01983_b200.tree import ClusterCriterion

@@ -1,9 +1,9 @@
-"""Config 4 hyperpair kernel variants (ptrom_set_tuning "hyperpair_variant"):
+"""Config 4 kernel variants (ptrom_set_tuning "hyperpair_variant", or the key given as the 4th argument):
 per variant, one batched march of B instances x S steps; prints the average
 hyperpair launch (library CUDA events around the launch), the march time and
 whether x̂ is bit-identical to variant 1 (the generic kernel).
 
-    python tools/sweep_hp.py [B] [steps] [variants, comma-separated]
+    python tools/sweep_hp.py [B] [steps] [variants, comma-separated] [tuning key]
 """
 import ctypes
 import json
@@ -22,6 +22,7 @@ from paper_2103_01983_b200.tree import ClusterCriterion  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 variants = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "1,0,2,3,4").split(",")]
+key = sys.argv[4] if len(sys.argv) > 4 else "hyperpair_variant"  # or gn_variant
 w = workloads.config4(n_inst=B)
 ctx = pt.default_context()
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -36,7 +37,7 @@ sys_ = pt.ParticleSystem(g1, w.delta)
 lib = ctx.lib
 ref = None
 for v in variants:
-    ctx.set_tuning("hyperpair_variant", v)
+    ctx.set_tuning(key, v)
     rom.ptrom_simulate_batch(basis, op, sur, w.gamma_a, w.gamma_b, w.mu[:B], sys_, pt.TimeGrid(w.dt, 1), cfg, batch=B)
     torch.cuda.synchronize()
     lib.ptrom_profile_begin(ctx.handle)
