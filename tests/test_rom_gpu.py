@@ -412,3 +412,33 @@ def test_hyperpair_kernel_variants_bitwise(pt, prob, delta):
         xo, _, _ = prob.oracle.ptrom_simulate(prob.surrogate(), w.phi, w.sv, w.x0, prob.ids, prob.A,
                                               w.gamma_a + mu[i] * w.gamma_b, d, w.dt, steps, 1e-300, 5)
         assert max(rel(out[0][i, s], xo[:, s]) for s in range(steps)) <= 1e-12
+
+
+def test_batch_engine_inflow_scaled_form(pt, prob):
+    """The batched march's engine kernels with an inflow field and the
+    denominator-scaled kernel form (kernel.hpp:29-42): x̂ matches the oracle's
+    per-instance ptrom_simulate and the generic kernel bit for bit."""
+    from paper_2103_01983_b200 import rom
+    w = prob.w
+    rng = np.random.default_rng(11)
+    inflow = rng.uniform(-0.05, 0.05, 2 * w.n)
+    steps = 4
+    basis = rom.PODBasis(w.phi, w.sv, w.x0)
+    op = rom.GnatOperator(basis, prob.ids, prob.A)
+    ds = to_device(rom, prob.surrogate())
+    mu = np.array([0.6, 1.1, 1.9])
+    sys_ = pt.ParticleSystem(prob.g1, 0.02, inflow, 1)
+    out = {}
+    try:
+        for v in (0, 1):
+            ds.ctx.set_tuning("hyperpair_variant", v)
+            tr = rom.ptrom_simulate_batch(basis, op, ds, w.gamma_a, w.gamma_b, mu, sys_, pt.TimeGrid(w.dt, steps),
+                                          rom.RomConfig(1e-300, 5, 1.0))
+            out[v] = np.asarray(tr.x_hat).copy()
+    finally:
+        ds.ctx.set_tuning("hyperpair_variant", 0)
+    np.testing.assert_array_equal(out[0], out[1])
+    for i, m in enumerate(mu):
+        xo, _, _ = prob.oracle.ptrom_simulate(prob.surrogate(), w.phi, w.sv, w.x0, prob.ids, prob.A,
+                                              w.gamma_a + m * w.gamma_b, 0.02, w.dt, steps, 1e-300, 5, 1.0, 1, inflow)
+        assert max(rel(out[0][i, s], xo[:, s]) for s in range(steps)) <= 1e-12, m
