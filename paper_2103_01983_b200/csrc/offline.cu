@@ -5,10 +5,12 @@
 //   weighted_pod_space + build_weighted_pod_tree + cluster_pod
 //                        reduction.hpp:74-77, 236-385 (device quadtree + traversal)
 //
-// Small dense factorizations (the gappy least-squares fits of greedy
-// sampling, at most 2·n_samples x 31, and the n_d x m_r pseudo-inverse) run as
-// a column-pivoted Householder QR on the host: they are O(rows · m_r²) index-
-// sized problems next to the O(N · m_r) device scoring passes.
+// The dense factorizations (the gappy least-squares fits of greedy sampling,
+// up to 2·n_samples x 31 with their right-hand sides, and the n_d x m_r
+// pseudo-inverse) run on the device as one cooperative column-pivoted
+// Householder QR (dev_cpqr_kernel); only the k x k triangular solves of the
+// fits (k ≤ 31) are finished on the host.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -30,89 +32,257 @@ void rom_reassign_exact(ptrom_ctx* ctx, DSurrogate& s, const DBasis& b, const do
 
 namespace {
 
-// ---------------------------------------------------------- host dense LA --
-// Column-pivoted Householder QR of a rows x cols column-major matrix.
-struct PivotedQR {
-  long long rows, cols;
-  std::vector<double> a;     // R in the upper triangle, reflector tails below
-  std::vector<double> taus;  // reflector scalars
-  std::vector<int> piv;      // column j of R is input column piv[j]
-  int rank = 0;
+namespace cg = cooperative_groups;
 
-  PivotedQR(long long r, long long c, std::vector<double> m) : rows(r), cols(c), a(std::move(m)) {
-    const long long k = std::min(rows, cols);
-    piv.resize(cols);
-    std::iota(piv.begin(), piv.end(), 0);
-    taus.assign(k, 0.0);
-    std::vector<double> cn(cols);
-    for (long long j = 0; j < cols; ++j) {
-      double s = 0;
-      for (long long i = 0; i < rows; ++i) s += a[i + j * rows] * a[i + j * rows];
-      cn[j] = s;
-    }
-    double first = 0;
-    for (long long j = 0; j < k; ++j) {
-      long long p = j;
-      for (long long c2 = j + 1; c2 < cols; ++c2)
-        if (cn[c2] > cn[p]) p = c2;
-      if (p != j) {
-        for (long long i = 0; i < rows; ++i) std::swap(a[i + j * rows], a[i + p * rows]);
-        std::swap(cn[j], cn[p]);
-        std::swap(piv[j], piv[p]);
-      }
-      double* col = &a[j * rows];
-      double tail = 0;
-      for (long long i = j + 1; i < rows; ++i) tail += col[i] * col[i];
-      const double x0 = col[j];
-      double beta = x0, tau = 0;
-      if (tail > 0) {
-        beta = -std::copysign(std::sqrt(x0 * x0 + tail), x0);
-        tau = (beta - x0) / beta;
-        const double scale = 1.0 / (x0 - beta);
-        for (long long i = j + 1; i < rows; ++i) col[i] *= scale;
-      }
-      col[j] = beta;
-      taus[j] = tau;
-      for (long long c2 = j + 1; c2 < cols; ++c2) {
-        double* cc = &a[c2 * rows];
-        double w = cc[j];
-        for (long long i = j + 1; i < rows; ++i) w += col[i] * cc[i];
-        w *= tau;
-        cc[j] -= w;
-        for (long long i = j + 1; i < rows; ++i) cc[i] -= w * col[i];
-        double s = 0;
-        for (long long i = j + 1; i < rows; ++i) s += cc[i] * cc[i];
-        cn[c2] = s;
-      }
-      if (j == 0) first = std::fabs(beta);
-      if (std::fabs(beta) > 2.220446049250313e-16 * (double)k * first) rank = (int)j + 1;
-    }
-  }
-  // y <- Q^T y
-  void apply_qt(double* y) const {
-    for (size_t j = 0; j < taus.size(); ++j) {
-      if (taus[j] == 0) continue;
-      const double* v = &a[j * rows];
-      double w = y[j];
-      for (long long i = (long long)j + 1; i < rows; ++i) w += v[i] * y[i];
-      w *= taus[j];
-      y[j] -= w;
-      for (long long i = (long long)j + 1; i < rows; ++i) y[i] -= w * v[i];
-    }
-  }
-  // basic least-squares solution (free variables zero)
-  std::vector<double> solve(std::vector<double> b) const {
-    apply_qt(b.data());
-    std::vector<double> z(cols, 0.0), x(cols, 0.0);
-    for (int i = rank - 1; i >= 0; --i) {
-      double s = b[i];
-      for (int j = i + 1; j < rank; ++j) s -= a[i + (long long)j * rows] * z[j];
-      z[i] = s / a[i + (long long)i * rows];
-    }
-    for (long long j = 0; j < cols; ++j) x[piv[j]] = z[j];
-    return x;
-  }
+// ------------------------------------------------------ device dense LA ---
+// Column-pivoted Householder QR of a tall rows x ct column-major matrix in
+// global memory, the first cp columns pivot-eligible and the rest right-hand
+// sides that receive every reflector (so they end as Qᵀb). The algorithm is
+// the host PivotedQR's below (the same pivot rule — largest remaining norm,
+// lowest index on ties — the same reflector formulas and rank test), as one
+// cooperative launch: CTA b owns rows [b·rows/G, (b+1)·rows/G), and each
+// column step is three fixed-order grid reductions (the tail norm, the
+// reflector's dot products, the updated norms), so it is deterministic.
+constexpr int kQRT = 256;
+constexpr int kQRMaxCols = 64;
+
+struct DevQR {
+  double* a;  // rows x ct, column-major (R and the reflector tails in place)
+  long long rows;
+  int ct, cp;
+  double* taus;  // [cp]
+  int* piv;      // [cp]: column j of R is input column piv[j]
+  int* rank;     // [1]
+  double* red;   // [3][G][kQRMaxCols] per-CTA partials
+  double* rowj;  // [kQRMaxCols] row j of the columns right of j (published by its owner)
 };
+
+// fixed-order block sum (warp shuffles, then the warps in order), result in every thread
+__device__ double qr_block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < kQRT / 32; ++w) t += sh[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(kQRT) dev_cpqr_kernel(const __grid_constant__ DevQR q) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double cn[kQRMaxCols], wv[kQRMaxCols], sh[kQRT / 32];
+  __shared__ int pv[kQRMaxCols];
+  const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
+  const long long R = q.rows;
+  const long long r0 = R * bid / G, r1 = R * (bid + 1) / G;
+  const int ct = q.ct, cp = q.cp;
+  double* a = q.a;
+  auto col = [&](int c) { return a + (long long)c * R; };
+  // three partial regions (tail norm, dot products, column norms): each is
+  // read only between the two barriers that follow its writes
+  auto publish = [&](int region, int c, double v) {  // thread 0 of each CTA: its partial for column c
+    if (tid == 0) q.red[((long long)region * G + bid) * kQRMaxCols + c] = v;
+  };
+  auto gather = [&](int region, int c) {  // every CTA: the partials of column c in CTA order
+    double t = 0.0;
+    for (int b = 0; b < G; ++b) t += q.red[((long long)region * G + b) * kQRMaxCols + c];
+    return t;
+  };
+  for (int c = tid; c < cp; c += kQRT) pv[c] = c;
+  for (int c = 0; c < cp; ++c) {
+    double s = 0.0;
+    for (long long i = r0 + tid; i < r1; i += kQRT) s += col(c)[i] * col(c)[i];
+    publish(2, c, qr_block_sum(s, sh));
+  }
+  grid.sync();
+  for (int c = tid; c < cp; c += kQRT) cn[c] = gather(2, c);
+  __syncthreads();
+  const int k = (int)min((long long)cp, R);
+  double first = 0.0;
+  int rank = 0;
+  for (int j = 0; j < k; ++j) {
+    int p = j;
+    for (int c2 = j + 1; c2 < cp; ++c2)
+      if (cn[c2] > cn[p]) p = c2;
+    if (p != j) {
+      for (long long i = r0 + tid; i < r1; i += kQRT) {
+        const double t = col(j)[i];
+        col(j)[i] = col(p)[i];
+        col(p)[i] = t;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const double t = cn[j];
+        cn[j] = cn[p];
+        cn[p] = t;
+        const int ti = pv[j];
+        pv[j] = pv[p];
+        pv[p] = ti;
+      }
+      __syncthreads();
+    }
+    // tail norm Σ_{i>j} a_ij²; the owner of row j publishes row j of the columns right of j
+    {
+      double s = 0.0;
+      for (long long i = max(r0, (long long)j + 1) + tid; i < r1; i += kQRT) s += col(j)[i] * col(j)[i];
+      publish(0, j, qr_block_sum(s, sh));
+      if (j >= r0 && j < r1)
+        for (int c2 = j + tid; c2 < ct; c2 += kQRT) q.rowj[c2] = col(c2)[j];
+    }
+    grid.sync();
+    const double tail = gather(0, j);
+    const double x0 = q.rowj[j];
+    double beta = x0, tau = 0.0, scale = 0.0;
+    if (tail > 0) {
+      beta = -copysign(sqrt(x0 * x0 + tail), x0);
+      tau = (beta - x0) / beta;
+      scale = 1.0 / (x0 - beta);
+    }
+    // reflector tail v = a_{i>j, j}·scale, then the dot products with the columns right of j
+    for (long long i = max(r0, (long long)j + 1) + tid; i < r1; i += kQRT) col(j)[i] *= scale;
+    __syncthreads();
+    for (int c2 = j + 1; c2 < ct; ++c2) {
+      double s = 0.0;
+      for (long long i = max(r0, (long long)j + 1) + tid; i < r1; i += kQRT) s += col(j)[i] * col(c2)[i];
+      publish(1, c2, qr_block_sum(s, sh));
+    }
+    grid.sync();
+    for (int c2 = j + 1 + tid; c2 < ct; c2 += kQRT) wv[c2] = (q.rowj[c2] + gather(1, c2)) * tau;
+    __syncthreads();
+    if (j >= r0 && j < r1 && tid == 0) {
+      col(j)[j] = beta;
+      for (int c2 = j + 1; c2 < ct; ++c2) col(c2)[j] -= wv[c2];
+    }
+    for (int c2 = j + 1; c2 < ct; ++c2) {
+      const double w = wv[c2];
+      double s = 0.0;
+      for (long long i = max(r0, (long long)j + 1) + tid; i < r1; i += kQRT) {
+        const double v = col(c2)[i] - w * col(j)[i];
+        col(c2)[i] = v;
+        s += v * v;
+      }
+      if (c2 < cp) publish(2, c2, qr_block_sum(s, sh));
+    }
+    grid.sync();
+    for (int c2 = j + 1 + tid; c2 < cp; c2 += kQRT) cn[c2] = gather(2, c2);
+    __syncthreads();
+    if (j == 0) first = fabs(beta);
+    if (fabs(beta) > 2.220446049250313e-16 * (double)k * first) rank = j + 1;
+    if (bid == 0 && tid == 0) q.taus[j] = tau;
+  }
+  if (bid == 0) {
+    for (int c = tid; c < cp; c += kQRT) q.piv[c] = pv[c];
+    if (tid == 0) *q.rank = rank;
+  }
+}
+
+// Q1 = H_0 … H_{k−1} [e_0 … e_{m−1}] (rows x m, column-major) from the
+// reflectors of dev_cpqr_kernel, applied in reverse order; one grid reduction
+// per reflector (the owner of row r folds row r into its partial).
+__global__ void __launch_bounds__(kQRT) dev_form_q1_kernel(const double* __restrict__ a, long long R, int m, int k,
+                                                          const double* __restrict__ taus, double* __restrict__ q1,
+                                                          double* __restrict__ red) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[kQRT / 32], wv[kQRMaxCols];
+  const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
+  const long long r0 = R * bid / G, r1 = R * (bid + 1) / G;
+  for (int c = 0; c < m; ++c)
+    for (long long i = r0 + tid; i < r1; i += kQRT) q1[i + (long long)c * R] = i == c ? 1.0 : 0.0;
+  for (int r = k - 1; r >= 0; --r) {
+    const double tau = taus[r];
+    if (tau == 0.0) continue;  // CTA-uniform
+    const double* v = a + (long long)r * R;
+    for (int c = 0; c < m; ++c) {
+      const double* qc = q1 + (long long)c * R;
+      double s = (r >= r0 && r < r1) ? qc[r] : 0.0;
+      s = (tid == 0) ? s : 0.0;
+      for (long long i = max(r0, (long long)r + 1) + tid; i < r1; i += kQRT) s += v[i] * qc[i];
+      const double t = qr_block_sum(s, sh);
+      if (tid == 0) red[(long long)bid * kQRMaxCols + c] = t;
+    }
+    grid.sync();
+    for (int c = tid; c < m; c += kQRT) {
+      double t = 0.0;
+      for (int b = 0; b < G; ++b) t += red[(long long)b * kQRMaxCols + c];
+      wv[c] = t * tau;
+    }
+    __syncthreads();
+    for (int c = 0; c < m; ++c) {
+      double* qc = q1 + (long long)c * R;
+      const double w = wv[c];
+      if (r >= r0 && r < r1 && tid == 0) qc[r] -= w;
+      for (long long i = max(r0, (long long)r + 1) + tid; i < r1; i += kQRT) qc[i] -= w * v[i];
+    }
+    grid.sync();  // red is rewritten by the next reflector
+  }
+}
+
+// pinv column k = P R⁻¹ (row k of Q1)ᵀ (back substitution; R from the top
+// m x m of the factorization), A is m x rows column-major.
+__global__ void pinv_rows_kernel(const double* __restrict__ a, long long R, int m, const int* __restrict__ piv,
+                                 const double* __restrict__ q1, double* __restrict__ A) {
+  __shared__ double rs[kQRMaxCols * kQRMaxCols];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) rs[e] = a[(e % m) + (long long)(e / m) * R];
+  __syncthreads();
+  const long long kr = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (kr >= R) return;
+  double z[kQRMaxCols];
+  for (int i = m - 1; i >= 0; --i) {
+    double s2 = q1[kr + (long long)i * R];
+    for (int j = i + 1; j < m; ++j) s2 -= rs[i + j * m] * z[j];
+    z[i] = s2 / rs[i + i * m];
+  }
+  for (int j = 0; j < m; ++j) A[piv[j] + kr * m] = z[j];
+}
+
+// sampled rows of Φ_r: row k ↦ ids[k] (k < nid), ids[k − nid] + n (x rows, then y rows),
+// columns [c0, c0 + nc) into out (rows x nc, column-major)
+__global__ void gather_rows_kernel(long long n_dofs, int nid, const long long* __restrict__ ids,
+                                   const double* __restrict__ phi_r, int c0, int nc, double* __restrict__ out) {
+  const long long rows = 2LL * nid;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= rows * nc) return;
+  const long long k = e % rows;
+  const int c = (int)(e / rows);
+  const long long r = k < nid ? ids[k] : ids[k - nid] + n_dofs / 2;
+  out[k + (long long)c * rows] = phi_r[r + (long long)(c0 + c) * n_dofs];
+}
+
+int coop_grid(ptrom_ctx* ctx, const void* kern, long long rows) {
+  int occ = 0;
+  PTROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQRT, 0));
+  const long long want = std::max<long long>(1, (rows + kQRT - 1) / kQRT);
+  return (int)std::max<long long>(1, std::min<long long>(want, (long long)ctx->num_sms * std::max(1, occ)));
+}
+
+struct DevQRResult {
+  int rank = 0;
+  std::vector<int> piv;
+  std::vector<double> top;  // the first min(rows, cp) rows of all ct columns (ld = that count)
+};
+
+// Factor d_a (rows x ct) in place on the device; returns rank, pivots and
+// the top rows (R, and Qᵀb of the right-hand-side columns).
+DevQRResult device_cpqr(ptrom_ctx* ctx, double* d_a, long long rows, int ct, int cp, double* d_taus, int* d_piv,
+                        int* d_rank, double* d_red, double* d_rowj) {
+  cudaStream_t s = ctx->stream;
+  DevQR q{d_a, rows, ct, cp, d_taus, d_piv, d_rank, d_red, d_rowj};
+  int G = coop_grid(ctx, (const void*)dev_cpqr_kernel, rows);
+  void* args[] = {&q};
+  PTROM_CUDA(cudaLaunchCooperativeKernel((const void*)dev_cpqr_kernel, dim3(G), dim3(kQRT), args, 0, s));
+  PTROM_LAUNCH_CHECK();
+  DevQRResult res;
+  const int kt = (int)std::min<long long>(rows, cp);
+  res.piv.resize(cp);
+  res.top.resize((size_t)kt * ct);
+  PTROM_CUDA(cudaMemcpyAsync(&res.rank, d_rank, 4, cudaMemcpyDeviceToHost, s));
+  PTROM_CUDA(cudaMemcpyAsync(res.piv.data(), d_piv, cp * 4, cudaMemcpyDeviceToHost, s));
+  if (kt > 0)
+    PTROM_CUDA(cudaMemcpy2DAsync(res.top.data(), kt * 8, d_a, rows * 8, kt * 8, ct, cudaMemcpyDeviceToHost, s));
+  PTROM_CUDA(cudaStreamSynchronize(s));
+  return res;
+}
 
 // -------------------------------------------------------- greedy kernels ---
 // work[:, q] = Φ_r[:, nb+q] − Φ_r[:, :nb]·coef[:, q]  (reduction.hpp:144)
@@ -224,6 +394,18 @@ std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, i
     PTROM_CUDA(cudaMallocAsync(&d_idx, n * 4, s));
     PTROM_CUDA(cudaMallocAsync(&d_idx_s, n * 4, s));
     PTROM_CUDA(cudaMallocAsync(&d_picked, n, s));
+    // device least-squares workspace (rows ≤ 2·n_target, ≤ n_r + max_ci ≤ 64 columns)
+    if (n_r + max_ci > kQRMaxCols) config_fail("greedy_sample: at most 32 residual modes");
+    double *d_fit, *d_taus, *d_red, *d_rowj;
+    long long* d_ids;
+    int *d_piv, *d_rank;
+    PTROM_CUDA(cudaMallocAsync(&d_fit, (size_t)2 * n_target * (n_r + max_ci) * 8, s));
+    PTROM_CUDA(cudaMallocAsync(&d_ids, (size_t)n_target * 8, s));
+    PTROM_CUDA(cudaMallocAsync(&d_taus, kQRMaxCols * 8, s));
+    PTROM_CUDA(cudaMallocAsync(&d_piv, kQRMaxCols * 4, s));
+    PTROM_CUDA(cudaMallocAsync(&d_rank, 4, s));
+    PTROM_CUDA(cudaMallocAsync(&d_red, (size_t)3 * ctx->num_sms * 32 * kQRMaxCols * 8, s));
+    PTROM_CUDA(cudaMallocAsync(&d_rowj, kQRMaxCols * 8, s));
     PTROM_CUDA(cudaMemcpyAsync(d_picked, picked_h.data(), n, cudaMemcpyHostToDevice, s));
     size_t sort_bytes = 0;
     cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, d_score, d_score_s, d_idx, d_idx_s, (int)n, 0, 64, s);
@@ -236,22 +418,29 @@ std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, i
       if (it == 1) {
         PTROM_CUDA(cudaMemcpyAsync(d_work, d_phi, n_dofs * n_ci * 8, cudaMemcpyDeviceToDevice, s));
       } else {
-        // gappy fit on the rows sampled so far (reduction.hpp:129-143)
+        // gappy fit on the rows sampled so far (reduction.hpp:129-143): the
+        // sampled basis with the n_ci right-hand sides appended, factored on
+        // the device; the basic solution from the k x k top (free variables 0)
         std::vector<long long> ids = chosen;
         std::sort(ids.begin(), ids.end());
-        const long long rows = 2 * (long long)ids.size();
-        std::vector<double> sb(rows * nb), rhs(rows * n_ci);
-        for (long long k = 0; k < rows; ++k) {
-          const long long r = k < (long long)ids.size() ? ids[k] : ids[k - ids.size()] + n;
-          for (long long c = 0; c < nb; ++c) sb[k + c * rows] = phi_r[r + c * n_dofs];
-          for (long long q = 0; q < n_ci; ++q) rhs[k + q * rows] = phi_r[r + (nb + q) * n_dofs];
-        }
-        PivotedQR qr(rows, nb, std::move(sb));
-        std::vector<double> coef(nb * n_ci);
+        const int nid = (int)ids.size();
+        const long long rows = 2LL * nid;
+        const int ct = (int)(nb + n_ci);
+        PTROM_CUDA(cudaMemcpyAsync(d_ids, ids.data(), nid * 8, cudaMemcpyHostToDevice, s));
+        gather_rows_kernel<<<(unsigned)((rows * ct + 255) / 256), 256, 0, s>>>(n_dofs, nid, d_ids, d_phi, 0, ct,
+                                                                              d_fit);
+        PTROM_LAUNCH_CHECK();
+        const DevQRResult qr = device_cpqr(ctx, d_fit, rows, ct, (int)nb, d_taus, d_piv, d_rank, d_red, d_rowj);
+        const int kt = (int)std::min<long long>(rows, nb);
+        std::vector<double> coef(nb * n_ci, 0.0), z(nb);
         for (long long q = 0; q < n_ci; ++q) {
-          std::vector<double> col(rhs.begin() + q * rows, rhs.begin() + (q + 1) * rows);
-          const std::vector<double> x = qr.solve(std::move(col));
-          for (long long c = 0; c < nb; ++c) coef[c + q * nb] = x[c];
+          const double* y = &qr.top[(size_t)(nb + q) * kt];  // Qᵀ b, first kt rows
+          for (int i = qr.rank - 1; i >= 0; --i) {
+            double s2 = y[i];
+            for (int j = i + 1; j < qr.rank; ++j) s2 -= qr.top[i + (size_t)j * kt] * z[j];
+            z[i] = s2 / qr.top[i + (size_t)i * kt];
+          }
+          for (int j = 0; j < qr.rank; ++j) coef[qr.piv[j] + q * nb] = z[j];
         }
         PTROM_CUDA(cudaMemcpyAsync(d_coef, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice, s));
         residual_columns_kernel<<<(unsigned)((n_dofs * n_ci + 255) / 256), 256, 0, s>>>(n_dofs, (int)nb, (int)n_ci,
@@ -269,7 +458,8 @@ std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, i
       for (int p : top) chosen.push_back(p);
       nb += n_ci;
     }
-    void* fr[] = {d_phi, d_work, d_coef, d_score, d_score_s, d_idx, d_idx_s, d_picked, d_tmp};
+    void* fr[] = {d_phi, d_work, d_coef, d_score, d_score_s, d_idx, d_idx_s, d_picked, d_tmp,
+                  d_fit, d_ids, d_taus, d_piv, d_rank, d_red, d_rowj};
     for (void* p : fr) cudaFreeAsync(p, s);
     PTROM_CUDA(cudaStreamSynchronize(s));
   }
@@ -277,8 +467,10 @@ std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, i
   return chosen;
 }
 
-// reduction.hpp:182-220: A = pinv(rows of Φ_r at the sampled dofs).
-std::vector<double> offline_gnat_operator(long long n_dofs, int m_r, const double* phi_r,
+// reduction.hpp:182-220: A = pinv(rows of Φ_r at the sampled dofs), on the
+// device: the sampled rows (n_d x m_r) factored by dev_cpqr_kernel, the rank
+// test of the COD, Q1 formed from the reflectors, and A = P R⁻¹ Q1ᵀ.
+std::vector<double> offline_gnat_operator(ptrom_ctx* ctx, long long n_dofs, int m_r, const double* phi_r,
                                           const std::vector<long long>& ids_in) {
   if (n_dofs % 2 != 0) config_fail("state dimension must be even");
   const long long n = n_dofs / 2;
@@ -291,44 +483,52 @@ std::vector<double> offline_gnat_operator(long long n_dofs, int m_r, const doubl
   if (nd < m_r)
     config_fail("build_gnat_operator: " + std::to_string(nd) + " sampled dofs cannot support " + std::to_string(m_r) +
                 " residual modes (need 2 * samples >= modes)");
+  if (m_r > kQRMaxCols) config_fail("build_gnat_operator: at most 64 residual modes");
   std::vector<double> sm(nd * m_r);
   for (long long k = 0; k < nd; ++k) {
     const long long r = k < (long long)ids.size() ? ids[k] : ids[k - ids.size()] + n;
     for (int c = 0; c < m_r; ++c) sm[k + c * nd] = phi_r[r + c * n_dofs];
   }
-  PivotedQR qr(nd, m_r, std::move(sm));
+  cudaStream_t s = ctx->stream;
+  double *d_a, *d_taus, *d_red, *d_rowj, *d_q1, *d_A;
+  int *d_piv, *d_rank;
+  const size_t red_n = (size_t)3 * ctx->num_sms * 32 * kQRMaxCols;
+  PTROM_CUDA(cudaMallocAsync(&d_a, nd * m_r * 8, s));
+  PTROM_CUDA(cudaMallocAsync(&d_taus, kQRMaxCols * 8, s));
+  PTROM_CUDA(cudaMallocAsync(&d_red, red_n * 8, s));
+  PTROM_CUDA(cudaMallocAsync(&d_rowj, kQRMaxCols * 8, s));
+  PTROM_CUDA(cudaMallocAsync(&d_q1, nd * m_r * 8, s));
+  PTROM_CUDA(cudaMallocAsync(&d_A, nd * m_r * 8, s));
+  PTROM_CUDA(cudaMallocAsync(&d_piv, kQRMaxCols * 4, s));
+  PTROM_CUDA(cudaMallocAsync(&d_rank, 4, s));
+  struct Free {
+    std::vector<void*> p;
+    cudaStream_t s;
+    ~Free() {
+      for (void* q : p) cudaFreeAsync(q, s);
+    }
+  } guard{{d_a, d_taus, d_red, d_rowj, d_q1, d_A, d_piv, d_rank}, s};
+  PTROM_CUDA(cudaMemcpyAsync(d_a, sm.data(), nd * m_r * 8, cudaMemcpyHostToDevice, s));
+  const DevQRResult qr = device_cpqr(ctx, d_a, nd, m_r, m_r, d_taus, d_piv, d_rank, d_red, d_rowj);
   if (qr.rank < m_r) {
     std::string cols;
     for (int k = qr.rank; k < m_r; ++k) cols += (cols.empty() ? "" : ", ") + std::to_string(qr.piv[k]);
     numerical_fail("build_gnat_operator: sampled residual basis has rank " + std::to_string(qr.rank) + " < " +
                    std::to_string(m_r) + "; dependent columns: " + cols);
   }
-  // pinv = P R^{-1} Q1^T: form Q1 (nd x m_r) by applying the reflectors to the
-  // first m_r identity columns, then back-substitute R on its rows.
-  std::vector<double> q1((size_t)nd * m_r, 0.0);
-  for (int j = 0; j < m_r; ++j) {
-    double* col = &q1[(size_t)j * nd];
-    col[j] = 1.0;
-    for (int r = m_r - 1; r >= 0; --r) {  // Q e_j = H_0 ... H_{m_r-1} e_j
-      if (qr.taus[r] == 0) continue;
-      const double* v = &qr.a[(size_t)r * nd];
-      double w = col[r];
-      for (long long i = r + 1; i < nd; ++i) w += v[i] * col[i];
-      w *= qr.taus[r];
-      col[r] -= w;
-      for (long long i = r + 1; i < nd; ++i) col[i] -= w * v[i];
-    }
+  {
+    long long R = nd;
+    int m = m_r, k = m_r;
+    int G = coop_grid(ctx, (const void*)dev_form_q1_kernel, nd);
+    void* args[] = {&d_a, &R, &m, &k, &d_taus, &d_q1, &d_red};
+    PTROM_CUDA(cudaLaunchCooperativeKernel((const void*)dev_form_q1_kernel, dim3(G), dim3(kQRT), args, 0, s));
+    PTROM_LAUNCH_CHECK();
   }
+  pinv_rows_kernel<<<(unsigned)((nd + 127) / 128), 128, 0, s>>>(d_a, nd, m_r, d_piv, d_q1, d_A);
+  PTROM_LAUNCH_CHECK();
   std::vector<double> A((size_t)m_r * nd);
-  std::vector<double> z(m_r);
-  for (long long k = 0; k < nd; ++k) {  // column k of pinv: R^{-1} (row k of Q1)^T, then P
-    for (int i = m_r - 1; i >= 0; --i) {
-      double s2 = q1[k + (size_t)i * nd];
-      for (int j = i + 1; j < m_r; ++j) s2 -= qr.a[i + (size_t)j * nd] * z[j];
-      z[i] = s2 / qr.a[i + (size_t)i * nd];
-    }
-    for (int j = 0; j < m_r; ++j) A[qr.piv[j] + (size_t)k * m_r] = z[j];
-  }
+  PTROM_CUDA(cudaMemcpyAsync(A.data(), d_A, A.size() * 8, cudaMemcpyDeviceToHost, s));
+  PTROM_CUDA(cudaStreamSynchronize(s));
   return A;
 }
 

@@ -27,7 +27,7 @@ unsigned long long rom_gnat_simulate(ptrom_ctx* ctx, const DSurrogate& s, const 
                                      double alpha, double* d_xhat_out, int* d_iters, unsigned char* d_conv);
 std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, int n_r, const double* phi_r,
                                              long long n_target, const std::vector<long long>& preseed);
-std::vector<double> offline_gnat_operator(long long n_dofs, int m_r, const double* phi_r,
+std::vector<double> offline_gnat_operator(ptrom_ctx* ctx, long long n_dofs, int m_r, const double* phi_r,
                                           const std::vector<long long>& ids);
 void offline_cluster_pod(ptrom_ctx* ctx, const DBasis& b, const double* d_gamma, long long leaf_cap, int crit_kind,
                          double crit_value, const std::vector<long long>& targets, DSurrogate& s,
@@ -515,7 +515,7 @@ int ptrom_greedy_sample_f64(ptrom_ctx* ctx, int64_t n_dofs, int64_t n_r, const d
 int ptrom_build_gnat_operator_f64(ptrom_ctx* ctx, int64_t n_dofs, int64_t m_r, const double* phi_r, int64_t n_s,
                                   const int64_t* ids, double* A) {
   return guarded(ctx, [&] {
-    const std::vector<double> a = offline_gnat_operator(n_dofs, (int)m_r, phi_r, std::vector<long long>(ids, ids + n_s));
+    const std::vector<double> a = offline_gnat_operator(ctx, n_dofs, (int)m_r, phi_r, std::vector<long long>(ids, ids + n_s));
     std::copy(a.begin(), a.end(), A);
   });
 }
