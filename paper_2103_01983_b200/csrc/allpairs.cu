@@ -835,7 +835,10 @@ void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double
   double* part;
   int chunks;
   const double dp = effective_delta(delta, form);
-  launch_allpairs_f64<false, true>(ctx, n, x, gamma, dp, t_begin, t_count, &part, &chunks);
+  if (t_begin == 0 && t_count == n && sym_velocity_applies(ctx, n))  // every target: unordered pairs
+    dev_jacobian_sym_part(ctx, n, x, gamma, dp, &part, &chunks, false);
+  else
+    launch_allpairs_f64<false, true>(ctx, n, x, gamma, dp, t_begin, t_count, &part, &chunks);
   if (inv) {
     reduce_jacobian_f64_kernel<true><<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
         t_begin, t_count, chunks, part, 3, 0, dp, dt_for_inverse / 2.0, nullptr, nullptr, nullptr, nullptr, inv,
@@ -851,6 +854,10 @@ void dev_jacobian_reserve_f64(ptrom_ctx* ctx, long long n, long long t_count) {
   if (t_count <= 0) return;
   double* part;
   int chunks;
+  if (t_count == n && sym_velocity_applies(ctx, n)) {
+    dev_jacobian_sym_part(ctx, n, nullptr, nullptr, 1.0, &part, &chunks, true);
+    return;
+  }
   g_size_only = true;
   try {
     launch_allpairs_f64<false, true>(ctx, n, nullptr, nullptr, 1.0, 0, t_count, &part, &chunks);

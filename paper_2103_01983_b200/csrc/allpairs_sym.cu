@@ -317,6 +317,215 @@ __global__ void reduce_sym_kernel(long long n, int nb, const double* __restrict_
   }
 }
 
+// ------------------------------------------------------------- Jacobian ---
+// The self-block Jacobian (inexact_kernel_jacobian, kernel.hpp:154-170) over
+// unordered pairs: its terms w·(rx ry, ry² − rx², 1) with w = Γ'/q² are even
+// in r, so pair (i, j) and pair (j, i) share q, u = 1/q, u² and the two
+// products and differ only in Γ'. Per unordered pair ~19 FP64 ops against
+// 2 × 14 one-sided. Same block decomposition as the velocity; part holds
+// (A, B, C) = Σ w·(rx ry, ry² − rx², 1) per target as [K][3][n], the layout
+// of the one-sided kernel's chunk partials (reduce_jacobian_f64_kernel).
+template <bool FAST4, bool TAIL>
+__device__ __forceinline__ void sym_pairs_jac(double px, double py, double g, bool vj, const double (&tx)[kST],
+                                              const double (&ty)[kST], const double (&gi)[kST], double dp,
+                                              double (&ja)[kST], double (&jb)[kST], double (&jc)[kST],
+                                              double& wa, double& wb, double& wc) {
+#pragma unroll
+  for (int k = 0; k < kST; k += 4) {
+    double rx[4], ry[4], q[4], u[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      rx[m] = tx[k + m] - px;
+      ry[m] = ty[k + m] - py;
+      q[m] = fma(rx[m], rx[m], fma(ry[m], ry[m], dp));
+    }
+    if (FAST4) {
+      const double p01 = q[0] * q[1], p23 = q[2] * q[3];
+      const double uP = rcp_cubic(p01 * p23);
+      const double u01 = uP * p23, u23 = uP * p01;
+      u[0] = u01 * q[1];
+      u[1] = u01 * q[0];
+      u[2] = u23 * q[3];
+      u[3] = u23 * q[2];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) u[m] = rcp_cubic(q[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const double uu = u[m] * u[m];
+      const double t1 = rx[m] * ry[m];
+      const double t2 = fma(ry[m], ry[m], -(rx[m] * rx[m]));
+      double a = g * uu;                // Γ'_j / q²: target i's weight (kernel.hpp:53-61)
+      const double b = gi[k + m] * uu;  // Γ'_i / q²: source j's weight
+      if (TAIL) a = vj ? a : 0.0;
+      ja[k + m] = fma(a, t1, ja[k + m]);
+      jb[k + m] = fma(a, t2, jb[k + m]);
+      jc[k + m] += a;
+      wa = fma(b, t1, wa);
+      wb = fma(b, t2, wb);
+      wc += b;
+    }
+  }
+}
+
+template <bool TAIL>
+__device__ void sym_item_jac(long long n, const double* __restrict__ xs, const double* __restrict__ ys,
+                             const double* __restrict__ gam, double inv2pi, double dp, long long B, int I, int J,
+                             double* __restrict__ part, long long ps, double2* sp, double* sg, double (*sj)[kSTPB][3]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i_blk = (long long)I * B, j_blk = (long long)J * B;
+  const long long j_end = min(j_blk + B, n);
+  const int passes = (int)((min(i_blk + B, n) - i_blk + kSPass - 1) / kSPass);
+  for (int pass = 0; pass < passes; ++pass) {
+    const long long i0 = i_blk + (long long)pass * kSPass;
+    double tx[kST], ty[kST], gi[kST], ja[kST], jb[kST], jc[kST];
+    bool my_ok4 = true;
+#pragma unroll
+    for (int k = 0; k < kST; ++k) {
+      const long long i = i0 + k * kSTPB + tid;
+      const bool ok = i < n;
+      tx[k] = ok ? xs[i] : 0.0;
+      ty[k] = ok ? ys[i] : 0.0;
+      gi[k] = ok ? gam[i] * inv2pi : 0.0;
+      ja[k] = jb[k] = jc[k] = 0.0;
+      my_ok4 = my_ok4 && coord_ok4(tx[k]) && coord_ok4(ty[k]);
+    }
+    // u² = 1/q² must stay normal too: the 4-way tier's q ∈ [2^-31, 2^31] keeps it in range
+    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
+    for (long long t0 = j_blk; t0 < j_end; t0 += kSTPB) {
+      const long long j = t0 + tid;
+      const bool vj = j < n;
+      const double px = vj ? xs[j] : 0.0, py = vj ? ys[j] : 0.0;
+      const double pg = vj ? gam[j] * inv2pi : 0.0;
+      sp[2 * tid - lane] = make_double2(px, py);
+      sp[2 * tid - lane + 32] = make_double2(px, py);
+      sg[2 * tid - lane] = pg;
+      sg[2 * tid - lane + 32] = pg;
+      const bool fast4 = __syncthreads_and(coord_ok4(px) && coord_ok4(py)) && targets_ok4;
+      const int cnt = (int)min((long long)kSTPB, j_end - t0);
+      for (int b0 = 0; b0 < kSTPB; b0 += 32) {
+        double wa = 0.0, wb = 0.0, wc = 0.0;
+        if (b0 < cnt) {
+          const double2* bp = sp + 2 * b0 + lane;
+          const double* bg = sg + 2 * b0 + lane;
+          const int nxt = (lane + 1) & 31;
+          auto batch = [&](auto fast_tag) {
+            constexpr bool F = decltype(fast_tag)::value;
+#pragma unroll 8
+            for (int s = 0; s < 32; ++s) {
+              const double2 p = bp[s];
+              const double g = bg[s];
+              const bool v = !TAIL || b0 + ((lane + s) & 31) < cnt;
+              sym_pairs_jac<F, TAIL>(p.x, p.y, g, v, tx, ty, gi, dp, ja, jb, jc, wa, wb, wc);
+              wa = __shfl_sync(0xffffffffu, wa, nxt);
+              wb = __shfl_sync(0xffffffffu, wb, nxt);
+              wc = __shfl_sync(0xffffffffu, wc, nxt);
+            }
+          };
+          if (fast4)
+            batch(std::true_type{});
+          else
+            batch(std::false_type{});
+        }
+        sj[warp][b0 + lane][0] = wa;
+        sj[warp][b0 + lane][1] = wb;
+        sj[warp][b0 + lane][2] = wc;
+      }
+      __syncthreads();
+      if (vj) {
+        double acc[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[c] = sj[0][tid][c];
+#pragma unroll
+          for (int w = 1; w < kSTPB / 32; ++w) acc[c] += sj[w][tid][c];
+        }
+        double* pj = part + (long long)I * 3 * ps + j;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pj[c * ps] = pass == 0 ? acc[c] : pj[c * ps] + acc[c];
+      }
+      __syncthreads();
+    }
+    double* out = part + (long long)J * 3 * ps;
+#pragma unroll
+    for (int k = 0; k < kST; ++k) {
+      const long long i = i0 + k * kSTPB + tid;
+      if (i < n) {
+        out[i] = ja[k];
+        out[ps + i] = jb[k];
+        out[2 * ps + i] = jc[k];
+      }
+    }
+  }
+}
+
+// Diagonal block: one-sided (tile_f64's Jacobian path, self pair masked).
+__device__ void diag_item_jac(long long n, const double* __restrict__ xs, const double* __restrict__ ys,
+                              const double* __restrict__ gam, double inv2pi, double dp, long long B, int I,
+                              double* __restrict__ part, long long ps, double2* sp, double* sg) {
+  constexpr int T = kST, TPB = kSTPB;
+  const int tid = threadIdx.x;
+  const long long blk = (long long)I * B, blk_end = min(blk + B, n);
+  const int passes = (int)((blk_end - blk + kSPass - 1) / kSPass);
+  for (int pass = 0; pass < passes; ++pass) {
+    const long long tile0 = blk + (long long)pass * kSPass;
+    double tx[T], ty[T], fx[T], fy[T], ja[T], jb[T], jc[T];
+    long long ti[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const long long i = tile0 + k * TPB + tid;
+      const bool ok = i < blk_end;
+      ti[k] = ok ? i : -1;
+      tx[k] = ok ? xs[i] : 0.0;
+      ty[k] = ok ? ys[i] : 0.0;
+      fx[k] = fy[k] = ja[k] = jb[k] = jc[k] = 0.0;
+    }
+    const long long tile_end = min(tile0 + (long long)kSPass, blk_end);
+    for (long long j0 = blk; j0 < blk_end; j0 += TPB) {
+      const int cnt = (int)min((long long)TPB, blk_end - j0);
+      const long long j = j0 + tid;
+      sp[tid] = make_double2(j < blk_end ? xs[j] : 0.0, j < blk_end ? ys[j] : 0.0);
+      sg[tid] = j < blk_end ? gam[j] * inv2pi : 0.0;
+      __syncthreads();
+      // the Jacobian always masks the self pair where the tile meets the diagonal
+      if ((j0 < tile_end) && (tile0 < j0 + cnt))
+        tile_f64<T, 2, false, true, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      else
+        tile_f64<T, 2, false, true, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+      __syncthreads();
+    }
+    double* out = part + (long long)I * 3 * ps;
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+      if (ti[k] >= 0) {
+        out[ti[k]] = ja[k];
+        out[ps + ti[k]] = jb[k];
+        out[2 * ps + ti[k]] = jc[k];
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kSTPB, 3) allpairs_sym_jac_kernel(long long n, const double* __restrict__ xs,
+                                                                    const double* __restrict__ ys,
+                                                                    const double* __restrict__ gam, double inv2pi,
+                                                                    double dp, long long B, double* __restrict__ part,
+                                                                    long long ps) {
+  __shared__ double2 sp[2 * kSTPB];
+  __shared__ double sg[2 * kSTPB];
+  __shared__ double sj[kSTPB / 32][kSTPB][3];
+  int I, J;
+  decode_pair(blockIdx.x, I, J);
+  if (I == J) {
+    diag_item_jac(n, xs, ys, gam, inv2pi, dp, B, I, part, ps, sp, sg);
+    return;
+  }
+  if ((long long)(J + 1) * B > n)
+    sym_item_jac<true>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, ps, sp, sg, sj);
+  else
+    sym_item_jac<false>(n, xs, ys, gam, inv2pi, dp, B, I, J, part, ps, sp, sg, sj);
+}
+
 // ----------------------------------------------------------------- fp32 ---
 // The same unordered-pair decomposition at S = float (kernel.hpp:107-129
 // instantiated for float): fp32 pair arithmetic, four targets sharing one
@@ -657,6 +866,35 @@ void dev_velocity_sym_f32(ptrom_ctx* ctx, long long n, const float* x, const flo
   const long long rg = std::min<long long>((n + 255) / 256, (long long)ctx->num_sms * 8);
   reduce_sym_f32_kernel<<<(unsigned)std::max<long long>(rg, 1), 256, 0, ctx->stream>>>(n, (int)nb, part, inflow, f,
                                                                                       ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
+static int sym_jac_occupancy() {
+  static int occ = [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, allpairs_sym_jac_kernel, kSTPB, 0);
+    return std::max(o, 1);
+  }();
+  return occ;
+}
+
+// The Jacobian's (A, B, C) partials over unordered pairs into the context
+// scratch ([nb][3][n]); size_only sizes the scratch without launching (before
+// a graph capture).
+void dev_jacobian_sym_part(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
+                           double** part_out, int* nb_out, bool size_only) {
+  const long long B = choose_sym_block(n, ctx->num_sms * sym_jac_occupancy(), 1);
+  const long long nb = (n + B - 1) / B;
+  const long long items = nb * (nb + 1) / 2;
+  ctx->scratch.reset();
+  ctx->scratch.reserve((size_t)nb * 3 * n * sizeof(double) + 4096);
+  double* part = ctx->scratch.take<double>((size_t)nb * 3 * n);
+  *part_out = part;
+  *nb_out = (int)nb;
+  if (size_only) return;
+  ProfScope prof(ctx);
+  allpairs_sym_jac_kernel<<<(unsigned)items, kSTPB, 0, ctx->stream>>>(n, x, x + n, gamma, 1.0 / (2.0 * M_PI), dp, B,
+                                                                      part, n);
   PTROM_LAUNCH_CHECK();
 }
 

@@ -24,6 +24,10 @@ void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const do
 bool sym_sharded_applies(ptrom_ctx* ctx, long long n, int world);
 void dev_velocity_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
                                   const double* gamma, double delta, int form, const double* inflow, double* f_local);
+// The Jacobian's (A, B, C) partials over unordered pairs, [nb][3][n] in the
+// context scratch (allpairs_sym.cu); every target of a full set.
+void dev_jacobian_sym_part(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
+                           double** part_out, int* nb_out, bool size_only);
 void dev_velocity_sym_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
                           const float* inflow, float* f);
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,

@@ -336,3 +336,30 @@ def test_unordered_pair_kernel_fp32_flags_coincident_pair(pt):
     x[17], x[n + 17] = x[15000], x[n + 15000]
     with pytest.raises(pt.NumericalError):
         pt.pairwise_velocity(x, pt.ParticleSystem(np.ones(n, np.float32), np.float32(0.0)))
+
+
+@pytest.mark.parametrize("n,scale,delta,form", [(16384, 1.0, 2.5e-5, 0), (20037, 1.0, 0.3, 1),
+                                                (40000, 2.0 ** 15, 1e3, 0), (33000, 1.0, 0.004, 0)])
+def test_unordered_pair_jacobian(pt, oracle, monkeypatch, n, scale, delta, form):
+    """Full-set self-block Jacobians (n ≥ 16,384) over unordered pairs
+    (allpairs_sym_jac_kernel: the even terms w·(rx ry, ry² − rx², 1) shared
+    by (i, j) and (j, i)): against the one-sided kernel (PTROM_ALLPAIRS_SYM=0)
+    and the oracle, ragged blocks, both forms, the safe tier (|x| ≥ 2^14);
+    run to run bit-identical."""
+    rng = np.random.default_rng(n + 7)
+    x = rng.uniform(-1.0, 1.0, 2 * n) * scale
+    g = rng.normal(0.0, 1.0, n) / n
+    sys_ = pt.ParticleSystem(g, delta, None, form)
+
+    def stack(j):
+        return np.stack([j.dfx_dx, j.dfx_dy, j.dfy_dx, j.dfy_dy])
+
+    got = stack(pt.inexact_kernel_jacobian(x, sys_))
+    assert np.array_equal(got, stack(pt.inexact_kernel_jacobian(x, sys_)))
+    monkeypatch.setenv("PTROM_ALLPAIRS_SYM", "0")
+    one_sided = stack(pt.inexact_kernel_jacobian(x, sys_))
+    monkeypatch.delenv("PTROM_ALLPAIRS_SYM")
+    assert rel(got, one_sided) <= FP64_TOL
+    for b in (0, n // 2, n - 600):
+        ref = oracle.inexact_kernel_jacobian(x, g, delta, form, t_begin=b, t_end=b + 600, threads=THREADS)
+        assert rel(got[:, b:b + 600], ref[:, b:b + 600]) <= FP64_TOL, b
