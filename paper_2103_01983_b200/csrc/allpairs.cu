@@ -850,6 +850,20 @@ void dev_jacobian_f64(ptrom_ctx* ctx, long long n, const double* x, const double
   PTROM_LAUNCH_CHECK();
 }
 
+void dev_jacobian_reduce_f64(ptrom_ctx* ctx, const double* part, int chunks, long long t_begin, long long t_count,
+                             double dp, double dt_for_inverse, double* jxx, double* jxy, double* jyx, double* jyy,
+                             double* inv) {
+  if (t_count <= 0) return;
+  if (inv)
+    reduce_jacobian_f64_kernel<true><<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+        t_begin, t_count, chunks, part, 3, 0, dp, dt_for_inverse / 2.0, nullptr, nullptr, nullptr, nullptr, inv,
+        ctx->d_status);
+  else
+    reduce_jacobian_f64_kernel<false><<<reduce_grid(ctx, t_count), kReduceThreads, 0, ctx->stream>>>(
+        t_begin, t_count, chunks, part, 3, 0, dp, 0.0, jxx, jxy, jyx, jyy, nullptr, ctx->d_status);
+  PTROM_LAUNCH_CHECK();
+}
+
 void dev_jacobian_reserve_f64(ptrom_ctx* ctx, long long n, long long t_count) {
   if (t_count <= 0) return;
   double* part;

@@ -510,12 +510,12 @@ __global__ void __launch_bounds__(kSTPB, 3) allpairs_sym_jac_kernel(long long n,
                                                                     const double* __restrict__ ys,
                                                                     const double* __restrict__ gam, double inv2pi,
                                                                     double dp, long long B, double* __restrict__ part,
-                                                                    long long ps) {
+                                                                    long long ps, long long k0) {
   __shared__ double2 sp[2 * kSTPB];
   __shared__ double sg[2 * kSTPB];
   __shared__ double sj[kSTPB / 32][kSTPB][3];
   int I, J;
-  decode_pair(blockIdx.x, I, J);
+  decode_pair(k0 + blockIdx.x, I, J);
   if (I == J) {
     diag_item_jac(n, xs, ys, gam, inv2pi, dp, B, I, part, ps, sp, sg);
     return;
@@ -894,8 +894,39 @@ void dev_jacobian_sym_part(ptrom_ctx* ctx, long long n, const double* x, const d
   if (size_only) return;
   ProfScope prof(ctx);
   allpairs_sym_jac_kernel<<<(unsigned)items, kSTPB, 0, ctx->stream>>>(n, x, x + n, gamma, 1.0 / (2.0 * M_PI), dp, B,
-                                                                      part, n);
+                                                                      part, n, 0);
   PTROM_LAUNCH_CHECK();
+}
+
+// Sharded: rank r computes its contiguous share of the block pairs into a
+// zeroed [nb][3][n] buffer, one reduce-scatter hands it the partial rows of
+// its own targets (one non-zero contributor per element: exact), and the
+// one-sided reduction forms the Newton blocks of rows [r·n/G, (r+1)·n/G):
+// bit-identical to the single-GPU evaluation's rows.
+void dev_jacobian_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
+                                  const double* gamma, double delta, int form, double dt_for_inverse,
+                                  double* inv_local) {
+  const int G = comm->world;
+  const long long B = choose_sym_block(n, ctx->num_sms * sym_jac_occupancy(), G);
+  const long long nb = (n + B - 1) / B;
+  const long long items = nb * (nb + 1) / 2;
+  const long long m = n / G;
+  const double dp = effective_delta(delta, form);
+  ctx->scratch.reset();
+  ctx->scratch.reserve(((size_t)nb * 3 * n + (size_t)nb * 3 * m) * sizeof(double) + 8192);
+  double* part = ctx->scratch.take<double>((size_t)nb * 3 * n);
+  double* mine = ctx->scratch.take<double>((size_t)nb * 3 * m);
+  PTROM_CUDA(cudaMemsetAsync(part, 0, (size_t)nb * 3 * n * sizeof(double), ctx->stream));
+  const long long k_lo = items * comm->rank / G, k_hi = items * (comm->rank + 1) / G;
+  if (k_hi > k_lo) {
+    ProfScope prof(ctx);
+    allpairs_sym_jac_kernel<<<(unsigned)(k_hi - k_lo), kSTPB, 0, ctx->stream>>>(
+        n, x_full, x_full + n, gamma, 1.0 / (2.0 * M_PI), dp, B, part, n, k_lo);
+  }
+  PTROM_LAUNCH_CHECK();
+  comm_reduce_scatter_rows(ctx, comm, part, 3 * nb, n, mine);
+  dev_jacobian_reduce_f64(ctx, mine, (int)nb, (long long)comm->rank * m, m, dp, dt_for_inverse, nullptr, nullptr,
+                          nullptr, nullptr, inv_local);
 }
 
 bool sym_sharded_applies(ptrom_ctx* ctx, long long n, int world) {

@@ -440,7 +440,10 @@ int ptrom_fom_simulate_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int64_t n, 
         }
         if (updates >= max_iters) break;
         if (refresh_due && !refreshed) {  // integrators.hpp:181-194: blocks at ξ (x_full = gathered ξ)
-          dev_jacobian_f64(ctx, n, x_full, g, delta, form, lo, hi, nullptr, nullptr, nullptr, nullptr, dt, inv);
+          if (sym)  // unordered pairs, rank share + reduce-scatter (bit-identical rows)
+            dev_jacobian_sym_sharded_f64(ctx, comm, n, x_full, g, delta, form, dt, inv);
+          else
+            dev_jacobian_f64(ctx, n, x_full, g, delta, form, lo, hi, nullptr, nullptr, nullptr, nullptr, dt, inv);
           refreshed = have_blocks = true;
         }
         if (m > 0) dev_newton_update_f64(ctx, m, m, inv, r, xi);

@@ -24,10 +24,20 @@ void dev_velocity_sym_f64(ptrom_ctx* ctx, long long n, const double* x, const do
 bool sym_sharded_applies(ptrom_ctx* ctx, long long n, int world);
 void dev_velocity_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
                                   const double* gamma, double delta, int form, const double* inflow, double* f_local);
+// The Newton blocks of this rank's rows over unordered pairs, sharded like
+// dev_velocity_sym_sharded_f64 (n divisible by the world size).
+void dev_jacobian_sym_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, long long n, const double* x_full,
+                                  const double* gamma, double delta, int form, double dt_for_inverse,
+                                  double* inv_local);
 // The Jacobian's (A, B, C) partials over unordered pairs, [nb][3][n] in the
 // context scratch (allpairs_sym.cu); every target of a full set.
 void dev_jacobian_sym_part(ptrom_ctx* ctx, long long n, const double* x, const double* gamma, double dp,
                            double** part_out, int* nb_out, bool size_only);
+// (A, B, C) partials [chunks][3][t_count] → the Jacobian rows or, with inv,
+// the Newton blocks (I − dt/2·J)⁻¹ (allpairs.cu's fixed-order reduction).
+void dev_jacobian_reduce_f64(ptrom_ctx* ctx, const double* part, int chunks, long long t_begin, long long t_count,
+                             double dp, double dt_for_inverse, double* jxx, double* jxy, double* jyx, double* jyy,
+                             double* inv);
 void dev_velocity_sym_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
                           const float* inflow, float* f);
 void dev_velocity_f32(ptrom_ctx* ctx, long long n, const float* x, const float* gamma, float delta, int form,
