@@ -394,12 +394,13 @@ std::vector<long long> offline_greedy_sample(ptrom_ctx* ctx, long long n_dofs, i
     PTROM_CUDA(cudaMallocAsync(&d_idx, n * 4, s));
     PTROM_CUDA(cudaMallocAsync(&d_idx_s, n * 4, s));
     PTROM_CUDA(cudaMallocAsync(&d_picked, n, s));
-    // device least-squares workspace (rows ≤ 2·n_target, ≤ n_r + max_ci ≤ 64 columns)
-    if (n_r + max_ci > kQRMaxCols) config_fail("greedy_sample: at most 32 residual modes");
+    // device least-squares workspace (rows ≤ 2·n_target; basis + right-hand
+    // sides nb + n_ci ≤ n_c columns)
+    if (n_c > kQRMaxCols) config_fail("greedy_sample: at most 64 working vectors (residual modes)");
     double *d_fit, *d_taus, *d_red, *d_rowj;
     long long* d_ids;
     int *d_piv, *d_rank;
-    PTROM_CUDA(cudaMallocAsync(&d_fit, (size_t)2 * n_target * (n_r + max_ci) * 8, s));
+    PTROM_CUDA(cudaMallocAsync(&d_fit, (size_t)2 * n_target * n_c * 8, s));
     PTROM_CUDA(cudaMallocAsync(&d_ids, (size_t)n_target * 8, s));
     PTROM_CUDA(cudaMallocAsync(&d_taus, kQRMaxCols * 8, s));
     PTROM_CUDA(cudaMallocAsync(&d_piv, kQRMaxCols * 4, s));
