@@ -413,7 +413,10 @@ FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x
   cudaStream_t st = ctx->stream;
   int occ = 0;
   PTROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fom_persistent_kernel, kPTPB, 0));
-  int per_sm = 4;  // CTAs per SM (tuning knob PTROM_FOM_PCTAS)
+  // CTAs per SM (tuning knob PTROM_FOM_PCTAS): 2 measured best on config 1
+  // (10.08 ms per trajectory vs 10.40 at 4, 13.2 at 1: fewer CTAs make each
+  // grid barrier cheaper, two per SM still hide the tile latency)
+  int per_sm = 2;
   if (const char* v = std::getenv("PTROM_FOM_PCTAS")) per_sm = std::max(1, std::atoi(v));
   const int grid = ctx->num_sms * std::max(1, std::min(occ, per_sm));
   PFom P{};
