@@ -1524,7 +1524,10 @@ unsigned long long rom_hyperpair(ptrom_ctx* ctx, const DSurrogate& s, const DGna
     }
     const bool off32 = (double)std::max(s.n_c, s.u) * (double)B < 4294967296.0;
     const int var = ctx->hp_variant;
-    if (et && off32 && s.n_t > 0 && var != 1) {
+    // the engine maps 32 instances to a warp: below 32 instances (the
+    // single-instance drop-in, small batches) the generic kernel's one thread
+    // per (target, instance) keeps the lanes full
+    if (et && off32 && s.n_t > 0 && var != 1 && B >= 32) {
       // batched march: hyperpair_engine_kernel (template table mode, no clamps)
       HpArgs ha{s, hg, t ? d_mu : nullptr, B, xbar, w.cxy, w.dxy, effective_delta(delta, form), d_inflow, n,
                 d_active, d_f, d_jac, w.pairs, ctx->d_status, w.sm_ctr};
