@@ -358,6 +358,13 @@ def bench_config4(args, world):
                 "flops_convention": "25 per fused velocity+Jacobian interaction (BASELINE.md §2)",
                 "hbm_view": {"algorithmic_bytes_per_launch": alg_bytes,
                              "achieved_gbs": alg_bytes / (avg_hp_ms * 1e-3) / 1e9, "peak_gbs": hbm},
+                # the bound that binds: 16-byte position gathers, one per
+                # interaction and lane, against the random-gather rate tools/gather_probe.cu
+                # measures for a working set larger than L2 (profiles/r02_gather_probe.txt)
+                "gather_view": {"gathered_bytes_per_launch": 16.0 * inter_per_launch,
+                                "achieved_tbs": 16.0 * inter_per_launch / (avg_hp_ms * 1e-3) / 1e12,
+                                "probe_tbs": 10.83, "frac": 16.0 * inter_per_launch / (avg_hp_ms * 1e-3) / 1e12 / 10.83,
+                                "probe": "tools/gather_probe.cu, 537 MB random 512-byte rows"},
                 "peak_source": "measured live: tools/peaks.cu DFMA chain"}
     e2e = {"value": units * K / wall, "unit": "instance-steps/s",
            "h2d_bytes_per_step": int(8 * B + 16 * w.n), "d2h_bytes_per_step": int(B * n_steps * (8 * basis.modes() + 5)),
