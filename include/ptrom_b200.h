@@ -431,6 +431,17 @@ int ptrom_ptrom_simulate_batch_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int
                                            int max_iters, double step_length, double* x_hat, int* iterations,
                                            uint8_t* converged, uint64_t* n_pair_evals);
 
+/* Sharded Barnes–Hut velocity (bh_velocity over integrators.hpp:83-102's
+ * BarnesHutModel: replicated build, far field split by
+ * target). Every rank passes the full state and gets the full f (2n) back,
+ * bit-identical to ptrom_barnes_hut_velocity_f64: each rank builds the same
+ * tree, evaluates tree slots [r·n/G, (r+1)·n/G), and the slot blocks are
+ * all-gathered and scattered to particle order. n_pair_evals sums the ranks. */
+int ptrom_barnes_hut_velocity_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int64_t n, const double* x,
+                                          const double* gamma, double delta, int form, int crit_kind,
+                                          double crit_value, int64_t leaf_capacity, const double* inflow, double* f,
+                                          uint64_t* n_pair_evals);
+
 /* --------------------------------------------------------- instrumentation -- */
 /* bench.py support: while enabled, the context records CUDA events on its own
  * stream around every launch of the dominant kernel of each call (the

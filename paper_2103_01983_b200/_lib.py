@@ -137,6 +137,9 @@ PROTOTYPES = {
         C.c_int, [c_ctxp, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_dp, c_dp, c_i64, c_dp,
                   c_i64, C.c_double, C.c_int, c_dp, C.c_double, c_i64, C.c_double, C.c_int, C.c_double, c_dp, c_dp,
                   c_dp, c_u64p]),
+    "ptrom_barnes_hut_velocity_sharded_f64": (
+        C.c_int, [c_ctxp, C.c_void_p, c_i64, c_dp, c_dp, C.c_double, C.c_int, C.c_int, C.c_double, c_i64, c_dp, c_dp,
+                  c_u64p]),
     "ptrom_profile_begin": (C.c_int, [c_ctxp]),
     "ptrom_profile_end": (C.c_int, [c_ctxp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

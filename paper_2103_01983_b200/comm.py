@@ -16,6 +16,9 @@ FOM and of the PTROM batch, so a C++ host can shard without Python. Here:
   (integrators.hpp:243-272 with the targets split across ranks).
 * :func:`ptrom_simulate_batch_sharded` → ``ptrom_ptrom_simulate_batch_sharded_f64``
   (rom.hpp:404-412 batched; instances split, shared tables broadcast once).
+* :func:`barnes_hut_velocity_sharded` → ``ptrom_barnes_hut_velocity_sharded_f64``
+  (BarnesHutModel velocity; replicated build, tree slots split, slot blocks
+  all-gathered).
 """
 from __future__ import annotations
 
@@ -179,6 +182,22 @@ def fom_simulate_sharded(comm: Comm, x0, system: ParticleSystem, grid: TimeGrid,
         float(grid.dt), steps, float(newton.tol), int(newton.max_iters), int(newton.jacobian_refresh_period),
         _p(snaps), _p(it), _p(cv), _p(rr), C.byref(cnt)))
     return ShardedFomResult(snaps[:steps].T.copy(), it[:steps], cv[:steps], rr[:steps], lo, hi, cnt.value)
+
+
+def barnes_hut_velocity_sharded(comm: Comm, x, system: ParticleSystem, criterion, leaf_capacity: int = 32):
+    """ptrom_barnes_hut_velocity_sharded_f64: every rank passes the full state
+    and gets the full velocity (2n) and the summed pair count."""
+    ctx = comm.ctx
+    xs = _f64(x)
+    g = _f64(system.circulation)
+    n = g.shape[0]
+    f = np.zeros(2 * n)
+    inflow = None if system.inflow is None else _f64(system.inflow)
+    cnt = C.c_uint64()
+    ctx.check(ctx.lib.ptrom_barnes_hut_velocity_sharded_f64(
+        ctx.handle, comm.handle, n, _p(xs), _p(g), float(system.delta), int(system.kernel_form),
+        int(criterion.kind), float(criterion.value), int(leaf_capacity), _p(inflow), _p(f), C.byref(cnt)))
+    return f, cnt.value
 
 
 def ptrom_simulate_batch_sharded(comm: Comm, basis, op, sur, gamma_a, gamma_b, mu, system: ParticleSystem,

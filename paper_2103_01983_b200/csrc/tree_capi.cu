@@ -4,6 +4,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "ops.cuh"
 #include "tree.cuh"
 
@@ -86,6 +87,21 @@ struct DevBuf {
     for (void* p : ptrs) cudaFreeAsync(p, s);
   }
 };
+
+// Shard blocks (slot order, x then y per rank block) back to particle order.
+__global__ void scatter_slots_kernel(long long n, int world, const int* __restrict__ perm,
+                                     const double* __restrict__ slots, double* __restrict__ f) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    // the rank block holding slot k (shard_bounds: lo_r = n·r / G)
+    int r = (int)((k * world) / n);
+    while (r > 0 && n * r / world > k) --r;
+    while (r + 1 < world && n * (r + 1) / world <= k) ++r;
+    const long long lo = n * r / world, hi = n * (r + 1) / world, m = hi - lo;
+    const long long p = perm[k];
+    f[p] = slots[2 * lo + (k - lo)];
+    f[p + n] = slots[2 * lo + m + (k - lo)];
+  }
+}
 
 }  // namespace
 
@@ -325,6 +341,67 @@ int ptrom_barnes_hut_velocity_f64(ptrom_ctx* ctx, int64_t n, const double* x, co
     t.free_all(ctx->stream);
     PTROM_CUDA(cudaMemcpyAsync(f, df, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
     check_device_status(ctx);
+  });
+}
+
+/* Sharded Barnes–Hut velocity (replicated build, far field
+ * split by target). Every rank passes the full state, builds the same tree
+ * (the build is deterministic), evaluates the contiguous tree slots
+ * [r·n/G, (r+1)·n/G), and the slot blocks are all-gathered and scattered
+ * back to particle order: every rank returns the full f (2n), bit-identical
+ * to ptrom_barnes_hut_velocity_f64. n_pair_evals is the sum over ranks. */
+int ptrom_barnes_hut_velocity_sharded_f64(ptrom_ctx* ctx, ptrom_comm* comm, int64_t n, const double* x,
+                                          const double* gamma, double delta, int form, int crit_kind,
+                                          double crit_value, int64_t leaf_capacity, const double* inflow, double* f,
+                                          uint64_t* n_pair_evals) {
+  return guarded(ctx, [&] {
+    if (!comm) config_fail("null communicator");
+    if (comm->device != ctx->device) config_fail("communicator and context are on different devices");
+    validate_eval_shape(n, form);
+    DevBuf b{ctx->stream};
+    const double* dx = b.up(x, 2 * n);
+    const double* dg = b.up(gamma, n);
+    const double* di = b.up(inflow, inflow ? 2 * n : 0);
+    validate_uploaded<double>(ctx, n, dx, dg, delta, di, "bh_velocity");
+    check_criterion(crit_kind, crit_value);
+    if (leaf_capacity < 1) config_fail("build_tree: leaf_capacity must be >= 1");
+    const int G = comm->world;
+    long long lo, hi;
+    shard_bounds(n, comm->rank, G, lo, hi);
+    double* slots = b.alloc<double>(2 * n);
+    double* df = b.alloc<double>(2 * n);
+    unsigned long long mine = 0;
+    Tree t;
+    try {
+      tree_build(ctx, t, n, dx, dx + n, dg, leaf_capacity, ctx->tree_seq_max);
+      if (hi > lo)
+        mine = tree_eval(ctx, t, dx, dg, delta, form, crit_kind, crit_value, di, nullptr, nullptr, nullptr, nullptr,
+                         nullptr, lo, hi, slots + 2 * lo);
+      std::vector<size_t> off(G), cnt(G);
+      for (int r = 0; r < G; ++r) {
+        long long l, h;
+        shard_bounds(n, r, G, l, h);
+        off[r] = (size_t)(2 * l) * 8;
+        cnt[r] = (size_t)(2 * (h - l)) * 8;
+      }
+      comm_allgatherv(ctx, comm, slots, off, cnt);
+      const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)ctx->num_sms * 8);
+      scatter_slots_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(n, G, t.perm, slots, df);
+      PTROM_LAUNCH_CHECK();
+    } catch (...) {
+      t.free_all(ctx->stream);
+      throw;
+    }
+    t.free_all(ctx->stream);
+    PTROM_CUDA(cudaMemcpyAsync(f, df, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    check_device_status(ctx);
+    if (n_pair_evals) {
+      std::vector<unsigned long long> all(G);
+      comm_allgather_host(ctx, comm, &mine, all.data(), sizeof(mine));
+      unsigned long long tot = 0;
+      for (unsigned long long v : all) tot += v;
+      *n_pair_evals = tot;
+    }
   });
 }
 

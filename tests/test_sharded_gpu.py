@@ -289,3 +289,44 @@ def test_host_transport_fom_sharded_unordered_pairs(pt, world, n):
         assert its == list(single.iterations)
     for s in range(steps):
         assert rel(full[:, s], single.snapshots[:, s]) <= 1e-12
+
+
+def _bh_worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2103_01983_b200 as pt
+        from paper_2103_01983_b200.comm import Comm, barnes_hut_velocity_sharded
+        from paper_2103_01983_b200.tree import ClusterCriterion
+        w = workloads.config3(n=n)
+        inflow = np.linspace(-0.1, 0.1, 2 * n)
+        comm = Comm.host()
+        f, cnt = barnes_hut_velocity_sharded(comm, w.x0, pt.ParticleSystem(w.gamma, w.delta, inflow),
+                                             ClusterCriterion.barnes_hut(0.5), 32)
+        comm.close()
+        if rank == 0:
+            q.put((f, cnt))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 20000), (3, 12345)])
+def test_host_transport_barnes_hut_sharded_bitwise(pt, world, n):
+    """ptrom_barnes_hut_velocity_sharded_f64: replicated
+    deterministic build, tree slots split across ranks, slot blocks all-gathered
+    and scattered back — the full velocity equals the single-GPU
+    ptrom_barnes_hut_velocity_f64 bit for bit, with the same pair count."""
+    import ctypes
+    f, cnt = _spawn(_bh_worker, world, (n,))
+    w = workloads.config3(n=n)
+    inflow = np.linspace(-0.1, 0.1, 2 * n)
+    ctx = pt.default_context()
+    single = np.zeros(2 * n)
+    c1 = ctypes.c_uint64()
+    ctx.check(ctx.lib.ptrom_barnes_hut_velocity_f64(ctx.handle, n, w.x0.ctypes.data, w.gamma.ctypes.data, w.delta, 0,
+                                                    0, 0.5, 32, inflow.ctypes.data, single.ctypes.data,
+                                                    ctypes.byref(c1)))
+    assert np.array_equal(f, single)
+    assert cnt == c1.value
