@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "ops.cuh"
@@ -30,12 +31,22 @@
 
 namespace cg = cooperative_groups;
 
+// Tile phases inlined (as separate __noinline__ functions they measured
+// 14.4 -> 17.6 us per evaluation); sources unrolled PTROM_FOM_UNR at a time.
+#ifndef PTROM_FOM_NOINLINE
+#define PTROM_FOM_NOINLINE
+#endif
+#ifndef PTROM_FOM_UNR
+#define PTROM_FOM_UNR 8
+#endif
+
 namespace ptrom {
 namespace {
 
-constexpr int kPTPB = 128;               // threads per CTA
-constexpr int kPT = 2;                   // targets per thread in a tile item
-constexpr int kPTile = kPTPB * kPT;      // targets per item
+// Threads per CTA is a template argument (128, 256 or 512; tuning knob
+// PTROM_FOM_TPB): the tile phases want ≥ 4 warps per SM sub-partition to hide
+// the FP64 latency, the grid barriers want few CTAs.
+// Targets per thread in a tile item (2 or 4; PTROM_FOM_TPT) likewise.
 constexpr long long kPersistentMaxN = 16384;
 
 struct PFom {
@@ -68,6 +79,7 @@ struct PFom {
 
 // Fixed-order block sum of one double per thread (warp shuffles, then the
 // warps in order); the result in every thread.
+template <int TPB>
 __device__ double block_sum(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
@@ -75,14 +87,14 @@ __device__ double block_sum(double v, double* red) {
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   double s = 0.0;
-  for (int w = 0; w < kPTPB / 32; ++w) s = __dadd_rn(s, red[w]);
+  for (int w = 0; w < TPB / 32; ++w) s = __dadd_rn(s, red[w]);
   return s;
 }
 
 // One tile item's partials (allpairs_f64_kernel's tile loop on SrcFlat).
-template <bool VEL, bool JAC>
-__device__ void pair_items(const PFom& P, const double* __restrict__ x, double2* sp, double* sg) {
-  constexpr int T = kPT, TPB = kPTPB, NCOMP = VEL ? 2 : 3;
+template <int TPB, int T, bool VEL, bool JAC>
+__device__ PTROM_FOM_NOINLINE void pair_items(const PFom& P, const double* __restrict__ x, double2* sp, double* sg) {
+  constexpr int kPTile = TPB * T, NCOMP = VEL ? 2 : 3;
   const double inv2pi = 1.0 / (2.0 * M_PI);
   const long long n = P.n;
   const int tid = threadIdx.x;
@@ -107,14 +119,16 @@ __device__ void pair_items(const PFom& P, const double* __restrict__ x, double2*
     const long long tile_end = min(tile0 + (long long)kPTile, n);
     const long long cbeg = (long long)chunk * P.chunk_len, cend = min(n, cbeg + P.chunk_len);
     const double dp = P.dp;
-    const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62 && dp <= 0x1p60;
-    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
+    // the first source tile's loads are issued with the target loads (one
+    // L2 round trip after the grid barrier, not two)
     double px = 0.0, py = 0.0, pg = 0.0;
     if (cbeg + tid < cend) {
       px = x[cbeg + tid];
       py = x[n + cbeg + tid];
       pg = P.g[cbeg + tid] * inv2pi;
     }
+    const bool targets_ok = __syncthreads_and(my_ok) && dp >= 0x1p-62 && dp <= 0x1p60;
+    const bool targets_ok4 = __syncthreads_and(my_ok4) && dp >= 0x1p-31 && dp <= 0x1p29;
     for (long long j0 = cbeg; j0 < cend; j0 += TPB) {
       const int cnt = (int)min((long long)TPB, cend - j0);
       sp[tid] = make_double2(px, py);
@@ -129,11 +143,11 @@ __device__ void pair_items(const PFom& P, const double* __restrict__ x, double2*
       }
       const bool masked = (j0 < tile_end) && (tile0 < j0 + cnt) && (JAC || !fast);
       if (masked)
-        tile_f64<T, 4, VEL, JAC, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+        tile_f64<T, PTROM_FOM_UNR, VEL, JAC, true, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
       else if (fast)
-        tile_f64<T, 4, VEL, JAC, false, 2>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+        tile_f64<T, PTROM_FOM_UNR, VEL, JAC, false, 2>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
       else
-        tile_f64<T, 4, VEL, JAC, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
+        tile_f64<T, PTROM_FOM_UNR, VEL, JAC, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
       __syncthreads();
     }
     double* out = P.part + (long long)chunk * NCOMP * n;
@@ -155,13 +169,19 @@ __device__ void pair_items(const PFom& P, const double* __restrict__ x, double2*
 // [velocity chunk reduction →] residual r = ξ − x_prev − h(f_ξ + f_prev)
 // (integrators.hpp:47-53) → ‖r‖ (every CTA, same fixed order). One fixed
 // thread→target mapping for every per-target phase.
+template <int TPB>
 __device__ double residual_norm(const PFom& P, bool with_velocity, int parity, double* red, cg::grid_group& grid) {
   const long long n = P.n;
   const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
   double acc = 0.0;
   for (long long i = g0; i < n; i += gs) {
+    // the thread's own state is loaded together with the chunk partials (one
+    // L2 round trip; f_ξ stays in registers instead of being stored and re-read)
+    const double xi0 = P.xi[i], xi1 = P.xi[n + i], xp0 = P.xp[i], xp1 = P.xp[n + i];
+    const double fp0 = P.fp[i], fp1 = P.fp[n + i];
+    double sx, sy;
     if (with_velocity) {  // chunk partials in ascending chunk order (fixed), + inflow
-      double sx = 0.0, sy = 0.0;
+      sx = sy = 0.0;
       int c = 0;
       for (; c + 16 <= P.nch; c += 16) {  // 16 chunks loaded ahead of their adds
         double vx[16], vy[16];
@@ -187,17 +207,19 @@ __device__ double residual_norm(const PFom& P, bool with_velocity, int parity, d
       if (!isfinite(sx) || !isfinite(sy)) latch_status(P.st, kStatusNonFiniteVelocity, i);
       P.fxi[i] = sx;
       P.fxi[n + i] = sy;
+    } else {
+      sx = P.fxi[i];
+      sy = P.fxi[n + i];
     }
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const long long k = i + half * n;
-      const double v = __dsub_rn(__dsub_rn(P.xi[k], P.xp[k]), __dmul_rn(P.h, __dadd_rn(P.fxi[k], P.fp[k])));
-      P.r[k] = v;
-      acc = __dadd_rn(acc, __dmul_rn(v, v));
-    }
+    const double v0 = __dsub_rn(__dsub_rn(xi0, xp0), __dmul_rn(P.h, __dadd_rn(sx, fp0)));
+    const double v1 = __dsub_rn(__dsub_rn(xi1, xp1), __dmul_rn(P.h, __dadd_rn(sy, fp1)));
+    P.r[i] = v0;
+    P.r[n + i] = v1;
+    acc = __dadd_rn(acc, __dmul_rn(v0, v0));
+    acc = __dadd_rn(acc, __dmul_rn(v1, v1));
   }
   double* bp = P.block_part + (long long)parity * gridDim.x;
-  const double s = block_sum(acc, red);
+  const double s = block_sum<TPB>(acc, red);
   if (threadIdx.x == 0) bp[blockIdx.x] = s;
   grid.sync();
   // every CTA: the same partials in the same order; only the CTAs that own
@@ -294,17 +316,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
     t_last = t_;                                            \
   }
 
-__global__ void __launch_bounds__(kPTPB) fom_persistent_kernel(PFom P) {
+template <int TPB, int T>
+__global__ void __launch_bounds__(TPB) fom_persistent_kernel(PFom P) {
   unsigned long long t_last = P.prof ? gtimer() : 0;
   cg::grid_group grid = cg::this_grid();
-  __shared__ double2 sp[kPTPB];
-  __shared__ double sg[kPTPB];
-  __shared__ double red[kPTPB / 32];
+  __shared__ double2 sp[TPB];
+  __shared__ double sg[TPB];
+  __shared__ double red[TPB / 32];
   const long long n = P.n;
   const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   // f = velocity(x0) (integrators.hpp:257-259); ξ = x_prev, f_ξ = f_prev
-  pair_items<true, false>(P, P.xp, sp, sg);
+  pair_items<TPB, T, true, false>(P, P.xp, sp, sg);
   grid.sync();
   for (long long i = g0; i < n; i += gs) {
     double sx = 0.0, sy = 0.0;
@@ -330,7 +353,7 @@ __global__ void __launch_bounds__(kPTPB) fom_persistent_kernel(PFom P) {
     bool refreshed = false, converged = false;
     int updates = 0;
     double r0 = 0.0, rel = 0.0;
-    double nr = residual_norm(P, false, parity, red, grid);  // f_ξ = f_prev: no evaluation
+    double nr = residual_norm<TPB>(P, false, parity, red, grid);  // f_ξ = f_prev: no evaluation
     parity ^= 1;
     while (true) {  // integrators.hpp:140-178
       if (updates == 0) {
@@ -349,7 +372,7 @@ __global__ void __launch_bounds__(kPTPB) fom_persistent_kernel(PFom P) {
       if (updates >= P.max_iters) break;
       PF_MARK(7);
       if (refresh_due && !refreshed) {
-        pair_items<false, true>(P, P.xi, sp, sg);
+        pair_items<TPB, T, false, true>(P, P.xi, sp, sg);
         PF_MARK(3);
         grid.sync();
         PF_MARK(4);
@@ -362,12 +385,18 @@ __global__ void __launch_bounds__(kPTPB) fom_persistent_kernel(PFom P) {
       PF_MARK(5);
       grid.sync();  // every ξ updated before any tile reads the sources
       PF_MARK(6);
-      pair_items<true, false>(P, P.xi, sp, sg);
+      const unsigned long long tc0 = (P.prof && threadIdx.x == 0) ? gtimer() : 0;
+      pair_items<TPB, T, true, false>(P, P.xi, sp, sg);
       ++evals;
       PF_MARK(0);
+      const unsigned long long tc1 = (P.prof && threadIdx.x == 0) ? gtimer() : 0;
       grid.sync();
       PF_MARK(1);
-      nr = residual_norm(P, true, parity, red, grid);
+      if (P.prof && threadIdx.x == 0) {  // per-CTA view: own tile time, own wait in the barrier
+        P.prof[8 + blockIdx.x] += tc1 - tc0;
+        P.prof[8 + gridDim.x + blockIdx.x] += gtimer() - tc1;
+      }
+      nr = residual_norm<TPB>(P, true, parity, red, grid);
       parity ^= 1;
       PF_MARK(2);
     }
@@ -411,14 +440,32 @@ FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x
                                   double tol, int max_iters, int refresh, double* snapshots_out, int* iters,
                                   unsigned char* conv, double* rel_out) {
   cudaStream_t st = ctx->stream;
-  int occ = 0;
-  PTROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fom_persistent_kernel, kPTPB, 0));
-  // CTAs per SM (tuning knob PTROM_FOM_PCTAS): 2 measured best on config 1
-  // (10.08 ms per trajectory vs 10.40 at 4, 13.2 at 1: fewer CTAs make each
-  // grid barrier cheaper, two per SM still hide the tile latency)
-  int per_sm = 2;
+  // CTA shape (tuning knobs PTROM_FOM_TPB x PTROM_FOM_PCTAS x PTROM_FOM_TPT:
+  // threads per CTA, CTAs per SM, targets per thread). Every phase ends in a
+  // grid barrier whose cost grows with the CTA count (1.5 us at 148 CTAs, the
+  // slowest CTA waits on), and the tile phase wants warps: 256 x 1 x 2
+  // measured 9.29 ms per config-1 trajectory, 128 x 2 x 2 10.06, 512 x 1 x 2
+  // 9.76 (37 source chunks to reduce instead of 18), 128 x 4 x 2 10.31
+  // (profiles/r02_fom_shape_sweep.txt).
+  int tpb = 256, per_sm = 1, tpt = 2;
+  if (const char* v = std::getenv("PTROM_FOM_TPB")) tpb = std::atoi(v);
+  if (tpb != 128 && tpb != 256 && tpb != 512) tpb = 256;
+  if (const char* v = std::getenv("PTROM_FOM_TPT")) tpt = std::atoi(v);
+  if (tpt != 1 && tpt != 2 && tpt != 4) tpt = 2;
   if (const char* v = std::getenv("PTROM_FOM_PCTAS")) per_sm = std::max(1, std::atoi(v));
+  auto pick = [&](auto t) -> const void* {
+    constexpr int T = decltype(t)::value;
+    return tpb == 512   ? (const void*)fom_persistent_kernel<512, T>
+           : tpb == 256 ? (const void*)fom_persistent_kernel<256, T>
+                        : (const void*)fom_persistent_kernel<128, T>;
+  };
+  const void* kernel = tpt == 4   ? pick(std::integral_constant<int, 4>{})
+                       : tpt == 1 ? pick(std::integral_constant<int, 1>{})
+                                  : pick(std::integral_constant<int, 2>{});
+  int occ = 0;
+  PTROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, tpb, 0));
   const int grid = ctx->num_sms * std::max(1, std::min(occ, per_sm));
+  const int kPTile = tpb * tpt;
   PFom P{};
   P.n = n;
   P.g = d_gamma;
@@ -464,12 +511,12 @@ FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x
   P.counters = (long long*)alloc(16);
   const bool prof = std::getenv("PTROM_FOM_PROFILE") != nullptr;
   if (prof) {
-    P.prof = (unsigned long long*)alloc(64);
-    PTROM_CUDA(cudaMemsetAsync(P.prof, 0, 64, st));
+    P.prof = (unsigned long long*)alloc(64 + 16 * (size_t)grid);
+    PTROM_CUDA(cudaMemsetAsync(P.prof, 0, 64 + 16 * (size_t)grid, st));
   }
   PTROM_CUDA(cudaMemcpyAsync(P.xp, d_x0, dim * 8, cudaMemcpyDeviceToDevice, st));
   void* args[] = {&P};
-  PTROM_CUDA(cudaLaunchCooperativeKernel((const void*)fom_persistent_kernel, dim3(grid), dim3(kPTPB), args, 0, st));
+  PTROM_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(tpb), args, 0, st));
   PTROM_LAUNCH_CHECK();
   long long cnt[2] = {0, 0};
   if (n_steps > 0) {
@@ -481,13 +528,26 @@ FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x
   }
   PTROM_CUDA(cudaMemcpyAsync(cnt, P.counters, 16, cudaMemcpyDeviceToHost, st));
   unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (prof) PTROM_CUDA(cudaMemcpyAsync(pr, P.prof, 64, cudaMemcpyDeviceToHost, st));
+  std::vector<unsigned long long> pc(prof ? 2 * (size_t)grid : 0);
+  if (prof) {
+    PTROM_CUDA(cudaMemcpyAsync(pr, P.prof, 64, cudaMemcpyDeviceToHost, st));
+    PTROM_CUDA(cudaMemcpyAsync(pc.data(), P.prof + 8, 16 * (size_t)grid, cudaMemcpyDeviceToHost, st));
+  }
   PTROM_CUDA(cudaStreamSynchronize(st));
   if (prof)
-    fprintf(stderr, "fom_persistent grid %d nch %d: vel %.3f ms, sync %.3f, reduce+norm %.3f, jac %.3f, sync %.3f, "
+    fprintf(stderr, "fom_persistent grid %d x %d x %d nch %d: vel %.3f ms, sync %.3f, reduce+norm %.3f, jac %.3f, sync %.3f, "
                     "blocks+update %.3f, sync %.3f, other %.3f\n",
-            grid, P.nch, pr[0] * 1e-6, pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6, pr[4] * 1e-6, pr[5] * 1e-6,
+            grid, tpb, tpt, P.nch, pr[0] * 1e-6, pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6, pr[4] * 1e-6, pr[5] * 1e-6,
             pr[6] * 1e-6, pr[7] * 1e-6);
+  if (prof) {  // velocity phase per CTA: tile time (min / median / max) and the smallest barrier wait
+    std::vector<unsigned long long> a(pc.begin(), pc.begin() + grid), w(pc.begin() + grid, pc.end());
+    std::sort(a.begin(), a.end());
+    std::sort(w.begin(), w.end());
+    const double per = 1e-3 / std::max<long long>(cnt[0] - 1, 1);
+    fprintf(stderr, "  velocity phase per evaluation, per CTA: tiles min %.2f / median %.2f / max %.2f us; barrier wait min "
+                    "%.2f / median %.2f / max %.2f us\n",
+            a.front() * per, a[grid / 2] * per, a.back() * per, w.front() * per, w[grid / 2] * per, w.back() * per);
+  }
   check_device_status(ctx);
   FomResult out;
   out.velocity_evals = cnt[0];
