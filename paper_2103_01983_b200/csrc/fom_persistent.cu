@@ -6,17 +6,32 @@
 // pairs each, which as separate launches are bound by launch latency and
 // graph-node overhead, not by the FP64 pipe).
 //
-// Work of one evaluation: items = target tiles (256 targets: 128 threads x 2
-// in registers) x source chunks, taken grid-stride by the resident CTAs, each
-// writing its partials part[chunk][comp][target] (the same tile arithmetic as
-// allpairs.cu, pair_tile.cuh). Between phases a grid barrier; per-target
-// phases (chunk reduction, residual, Newton blocks, update, record) use one
-// fixed thread→target mapping, so they need no barrier among themselves.
+// Work of one evaluation: items = target tiles (TPB threads x T targets in
+// registers; 256 x 2 by default) x source chunks, taken grid-stride by the
+// resident CTAs, each writing its partials part[chunk][comp][target] (the
+// same tile arithmetic as allpairs.cu, pair_tile.cuh). Between phases a grid
+// barrier; per-target phases (chunk reduction, residual, Newton blocks,
+// update, record) use one fixed thread→target mapping, so they need no
+// barrier among themselves.
 // ‖r‖: per-CTA fixed-order partials, then every CTA sums them in the same
 // fixed order, so all CTAs take the reference's decision (integrators.hpp:
 // 140-155) identically; the partials are double-buffered by call parity.
 // Residual, Newton blocks and update use the reference's rounding order
 // (_rn intrinsics), as fom.cu.
+//
+// A Newton iteration costs two grid barriers (tiles → residual + norm):
+//  * the update ξ + blocks·(−r) is formed in the residual phase into the
+//    second ξ buffer (before the norm's barrier); when the step continues the
+//    two buffers are swapped — no update phase, no third barrier;
+//  * a step's Jacobian point is the previous step's accepted ξ, whose
+//    velocity was that step's last evaluation: the evaluation expected to be
+//    the last (the previous step's update count) forms the (A, B, C)
+//    partials in the same tile pass (shared r, q and reciprocal), and the
+//    next step forms its Newton blocks from them before its first residual,
+//    into the second block buffer, adopted only when the refresh happens
+//    (the reference refreshes inside the loop, after the r0 == 0 exit). A
+//    wrong guess costs one separate Jacobian pass, never a different result
+//    path: decisions, counters and error latches are the reference's.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -58,10 +73,13 @@ struct PFom {
   double* xp;            // x_prev (2n); holds x0 on entry
   double* fp;            // f_prev (2n)
   double* xi;            // ξ
+  double* xi2;           // the other ξ buffer (speculative Newton update, swapped in)
   double* fxi;           // f_ξ
   double* r;             // residual
   double* inv;           // 4n Newton blocks
-  double* part;          // [nch][3][n]
+  double* inv2;          // blocks formed ahead of the refresh that adopts them (swapped in)
+  double* part;          // [nch][2][n] velocity partials
+  double* part_j;        // [nch][3][n] Jacobian (A, B, C) partials
   double* block_part;    // [2][gridDim] per-CTA partial ‖r‖² (double-buffered by parity)
   double* snaps;         // 2n x n_steps
   int* iters;
@@ -94,7 +112,7 @@ __device__ double block_sum(double v, double* red) {
 // One tile item's partials (allpairs_f64_kernel's tile loop on SrcFlat).
 template <int TPB, int T, bool VEL, bool JAC>
 __device__ PTROM_FOM_NOINLINE void pair_items(const PFom& P, const double* __restrict__ x, double2* sp, double* sg) {
-  constexpr int kPTile = TPB * T, NCOMP = VEL ? 2 : 3;
+  constexpr int kPTile = TPB * T;
   const double inv2pi = 1.0 / (2.0 * M_PI);
   const long long n = P.n;
   const int tid = threadIdx.x;
@@ -150,17 +168,19 @@ __device__ PTROM_FOM_NOINLINE void pair_items(const PFom& P, const double* __res
         tile_f64<T, PTROM_FOM_UNR, VEL, JAC, false, 0>(cnt, sp, sg, j0, tx, ty, ti, dp, fx, fy, ja, jb, jc);
       __syncthreads();
     }
-    double* out = P.part + (long long)chunk * NCOMP * n;
+    double* out = P.part + (long long)chunk * 2 * n;
+    double* outj = P.part_j + (long long)chunk * 3 * n;
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       if (ti[k] < 0) continue;
       if (VEL) {
         out[ti[k]] = fx[k];
         out[n + ti[k]] = fy[k];
-      } else {
-        out[ti[k]] = ja[k];
-        out[n + ti[k]] = jb[k];
-        out[2 * n + ti[k]] = jc[k];
+      }
+      if (JAC) {
+        outj[ti[k]] = ja[k];
+        outj[n + ti[k]] = jb[k];
+        outj[2 * n + ti[k]] = jc[k];
       }
     }
   }
@@ -169,16 +189,29 @@ __device__ PTROM_FOM_NOINLINE void pair_items(const PFom& P, const double* __res
 // [velocity chunk reduction →] residual r = ξ − x_prev − h(f_ξ + f_prev)
 // (integrators.hpp:47-53) → ‖r‖ (every CTA, same fixed order). One fixed
 // thread→target mapping for every per-target phase.
+// With spec_out, the Newton update ξ + blocks·(−r) this residual would lead to
+// (newton_update's arithmetic, the current blocks) is also written to spec_out:
+// if the step continues, the kernel swaps the two ξ buffers instead of running
+// an update phase and its grid barrier.
 template <int TPB>
-__device__ double residual_norm(const PFom& P, bool with_velocity, int parity, double* red, cg::grid_group& grid) {
+__device__ double residual_norm(const PFom& P, const double* xi, double* spec_out, const double* blocks,
+                                bool with_velocity, int parity, double* red, cg::grid_group& grid) {
   const long long n = P.n;
   const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
   double acc = 0.0;
   for (long long i = g0; i < n; i += gs) {
     // the thread's own state is loaded together with the chunk partials (one
     // L2 round trip; f_ξ stays in registers instead of being stored and re-read)
-    const double xi0 = P.xi[i], xi1 = P.xi[n + i], xp0 = P.xp[i], xp1 = P.xp[n + i];
+    const double xi0 = xi[i], xi1 = xi[n + i], xp0 = P.xp[i], xp1 = P.xp[n + i];
     const double fp0 = P.fp[i], fp1 = P.fp[n + i];
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+    if (spec_out) {
+      const double* b = blocks + 4 * i;
+      b0 = b[0];
+      b1 = b[1];
+      b2 = b[2];
+      b3 = b[3];
+    }
     double sx, sy;
     if (with_velocity) {  // chunk partials in ascending chunk order (fixed), + inflow
       sx = sy = 0.0;
@@ -217,6 +250,13 @@ __device__ double residual_norm(const PFom& P, bool with_velocity, int parity, d
     P.r[n + i] = v1;
     acc = __dadd_rn(acc, __dmul_rn(v0, v0));
     acc = __dadd_rn(acc, __dmul_rn(v1, v1));
+    if (spec_out) {  // newton_update's arithmetic
+      const double rhs0 = -v0, rhs1 = -v1;
+      const double d0 = __dadd_rn(__dmul_rn(b0, rhs0), __dmul_rn(b1, rhs1));
+      const double d1 = __dadd_rn(__dmul_rn(b2, rhs0), __dmul_rn(b3, rhs1));
+      spec_out[i] = __dadd_rn(xi0, d0);
+      spec_out[n + i] = __dadd_rn(xi1, d1);
+    }
   }
   double* bp = P.block_part + (long long)parity * gridDim.x;
   const double s = block_sum<TPB>(acc, red);
@@ -242,7 +282,11 @@ __device__ double residual_norm(const PFom& P, bool with_velocity, int parity, d
 
 // Newton blocks (I − h·J)^-1 at ξ from the Jacobian partials
 // (integrators.hpp:181-194, reduce_jacobian_f64_kernel<true>'s rounding).
-__device__ void newton_blocks(const PFom& P) {
+// Returns the thread's first singular block (or -1); latched at once unless
+// the blocks are formed ahead of a refresh that may not happen (the caller
+// latches when it adopts them).
+__device__ long long newton_blocks(const PFom& P, double* inv, bool latch) {
+  long long first_singular = -1;
   const long long n = P.n;
   const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
   for (long long i = g0; i < n; i += gs) {
@@ -252,7 +296,7 @@ __device__ void newton_blocks(const PFom& P) {
       double va[8], vb[8], vc[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const double* pc = P.part + (long long)(ch + u) * 3 * n + i;
+        const double* pc = P.part_j + (long long)(ch + u) * 3 * n + i;
         va[u] = __ldcg(pc);
         vb[u] = __ldcg(pc + n);
         vc[u] = __ldcg(pc + 2 * n);
@@ -265,7 +309,7 @@ __device__ void newton_blocks(const PFom& P) {
       }
     }
     for (; ch < P.nch; ++ch) {
-      const double* pc = P.part + (long long)ch * 3 * n + i;
+      const double* pc = P.part_j + (long long)ch * 3 * n + i;
       a += __ldcg(pc);
       b += __ldcg(pc + n);
       c += __ldcg(pc + 2 * n);
@@ -277,26 +321,30 @@ __device__ void newton_blocks(const PFom& P) {
     const double b10 = __dsub_rn(0.0, __dmul_rn(P.h, j10));
     const double b11 = __dsub_rn(1.0, __dmul_rn(P.h, j11));
     const double det = __dsub_rn(__dmul_rn(b00, b11), __dmul_rn(b01, b10));
-    if (det == 0.0 || !isfinite(det)) latch_status(P.st, kStatusSingularBlock, i);
-    double* o = P.inv + 4 * i;
+    if (det == 0.0 || !isfinite(det)) {
+      if (latch) latch_status(P.st, kStatusSingularBlock, i);
+      if (first_singular < 0) first_singular = i;
+    }
+    double* o = inv + 4 * i;
     o[0] = __ddiv_rn(b11, det);
     o[1] = __ddiv_rn(-b01, det);
     o[2] = __ddiv_rn(-b10, det);
     o[3] = __ddiv_rn(b00, det);
   }
+  return first_singular;
 }
 
 // ξ += blocks · (−r) (integrators.hpp:161-167, newton_update_kernel's rounding).
-__device__ void newton_update(const PFom& P) {
+__device__ void newton_update(const PFom& P, const double* inv, double* xi) {
   const long long n = P.n;
   const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
   for (long long i = g0; i < n; i += gs) {
-    const double* b = P.inv + 4 * i;
+    const double* b = inv + 4 * i;
     const double rhs0 = -P.r[i], rhs1 = -P.r[n + i];
     const double d0 = __dadd_rn(__dmul_rn(b[0], rhs0), __dmul_rn(b[1], rhs1));
     const double d1 = __dadd_rn(__dmul_rn(b[2], rhs0), __dmul_rn(b[3], rhs1));
-    P.xi[i] = __dadd_rn(P.xi[i], d0);
-    P.xi[n + i] = __dadd_rn(P.xi[n + i], d1);
+    xi[i] = __dadd_rn(xi[i], d0);
+    xi[n + i] = __dadd_rn(xi[n + i], d1);
   }
 }
 
@@ -326,8 +374,14 @@ __global__ void __launch_bounds__(TPB) fom_persistent_kernel(PFom P) {
   const long long n = P.n;
   const long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  // f = velocity(x0) (integrators.hpp:257-259); ξ = x_prev, f_ξ = f_prev
-  pair_items<TPB, T, true, false>(P, P.xp, sp, sg);
+  double* xi = P.xi;    // the current iterate
+  double* xi2 = P.xi2;  // the speculative next iterate (swapped in when the step continues)
+  double* inv = P.inv;  // the Newton blocks in use / the buffer early refreshes are formed into
+  double* inv2 = P.inv2;
+  // f = velocity(x0) (integrators.hpp:257-259); ξ = x_prev, f_ξ = f_prev. The
+  // first step's Jacobian point is x0 too: both in one tile pass.
+  pair_items<TPB, T, true, true>(P, P.xp, sp, sg);
+  bool jac_ready = true;  // part_j holds the Jacobian partials at the current ξ
   grid.sync();
   for (long long i = g0; i < n; i += gs) {
     double sx = 0.0, sy = 0.0;
@@ -342,18 +396,28 @@ __global__ void __launch_bounds__(TPB) fom_persistent_kernel(PFom P) {
     if (!isfinite(sx) || !isfinite(sy)) latch_status(P.st, kStatusNonFiniteVelocity, i);
     P.fp[i] = P.fxi[i] = sx;
     P.fp[n + i] = P.fxi[n + i] = sy;
-    P.xi[i] = P.xp[i];
-    P.xi[n + i] = P.xp[n + i];
+    xi[i] = P.xp[i];
+    xi[n + i] = P.xp[n + i];
   }
   long long evals = 1, jevals = 0;
   int parity = 0;
   bool have_blocks = false;
+  int predicted = -1;  // the previous step's update count: its last evaluation is the next Jacobian point
   for (long long s = 0; s < P.n_steps; ++s) {
     const bool refresh_due = (s % P.refresh) == 0 || !have_blocks;
+    const bool next_refresh = s + 1 < P.n_steps && ((s + 1) % P.refresh) == 0;
     bool refreshed = false, converged = false;
     int updates = 0;
     double r0 = 0.0, rel = 0.0;
-    double nr = residual_norm<TPB>(P, false, parity, red, grid);  // f_ξ = f_prev: no evaluation
+    // f_ξ = f_prev: no evaluation. The update is formed speculatively with the
+    // blocks the step's first update will use: the current ones, or — when a
+    // refresh is due and the Jacobian partials at this ξ are ready — the new
+    // blocks, formed into the second buffer and adopted only if the refresh
+    // happens (a step that converges at once leaves the old blocks in place).
+    const bool early_blocks = refresh_due && jac_ready;
+    const long long early_singular = early_blocks ? newton_blocks(P, inv2, false) : -1;
+    bool spec = early_blocks || (have_blocks && !refresh_due);
+    double nr = residual_norm<TPB>(P, xi, spec ? xi2 : nullptr, early_blocks ? inv2 : inv, false, parity, red, grid);
     parity ^= 1;
     while (true) {  // integrators.hpp:140-178
       if (updates == 0) {
@@ -372,21 +436,44 @@ __global__ void __launch_bounds__(TPB) fom_persistent_kernel(PFom P) {
       if (updates >= P.max_iters) break;
       PF_MARK(7);
       if (refresh_due && !refreshed) {
-        pair_items<TPB, T, false, true>(P, P.xi, sp, sg);
-        PF_MARK(3);
-        grid.sync();
-        PF_MARK(4);
-        newton_blocks(P);  // same thread→target mapping as the update below
+        if (early_blocks) {  // formed before the residual: adopt them
+          double* t = inv;
+          inv = inv2;
+          inv2 = t;
+          if (early_singular >= 0) latch_status(P.st, kStatusSingularBlock, early_singular);
+        } else {  // Jacobian not evaluated together with the velocity at this ξ
+          pair_items<TPB, T, false, true>(P, xi, sp, sg);
+          PF_MARK(3);
+          grid.sync();
+          PF_MARK(4);
+          newton_blocks(P, inv, true);  // same thread→target mapping as the update below
+          spec = false;           // no speculative update with these blocks
+        }
         refreshed = have_blocks = true;
         ++jevals;
       }
-      newton_update(P);
+      if (spec) {  // ξ ← the update formed with the residual (stored before the norm's grid barrier)
+        double* t = xi;
+        xi = xi2;
+        xi2 = t;
+        PF_MARK(5);
+      } else {
+        newton_update(P, inv, xi);
+        PF_MARK(5);
+        grid.sync();  // every ξ updated before any tile reads the sources
+        PF_MARK(6);
+      }
       ++updates;
-      PF_MARK(5);
-      grid.sync();  // every ξ updated before any tile reads the sources
-      PF_MARK(6);
+      jac_ready = false;  // ξ moved
+      // the evaluation expected to be the step's last (the previous step's
+      // update count) also forms the next step's Jacobian partials at the same ξ
+      const bool fuse = next_refresh && updates == predicted;
       const unsigned long long tc0 = (P.prof && threadIdx.x == 0) ? gtimer() : 0;
-      pair_items<TPB, T, true, false>(P, P.xi, sp, sg);
+      if (fuse)
+        pair_items<TPB, T, true, true>(P, xi, sp, sg);
+      else
+        pair_items<TPB, T, true, false>(P, xi, sp, sg);
+      jac_ready = fuse;
       ++evals;
       PF_MARK(0);
       const unsigned long long tc1 = (P.prof && threadIdx.x == 0) ? gtimer() : 0;
@@ -396,15 +483,17 @@ __global__ void __launch_bounds__(TPB) fom_persistent_kernel(PFom P) {
         P.prof[8 + blockIdx.x] += tc1 - tc0;
         P.prof[8 + gridDim.x + blockIdx.x] += gtimer() - tc1;
       }
-      nr = residual_norm<TPB>(P, true, parity, red, grid);
+      spec = true;  // blocks are current for the rest of the step
+      nr = residual_norm<TPB>(P, xi, xi2, inv, true, parity, red, grid);
       parity ^= 1;
       PF_MARK(2);
     }
+    predicted = updates;
     // the accepted state is the next step's history and initial guess
     // (integrators.hpp:262-264, 130-131), recorded as a snapshot column
     double* col = P.snaps + s * 2 * n;
     for (long long i = g0; i < n; i += gs) {
-      const double x0 = P.xi[i], x1 = P.xi[n + i];
+      const double x0 = xi[i], x1 = xi[n + i];
       col[i] = x0;
       col[n + i] = x1;
       P.xp[i] = x0;
@@ -498,10 +587,13 @@ FomResult fom_simulate_persistent(ptrom_ctx* ctx, long long n, const double* d_x
   P.xp = (double*)alloc(dim * 8);
   P.fp = (double*)alloc(dim * 8);
   P.xi = (double*)alloc(dim * 8);
+  P.xi2 = (double*)alloc(dim * 8);
   P.fxi = (double*)alloc(dim * 8);
   P.r = (double*)alloc(dim * 8);
   P.inv = (double*)alloc(4 * (size_t)n * 8);
-  P.part = (double*)alloc((size_t)P.nch * 3 * n * 8);
+  P.inv2 = (double*)alloc(4 * (size_t)n * 8);
+  P.part = (double*)alloc((size_t)P.nch * 2 * n * 8);
+  P.part_j = (double*)alloc((size_t)P.nch * 3 * n * 8);
   P.block_part = (double*)alloc(2 * (size_t)grid * 8);
   const bool own_snaps = snapshots_out == nullptr;
   P.snaps = (double*)alloc(dim * std::max<long long>(n_steps, 1) * 8);
