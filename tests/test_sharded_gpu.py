@@ -24,7 +24,7 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-def test_nccl_world1_fom_sharded_equals_single_gpu(pt, oracle):
+def test_nccl_world1_fom_sharded_equals_single_gpu(pt, oracle, monkeypatch):
     from paper_2103_01983_b200.comm import Comm, fom_simulate_sharded
     w = workloads.config1(n=1500)
     steps = 6
@@ -32,10 +32,17 @@ def test_nccl_world1_fom_sharded_equals_single_gpu(pt, oracle):
     assert comm.transport == "nccl" and comm.world == 1
     sys_ = pt.ParticleSystem(w.gamma, w.delta)
     res = fom_simulate_sharded(comm, w.x0, sys_, pt.TimeGrid(w.dt, steps))
-    single = pt.fom_simulate(w.x0, sys_, pt.TimeGrid(w.dt, steps))
     # same kernels, same fixed-order norm: bit-identical to the single-GPU graph path
+    monkeypatch.setenv("PTROM_FOM_PERSISTENT", "0")
+    single = pt.fom_simulate(w.x0, sys_, pt.TimeGrid(w.dt, steps))
+    monkeypatch.delenv("PTROM_FOM_PERSISTENT")
     assert np.array_equal(res.snapshots_local, single.snapshots)
     assert list(res.iterations) == list(single.iterations)
+    # the persistent small-system kernel (the default at this size) evaluates the
+    # step's last velocity together with the next Jacobian: same states to rounding
+    small = pt.fom_simulate(w.x0, sys_, pt.TimeGrid(w.dt, steps))
+    assert list(small.iterations) == list(single.iterations)
+    assert max(rel(small.snapshots[:, s], single.snapshots[:, s]) for s in range(steps)) <= 1e-12
     snaps, iters, _, _ = oracle.fom_simulate(w.x0, w.gamma, w.delta, w.dt, steps)
     assert max(rel(res.snapshots_local[:, s], snaps[:, s]) for s in range(steps)) <= 1e-12
     assert res.pair_evals == (1 + int(np.sum(res.iterations))) * w.n * (w.n - 1)
