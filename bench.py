@@ -492,8 +492,12 @@ def config1_line(args, K, W, local, cpu_seconds):
     peaks = measured_peaks(local)
     achieved = flops / (total_ms * 1e-3) / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_dfma_tflops"] if peaks else None,
-                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"] if peaks else None, "traffic": None,
-                "scope": "whole trajectory (launch/latency-bound at N = 4,096: ~900 small graph-launched kernels)",
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"] if peaks else None,
+                "traffic": ncu_traffic("r02_fom_persistent_ncu_summary.json"),
+                "kernel": "fom_persistent_kernel<256, 2> (csrc/fom_persistent.cu): the whole trajectory in one "
+                          "cooperative launch",
+                "scope": "whole trajectory (latency-bound at N = 4,096: two grid barriers per Newton iteration, "
+                         "148 CTAs)",
                 "flops_convention": "12 per velocity pair + 21 per Jacobian pair (BASELINE.md §2)",
                 "velocity_evals_per_trajectory": nv / K, "jacobian_evals_per_trajectory": nj / K,
                 "peak_source": "measured live: tools/peaks.cu DFMA chain"}
