@@ -103,6 +103,35 @@ def test_refresh_period_matches_oracle(pt, oracle):
     assert max(rel(run.snapshots[:, s], snaps[:, s]) for s in range(12)) <= 1e-12
 
 
+@pytest.mark.parametrize("dt,tol,max_iters,refresh,use_inflow", [
+    (2e-2, 1e-11, 100, 1, False),   # 20 → 18 updates per step: the guess of the last evaluation misses
+    (1e-2, 1e-11, 3, 2, True),      # the update cap ends every step; refresh every other step
+    (1e-3, 1e-6, 100, 4, False),    # three updates per step, stale blocks for three steps in four
+    (5e-3, 1e-10, 100, 3, True),
+])
+def test_persistent_flow_variants_match_oracle(pt, oracle, dt, tol, max_iters, refresh, use_inflow):
+    """The persistent kernel forms the update with the residual and guesses
+    which evaluation ends a step (fom_persistent.cu): update counts that
+    change between steps, capped steps and refresh periods > 1 must give the
+    reference's states, counts and flags (integrators.hpp:117-201)."""
+    w = workloads.config1(n=700, seed=9)
+    gamma = w.gamma * 10.0
+    steps = 14
+    inflow = None
+    if use_inflow:
+        inflow = np.concatenate([np.full(w.n, 0.3), np.linspace(-0.2, 0.2, w.n)])
+    run = pt.fom_simulate(w.x0, pt.ParticleSystem(gamma, w.delta, inflow), pt.TimeGrid(dt, steps),
+                          pt.NewtonConfig(tol=tol, max_iters=max_iters, jacobian_refresh_period=refresh))
+    snaps, iters, conv, _ = oracle.fom_simulate(w.x0, gamma, w.delta, dt, steps, inflow=inflow, tol=tol,
+                                                max_iters=max_iters, refresh=refresh)
+    print("iterations", list(run.iterations), "oracle", list(iters))
+    flips = int(np.sum(np.asarray(run.iterations) != iters))
+    assert flips <= 1, (list(run.iterations), list(iters))
+    if flips == 0:
+        assert list(run.converged) == [int(c) for c in conv]
+    assert max(rel(run.snapshots[:, s], snaps[:, s]) for s in range(steps)) <= (1e-12 if flips == 0 else 1e-9)
+
+
 def test_singularity_raises_numerical_error(pt):
     x = np.array([0.0, 1e-100, 0.0, 0.0])
     with pytest.raises(pt.NumericalError):
