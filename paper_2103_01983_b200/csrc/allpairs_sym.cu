@@ -43,7 +43,11 @@ namespace {
 constexpr int kSTPB = 128;                 // threads per CTA
 constexpr int kST = 8;                     // targets per thread
 constexpr int kSPass = kSTPB * kST;        // targets per pass (1,024)
-constexpr long long kSymMinN = 16384;      // below: the one-sided kernels (launch-bound sizes)
+constexpr long long kSymMinN = 16384;
+#ifndef PTROM_SYM_UNR
+#define PTROM_SYM_UNR 16
+#endif
+constexpr int kSymUnr = PTROM_SYM_UNR;     // sub-steps unrolled in the fp64 velocity batch loop      // below: the one-sided kernels (launch-bound sizes)
 
 __device__ __forceinline__ double rcp_cubic(double q) {
   const double y0 = rcp_seed(q);
@@ -151,7 +155,7 @@ __device__ void sym_item(long long n, const double* __restrict__ xs, const doubl
           // the tier is uniform over the tile: one loop per tier, no branch per sub-step
           auto batch = [&](auto fast_tag) {
             constexpr bool F = decltype(fast_tag)::value;
-#pragma unroll 16
+#pragma unroll kSymUnr
             for (int s = 0; s < 32; ++s) {
               const double2 p = bp[s];
               const double g = bg[s];
