@@ -825,6 +825,31 @@ struct HpArgs {
   int* sm_ctr;  // per-SM work counters (hyperpair_engine_sm_kernel), zeroed before the launch
 };
 
+// Cache-hint probes for the engine kernel's loads (PTROM_HP_HINT, measured in
+// profiles/r02_hp_hint_sweep.txt): 0 plain; 1 the list entries do not allocate in
+// L1; 2 also the position gathers are kept (evict_last); 3 positions evict_last only.
+#ifndef PTROM_HP_HINT
+#define PTROM_HP_HINT 0
+#endif
+__device__ __forceinline__ unsigned hp_ld_list(const int* p) {
+#if PTROM_HP_HINT == 1 || PTROM_HP_HINT == 2
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return (unsigned)v;
+#else
+  return (unsigned)*p;
+#endif
+}
+__device__ __forceinline__ double2 hp_ld_pos(const double2* p) {
+#if PTROM_HP_HINT == 2 || PTROM_HP_HINT == 3
+  double2 v;
+  asm volatile("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // One warp's item: target tt of t_order, instances [32·chunk, 32·chunk + 32).
 // Returns the lane's interaction count.
 template <bool AFFINE, bool CHECK, int U>
@@ -882,12 +907,12 @@ __device__ __forceinline__ unsigned long long hp_engine_item(const HpArgs& a, lo
     unsigned cn[U];
     if (nk >= U) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) cn[u] = (unsigned)lp[u];
+      for (int u = 0; u < U; ++u) cn[u] = hp_ld_list(lp + u);
     }
     auto round = [&](const unsigned (&ci)[U]) {
       double2 p[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) p[u] = __ldg(cpb + ci[u] * ub);
+      for (int u = 0; u < U; ++u) p[u] = hp_ld_pos(cpb + ci[u] * ub);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (CHECK && p[u].x == px && p[u].y == py) {  // rom.hpp:129 (δ = 0 only)
@@ -903,7 +928,7 @@ __device__ __forceinline__ unsigned long long hp_engine_item(const HpArgs& a, lo
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         ci[u] = cn[u];
-        cn[u] = (unsigned)lq[u];
+        cn[u] = hp_ld_list(lq + u);
       }
       round(ci);
     }
